@@ -1,0 +1,347 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY (see orc_spatial.hpp header).
+//
+// Flat C entry points over the oracle so Python tests / bench.py's
+// cpu_baseline leg can drive it with ctypes.  Every batch entry point takes
+// SoA column-major buffers (element (i, k) at k*N + i, exactly Eigen's
+// column-major N x K used by StateBatch and batch_crba, batch.hpp:15-19,
+// 147-148) and runs through orc::batch_eval (batch.hpp:82-125).
+#include <cstring>
+#include <string>
+
+#include "orc_batch.hpp"
+
+using namespace orc;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const ParseError*>(&e)) return 2;
+  if (dynamic_cast<const UnknownFrameError*>(&e)) return 4;
+  if (dynamic_cast<const ModelError*>(&e)) return 3;
+  if (dynamic_cast<const DimensionError*>(&e)) return 1;
+  if (dynamic_cast<const UnsupportedFeatureError*>(&e)) return 5;
+  if (dynamic_cast<const UnsupportedStructureError*>(&e)) return 6;
+  if (dynamic_cast<const SingularInertiaError*>(&e)) return 7;
+  return 99;
+}
+
+Gravity grav(const double* g3) {
+  Gravity g;
+  if (g3) g.lin = V3<double>(g3[0], g3[1], g3[2]);
+  return g;
+}
+
+template <class T>
+std::vector<T> plane_row(const double* a, int64_t N, int n, int64_t i) {
+  std::vector<T> r((size_t)n);
+  for (int j = 0; j < n; ++j) r[(size_t)j] = T(a[j * N + i]);
+  return r;
+}
+
+template <class T>
+ExtForces<T> fext_row(const double* f, int64_t N, int n, int64_t i) {
+  if (!f) return ExtForces<T>();
+  ExtForces<T> e(n);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < 6; ++k) e.w[(size_t)j].at(k) = T(f[(j * 6 + k) * N + i]);
+  return e;
+}
+
+const Model& M(void* h) { return *static_cast<Model*>(h); }
+
+void put_xform(double* out, int64_t N, int64_t i, int base, const Xform<double>& x) {
+  // R column-major (Eigen Mat3 storage), then p.
+  for (int c = 0; c < 3; ++c)
+    for (int r = 0; r < 3; ++r) out[(base + c * 3 + r) * N + i] = x.R(r, c);
+  for (int r = 0; r < 3; ++r) out[(base + 9 + r) * N + i] = x.p[r];
+}
+}  // namespace
+
+extern "C" {
+
+const char* orc_last_error() { return g_err.c_str(); }
+
+void* orc_model_builtin(const char* name) {
+  try {
+    return new Model(robots::by_name(name));
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+void* orc_model_from_urdf(const char* text) {
+  try {
+    return new Model(urdf::load_model_from_string(text));
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+int orc_model_from_urdf_status(const char* text, void** out) {
+  try {
+    *out = new Model(urdf::load_model_from_string(text));
+    return 0;
+  } catch (const std::exception& e) {
+    *out = nullptr;
+    return fail(e);
+  }
+}
+
+void* orc_model_floating(void* h) {
+  try {
+    return new Model(floating_base(M(h)));
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+void orc_model_free(void* h) { delete static_cast<Model*>(h); }
+int orc_model_dof(void* h) { return M(h).dof(); }
+double orc_model_total_mass(void* h) { return M(h).total_mass; }
+int orc_model_max_depth(void* h) { return M(h).max_depth; }
+int orc_model_is_serial(void* h) { return M(h).serial ? 1 : 0; }
+int orc_model_warning_count(void* h) { return (int)M(h).warnings.size(); }
+
+// parents[n], types[n] (0 revolute, 1 prismatic), axes[n*3], offsets[n*12]
+// (R row-major 9, p 3), inertias[n*36] (row-major), mask[n*n] (row-major).
+void orc_model_arrays(void* h, int* parents, int* types, double* axes, double* offsets, double* inertias,
+                      double* mask) {
+  const Model& m = M(h);
+  const int n = m.dof();
+  for (int i = 0; i < n; ++i) {
+    const Joint& j = m.joints[(size_t)i];
+    if (parents) parents[i] = j.parent;
+    if (types) types[i] = j.type == JointType::Revolute ? 0 : 1;
+    for (int k = 0; k < 3; ++k) {
+      if (axes) axes[i * 3 + k] = j.axis[k];
+      if (offsets) offsets[i * 12 + 9 + k] = j.offset.p[k];
+    }
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c)
+        if (offsets) offsets[i * 12 + r * 3 + c] = j.offset.R(r, c);
+    for (int r = 0; r < 6; ++r)
+      for (int c = 0; c < 6; ++c)
+        if (inertias) inertias[i * 36 + r * 6 + c] = m.inertias[(size_t)i](r, c);
+  }
+  if (mask)
+    for (size_t k = 0; k < m.mask.size(); ++k) mask[k] = m.mask[k];
+}
+
+int orc_model_joint_name(void* h, int i, char* buf, int len) {
+  const std::string& s = M(h).joints[(size_t)i].name;
+  std::snprintf(buf, (size_t)len, "%s", s.c_str());
+  return (int)s.size();
+}
+
+int orc_model_frame_count(void* h) { return (int)M(h).frames.size(); }
+// Frame k: name into buf, joint index returned via *joint, offset as R row-major + p.
+int orc_model_frame(void* h, int k, char* buf, int len, int* joint, double* off12) {
+  const Frame& f = M(h).frames[(size_t)k];
+  std::snprintf(buf, (size_t)len, "%s", f.name.c_str());
+  *joint = f.joint;
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) off12[r * 3 + c] = f.offset.R(r, c);
+    off12[9 + r] = f.offset.p[r];
+  }
+  return 0;
+}
+
+int orc_frame_id(void* h, const char* name) {
+  try {
+    return M(h).frame_id(name);
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1;
+  }
+}
+
+// batch.hpp:48-75; any of qdd / tau may be null (with_qdd / with_tau false).
+void orc_random_states(void* h, int64_t N, uint64_t seed, double* q, double* qd, double* qdd, double* tau) {
+  StateBatch b = random_states(M(h), (int)N, seed, qdd != nullptr, tau != nullptr);
+  std::memcpy(q, b.q.data(), b.q.size() * sizeof(double));
+  std::memcpy(qd, b.qd.data(), b.qd.size() * sizeof(double));
+  if (qdd) std::memcpy(qdd, b.qdd.data(), b.qdd.size() * sizeof(double));
+  if (tau) std::memcpy(tau, b.tau.data(), b.tau.size() * sizeof(double));
+}
+
+// variant 0: vectorized mask form (dynamics.hpp:405-414); 1: rnea_loop.
+// f32 != 0 evaluates in single precision (inputs rounded to float).
+int orc_batch_rnea(void* h, int64_t N, const double* q, const double* qd, const double* qdd, const double* g3,
+                   const double* fext, double* tau, int threads, int variant, int f32) {
+  try {
+    const Model& m = M(h);
+    const int n = m.dof();
+    const Gravity g = grav(g3);
+    batch_eval((int)N,
+               [&](int i) {
+                 std::vector<double> r;
+                 if (f32) {
+                   auto a = plane_row<float>(q, N, n, i), b = plane_row<float>(qd, N, n, i),
+                        c = plane_row<float>(qdd, N, n, i);
+                   auto t = variant ? rnea_loop<float>(m, a, b, c, g, fext_row<float>(fext, N, n, i))
+                                    : rnea<float>(m, a, b, c, g, fext_row<float>(fext, N, n, i));
+                   r.assign(t.begin(), t.end());
+                 } else {
+                   auto a = plane_row<double>(q, N, n, i), b = plane_row<double>(qd, N, n, i),
+                        c = plane_row<double>(qdd, N, n, i);
+                   r = variant ? rnea_loop<double>(m, a, b, c, g, fext_row<double>(fext, N, n, i))
+                               : rnea<double>(m, a, b, c, g, fext_row<double>(fext, N, n, i));
+                 }
+                 for (int j = 0; j < n; ++j) tau[j * N + i] = r[(size_t)j];
+               },
+               threads);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// M column-major n x n per instance: plane c*n + r.  variant 0 vectorized, 1 loop.
+int orc_batch_crba(void* h, int64_t N, const double* q, double* Mout, int threads, int variant, int f32) {
+  try {
+    const Model& m = M(h);
+    const int n = m.dof();
+    batch_eval((int)N,
+               [&](int i) {
+                 if (f32) {
+                   auto a = plane_row<float>(q, N, n, i);
+                   Dense<float> mm = variant ? crba_loop<float>(m, a) : crba<float>(m, a);
+                   for (int k = 0; k < n * n; ++k) Mout[k * N + i] = mm.d[(size_t)k];
+                 } else {
+                   auto a = plane_row<double>(q, N, n, i);
+                   Dense<double> mm = variant ? crba_loop<double>(m, a) : crba<double>(m, a);
+                   for (int k = 0; k < n * n; ++k) Mout[k * N + i] = mm.d[(size_t)k];
+                 }
+               },
+               threads);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// Forward dynamics. variant 0: reference LLT path (dynamics.hpp:421-444);
+// 1: aba_loop.  status[i] = 0 ok, 7 singular (SingularInertiaError).
+int orc_batch_fd(void* h, int64_t N, const double* q, const double* qd, const double* tau, const double* g3,
+                 const double* fext, double* qdd, int* status, int threads, int variant) {
+  try {
+    const Model& m = M(h);
+    const int n = m.dof();
+    const Gravity g = grav(g3);
+    batch_eval((int)N,
+               [&](int i) {
+                 auto a = plane_row<double>(q, N, n, i), b = plane_row<double>(qd, N, n, i),
+                      c = plane_row<double>(tau, N, n, i);
+                 int st = 0;
+                 std::vector<double> r((size_t)n, 0.0);
+                 try {
+                   r = variant ? aba_loop<double>(m, a, b, c, g, fext_row<double>(fext, N, n, i))
+                               : forward_dynamics<double>(m, a, b, c, g, fext_row<double>(fext, N, n, i));
+                 } catch (const SingularInertiaError&) {
+                   st = 7;
+                 }
+                 for (int j = 0; j < n; ++j) qdd[j * N + i] = r[(size_t)j];
+                 if (status) status[i] = st;
+               },
+               threads);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// All joint world transforms: plane (j*12 + k), k 0..8 = R column-major, 9..11 = p.
+int orc_batch_fk(void* h, int64_t N, const double* q, double* out, int threads, int scan) {
+  try {
+    const Model& m = M(h);
+    const int n = m.dof();
+    batch_eval((int)N,
+               [&](int i) {
+                 auto a = plane_row<double>(q, N, n, i);
+                 Frames<double> w = scan ? forward_kinematics_scan<double>(m, a) : forward_kinematics<double>(m, a);
+                 for (int j = 0; j < n; ++j) put_xform(out, N, i, j * 12, w[(size_t)j]);
+               },
+               threads);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// Frame pose (12 planes) and 6 x n Jacobian (plane c*6 + r).
+int orc_batch_jacobian(void* h, int64_t N, const double* q, const char* frame, double* pose, double* J,
+                       int threads) {
+  try {
+    const Model& m = M(h);
+    const int n = m.dof();
+    (void)m.frame(frame);
+    batch_eval((int)N,
+               [&](int i) {
+                 auto a = plane_row<double>(q, N, n, i);
+                 Frames<double> w = forward_kinematics<double>(m, a);
+                 if (pose) put_xform(pose, N, i, 0, frame_transform<double>(m, w, frame));
+                 if (J) {
+                   Dense<double> jj = geometric_jacobian<double>(m, w, frame);
+                   for (int k = 0; k < 6 * n; ++k) J[k * N + i] = jj.d[(size_t)k];
+                 }
+               },
+               threads);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// OSC (control.hpp:108-155).  target12 = R row-major + p; kp/kd/accel_ff 6
+// each (angular first); posture n values shared by the batch.
+int orc_batch_osc(void* h, int64_t N, const double* q, const double* qd, const char* frame, const double* target12,
+                  const double* kp, const double* kd, const double* accel_ff, const double* posture, double pkp,
+                  double pkd, const double* g3, double eps, double* tau, double* lambda, int* status, int threads) {
+  try {
+    const Model& m = M(h);
+    const int n = m.dof();
+    TaskTarget t;
+    t.frame = frame;
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) t.pose.R(r, c) = target12[r * 3 + c];
+      t.pose.p[r] = target12[9 + r];
+    }
+    for (int k = 0; k < 6; ++k) {
+      t.gains.kp[k] = kp[k];
+      t.gains.kd[k] = kd[k];
+      t.accel_ff.at(k) = accel_ff ? accel_ff[k] : 0.0;
+    }
+    (void)m.frame(frame);
+    const std::vector<double> post(posture, posture + n);
+    const PostureGains pg{pkp, pkd};
+    const Gravity g = grav(g3);
+    batch_eval((int)N,
+               [&](int i) {
+                 auto a = plane_row<double>(q, N, n, i), b = plane_row<double>(qd, N, n, i);
+                 int st = 0;
+                 OscResult r;
+                 r.tau.assign((size_t)n, 0.0);
+                 for (double& x : r.Lambda) x = 0.0;
+                 try {
+                   r = osc_step_full(m, a, b, t, post, pg, g, eps);
+                 } catch (const SingularInertiaError&) {
+                   st = 7;
+                 }
+                 for (int j = 0; j < n; ++j) tau[j * N + i] = r.tau[(size_t)j];
+                 if (lambda)
+                   for (int k = 0; k < 36; ++k) lambda[k * N + i] = r.Lambda[k];
+                 if (status) status[i] = st;
+               },
+               threads);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+}  // extern "C"
