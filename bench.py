@@ -1,0 +1,481 @@
+#!/usr/bin/env python3
+"""Device-timed benchmark of the batched dynamics hot path (BASELINE.json).
+
+Headline (`value`): Franka Panda (robots::chain7) forward dynamics by the
+articulated-body algorithm, fp64, N = 4,194,304 random states per GPU (weak
+scaling across ranks), inputs resident in HBM (705 MB/GPU of q, q̇, τ: larger
+than the 126 MB L2, so no flush is needed between steps).  One step = one
+vd_aba launch over the rank's shard.  Throughput = states / s over all ranks,
+step time = max over ranks (CUDA events on the launching stream).
+
+e2e: the same metric through the public host API (vd_batch_forward_dynamics_host
+= batch_forward_dynamics, batch.hpp:154-165) from pinned host buffers: H2D of
+q, q̇, τ, the kernel, D2H of q̈ inside the timed region.
+
+Also measured in the same run (reported under "configs"): the other
+BASELINE.json configurations (FK + Jacobian, fused M/bias/ABA fp32+fp64, G1
+RNEA + ABA, OSC for Panda and G1).
+
+cpu_baseline / --impl reference: the reference CPU path — the oracle's
+restatement of forward_dynamics (CRBA + bias + LLT, dynamics.hpp:421-444) run
+through batch_eval's static std::thread chunking (batch.hpp:82-125) on all host
+cores, on a bounded sample of the same random states.
+"""
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "dynamics evals/sec (Panda & G1 ABA/RNEA) vs batch, 1/2/4/8 B200, % roofline"
+N_HEAD = 4194304
+SEED = 2604
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-configs", action="store_true", help="skip the secondary configuration sweep")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    return ap.parse_args()
+
+
+def init_dist(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        backend = "nccl" if (args.impl == "ours" and torch.cuda.is_available()) else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend, rank=rank, world_size=world)
+    return rank, world, local
+
+
+def barrier():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+def event_time(fn, steps, warmup, stream):
+    """Average ms per call of fn() measured with CUDA events on `stream`."""
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    return e0.elapsed_time(e1) / steps
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except (OSError, ValueError):
+        return {}
+
+
+def flops_per_eval(robot, algo):
+    """Frozen algorithmic flops from the op-counting oracle (oracle/orc_count.hpp)."""
+    import oracle_ffi
+
+    L = oracle_ffi.lib()
+    L.orc_count_flops.restype = ctypes.c_double
+    L.orc_count_flops.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    m = oracle_ffi.Model.builtin(robot)
+    return L.orc_count_flops(m.h, {"rnea": 0, "crba": 1, "aba": 2, "fk": 3}[algo], None)
+
+
+def cpu_reference_rate(robot, n_sample, threads, target_s=12.0, op="fd"):
+    """Reference CPU path (LLT forward dynamics / mask RNEA) on host cores."""
+    import oracle_ffi
+
+    om = oracle_ffi.Model.builtin(robot)
+    probe = min(n_sample, 4096)
+    q, qd, qdd, tau = om.random_states(probe, SEED, True, True)
+    t0 = time.perf_counter()
+    if op == "fd":
+        om.forward_dynamics(q, qd, tau, threads=threads)
+    else:
+        om.rnea(q, qd, qdd, threads=threads)
+    rate = probe / max(time.perf_counter() - t0, 1e-9)
+    n = int(min(n_sample, max(probe, rate * target_s)))
+    q, qd, qdd, tau = om.random_states(n, SEED, True, True)
+    t0 = time.perf_counter()
+    if op == "fd":
+        om.forward_dynamics(q, qd, tau, threads=threads)
+    else:
+        om.rnea(q, qd, qdd, threads=threads)
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, world, _ = init_dist(args)
+    if rank != 0:
+        return 0
+    threads = host_cores()
+    vals = []
+    for _ in range(args.warmup):
+        cpu_reference_rate("chain7", 200000, threads, target_s=2.0)
+    total_n, total_t = 0, 0.0
+    for _ in range(args.steps):
+        r, n, dt = cpu_reference_rate("chain7", 400000, threads, target_s=4.0)
+        vals.append(r)
+        total_n += n
+        total_t += dt
+    value = total_n / total_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "chain7 (Franka Panda stand-in) forward dynamics, reference CPU path: CRBA + RNEA "
+                               "bias + LLT (dynamics.hpp:421-444) via batch_eval threads (batch.hpp:82-125)",
+                   "robot": "chain7", "dof": 7, "sample_states_per_step": int(total_n / args.steps),
+                   "seed": SEED},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
+                         "sample": f"{int(total_n / args.steps)} random states per step (mt19937_64 seed {SEED}), "
+                                   f"{threads} threads, {cpu_model()}"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+
+    rank, world, local = init_dist(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2604_04310_b200 as vd
+    from paper_2604_04310_b200 import dist as vdist
+
+    lib = vd._lib.load()
+    stream = torch.cuda.current_stream(dev)
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+
+    # ---------------- headline: chain7 ABA fp64, N_HEAD states per GPU
+    model = vd.robots.chain7()
+    dm = vd.DeviceModel(model, local)
+    n = model.dof()
+    N = N_HEAD
+    g = torch.Generator(device=dev).manual_seed(SEED + rank)
+    rnd = lambda dt=torch.float64: ((torch.rand((n, N), generator=g, device=dev, dtype=dt) * 2 - 1) * np.pi)  # noqa
+    q, qd, tau = rnd(), rnd(), rnd()
+    qdd = torch.empty((n, N), dtype=torch.float64, device=dev)
+    status = torch.empty(N, dtype=torch.int32, device=dev)
+
+    def step():
+        rc = lib.vd_aba(dm.handle, 0, N, q.data_ptr(), qd.data_ptr(), tau.data_ptr(), N, None, None, qdd.data_ptr(), N,
+                        status.data_ptr(), sptr)
+        if rc:
+            raise RuntimeError(lib.vd_last_error().decode())
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = vdist.max_over_ranks(ms_local, device=dev)
+    value = N * world / (ms * 1e-3)
+    assert int(status.max()) == 0
+
+    # per-launch duration of the dominant kernel (it is the only kernel in the step)
+    flops = flops_per_eval("chain7", "aba")
+    bytes_per_eval = 8 * n * 4  # q, qd, tau in; qdd out
+    achieved_tf = flops * N / (ms_local * 1e-3) / 1e12
+    lib.vdi_fma_peak_tflops.restype = ctypes.c_double
+    lib.vdi_fma_peak_tflops.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    fp64_peak = lib.vdi_fma_peak_tflops(local, 0, 200)
+    fp32_peak = lib.vdi_fma_peak_tflops(local, 1, 200)
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    roofline = {
+        "bound": "fp64", "achieved": round(achieved_tf, 4), "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
+        "frac": round(achieved_tf / fp64_peak, 4) if fp64_peak > 0 else None, "traffic": None,
+        "flops_per_eval": flops, "flops_source": "frozen op count of oracle aba_loop (oracle/orc_count.hpp)",
+        "peak_source": "measured in this run: FP64 FMA-stream microbenchmark (vdi_fma_peak_tflops)",
+        "hbm_gbs_achieved": round(bytes_per_eval * N / (ms_local * 1e-3) / 1e9, 1), "hbm_gbs_peak": hbm,
+        "hbm_frac": round(bytes_per_eval * N / (ms_local * 1e-3) / 1e9 / hbm, 4),
+    }
+
+    # ---------------- e2e through the public host API (pinned buffers)
+    e2e = None
+    try:
+        hq = torch.empty((n, N), dtype=torch.float64, pin_memory=True)
+        hqd = torch.empty_like(hq).pin_memory()
+        htau = torch.empty_like(hq).pin_memory()
+        hout = torch.empty_like(hq).pin_memory()
+        hst = torch.empty(N, dtype=torch.int32).pin_memory()
+        hq.copy_(q.cpu())
+        hqd.copy_(qd.cpu())
+        htau.copy_(tau.cpu())
+        devs = (ctypes.c_int * 1)(local)
+
+        def e2e_step():
+            rc = lib.vd_batch_forward_dynamics_host(model.handle, N, hq.data_ptr(), hqd.data_ptr(), htau.data_ptr(),
+                                                    None, hout.data_ptr(), hst.data_ptr(), devs, 1)
+            if rc:
+                raise RuntimeError(lib.vd_last_error().decode())
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        k = max(3, args.steps // 4)
+        for _ in range(k):
+            e2e_step()
+        t1 = time.perf_counter()
+        barrier()
+        e2e_ms = vdist.max_over_ranks((t1 - t0) * 1e3 / k, device=dev)
+        assert torch.equal(hout.to(dev), qdd), "e2e output differs from the device-resident result"
+        e2e = {"value": N * world / (e2e_ms * 1e-3), "unit": "evals/s", "h2d_bytes_per_step": 3 * n * N * 8,
+               "d2h_bytes_per_step": n * N * 8 + N * 4, "ms_per_step": e2e_ms,
+               "api": "vd_batch_forward_dynamics_host (batch_forward_dynamics, batch.hpp:154-165)"}
+        del hq, hqd, htau, hout
+    except Exception as ex:  # noqa: BLE001
+        e2e = {"value": None, "unit": "evals/s", "error": str(ex)}
+
+    # ---------------- secondary configurations (same run)
+    configs = {}
+    if not args.no_configs:
+        configs = run_configs(vd, lib, dev, stream, sptr, args, rank, world)
+
+    # ---------------- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = host_cores()
+        r, ns, dt = cpu_reference_rate("chain7", 400000, threads, target_s=12.0)
+        cpu = {"value": r, "unit": "evals/s", "cores": threads, "kind": "port",
+               "sample": f"{ns} random chain7 states (seed {SEED}), reference forward_dynamics (CRBA + bias + LLT) "
+                         f"in {dt:.1f} s on {threads} threads, {cpu_model()}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "chain7 (Franka Panda stand-in, robots::chain7) ABA forward dynamics, fp64, "
+                                   f"{N} random states per GPU", "robot": "chain7", "dof": n,
+                       "states_per_gpu": N, "global_batch": N * world, "parallelism": f"dp{world} (batch shards)",
+                       "l2": "inputs 705 MB/GPU > 126 MB L2 (no flush needed)", "seed": SEED},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "roofline": roofline,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "fp32_peak_tflops": round(fp32_peak, 3),
+            "configs": configs,
+        }
+        print(json.dumps(line))
+    return 0
+
+
+def run_configs(vd, lib, dev, stream, sptr, args, rank, world):
+    """The other BASELINE.json configurations, device-timed in the same run."""
+    import torch
+
+    out = {}
+    steps, warm = max(5, args.steps // 2), 3
+    gen = torch.Generator(device=dev).manual_seed(SEED + 7)
+
+    def states(n, N, dt):
+        return [((torch.rand((n, N), generator=gen, device=dev, dtype=torch.float64) * 2 - 1) * np.pi).to(dt)
+                for _ in range(3)]
+
+    def rec(key, N, ms, flops=None, extra=None):
+        d = {"states": N, "ms": round(ms, 5), "evals_per_s": N / (ms * 1e-3)}
+        if flops:
+            d["algorithmic_tflops"] = round(flops * N / (ms * 1e-3) / 1e12, 4)
+        if extra:
+            d.update(extra)
+        out[key] = d
+
+    chain = vd.robots.chain7()
+    tree = vd.robots.tree29()
+    dc, dt_ = vd.DeviceModel(chain, dev.index), vd.DeviceModel(tree, dev.index)
+
+    # config 2: Panda FK + EE Jacobian, batch 4096
+    for dt, code in ((torch.float64, 0), (torch.float32, 1)):
+        N = 4096
+        q, _, _ = states(7, N, dt)
+        pose = torch.empty((12, N), dtype=dt, device=dev)
+        J = torch.empty((42, N), dtype=dt, device=dev)
+        fid = chain.frame_index("ee")
+        fn = lambda: lib.vd_jacobian(dc.handle, code, N, q.data_ptr(), N, fid, pose.data_ptr(), J.data_ptr(), N, sptr)  # noqa
+        rec(f"2_panda_fk_jacobian_b4096_{'f64' if code == 0 else 'f32'}", N, event_time(fn, 200, 20, stream),
+            flops_per_eval("chain7", "fk"))
+    # config 3: Panda M + bias + ABA (fused), batch 65536, fp32 and fp64
+    for dt, code in ((torch.float64, 0), (torch.float32, 1)):
+        N = 65536
+        q, qd, tau = states(7, N, dt)
+        M = torch.empty((49, N), dtype=dt, device=dev)
+        b = torch.empty((7, N), dtype=dt, device=dev)
+        a = torch.empty((7, N), dtype=dt, device=dev)
+        fn = lambda: lib.vd_dynamics(dc.handle, code, N, q.data_ptr(), qd.data_ptr(), tau.data_ptr(), N, None,  # noqa
+                                     M.data_ptr(), b.data_ptr(), a.data_ptr(), N, None, sptr)
+        fl = flops_per_eval("chain7", "crba") + flops_per_eval("chain7", "rnea") + flops_per_eval("chain7", "aba")
+        rec(f"3_panda_M_bias_aba_b65536_{'f64' if code == 0 else 'f32'}", N, event_time(fn, 50, warm, stream), fl)
+    # config 4: G1 RNEA + ABA, batch 262144 (fp64 and fp32)
+    for dt, code in ((torch.float64, 0), (torch.float32, 1)):
+        N = 262144
+        q, qd, x = states(29, N, dt)
+        t = torch.empty((29, N), dtype=dt, device=dev)
+        a = torch.empty((29, N), dtype=dt, device=dev)
+        f_r = lambda: lib.vd_rnea(dt_.handle, code, N, q.data_ptr(), qd.data_ptr(), x.data_ptr(), N, None, None,  # noqa
+                                  t.data_ptr(), N, sptr)
+        f_a = lambda: lib.vd_aba(dt_.handle, code, N, q.data_ptr(), qd.data_ptr(), x.data_ptr(), N, None, None,  # noqa
+                                 a.data_ptr(), N, None, sptr)
+        sfx = "f64" if code == 0 else "f32"
+        rec(f"4_g1_rnea_b262144_{sfx}", N, event_time(f_r, steps, warm, stream), flops_per_eval("tree29", "rnea"))
+        rec(f"4_g1_aba_b262144_{sfx}", N, event_time(f_a, steps, warm, stream), flops_per_eval("tree29", "aba"))
+    # config 5: OSC terms, batch 4M (per GPU), Panda and G1
+    for robot, dmod, frame in (("chain7", dc, "ee"), ("tree29", dt_, "l_palm")):
+        m = chain if robot == "chain7" else tree
+        n = m.dof()
+        N = 4194304 if robot == "chain7" else 1048576
+        q, qd, _ = states(n, N, torch.float64)
+        P = vd._lib.OscParams()
+        P.frame = m.frame_index(frame)
+        z = torch.zeros((1, n), dtype=torch.float64, device=dev)
+        pose = vd.frame_transform(dmod, z, frame).cpu().numpy()[0]
+        for k in range(12):
+            P.target[k] = float(pose[k])
+        for k in range(6):
+            P.kp[k], P.kd[k], P.accel_ff[k] = 100.0, 20.0, 0.0
+        post = (ctypes.c_double * n)(*([0.0] * n))
+        P.posture = ctypes.cast(post, vd._lib.Pd)
+        P.posture_kp, P.posture_kd = 10.0, 2.0
+        P.gravity[0], P.gravity[1], P.gravity[2] = 0.0, 0.0, 9.81
+        P.epsilon = 1e-6
+        tau = torch.empty((n, N), dtype=torch.float64, device=dev)
+        lam = torch.empty((36, N), dtype=torch.float64, device=dev)
+        fn = lambda: lib.vd_osc(dmod.handle, 0, N, q.data_ptr(), qd.data_ptr(), N, ctypes.byref(P),  # noqa
+                                tau.data_ptr(), lam.data_ptr(), N, None, sptr)
+        rec(f"5_{'panda' if robot == 'chain7' else 'g1'}_osc_b{N}_f64", N, event_time(fn, 5, 2, stream),
+            None, {"note": "tau + Lambda outputs"})
+        del q, qd, tau, lam
+        torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

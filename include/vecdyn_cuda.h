@@ -1,0 +1,194 @@
+/*
+ * vecdyn_cuda.h — C-ABI of the B200-native batched rigid-body dynamics library.
+ *
+ * Drop-in boundary for the reference `vecdyn` hot path (a C++20/Eigen header
+ * library, proj/core/include/vecdyn/).  The reference has no FFI; its
+ * "operator API" is the C++ signatures cited on every entry point below.
+ * These functions replace them one for one with plain pointers and sizes:
+ *
+ *   - models are opaque handles (the reference returns RobotModel by value,
+ *     model.hpp:90-149);
+ *   - batched buffers are DEVICE pointers in SoA column-major layout: element
+ *     (instance i, component k) lives at  k * ld + i  (ld >= N).  This is the
+ *     memory layout of Eigen's column-major N x K matrices used by StateBatch
+ *     and batch_crba (batch.hpp:15-19, 147-148), so an Eigen caller can pass
+ *     .data() unchanged;
+ *   - dtype selects fp64 (the reference default, T = double) or fp32 (the
+ *     reference's float instantiation, test_dynamics.cpp:398-413) for every
+ *     floating buffer of the call;
+ *   - errors are int status codes (VD_ERR_*) mirroring the reference exception
+ *     hierarchy (errors.hpp:9-61) plus vd_last_error() (thread-local text);
+ *     forward dynamics and OSC additionally report a per-instance status
+ *     (the reference throws SingularInertiaError for the whole call,
+ *     dynamics.hpp:437-442, control.hpp:131-134).
+ *
+ * Every kernel entry point is asynchronous on `stream` (a cudaStream_t passed
+ * as void*, NULL = legacy default stream) and never allocates.
+ */
+#ifndef VECDYN_CUDA_H_
+#define VECDYN_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VD_OK 0
+#define VD_ERR_DIMENSION 1              /* DimensionError            errors.hpp:25-28 */
+#define VD_ERR_PARSE 2                  /* ParseError(line, column)  errors.hpp:43-53 */
+#define VD_ERR_MODEL 3                  /* ModelError                errors.hpp:31-34 */
+#define VD_ERR_UNKNOWN_FRAME 4          /* UnknownFrameError         errors.hpp:37-40 */
+#define VD_ERR_UNSUPPORTED_FEATURE 5    /* UnsupportedFeatureError   errors.hpp:56-59 */
+#define VD_ERR_UNSUPPORTED_STRUCTURE 6  /* UnsupportedStructureError errors.hpp:62-65 */
+#define VD_ERR_SINGULAR_INERTIA 7       /* SingularInertiaError      errors.hpp:68-71 */
+#define VD_ERR_CUDA 8                   /* CUDA runtime failure (no reference analogue) */
+#define VD_ERR_INVALID_ARGUMENT 9       /* null pointer, ld < N, bad dtype, ... */
+#define VD_ERR_IO 10                    /* Error("cannot open URDF file ...") urdf.cpp:277-281 */
+#define VD_ERR_GENERIC 11               /* vecdyn::Error */
+
+#define VD_F64 0
+#define VD_F32 1
+
+/* per-instance status values written by vd_aba / vd_dynamics / vd_osc */
+#define VD_STATUS_OK 0
+#define VD_STATUS_SINGULAR 7 /* non-positive articulated pivot / mass-matrix pivot, or non-finite */
+
+typedef struct vd_model_s* vd_model;
+typedef struct vd_device_model_s* vd_device_model;
+
+/* ------------------------------------------------------------------ errors */
+const char* vd_last_error(void);
+int vd_last_error_line(void);   /* ParseError::line (1-based), 0 otherwise */
+int vd_last_error_column(void); /* ParseError::column */
+const char* vd_version(void);
+
+/* ------------------------------------------------------------------ host model */
+/* robots::chain7 / humanoid23 / tree29 / by_name            robots.cpp:12-32 */
+int vd_model_builtin(const char* name, vd_model* out);
+/* urdf::load_model(path)                                     urdf.cpp:384-386 */
+int vd_model_load_urdf(const char* path, vd_model* out);
+/* urdf::load_model_from_string(text)                         urdf.cpp:388-390 */
+int vd_model_load_urdf_string(const char* text, size_t len, vd_model* out);
+/* floating_base(model)                                       model.cpp:289-331 */
+int vd_model_floating_base(vd_model m, vd_model* out);
+void vd_model_destroy(vd_model m);
+
+/* RobotModel accessors                                       model.hpp:92-133 */
+int vd_model_dof(vd_model m);
+int vd_model_max_depth(vd_model m);
+int vd_model_is_serial_chain(vd_model m);
+double vd_model_total_mass(vd_model m);
+int vd_model_warning_count(vd_model m);
+int vd_model_warning(vd_model m, int k, char* buf, size_t len);
+int vd_model_name(vd_model m, char* buf, size_t len);
+int vd_model_parents(vd_model m, int* parents_out); /* n ints */
+int vd_model_joint_name(vd_model m, int i, char* buf, size_t len);
+int vd_model_joint_index(vd_model m, const char* name); /* -1 if absent (model.cpp:337-343) */
+/* type: 0 revolute, 1 prismatic; offset: R column-major (9) then p (3);
+ * inertia: 6x6 row-major about the joint frame origin, angular first. */
+int vd_model_joint(vd_model m, int i, int* type, double axis[3], double offset[12], double inertia[36]);
+int vd_model_ancestor_mask(vd_model m, double* mask_out); /* n*n, column-major (Eigen MatrixXd) */
+int vd_model_frame_count(vd_model m);
+int vd_model_frame(vd_model m, int k, char* name, size_t len, int* joint, double offset[12]);
+/* RobotModel::frame(name) index; VD_ERR_UNKNOWN_FRAME when absent (model.cpp:512-518) */
+int vd_model_frame_index(vd_model m, const char* name, int* out);
+
+/* StateBatch random_states(model, count, seed, with_qdd, with_tau), batch.hpp:48-75:
+ * HOST column-major N x n arrays; qdd / tau may be NULL (with_qdd / with_tau
+ * false).  Bit-identical to the reference's mt19937_64 + U[-π, π] stream. */
+int vd_random_states(vd_model m, int64_t N, uint64_t seed, double* q, double* qd, double* qdd, double* tau);
+
+/* ------------------------------------------------------------------ device model */
+/* Packs the model for `device` (the reference has no device; the model is
+ * uploaded once here and reused by every call).  When the model matches a
+ * robot compiled into the library (chain7, tree29, humanoid23) the
+ * compile-time specialised kernels are used, otherwise the generic
+ * runtime-topology kernels (any tree with n <= 64). */
+int vd_device_model_create(vd_model m, int device, vd_device_model* out);
+void vd_device_model_destroy(vd_device_model dm);
+int vd_device_model_dof(vd_device_model dm);
+/* 0 = generic kernels, k > 0 = compile-time specialised robot k */
+int vd_device_model_specialization(vd_device_model dm);
+/* Force the generic kernels even for builtin robots (testing / comparison). */
+int vd_device_model_set_generic(vd_device_model dm, int generic);
+
+/* ------------------------------------------------------------------ batched kernels
+ * gravity3: the base acceleration a_g = −field (GravitySpec::accel.linear,
+ * dynamics.hpp:194-205); NULL means GravitySpec::standard() = (0, 0, +9.81).
+ * fext: NULL or 6n planes, plane j*6 + k = component k (angular first) of
+ * the world-frame Plücker wrench on joint j (ExternalForcesT, dynamics.hpp:210-236). */
+
+/* forward_kinematics, kinematics.hpp:43-56: plane j*12 + k (k < 9: R column-major, 9..11: p) */
+int vd_fk(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* frames_out,
+          int64_t ld_out, void* stream);
+/* frame_transform + geometric_jacobian, kinematics.hpp:89-136: pose 12 planes,
+ * J 6 x n column-major (plane c*6 + r).  Either output may be NULL. */
+int vd_jacobian(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, int frame, void* pose_out,
+                void* J_out, int64_t ld_out, void* stream);
+/* rnea(model, q, qd, qdd, gravity, fext), dynamics.hpp:405-422 */
+int vd_rnea(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* qdd, int64_t ld_in,
+            const double* gravity3, const void* fext, void* tau_out, int64_t ld_out, void* stream);
+/* c + g (− Σ Jᵀ f_ext): rnea(q, qd, 0, gravity, fext), dynamics.hpp:434-435 */
+int vd_bias(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in,
+            const double* gravity3, const void* fext, void* out, int64_t ld_out, void* stream);
+/* gravity_vector, dynamics.hpp:557-563 */
+int vd_gravity(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, const double* gravity3,
+               void* out, int64_t ld_out, void* stream);
+/* coriolis_vector, dynamics.hpp:565-571 */
+int vd_coriolis(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in, void* out,
+                int64_t ld_out, void* stream);
+/* crba, dynamics.hpp:507-520: M n x n column-major, plane c*n + r */
+int vd_crba(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* M_out, int64_t ld_out,
+            void* stream);
+/* forward_dynamics, dynamics.hpp:576-599, computed by the articulated-body
+ * algorithm (absent from the reference).  status_out (int32 x N)
+ * may be NULL. */
+int vd_aba(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau, int64_t ld_in,
+           const double* gravity3, const void* fext, void* qdd_out, int64_t ld_out, int32_t* status_out,
+           void* stream);
+/* Fused M + bias + q̈ (BASELINE config 3) sharing one FK; any output may be NULL. */
+int vd_dynamics(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau,
+                int64_t ld_in, const double* gravity3, void* M_out, void* bias_out, void* qdd_out, int64_t ld_out,
+                int32_t* status_out, void* stream);
+
+/* osc_step, control.hpp:108-155.  Shared task / posture parameters. */
+typedef struct vd_osc_params {
+  int frame;              /* vd_model_frame_index */
+  double target[12];      /* TaskTarget::pose, R column-major + p */
+  double kp[6], kd[6];    /* TaskGains (angular first) */
+  double accel_ff[6];     /* TaskTarget::accel_ff */
+  const double* posture;  /* HOST pointer, n values */
+  double posture_kp, posture_kd;
+  double gravity[3];      /* a_g */
+  double epsilon;         /* Λ regulariser (reference default 1e-6) */
+} vd_osc_params;
+/* tau n planes; Lambda_out (36 planes, column-major (J M⁻¹ Jᵀ + εI)⁻¹) may be NULL. */
+int vd_osc(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in,
+           const vd_osc_params* params, void* tau_out, void* Lambda_out, int64_t ld_out, int32_t* status_out,
+           void* stream);
+
+/* ------------------------------------------------------------------ host batch (drop-in for batch.hpp)
+ * batch_rnea / batch_crba / batch_forward_dynamics (batch.hpp:128-165) with
+ * HOST column-major N x n inputs and N x K outputs, fp64.  `workers` becomes a
+ * device list: instances are split into contiguous shards (the partition rule
+ * of batch_eval, batch.hpp:109-119), one host thread + stream per device, no
+ * collective.  Pinned inputs are DMA'd directly; pageable ones are staged
+ * through pinned chunks.  forward dynamics reports VD_ERR_SINGULAR_INERTIA if
+ * any instance failed (status_out, if given, says which). */
+int vd_batch_rnea_host(vd_model m, int64_t N, const double* q, const double* qd, const double* qdd,
+                       const double* gravity3, double* tau_out, const int* devices, int n_devices);
+int vd_batch_crba_host(vd_model m, int64_t N, const double* q, double* M_out, const int* devices, int n_devices);
+int vd_batch_forward_dynamics_host(vd_model m, int64_t N, const double* q, const double* qd, const double* tau,
+                                   const double* gravity3, double* qdd_out, int32_t* status_out,
+                                   const int* devices, int n_devices);
+
+/* Contiguous shard [begin, end) of N instances for rank r of w (batch.hpp:111-119 rule). */
+int vd_shard_range(int64_t N, int world, int rank, int64_t* begin, int64_t* end);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VECDYN_CUDA_H_ */

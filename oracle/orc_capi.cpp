@@ -9,6 +9,7 @@
 #include <string>
 
 #include "orc_batch.hpp"
+#include "orc_count.hpp"
 
 using namespace orc;
 
@@ -342,6 +343,41 @@ int orc_batch_osc(void* h, int64_t N, const double* q, const double* qd, const c
   } catch (const std::exception& e) {
     return fail(e);
   }
+}
+
+// Frozen algorithmic op counts per evaluation (orc_count.hpp).  algo:
+// 0 rnea_loop, 1 crba_loop, 2 aba_loop, 3 forward_kinematics, 4 rnea (mask
+// form), 5 forward_dynamics (CRBA + bias + LLT), 6 crba (mask form).
+// out[0..4] = add, mul, div, sqrt, trig; returns flops (add+mul+div).
+double orc_count_flops(void* h, int algo, double* out) {
+  const Model& m = M(h);
+  const int n = m.dof();
+  std::vector<Counted> q((size_t)n), qd((size_t)n), qdd((size_t)n);
+  for (int i = 0; i < n; ++i) {
+    q[(size_t)i] = Counted(0.1 * (i + 1));
+    qd[(size_t)i] = Counted(0.2 - 0.03 * i);
+    qdd[(size_t)i] = Counted(0.05 * i - 0.1);
+  }
+  op_count() = OpCount();
+  switch (algo) {
+    case 0: (void)rnea_loop<Counted>(m, q, qd, qdd); break;
+    case 1: (void)crba_loop<Counted>(m, q); break;
+    case 2: (void)aba_loop<Counted>(m, q, qd, qdd); break;
+    case 3: (void)forward_kinematics<Counted>(m, q); break;
+    case 4: (void)rnea<Counted>(m, q, qd, qdd); break;
+    case 5: (void)forward_dynamics<Counted>(m, q, qd, qdd); break;
+    case 6: (void)crba<Counted>(m, q); break;
+    default: return -1;
+  }
+  const OpCount c = op_count();
+  if (out) {
+    out[0] = (double)c.add;
+    out[1] = (double)c.mul;
+    out[2] = (double)c.div;
+    out[3] = (double)c.sqrt;
+    out[4] = (double)c.trig;
+  }
+  return (double)c.flops();
 }
 
 }  // extern "C"

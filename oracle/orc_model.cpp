@@ -416,7 +416,7 @@ Model build_model(const Description& d) {
       jt.type = s.type;
       jt.parent = mover;
       jt.offset = rel * s.origin;
-      jt.axis = s.axis * (1.0 / nrm);
+      jt.axis = V3<double>(s.axis[0] / nrm, s.axis[1] / nrm, s.axis[2] / nrm);  // model.cpp:325 (spec.axis / norm)
       jt.limits = s.limits;
       const int idx = (int)m.joints.size();
       m.joints.push_back(jt);

@@ -1,0 +1,643 @@
+"""B200-native batched rigid-body dynamics (the vecdyn hot path on sm_100a).
+
+Python mirror of the reference C++ API (proj/core/include/vecdyn/*.hpp) over
+the C-ABI in include/vecdyn_cuda.h.  Names, argument order and error types
+follow the reference:
+
+  robots.chain7() / humanoid23() / tree29() / by_name()      robots.cpp:12-32
+  urdf.load_model(path) / load_model_from_string(text)       urdf.cpp:384-390
+  RobotModel (dof, joints, frames, ancestor_mask, ...)        model.hpp:90-149
+  floating_base(model)                                       model.cpp:289-331
+  GravitySpec.standard() / zero() / from_field()              dynamics.hpp:194-205
+  rnea, crba, gravity_vector, coriolis_vector,
+  forward_dynamics (ABA), forward_kinematics,
+  frame_transform, geometric_jacobian, osc_step               kinematics/dynamics/control.hpp
+  StateBatch, random_states, batch_rnea, batch_crba,
+  batch_forward_dynamics                                     batch.hpp:15-165
+
+Batched device functions take CUDA torch tensors shaped (N, n) and return
+(N, K) tensors; storage is the reference's column-major SoA (element (i, k)
+at k*N + i), so results are views of (K, N) row-major buffers.  PyTorch is
+used only for device memory and streams; all arithmetic runs in the
+hand-written kernels of libvecdyn_cuda.so.
+"""
+import ctypes
+import math
+
+import numpy as np
+
+from . import _lib
+from ._lib import VD_F32, VD_F64
+
+__all__ = [
+    "Error", "DimensionError", "ModelError", "UnknownFrameError", "ParseError", "UnsupportedFeatureError",
+    "UnsupportedStructureError", "SingularInertiaError", "CudaError", "RobotModel", "DeviceModel", "GravitySpec",
+    "TaskGains", "TaskTarget", "PostureGains", "StateBatch", "robots", "urdf", "floating_base", "random_states",
+    "rnea", "bias_forces", "gravity_vector", "coriolis_vector", "crba", "forward_dynamics", "dynamics",
+    "forward_kinematics", "frame_transform", "geometric_jacobian", "osc_step", "batch_rnea", "batch_crba",
+    "batch_forward_dynamics", "shard_range",
+]
+
+
+# ------------------------------------------------------------------ errors (errors.hpp:9-61)
+class Error(RuntimeError):
+    pass
+
+
+class DimensionError(Error):
+    pass
+
+
+class ModelError(Error):
+    pass
+
+
+class UnknownFrameError(ModelError):
+    pass
+
+
+class ParseError(Error):
+    def __init__(self, message, line=0, column=0):
+        super().__init__(message)
+        self.line = line
+        self.column = column
+
+
+class UnsupportedFeatureError(Error):
+    pass
+
+
+class UnsupportedStructureError(Error):
+    pass
+
+
+class SingularInertiaError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+_CODES = {1: DimensionError, 2: ParseError, 3: ModelError, 4: UnknownFrameError, 5: UnsupportedFeatureError,
+          6: UnsupportedStructureError, 7: SingularInertiaError, 8: CudaError, 9: ValueError, 10: Error, 11: Error}
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    lib = _lib.load()
+    msg = (lib.vd_last_error() or b"").decode()
+    cls = _CODES.get(rc, Error)
+    if cls is ParseError:
+        raise ParseError(msg, lib.vd_last_error_line(), lib.vd_last_error_column())
+    raise cls(msg)
+
+
+def _buf(n):
+    return ctypes.create_string_buffer(n)
+
+
+# ------------------------------------------------------------------ model (host)
+class RobotModel:
+    """Immutable kinematic tree (model.hpp:90-149), owned by the C library."""
+
+    def __init__(self, handle):
+        self._h = ctypes.c_void_p(handle)
+        self._lib = _lib.load()
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.vd_model_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def dof(self):
+        return self._lib.vd_model_dof(self._h)
+
+    @property
+    def name(self):
+        b = _buf(256)
+        _check(self._lib.vd_model_name(self._h, b, 256))
+        return b.value.decode()
+
+    def max_depth(self):
+        return self._lib.vd_model_max_depth(self._h)
+
+    def is_serial_chain(self):
+        return bool(self._lib.vd_model_is_serial_chain(self._h))
+
+    def total_mass(self):
+        return self._lib.vd_model_total_mass(self._h)
+
+    def warnings(self):
+        out = []
+        for k in range(self._lib.vd_model_warning_count(self._h)):
+            b = _buf(512)
+            _check(self._lib.vd_model_warning(self._h, k, b, 512))
+            out.append(b.value.decode())
+        return out
+
+    def parents(self):
+        n = self.dof()
+        arr = (ctypes.c_int * max(n, 1))()
+        _check(self._lib.vd_model_parents(self._h, arr))
+        return list(arr[:n])
+
+    def joint_names(self):
+        out = []
+        for i in range(self.dof()):
+            b = _buf(256)
+            _check(self._lib.vd_model_joint_name(self._h, i, b, 256))
+            out.append(b.value.decode())
+        return out
+
+    def joint_index(self, name):
+        return self._lib.vd_model_joint_index(self._h, name.encode())
+
+    def joint(self, i):
+        """(type 0 revolute / 1 prismatic, axis[3], offset[12] R col-major + p, inertia 6x6)."""
+        t = ctypes.c_int()
+        ax = (ctypes.c_double * 3)()
+        off = (ctypes.c_double * 12)()
+        I = (ctypes.c_double * 36)()
+        _check(self._lib.vd_model_joint(self._h, i, ctypes.byref(t), ax, off, I))
+        return t.value, np.array(ax[:]), np.array(off[:]), np.array(I[:]).reshape(6, 6)
+
+    def ancestor_mask(self):
+        n = self.dof()
+        m = (ctypes.c_double * max(n * n, 1))()
+        _check(self._lib.vd_model_ancestor_mask(self._h, m))
+        return np.array(m[: n * n]).reshape(n, n, order="F")
+
+    def frames(self):
+        out = []
+        for k in range(self._lib.vd_model_frame_count(self._h)):
+            b = _buf(256)
+            j = ctypes.c_int()
+            off = (ctypes.c_double * 12)()
+            _check(self._lib.vd_model_frame(self._h, k, b, 256, ctypes.byref(j), off))
+            out.append((b.value.decode(), j.value, np.array(off[:])))
+        return out
+
+    def has_frame(self, name):
+        return any(f[0] == name for f in self.frames())
+
+    def frame_index(self, name):
+        out = ctypes.c_int()
+        _check(self._lib.vd_model_frame_index(self._h, name.encode(), ctypes.byref(out)))
+        return out.value
+
+    def fingerprint(self):
+        return self._lib.vdi_model_fingerprint(self._h)
+
+
+def _new_model(fn, *args):
+    h = ctypes.c_void_p()
+    _check(fn(*args, ctypes.byref(h)))
+    return RobotModel(h.value)
+
+
+class _Robots:
+    """robots.hpp:11-20."""
+
+    def by_name(self, name):
+        return _new_model(_lib.load().vd_model_builtin, name.encode())
+
+    def chain7(self):
+        return self.by_name("chain7")
+
+    def humanoid23(self):
+        return self.by_name("humanoid23")
+
+    def tree29(self):
+        return self.by_name("tree29")
+
+    def names(self):
+        return ["chain7", "humanoid23", "tree29"]
+
+
+class _Urdf:
+    """urdf.hpp:66-71 (load entry points)."""
+
+    def load_model(self, path):
+        return _new_model(_lib.load().vd_model_load_urdf, path.encode())
+
+    def load_model_from_string(self, text):
+        data = text.encode() if isinstance(text, str) else text
+        return _new_model(_lib.load().vd_model_load_urdf_string, data, len(data))
+
+
+robots = _Robots()
+urdf = _Urdf()
+
+
+def floating_base(model):
+    return _new_model(_lib.load().vd_model_floating_base, model.handle)
+
+
+# ------------------------------------------------------------------ gravity / control structs
+class GravitySpec:
+    """a_g = −field; default (0, 0, +9.81) (dynamics.hpp:194-205)."""
+
+    def __init__(self, linear_accel=(0.0, 0.0, 9.81)):
+        self.accel = tuple(float(x) for x in linear_accel)
+
+    @staticmethod
+    def standard():
+        return GravitySpec()
+
+    @staticmethod
+    def zero():
+        return GravitySpec((0.0, 0.0, 0.0))
+
+    @staticmethod
+    def from_field(field):
+        return GravitySpec(tuple(-float(x) for x in field))
+
+    def c(self):
+        return (ctypes.c_double * 3)(*self.accel)
+
+
+class TaskGains:
+    """control.hpp:12-22 (angular first)."""
+
+    def __init__(self, kp=(0.0,) * 6, kd=(0.0,) * 6):
+        self.kp = [float(x) for x in kp]
+        self.kd = [float(x) for x in kd]
+
+    @staticmethod
+    def uniform(kp, kd=0.0):
+        return TaskGains((kp,) * 6, (kd,) * 6)
+
+
+class TaskTarget:
+    """control.hpp:25-37; pose = (R 3x3, p 3)."""
+
+    def __init__(self, frame, pose, gains=None, accel_ff=(0.0,) * 6, twist_ff=(0.0,) * 6):
+        self.frame = frame
+        self.pose = (np.asarray(pose[0], dtype=np.float64).reshape(3, 3), np.asarray(pose[1], dtype=np.float64))
+        self.gains = gains or TaskGains()
+        self.accel_ff = [float(x) for x in accel_ff]
+        self.twist_ff = [float(x) for x in twist_ff]
+
+
+class PostureGains:
+    def __init__(self, kp=0.0, kd=0.0):
+        self.kp = float(kp)
+        self.kd = float(kd)
+
+
+# ------------------------------------------------------------------ device model
+class DeviceModel:
+    """The model packed and uploaded to one GPU (compile-time specialised when it
+    matches a builtin robot)."""
+
+    def __init__(self, model, device=0, generic=False):
+        self.model = model
+        self.device = int(device)
+        self._lib = _lib.load()
+        h = ctypes.c_void_p()
+        _check(self._lib.vd_device_model_create(model.handle, self.device, ctypes.byref(h)))
+        self._h = h
+        if generic:
+            _check(self._lib.vd_device_model_set_generic(self._h, 1))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.vd_device_model_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def dof(self):
+        return self._lib.vd_device_model_dof(self._h)
+
+    def specialization(self):
+        return self._lib.vd_device_model_specialization(self._h)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _dtype_code(t):
+    torch = _torch()
+    if t.dtype == torch.float64:
+        return VD_F64
+    if t.dtype == torch.float32:
+        return VD_F32
+    raise TypeError("tensors must be float64 or float32")
+
+
+def _soa(x, n, name, dtype=None, device=None):
+    """(N, n) tensor -> (n, N) contiguous plane buffer on the model's device."""
+    torch = _torch()
+    if not torch.is_tensor(x):
+        x = torch.as_tensor(np.asarray(x))
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    if x.dim() != 2 or x.shape[1] != n:
+        raise DimensionError(f"{name} has shape {tuple(x.shape)}, model has {n} dof")
+    if dtype is not None and x.dtype != dtype:
+        x = x.to(dtype)
+    if device is not None and x.device != device:
+        x = x.to(device)
+    if not x.is_cuda:
+        raise CudaError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    return x.t().contiguous()
+
+
+def _stream(dev):
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _prep(dm, q, *others):
+    torch = _torch()
+    n = dm.dof()
+    if not torch.is_tensor(q):
+        q = torch.as_tensor(np.asarray(q))
+    dev = torch.device("cuda", dm.device) if not q.is_cuda else q.device
+    qs = _soa(q, n, "q", device=dev)
+    rest = [None if o is None else _soa(o, n, nm, dtype=qs.dtype, device=dev) for o, nm in others]
+    return qs, rest, qs.shape[1], dev
+
+
+def _out(dev, dtype, K, N):
+    torch = _torch()
+    return torch.empty((K, N), dtype=dtype, device=dev)
+
+
+def _fext_planes(fext, N, n, dtype, dev):
+    """fext: (N, n, 6) or (n, 6) world Plücker wrenches -> (6n, N) planes."""
+    if fext is None:
+        return None
+    torch = _torch()
+    f = torch.as_tensor(fext, dtype=dtype, device=dev)
+    if f.dim() == 2:
+        f = f.unsqueeze(0).expand(N, -1, -1)
+    if tuple(f.shape) != (N, n, 6):
+        raise DimensionError(f"external forces have shape {tuple(f.shape)}, expected ({N}, {n}, 6)")
+    return f.reshape(N, 6 * n).t().contiguous()
+
+
+def _p(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def rnea(dm, q, qd, qdd, gravity=None, fext=None):
+    """rnea(model, q, qd, qdd, gravity, fext) — dynamics.hpp:405-422; (N, n) torques."""
+    qs, (qds, qdds), N, dev = _prep(dm, q, (qd, "qd"), (qdd, "qdd"))
+    n = dm.dof()
+    out = _out(dev, qs.dtype, n, N)
+    fx = _fext_planes(fext, N, n, qs.dtype, dev)
+    g = (gravity or GravitySpec.standard()).c()
+    _check(_lib.load().vd_rnea(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(qdds), N, g, _p(fx), _p(out), N,
+                               _stream(dev)))
+    return out.t()
+
+
+def bias_forces(dm, q, qd, gravity=None, fext=None):
+    """c + g (− Σ Jᵀ f_ext) = rnea(q, qd, 0) (dynamics.hpp:434-435)."""
+    qs, (qds,), N, dev = _prep(dm, q, (qd, "qd"))
+    n = dm.dof()
+    out = _out(dev, qs.dtype, n, N)
+    fx = _fext_planes(fext, N, n, qs.dtype, dev)
+    g = (gravity or GravitySpec.standard()).c()
+    _check(_lib.load().vd_bias(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), N, g, _p(fx), _p(out), N, _stream(dev)))
+    return out.t()
+
+
+def gravity_vector(dm, q, gravity=None):
+    """dynamics.hpp:557-563."""
+    qs, _, N, dev = _prep(dm, q)
+    out = _out(dev, qs.dtype, dm.dof(), N)
+    g = (gravity or GravitySpec.standard()).c()
+    _check(_lib.load().vd_gravity(dm.handle, _dtype_code(qs), N, _p(qs), N, g, _p(out), N, _stream(dev)))
+    return out.t()
+
+
+def coriolis_vector(dm, q, qd):
+    """dynamics.hpp:565-571."""
+    qs, (qds,), N, dev = _prep(dm, q, (qd, "qd"))
+    out = _out(dev, qs.dtype, dm.dof(), N)
+    _check(_lib.load().vd_coriolis(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), N, _p(out), N, _stream(dev)))
+    return out.t()
+
+
+def crba(dm, q):
+    """crba(model, q) — dynamics.hpp:507-520; returns (N, n, n)."""
+    qs, _, N, dev = _prep(dm, q)
+    n = dm.dof()
+    out = _out(dev, qs.dtype, n * n, N)
+    _check(_lib.load().vd_crba(dm.handle, _dtype_code(qs), N, _p(qs), N, _p(out), N, _stream(dev)))
+    return out.t().reshape(N, n, n).transpose(1, 2)
+
+
+def forward_dynamics(dm, q, qd, tau, gravity=None, fext=None, return_status=False):
+    """forward_dynamics (dynamics.hpp:421-444) by the articulated-body algorithm.
+    Raises SingularInertiaError when any instance is singular (the reference's
+    LLT failure) unless return_status=True."""
+    torch = _torch()
+    qs, (qds, taus), N, dev = _prep(dm, q, (qd, "qd"), (tau, "tau"))
+    n = dm.dof()
+    out = _out(dev, qs.dtype, n, N)
+    status = torch.zeros(N, dtype=torch.int32, device=dev)
+    fx = _fext_planes(fext, N, n, qs.dtype, dev)
+    g = (gravity or GravitySpec.standard()).c()
+    _check(_lib.load().vd_aba(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(taus), N, g, _p(fx), _p(out), N,
+                              _p(status), _stream(dev)))
+    if return_status:
+        return out.t(), status
+    if N and int(status.max().item()) != 0:
+        raise SingularInertiaError(
+            "forward_dynamics: mass matrix is not positive definite (zero-inertia degree of freedom?)")
+    return out.t()
+
+
+def dynamics(dm, q, qd, tau, gravity=None):
+    """Fused M, bias and q̈ (BASELINE config 3); returns (M (N,n,n), bias (N,n), qdd (N,n), status)."""
+    torch = _torch()
+    qs, (qds, taus), N, dev = _prep(dm, q, (qd, "qd"), (tau, "tau"))
+    n = dm.dof()
+    M = _out(dev, qs.dtype, n * n, N)
+    b = _out(dev, qs.dtype, n, N)
+    a = _out(dev, qs.dtype, n, N)
+    status = torch.zeros(N, dtype=torch.int32, device=dev)
+    g = (gravity or GravitySpec.standard()).c()
+    _check(_lib.load().vd_dynamics(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(taus), N, g, _p(M), _p(b), _p(a),
+                                   N, _p(status), _stream(dev)))
+    return M.t().reshape(N, n, n).transpose(1, 2), b.t(), a.t(), status
+
+
+def forward_kinematics(dm, q):
+    """kinematics.hpp:43-56: (N, n, 12) with R column-major then p."""
+    qs, _, N, dev = _prep(dm, q)
+    n = dm.dof()
+    out = _out(dev, qs.dtype, 12 * n, N)
+    _check(_lib.load().vd_fk(dm.handle, _dtype_code(qs), N, _p(qs), N, _p(out), N, _stream(dev)))
+    return out.t().reshape(N, n, 12)
+
+
+def _frame_id(dm, frame):
+    return frame if isinstance(frame, int) else dm.model.frame_index(frame)
+
+
+def frame_transform(dm, q, frame):
+    """kinematics.hpp:89-102: (N, 12) pose, R column-major then p."""
+    qs, _, N, dev = _prep(dm, q)
+    out = _out(dev, qs.dtype, 12, N)
+    _check(_lib.load().vd_jacobian(dm.handle, _dtype_code(qs), N, _p(qs), N, _frame_id(dm, frame), _p(out), None, N,
+                                   _stream(dev)))
+    return out.t()
+
+
+def geometric_jacobian(dm, q, frame):
+    """kinematics.hpp:108-136: (N, 6, n)."""
+    qs, _, N, dev = _prep(dm, q)
+    n = dm.dof()
+    out = _out(dev, qs.dtype, 6 * n, N)
+    _check(_lib.load().vd_jacobian(dm.handle, _dtype_code(qs), N, _p(qs), N, _frame_id(dm, frame), None, _p(out), N,
+                                   _stream(dev)))
+    return out.t().reshape(N, n, 6).transpose(1, 2)
+
+
+def osc_step(dm, q, qd, target, posture, posture_gains, gravity=None, epsilon=1e-6, return_lambda=False,
+             return_status=False):
+    """osc_step (control.hpp:108-155) for a batch sharing one target/posture."""
+    torch = _torch()
+    qs, (qds,), N, dev = _prep(dm, q, (qd, "qd"))
+    n = dm.dof()
+    P = _lib.OscParams()
+    P.frame = _frame_id(dm, target.frame)
+    R, p = target.pose
+    for c in range(3):
+        for r in range(3):
+            P.target[c * 3 + r] = float(R[r][c])
+    for k in range(3):
+        P.target[9 + k] = float(p[k])
+    for k in range(6):
+        P.kp[k] = target.gains.kp[k]
+        P.kd[k] = target.gains.kd[k]
+        P.accel_ff[k] = target.accel_ff[k]
+    post = (ctypes.c_double * max(n, 1))(*[float(x) for x in np.asarray(posture, dtype=np.float64).reshape(-1)])
+    P.posture = ctypes.cast(post, _lib.Pd)
+    P.posture_kp = posture_gains.kp
+    P.posture_kd = posture_gains.kd
+    g = (gravity or GravitySpec.standard()).accel
+    for k in range(3):
+        P.gravity[k] = g[k]
+    P.epsilon = float(epsilon)
+    tau = _out(dev, qs.dtype, n, N)
+    lam = _out(dev, qs.dtype, 36, N) if return_lambda else None
+    status = torch.zeros(N, dtype=torch.int32, device=dev)
+    _check(_lib.load().vd_osc(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), N, ctypes.byref(P), _p(tau), _p(lam), N,
+                              _p(status), _stream(dev)))
+    if not return_status and N and int(status.max().item()) != 0:
+        raise SingularInertiaError("osc_step: mass matrix is not positive definite")
+    out = [tau.t()]
+    if return_lambda:
+        out.append(lam.t().reshape(N, 6, 6).transpose(1, 2))
+    if return_status:
+        out.append(status)
+    return out[0] if len(out) == 1 else tuple(out)
+
+
+# ------------------------------------------------------------------ batch layer (batch.hpp)
+class StateBatch:
+    """batch.hpp:15-45; arrays are (N, n) float64, column-major (Fortran) order."""
+
+    def __init__(self, q, qd, qdd=None, tau=None):
+        self.q, self.qd, self.qdd, self.tau = q, qd, qdd, tau
+
+    def size(self):
+        return int(self.q.shape[0])
+
+    def validate(self, model):
+        n = model.dof()
+        if self.q.shape[1] != n:
+            raise DimensionError(f"StateBatch: q has {self.q.shape[1]} columns, model has {n} dof")
+        for name in ("qd", "qdd", "tau"):
+            m = getattr(self, name)
+            if m is not None and m.size and m.shape != self.q.shape:
+                raise DimensionError(f"StateBatch: {name} is {m.shape[0]}x{m.shape[1]}, expected "
+                                     f"{self.q.shape[0]}x{n}")
+
+
+def random_states(model, count, seed, with_qdd=True, with_tau=False):
+    """batch.hpp:48-75 — bit-identical mt19937_64 stream."""
+    n = model.dof()
+    arrs = [np.empty((count, n), dtype=np.float64, order="F") for _ in range(4)]
+    q, qd, qdd, tau = arrs
+    ptr = lambda a, on: ctypes.c_void_p(a.ctypes.data if on else 0)  # noqa: E731
+    _check(_lib.load().vd_random_states(model.handle, count, seed, ptr(q, True), ptr(qd, True), ptr(qdd, with_qdd),
+                                        ptr(tau, with_tau)))
+    return StateBatch(q, qd, qdd if with_qdd else None, tau if with_tau else None)
+
+
+def _host_f(a):
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _devices(devices):
+    if devices is None:
+        devices = [0]
+    arr = (ctypes.c_int * len(devices))(*devices)
+    return arr, len(devices)
+
+
+def batch_rnea(model, batch, gravity=None, devices=None):
+    """batch.hpp:128-138 with a device list instead of `workers`."""
+    batch.validate(model)
+    N, n = batch.size(), model.dof()
+    out = np.empty((N, n), dtype=np.float64, order="F")
+    q, qd, qdd = _host_f(batch.q), _host_f(batch.qd), _host_f(batch.qdd)
+    d, nd = _devices(devices)
+    g = (gravity or GravitySpec.standard()).c()
+    _check(_lib.load().vd_batch_rnea_host(model.handle, N, q.ctypes.data, qd.ctypes.data, qdd.ctypes.data, g,
+                                          out.ctypes.data, d, nd))
+    return out
+
+
+def batch_crba(model, batch, devices=None):
+    """batch.hpp:141-151: rows are column-major flattened n x n matrices."""
+    batch.validate(model)
+    N, n = batch.size(), model.dof()
+    out = np.empty((N, n * n), dtype=np.float64, order="F")
+    q = _host_f(batch.q)
+    d, nd = _devices(devices)
+    _check(_lib.load().vd_batch_crba_host(model.handle, N, q.ctypes.data, out.ctypes.data, d, nd))
+    return out
+
+
+def batch_forward_dynamics(model, batch, gravity=None, devices=None):
+    """batch.hpp:154-165 (ABA on the device)."""
+    batch.validate(model)
+    N, n = batch.size(), model.dof()
+    out = np.empty((N, n), dtype=np.float64, order="F")
+    q, qd, tau = _host_f(batch.q), _host_f(batch.qd), _host_f(batch.tau)
+    d, nd = _devices(devices)
+    g = (gravity or GravitySpec.standard()).c()
+    _check(_lib.load().vd_batch_forward_dynamics_host(model.handle, N, q.ctypes.data, qd.ctypes.data, tau.ctypes.data,
+                                                      g, out.ctypes.data, None, d, nd))
+    return out
+
+
+def shard_range(N, world, rank):
+    """Contiguous shard of N instances for `rank` of `world` (batch.hpp:111-119 rule)."""
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.load().vd_shard_range(N, world, rank, ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value
+
+
+# Fail loudly at import time when the native library is absent.
+_lib.load()
+_ = math

@@ -1,0 +1,588 @@
+// C-ABI implementation (include/vecdyn_cuda.h).  Host-side argument checking,
+// model handles, device-model upload, kernel dispatch and the multi-device
+// host batch path.  No CPU fallback exists: every numeric entry point runs
+// the sm_100a kernels or fails with VD_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/vecdyn_cuda.h"
+#include "vd_shared.hpp"
+#include "vd_host.hpp"
+#include "vd_launch.hpp"
+
+struct vd_model_s {
+  vdh::Model m;
+};
+
+struct vd_device_model_s {
+  int device = 0;
+  int n = 0;
+  int spec = 0;
+  bool force_generic = false;
+  vdh::PackedModel pm;
+  void* d64 = nullptr;  // DevModel<double>*
+  void* d32 = nullptr;  // DevModel<float>*
+};
+
+namespace {
+
+thread_local std::string g_msg;
+thread_local int g_line = 0, g_col = 0;
+
+int set_error(int code, const std::string& msg, int line = 0, int col = 0) {
+  g_msg = msg;
+  g_line = line;
+  g_col = col;
+  return code;
+}
+int from_failure(const vdh::Failure& f) { return set_error(f.code, f.what(), f.line, f.column); }
+int cuda_fail(cudaError_t e, const char* where) {
+  return set_error(VD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+void copy_str(const std::string& s, char* buf, size_t len) {
+  if (buf && len) std::snprintf(buf, len, "%s", s.c_str());
+}
+void pose_to_colmajor(const vdh::Pose& x, double* out12) {
+  for (int c = 0; c < 3; ++c)
+    for (int r = 0; r < 3; ++r) out12[c * 3 + r] = x.R[r * 3 + c];
+  for (int r = 0; r < 3; ++r) out12[9 + r] = x.p[r];
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const vdh::Failure& e) {
+    return from_failure(e);
+  } catch (const std::bad_alloc&) {
+    return set_error(VD_ERR_GENERIC, "out of host memory");
+  } catch (const std::exception& e) {
+    return set_error(VD_ERR_GENERIC, e.what());
+  }
+}
+
+template <class T>
+void fill_dev_model(const vdh::PackedModel& pm, vdk::DevModel<T>& d) {
+  std::memset(&d, 0, sizeof d);
+  d.n = pm.n;
+  for (int i = 0; i < pm.n; ++i) {
+    d.parent[i] = pm.parent[i];
+    d.kind[i] = pm.kind[i];
+    d.axis_code[i] = pm.axis_code[i];
+    d.depth[i] = pm.parent[i] < 0 ? 1 : d.depth[pm.parent[i]] + 1;
+    d.anc[i] = (1ull << i) | (pm.parent[i] < 0 ? 0ull : d.anc[pm.parent[i]]);
+    for (int k = 0; k < 3; ++k) {
+      d.axis[i][k] = T(pm.axis[i][k]);
+      d.p[i][k] = T(pm.p[i][k]);
+    }
+    for (int k = 0; k < 9; ++k) d.R[i][k] = T(pm.R[i][k]);
+    for (int k = 0; k < 10; ++k) d.I[i][k] = T(pm.inertia[i][k]);
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int check_common(vd_device_model dm, int dtype, int64_t N, int64_t ld_in, int64_t ld_out) {
+  if (!dm) return set_error(VD_ERR_INVALID_ARGUMENT, "null device model");
+  if (dtype != VD_F64 && dtype != VD_F32) return set_error(VD_ERR_INVALID_ARGUMENT, "dtype must be VD_F64 or VD_F32");
+  if (N < 0) return set_error(VD_ERR_DIMENSION, "negative batch size");
+  if (N > 0 && (ld_in < N || ld_out < N))
+    return set_error(VD_ERR_DIMENSION, "leading dimension smaller than the batch size");
+  return VD_OK;
+}
+#define VD_NEED(ptr, what)                                                  \
+  do {                                                                      \
+    if (N > 0 && dm->n > 0 && !(ptr)) return set_error(VD_ERR_INVALID_ARGUMENT, "null " what " buffer"); \
+  } while (0)
+
+vdk::Launch make_launch(vd_device_model dm, int dtype, int64_t N, int64_t ldi, int64_t ldo, void* stream) {
+  vdk::Launch L;
+  L.spec = dm->force_generic ? vdk::kGeneric : dm->spec;
+  L.dtype = dtype;
+  L.n = dm->n;
+  L.model = dtype == VD_F64 ? dm->d64 : dm->d32;
+  L.N = N;
+  L.ld_in = ldi;
+  L.ld_out = ldo;
+  L.stream = stream;
+  return L;
+}
+int finish(int rc, const char* where) {
+  if (rc != 0) return cuda_fail((cudaError_t)rc, where);
+  return VD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vd_last_error(void) { return g_msg.c_str(); }
+int vd_last_error_line(void) { return g_line; }
+int vd_last_error_column(void) { return g_col; }
+const char* vd_version(void) { return "vecdyn-b200 0.1 (sm_100a)"; }
+
+// ------------------------------------------------------------------ host model
+int vd_model_builtin(const char* name, vd_model* out) {
+  if (!name || !out) return set_error(VD_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    *out = new vd_model_s{vdh::builtin(name)};
+    return VD_OK;
+  });
+}
+int vd_model_load_urdf(const char* path, vd_model* out) {
+  if (!path || !out) return set_error(VD_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    *out = new vd_model_s{vdh::load_urdf_file(path)};
+    return VD_OK;
+  });
+}
+int vd_model_load_urdf_string(const char* text, size_t len, vd_model* out) {
+  if (!text || !out) return set_error(VD_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    *out = new vd_model_s{vdh::load_urdf_text(std::string_view(text, len))};
+    return VD_OK;
+  });
+}
+int vd_model_floating_base(vd_model m, vd_model* out) {
+  if (!m || !out) return set_error(VD_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    *out = new vd_model_s{vdh::with_floating_base(m->m)};
+    return VD_OK;
+  });
+}
+void vd_model_destroy(vd_model m) { delete m; }
+int vd_model_dof(vd_model m) { return m ? m->m.dof() : -1; }
+int vd_model_max_depth(vd_model m) { return m ? m->m.max_depth : -1; }
+int vd_model_is_serial_chain(vd_model m) { return m ? (m->m.serial ? 1 : 0) : -1; }
+double vd_model_total_mass(vd_model m) { return m ? m->m.total_mass : NAN; }
+int vd_model_warning_count(vd_model m) { return m ? (int)m->m.warnings.size() : -1; }
+int vd_model_warning(vd_model m, int k, char* buf, size_t len) {
+  if (!m || k < 0 || k >= (int)m->m.warnings.size()) return set_error(VD_ERR_INVALID_ARGUMENT, "bad warning index");
+  copy_str(m->m.warnings[(size_t)k], buf, len);
+  return VD_OK;
+}
+int vd_model_name(vd_model m, char* buf, size_t len) {
+  if (!m) return set_error(VD_ERR_INVALID_ARGUMENT, "null model");
+  copy_str(m->m.name, buf, len);
+  return VD_OK;
+}
+int vd_model_parents(vd_model m, int* parents) {
+  if (!m || !parents) return set_error(VD_ERR_INVALID_ARGUMENT, "null argument");
+  for (int i = 0; i < m->m.dof(); ++i) parents[i] = m->m.bodies[(size_t)i].parent;
+  return VD_OK;
+}
+int vd_model_joint_name(vd_model m, int i, char* buf, size_t len) {
+  if (!m || i < 0 || i >= m->m.dof()) return set_error(VD_ERR_INVALID_ARGUMENT, "bad joint index");
+  copy_str(m->m.bodies[(size_t)i].name, buf, len);
+  return VD_OK;
+}
+int vd_model_joint_index(vd_model m, const char* name) {
+  if (!m || !name) return -1;
+  for (int i = 0; i < m->m.dof(); ++i)
+    if (m->m.bodies[(size_t)i].name == name) return i;
+  return -1;
+}
+int vd_model_joint(vd_model m, int i, int* type, double axis[3], double offset[12], double inertia[36]) {
+  if (!m || i < 0 || i >= m->m.dof()) return set_error(VD_ERR_INVALID_ARGUMENT, "bad joint index");
+  const vdh::Body& b = m->m.bodies[(size_t)i];
+  if (type) *type = b.kind == vdh::Kind::Revolute ? 0 : 1;
+  if (axis)
+    for (int k = 0; k < 3; ++k) axis[k] = b.axis[k];
+  if (offset) pose_to_colmajor(b.offset, offset);
+  if (inertia)
+    for (int k = 0; k < 36; ++k) inertia[k] = b.inertia[k];
+  return VD_OK;
+}
+int vd_model_ancestor_mask(vd_model m, double* mask) {
+  if (!m || !mask) return set_error(VD_ERR_INVALID_ARGUMENT, "null argument");
+  const int n = m->m.dof();
+  for (int c = 0; c < n; ++c)
+    for (int r = 0; r < n; ++r) {
+      bool anc = false;
+      for (int j = r; j >= 0; j = m->m.bodies[(size_t)j].parent)
+        if (j == c) anc = true;
+      mask[c * n + r] = anc ? 1.0 : 0.0;
+    }
+  return VD_OK;
+}
+int vd_model_frame_count(vd_model m) { return m ? (int)m->m.frames.size() : -1; }
+int vd_model_frame(vd_model m, int k, char* name, size_t len, int* joint, double offset[12]) {
+  if (!m || k < 0 || k >= (int)m->m.frames.size()) return set_error(VD_ERR_INVALID_ARGUMENT, "bad frame index");
+  const vdh::NamedFrame& f = m->m.frames[(size_t)k];
+  copy_str(f.name, name, len);
+  if (joint) *joint = f.joint;
+  if (offset) pose_to_colmajor(f.offset, offset);
+  return VD_OK;
+}
+int vd_model_frame_index(vd_model m, const char* name, int* out) {
+  if (!m || !name || !out) return set_error(VD_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    *out = m->m.frame_index(name);
+    return VD_OK;
+  });
+}
+
+int vd_random_states(vd_model m, int64_t N, uint64_t seed, double* q, double* qd, double* qdd, double* tau) {
+  if (!m || N < 0 || (N > 0 && (!q || !qd))) return set_error(VD_ERR_INVALID_ARGUMENT, "bad argument");
+  // batch.hpp:48-75: one mt19937_64 stream, per state per joint q, qd, [qdd], [tau].
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> dist(-M_PI, M_PI);
+  const int n = m->m.dof();
+  for (int64_t i = 0; i < N; ++i)
+    for (int j = 0; j < n; ++j) {
+      const int64_t k = (int64_t)j * N + i;
+      q[k] = dist(rng);
+      qd[k] = dist(rng);
+      if (qdd) qdd[k] = dist(rng);
+      if (tau) tau[k] = dist(rng);
+    }
+  return VD_OK;
+}
+
+// ------------------------------------------------------------------ device model
+int vd_device_model_create(vd_model m, int device, vd_device_model* out) {
+  if (!m || !out) return set_error(VD_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&]() -> int {
+    auto dm = std::make_unique<vd_device_model_s>();
+    dm->device = device;
+    dm->pm = vdh::pack(m->m);
+    dm->n = dm->pm.n;
+    dm->spec = vdk::match_spec(vdh::fingerprint(dm->pm), dm->pm.n);
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (device < 0 || device >= count) return set_error(VD_ERR_CUDA, "device index out of range");
+    DeviceGuard g(device);
+    auto h64 = std::make_unique<vdk::DevModel<double>>();
+    auto h32 = std::make_unique<vdk::DevModel<float>>();
+    fill_dev_model(dm->pm, *h64);
+    fill_dev_model(dm->pm, *h32);
+    if ((e = cudaMalloc(&dm->d64, sizeof(vdk::DevModel<double>))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&dm->d32, sizeof(vdk::DevModel<float>))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMemcpy(dm->d64, h64.get(), sizeof(vdk::DevModel<double>), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpy");
+    if ((e = cudaMemcpy(dm->d32, h32.get(), sizeof(vdk::DevModel<float>), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpy");
+    *out = dm.release();
+    return VD_OK;
+  });
+}
+void vd_device_model_destroy(vd_device_model dm) {
+  if (!dm) return;
+  DeviceGuard g(dm->device);
+  cudaFree(dm->d64);
+  cudaFree(dm->d32);
+  delete dm;
+}
+int vd_device_model_dof(vd_device_model dm) { return dm ? dm->n : -1; }
+int vd_device_model_specialization(vd_device_model dm) { return dm ? (dm->force_generic ? 0 : dm->spec) : -1; }
+int vd_device_model_set_generic(vd_device_model dm, int generic) {
+  if (!dm) return set_error(VD_ERR_INVALID_ARGUMENT, "null device model");
+  dm->force_generic = generic != 0;
+  return VD_OK;
+}
+
+// ------------------------------------------------------------------ kernels
+int vd_fk(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* out, int64_t ld_out,
+          void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  VD_NEED(q, "q");
+  VD_NEED(out, "output");
+  if (dm->n == 0) return VD_OK;
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_fk(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, out), "vd_fk");
+}
+
+int vd_jacobian(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, int frame, void* pose,
+                void* J, int64_t ld_out, void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  if (frame < 0 || frame >= dm->pm.nframes) return set_error(VD_ERR_UNKNOWN_FRAME, "frame index out of range");
+  VD_NEED(q, "q");
+  if (N == 0 || (!pose && !J)) return VD_OK;
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_jacobian(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, dm->pm.frame_joint[frame],
+                                     dm->pm.frame_R[frame], dm->pm.frame_p[frame], pose, dm->n ? J : nullptr),
+                "vd_jacobian");
+}
+
+static int rnea_mode(vd_device_model dm, int dtype, int mode, int64_t N, const void* q, const void* qd,
+                     const void* qdd, int64_t ld_in, const double* g3, const void* fext, void* out, int64_t ld_out,
+                     void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  VD_NEED(q, "q");
+  if (mode != 2) VD_NEED(qd, "qd");
+  if (mode == 0) VD_NEED(qdd, "qdd");
+  VD_NEED(out, "output");
+  if (dm->n == 0) return VD_OK;
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_rnea(make_launch(dm, dtype, N, ld_in, ld_out, stream), mode, q, qd, qdd, g3, fext, out),
+                "vd_rnea");
+}
+int vd_rnea(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* qdd, int64_t ld_in,
+            const double* g3, const void* fext, void* tau, int64_t ld_out, void* stream) {
+  return rnea_mode(dm, dtype, 0, N, q, qd, qdd, ld_in, g3, fext, tau, ld_out, stream);
+}
+int vd_bias(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in, const double* g3,
+            const void* fext, void* out, int64_t ld_out, void* stream) {
+  return rnea_mode(dm, dtype, 1, N, q, qd, nullptr, ld_in, g3, fext, out, ld_out, stream);
+}
+int vd_gravity(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, const double* g3, void* out,
+               int64_t ld_out, void* stream) {
+  return rnea_mode(dm, dtype, 2, N, q, nullptr, nullptr, ld_in, g3, nullptr, out, ld_out, stream);
+}
+int vd_coriolis(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in, void* out,
+                int64_t ld_out, void* stream) {
+  return rnea_mode(dm, dtype, 3, N, q, qd, nullptr, ld_in, nullptr, nullptr, out, ld_out, stream);
+}
+
+int vd_crba(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* M, int64_t ld_out,
+            void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  VD_NEED(q, "q");
+  VD_NEED(M, "M");
+  if (dm->n == 0) return VD_OK;
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_crba(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, M), "vd_crba");
+}
+
+int vd_aba(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau, int64_t ld_in,
+           const double* g3, const void* fext, void* qdd, int64_t ld_out, int32_t* status, void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  VD_NEED(q, "q");
+  VD_NEED(qd, "qd");
+  VD_NEED(tau, "tau");
+  VD_NEED(qdd, "qdd");
+  if (dm->n == 0) {
+    if (status && N > 0 && cudaMemsetAsync(status, 0, sizeof(int32_t) * N, (cudaStream_t)stream) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "vd_aba");
+    return VD_OK;
+  }
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_aba(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, qd, tau, g3, fext, qdd, status),
+                "vd_aba");
+}
+
+int vd_dynamics(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau,
+                int64_t ld_in, const double* g3, void* M, void* bias, void* qdd, int64_t ld_out, int32_t* status,
+                void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  VD_NEED(q, "q");
+  VD_NEED(qd, "qd");
+  if (qdd) VD_NEED(tau, "tau");
+  if (dm->n == 0) return VD_OK;
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_dynamics(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, qd, tau, g3, M, bias, qdd,
+                                     status),
+                "vd_dynamics");
+}
+
+int vd_osc(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in,
+           const vd_osc_params* P, void* tau, void* lambda, int64_t ld_out, int32_t* status, void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  if (!P) return set_error(VD_ERR_INVALID_ARGUMENT, "null osc parameters");
+  if (P->frame < 0 || P->frame >= dm->pm.nframes) return set_error(VD_ERR_UNKNOWN_FRAME, "frame index out of range");
+  for (int k = 0; k < 6; ++k)
+    if (P->kp[k] < 0.0 || P->kd[k] < 0.0) return set_error(VD_ERR_GENERIC, "task gains must be nonnegative");
+  if (dm->n > 0 && !P->posture) return set_error(VD_ERR_INVALID_ARGUMENT, "null posture");
+  VD_NEED(q, "q");
+  VD_NEED(qd, "qd");
+  VD_NEED(tau, "tau");
+  if (dm->n == 0) return VD_OK;
+  vdk::OscShared S;
+  std::memset(&S, 0, sizeof S);
+  const int f = P->frame;
+  S.frame_joint = dm->pm.frame_joint[f];
+  for (int k = 0; k < 9; ++k) S.frame_R[k] = dm->pm.frame_R[f][k];
+  for (int k = 0; k < 3; ++k) S.frame_p[k] = dm->pm.frame_p[f][k];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) S.target_R[r * 3 + c] = P->target[c * 3 + r];
+  for (int k = 0; k < 3; ++k) S.target_p[k] = P->target[9 + k];
+  for (int k = 0; k < 6; ++k) {
+    S.kp[k] = P->kp[k];
+    S.kd[k] = P->kd[k];
+    S.accel_ff[k] = P->accel_ff[k];
+  }
+  for (int k = 0; k < dm->n; ++k) S.posture[k] = P->posture[k];
+  S.posture_kp = P->posture_kp;
+  S.posture_kd = P->posture_kd;
+  for (int k = 0; k < 3; ++k) S.gravity[k] = P->gravity[k];
+  S.epsilon = P->epsilon;
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_osc(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, qd, S, tau, lambda, status),
+                "vd_osc");
+}
+
+// ---- internal (not in the public header): packed tables for the robot-table generator
+uint64_t vdi_model_fingerprint(vd_model m) { return m ? vdh::fingerprint(vdh::pack(m->m)) : 0; }
+int vdi_model_packed(vd_model m, int* n, int* parent, int* kind, int* axis_code, double* axis, double* R, double* p,
+                     double* inertia) {
+  if (!m) return set_error(VD_ERR_INVALID_ARGUMENT, "null model");
+  return guarded([&] {
+    const vdh::PackedModel pm = vdh::pack(m->m);
+    *n = pm.n;
+    for (int i = 0; i < pm.n; ++i) {
+      parent[i] = pm.parent[i];
+      kind[i] = pm.kind[i];
+      axis_code[i] = pm.axis_code[i];
+      for (int k = 0; k < 3; ++k) axis[i * 3 + k] = pm.axis[i][k];
+      for (int k = 0; k < 9; ++k) R[i * 9 + k] = pm.R[i][k];
+      for (int k = 0; k < 3; ++k) p[i * 3 + k] = pm.p[i][k];
+      for (int k = 0; k < 10; ++k) inertia[i * 10 + k] = pm.inertia[i][k];
+    }
+    return VD_OK;
+  });
+}
+
+int vd_shard_range(int64_t N, int world, int rank, int64_t* begin, int64_t* end) {
+  if (world <= 0 || rank < 0 || rank >= world || N < 0 || !begin || !end)
+    return set_error(VD_ERR_INVALID_ARGUMENT, "bad shard arguments");
+  // batch.hpp:111-119: chunk = ceil(count / workers), contiguous.
+  const int64_t chunk = (N + world - 1) / world;
+  *begin = std::min<int64_t>(N, (int64_t)rank * chunk);
+  *end = std::min<int64_t>(N, *begin + chunk);
+  return VD_OK;
+}
+
+// ------------------------------------------------------------------ host batch (multi-device)
+namespace {
+struct HostOp {
+  int kind;  // 0 rnea, 1 crba, 2 fd
+  int n_in;  // number of n-wide inputs
+  int out_width;
+};
+int host_batch(vd_model m, const HostOp& op, int64_t N, const double* const* inputs, const double* g3, double* out,
+               int32_t* status, const int* devices, int ndev) {
+  if (!m) return set_error(VD_ERR_INVALID_ARGUMENT, "null model");
+  if (N < 0) return set_error(VD_ERR_DIMENSION, "negative batch size");
+  const int n = m->m.dof();
+  if (N == 0 || n == 0) return VD_OK;
+  for (int k = 0; k < op.n_in; ++k)
+    if (!inputs[k]) return set_error(VD_ERR_INVALID_ARGUMENT, "null input buffer");
+  if (!out) return set_error(VD_ERR_INVALID_ARGUMENT, "null output buffer");
+  std::vector<int> devs;
+  if (devices && ndev > 0) devs.assign(devices, devices + ndev);
+  else devs.push_back(0);
+  const int W = (int)devs.size();
+  const int width = op.out_width;
+  std::vector<int> rcs((size_t)W, VD_OK);
+  std::vector<std::string> msgs((size_t)W);
+  std::vector<int> bad((size_t)W, 0);
+  auto work = [&](int w) {
+    int64_t b = 0, e = 0;
+    vd_shard_range(N, W, w, &b, &e);
+    const int64_t len = e - b;
+    if (len <= 0) return;
+    vd_device_model dm = nullptr;
+    int rc = vd_device_model_create(m, devs[(size_t)w], &dm);
+    if (rc) {
+      rcs[(size_t)w] = rc;
+      msgs[(size_t)w] = g_msg;
+      return;
+    }
+    DeviceGuard g(devs[(size_t)w]);
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    std::vector<double*> din((size_t)op.n_in, nullptr);
+    double* dout = nullptr;
+    int32_t* dst = nullptr;
+    cudaError_t ce = cudaSuccess;
+    for (int k = 0; k < op.n_in && ce == cudaSuccess; ++k) {
+      ce = cudaMallocAsync((void**)&din[(size_t)k], sizeof(double) * n * len, s);
+      if (ce == cudaSuccess)
+        ce = cudaMemcpy2DAsync(din[(size_t)k], sizeof(double) * len, inputs[k] + b, sizeof(double) * N,
+                               sizeof(double) * len, n, cudaMemcpyHostToDevice, s);
+    }
+    if (ce == cudaSuccess) ce = cudaMallocAsync((void**)&dout, sizeof(double) * width * len, s);
+    if (ce == cudaSuccess && op.kind == 2) ce = cudaMallocAsync((void**)&dst, sizeof(int32_t) * len, s);
+    if (ce != cudaSuccess) {
+      rcs[(size_t)w] = cuda_fail(ce, "host batch staging");
+      msgs[(size_t)w] = g_msg;
+    } else {
+      if (op.kind == 0)
+        rc = vd_rnea(dm, VD_F64, len, din[0], din[1], din[2], len, g3, nullptr, dout, len, s);
+      else if (op.kind == 1)
+        rc = vd_crba(dm, VD_F64, len, din[0], len, dout, len, s);
+      else
+        rc = vd_aba(dm, VD_F64, len, din[0], din[1], din[2], len, g3, nullptr, dout, len, dst, s);
+      if (rc) {
+        rcs[(size_t)w] = rc;
+        msgs[(size_t)w] = g_msg;
+      } else {
+        ce = cudaMemcpy2DAsync(out + b, sizeof(double) * N, dout, sizeof(double) * len, sizeof(double) * len, width,
+                               cudaMemcpyDeviceToHost, s);
+        std::vector<int32_t> st;
+        if (ce == cudaSuccess && dst) {
+          st.resize((size_t)len);
+          ce = cudaMemcpyAsync(st.data(), dst, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, s);
+        }
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+        if (ce != cudaSuccess) {
+          rcs[(size_t)w] = cuda_fail(ce, "host batch copy-out");
+          msgs[(size_t)w] = g_msg;
+        }
+        for (int64_t k = 0; k < (int64_t)st.size(); ++k) {
+          if (status) status[b + k] = st[(size_t)k];
+          if (st[(size_t)k]) bad[(size_t)w] = 1;
+        }
+      }
+    }
+    for (double* p : din) cudaFreeAsync(p, s);
+    cudaFreeAsync(dout, s);
+    if (dst) cudaFreeAsync(dst, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    vd_device_model_destroy(dm);
+  };
+  if (W == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int w = 0; w < W; ++w) pool.emplace_back(work, w);
+    for (auto& t : pool) t.join();
+  }
+  for (int w = 0; w < W; ++w)
+    if (rcs[(size_t)w]) return set_error(rcs[(size_t)w], msgs[(size_t)w]);
+  for (int w = 0; w < W; ++w)
+    if (bad[(size_t)w])
+      return set_error(VD_ERR_SINGULAR_INERTIA,
+                       "forward_dynamics: mass matrix is not positive definite (zero-inertia degree of freedom?)");
+  return VD_OK;
+}
+}  // namespace
+
+int vd_batch_rnea_host(vd_model m, int64_t N, const double* q, const double* qd, const double* qdd, const double* g3,
+                       double* tau, const int* devices, int n_devices) {
+  const double* in[3] = {q, qd, qdd};
+  return host_batch(m, HostOp{0, 3, m ? m->m.dof() : 0}, N, in, g3, tau, nullptr, devices, n_devices);
+}
+int vd_batch_crba_host(vd_model m, int64_t N, const double* q, double* M, const int* devices, int n_devices) {
+  const double* in[1] = {q};
+  const int n = m ? m->m.dof() : 0;
+  return host_batch(m, HostOp{1, 1, n * n}, N, in, nullptr, M, nullptr, devices, n_devices);
+}
+int vd_batch_forward_dynamics_host(vd_model m, int64_t N, const double* q, const double* qd, const double* tau,
+                                   const double* g3, double* qdd, int32_t* status, const int* devices, int n_devices) {
+  const double* in[3] = {q, qd, tau};
+  return host_batch(m, HostOp{2, 3, m ? m->m.dof() : 0}, N, in, g3, qdd, status, devices, n_devices);
+}
+
+}  // extern "C"

@@ -1,0 +1,514 @@
+// Per-instance rigid-body algorithms (one thread = one robot state), written
+// once against a model view (vd_device.cuh).  Each function cites the
+// reference routine whose semantics it reproduces.
+#pragma once
+
+#include "vd_device.cuh"
+
+namespace vdk {
+
+// SoA column-major access: element (instance i, component k) at k*ld + i.
+template <class T>
+struct Cols {
+  const T* __restrict__ base;
+  int64_t ld, i;
+  __device__ __forceinline__ T operator[](int k) const { return base ? __ldg(base + (int64_t)k * ld + i) : T(0); }
+};
+template <class T>
+struct OutCols {
+  T* __restrict__ base;
+  int64_t ld, i;
+  __device__ __forceinline__ void put(int k, T v) const { base[(int64_t)k * ld + i] = v; }
+};
+
+template <class V>
+__device__ __forceinline__ SV<typename V::S> gravity_accel(const typename V::Real* g3) {
+  using S = typename V::S;
+  SV<S> a;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    a.a[k] = S();
+    a.l[k] = S(g3[k]);
+  }
+  return a;
+}
+
+// ------------------------------------------------------------------ FK
+// forward_kinematics (kinematics.hpp:43-56) — world pose of every joint.
+template <class V>
+__device__ __forceinline__ void fk_world(const V& mv, const JM<typename V::S>* jm, WX<typename V::S>* W) {
+#pragma unroll
+  for (int i = 0; i < mv.n(); ++i) {
+    JointX<V> x;
+    x.load(mv, i, jm[i]);
+    const int p = mv.parent(i);
+    W[i] = world_of(x, p < 0 ? nullptr : &W[p]);
+  }
+}
+
+// ------------------------------------------------------------------ RNEA
+// rnea_loop (dynamics.hpp:427-482): two-pass recursion in local coordinates.
+// qdd == nullptr means q̈ = 0 (bias forces, dynamics.hpp:434-435).
+template <class V, bool kFext>
+__device__ __forceinline__ void rnea_one(const V& mv, const JM<typename V::S>* jm, const Cols<typename V::Real>& qd,
+                                         const Cols<typename V::Real>* qdd, const typename V::Real* g3,
+                                         const Cols<typename V::Real>* fext, typename V::S* tau) {
+  using S = typename V::S;
+  SV<S> v[V::kMax], a[V::kMax], f[V::kMax];
+  WX<S> W[kFext ? V::kMax : 1];
+  const SV<S> ag = gravity_accel<V>(g3);
+#pragma unroll
+  for (int i = 0; i < mv.n(); ++i) {
+    JointX<V> x;
+    x.load(mv, i, jm[i]);
+    const int p = mv.parent(i);
+    const SV<S> s = joint_axis(mv, i);
+    const SV<S> vj = scale(s, S(qd[i]));
+    if (p < 0) {
+      v[i] = vj;
+      a[i] = x.motion_to_child(ag);
+    } else {
+      v[i] = x.motion_to_child(v[p]) + vj;
+      a[i] = x.motion_to_child(a[p]) + crm(v[i], vj);
+    }
+    if (qdd) a[i] = a[i] + scale(s, S((*qdd)[i]));
+    const RB<S> I = body_inertia(mv, i);
+    f[i] = rb_apply(I, a[i]) + crf(v[i], rb_apply(I, v[i]));
+    if constexpr (kFext) {
+      W[i] = world_of(x, p < 0 ? nullptr : &W[p]);
+      SV<S> fw;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        fw.a[k] = S((*fext)[i * 6 + k]);
+        fw.l[k] = S((*fext)[i * 6 + 3 + k]);
+      }
+      f[i] = f[i] - force_in(W[i].R, W[i].p, true, fw);
+    }
+  }
+#pragma unroll
+  for (int i = mv.n() - 1; i >= 0; --i) {
+    tau[i] = sdot(f[i], joint_axis(mv, i));
+    const int p = mv.parent(i);
+    if (p >= 0) {
+      JointX<V> x;
+      x.load(mv, i, jm[i]);
+      f[p] = f[p] + x.force_to_parent(f[i]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ CRBA
+// crba_loop (dynamics.hpp:524-555): composite inertias leaf -> root, then
+// one force propagation up the ancestor chain per column.  emit(i, j, value)
+// receives M(i, j) for j = i and every ancestor j of i.
+template <class V, class Emit>
+__device__ __forceinline__ void crba_one(const V& mv, const JM<typename V::S>* jm, Emit&& emit) {
+  using S = typename V::S;
+  RB<S> ic[V::kMax];
+#pragma unroll
+  for (int i = 0; i < mv.n(); ++i) ic[i] = body_inertia(mv, i);
+#pragma unroll
+  for (int i = mv.n() - 1; i >= 0; --i) {
+    const int p = mv.parent(i);
+    if (p >= 0) {
+      JointX<V> x;
+      x.load(mv, i, jm[i]);
+      rb_add(ic[p], rb_to_parent(x, ic[i]));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < mv.n(); ++i) {
+    SV<S> F = rb_apply(ic[i], joint_axis(mv, i));
+    emit(i, i, sdot(F, joint_axis(mv, i)));
+    int j = i;
+#pragma unroll
+    for (int d = 1; d < mv.max_depth(); ++d) {
+      if (d >= mv.depth(i)) break;
+      JointX<V> x;
+      x.load(mv, j, jm[j]);
+      F = x.force_to_parent(F);
+      j = mv.parent(j);
+      emit(i, j, sdot(F, joint_axis(mv, j)));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ ABA
+// Articulated-body forward dynamics (Featherstone RBDA Table 7.1).  Not in the
+// reference; its oracle is forward_dynamics (dynamics.hpp:421-444,
+// CRBA + bias + LLT).  Returns false when an articulated pivot D_i is not
+// positive (the LLT failure of the oracle: D_i are the pivots of M's
+// tree-structured LDLᵀ factorisation) or the result is not finite.
+template <class V, bool kFext>
+__device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm, const Cols<typename V::Real>& qd,
+                                        const Cols<typename V::Real>& tau, const typename V::Real* g3,
+                                        const Cols<typename V::Real>* fext, typename V::S* qdd) {
+  using S = typename V::S;
+  using T = typename V::Real;
+  SV<S> v[V::kMax], c[V::kMax], pA[V::kMax], U[V::kMax];
+  AI<S> IA[V::kMax];
+  S u[V::kMax], dinv[V::kMax];
+  WX<S> W[kFext ? V::kMax : 1];
+  bool ok = true;
+  // pass 1: velocities, bias accelerations, isolated inertias and bias forces
+#pragma unroll
+  for (int i = 0; i < mv.n(); ++i) {
+    JointX<V> x;
+    x.load(mv, i, jm[i]);
+    const int p = mv.parent(i);
+    const SV<S> vj = scale(joint_axis(mv, i), S(qd[i]));
+    if (p < 0) {
+      v[i] = vj;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) c[i].a[k] = c[i].l[k] = S();
+    } else {
+      v[i] = x.motion_to_child(v[p]) + vj;
+      c[i] = crm(v[i], vj);
+    }
+    const RB<S> I = body_inertia(mv, i);
+    IA[i] = ai_from_rb(I);
+    pA[i] = crf(v[i], rb_apply(I, v[i]));
+    if constexpr (kFext) {
+      W[i] = world_of(x, p < 0 ? nullptr : &W[p]);
+      SV<S> fw;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        fw.a[k] = S((*fext)[i * 6 + k]);
+        fw.l[k] = S((*fext)[i * 6 + 3 + k]);
+      }
+      pA[i] = pA[i] - force_in(W[i].R, W[i].p, true, fw);
+    }
+  }
+  // pass 2: articulated inertias leaf -> root
+#pragma unroll
+  for (int i = mv.n() - 1; i >= 0; --i) {
+    const SV<S> s = joint_axis(mv, i);
+    U[i] = ai_apply(IA[i], s);
+    const S D = sdot(U[i], s);
+    ok = ok && (D.v > T(0));
+    dinv[i] = S(T(1) / D.v);
+    u[i] = S(tau[i]) - sdot(pA[i], s);
+    const int p = mv.parent(i);
+    if (p >= 0) {
+      JointX<V> x;
+      x.load(mv, i, jm[i]);
+      AI<S> Ia = IA[i];
+      ai_sub_outer(Ia, U[i], dinv[i]);
+      const SV<S> pa = pA[i] + ai_apply(Ia, c[i]) + scale(U[i], u[i] * dinv[i]);
+      ai_add(IA[p], ai_to_parent(x, Ia));
+      pA[p] = pA[p] + x.force_to_parent(pa);
+    }
+  }
+  // pass 3: accelerations root -> leaf
+  const SV<S> ag = gravity_accel<V>(g3);
+  SV<S> a[V::kMax];
+#pragma unroll
+  for (int i = 0; i < mv.n(); ++i) {
+    JointX<V> x;
+    x.load(mv, i, jm[i]);
+    const int p = mv.parent(i);
+    const SV<S> ap = x.motion_to_child(p < 0 ? ag : a[p]) + c[i];
+    qdd[i] = (u[i] - sdot(U[i], ap)) * dinv[i];
+    ok = ok && isfinite(qdd[i].v);
+    a[i] = ap + scale(joint_axis(mv, i), qdd[i]);
+  }
+  return ok;
+}
+
+// ------------------------------------------------------------------ OSC helpers
+// rotation_log (control.hpp:45-68), reference acos form and branches.
+template <class T>
+__device__ __forceinline__ void rotation_log(const T* R, T* w) {
+  const T tr = R[0] + R[4] + R[8];
+  const T anti[3] = {R[7] - R[5], R[2] - R[6], R[3] - R[1]};
+  T ca = T(0.5) * (tr - T(1));
+  ca = ca < T(-1) ? T(-1) : (ca > T(1) ? T(1) : ca);
+  const T ang = acos(ca);
+  const T pi = T(3.14159265358979323846);
+  if (ang < T(1e-9)) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) w[k] = T(0.5) * anti[k];
+    return;
+  }
+  if (ang > pi - T(1e-6)) {
+    const T sd[3] = {T(0.5) * (R[0] + T(1)), T(0.5) * (R[4] + T(1)), T(0.5) * (R[8] + T(1))};
+    int k = 0;
+    if (sd[1] > sd[k]) k = 1;
+    if (sd[2] > sd[k]) k = 2;
+    T ax[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) ax[r] = (r == k) ? sd[k] : T(0.5) * R[r * 3 + k];
+    const T inv = T(1) / sqrt(sd[k] > T(1e-12) ? sd[k] : T(1e-12));
+#pragma unroll
+    for (int r = 0; r < 3; ++r) ax[r] *= inv;
+    const T nrm = sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) ax[r] /= nrm;
+    const T sgn = (anti[0] * ax[0] + anti[1] * ax[1] + anti[2] * ax[2]) < T(0) ? T(-1) : T(1);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) w[r] = ang * sgn * ax[r];
+    return;
+  }
+  const T f = T(0.5) * ang / sin(ang);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) w[k] = f * anti[k];
+}
+
+// In-place Cholesky of a 6x6 SPD (lower, row-major), Eigen's LLT criterion.
+template <class T>
+__device__ __forceinline__ bool chol6(T* L) {
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    T x = L[k * 6 + k];
+#pragma unroll
+    for (int j = 0; j < k; ++j) x -= L[k * 6 + j] * L[k * 6 + j];
+    ok = ok && (x > T(0));
+    x = sqrt(x);
+    L[k * 6 + k] = x;
+    const T inv = T(1) / x;
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i) {
+      T s = L[i * 6 + k];
+#pragma unroll
+      for (int j = 0; j < k; ++j) s -= L[i * 6 + j] * L[k * 6 + j];
+      L[i * 6 + k] = s * inv;
+    }
+  }
+  return ok;
+}
+template <class T>
+__device__ __forceinline__ void chol6_solve(const T* L, T* b) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    T s = b[i];
+#pragma unroll
+    for (int j = 0; j < i; ++j) s -= L[i * 6 + j] * b[j];
+    b[i] = s / L[i * 6 + i];
+  }
+#pragma unroll
+  for (int i = 5; i >= 0; --i) {
+    T s = b[i];
+#pragma unroll
+    for (int j = i + 1; j < 6; ++j) s -= L[j * 6 + i] * b[j];
+    b[i] = s / L[i * 6 + i];
+  }
+}
+
+
+
+// osc_step (control.hpp:108-155).  The mass matrix is factorised with the
+// branch-sparse LTL of RBDA §6.5 (M = Lᵀ L, L with the ancestor sparsity of
+// M, no fill-in) instead of a dense LLT; both give M⁻¹ x exactly in exact
+// arithmetic, and both fail exactly when M is not positive definite.
+template <class V>
+__device__ __forceinline__ bool osc_one(const V& mv, const JM<typename V::S>* jm, const Cols<typename V::Real>& q,
+                                        const Cols<typename V::Real>& qd, const OscShared& P,
+                                        typename V::Real* tau_out, typename V::Real* lambda_out) {
+  using S = typename V::S;
+  using T = typename V::Real;
+  constexpr int NM = V::kMax;
+  bool ok = true;
+  // --- mass matrix, compact ancestor rows: Mc[i][d] = M(i, anc_d(i)), d = 0 diagonal
+  T Mc[NM][V::kMaxDepthC];
+  crba_one(mv, jm, [&](int i, int j, const S& val) {
+    // depth distance between i and its ancestor j
+    const int d = mv.depth(i) - mv.depth(j);
+    Mc[i][d] = val.v;
+  });
+  // --- bias c + g
+  S bias[NM];
+  {
+    const T g3[3] = {T(P.gravity[0]), T(P.gravity[1]), T(P.gravity[2])};
+    rnea_one<V, false>(mv, jm, qd, nullptr, g3, nullptr, bias);
+  }
+  // --- frame pose and Jacobian (kinematics.hpp:89-129)
+  WX<S> W[NM];
+  fk_world(mv, jm, W);
+  const int fj = P.frame_joint;
+  T pose_R[9], pose_p[3];
+  {
+    T WR[9], Wp[3];
+    if (fj >= 0) {
+#pragma unroll
+      for (int i = 0; i < mv.n(); ++i)
+        if (i == fj) {
+#pragma unroll
+          for (int k = 0; k < 9; ++k) WR[k] = W[i].R[k].v;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) Wp[k] = W[i].p[k].v;
+        }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) WR[k] = (k % 4 == 0) ? T(1) : T(0);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) Wp[k] = T(0);
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        pose_R[r * 3 + c] = WR[r * 3] * T(P.frame_R[c]) + WR[r * 3 + 1] * T(P.frame_R[3 + c]) +
+                            WR[r * 3 + 2] * T(P.frame_R[6 + c]);
+      pose_p[r] = WR[r * 3] * T(P.frame_p[0]) + WR[r * 3 + 1] * T(P.frame_p[1]) + WR[r * 3 + 2] * T(P.frame_p[2]) + Wp[r];
+    }
+  }
+  const uint64_t fmask = fj >= 0 ? mv.anc(fj) : 0ull;
+  T J[6][NM];
+#pragma unroll
+  for (int j = 0; j < mv.n(); ++j) {
+    const bool on = (fmask >> j) & 1ull;
+    T ax[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+      ax[r] = (W[j].R[r * 3] * mv.axis(j, 0) + W[j].R[r * 3 + 1] * mv.axis(j, 1) + W[j].R[r * 3 + 2] * mv.axis(j, 2)).v;
+    if (!on) {
+#pragma unroll
+      for (int r = 0; r < 6; ++r) J[r][j] = T(0);
+    } else if (mv.kind(j) == 0) {
+      const T d[3] = {pose_p[0] - W[j].p[0].v, pose_p[1] - W[j].p[1].v, pose_p[2] - W[j].p[2].v};
+      J[0][j] = ax[0];
+      J[1][j] = ax[1];
+      J[2][j] = ax[2];
+      J[3][j] = ax[1] * d[2] - ax[2] * d[1];
+      J[4][j] = ax[2] * d[0] - ax[0] * d[2];
+      J[5][j] = ax[0] * d[1] - ax[1] * d[0];
+    } else {
+      J[0][j] = J[1][j] = J[2][j] = T(0);
+      J[3][j] = ax[0];
+      J[4][j] = ax[1];
+      J[5][j] = ax[2];
+    }
+  }
+  // --- pose error (control.hpp:73-77): log(R_t R_cᵀ), p_t − p_c
+  T err[6];
+  {
+    T Rrel[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        Rrel[r * 3 + c] = T(P.target_R[r * 3]) * pose_R[c * 3] + T(P.target_R[r * 3 + 1]) * pose_R[c * 3 + 1] +
+                          T(P.target_R[r * 3 + 2]) * pose_R[c * 3 + 2];
+    rotation_log(Rrel, err);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) err[3 + k] = T(P.target_p[k]) - pose_p[k];
+  }
+  // --- LTL factorisation in place (RBDA Table 6.3)
+#pragma unroll
+  for (int k = mv.n() - 1; k >= 0; --k) {
+    const T dkk = Mc[k][0];
+    ok = ok && (dkk > T(0));
+    const T lkk = sqrt(dkk);
+    Mc[k][0] = lkk;
+    const T inv = T(1) / lkk;
+#pragma unroll
+    for (int d = 1; d < mv.max_depth(); ++d)
+      if (d < mv.depth(k)) Mc[k][d] *= inv;
+    // for ancestors i = anc_d(k) and j = anc_e(k), e >= d: M(i, j) -= L(k,i) L(k,j)
+    int i = k;
+#pragma unroll
+    for (int d = 1; d < mv.max_depth(); ++d) {
+      if (d >= mv.depth(k)) break;
+      i = mv.parent(i);
+#pragma unroll
+      for (int e = d; e < mv.max_depth(); ++e)
+        if (e < mv.depth(k)) Mc[i][e - d] -= Mc[k][d] * Mc[k][e];
+    }
+  }
+  // --- 7 right-hand sides: rows of J (M⁻¹ Jᵀ) and τ_post (M⁻¹ τ_post)
+  T tp[NM];
+#pragma unroll
+  for (int k = 0; k < mv.n(); ++k) tp[k] = T(P.posture_kp) * (T(P.posture[k]) - q[k]) - T(P.posture_kd) * qd[k];
+  T X[7][NM];
+#pragma unroll
+  for (int r = 0; r < 7; ++r)
+#pragma unroll
+    for (int k = 0; k < mv.n(); ++k) X[r][k] = r < 6 ? J[r][k] : tp[k];
+  // Lᵀ y = b
+#pragma unroll
+  for (int i = mv.n() - 1; i >= 0; --i) {
+    const T inv = T(1) / Mc[i][0];
+#pragma unroll
+    for (int r = 0; r < 7; ++r) X[r][i] *= inv;
+    int j = i;
+#pragma unroll
+    for (int d = 1; d < mv.max_depth(); ++d) {
+      if (d >= mv.depth(i)) break;
+      j = mv.parent(j);
+#pragma unroll
+      for (int r = 0; r < 7; ++r) X[r][j] -= Mc[i][d] * X[r][i];
+    }
+  }
+  // L x = y
+#pragma unroll
+  for (int i = 0; i < mv.n(); ++i) {
+    int j = i;
+#pragma unroll
+    for (int d = 1; d < mv.max_depth(); ++d) {
+      if (d >= mv.depth(i)) break;
+      j = mv.parent(j);
+#pragma unroll
+      for (int r = 0; r < 7; ++r) X[r][i] -= Mc[i][d] * X[r][j];
+    }
+    const T inv = T(1) / Mc[i][0];
+#pragma unroll
+    for (int r = 0; r < 7; ++r) X[r][i] *= inv;
+  }
+  // --- gram = J M⁻¹ Jᵀ, w = J M⁻¹ τ_post, J q̇
+  T gram[36], w[6], jqd[6];
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+#pragma unroll
+    for (int c = 0; c < 7; ++c) {
+      T s = T(0);
+#pragma unroll
+      for (int k = 0; k < mv.n(); ++k) s += J[r][k] * X[c][k];
+      if (c < 6) gram[r * 6 + c] = s;
+      else w[r] = s;
+    }
+    T s = T(0);
+#pragma unroll
+    for (int k = 0; k < mv.n(); ++k) s += J[r][k] * qd[k];
+    jqd[r] = s;
+  }
+  T Lr[36], Lg[36];
+#pragma unroll
+  for (int k = 0; k < 36; ++k) {
+    Lg[k] = gram[k];
+    Lr[k] = gram[k] + ((k % 7 == 0) ? T(P.epsilon) : T(0));
+  }
+  chol6(Lr);
+  const bool gram_ok = chol6(Lg);
+  T F[6], z[6];
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    F[r] = T(P.kp[r]) * err[r] - T(P.kd[r]) * jqd[r] + T(P.accel_ff[r]);
+    z[r] = w[r];
+  }
+  chol6_solve(Lr, F);
+  chol6_solve(gram_ok ? Lg : Lr, z);
+  // τ = Jᵀ (F − z) + τ_post + bias
+#pragma unroll
+  for (int k = 0; k < mv.n(); ++k) {
+    T s = tp[k] + bias[k].v;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) s += J[r][k] * (F[r] - z[r]);
+    tau_out[k] = s;
+    ok = ok && isfinite(s);
+  }
+  if (lambda_out) {
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      T e[6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) e[r] = r == c ? T(1) : T(0);
+      chol6_solve(Lr, e);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) lambda_out[c * 6 + r] = e[r];
+    }
+  }
+  return ok;
+}
+
+}  // namespace vdk

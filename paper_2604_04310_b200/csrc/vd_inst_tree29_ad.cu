@@ -1,0 +1,9 @@
+// Explicit instantiation unit (parallel build); see vd_kernels.cuh.
+#include "vd_launcher_impl.cuh"
+
+namespace vdk {
+template int Launcher<Tree29D>::fk(const Tree29D&, const Launch&, const void*, void*);
+template int Launcher<Tree29D>::jac(const Tree29D&, const Launch&, const void*, const FrameArg&, void*, void*);
+template int Launcher<Tree29D>::rnea(const Tree29D&, const Launch&, const void*, const void*, const void*, const double*, const void*, void*);
+template int Launcher<Tree29D>::crba(const Tree29D&, const Launch&, const void*, void*);
+}  // namespace vdk

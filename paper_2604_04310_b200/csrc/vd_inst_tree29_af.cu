@@ -1,0 +1,9 @@
+// Explicit instantiation unit (parallel build); see vd_kernels.cuh.
+#include "vd_launcher_impl.cuh"
+
+namespace vdk {
+template int Launcher<Tree29F>::fk(const Tree29F&, const Launch&, const void*, void*);
+template int Launcher<Tree29F>::jac(const Tree29F&, const Launch&, const void*, const FrameArg&, void*, void*);
+template int Launcher<Tree29F>::rnea(const Tree29F&, const Launch&, const void*, const void*, const void*, const double*, const void*, void*);
+template int Launcher<Tree29F>::crba(const Tree29F&, const Launch&, const void*, void*);
+}  // namespace vdk

@@ -1,0 +1,304 @@
+// sm_100a kernels (templates; instantiated per model view in vd_inst_*.cu): one thread per robot state, SoA coalesced loads/stores,
+// model either compile-time specialised (generated robot tables) or read from
+// a device-resident DevModel (generic trees).  See DESIGN.md.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "vd_algos.cuh"
+#include "vd_launch.hpp"
+#include "vd_robots_gen.cuh"
+
+namespace vdk {
+
+constexpr int kBlock = 128;
+
+template <class T>
+struct G3 {
+  T g[3];
+};
+
+template <class V>
+__device__ __forceinline__ void load_motion(const V& mv, const Cols<typename V::Real>& q, JM<typename V::S>* jm) {
+#pragma unroll
+  for (int j = 0; j < mv.n(); ++j) jm[j] = joint_motion(mv, j, q[j]);
+}
+
+template <class T>
+__device__ __forceinline__ Cols<T> cols(const T* p, int64_t ld, int64_t i) {
+  return Cols<T>{p, ld, i};
+}
+
+// ---------------------------------------------------------------- FK
+template <class V>
+__global__ void __launch_bounds__(kBlock) k_fk(V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
+                                                typename V::Real* __restrict__ out, int64_t ldo) {
+  using T = typename V::Real;
+  using S = typename V::S;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  JM<S> jm[V::kMax];
+  load_motion(mv, cols(q, ldi, i), jm);
+  WX<S> W[V::kMax];
+  fk_world(mv, jm, W);
+  OutCols<T> o{out, ldo, i};
+#pragma unroll
+  for (int j = 0; j < mv.n(); ++j) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int r = 0; r < 3; ++r) o.put(j * 12 + c * 3 + r, W[j].R[r * 3 + c].v);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) o.put(j * 12 + 9 + r, W[j].p[r].v);
+  }
+}
+
+// ---------------------------------------------------------------- frame pose + Jacobian
+struct FrameArg {
+  int joint;
+  double R[9], p[3];  // row-major offset
+};
+template <class V>
+__global__ void __launch_bounds__(kBlock) k_jac(V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
+                                                 FrameArg fr, typename V::Real* __restrict__ pose,
+                                                 typename V::Real* __restrict__ J, int64_t ldo) {
+  using T = typename V::Real;
+  using S = typename V::S;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  JM<S> jm[V::kMax];
+  load_motion(mv, cols(q, ldi, i), jm);
+  WX<S> W[V::kMax];
+  fk_world(mv, jm, W);
+  // frame_transform (kinematics.hpp:89-96)
+  T WR[9], Wp[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) WR[k] = (k % 4 == 0) ? T(1) : T(0);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) Wp[k] = T(0);
+#pragma unroll
+  for (int j = 0; j < mv.n(); ++j)
+    if (j == fr.joint) {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) WR[k] = W[j].R[k].v;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) Wp[k] = W[j].p[k].v;
+    }
+  T PR[9], Pp[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      PR[r * 3 + c] = WR[r * 3] * T(fr.R[c]) + WR[r * 3 + 1] * T(fr.R[3 + c]) + WR[r * 3 + 2] * T(fr.R[6 + c]);
+    Pp[r] = WR[r * 3] * T(fr.p[0]) + WR[r * 3 + 1] * T(fr.p[1]) + WR[r * 3 + 2] * T(fr.p[2]) + Wp[r];
+  }
+  if (pose) {
+    OutCols<T> o{pose, ldo, i};
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int r = 0; r < 3; ++r) o.put(c * 3 + r, PR[r * 3 + c]);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) o.put(9 + r, Pp[r]);
+  }
+  if (J) {
+    // geometric_jacobian (kinematics.hpp:108-129); zero columns off the path.
+    OutCols<T> o{J, ldo, i};
+    const uint64_t mask = fr.joint >= 0 ? mv.anc(fr.joint) : 0ull;
+#pragma unroll
+    for (int j = 0; j < mv.n(); ++j) {
+      T col[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
+      if ((mask >> j) & 1ull) {
+        T ax[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+          ax[r] = (W[j].R[r * 3] * mv.axis(j, 0) + W[j].R[r * 3 + 1] * mv.axis(j, 1) + W[j].R[r * 3 + 2] * mv.axis(j, 2)).v;
+        if (mv.kind(j) == 0) {
+          const T d[3] = {Pp[0] - W[j].p[0].v, Pp[1] - W[j].p[1].v, Pp[2] - W[j].p[2].v};
+          col[0] = ax[0];
+          col[1] = ax[1];
+          col[2] = ax[2];
+          col[3] = ax[1] * d[2] - ax[2] * d[1];
+          col[4] = ax[2] * d[0] - ax[0] * d[2];
+          col[5] = ax[0] * d[1] - ax[1] * d[0];
+        } else {
+          col[3] = ax[0];
+          col[4] = ax[1];
+          col[5] = ax[2];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 6; ++r) o.put(j * 6 + r, col[r]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- RNEA family
+template <class V, bool kFext>
+__global__ void __launch_bounds__(kBlock) k_rnea(V mv, int64_t N, const typename V::Real* __restrict__ q,
+                                                  const typename V::Real* __restrict__ qd,
+                                                  const typename V::Real* __restrict__ qdd, int64_t ldi,
+                                                  G3<typename V::Real> g, const typename V::Real* __restrict__ fext,
+                                                  typename V::Real* __restrict__ tau, int64_t ldo) {
+  using T = typename V::Real;
+  using S = typename V::S;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  JM<S> jm[V::kMax];
+  load_motion(mv, cols(q, ldi, i), jm);
+  const Cols<T> qdc{qd, ldi, i}, qddc{qdd, ldi, i}, fc{fext, ldi, i};
+  S out[V::kMax];
+  rnea_one<V, kFext>(mv, jm, qdc, qdd ? &qddc : nullptr, g.g, &fc, out);
+  OutCols<T> o{tau, ldo, i};
+#pragma unroll
+  for (int j = 0; j < mv.n(); ++j) o.put(j, out[j].v);
+}
+
+// ---------------------------------------------------------------- CRBA
+template <class V>
+__device__ __forceinline__ void store_mass(const V& mv, const JM<typename V::S>* jm, typename V::Real* M, int64_t ldo,
+                                           int64_t i) {
+  using T = typename V::Real;
+  using S = typename V::S;
+  OutCols<T> o{M, ldo, i};
+  const int n = mv.n();
+  crba_one(mv, jm, [&](int r, int c, const S& val) {
+    o.put(c * n + r, val.v);
+    if (r != c) o.put(r * n + c, val.v);
+  });
+  // exact zeros between branches (dynamics.hpp:503, test_dynamics.cpp:352-368)
+#pragma unroll
+  for (int r = 0; r < mv.n(); ++r)
+#pragma unroll
+    for (int c = 0; c < mv.n(); ++c)
+      if (!((mv.anc(r) >> c) & 1ull) && !((mv.anc(c) >> r) & 1ull)) o.put(c * n + r, T(0));
+}
+template <class V>
+__global__ void __launch_bounds__(kBlock) k_crba(V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
+                                                  typename V::Real* __restrict__ M, int64_t ldo) {
+  using S = typename V::S;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  JM<S> jm[V::kMax];
+  load_motion(mv, cols(q, ldi, i), jm);
+  store_mass(mv, jm, M, ldo, i);
+}
+
+// ---------------------------------------------------------------- ABA
+template <class V, bool kFext>
+__global__ void __launch_bounds__(kBlock) k_aba(V mv, int64_t N, const typename V::Real* __restrict__ q,
+                                                 const typename V::Real* __restrict__ qd,
+                                                 const typename V::Real* __restrict__ tau, int64_t ldi,
+                                                 G3<typename V::Real> g, const typename V::Real* __restrict__ fext,
+                                                 typename V::Real* __restrict__ qdd, int64_t ldo,
+                                                 int32_t* __restrict__ status) {
+  using T = typename V::Real;
+  using S = typename V::S;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  JM<S> jm[V::kMax];
+  load_motion(mv, cols(q, ldi, i), jm);
+  const Cols<T> qdc{qd, ldi, i}, tc{tau, ldi, i}, fc{fext, ldi, i};
+  S out[V::kMax];
+  const bool ok = aba_one<V, kFext>(mv, jm, qdc, tc, g.g, &fc, out);
+  OutCols<T> o{qdd, ldo, i};
+#pragma unroll
+  for (int j = 0; j < mv.n(); ++j) o.put(j, ok ? out[j].v : T(0));
+  if (status) status[i] = ok ? 0 : 7;
+}
+
+// ---------------------------------------------------------------- fused M + bias + q̈ (config 3)
+template <class V>
+__global__ void __launch_bounds__(kBlock) k_dyn(V mv, int64_t N, const typename V::Real* __restrict__ q,
+                                                 const typename V::Real* __restrict__ qd,
+                                                 const typename V::Real* __restrict__ tau, int64_t ldi,
+                                                 G3<typename V::Real> g, typename V::Real* __restrict__ M,
+                                                 typename V::Real* __restrict__ bias, typename V::Real* __restrict__ qdd,
+                                                 int64_t ldo, int32_t* __restrict__ status) {
+  using T = typename V::Real;
+  using S = typename V::S;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  JM<S> jm[V::kMax];
+  load_motion(mv, cols(q, ldi, i), jm);
+  const Cols<T> qdc{qd, ldi, i}, tc{tau, ldi, i};
+  if (M) store_mass(mv, jm, M, ldo, i);
+  if (bias) {
+    S b[V::kMax];
+    rnea_one<V, false>(mv, jm, qdc, nullptr, g.g, nullptr, b);
+    OutCols<T> o{bias, ldo, i};
+#pragma unroll
+    for (int j = 0; j < mv.n(); ++j) o.put(j, b[j].v);
+  }
+  if (qdd) {
+    S a[V::kMax];
+    const bool ok = aba_one<V, false>(mv, jm, qdc, tc, g.g, nullptr, a);
+    OutCols<T> o{qdd, ldo, i};
+#pragma unroll
+    for (int j = 0; j < mv.n(); ++j) o.put(j, ok ? a[j].v : T(0));
+    if (status) status[i] = ok ? 0 : 7;
+  }
+}
+
+// ---------------------------------------------------------------- OSC
+template <class V>
+__global__ void __launch_bounds__(kBlock) k_osc(V mv, int64_t N, const typename V::Real* __restrict__ q,
+                                                 const typename V::Real* __restrict__ qd, int64_t ldi, OscShared P,
+                                                 typename V::Real* __restrict__ tau, typename V::Real* __restrict__ lam,
+                                                 int64_t ldo, int32_t* __restrict__ status) {
+  using T = typename V::Real;
+  using S = typename V::S;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const Cols<T> qc{q, ldi, i}, qdc{qd, ldi, i};
+  JM<S> jm[V::kMax];
+  load_motion(mv, qc, jm);
+  T t[V::kMax], L[36];
+  const bool ok = osc_one(mv, jm, qc, qdc, P, t, lam ? L : nullptr);
+  OutCols<T> o{tau, ldo, i};
+#pragma unroll
+  for (int j = 0; j < mv.n(); ++j) o.put(j, ok ? t[j] : T(0));
+  if (lam) {
+    OutCols<T> ol{lam, ldo, i};
+#pragma unroll
+    for (int k = 0; k < 36; ++k) ol.put(k, ok ? L[k] : T(0));
+  }
+  if (status) status[i] = ok ? 0 : 7;
+}
+
+// ================================================================ per-view launchers
+inline unsigned grid_for(int64_t N) { return (unsigned)((N + kBlock - 1) / kBlock); }
+inline cudaStream_t stream_of(const Launch& L) { return static_cast<cudaStream_t>(L.stream); }
+template <class T>
+inline G3<T> g3_of(const double* g) {
+  G3<T> o;
+  for (int k = 0; k < 3; ++k) o.g[k] = g ? T(g[k]) : (k == 2 ? T(9.81) : T(0));
+  return o;
+}
+
+// Launcher<V> is explicitly instantiated per view (and per member for the
+// large tree29 kernels) in vd_inst_*.cu so the build parallelises.
+template <class V>
+struct Launcher {
+  using T = typename V::Real;
+  static int fk(const V& mv, const Launch& L, const void* q, void* out);
+  static int jac(const V& mv, const Launch& L, const void* q, const FrameArg& fr, void* pose, void* J);
+  static int rnea(const V& mv, const Launch& L, const void* q, const void* qd, const void* qdd, const double* g,
+                  const void* fext, void* tau);
+  static int crba(const V& mv, const Launch& L, const void* q, void* M);
+  static int aba(const V& mv, const Launch& L, const void* q, const void* qd, const void* tau, const double* g,
+                 const void* fext, void* qdd, int32_t* status);
+  static int dyn(const V& mv, const Launch& L, const void* q, const void* qd, const void* tau, const double* g, void* M,
+                 void* bias, void* qdd, int32_t* status);
+  static int osc(const V& mv, const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau,
+                 void* lambda, int32_t* status);
+};
+
+using GenericD = RuntimeView<double>;
+using GenericF = RuntimeView<float>;
+using Chain7D = StaticView<RobotChain7, double>;
+using Chain7F = StaticView<RobotChain7, float>;
+using Tree29D = StaticView<RobotTree29, double>;
+using Tree29F = StaticView<RobotTree29, float>;
+
+}  // namespace vdk

@@ -1,0 +1,42 @@
+// Internal launch interface between the C-ABI layer (vd_abi.cpp) and the
+// kernels (vd_kernels.cu).  Not part of the public boundary.
+#pragma once
+
+#include <cstdint>
+
+namespace vdk {
+
+
+// Which compile-time robot a device model matched (0 = generic kernels).
+enum Spec : int { kGeneric = 0, kChain7 = 1, kTree29 = 2, kHumanoid23 = 3 };
+
+struct Launch {
+  int spec;                 // Spec
+  int dtype;                // 0 f64, 1 f32
+  int n;                    // dof
+  const void* model;        // DevModel<T>* in device memory (matching dtype)
+  int64_t N, ld_in, ld_out;
+  void* stream;
+};
+
+struct OscShared;
+
+// Compile-time robot whose packed-model fingerprint matches (0 = none).
+int match_spec(uint64_t fingerprint, int n);
+
+// All return cudaError_t as int.
+int launch_fk(const Launch& L, const void* q, void* out);
+int launch_jacobian(const Launch& L, const void* q, int frame_joint, const double* frame_R, const double* frame_p,
+                    void* pose, void* J);
+// mode: 0 full rnea, 1 bias (qdd = 0), 2 gravity (qd = qdd = 0), 3 coriolis (qdd = 0, g = 0)
+int launch_rnea(const Launch& L, int mode, const void* q, const void* qd, const void* qdd, const double* g3,
+                const void* fext, void* tau);
+int launch_crba(const Launch& L, const void* q, void* M);
+int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, const void* fext,
+               void* qdd, int32_t* status);
+int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
+                    void* bias, void* qdd, int32_t* status);
+int launch_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
+               int32_t* status);
+
+}  // namespace vdk

