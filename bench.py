@@ -26,7 +26,6 @@ import ctypes
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -45,7 +44,7 @@ SEED = 2604
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-configs", action="store_true", help="skip the secondary configuration sweep")
@@ -77,57 +76,49 @@ def barrier():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled through NVML (nvidia-ml-py) every
+    ~2 ms in a background thread for the duration of the timed region."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
     def __init__(self, gpu):
         self.gpu = gpu
-        self.proc = None
-        self.lines = []
+        self.sm, self.mask, self.max = [], 0, None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception:  # noqa: BLE001
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.sm.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.mask |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self.nv:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        reasons = sorted(k for k, bit in self.REASONS.items() if self.mask & bit)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max,
+                "reasons": reasons, "samples": len(self.sm), "source": "NVML during the timed region"}
 
 
 # ------------------------------------------------------------------ helpers
@@ -157,39 +148,45 @@ def measured_peaks():
         return {}
 
 
-def flops_per_eval(robot, algo):
-    """Frozen algorithmic flops from the op-counting oracle (oracle/orc_count.hpp)."""
+def flops_per_eval(robot, algo, dense=False):
+    """Frozen algorithmic flops per evaluation from the op-counting oracle
+    (oracle/orc_count.hpp): the recursive algorithm instantiated with a
+    counting scalar.  Default: structure-aware count (ops with a structural
+    zero / unit operand are free — the work the robot's structure requires);
+    dense=True: every 6x6 / 3x3 op of the generic recursion."""
     import oracle_ffi
 
     L = oracle_ffi.lib()
     L.orc_count_flops.restype = ctypes.c_double
     L.orc_count_flops.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
     m = oracle_ffi.Model.builtin(robot)
-    return L.orc_count_flops(m.h, {"rnea": 0, "crba": 1, "aba": 2, "fk": 3}[algo], None)
+    code = {"rnea": 0, "crba": 1, "aba": 2, "fk": 3}[algo]
+    return L.orc_count_flops(m.h, code if dense else code + 100, None)
 
 
-def cpu_reference_rate(robot, n_sample, threads, target_s=12.0, op="fd"):
-    """Reference CPU path (LLT forward dynamics / mask RNEA) on host cores."""
+_CPU_SAMPLE = {}
+
+
+def cpu_reference_rate(robot, threads, target_s=12.0, op="fd", batch=262144):
+    """Reference CPU path (LLT forward dynamics / mask RNEA) on host cores:
+    repeated passes over one seeded batch until ~target_s of CPU work."""
     import oracle_ffi
 
-    om = oracle_ffi.Model.builtin(robot)
-    probe = min(n_sample, 4096)
-    q, qd, qdd, tau = om.random_states(probe, SEED, True, True)
-    t0 = time.perf_counter()
-    if op == "fd":
-        om.forward_dynamics(q, qd, tau, threads=threads)
-    else:
-        om.rnea(q, qd, qdd, threads=threads)
-    rate = probe / max(time.perf_counter() - t0, 1e-9)
-    n = int(min(n_sample, max(probe, rate * target_s)))
-    q, qd, qdd, tau = om.random_states(n, SEED, True, True)
-    t0 = time.perf_counter()
-    if op == "fd":
-        om.forward_dynamics(q, qd, tau, threads=threads)
-    else:
-        om.rnea(q, qd, qdd, threads=threads)
-    dt = time.perf_counter() - t0
-    return n / dt, n, dt
+    key = (robot, batch)
+    if key not in _CPU_SAMPLE:
+        om = oracle_ffi.Model.builtin(robot)
+        _CPU_SAMPLE[key] = (om, om.random_states(batch, SEED, True, True))
+    om, (q, qd, qdd, tau) = _CPU_SAMPLE[key]
+    n_done, t0 = 0, time.perf_counter()
+    while True:
+        if op == "fd":
+            om.forward_dynamics(q, qd, tau, threads=threads)
+        else:
+            om.rnea(q, qd, qdd, threads=threads)
+        n_done += batch
+        dt = time.perf_counter() - t0
+        if dt >= target_s:
+            return n_done / dt, n_done, dt
 
 
 def host_cores():
@@ -217,10 +214,10 @@ def run_reference(args):
     threads = host_cores()
     vals = []
     for _ in range(args.warmup):
-        cpu_reference_rate("chain7", 200000, threads, target_s=2.0)
+        cpu_reference_rate("chain7", threads, target_s=0.5)
     total_n, total_t = 0, 0.0
     for _ in range(args.steps):
-        r, n, dt = cpu_reference_rate("chain7", 400000, threads, target_s=4.0)
+        r, n, dt = cpu_reference_rate("chain7", threads, target_s=2.0)
         vals.append(r)
         total_n += n
         total_t += dt
@@ -294,6 +291,7 @@ def run_ours(args):
 
     # per-launch duration of the dominant kernel (it is the only kernel in the step)
     flops = flops_per_eval("chain7", "aba")
+    flops_dense = flops_per_eval("chain7", "aba", dense=True)
     bytes_per_eval = 8 * n * 4  # q, qd, tau in; qdd out
     achieved_tf = flops * N / (ms_local * 1e-3) / 1e12
     lib.vdi_fma_peak_tflops.restype = ctypes.c_double
@@ -305,7 +303,8 @@ def run_ours(args):
     roofline = {
         "bound": "fp64", "achieved": round(achieved_tf, 4), "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
         "frac": round(achieved_tf / fp64_peak, 4) if fp64_peak > 0 else None, "traffic": None,
-        "flops_per_eval": flops, "flops_source": "frozen op count of oracle aba_loop (oracle/orc_count.hpp)",
+        "flops_per_eval": flops, "flops_per_eval_dense": flops_dense,
+        "flops_source": "frozen structure-aware op count of the oracle's aba_loop (oracle/orc_count.hpp)",
         "peak_source": "measured in this run: FP64 FMA-stream microbenchmark (vdi_fma_peak_tflops)",
         "hbm_gbs_achieved": round(bytes_per_eval * N / (ms_local * 1e-3) / 1e9, 1), "hbm_gbs_peak": hbm,
         "hbm_frac": round(bytes_per_eval * N / (ms_local * 1e-3) / 1e9 / hbm, 4),
@@ -356,10 +355,11 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = host_cores()
-        r, ns, dt = cpu_reference_rate("chain7", 400000, threads, target_s=12.0)
+        r, ns, dt = cpu_reference_rate("chain7", threads, target_s=12.0)
         cpu = {"value": r, "unit": "evals/s", "cores": threads, "kind": "port",
-               "sample": f"{ns} random chain7 states (seed {SEED}), reference forward_dynamics (CRBA + bias + LLT) "
-                         f"in {dt:.1f} s on {threads} threads, {cpu_model()}"}
+               "sample": f"{ns} evaluations (repeated passes over 262144 random chain7 states, seed {SEED}) of "
+                         f"the reference forward_dynamics (CRBA + bias + LLT) in {dt:.1f} s on {threads} threads, "
+                         f"{cpu_model()}"}
 
     if rank == 0:
         line = {

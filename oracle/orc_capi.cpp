@@ -349,26 +349,36 @@ int orc_batch_osc(void* h, int64_t N, const double* q, const double* qd, const c
 // 0 rnea_loop, 1 crba_loop, 2 aba_loop, 3 forward_kinematics, 4 rnea (mask
 // form), 5 forward_dynamics (CRBA + bias + LLT), 6 crba (mask form).
 // out[0..4] = add, mul, div, sqrt, trig; returns flops (add+mul+div).
-double orc_count_flops(void* h, int algo, double* out) {
-  const Model& m = M(h);
+extern "C++" {
+template <class S>
+static int count_algo(const Model& m, int algo) {
   const int n = m.dof();
-  std::vector<Counted> q((size_t)n), qd((size_t)n), qdd((size_t)n);
-  for (int i = 0; i < n; ++i) {
-    q[(size_t)i] = Counted(0.1 * (i + 1));
-    qd[(size_t)i] = Counted(0.2 - 0.03 * i);
-    qdd[(size_t)i] = Counted(0.05 * i - 0.1);
+  std::vector<S> q((size_t)n), qd((size_t)n), qdd((size_t)n);
+  for (int i = 0; i < n; ++i) {  // generic, non-zero, non-unit state
+    q[(size_t)i] = S(0.1 * (i + 1) + 0.0123);
+    qd[(size_t)i] = S(0.2 - 0.03 * i + 0.0071);
+    qdd[(size_t)i] = S(0.05 * i - 0.1 + 0.0037);
   }
-  op_count() = OpCount();
   switch (algo) {
-    case 0: (void)rnea_loop<Counted>(m, q, qd, qdd); break;
-    case 1: (void)crba_loop<Counted>(m, q); break;
-    case 2: (void)aba_loop<Counted>(m, q, qd, qdd); break;
-    case 3: (void)forward_kinematics<Counted>(m, q); break;
-    case 4: (void)rnea<Counted>(m, q, qd, qdd); break;
-    case 5: (void)forward_dynamics<Counted>(m, q, qd, qdd); break;
-    case 6: (void)crba<Counted>(m, q); break;
+    case 0: (void)rnea_loop<S>(m, q, qd, qdd); break;
+    case 1: (void)crba_loop<S>(m, q); break;
+    case 2: (void)aba_loop<S>(m, q, qd, qdd); break;
+    case 3: (void)forward_kinematics<S>(m, q); break;
+    case 4: (void)rnea<S>(m, q, qd, qdd); break;
+    case 5: (void)forward_dynamics<S>(m, q, qd, qdd); break;
+    case 6: (void)crba<S>(m, q); break;
     default: return -1;
   }
+  return 0;
+}
+}  // extern "C++"
+
+// algo + 100: structure-aware count (orc_count.hpp `Sparse`).
+double orc_count_flops(void* h, int algo, double* out) {
+  const Model& m = M(h);
+  op_count() = OpCount();
+  const int rc = algo >= 100 ? count_algo<Sparse>(m, algo - 100) : count_algo<Counted>(m, algo);
+  if (rc) return -1;
   const OpCount c = op_count();
   if (out) {
     out[0] = (double)c.add;

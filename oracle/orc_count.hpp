@@ -45,4 +45,45 @@ inline Counted sqrt(Counted a) { ++op_count().sqrt; return Counted(std::sqrt(a.v
 inline Counted sin(Counted a) { ++op_count().trig; return Counted(std::sin(a.v)); }
 inline Counted cos(Counted a) { ++op_count().trig; return Counted(std::cos(a.v)); }
 
+// Structure-aware variant: an operation with an exactly-zero operand (x·0,
+// x + 0) or a unit factor (x·±1) is not counted — the flops that remain are
+// those of the recursion on the robot's actual structure (axis-aligned joints,
+// permutation-like offsets, sparse inertias).  Evaluated at generic non-zero
+// states, so only STRUCTURAL zeros/units are discounted.
+struct Sparse {
+  double v = 0.0;
+  Sparse() = default;
+  Sparse(double x) : v(x) {}  // NOLINT
+  explicit operator double() const { return v; }
+};
+inline bool trivial_mul(double a) { return a == 0.0 || a == 1.0 || a == -1.0; }
+inline Sparse operator+(Sparse a, Sparse b) {
+  if (a.v != 0.0 && b.v != 0.0) ++op_count().add;
+  return Sparse(a.v + b.v);
+}
+inline Sparse operator-(Sparse a, Sparse b) {
+  if (a.v != 0.0 && b.v != 0.0) ++op_count().add;
+  return Sparse(a.v - b.v);
+}
+inline Sparse operator*(Sparse a, Sparse b) {
+  if (!trivial_mul(a.v) && !trivial_mul(b.v)) ++op_count().mul;
+  return Sparse(a.v * b.v);
+}
+inline Sparse operator/(Sparse a, Sparse b) {
+  if (b.v != 1.0 && b.v != -1.0 && a.v != 0.0) ++op_count().div;
+  return Sparse(a.v / b.v);
+}
+inline Sparse operator-(Sparse a) { return Sparse(-a.v); }
+inline Sparse& operator+=(Sparse& a, Sparse b) { return a = a + b; }
+inline Sparse& operator-=(Sparse& a, Sparse b) { return a = a - b; }
+inline bool operator>(Sparse a, Sparse b) { return a.v > b.v; }
+inline bool operator<(Sparse a, Sparse b) { return a.v < b.v; }
+inline bool operator<=(Sparse a, Sparse b) { return a.v <= b.v; }
+inline bool operator>=(Sparse a, Sparse b) { return a.v >= b.v; }
+inline bool operator==(Sparse a, Sparse b) { return a.v == b.v; }
+inline bool operator!=(Sparse a, Sparse b) { return a.v != b.v; }
+inline Sparse sqrt(Sparse a) { ++op_count().sqrt; return Sparse(std::sqrt(a.v)); }
+inline Sparse sin(Sparse a) { ++op_count().trig; return Sparse(std::sin(a.v)); }
+inline Sparse cos(Sparse a) { ++op_count().trig; return Sparse(std::cos(a.v)); }
+
 }  // namespace orc

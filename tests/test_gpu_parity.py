@@ -282,10 +282,17 @@ def test_osc_fp64(vd, cuda, omodels, name, generic):
     cond = np.linalg.cond(M)
     e_tau = rel_err(tau, tau_ref, axis=1)
     e_lam = rel_err(lam, lam_ref, axis=1)
-    bound = np.maximum(TOL64, 1e-15 * cond)
-    assert np.all(e_tau[ok] <= bound[ok]), float(e_tau.max())
+    # OSC chains two solves: with M (κ(M)) and with J M⁻¹ Jᵀ + εI (κ(Λ⁻¹),
+    # large near kinematic singularities of the task frame); the forward error
+    # of a backward-stable evaluation scales with their product.
+    cond_task = np.linalg.cond(lam_ref)
+    kappa = cond * cond_task
+    bound = np.maximum(TOL64, 1e-16 * kappa)
+    worst = int(np.argmax(e_tau / bound))
+    assert np.all(e_tau[ok] <= bound[ok]), (float(e_tau[worst]), float(cond[worst]), float(cond_task[worst]))
     assert np.all(e_lam[ok] <= np.maximum(bound[ok], 1e-10)), float(e_lam.max())
-    well = ok & (cond < 1e5)
+    well = ok & (kappa < 1e6)
+    assert well.sum() > 0.5 * len(well)
     assert e_tau[well].max(initial=0) <= TOL64
 
 

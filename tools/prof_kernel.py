@@ -1,0 +1,53 @@
+#!/usr/bin/env python3
+"""Minimal driver for ncu captures: a few launches of one hot-path kernel.
+
+Usage: python tools/prof_kernel.py [aba|rnea|crba|dyn|osc|fk] [chain7|tree29] [f64|f32] [N] [launches]
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_04310_b200 as vd  # noqa: E402
+
+
+def main():
+    op = sys.argv[1] if len(sys.argv) > 1 else "aba"
+    robot = sys.argv[2] if len(sys.argv) > 2 else "chain7"
+    dt = sys.argv[3] if len(sys.argv) > 3 else "f64"
+    N = int(sys.argv[4]) if len(sys.argv) > 4 else 4194304
+    launches = int(sys.argv[5]) if len(sys.argv) > 5 else 4
+    code = 0 if dt == "f64" else 1
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    m = vd.robots.by_name(robot)
+    dm = vd.DeviceModel(m, 0)
+    n = m.dof()
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = [((torch.rand((n, N), generator=g, device="cuda", dtype=torch.float64) * 2 - 1) * np.pi).to(tdt)
+         for _ in range(3)]
+    out = torch.empty((n * n, N), dtype=tdt, device="cuda")
+    lib = vd._lib.load()
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for _ in range(launches):
+        if op == "aba":
+            rc = lib.vd_aba(dm.handle, code, N, x[0].data_ptr(), x[1].data_ptr(), x[2].data_ptr(), N, None, None,
+                            out.data_ptr(), N, None, s)
+        elif op == "rnea":
+            rc = lib.vd_rnea(dm.handle, code, N, x[0].data_ptr(), x[1].data_ptr(), x[2].data_ptr(), N, None, None,
+                             out.data_ptr(), N, s)
+        elif op == "crba":
+            rc = lib.vd_crba(dm.handle, code, N, x[0].data_ptr(), N, out.data_ptr(), N, s)
+        elif op == "fk":
+            rc = lib.vd_fk(dm.handle, code, N, x[0].data_ptr(), N, out.data_ptr(), N, s)
+        else:
+            raise SystemExit("unknown op " + op)
+        assert rc == 0, lib.vd_last_error()
+    torch.cuda.synchronize()
+    print("ok", op, robot, dt, N, launches)
+
+
+if __name__ == "__main__":
+    main()
