@@ -28,8 +28,11 @@ struct vd_device_model_s {
   int spec = 0;
   bool force_generic = false;
   vdh::PackedModel pm;
-  void* d64 = nullptr;  // DevModel<double>*
-  void* d32 = nullptr;  // DevModel<float>*
+  // Host copies of the packed model; the generic kernels receive them by
+  // value in their parameter space (__grid_constant__), so no device
+  // allocation is needed and a device model is valid on its device only.
+  std::unique_ptr<vdk::DevModel<double>> h64;
+  std::unique_ptr<vdk::DevModel<float>> h32;
 };
 
 namespace {
@@ -79,12 +82,19 @@ void fill_dev_model(const vdh::PackedModel& pm, vdk::DevModel<T>& d) {
     d.axis_code[i] = pm.axis_code[i];
     d.depth[i] = pm.parent[i] < 0 ? 1 : d.depth[pm.parent[i]] + 1;
     d.anc[i] = (1ull << i) | (pm.parent[i] < 0 ? 0ull : d.anc[pm.parent[i]]);
+    d.flags[i] = vdk::kFlagLeaf;
     for (int k = 0; k < 3; ++k) {
       d.axis[i][k] = T(pm.axis[i][k]);
       d.p[i][k] = T(pm.p[i][k]);
     }
     for (int k = 0; k < 9; ++k) d.R[i][k] = T(pm.R[i][k]);
     for (int k = 0; k < 10; ++k) d.I[i][k] = T(pm.inertia[i][k]);
+  }
+  for (int i = 0; i < pm.n; ++i) {
+    const int p = pm.parent[i];
+    if (p < 0) continue;
+    d.flags[p] &= ~vdk::kFlagLeaf;
+    if (p != i - 1) d.flags[p] |= vdk::kFlagBranch;
   }
 }
 
@@ -119,7 +129,7 @@ vdk::Launch make_launch(vd_device_model dm, int dtype, int64_t N, int64_t ldi, i
   L.spec = dm->force_generic ? vdk::kGeneric : dm->spec;
   L.dtype = dtype;
   L.n = dm->n;
-  L.model = dtype == VD_F64 ? dm->d64 : dm->d32;
+  L.model = dtype == VD_F64 ? static_cast<const void*>(dm->h64.get()) : static_cast<const void*>(dm->h32.get());
   L.N = N;
   L.ld_in = ldi;
   L.ld_out = ldo;
@@ -272,25 +282,18 @@ int vd_device_model_create(vd_model m, int device, vd_device_model* out) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
     if (device < 0 || device >= count) return set_error(VD_ERR_CUDA, "device index out of range");
     DeviceGuard g(device);
-    auto h64 = std::make_unique<vdk::DevModel<double>>();
-    auto h32 = std::make_unique<vdk::DevModel<float>>();
-    fill_dev_model(dm->pm, *h64);
-    fill_dev_model(dm->pm, *h32);
-    if ((e = cudaMalloc(&dm->d64, sizeof(vdk::DevModel<double>))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-    if ((e = cudaMalloc(&dm->d32, sizeof(vdk::DevModel<float>))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-    if ((e = cudaMemcpy(dm->d64, h64.get(), sizeof(vdk::DevModel<double>), cudaMemcpyHostToDevice)) != cudaSuccess)
-      return cuda_fail(e, "cudaMemcpy");
-    if ((e = cudaMemcpy(dm->d32, h32.get(), sizeof(vdk::DevModel<float>), cudaMemcpyHostToDevice)) != cudaSuccess)
-      return cuda_fail(e, "cudaMemcpy");
+    dm->h64 = std::make_unique<vdk::DevModel<double>>();
+    dm->h32 = std::make_unique<vdk::DevModel<float>>();
+    fill_dev_model(dm->pm, *dm->h64);
+    fill_dev_model(dm->pm, *dm->h32);
+    // touch the device so a missing / broken GPU fails here, loudly
+    if ((e = cudaFree(nullptr)) != cudaSuccess) return cuda_fail(e, "cudaFree(0)");
     *out = dm.release();
     return VD_OK;
   });
 }
 void vd_device_model_destroy(vd_device_model dm) {
   if (!dm) return;
-  DeviceGuard g(dm->device);
-  cudaFree(dm->d64);
-  cudaFree(dm->d32);
   delete dm;
 }
 int vd_device_model_dof(vd_device_model dm) { return dm ? dm->n : -1; }

@@ -137,80 +137,139 @@ __device__ __forceinline__ void crba_one(const V& mv, const JM<typename V::S>* j
 // Articulated-body forward dynamics (Featherstone RBDA Table 7.1).  Not in the
 // reference; its oracle is forward_dynamics (dynamics.hpp:421-444,
 // CRBA + bias + LLT).  Returns false when an articulated pivot D_i is not
-// positive (the LLT failure of the oracle: D_i are the pivots of M's
+// positive (the LLT failure of the oracle: the D_i are the pivots of M's
 // tree-structured LDLᵀ factorisation) or the result is not finite.
+//
+// State is kept small so the large-tree kernels stay in L1/L2 and the chain
+// kernels stay in registers:
+//  * joints are in DFS order, so a non-leaf joint i always has child i+1:
+//    contributions to the parent travel in a register "carry" when
+//    parent(j) == j-1 and only go through per-joint slots at branch points;
+//  * velocities are stored only at leaves and branch joints in pass 1; pass 2
+//    (leaf -> root) reconstructs v_{i-1} = X_i (v_i − S_i q̇_i) from its child,
+//    pass 3 recomputes them root -> leaf;
+//  * the per-joint state carried from pass 2 to pass 3 is U_i, u_i, 1/D_i.
 template <class V, bool kFext>
 __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm, const Cols<typename V::Real>& qd,
                                         const Cols<typename V::Real>& tau, const typename V::Real* g3,
                                         const Cols<typename V::Real>* fext, typename V::S* qdd) {
   using S = typename V::S;
   using T = typename V::Real;
-  SV<S> v[V::kMax], c[V::kMax], pA[V::kMax], U[V::kMax];
-  AI<S> IA[V::kMax];
-  S u[V::kMax], dinv[V::kMax];
-  WX<S> W[kFext ? V::kMax : 1];
+  constexpr int NM = V::kMax;
+  SV<S> U[NM], vkeep[NM];
+  S u[NM], dinv[NM];
+  SV<S> fl[kFext ? NM : 1];
+  WX<S> W[kFext ? NM : 1];
   bool ok = true;
-  // pass 1: velocities, bias accelerations, isolated inertias and bias forces
+  SV<S> zero;
 #pragma unroll
-  for (int i = 0; i < mv.n(); ++i) {
-    JointX<V> x;
-    x.load(mv, i, jm[i]);
-    const int p = mv.parent(i);
-    const SV<S> vj = scale(joint_axis(mv, i), S(qd[i]));
-    if (p < 0) {
-      v[i] = vj;
+  for (int k = 0; k < 3; ++k) zero.a[k] = zero.l[k] = S();
+
+  // pass 1: velocities root -> leaf (kept at leaves / branch joints)
+  {
+    SV<S> vprev = zero;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) c[i].a[k] = c[i].l[k] = S();
-    } else {
-      v[i] = x.motion_to_child(v[p]) + vj;
-      c[i] = crm(v[i], vj);
-    }
-    const RB<S> I = body_inertia(mv, i);
-    IA[i] = ai_from_rb(I);
-    pA[i] = crf(v[i], rb_apply(I, v[i]));
-    if constexpr (kFext) {
-      W[i] = world_of(x, p < 0 ? nullptr : &W[p]);
-      SV<S> fw;
+    for (int i = 0; i < mv.n(); ++i) {
+      JointX<V> x;
+      x.load(mv, i, jm[i]);
+      const int p = mv.parent(i);
+      const SV<S> vj = scale(joint_axis(mv, i), S(qd[i]));
+      SV<S> v = vj;
+      if (p >= 0) v = x.motion_to_child(p == i - 1 ? vprev : vkeep[p]) + vj;
+      if (mv.flags(i) & (kFlagLeaf | kFlagBranch)) vkeep[i] = v;
+      vprev = v;
+      if constexpr (kFext) {
+        W[i] = world_of(x, p < 0 ? nullptr : &W[p]);
+        SV<S> fw;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        fw.a[k] = S((*fext)[i * 6 + k]);
-        fw.l[k] = S((*fext)[i * 6 + 3 + k]);
+        for (int k = 0; k < 3; ++k) {
+          fw.a[k] = S((*fext)[i * 6 + k]);
+          fw.l[k] = S((*fext)[i * 6 + 3 + k]);
+        }
+        fl[i] = force_in(W[i].R, W[i].p, true, fw);
       }
-      pA[i] = pA[i] - force_in(W[i].R, W[i].p, true, fw);
     }
   }
   // pass 2: articulated inertias leaf -> root
+  {
+    AI<S> carryI, slotI[NM];
+    SV<S> carryP = zero, slotP[NM], vrec = zero;
+    uint64_t used = 0;
+    int carry_to = -1;
 #pragma unroll
-  for (int i = mv.n() - 1; i >= 0; --i) {
-    const SV<S> s = joint_axis(mv, i);
-    U[i] = ai_apply(IA[i], s);
-    const S D = sdot(U[i], s);
-    ok = ok && (D.v > T(0));
-    dinv[i] = S(T(1) / D.v);
-    u[i] = S(tau[i]) - sdot(pA[i], s);
-    const int p = mv.parent(i);
-    if (p >= 0) {
-      JointX<V> x;
-      x.load(mv, i, jm[i]);
-      AI<S> Ia = IA[i];
-      ai_sub_outer(Ia, U[i], dinv[i]);
-      const SV<S> pa = pA[i] + ai_apply(Ia, c[i]) + scale(U[i], u[i] * dinv[i]);
-      ai_add(IA[p], ai_to_parent(x, Ia));
-      pA[p] = pA[p] + x.force_to_parent(pa);
+    for (int i = mv.n() - 1; i >= 0; --i) {
+      const SV<S> s = joint_axis(mv, i);
+      const SV<S> vj = scale(s, S(qd[i]));
+      const SV<S> v = (mv.flags(i) & kFlagLeaf) ? vkeep[i] : vrec;
+      const RB<S> I = body_inertia(mv, i);
+      AI<S> IA = ai_from_rb(I);
+      SV<S> pA = crf(v, rb_apply(I, v));
+      if constexpr (kFext) pA = pA - fl[i];
+      if (carry_to == i) {
+        ai_add(IA, carryI);
+        pA = pA + carryP;
+      }
+      if ((used >> i) & 1ull) {
+        ai_add(IA, slotI[i]);
+        pA = pA + slotP[i];
+      }
+      U[i] = ai_apply(IA, s);
+      const S D = sdot(U[i], s);
+      ok = ok && (D.v > T(0));
+      dinv[i] = S(T(1) / D.v);
+      u[i] = S(tau[i]) - sdot(pA, s);
+      const int p = mv.parent(i);
+      if (p >= 0) {
+        JointX<V> x;
+        x.load(mv, i, jm[i]);
+        const SV<S> c = crm(v, vj);
+        AI<S> Ia = IA;
+        ai_sub_outer(Ia, U[i], dinv[i]);
+        const SV<S> pa = pA + ai_apply(Ia, c) + scale(U[i], u[i] * dinv[i]);
+        const AI<S> IAp = ai_to_parent(x, Ia);
+        const SV<S> pAp = x.force_to_parent(pa);
+        if (p == i - 1) {
+          carryI = IAp;
+          carryP = pAp;
+          carry_to = p;
+          vrec = x.motion_to_parent(v - vj);  // v_{i-1}
+        } else if ((used >> p) & 1ull) {
+          ai_add(slotI[p], IAp);
+          slotP[p] = slotP[p] + pAp;
+        } else {
+          slotI[p] = IAp;
+          slotP[p] = pAp;
+          used |= 1ull << p;
+        }
+      }
     }
   }
   // pass 3: accelerations root -> leaf
-  const SV<S> ag = gravity_accel<V>(g3);
-  SV<S> a[V::kMax];
+  {
+    const SV<S> ag = gravity_accel<V>(g3);
+    SV<S> aprev = zero, vprev = zero, akeep[NM];
 #pragma unroll
-  for (int i = 0; i < mv.n(); ++i) {
-    JointX<V> x;
-    x.load(mv, i, jm[i]);
-    const int p = mv.parent(i);
-    const SV<S> ap = x.motion_to_child(p < 0 ? ag : a[p]) + c[i];
-    qdd[i] = (u[i] - sdot(U[i], ap)) * dinv[i];
-    ok = ok && isfinite(qdd[i].v);
-    a[i] = ap + scale(joint_axis(mv, i), qdd[i]);
+    for (int i = 0; i < mv.n(); ++i) {
+      JointX<V> x;
+      x.load(mv, i, jm[i]);
+      const int p = mv.parent(i);
+      const SV<S> s = joint_axis(mv, i);
+      const SV<S> vj = scale(s, S(qd[i]));
+      SV<S> v = vj, ap;
+      if (p < 0) {
+        ap = x.motion_to_child(ag);
+      } else {
+        const bool adj = p == i - 1;
+        v = x.motion_to_child(adj ? vprev : vkeep[p]) + vj;
+        ap = x.motion_to_child(adj ? aprev : akeep[p]) + crm(v, vj);
+      }
+      qdd[i] = (u[i] - sdot(U[i], ap)) * dinv[i];
+      ok = ok && isfinite(qdd[i].v);
+      const SV<S> a = ap + scale(s, qdd[i]);
+      if (mv.flags(i) & kFlagBranch) akeep[i] = a;
+      aprev = a;
+      vprev = v;
+    }
   }
   return ok;
 }

@@ -5,5 +5,4 @@ namespace vdk {
 template int Launcher<Tree29D>::fk(const Tree29D&, const Launch&, const void*, void*);
 template int Launcher<Tree29D>::jac(const Tree29D&, const Launch&, const void*, const FrameArg&, void*, void*);
 template int Launcher<Tree29D>::rnea(const Tree29D&, const Launch&, const void*, const void*, const void*, const double*, const void*, void*);
-template int Launcher<Tree29D>::crba(const Tree29D&, const Launch&, const void*, void*);
 }  // namespace vdk

@@ -14,7 +14,7 @@ struct Launch {
   int spec;                 // Spec
   int dtype;                // 0 f64, 1 f32
   int n;                    // dof
-  const void* model;        // DevModel<T>* in device memory (matching dtype)
+  const void* model;        // host DevModel<T>* (matching dtype), passed by value to the kernels
   int64_t N, ld_in, ld_out;
   void* stream;
 };

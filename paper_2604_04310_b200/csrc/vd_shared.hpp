@@ -7,6 +7,9 @@ namespace vdk {
 
 constexpr int kMaxDof = 64;
 
+constexpr int kFlagLeaf = 1;
+constexpr int kFlagBranch = 2;
+
 // Device-resident model for the generic (runtime-topology) kernels.
 template <class T>
 struct DevModel {
@@ -16,6 +19,7 @@ struct DevModel {
   int axis_code[kMaxDof];  // 0..2 +x,+y,+z; 3..5 -x,-y,-z; 6 general
   int depth[kMaxDof];      // moving joints on the path root..i (1 for root joints)
   uint64_t anc[kMaxDof];   // bit j set iff j is i or an ancestor of i (ancestor mask row)
+  int flags[kMaxDof];      // kFlagLeaf: no children; kFlagBranch: has a child other than i+1
   T axis[kMaxDof][3];
   T R[kMaxDof][9];         // offset rotation, row-major
   T p[kMaxDof][3];

