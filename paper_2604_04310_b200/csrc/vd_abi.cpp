@@ -7,7 +7,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <string>
 #include <thread>
@@ -466,12 +468,185 @@ int vd_shard_range(int64_t N, int world, int rank, int64_t* begin, int64_t* end)
 }
 
 // ------------------------------------------------------------------ host batch (multi-device)
+// Drop-in for batch.hpp's batch_* helpers on HOST buffers.  Each device owns a
+// persistent context (device model, two streams, double-buffered device
+// chunks) so repeated calls do not re-allocate; the shard of each device is
+// streamed in chunks with H2D(k+1) / kernel(k) / D2H(k-1) overlapping across
+// the two streams.  Pinned host buffers are DMA'd directly; pageable ones go
+// through pinned staging buffers.
 namespace {
 struct HostOp {
   int kind;  // 0 rnea, 1 crba, 2 fd
   int n_in;  // number of n-wide inputs
   int out_width;
 };
+
+struct DevCtx {
+  std::mutex mu;
+  int device = -1;
+  vd_device_model dm = nullptr;
+  uint64_t fp = 0;
+  int n = -1;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  double* din[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  double* dout[2] = {nullptr, nullptr};
+  int32_t* dst[2] = {nullptr, nullptr};
+  double* pin_in[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};  // staging (pageable inputs)
+  double* pin_out[2] = {nullptr, nullptr};
+  int32_t* pin_st[2] = {nullptr, nullptr};
+  int64_t cap = 0;      // states per chunk buffer
+  int64_t cap_out = 0;  // doubles per output chunk buffer
+  int64_t cap_pin = 0;
+};
+
+DevCtx& ctx_for(int device) {
+  static std::mutex g;
+  static std::map<int, std::unique_ptr<DevCtx>> all;
+  std::lock_guard<std::mutex> lk(g);
+  auto& p = all[device];
+  if (!p) {
+    p = std::make_unique<DevCtx>();
+    p->device = device;
+  }
+  return *p;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+int prepare_ctx(DevCtx& c, vd_model m, int n, int64_t chunk, int width, bool staging) {
+  cudaError_t e;
+  const uint64_t fp = vdh::fingerprint(vdh::pack(m->m));
+  if (!c.dm || c.fp != fp || c.n != n) {
+    if (c.dm) vd_device_model_destroy(c.dm);
+    c.dm = nullptr;
+    if (int rc = vd_device_model_create(m, c.device, &c.dm)) return rc;
+    c.fp = fp;
+    c.n = n;
+  }
+  if (!c.st[0]) {
+    for (int k = 0; k < 2; ++k) {
+      if ((e = cudaStreamCreateWithFlags(&c.st[k], cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+      if ((e = cudaEventCreateWithFlags(&c.done[k], cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+    }
+  }
+  const int64_t need_out = chunk * width;
+  if (chunk * n > c.cap * std::max(c.n, 1) || need_out > c.cap_out || c.cap < chunk) {
+    for (int b = 0; b < 2; ++b) {
+      for (int k = 0; k < 3; ++k) cudaFree(c.din[b][k]);
+      cudaFree(c.dout[b]);
+      cudaFree(c.dst[b]);
+      for (int k = 0; k < 3; ++k)
+        if ((e = cudaMalloc(&c.din[b][k], sizeof(double) * n * chunk)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+      if ((e = cudaMalloc(&c.dout[b], sizeof(double) * need_out)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+      if ((e = cudaMalloc(&c.dst[b], sizeof(int32_t) * chunk)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    }
+    c.cap = chunk;
+    c.cap_out = need_out;
+  }
+  if (staging && c.cap_pin < chunk * std::max(n, width)) {
+    for (int b = 0; b < 2; ++b) {
+      for (int k = 0; k < 3; ++k) cudaFreeHost(c.pin_in[b][k]);
+      cudaFreeHost(c.pin_out[b]);
+      cudaFreeHost(c.pin_st[b]);
+      const int64_t cnt = chunk * std::max(n, width);
+      for (int k = 0; k < 3; ++k)
+        if ((e = cudaMallocHost(&c.pin_in[b][k], sizeof(double) * cnt)) != cudaSuccess) return cuda_fail(e, "pinned");
+      if ((e = cudaMallocHost(&c.pin_out[b], sizeof(double) * cnt)) != cudaSuccess) return cuda_fail(e, "pinned");
+      if ((e = cudaMallocHost(&c.pin_st[b], sizeof(int32_t) * chunk)) != cudaSuccess) return cuda_fail(e, "pinned");
+    }
+    c.cap_pin = chunk * std::max(n, width);
+  }
+  return VD_OK;
+}
+
+// Stream one device's shard [b, e) through the double-buffered pipeline.
+int run_shard(DevCtx& c, vd_model m, const HostOp& op, int64_t N, int64_t b, int64_t e, const double* const* inputs,
+              const double* g3, double* out, int32_t* status, bool* any_bad) {
+  const int n = m->m.dof();
+  const int width = op.out_width;
+  const int64_t len = e - b;
+  const int64_t chunk = std::min<int64_t>(len, std::max<int64_t>(65536, (int64_t)(48ll << 20) / (8ll * (n * op.n_in + width))));
+  bool pinned = is_pinned(out);
+  for (int k = 0; k < op.n_in; ++k) pinned = pinned && is_pinned(inputs[k]);
+  const bool st_direct = pinned && status && is_pinned(status);
+  if (int rc = prepare_ctx(c, m, n, chunk, width, !pinned || (op.kind == 2 && !st_direct))) return rc;
+  const int64_t nchunks = (len + chunk - 1) / chunk;
+  std::vector<int32_t> st_host;
+  int32_t* st_dst = status;
+  if (op.kind == 2 && !status) {
+    st_host.resize((size_t)len);
+    st_dst = st_host.data() - b;  // indexed with the global row below
+  }
+  std::vector<int64_t> pending_lo(2, -1), pending_len(2, 0);
+  auto finish_slot = [&](int slot) -> int {
+    if (pending_lo[(size_t)slot] < 0) return VD_OK;
+    cudaError_t ce = cudaEventSynchronize(c.done[slot]);
+    if (ce != cudaSuccess) return cuda_fail(ce, "host batch");
+    const int64_t lo = pending_lo[(size_t)slot], cl = pending_len[(size_t)slot];
+    if (!pinned) {  // unstage
+      for (int r = 0; r < width; ++r)
+        std::memcpy(out + (int64_t)r * N + lo, c.pin_out[slot] + (int64_t)r * cl, sizeof(double) * cl);
+    }
+    if (op.kind == 2 && !st_direct) std::memcpy(st_dst + lo, c.pin_st[slot], sizeof(int32_t) * cl);
+    if (op.kind == 2)
+      for (int64_t k = 0; k < cl; ++k)
+        if (st_dst[lo + k]) *any_bad = true;
+    pending_lo[(size_t)slot] = -1;
+    return VD_OK;
+  };
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int slot = (int)(k & 1);
+    if (int rc = finish_slot(slot)) return rc;
+    const int64_t lo = b + k * chunk, cl = std::min<int64_t>(chunk, e - lo);
+    cudaStream_t s = c.st[slot];
+    cudaError_t ce = cudaSuccess;
+    for (int i = 0; i < op.n_in && ce == cudaSuccess; ++i) {
+      const double* src = inputs[i] + lo;
+      size_t spitch = sizeof(double) * N;
+      if (!pinned) {
+        for (int r = 0; r < n; ++r)
+          std::memcpy(c.pin_in[slot][i] + (int64_t)r * cl, inputs[i] + (int64_t)r * N + lo, sizeof(double) * cl);
+        src = c.pin_in[slot][i];
+        spitch = sizeof(double) * cl;
+      }
+      ce = cudaMemcpy2DAsync(c.din[slot][i], sizeof(double) * cl, src, spitch, sizeof(double) * cl, n,
+                             cudaMemcpyHostToDevice, s);
+    }
+    if (ce != cudaSuccess) return cuda_fail(ce, "host batch H2D");
+    int rc;
+    if (op.kind == 0)
+      rc = vd_rnea(c.dm, VD_F64, cl, c.din[slot][0], c.din[slot][1], c.din[slot][2], cl, g3, nullptr, c.dout[slot], cl, s);
+    else if (op.kind == 1)
+      rc = vd_crba(c.dm, VD_F64, cl, c.din[slot][0], cl, c.dout[slot], cl, s);
+    else
+      rc = vd_aba(c.dm, VD_F64, cl, c.din[slot][0], c.din[slot][1], c.din[slot][2], cl, g3, nullptr, c.dout[slot], cl,
+                  c.dst[slot], s);
+    if (rc) return rc;
+    double* dst = pinned ? out + lo : c.pin_out[slot];
+    const size_t dpitch = pinned ? sizeof(double) * N : sizeof(double) * cl;
+    ce = cudaMemcpy2DAsync(dst, dpitch, c.dout[slot], sizeof(double) * cl, sizeof(double) * cl, width,
+                           cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess && op.kind == 2)
+      ce = cudaMemcpyAsync(st_direct ? st_dst + lo : c.pin_st[slot], c.dst[slot], sizeof(int32_t) * cl,
+                           cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaEventRecord(c.done[slot], s);
+    if (ce != cudaSuccess) return cuda_fail(ce, "host batch D2H");
+    pending_lo[(size_t)slot] = lo;
+    pending_len[(size_t)slot] = cl;
+  }
+  for (int slot = 0; slot < 2; ++slot)
+    if (int rc = finish_slot(slot)) return rc;
+  return VD_OK;
+}
+
 int host_batch(vd_model m, const HostOp& op, int64_t N, const double* const* inputs, const double* g3, double* out,
                int32_t* status, const int* devices, int ndev) {
   if (!m) return set_error(VD_ERR_INVALID_ARGUMENT, "null model");
@@ -485,75 +660,28 @@ int host_batch(vd_model m, const HostOp& op, int64_t N, const double* const* inp
   if (devices && ndev > 0) devs.assign(devices, devices + ndev);
   else devs.push_back(0);
   const int W = (int)devs.size();
-  const int width = op.out_width;
   std::vector<int> rcs((size_t)W, VD_OK);
   std::vector<std::string> msgs((size_t)W);
-  std::vector<int> bad((size_t)W, 0);
+  std::vector<char> bad((size_t)W, 0);
   auto work = [&](int w) {
     int64_t b = 0, e = 0;
     vd_shard_range(N, W, w, &b, &e);
-    const int64_t len = e - b;
-    if (len <= 0) return;
-    vd_device_model dm = nullptr;
-    int rc = vd_device_model_create(m, devs[(size_t)w], &dm);
+    if (e <= b) return;
+    DevCtx& c = ctx_for(devs[(size_t)w]);
+    std::lock_guard<std::mutex> lk(c.mu);
+    DeviceGuard g(devs[(size_t)w]);
+    bool any_bad = false;
+    int rc = VD_OK;
+    try {
+      rc = run_shard(c, m, op, N, b, e, inputs, g3, out, status, &any_bad);
+    } catch (const std::exception& ex) {
+      rc = set_error(VD_ERR_GENERIC, ex.what());
+    }
     if (rc) {
       rcs[(size_t)w] = rc;
       msgs[(size_t)w] = g_msg;
-      return;
     }
-    DeviceGuard g(devs[(size_t)w]);
-    cudaStream_t s;
-    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    std::vector<double*> din((size_t)op.n_in, nullptr);
-    double* dout = nullptr;
-    int32_t* dst = nullptr;
-    cudaError_t ce = cudaSuccess;
-    for (int k = 0; k < op.n_in && ce == cudaSuccess; ++k) {
-      ce = cudaMallocAsync((void**)&din[(size_t)k], sizeof(double) * n * len, s);
-      if (ce == cudaSuccess)
-        ce = cudaMemcpy2DAsync(din[(size_t)k], sizeof(double) * len, inputs[k] + b, sizeof(double) * N,
-                               sizeof(double) * len, n, cudaMemcpyHostToDevice, s);
-    }
-    if (ce == cudaSuccess) ce = cudaMallocAsync((void**)&dout, sizeof(double) * width * len, s);
-    if (ce == cudaSuccess && op.kind == 2) ce = cudaMallocAsync((void**)&dst, sizeof(int32_t) * len, s);
-    if (ce != cudaSuccess) {
-      rcs[(size_t)w] = cuda_fail(ce, "host batch staging");
-      msgs[(size_t)w] = g_msg;
-    } else {
-      if (op.kind == 0)
-        rc = vd_rnea(dm, VD_F64, len, din[0], din[1], din[2], len, g3, nullptr, dout, len, s);
-      else if (op.kind == 1)
-        rc = vd_crba(dm, VD_F64, len, din[0], len, dout, len, s);
-      else
-        rc = vd_aba(dm, VD_F64, len, din[0], din[1], din[2], len, g3, nullptr, dout, len, dst, s);
-      if (rc) {
-        rcs[(size_t)w] = rc;
-        msgs[(size_t)w] = g_msg;
-      } else {
-        ce = cudaMemcpy2DAsync(out + b, sizeof(double) * N, dout, sizeof(double) * len, sizeof(double) * len, width,
-                               cudaMemcpyDeviceToHost, s);
-        std::vector<int32_t> st;
-        if (ce == cudaSuccess && dst) {
-          st.resize((size_t)len);
-          ce = cudaMemcpyAsync(st.data(), dst, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, s);
-        }
-        if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
-        if (ce != cudaSuccess) {
-          rcs[(size_t)w] = cuda_fail(ce, "host batch copy-out");
-          msgs[(size_t)w] = g_msg;
-        }
-        for (int64_t k = 0; k < (int64_t)st.size(); ++k) {
-          if (status) status[b + k] = st[(size_t)k];
-          if (st[(size_t)k]) bad[(size_t)w] = 1;
-        }
-      }
-    }
-    for (double* p : din) cudaFreeAsync(p, s);
-    cudaFreeAsync(dout, s);
-    if (dst) cudaFreeAsync(dst, s);
-    cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
-    vd_device_model_destroy(dm);
+    bad[(size_t)w] = any_bad ? 1 : 0;
   };
   if (W == 1) {
     work(0);

@@ -46,7 +46,10 @@ template <class T>
 struct sp<T, false> {
   T v;
   static constexpr bool nz = true;
-  __device__ __forceinline__ sp() : v(T(0)) {}
+  // Trivial default constructor: per-joint scratch arrays of the loop kernels
+  // must not be zero-filled on entry (that turned into kilobytes of local
+  // memory stores per thread).  S() still value-initialises to zero.
+  sp() = default;
   __device__ __forceinline__ sp(T x) : v(x) {}
   __device__ __forceinline__ sp(T x, bool) : v(x) {}
 };
