@@ -8,7 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libvecdyn_cuda.so")
+LIB_PATH = os.environ.get("VD_LIB_PATH") or os.path.join(_HERE, "lib", "libvecdyn_cuda.so")
 
 VD_OK = 0
 VD_ERR_DIMENSION = 1

@@ -85,6 +85,13 @@ void fill_dev_model(const vdh::PackedModel& pm, vdk::DevModel<T>& d) {
     d.depth[i] = pm.parent[i] < 0 ? 1 : d.depth[pm.parent[i]] + 1;
     d.anc[i] = (1ull << i) | (pm.parent[i] < 0 ? 0ull : d.anc[pm.parent[i]]);
     d.flags[i] = vdk::kFlagLeaf;
+    {
+      bool rid = true, tz = true, ml = true;
+      for (int k = 0; k < 9; ++k) rid = rid && pm.R[i][k] == ((k % 4 == 0) ? 1.0 : 0.0);
+      for (int k = 0; k < 3; ++k) tz = tz && pm.p[i][k] == 0.0;
+      for (int k = 0; k < 10; ++k) ml = ml && pm.inertia[i][k] == 0.0;
+      d.oflags[i] = (rid ? vdk::kOffRotIdentity : 0) | (tz ? vdk::kOffTransZero : 0) | (ml ? vdk::kMassless : 0);
+    }
     for (int k = 0; k < 3; ++k) {
       d.axis[i][k] = T(pm.axis[i][k]);
       d.p[i][k] = T(pm.p[i][k]);
@@ -496,6 +503,7 @@ struct DevCtx {
   double* pin_out[2] = {nullptr, nullptr};
   int32_t* pin_st[2] = {nullptr, nullptr};
   int64_t cap = 0;      // states per chunk buffer
+  int64_t cap_in = 0;   // doubles per input chunk buffer
   int64_t cap_out = 0;  // doubles per output chunk buffer
   int64_t cap_pin = 0;
 };
@@ -538,7 +546,7 @@ int prepare_ctx(DevCtx& c, vd_model m, int n, int64_t chunk, int width, bool sta
     }
   }
   const int64_t need_out = chunk * width;
-  if (chunk * n > c.cap * std::max(c.n, 1) || need_out > c.cap_out || c.cap < chunk) {
+  if (chunk * n > c.cap_in || need_out > c.cap_out || c.cap < chunk) {
     for (int b = 0; b < 2; ++b) {
       for (int k = 0; k < 3; ++k) cudaFree(c.din[b][k]);
       cudaFree(c.dout[b]);
@@ -549,6 +557,7 @@ int prepare_ctx(DevCtx& c, vd_model m, int n, int64_t chunk, int width, bool sta
       if ((e = cudaMalloc(&c.dst[b], sizeof(int32_t) * chunk)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
     }
     c.cap = chunk;
+    c.cap_in = chunk * n;
     c.cap_out = need_out;
   }
   if (staging && c.cap_pin < chunk * std::max(n, width)) {

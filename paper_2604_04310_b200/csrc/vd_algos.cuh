@@ -61,19 +61,25 @@ __device__ __forceinline__ void rnea_one(const V& mv, const JM<typename V::S>* j
   for (int i = 0; i < mv.n(); ++i) {
     JointX<V> x;
     x.load(mv, i, jm[i]);
+    const JAxis<V> ax(mv, i);
     const int p = mv.parent(i);
-    const SV<S> s = joint_axis(mv, i);
-    const SV<S> vj = scale(s, S(qd[i]));
+    const S qdi = S(qd[i]);
     if (p < 0) {
-      v[i] = vj;
+      v[i] = ax.scaled(qdi);
       a[i] = x.motion_to_child(ag);
     } else {
-      v[i] = x.motion_to_child(v[p]) + vj;
-      a[i] = x.motion_to_child(a[p]) + crm(v[i], vj);
+      v[i] = x.motion_to_child(v[p]);
+      ax.add(v[i], qdi);
+      a[i] = x.motion_to_child(a[p]) + ax.crm(v[i], qdi);
     }
-    if (qdd) a[i] = a[i] + scale(s, S((*qdd)[i]));
-    const RB<S> I = body_inertia(mv, i);
-    f[i] = rb_apply(I, a[i]) + crf(v[i], rb_apply(I, v[i]));
+    if (qdd) ax.add(a[i], S((*qdd)[i]));
+    if (mv.oflags(i) & kMassless) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) f[i].a[k] = f[i].l[k] = S();
+    } else {
+      const RB<S> I = body_inertia(mv, i);
+      f[i] = rb_apply(I, a[i]) + crf(v[i], rb_apply(I, v[i]));
+    }
     if constexpr (kFext) {
       W[i] = world_of(x, p < 0 ? nullptr : &W[p]);
       SV<S> fw;
@@ -87,7 +93,7 @@ __device__ __forceinline__ void rnea_one(const V& mv, const JM<typename V::S>* j
   }
 #pragma unroll
   for (int i = mv.n() - 1; i >= 0; --i) {
-    tau[i] = sdot(f[i], joint_axis(mv, i));
+    tau[i] = JAxis<V>(mv, i).dot(f[i]);
     const int p = mv.parent(i);
     if (p >= 0) {
       JointX<V> x;
@@ -118,8 +124,9 @@ __device__ __forceinline__ void crba_one(const V& mv, const JM<typename V::S>* j
   }
 #pragma unroll
   for (int i = 0; i < mv.n(); ++i) {
-    SV<S> F = rb_apply(ic[i], joint_axis(mv, i));
-    emit(i, i, sdot(F, joint_axis(mv, i)));
+    const JAxis<V> ax(mv, i);
+    SV<S> F = rb_apply(ic[i], ax.scaled(S(typename V::Real(1), true)));
+    emit(i, i, ax.dot(F));
     int j = i;
 #pragma unroll
     for (int d = 1; d < mv.max_depth(); ++d) {
@@ -128,7 +135,7 @@ __device__ __forceinline__ void crba_one(const V& mv, const JM<typename V::S>* j
       x.load(mv, j, jm[j]);
       F = x.force_to_parent(F);
       j = mv.parent(j);
-      emit(i, j, sdot(F, joint_axis(mv, j)));
+      emit(i, j, JAxis<V>(mv, j).dot(F));
     }
   }
 }
@@ -173,9 +180,14 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
       JointX<V> x;
       x.load(mv, i, jm[i]);
       const int p = mv.parent(i);
-      const SV<S> vj = scale(joint_axis(mv, i), S(qd[i]));
-      SV<S> v = vj;
-      if (p >= 0) v = x.motion_to_child(p == i - 1 ? vprev : vkeep[p]) + vj;
+      const JAxis<V> ax(mv, i);
+      SV<S> v;
+      if (p >= 0) {
+        v = x.motion_to_child(p == i - 1 ? vprev : vkeep[p]);
+        ax.add(v, S(qd[i]));
+      } else {
+        v = ax.scaled(S(qd[i]));
+      }
       if (mv.flags(i) & (kFlagLeaf | kFlagBranch)) vkeep[i] = v;
       vprev = v;
       if constexpr (kFext) {
@@ -198,12 +210,22 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
     int carry_to = -1;
 #pragma unroll
     for (int i = mv.n() - 1; i >= 0; --i) {
-      const SV<S> s = joint_axis(mv, i);
-      const SV<S> vj = scale(s, S(qd[i]));
+      const JAxis<V> ax(mv, i);
+      const S qdi = S(qd[i]);
       const SV<S> v = (mv.flags(i) & kFlagLeaf) ? vkeep[i] : vrec;
-      const RB<S> I = body_inertia(mv, i);
-      AI<S> IA = ai_from_rb(I);
-      SV<S> pA = crf(v, rb_apply(I, v));
+      AI<S> IA;
+      SV<S> pA;
+      if (mv.oflags(i) & kMassless) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) IA.A[k] = IA.C[k] = S();
+#pragma unroll
+        for (int k = 0; k < 9; ++k) IA.B[k] = S();
+        pA = zero;
+      } else {
+        const RB<S> I = body_inertia(mv, i);
+        IA = ai_from_rb(I);
+        pA = crf(v, rb_apply(I, v));
+      }
       if constexpr (kFext) pA = pA - fl[i];
       if (carry_to == i) {
         ai_add(IA, carryI);
@@ -213,16 +235,16 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
         ai_add(IA, slotI[i]);
         pA = pA + slotP[i];
       }
-      U[i] = ai_apply(IA, s);
-      const S D = sdot(U[i], s);
+      U[i] = ai_axis(ax, IA);
+      const S D = ax.dot(U[i]);
       ok = ok && (D.v > T(0));
       dinv[i] = S(T(1) / D.v);
-      u[i] = S(tau[i]) - sdot(pA, s);
+      u[i] = S(tau[i]) - ax.dot(pA);
       const int p = mv.parent(i);
       if (p >= 0) {
         JointX<V> x;
         x.load(mv, i, jm[i]);
-        const SV<S> c = crm(v, vj);
+        const SV<S> c = ax.crm(v, qdi);
         AI<S> Ia = IA;
         ai_sub_outer(Ia, U[i], dinv[i]);
         const SV<S> pa = pA + ai_apply(Ia, c) + scale(U[i], u[i] * dinv[i]);
@@ -232,7 +254,9 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
           carryI = IAp;
           carryP = pAp;
           carry_to = p;
-          vrec = x.motion_to_parent(v - vj);  // v_{i-1}
+          SV<S> vmj = v;
+          ax.add(vmj, -qdi);
+          vrec = x.motion_to_parent(vmj);  // v_{i-1}
         } else if ((used >> p) & 1ull) {
           ai_add(slotI[p], IAp);
           slotP[p] = slotP[p] + pAp;
@@ -253,19 +277,22 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
       JointX<V> x;
       x.load(mv, i, jm[i]);
       const int p = mv.parent(i);
-      const SV<S> s = joint_axis(mv, i);
-      const SV<S> vj = scale(s, S(qd[i]));
-      SV<S> v = vj, ap;
+      const JAxis<V> ax(mv, i);
+      const S qdi = S(qd[i]);
+      SV<S> v, ap;
       if (p < 0) {
+        v = ax.scaled(qdi);
         ap = x.motion_to_child(ag);
       } else {
         const bool adj = p == i - 1;
-        v = x.motion_to_child(adj ? vprev : vkeep[p]) + vj;
-        ap = x.motion_to_child(adj ? aprev : akeep[p]) + crm(v, vj);
+        v = x.motion_to_child(adj ? vprev : vkeep[p]);
+        ax.add(v, qdi);
+        ap = x.motion_to_child(adj ? aprev : akeep[p]) + ax.crm(v, qdi);
       }
       qdd[i] = (u[i] - sdot(U[i], ap)) * dinv[i];
       ok = ok && isfinite(qdd[i].v);
-      const SV<S> a = ap + scale(s, qdd[i]);
+      SV<S> a = ap;
+      ax.add(a, qdd[i]);
       if (mv.flags(i) & kFlagBranch) akeep[i] = a;
       aprev = a;
       vprev = v;

@@ -28,6 +28,10 @@
 
 #include "vd_shared.hpp"
 
+#ifndef VD_RT_MINBLOCKS
+#define VD_RT_MINBLOCKS 4
+#endif
+
 namespace vdk {
 
 // ================================================================== sparse-aware scalar
@@ -111,6 +115,9 @@ struct RuntimeView {
   static constexpr bool kStatic = false;
   static constexpr int kMax = kMaxDof;
   static constexpr int kMaxDepthC = kMaxDof;
+  // >= 4 resident 128-thread blocks per SM (<= 128 registers): the loop
+  // kernels are latency-bound on their per-joint local-memory state.
+  static constexpr int kMinBlocks = VD_RT_MINBLOCKS;
   // The whole model travels by value in the kernel's parameter space
   // (__grid_constant__): warp-uniform indexed reads hit the constant cache.
   DevModel<T> m;
@@ -122,6 +129,7 @@ struct RuntimeView {
   __device__ __forceinline__ int depth(int i) const { return m.depth[i]; }
   __device__ __forceinline__ uint64_t anc(int i) const { return m.anc[i]; }
   __device__ __forceinline__ int flags(int i) const { return m.flags[i]; }
+  __device__ __forceinline__ int oflags(int i) const { return m.oflags[i]; }
   __device__ __forceinline__ S axis(int i, int k) const { return S(m.axis[i][k]); }
   __device__ __forceinline__ S R(int i, int k) const { return S(m.R[i][k]); }
   __device__ __forceinline__ S p(int i, int k) const { return S(m.p[i][k]); }
@@ -138,6 +146,10 @@ struct StaticView {
   static constexpr bool kStatic = true;
   static constexpr int kMax = Robot::kN;
   static constexpr int kMaxDepthC = Robot::kMaxDepth;
+  // 0 = no .minnctapersm: ptxas then keeps register use (and occupancy) as
+  // in a plain __launch_bounds__(128); minBlocks=1 let it grow FK from 64 to
+  // 126 registers and cost 10-30% on the chain kernels.
+  static constexpr int kMinBlocks = 0;
   __device__ __forceinline__ static constexpr int n() { return Robot::kN; }
   __device__ __forceinline__ static constexpr int max_depth() { return Robot::kMaxDepth; }
   __device__ __forceinline__ int parent(int i) const { return Robot::parent()[i]; }
@@ -146,6 +158,7 @@ struct StaticView {
   __device__ __forceinline__ int depth(int i) const { return Robot::depth()[i]; }
   __device__ __forceinline__ uint64_t anc(int i) const { return Robot::anc()[i]; }
   __device__ __forceinline__ int flags(int i) const { return Robot::flags()[i]; }
+  __device__ __forceinline__ int oflags(int i) const { return Robot::oflags()[i]; }
   __device__ __forceinline__ S cst(double x) const { return S(T(x), x != 0.0); }
   __device__ __forceinline__ S axis(int i, int k) const { return cst(Robot::axis()[i * 3 + k]); }
   __device__ __forceinline__ S R(int i, int k) const { return cst(Robot::rot()[i * 9 + k]); }
@@ -380,52 +393,310 @@ __device__ __forceinline__ SV<S> force_in(const S* Q, const S* t, bool has_t, co
   return o;
 }
 
-// Stage helpers for X = X_off ∘ X_J.
+// ------------------------------------------------------------------ axis-specialised helpers
+template <int K>
+struct IC {
+  static constexpr int v = K;
+};
+// Calls f(IC<k>) for k in {0,1,2}: per-axis code with constant indices (a
+// uniform branch for runtime views, folded for static views).
+template <class F>
+__device__ __forceinline__ void with_axis(int k, F&& f) {
+  if (k == 0) f(IC<0>());
+  else if (k == 1) f(IC<1>());
+  else f(IC<2>());
+}
+// Same as with_axis but as a plain switch (no lambda), so nothing can stop the
+// body from inlining into the unrolled static kernels.
+#define VD_WITH_AXIS(kexpr, ...)          \
+  switch (kexpr) {                        \
+    case 0: {                             \
+      constexpr int K = 0;                \
+      __VA_ARGS__;                        \
+    } break;                              \
+    case 1: {                             \
+      constexpr int K = 1;                \
+      __VA_ARGS__;                        \
+    } break;                              \
+    default: {                            \
+      constexpr int K = 2;                \
+      __VA_ARGS__;                        \
+    } break;                              \
+  }
+
+// y = R x for the plane rotation about axis K by (c, s)
+template <int K, class S>
+__device__ __forceinline__ void plane_rot(const S& c, const S& s, const S* x, S* y) {
+  constexpr int k1 = (K + 1) % 3, k2 = (K + 2) % 3;
+  y[K] = x[K];
+  y[k1] = c * x[k1] - s * x[k2];
+  y[k2] = s * x[k1] + c * x[k2];
+}
+// symmetric (xx yy zz xy xz yz) rotated in the plane about axis K: R S Rᵀ
+template <int K>
+__device__ __forceinline__ constexpr int sidx(int r, int c) {
+  return r == c ? r : (r + c == 1 ? 3 : (r + c == 2 ? 4 : 5));
+}
+template <int K, class S>
+__device__ __forceinline__ void plane_rot_sym(const S& c, const S& s, const S* a, S* o) {
+  constexpr int k1 = (K + 1) % 3, k2 = (K + 2) % 3;
+  const S s11 = a[sidx<K>(k1, k1)], s22 = a[sidx<K>(k2, k2)], s12 = a[sidx<K>(k1, k2)];
+  const S s1k = a[sidx<K>(k1, K)], s2k = a[sidx<K>(k2, K)];
+  const S cc = c * c, ss = s * s, cs = c * s;
+  const S t = cs * (s12 + s12);
+  o[sidx<K>(K, K)] = a[sidx<K>(K, K)];
+  o[sidx<K>(k1, k1)] = cc * s11 - t + ss * s22;
+  o[sidx<K>(k2, k2)] = ss * s11 + t + cc * s22;
+  o[sidx<K>(k1, k2)] = cs * (s11 - s22) + (cc - ss) * s12;
+  o[sidx<K>(k1, K)] = c * s1k - s * s2k;
+  o[sidx<K>(k2, K)] = s * s1k + c * s2k;
+}
+// general 3x3 (row-major) rotated in the plane about axis K: R B Rᵀ
+template <int K, class S>
+__device__ __forceinline__ void plane_rot_full(const S& c, const S& s, const S* B, S* o) {
+  constexpr int k1 = (K + 1) % 3, k2 = (K + 2) % 3;
+  S t[9];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {  // rows
+    t[K * 3 + j] = B[K * 3 + j];
+    t[k1 * 3 + j] = c * B[k1 * 3 + j] - s * B[k2 * 3 + j];
+    t[k2 * 3 + j] = s * B[k1 * 3 + j] + c * B[k2 * 3 + j];
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {  // columns
+    o[r * 3 + K] = t[r * 3 + K];
+    o[r * 3 + k1] = c * t[r * 3 + k1] - s * t[r * 3 + k2];
+    o[r * 3 + k2] = s * t[r * 3 + k1] + c * t[r * 3 + k2];
+  }
+}
+
+// Stage helpers for X = X_off ∘ X_J.  The joint stage is a plane rotation
+// (axis-aligned revolute), Rodrigues (general revolute) or a translation
+// along the axis (prismatic); the offset stage skips an identity rotation /
+// zero translation (model flags, uniform per joint).
 template <class V>
 struct JointX {
   using S = typename V::S;
-  S QJ[9], tJ[3], QO[9], tO[3];
+  int code;        // 0..5 unit axis ±x,±y,±z ; 6 general
   bool prismatic;
+  bool qo_id, to_zero;
+  S c, s;          // revolute: cos q, ±sin q (sign of the axis folded in)
+  S QJ[9];         // general revolute only
+  S tJ[3];         // prismatic only
+  S QO[9], tO[3];
   __device__ __forceinline__ void load(const V& mv, int i, const JM<S>& j) {
     prismatic = mv.kind(i) == 1;
+    code = mv.axis_code(i);
+    const int of = mv.oflags(i);
+    qo_id = (of & kOffRotIdentity) != 0;
+    to_zero = (of & kOffTransZero) != 0;
     if (prismatic) {
+      joint_translation(mv, i, j, tJ);
+    } else if (V::kStatic || code == 6) {
+      // static views: a full Q whose structural zeros fold (sp flags)
+      joint_rotation(mv, i, j, QJ);
+    } else {
+      c = j.c;
+      s = code < 3 ? j.s : -j.s;
+    }
+    if (V::kStatic || !qo_id) offset_rotation(mv, i, QO);
+    if (V::kStatic || !to_zero) offset_translation(mv, i, tO);
+    if (V::kStatic && prismatic) {  // identity joint rotation with folding zeros
       const S one(typename V::Real(1), true);
 #pragma unroll
       for (int k = 0; k < 9; ++k) QJ[k] = (k % 4 == 0) ? one : S();
-      joint_translation(mv, i, j, tJ);
-    } else {
-      joint_rotation(mv, i, j, QJ);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) tJ[k] = S();
     }
-    offset_rotation(mv, i, QO);
-    offset_translation(mv, i, tO);
+  }
+  // R_J x (dir > 0) or R_Jᵀ x (dir < 0); revolute only
+  __device__ __forceinline__ void jrot(const S* x, S* y, int dir) const {
+    if (!V::kStatic && code < 6) {
+      const S sg = dir > 0 ? s : -s;
+      VD_WITH_AXIS(code % 3, plane_rot<K>(c, sg, x, y);)
+    } else if (dir > 0) {
+      matvec(QJ, x, y);
+    } else {
+      matTvec(QJ, x, y);
+    }
+  }
+  // joint stage, parent side -> child side (inverse_transform_motion)
+  __device__ __forceinline__ SV<S> j_motion_in(const SV<S>& m) const {
+    SV<S> o;
+    if (!prismatic) {
+      jrot(m.a, o.a, -1);
+      jrot(m.l, o.l, -1);
+    } else {
+      S tw[3];
+      cross3(tJ, m.a, tw);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        o.a[k] = m.a[k];
+        o.l[k] = m.l[k] - tw[k];
+      }
+    }
+    return o;
+  }
+  __device__ __forceinline__ SV<S> j_motion_out(const SV<S>& m) const {
+    SV<S> o;
+    if (!prismatic) {
+      jrot(m.a, o.a, 1);
+      jrot(m.l, o.l, 1);
+    } else {
+      S tw[3];
+      cross3(tJ, m.a, tw);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        o.a[k] = m.a[k];
+        o.l[k] = m.l[k] + tw[k];
+      }
+    }
+    return o;
+  }
+  __device__ __forceinline__ SV<S> j_force_out(const SV<S>& f) const {
+    SV<S> o;
+    if (!prismatic) {
+      jrot(f.a, o.a, 1);
+      jrot(f.l, o.l, 1);
+    } else {
+      S tf[3];
+      cross3(tJ, f.l, tf);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        o.a[k] = f.a[k] + tf[k];
+        o.l[k] = f.l[k];
+      }
+    }
+    return o;
+  }
+  // offset stage
+  __device__ __forceinline__ SV<S> o_motion_in(const SV<S>& m) const {
+    if (qo_id && to_zero) return m;
+    if (qo_id) {
+      SV<S> o = m;
+      S tw[3];
+      cross3(tO, m.a, tw);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) o.l[k] = m.l[k] - tw[k];
+      return o;
+    }
+    return motion_in(QO, tO, !to_zero, m);
+  }
+  __device__ __forceinline__ SV<S> o_motion_out(const SV<S>& m) const {
+    if (qo_id && to_zero) return m;
+    if (qo_id) {
+      SV<S> o = m;
+      S tw[3];
+      cross3(tO, m.a, tw);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) o.l[k] = m.l[k] + tw[k];
+      return o;
+    }
+    return motion_out(QO, tO, !to_zero, m);
+  }
+  __device__ __forceinline__ SV<S> o_force_out(const SV<S>& f) const {
+    if (qo_id && to_zero) return f;
+    if (qo_id) {
+      SV<S> o = f;
+      S tf[3];
+      cross3(tO, f.l, tf);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) o.a[k] = f.a[k] + tf[k];
+      return o;
+    }
+    return force_out(QO, tO, !to_zero, f);
   }
   // parent -> child (inverse_transform_motion of X)
   __device__ __forceinline__ SV<S> motion_to_child(const SV<S>& m) const {
-    return motion_in(QJ, tJ, prismatic, motion_in(QO, tO, true, m));
+    if constexpr (V::kStatic) return motion_in(QJ, tJ, prismatic, motion_in(QO, tO, true, m));
+    return j_motion_in(o_motion_in(m));
   }
   // child -> parent (transform_force of X)
   __device__ __forceinline__ SV<S> force_to_parent(const SV<S>& f) const {
-    return force_out(QO, tO, true, force_out(QJ, tJ, prismatic, f));
+    if constexpr (V::kStatic) return force_out(QO, tO, true, force_out(QJ, tJ, prismatic, f));
+    return o_force_out(j_force_out(f));
   }
   __device__ __forceinline__ SV<S> motion_to_parent(const SV<S>& m) const {
-    return motion_out(QO, tO, true, motion_out(QJ, tJ, prismatic, m));
+    if constexpr (V::kStatic) return motion_out(QO, tO, true, motion_out(QJ, tJ, prismatic, m));
+    return o_motion_out(j_motion_out(m));
   }
 };
 
-// Motion subspace S_i (dynamics.hpp:324-330) in the joint frame.
+// Joint motion subspace S_i and the products with it that the recursions need,
+// specialised for unit axes (the column / component selected directly).
 template <class V>
-__device__ __forceinline__ SV<typename V::S> joint_axis(const V& mv, int i) {
+struct JAxis {
   using S = typename V::S;
-  SV<S> s;
+  int kind, code;
+  S a[3];  // axis (general code)
+  __device__ __forceinline__ JAxis(const V& mv, int i) : kind(mv.kind(i)), code(mv.axis_code(i)) {
+    // static views take the generic path (structural zeros fold through sp)
+    if (V::kStatic) code = 6;
+    if (code == 6)
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    s.a[k] = mv.kind(i) == 0 ? mv.axis(i, k) : S();
-    s.l[k] = mv.kind(i) == 1 ? mv.axis(i, k) : S();
+      for (int k = 0; k < 3; ++k) a[k] = mv.axis(i, k);
   }
-  return s;
-}
+  __device__ __forceinline__ S sgn(const S& x) const { return code < 3 ? x : -x; }
+  // m += S x
+  __device__ __forceinline__ void add(SV<S>& m, const S& x) const {
+    if (code < 6) {
+      const S y = sgn(x);
+      VD_WITH_AXIS(code % 3, if (kind == 0) m.a[K] += y;
+        else m.l[K] += y;)
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        if (kind == 0) m.a[k] += a[k] * x;
+        else m.l[k] += a[k] * x;
+      }
+    }
+  }
+  __device__ __forceinline__ SV<S> scaled(const S& x) const {
+    SV<S> m;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) m.a[k] = m.l[k] = S();
+    add(m, x);
+    return m;
+  }
+  // Sᵀ f
+  __device__ __forceinline__ S dot(const SV<S>& f) const {
+    if (code < 6) {
+      S r;
+      VD_WITH_AXIS(code % 3, r = kind == 0 ? f.a[K] : f.l[K];)
+      return sgn(r);
+    }
+    return kind == 0 ? dot3(a, f.a) : dot3(a, f.l);
+  }
+  // v × (S x)  (spatial.hpp:204-208 with m = S x)
+  __device__ __forceinline__ SV<S> crm(const SV<S>& v, const S& x) const {
+    if (code < 6) {
+      SV<S> o;
+      const S y = sgn(x);
+      VD_WITH_AXIS(code % 3, constexpr int k = K, k1 = (k + 1) % 3, k2 = (k + 2) % 3;
+        // w × e_k = (.., w_k2 at k1, -w_k1 at k2)
+        if (kind == 0) {
+          o.a[k] = S();
+          o.a[k1] = v.a[k2] * y;
+          o.a[k2] = -(v.a[k1] * y);
+          o.l[k] = S();
+          o.l[k1] = v.l[k2] * y;
+          o.l[k2] = -(v.l[k1] * y);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 3; ++j) o.a[j] = S();
+          o.l[k] = S();
+          o.l[k1] = v.a[k2] * y;
+          o.l[k2] = -(v.a[k1] * y);
+        })
+      return o;
+    }
+    SV<S> m;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      m.a[k] = kind == 0 ? a[k] * x : S();
+      m.l[k] = kind == 1 ? a[k] * x : S();
+    }
+    return vdk::crm(v, m);
+  }
+};
 
 // ================================================================== rigid-body inertia (10 params)
 template <class S>
@@ -496,12 +767,19 @@ __device__ __forceinline__ void full_rotate(const S* Q, const S* B, S* out) {  /
 // transform_inertia (spatial.hpp:259-267) on the 10-param form, X = (Q, t):
 //   h' = Q h + m t ;  I' = Q I Qᵀ − t gᵀ − g tᵀ + 2 (g·t) 1 + m (|t|² 1 − t tᵀ),  g = Q h
 template <class S>
-__device__ __forceinline__ RB<S> rb_out(const RB<S>& b, const S* Q, const S* t, bool has_t) {
+__device__ __forceinline__ RB<S> rb_out(const RB<S>& b, const S* Q, const S* t, bool has_t, bool has_q = true) {
   RB<S> o;
   o.m = b.m;
   S g[3];
-  matvec(Q, b.h, g);
-  sym_rotate(Q, b.I, o.I);
+  if (has_q) {
+    matvec(Q, b.h, g);
+    sym_rotate(Q, b.I, o.I);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g[k] = b.h[k];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) o.I[k] = b.I[k];
+  }
   if (!has_t) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) o.h[k] = g[k];
@@ -527,7 +805,20 @@ __device__ __forceinline__ RB<S> rb_out(const RB<S>& b, const S* Q, const S* t, 
 }
 template <class V>
 __device__ __forceinline__ RB<typename V::S> rb_to_parent(const JointX<V>& x, const RB<typename V::S>& b) {
-  return rb_out(rb_out(b, x.QJ, x.tJ, x.prismatic), x.QO, x.tO, true);
+  using S = typename V::S;
+  if constexpr (V::kStatic) return rb_out(rb_out(b, x.QJ, x.tJ, x.prismatic), x.QO, x.tO, true);
+  RB<S> mid;
+  if (x.prismatic) {
+    mid = rb_out(b, static_cast<const S*>(nullptr), x.tJ, true, false);
+  } else if (!V::kStatic && x.code < 6) {
+    mid.m = b.m;
+    VD_WITH_AXIS(x.code % 3, plane_rot<K>(x.c, x.s, b.h, mid.h);
+      plane_rot_sym<K>(x.c, x.s, b.I, mid.I);)
+  } else {
+    mid = rb_out(b, x.QJ, x.tJ, false, true);
+  }
+  if (x.qo_id && x.to_zero) return mid;
+  return rb_out(mid, x.QO, x.tO, !x.to_zero, !x.qo_id);
 }
 
 // ================================================================== articulated inertia (sym 6x6)
@@ -564,6 +855,40 @@ __device__ __forceinline__ SV<S> ai_apply(const AI<S>& I, const SV<S>& v) {
   }
   return f;
 }
+// IA S for the joint's motion subspace: a column of IA for unit axes.
+template <class V>
+__device__ __forceinline__ SV<typename V::S> ai_axis(const JAxis<V>& ax, const AI<typename V::S>& I) {
+  using S = typename V::S;
+  if (!V::kStatic && ax.code < 6) {
+    SV<S> o;
+    VD_WITH_AXIS(ax.code % 3, constexpr int k = K;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        if (ax.kind == 0) {  // column k: (A[:,k]; Bᵀ[:,k] = B[k,:])
+          o.a[r] = sym_at(I.A, r, k);
+          o.l[r] = I.B[k * 3 + r];
+        } else {  // column 3+k: (B[:,k]; C[:,k])
+          o.a[r] = I.B[r * 3 + k];
+          o.l[r] = sym_at(I.C, r, k);
+        }
+      })
+    if (ax.code >= 3) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        o.a[r] = -o.a[r];
+        o.l[r] = -o.l[r];
+      }
+    }
+    return o;
+  }
+  SV<S> s;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    s.a[r] = ax.kind == 0 ? ax.a[r] : S();
+    s.l[r] = ax.kind == 1 ? ax.a[r] : S();
+  }
+  return ai_apply(I, s);
+}
 template <class S>
 __device__ __forceinline__ void ai_add(AI<S>& a, const AI<S>& b) {
 #pragma unroll
@@ -597,11 +922,15 @@ __device__ __forceinline__ void ai_sub_outer(AI<S>& I, const SV<S>& U, const S& 
 // X* IA X*ᵀ for X* = [[Q, t×Q], [0, Q]]: rotate all blocks, then shift by t:
 //   A' = A1 + P B1ᵀ − B1 P − P C1 P ;  B' = B1 + P C1 ;  C' = C1   (P = t×)
 template <class S>
-__device__ __forceinline__ AI<S> ai_out(const AI<S>& I, const S* Q, const S* t, bool has_t) {
+__device__ __forceinline__ AI<S> ai_out(const AI<S>& I, const S* Q, const S* t, bool has_t, bool has_q = true) {
   AI<S> o;
-  sym_rotate(Q, I.A, o.A);
-  sym_rotate(Q, I.C, o.C);
-  full_rotate(Q, I.B, o.B);
+  if (has_q) {
+    sym_rotate(Q, I.A, o.A);
+    sym_rotate(Q, I.C, o.C);
+    full_rotate(Q, I.B, o.B);
+  } else {
+    o = I;
+  }
   if (!has_t) return o;
   S C1[3][3], PC[3][3], W[3][3], Z[3][3];
 #pragma unroll
@@ -637,7 +966,20 @@ __device__ __forceinline__ AI<S> ai_out(const AI<S>& I, const S* Q, const S* t, 
 }
 template <class V>
 __device__ __forceinline__ AI<typename V::S> ai_to_parent(const JointX<V>& x, const AI<typename V::S>& I) {
-  return ai_out(ai_out(I, x.QJ, x.tJ, x.prismatic), x.QO, x.tO, true);
+  using S = typename V::S;
+  if constexpr (V::kStatic) return ai_out(ai_out(I, x.QJ, x.tJ, x.prismatic), x.QO, x.tO, true);
+  AI<S> mid;
+  if (x.prismatic) {
+    mid = ai_out(I, static_cast<const S*>(nullptr), x.tJ, true, false);
+  } else if (!V::kStatic && x.code < 6) {
+    VD_WITH_AXIS(x.code % 3, plane_rot_sym<K>(x.c, x.s, I.A, mid.A);
+      plane_rot_sym<K>(x.c, x.s, I.C, mid.C);
+      plane_rot_full<K>(x.c, x.s, I.B, mid.B);)
+  } else {
+    mid = ai_out(I, x.QJ, x.tJ, false, true);
+  }
+  if (x.qo_id && x.to_zero) return mid;
+  return ai_out(mid, x.QO, x.tO, !x.to_zero, !x.qo_id);
 }
 
 // ================================================================== world poses
@@ -649,20 +991,43 @@ struct WX {  // R row-major, p
 template <class V>
 __device__ __forceinline__ WX<typename V::S> world_of(const JointX<V>& x, const WX<typename V::S>* wp) {
   using S = typename V::S;
+  // local rotation Rl = R_off R_J, translation pl = p_off + R_off t_J
   S Rl[9], pl[3];
+  if constexpr (V::kStatic) {
 #pragma unroll
-  for (int r = 0; r < 3; ++r)
+    for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-      Rl[r * 3 + c] = x.QO[r * 3] * x.QJ[c] + x.QO[r * 3 + 1] * x.QJ[3 + c] + x.QO[r * 3 + 2] * x.QJ[6 + c];
-  if (x.prismatic) {
-    S rt[3];
-    matvec(x.QO, x.tJ, rt);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) pl[k] = x.tO[k] + rt[k];
-  } else {
+      for (int c = 0; c < 3; ++c)
+        Rl[r * 3 + c] = x.QO[r * 3] * x.QJ[c] + x.QO[r * 3 + 1] * x.QJ[3 + c] + x.QO[r * 3 + 2] * x.QJ[6 + c];
 #pragma unroll
     for (int k = 0; k < 3; ++k) pl[k] = x.tO[k];
+    if (x.prismatic) {
+      S rt[3];
+      matvec(x.QO, x.tJ, rt);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) pl[k] += rt[k];
+    }
+  } else {
+    S QOm[9];
+    const S one(typename V::Real(1), true);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) QOm[k] = x.qo_id ? ((k % 4 == 0) ? one : S()) : x.QO[k];
+    if (x.prismatic) {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) Rl[k] = QOm[k];
+    } else {
+      // columns of R_off R_J = R_J applied to rows of R_off: (R_off R_J)[r][:] = R_Jᵀ (row r of R_off)
+#pragma unroll
+      for (int r = 0; r < 3; ++r) x.jrot(&QOm[r * 3], &Rl[r * 3], -1);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) pl[k] = x.to_zero ? S() : x.tO[k];
+    if (x.prismatic) {
+      S rt[3];
+      matvec(QOm, x.tJ, rt);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) pl[k] += rt[k];
+    }
   }
   WX<S> w;
   if (!wp) {

@@ -32,7 +32,7 @@ int match_spec(uint64_t fp, int n) { return match_spec_tables(fp, n); }
 
 int launch_fk(const Launch& L, const void* q, void* out) {
   if (L.N == 0) return 0;
-  return with_view<true>(L, [&](auto mv) { return Launcher<decltype(mv)>::fk(mv, L, q, out); });
+  return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::fk(mv, L, q, out); });
 }
 
 int launch_jacobian(const Launch& L, const void* q, int frame_joint, const double* frame_R, const double* frame_p,
@@ -42,7 +42,7 @@ int launch_jacobian(const Launch& L, const void* q, int frame_joint, const doubl
   fr.joint = frame_joint;
   for (int k = 0; k < 9; ++k) fr.R[k] = frame_R[k];
   for (int k = 0; k < 3; ++k) fr.p[k] = frame_p[k];
-  return with_view<true>(L, [&](auto mv) { return Launcher<decltype(mv)>::jac(mv, L, q, fr, pose, J); });
+  return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::jac(mv, L, q, fr, pose, J); });
 }
 
 int launch_rnea(const Launch& L, int mode, const void* q, const void* qd, const void* qdd, const double* g3,

@@ -2,7 +2,5 @@
 #include "vd_launcher_impl.cuh"
 
 namespace vdk {
-template int Launcher<Tree29D>::fk(const Tree29D&, const Launch&, const void*, void*);
-template int Launcher<Tree29D>::jac(const Tree29D&, const Launch&, const void*, const FrameArg&, void*, void*);
 template int Launcher<Tree29D>::rnea(const Tree29D&, const Launch&, const void*, const void*, const void*, const double*, const void*, void*);
 }  // namespace vdk

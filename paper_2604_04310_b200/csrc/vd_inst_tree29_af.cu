@@ -2,7 +2,5 @@
 #include "vd_launcher_impl.cuh"
 
 namespace vdk {
-template int Launcher<Tree29F>::fk(const Tree29F&, const Launch&, const void*, void*);
-template int Launcher<Tree29F>::jac(const Tree29F&, const Launch&, const void*, const FrameArg&, void*, void*);
 template int Launcher<Tree29F>::rnea(const Tree29F&, const Launch&, const void*, const void*, const void*, const double*, const void*, void*);
 }  // namespace vdk

@@ -31,7 +31,7 @@ __device__ __forceinline__ Cols<T> cols(const T* p, int64_t ld, int64_t i) {
 
 // ---------------------------------------------------------------- FK
 template <class V>
-__global__ void __launch_bounds__(kBlock) k_fk(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_fk(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
                                                 typename V::Real* __restrict__ out, int64_t ldo) {
   using T = typename V::Real;
   using S = typename V::S;
@@ -59,7 +59,7 @@ struct FrameArg {
   double R[9], p[3];  // row-major offset
 };
 template <class V>
-__global__ void __launch_bounds__(kBlock) k_jac(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_jac(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
                                                  FrameArg fr, typename V::Real* __restrict__ pose,
                                                  typename V::Real* __restrict__ J, int64_t ldo) {
   using T = typename V::Real;
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kBlock) k_jac(const __grid_constant__ V mv, in
 
 // ---------------------------------------------------------------- RNEA family
 template <class V, bool kFext>
-__global__ void __launch_bounds__(kBlock) k_rnea(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q,
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_rnea(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q,
                                                   const typename V::Real* __restrict__ qd,
                                                   const typename V::Real* __restrict__ qdd, int64_t ldi,
                                                   G3<typename V::Real> g, const typename V::Real* __restrict__ fext,
@@ -174,7 +174,7 @@ __device__ __forceinline__ void store_mass(const V& mv, const JM<typename V::S>*
       if (!((mv.anc(r) >> c) & 1ull) && !((mv.anc(c) >> r) & 1ull)) o.put(c * n + r, T(0));
 }
 template <class V>
-__global__ void __launch_bounds__(kBlock) k_crba(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_crba(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
                                                   typename V::Real* __restrict__ M, int64_t ldo) {
   using S = typename V::S;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kBlock) k_crba(const __grid_constant__ V mv, i
 
 // ---------------------------------------------------------------- ABA
 template <class V, bool kFext>
-__global__ void __launch_bounds__(kBlock) k_aba(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q,
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_aba(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q,
                                                  const typename V::Real* __restrict__ qd,
                                                  const typename V::Real* __restrict__ tau, int64_t ldi,
                                                  G3<typename V::Real> g, const typename V::Real* __restrict__ fext,
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kBlock) k_aba(const __grid_constant__ V mv, in
 
 // ---------------------------------------------------------------- fused M + bias + q̈ (config 3)
 template <class V>
-__global__ void __launch_bounds__(kBlock) k_dyn(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q,
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_dyn(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q,
                                                  const typename V::Real* __restrict__ qd,
                                                  const typename V::Real* __restrict__ tau, int64_t ldi,
                                                  G3<typename V::Real> g, typename V::Real* __restrict__ M,
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kBlock) k_dyn(const __grid_constant__ V mv, in
 
 // ---------------------------------------------------------------- OSC
 template <class V>
-__global__ void __launch_bounds__(kBlock) k_osc(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q,
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_osc(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q,
                                                  const typename V::Real* __restrict__ qd, int64_t ldi, OscShared P,
                                                  typename V::Real* __restrict__ tau, typename V::Real* __restrict__ lam,
                                                  int64_t ldo, int32_t* __restrict__ status) {

@@ -9,6 +9,9 @@ constexpr int kMaxDof = 64;
 
 constexpr int kFlagLeaf = 1;
 constexpr int kFlagBranch = 2;
+constexpr int kOffRotIdentity = 1;  // offset rotation is exactly the identity
+constexpr int kOffTransZero = 2;    // offset translation is exactly zero
+constexpr int kMassless = 4;        // all 10 inertia parameters are zero
 
 // Device-resident model for the generic (runtime-topology) kernels.
 template <class T>
@@ -20,6 +23,7 @@ struct DevModel {
   int depth[kMaxDof];      // moving joints on the path root..i (1 for root joints)
   uint64_t anc[kMaxDof];   // bit j set iff j is i or an ancestor of i (ancestor mask row)
   int flags[kMaxDof];      // kFlagLeaf: no children; kFlagBranch: has a child other than i+1
+  int oflags[kMaxDof];     // kOffRotIdentity | kOffTransZero | kMassless
   T axis[kMaxDof][3];
   T R[kMaxDof][9];         // offset rotation, row-major
   T p[kMaxDof][3];
