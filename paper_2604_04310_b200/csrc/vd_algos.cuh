@@ -14,6 +14,13 @@ struct Cols {
   int64_t ld, i;
   __device__ __forceinline__ T operator[](int k) const { return base ? __ldg(base + (int64_t)k * ld + i) : T(0); }
 };
+// A per-thread copy of an input row (loop kernels preload their inputs so the
+// n independent global loads are all in flight at once).
+template <class T>
+struct Row {
+  const T* v;
+  __device__ __forceinline__ T operator[](int k) const { return v[k]; }
+};
 template <class T>
 struct OutCols {
   T* __restrict__ base;
@@ -156,10 +163,10 @@ __device__ __forceinline__ void crba_one(const V& mv, const JM<typename V::S>* j
 //    (leaf -> root) reconstructs v_{i-1} = X_i (v_i − S_i q̇_i) from its child,
 //    pass 3 recomputes them root -> leaf;
 //  * the per-joint state carried from pass 2 to pass 3 is U_i, u_i, 1/D_i.
-template <class V, bool kFext>
-__device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm, const Cols<typename V::Real>& qd,
-                                        const Cols<typename V::Real>& tau, const typename V::Real* g3,
-                                        const Cols<typename V::Real>* fext, typename V::S* qdd) {
+template <class V, bool kFext, class QdAcc, class TauAcc>
+__device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm, const QdAcc& qd, const TauAcc& tau,
+                                        const typename V::Real* g3, const Cols<typename V::Real>* fext,
+                                        typename V::S* qdd) {
   using S = typename V::S;
   using T = typename V::Real;
   constexpr int NM = V::kMax;

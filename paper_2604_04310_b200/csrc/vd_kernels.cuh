@@ -200,7 +200,17 @@ __global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_aba(const __grid_cons
   load_motion(mv, cols(q, ldi, i), jm);
   const Cols<T> qdc{qd, ldi, i}, tc{tau, ldi, i}, fc{fext, ldi, i};
   S out[V::kMax];
-  const bool ok = aba_one<V, kFext>(mv, jm, qdc, tc, g.g, &fc, out);
+  bool ok;
+  if constexpr (V::kStatic) {
+    ok = aba_one<V, kFext>(mv, jm, qdc, tc, g.g, &fc, out);
+  } else {
+    T qdl[V::kMax], taul[V::kMax];
+    for (int j = 0; j < mv.n(); ++j) {
+      qdl[j] = qdc[j];
+      taul[j] = tc[j];
+    }
+    ok = aba_one<V, kFext>(mv, jm, Row<T>{qdl}, Row<T>{taul}, g.g, &fc, out);
+  }
   OutCols<T> o{qdd, ldo, i};
 #pragma unroll
   for (int j = 0; j < mv.n(); ++j) o.put(j, ok ? out[j].v : T(0));
