@@ -56,10 +56,10 @@ __device__ __forceinline__ void fk_world(const V& mv, const JM<typename V::S>* j
 // ------------------------------------------------------------------ RNEA
 // rnea_loop (dynamics.hpp:427-482): two-pass recursion in local coordinates.
 // qdd == nullptr means q̈ = 0 (bias forces, dynamics.hpp:434-435).
-template <class V, bool kFext>
-__device__ __forceinline__ void rnea_one(const V& mv, const JM<typename V::S>* jm, const Cols<typename V::Real>& qd,
-                                         const Cols<typename V::Real>* qdd, const typename V::Real* g3,
-                                         const Cols<typename V::Real>* fext, typename V::S* tau) {
+template <class V, bool kFext, class QdA, class QddA>
+__device__ __forceinline__ void rnea_one(const V& mv, const JM<typename V::S>* jm, const QdA& qd, const QddA* qdd,
+                                         const typename V::Real* g3, const Cols<typename V::Real>* fext,
+                                         typename V::S* tau) {
   using S = typename V::S;
   SV<S> v[V::kMax], a[V::kMax], f[V::kMax];
   WX<S> W[kFext ? V::kMax : 1];
@@ -394,10 +394,9 @@ __device__ __forceinline__ void chol6_solve(const T* L, T* b) {
 // branch-sparse LTL of RBDA §6.5 (M = Lᵀ L, L with the ancestor sparsity of
 // M, no fill-in) instead of a dense LLT; both give M⁻¹ x exactly in exact
 // arithmetic, and both fail exactly when M is not positive definite.
-template <class V>
-__device__ __forceinline__ bool osc_one(const V& mv, const JM<typename V::S>* jm, const Cols<typename V::Real>& q,
-                                        const Cols<typename V::Real>& qd, const OscShared& P,
-                                        typename V::Real* tau_out, typename V::Real* lambda_out) {
+template <class V, class QA>
+__device__ __forceinline__ bool osc_one(const V& mv, const JM<typename V::S>* jm, const QA& q, const QA& qd,
+                                        const OscShared& P, typename V::Real* tau_out, typename V::Real* lambda_out) {
   using S = typename V::S;
   using T = typename V::Real;
   constexpr int NM = V::kMax;
@@ -413,7 +412,7 @@ __device__ __forceinline__ bool osc_one(const V& mv, const JM<typename V::S>* jm
   S bias[NM];
   {
     const T g3[3] = {T(P.gravity[0]), T(P.gravity[1]), T(P.gravity[2])};
-    rnea_one<V, false>(mv, jm, qd, nullptr, g3, nullptr, bias);
+    rnea_one<V, false, QA, QA>(mv, jm, qd, static_cast<const QA*>(nullptr), g3, nullptr, bias);
   }
   // --- frame pose and Jacobian (kinematics.hpp:89-129)
   WX<S> W[NM];

@@ -1,0 +1,6 @@
+// Explicit instantiation unit (parallel build); see vd_kernels.cuh.
+#include "vd_launcher_impl.cuh"
+
+namespace vdk {
+template int Launcher<Chain7D>::aba(const Chain7D&, const Launch&, const void*, const void*, const void*, const double*, const void*, void*, int32_t*);
+}  // namespace vdk

@@ -2,6 +2,5 @@
 #include "vd_launcher_impl.cuh"
 
 namespace vdk {
-template struct Launcher<Chain7D>;
-template struct Launcher<Chain7F>;
+template int Launcher<Chain7D>::osc(const Chain7D&, const Launch&, const void*, const void*, const OscShared&, void*, void*, int32_t*);
 }  // namespace vdk

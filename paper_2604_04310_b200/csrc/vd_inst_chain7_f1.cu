@@ -1,0 +1,6 @@
+// Explicit instantiation unit (parallel build); see vd_kernels.cuh.
+#include "vd_launcher_impl.cuh"
+
+namespace vdk {
+template int Launcher<Chain7F>::rnea(const Chain7F&, const Launch&, const void*, const void*, const void*, const double*, const void*, void*);
+}  // namespace vdk

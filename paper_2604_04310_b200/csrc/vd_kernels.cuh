@@ -8,6 +8,7 @@
 #include "vd_algos.cuh"
 #include "vd_launch.hpp"
 #include "vd_robots_gen.cuh"
+#include "vd_tma.cuh"
 
 namespace vdk {
 
@@ -18,8 +19,8 @@ struct G3 {
   T g[3];
 };
 
-template <class V>
-__device__ __forceinline__ void load_motion(const V& mv, const Cols<typename V::Real>& q, JM<typename V::S>* jm) {
+template <class V, class A>
+__device__ __forceinline__ void load_motion(const V& mv, const A& q, JM<typename V::S>* jm) {
 #pragma unroll
   for (int j = 0; j < mv.n(); ++j) jm[j] = joint_motion(mv, j, q[j]);
 }
@@ -30,15 +31,12 @@ __device__ __forceinline__ Cols<T> cols(const T* p, int64_t ld, int64_t i) {
 }
 
 // ---------------------------------------------------------------- FK
-template <class V>
-__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_fk(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
-                                                typename V::Real* __restrict__ out, int64_t ldo) {
+template <class V, class A>
+__device__ __forceinline__ void fk_body(const V& mv, const A& q, int64_t i, typename V::Real* out, int64_t ldo) {
   using T = typename V::Real;
   using S = typename V::S;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= N) return;
   JM<S> jm[V::kMax];
-  load_motion(mv, cols(q, ldi, i), jm);
+  load_motion(mv, q, jm);
   WX<S> W[V::kMax];
   fk_world(mv, jm, W);
   OutCols<T> o{out, ldo, i};
@@ -52,22 +50,27 @@ __global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_fk(const __grid_const
     for (int r = 0; r < 3; ++r) o.put(j * 12 + 9 + r, W[j].p[r].v);
   }
 }
+template <class V>
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_fk(const __grid_constant__ V mv, int64_t N,
+                                                              const typename V::Real* __restrict__ q, int64_t ldi,
+                                                              typename V::Real* __restrict__ out, int64_t ldo) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  fk_body(mv, cols(q, ldi, i), i, out, ldo);
+}
 
 // ---------------------------------------------------------------- frame pose + Jacobian
 struct FrameArg {
   int joint;
   double R[9], p[3];  // row-major offset
 };
-template <class V>
-__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_jac(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q, int64_t ldi,
-                                                 FrameArg fr, typename V::Real* __restrict__ pose,
-                                                 typename V::Real* __restrict__ J, int64_t ldo) {
+template <class V, class A>
+__device__ __forceinline__ void jac_body(const V& mv, const A& q, int64_t i, const FrameArg& fr,
+                                         typename V::Real* pose, typename V::Real* J, int64_t ldo) {
   using T = typename V::Real;
   using S = typename V::S;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= N) return;
   JM<S> jm[V::kMax];
-  load_motion(mv, cols(q, ldi, i), jm);
+  load_motion(mv, q, jm);
   WX<S> W[V::kMax];
   fk_world(mv, jm, W);
   // frame_transform (kinematics.hpp:89-96)
@@ -132,6 +135,15 @@ __global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_jac(const __grid_cons
     }
   }
 }
+template <class V>
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_jac(const __grid_constant__ V mv, int64_t N,
+                                                               const typename V::Real* __restrict__ q, int64_t ldi,
+                                                               FrameArg fr, typename V::Real* __restrict__ pose,
+                                                               typename V::Real* __restrict__ J, int64_t ldo) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  jac_body(mv, cols(q, ldi, i), i, fr, pose, J, ldo);
+}
 
 // ---------------------------------------------------------------- RNEA family
 template <class V, bool kFext>
@@ -148,7 +160,7 @@ __global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_rnea(const __grid_con
   load_motion(mv, cols(q, ldi, i), jm);
   const Cols<T> qdc{qd, ldi, i}, qddc{qdd, ldi, i}, fc{fext, ldi, i};
   S out[V::kMax];
-  rnea_one<V, kFext>(mv, jm, qdc, qdd ? &qddc : nullptr, g.g, &fc, out);
+  rnea_one<V, kFext>(mv, jm, qdc, qdd ? &qddc : static_cast<const Cols<T>*>(nullptr), g.g, &fc, out);
   OutCols<T> o{tau, ldo, i};
 #pragma unroll
   for (int j = 0; j < mv.n(); ++j) o.put(j, out[j].v);
@@ -218,53 +230,56 @@ __global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_aba(const __grid_cons
 }
 
 // ---------------------------------------------------------------- fused M + bias + q̈ (config 3)
-template <class V>
-__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_dyn(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q,
-                                                 const typename V::Real* __restrict__ qd,
-                                                 const typename V::Real* __restrict__ tau, int64_t ldi,
-                                                 G3<typename V::Real> g, typename V::Real* __restrict__ M,
-                                                 typename V::Real* __restrict__ bias, typename V::Real* __restrict__ qdd,
-                                                 int64_t ldo, int32_t* __restrict__ status) {
+template <class V, class A>
+__device__ __forceinline__ void dyn_body(const V& mv, const A& q, const A& qd, const A& tau, int64_t i,
+                                         const G3<typename V::Real>& g, typename V::Real* M, typename V::Real* bias,
+                                         typename V::Real* qdd, int64_t ldo, int32_t* status) {
   using T = typename V::Real;
   using S = typename V::S;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= N) return;
   JM<S> jm[V::kMax];
-  load_motion(mv, cols(q, ldi, i), jm);
-  const Cols<T> qdc{qd, ldi, i}, tc{tau, ldi, i};
+  load_motion(mv, q, jm);
   if (M) store_mass(mv, jm, M, ldo, i);
   if (bias) {
     S b[V::kMax];
-    rnea_one<V, false>(mv, jm, qdc, nullptr, g.g, nullptr, b);
+    rnea_one<V, false>(mv, jm, qd, static_cast<const A*>(nullptr), g.g, nullptr, b);
     OutCols<T> o{bias, ldo, i};
 #pragma unroll
     for (int j = 0; j < mv.n(); ++j) o.put(j, b[j].v);
   }
   if (qdd) {
     S a[V::kMax];
-    const bool ok = aba_one<V, false>(mv, jm, qdc, tc, g.g, nullptr, a);
+    const bool ok = aba_one<V, false>(mv, jm, qd, tau, g.g, nullptr, a);
     OutCols<T> o{qdd, ldo, i};
 #pragma unroll
     for (int j = 0; j < mv.n(); ++j) o.put(j, ok ? a[j].v : T(0));
     if (status) status[i] = ok ? 0 : 7;
   }
 }
-
-// ---------------------------------------------------------------- OSC
 template <class V>
-__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_osc(const __grid_constant__ V mv, int64_t N, const typename V::Real* __restrict__ q,
-                                                 const typename V::Real* __restrict__ qd, int64_t ldi, OscShared P,
-                                                 typename V::Real* __restrict__ tau, typename V::Real* __restrict__ lam,
-                                                 int64_t ldo, int32_t* __restrict__ status) {
-  using T = typename V::Real;
-  using S = typename V::S;
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_dyn(const __grid_constant__ V mv, int64_t N,
+                                                               const typename V::Real* __restrict__ q,
+                                                               const typename V::Real* __restrict__ qd,
+                                                               const typename V::Real* __restrict__ tau, int64_t ldi,
+                                                               G3<typename V::Real> g, typename V::Real* __restrict__ M,
+                                                               typename V::Real* __restrict__ bias,
+                                                               typename V::Real* __restrict__ qdd, int64_t ldo,
+                                                               int32_t* __restrict__ status) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= N) return;
-  const Cols<T> qc{q, ldi, i}, qdc{qd, ldi, i};
+  dyn_body(mv, cols(q, ldi, i), cols(qd, ldi, i), cols(tau, ldi, i), i, g, M, bias, qdd, ldo, status);
+}
+
+// ---------------------------------------------------------------- OSC
+template <class V, class A>
+__device__ __forceinline__ void osc_body(const V& mv, const A& q, const A& qd, int64_t i, const OscShared& P,
+                                         typename V::Real* tau, typename V::Real* lam, int64_t ldo,
+                                         int32_t* status) {
+  using T = typename V::Real;
+  using S = typename V::S;
   JM<S> jm[V::kMax];
-  load_motion(mv, qc, jm);
+  load_motion(mv, q, jm);
   T t[V::kMax], L[36];
-  const bool ok = osc_one(mv, jm, qc, qdc, P, t, lam ? L : nullptr);
+  const bool ok = osc_one(mv, jm, q, qd, P, t, lam ? L : nullptr);
   OutCols<T> o{tau, ldo, i};
 #pragma unroll
   for (int j = 0; j < mv.n(); ++j) o.put(j, ok ? t[j] : T(0));
@@ -275,6 +290,182 @@ __global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_osc(const __grid_cons
   }
   if (status) status[i] = ok ? 0 : 7;
 }
+template <class V>
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_osc(const __grid_constant__ V mv, int64_t N,
+                                                               const typename V::Real* __restrict__ q,
+                                                               const typename V::Real* __restrict__ qd, int64_t ldi,
+                                                               OscShared P, typename V::Real* __restrict__ tau,
+                                                               typename V::Real* __restrict__ lam, int64_t ldo,
+                                                               int32_t* __restrict__ status) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  osc_body(mv, cols(q, ldi, i), cols(qd, ldi, i), i, P, tau, lam, ldo, status);
+}
+
+// ---------------------------------------------------------------- TMA-staged persistent driver (static views)
+// Same math as the plain kernels; inputs arrive through the two-stage
+// bulk-copy pipeline of vd_tma.cuh.  Full tiles only; the N % kBlock tail is
+// done by CTA 0 with direct loads.  Requires 16-byte aligned planes (checked
+// on the host) and 2 stages x Op::kGroups x n planes x kBlock of shared memory.
+template <class V, class Op>
+__global__ void __launch_bounds__(kBlock, Op::kMinBlocks) k_tiled(const __grid_constant__ V mv,
+                                                                 const __grid_constant__ Op op, int64_t N,
+                                                                 tma::Inputs<typename V::Real> in, int64_t ldi) {
+  using T = typename V::Real;
+  constexpr int n = V::kMax;
+  constexpr int G = Op::kGroups;
+  __shared__ __align__(128) T buf[2][G * n * kBlock];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  const int64_t full = N / kBlock;
+  if (tid == 0) {
+    tma::mbar_init(&bar[0], 1);
+    tma::mbar_init(&bar[1], 1);
+    tma::fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t t0 = blockIdx.x, step = gridDim.x;
+  if (tid == 0) {
+    if (t0 < full) tma::issue_tile<T, kBlock>(buf[0], in, n, ldi, t0, &bar[0]);
+    if (t0 + step < full) tma::issue_tile<T, kBlock>(buf[1], in, n, ldi, t0 + step, &bar[1]);
+  }
+  int it = 0;
+  for (int64_t t = t0; t < full; t += step, ++it) {
+    const int st = it & 1;
+    tma::mbar_wait(&bar[st], (it >> 1) & 1);
+    const T* b = buf[st] + tid;
+    op.run(mv, SmemRow<T, kBlock>{b}, SmemRow<T, kBlock>{b + (G > 1 ? n : 0) * kBlock},
+           SmemRow<T, kBlock>{b + (G > 2 ? 2 * n : 0) * kBlock}, t * kBlock + tid);
+    __syncthreads();  // every thread is done reading stage st
+    if (tid == 0 && t + 2 * step < full) {
+      tma::fence_proxy_async();
+      tma::issue_tile<T, kBlock>(buf[st], in, n, ldi, t + 2 * step, &bar[st]);
+    }
+  }
+  if (blockIdx.x == 0) {  // tail
+    const int64_t i = full * kBlock + tid;
+    if (i < N) op.run(mv, cols(in.p[0], ldi, i), cols(in.p[1], ldi, i), cols(in.p[2], ldi, i), i);
+  }
+}
+
+template <class T>
+struct OpABA {
+  static constexpr int kMinBlocks = 3;
+  static constexpr bool kEnabled = true;
+  static constexpr int kGroups = 3;
+  G3<T> g;
+  T* qdd;
+  int64_t ldo;
+  int32_t* status;
+  template <class V, class A>
+  __device__ __forceinline__ void run(const V& mv, const A& q, const A& qd, const A& tau, int64_t i) const {
+    using S = typename V::S;
+    JM<S> jm[V::kMax];
+    load_motion(mv, q, jm);
+    S out[V::kMax];
+    const bool ok = aba_one<V, false>(mv, jm, qd, tau, g.g, nullptr, out);
+    OutCols<T> o{qdd, ldo, i};
+#pragma unroll
+    for (int j = 0; j < mv.n(); ++j) o.put(j, ok ? out[j].v : T(0));
+    if (status) status[i] = ok ? 0 : 7;
+  }
+};
+// G = 3: rnea(q, qd, qdd); G = 2: qdd = 0 (bias / coriolis); G = 1: qd = qdd = 0 (gravity)
+template <class T, int G>
+struct OpRNEA {
+  static constexpr int kMinBlocks = 0;
+  static constexpr bool kEnabled = true;
+  static constexpr int kGroups = G;
+  G3<T> g;
+  T* tau;
+  int64_t ldo;
+  template <class V, class A>
+  __device__ __forceinline__ void run(const V& mv, const A& q, const A& qd, const A& qdd, int64_t i) const {
+    using S = typename V::S;
+    JM<S> jm[V::kMax];
+    load_motion(mv, q, jm);
+    S out[V::kMax];
+    if constexpr (G == 3) {
+      rnea_one<V, false>(mv, jm, qd, &qdd, g.g, nullptr, out);
+    } else if constexpr (G == 2) {
+      rnea_one<V, false>(mv, jm, qd, static_cast<const A*>(nullptr), g.g, nullptr, out);
+    } else {
+      const Cols<T> zero{nullptr, 0, 0};
+      rnea_one<V, false>(mv, jm, zero, static_cast<const Cols<T>*>(nullptr), g.g, nullptr, out);
+    }
+    OutCols<T> o{tau, ldo, i};
+#pragma unroll
+    for (int j = 0; j < mv.n(); ++j) o.put(j, out[j].v);
+  }
+};
+template <class T>
+struct OpCRBA {
+  static constexpr int kMinBlocks = 0;
+  static constexpr bool kEnabled = true;
+  static constexpr int kGroups = 1;
+  T* M;
+  int64_t ldo;
+  template <class V, class A>
+  __device__ __forceinline__ void run(const V& mv, const A& q, const A&, const A&, int64_t i) const {
+    JM<typename V::S> jm[V::kMax];
+    load_motion(mv, q, jm);
+    store_mass(mv, jm, M, ldo, i);
+  }
+};
+template <class T>
+struct OpFK {
+  static constexpr int kMinBlocks = 0;
+  static constexpr bool kEnabled = true;
+  static constexpr int kGroups = 1;
+  T* out;
+  int64_t ldo;
+  template <class V, class A>
+  __device__ __forceinline__ void run(const V& mv, const A& q, const A&, const A&, int64_t i) const {
+    fk_body(mv, q, i, out, ldo);
+  }
+};
+template <class T>
+struct OpJac {
+  static constexpr int kMinBlocks = 0;
+  static constexpr bool kEnabled = false;
+  static constexpr int kGroups = 1;
+  FrameArg fr;
+  T* pose;
+  T* J;
+  int64_t ldo;
+  template <class V, class A>
+  __device__ __forceinline__ void run(const V& mv, const A& q, const A&, const A&, int64_t i) const {
+    jac_body(mv, q, i, fr, pose, J, ldo);
+  }
+};
+template <class T>
+struct OpDyn {
+  static constexpr int kMinBlocks = 3;
+  static constexpr bool kEnabled = true;
+  static constexpr int kGroups = 3;
+  G3<T> g;
+  T *M, *bias, *qdd;
+  int64_t ldo;
+  int32_t* status;
+  template <class V, class A>
+  __device__ __forceinline__ void run(const V& mv, const A& q, const A& qd, const A& tau, int64_t i) const {
+    dyn_body(mv, q, qd, tau, i, g, M, bias, qdd, ldo, status);
+  }
+};
+template <class T>
+struct OpOSC {
+  static constexpr int kMinBlocks = 0;
+  static constexpr bool kEnabled = false;
+  static constexpr int kGroups = 2;
+  OscShared P;
+  T *tau, *lam;
+  int64_t ldo;
+  int32_t* status;
+  template <class V, class A>
+  __device__ __forceinline__ void run(const V& mv, const A& q, const A& qd, const A&, int64_t i) const {
+    osc_body(mv, q, qd, i, P, tau, lam, ldo, status);
+  }
+};
 
 // ================================================================ per-view launchers
 inline unsigned grid_for(int64_t N) { return (unsigned)((N + kBlock - 1) / kBlock); }

@@ -2,67 +2,132 @@
 // instantiation units so vd_dispatch.cu never re-instantiates the kernels.
 #pragma once
 
+#include <algorithm>
+
 #include "vd_kernels.cuh"
 
 namespace vdk {
 
+// Launch the TMA-staged persistent kernel when the view is compile-time, the
+// two shared-memory stages fit the 48 KB static limit and every input plane
+// is 16-byte aligned; returns -1 when not eligible (caller uses the plain kernel).
+template <class V, class Op>
+int try_tiled(const V& mv, const Launch& L, const Op& op, const void* a, const void* b, const void* c) {
+  using T = typename V::Real;
+  if constexpr (!V::kStatic || !Op::kEnabled) {
+    return -1;
+  } else {
+    constexpr size_t smem = 2ull * Op::kGroups * V::kMax * kBlock * sizeof(T);
+    if constexpr (smem > 48 * 1024) {
+      return -1;
+    } else {
+      const void* ptrs[3] = {a, b, c};
+      bool ok = L.N >= kBlock && (L.ld_in * (int64_t)sizeof(T)) % 16 == 0;
+      for (int g = 0; g < Op::kGroups; ++g) ok = ok && ptrs[g] && ((uintptr_t)ptrs[g] % 16 == 0);
+      if (!ok) return -1;
+      static int blocks_per_sm = 0, sms = 0;
+      if (!blocks_per_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_tiled<V, Op>, kBlock, 0);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+      }
+      const int64_t tiles = L.N / kBlock;
+      const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * blocks_per_sm);
+      tma::Inputs<T> in{{(const T*)a, (const T*)b, (const T*)c}, Op::kGroups};
+      k_tiled<V, Op><<<grid, kBlock, 0, stream_of(L)>>>(mv, op, L.N, in, L.ld_in);
+      return (int)cudaGetLastError();
+    }
+  }
+}
+
 template <class V>
 int Launcher<V>::fk(const V& mv, const Launch& L, const void* q, void* out) {
-  k_fk<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const typename V::Real*)q, L.ld_in, (typename V::Real*)out, L.ld_out);
+  using T = typename V::Real;
+  const int rc = try_tiled(mv, L, OpFK<T>{(T*)out, L.ld_out}, q, nullptr, nullptr);
+  if (rc >= 0) return rc;
+  k_fk<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, L.ld_in, (T*)out, L.ld_out);
   return (int)cudaGetLastError();
 }
 
 template <class V>
 int Launcher<V>::jac(const V& mv, const Launch& L, const void* q, const FrameArg& fr, void* pose, void* J) {
-  k_jac<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const typename V::Real*)q, L.ld_in, fr, (typename V::Real*)pose, (typename V::Real*)J, L.ld_out);
+  using T = typename V::Real;
+  const int rc = try_tiled(mv, L, OpJac<T>{fr, (T*)pose, (T*)J, L.ld_out}, q, nullptr, nullptr);
+  if (rc >= 0) return rc;
+  k_jac<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, L.ld_in, fr, (T*)pose, (T*)J, L.ld_out);
   return (int)cudaGetLastError();
 }
 
 template <class V>
 int Launcher<V>::rnea(const V& mv, const Launch& L, const void* q, const void* qd, const void* qdd, const double* g,
-                  const void* fext, void* tau) {
+                      const void* fext, void* tau) {
+  using T = typename V::Real;
+  if (!fext) {
+    int rc;
+    if (qdd) rc = try_tiled(mv, L, OpRNEA<T, 3>{g3_of<T>(g), (T*)tau, L.ld_out}, q, qd, qdd);
+    else if (qd) rc = try_tiled(mv, L, OpRNEA<T, 2>{g3_of<T>(g), (T*)tau, L.ld_out}, q, qd, nullptr);
+    else rc = try_tiled(mv, L, OpRNEA<T, 1>{g3_of<T>(g), (T*)tau, L.ld_out}, q, nullptr, nullptr);
+    if (rc >= 0) return rc;
+  }
   if (fext)
-    k_rnea<V, true><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const typename V::Real*)q, (const typename V::Real*)qd, (const typename V::Real*)qdd,
-                                                                L.ld_in, g3_of<typename V::Real>(g), (const typename V::Real*)fext, (typename V::Real*)tau, L.ld_out);
+    k_rnea<V, true><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, (const T*)qd, (const T*)qdd,
+                                                                L.ld_in, g3_of<T>(g), (const T*)fext, (T*)tau, L.ld_out);
   else
-    k_rnea<V, false><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const typename V::Real*)q, (const typename V::Real*)qd, (const typename V::Real*)qdd,
-                                                                 L.ld_in, g3_of<typename V::Real>(g), nullptr, (typename V::Real*)tau, L.ld_out);
+    k_rnea<V, false><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, (const T*)qd, (const T*)qdd,
+                                                                 L.ld_in, g3_of<T>(g), nullptr, (T*)tau, L.ld_out);
   return (int)cudaGetLastError();
 }
 
 template <class V>
 int Launcher<V>::crba(const V& mv, const Launch& L, const void* q, void* M) {
-  k_crba<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const typename V::Real*)q, L.ld_in, (typename V::Real*)M, L.ld_out);
+  using T = typename V::Real;
+  const int rc = try_tiled(mv, L, OpCRBA<T>{(T*)M, L.ld_out}, q, nullptr, nullptr);
+  if (rc >= 0) return rc;
+  k_crba<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, L.ld_in, (T*)M, L.ld_out);
   return (int)cudaGetLastError();
 }
 
 template <class V>
 int Launcher<V>::aba(const V& mv, const Launch& L, const void* q, const void* qd, const void* tau, const double* g,
-                 const void* fext, void* qdd, int32_t* status) {
+                     const void* fext, void* qdd, int32_t* status) {
+  using T = typename V::Real;
+  if (!fext) {
+    const int rc = try_tiled(mv, L, OpABA<T>{g3_of<T>(g), (T*)qdd, L.ld_out, status}, q, qd, tau);
+    if (rc >= 0) return rc;
+  }
   if (fext)
-    k_aba<V, true><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const typename V::Real*)q, (const typename V::Real*)qd, (const typename V::Real*)tau,
-                                                               L.ld_in, g3_of<typename V::Real>(g), (const typename V::Real*)fext, (typename V::Real*)qdd, L.ld_out,
+    k_aba<V, true><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, (const T*)qd, (const T*)tau,
+                                                               L.ld_in, g3_of<T>(g), (const T*)fext, (T*)qdd, L.ld_out,
                                                                status);
   else
-    k_aba<V, false><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const typename V::Real*)q, (const typename V::Real*)qd, (const typename V::Real*)tau,
-                                                                L.ld_in, g3_of<typename V::Real>(g), nullptr, (typename V::Real*)qdd, L.ld_out,
+    k_aba<V, false><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, (const T*)qd, (const T*)tau,
+                                                                L.ld_in, g3_of<T>(g), nullptr, (T*)qdd, L.ld_out,
                                                                 status);
   return (int)cudaGetLastError();
 }
 
 template <class V>
-int Launcher<V>::dyn(const V& mv, const Launch& L, const void* q, const void* qd, const void* tau, const double* g, void* M,
-                 void* bias, void* qdd, int32_t* status) {
-  k_dyn<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const typename V::Real*)q, (const typename V::Real*)qd, (const typename V::Real*)tau, L.ld_in,
-                                                        g3_of<typename V::Real>(g), (typename V::Real*)M, (typename V::Real*)bias, (typename V::Real*)qdd, L.ld_out, status);
+int Launcher<V>::dyn(const V& mv, const Launch& L, const void* q, const void* qd, const void* tau, const double* g,
+                     void* M, void* bias, void* qdd, int32_t* status) {
+  using T = typename V::Real;
+  const int rc = try_tiled(mv, L, OpDyn<T>{g3_of<T>(g), (T*)M, (T*)bias, (T*)qdd, L.ld_out, status}, q, qd,
+                           tau ? tau : qd);
+  if (rc >= 0) return rc;
+  k_dyn<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, (const T*)qd, (const T*)tau, L.ld_in,
+                                                        g3_of<T>(g), (T*)M, (T*)bias, (T*)qdd, L.ld_out, status);
   return (int)cudaGetLastError();
 }
 
 template <class V>
 int Launcher<V>::osc(const V& mv, const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau,
-                 void* lambda, int32_t* status) {
-  k_osc<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const typename V::Real*)q, (const typename V::Real*)qd, L.ld_in, P, (typename V::Real*)tau,
-                                                        (typename V::Real*)lambda, L.ld_out, status);
+                     void* lambda, int32_t* status) {
+  using T = typename V::Real;
+  const int rc = try_tiled(mv, L, OpOSC<T>{P, (T*)tau, (T*)lambda, L.ld_out, status}, q, qd, nullptr);
+  if (rc >= 0) return rc;
+  k_osc<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, (const T*)qd, L.ld_in, P, (T*)tau,
+                                                        (T*)lambda, L.ld_out, status);
   return (int)cudaGetLastError();
 }
 
