@@ -123,6 +123,11 @@ int vd_device_model_set_generic(vd_device_model dm, int generic);
 /* forward_kinematics, kinematics.hpp:43-56: plane j*12 + k (k < 9: R column-major, 9..11: p) */
 int vd_fk(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* frames_out,
           int64_t ld_out, void* stream);
+/* forward_kinematics_scan, kinematics.hpp:61-86: same output as vd_fk by a
+ * Hillis–Steele scan (one lane segment per state); serial chains with n <= 32,
+ * VD_ERR_UNSUPPORTED_STRUCTURE otherwise (kinematics.hpp:63-67). */
+int vd_fk_scan(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* frames_out,
+               int64_t ld_out, void* stream);
 /* frame_transform + geometric_jacobian, kinematics.hpp:89-136: pose 12 planes,
  * J 6 x n column-major (plane c*6 + r).  Either output may be NULL. */
 int vd_jacobian(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, int frame, void* pose_out,

@@ -34,7 +34,7 @@ __all__ = [
     "UnsupportedStructureError", "SingularInertiaError", "CudaError", "RobotModel", "DeviceModel", "GravitySpec",
     "TaskGains", "TaskTarget", "PostureGains", "StateBatch", "robots", "urdf", "floating_base", "random_states",
     "rnea", "bias_forces", "gravity_vector", "coriolis_vector", "crba", "forward_dynamics", "dynamics",
-    "forward_kinematics", "frame_transform", "geometric_jacobian", "osc_step", "batch_rnea", "batch_crba",
+    "forward_kinematics", "forward_kinematics_scan", "frame_transform", "geometric_jacobian", "osc_step", "batch_rnea", "batch_crba",
     "batch_forward_dynamics", "shard_range",
 ]
 
@@ -484,6 +484,15 @@ def forward_kinematics(dm, q):
     n = dm.dof()
     out = _out(dev, qs.dtype, 12 * n, N)
     _check(_lib.load().vd_fk(dm.handle, _dtype_code(qs), N, _p(qs), N, _p(out), N, _stream(dev)))
+    return out.t().reshape(N, n, 12)
+
+
+def forward_kinematics_scan(dm, q):
+    """kinematics.hpp:61-86 (serial chains; UnsupportedStructureError otherwise)."""
+    qs, _, N, dev = _prep(dm, q)
+    n = dm.dof()
+    out = _out(dev, qs.dtype, 12 * n, N)
+    _check(_lib.load().vd_fk_scan(dm.handle, _dtype_code(qs), N, _p(qs), N, _p(out), N, _stream(dev)))
     return out.t().reshape(N, n, 12)
 
 

@@ -71,6 +71,7 @@ SIGNATURES = {
     "vd_device_model_specialization": (c_int, [P]),
     "vd_device_model_set_generic": (c_int, [P, c_int]),
     "vd_fk": (c_int, [P, c_int, c_int64, P, c_int64, P, c_int64, P]),
+    "vd_fk_scan": (c_int, [P, c_int, c_int64, P, c_int64, P, c_int64, P]),
     "vd_jacobian": (c_int, [P, c_int, c_int64, P, c_int64, c_int, P, P, c_int64, P]),
     "vd_rnea": (c_int, [P, c_int, c_int64, P, P, P, c_int64, Pd, P, P, c_int64, P]),
     "vd_bias": (c_int, [P, c_int, c_int64, P, P, c_int64, Pd, P, P, c_int64, P]),

@@ -324,6 +324,25 @@ int vd_fk(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in
   return finish(vdk::launch_fk(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, out), "vd_fk");
 }
 
+int vd_fk_scan(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* out, int64_t ld_out,
+               void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  // kinematics.hpp:63-67: serial chains only
+  bool serial = true;
+  for (int i = 0; i < dm->n; ++i) serial = serial && dm->pm.parent[i] == i - 1;
+  if (!serial)
+    return set_error(VD_ERR_UNSUPPORTED_STRUCTURE,
+                     "forward_kinematics_scan requires a serial chain (every joint's parent must be its predecessor)");
+  if (dm->n > 32) return set_error(VD_ERR_UNSUPPORTED_STRUCTURE, "forward_kinematics_scan supports at most 32 joints");
+  VD_NEED(q, "q");
+  VD_NEED(out, "output");
+  if (dm->n == 0) return VD_OK;
+  DeviceGuard g(dm->device);
+  vdk::Launch L = make_launch(dm, dtype, N, ld_in, ld_out, stream);
+  L.spec = vdk::kGeneric;
+  return finish(vdk::launch_fk_scan(L, q, out), "vd_fk_scan");
+}
+
 int vd_jacobian(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, int frame, void* pose,
                 void* J, int64_t ld_out, void* stream) {
   if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;

@@ -80,3 +80,86 @@ int launch_osc(const Launch& L, const void* q, const void* qd, const OscShared& 
 }
 
 }  // namespace vdk
+
+// ---------------------------------------------------------------- forward_kinematics_scan
+// kinematics.hpp:61-86: Hillis–Steele inclusive scan over transform
+// composition, serial chains only.  One segment of `seg` lanes (seg = next
+// power of two >= n, <= 32) per robot state: lane j builds the local
+// transform of joint j, then log2(seg) shuffle rounds compose
+// X_{j-d} ∘ X_j.  Wins over the sequential kernel when N is small (more
+// threads in flight per state, log2 n dependent steps instead of n).
+namespace vdk {
+namespace {
+template <class T>
+__global__ void __launch_bounds__(128) k_fk_scan(const __grid_constant__ DevModel<T> m, int seg, int64_t N,
+                                                 const T* __restrict__ q, int64_t ldi, T* __restrict__ out,
+                                                 int64_t ldo) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % seg;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t i = warp * (32 / seg) + lane / seg;
+  const bool active = i < N && sub < m.n;
+  T R[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)}, p[3] = {T(0), T(0), T(0)};
+  if (active) {
+    const T qi = q[(int64_t)sub * ldi + i];
+    T QJ[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)}, tJ[3] = {T(0), T(0), T(0)};
+    const T a[3] = {m.axis[sub][0], m.axis[sub][1], m.axis[sub][2]};
+    if (m.kind[sub] == 0) {  // Rodrigues, spatial.hpp:302-308
+      T s, c;
+      sincos_t<T>(qi, &s, &c);
+      const T omc = T(1) - c;
+      for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) QJ[r * 3 + k] = a[r] * a[k] * omc + (r == k ? c : T(0));
+      QJ[1] -= a[2] * s;
+      QJ[2] += a[1] * s;
+      QJ[3] += a[2] * s;
+      QJ[5] -= a[0] * s;
+      QJ[6] -= a[1] * s;
+      QJ[7] += a[0] * s;
+    } else {
+      for (int k = 0; k < 3; ++k) tJ[k] = a[k] * qi;
+    }
+    for (int r = 0; r < 3; ++r) {  // X_off ∘ X_J
+      for (int k = 0; k < 3; ++k)
+        R[r * 3 + k] = m.R[sub][r * 3] * QJ[k] + m.R[sub][r * 3 + 1] * QJ[3 + k] + m.R[sub][r * 3 + 2] * QJ[6 + k];
+      p[r] = m.R[sub][r * 3] * tJ[0] + m.R[sub][r * 3 + 1] * tJ[1] + m.R[sub][r * 3 + 2] * tJ[2] + m.p[sub][r];
+    }
+  }
+  for (int d = 1; d < seg; d <<= 1) {
+    T Rn[9], pn[3];
+    for (int k = 0; k < 9; ++k) Rn[k] = __shfl_up_sync(0xffffffffu, R[k], d, seg);
+    for (int k = 0; k < 3; ++k) pn[k] = __shfl_up_sync(0xffffffffu, p[k], d, seg);
+    if (sub >= d) {
+      T R2[9], p2[3];
+      for (int r = 0; r < 3; ++r) {
+        for (int k = 0; k < 3; ++k) R2[r * 3 + k] = Rn[r * 3] * R[k] + Rn[r * 3 + 1] * R[3 + k] + Rn[r * 3 + 2] * R[6 + k];
+        p2[r] = Rn[r * 3] * p[0] + Rn[r * 3 + 1] * p[1] + Rn[r * 3 + 2] * p[2] + pn[r];
+      }
+      for (int k = 0; k < 9; ++k) R[k] = R2[k];
+      for (int k = 0; k < 3; ++k) p[k] = p2[k];
+    }
+  }
+  if (active) {
+    for (int c = 0; c < 3; ++c)
+      for (int r = 0; r < 3; ++r) out[(int64_t)(sub * 12 + c * 3 + r) * ldo + i] = R[r * 3 + c];
+    for (int r = 0; r < 3; ++r) out[(int64_t)(sub * 12 + 9 + r) * ldo + i] = p[r];
+  }
+}
+}  // namespace
+
+int launch_fk_scan(const Launch& L, const void* q, void* out) {
+  if (L.N == 0) return 0;
+  int seg = 1;
+  while (seg < L.n) seg <<= 1;
+  const int64_t threads = ((L.N + (32 / seg) - 1) / (32 / seg)) * 32;
+  const unsigned grid = (unsigned)((threads + 127) / 128);
+  if (L.dtype == 0)
+    k_fk_scan<double><<<grid, 128, 0, static_cast<cudaStream_t>(L.stream)>>>(
+        *static_cast<const DevModel<double>*>(L.model), seg, L.N, (const double*)q, L.ld_in, (double*)out, L.ld_out);
+  else
+    k_fk_scan<float><<<grid, 128, 0, static_cast<cudaStream_t>(L.stream)>>>(
+        *static_cast<const DevModel<float>*>(L.model), seg, L.N, (const float*)q, L.ld_in, (float*)out, L.ld_out);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace vdk

@@ -26,6 +26,8 @@ int match_spec(uint64_t fingerprint, int n);
 
 // All return cudaError_t as int.
 int launch_fk(const Launch& L, const void* q, void* out);
+// forward_kinematics_scan (serial chains, n <= 32)
+int launch_fk_scan(const Launch& L, const void* q, void* out);
 int launch_jacobian(const Launch& L, const void* q, int frame_joint, const double* frame_R, const double* frame_p,
                     void* pose, void* J);
 // mode: 0 full rnea, 1 bias (qdd = 0), 2 gravity (qd = qdd = 0), 3 coriolis (qdd = 0, g = 0)

@@ -253,6 +253,27 @@ def test_fk_and_jacobian(vd, cuda, omodels, name, frame, generic):
     assert rel_err(fk32, fk_ref, axis=1).max() <= TOL32
 
 
+def test_fk_scan(vd, cuda, omodels, oracle):
+    """forward_kinematics_scan (kinematics.hpp:61-86) ≡ sequential FK; rejects trees."""
+    om = omodels["chain7"]
+    m, dm = _dm(vd, "chain7")
+    for N in (1, 5, 4096, 4099):
+        q, _, _, _ = _states(om, N, 81 + N, with_tau=False)
+        ref = om.fk(q, scan=True)
+        assert rel_err(_np(vd.forward_kinematics_scan(dm, _t(q))), ref, axis=1).max() <= 1e-12
+        assert rel_err(_np(vd.forward_kinematics_scan(dm, _t(q, torch.float32))), ref, axis=1).max() <= TOL32
+    # random serial chains n = 1..16 (test_kinematics.cpp:105-120)
+    for n in (1, 3, 8, 9, 16):
+        text = random_urdf(500 + n, n=n, branchiness=0.0, fixed_prob=0.0)
+        o = OModel.from_urdf(text)
+        dmr = vd.DeviceModel(vd.urdf.load_model_from_string(text), 0)
+        q, _, _, _ = o.random_states(300, 7, True, False)
+        assert rel_err(_np(vd.forward_kinematics_scan(dmr, _t(q))), o.fk(q), axis=1).max() <= 1e-12
+    with pytest.raises(vd.UnsupportedStructureError):
+        _, dt = _dm(vd, "tree29")
+        vd.forward_kinematics_scan(dt, _t(np.zeros((4, 29))))
+
+
 # ---------------------------------------------------------------- OSC
 def _osc_case(vd, om, m, dm, name, N, seed, dtype=torch.float64):
     frame = "ee" if name == "chain7" else ("l_palm" if name != "humanoid23" else "r_palm")
