@@ -601,7 +601,8 @@ int run_shard(DevCtx& c, vd_model m, const HostOp& op, int64_t N, int64_t b, int
   const int n = m->m.dof();
   const int width = op.out_width;
   const int64_t len = e - b;
-  const int64_t chunk = std::min<int64_t>(len, std::max<int64_t>(65536, (int64_t)(48ll << 20) / (8ll * (n * op.n_in + width))));
+  int64_t chunk = std::min<int64_t>(len, std::max<int64_t>(65536, (int64_t)(48ll << 20) / (8ll * (n * op.n_in + width))));
+  chunk = (chunk + 127) / 128 * 128;  // device leading dimension: a multiple of the kernels' tile
   bool pinned = is_pinned(out);
   for (int k = 0; k < op.n_in; ++k) pinned = pinned && is_pinned(inputs[k]);
   const bool st_direct = pinned && status && is_pinned(status);
@@ -645,22 +646,23 @@ int run_shard(DevCtx& c, vd_model m, const HostOp& op, int64_t N, int64_t b, int
         src = c.pin_in[slot][i];
         spitch = sizeof(double) * cl;
       }
-      ce = cudaMemcpy2DAsync(c.din[slot][i], sizeof(double) * cl, src, spitch, sizeof(double) * cl, n,
+      ce = cudaMemcpy2DAsync(c.din[slot][i], sizeof(double) * chunk, src, spitch, sizeof(double) * cl, n,
                              cudaMemcpyHostToDevice, s);
     }
     if (ce != cudaSuccess) return cuda_fail(ce, "host batch H2D");
     int rc;
     if (op.kind == 0)
-      rc = vd_rnea(c.dm, VD_F64, cl, c.din[slot][0], c.din[slot][1], c.din[slot][2], cl, g3, nullptr, c.dout[slot], cl, s);
+      rc = vd_rnea(c.dm, VD_F64, cl, c.din[slot][0], c.din[slot][1], c.din[slot][2], chunk, g3, nullptr, c.dout[slot],
+                   chunk, s);
     else if (op.kind == 1)
-      rc = vd_crba(c.dm, VD_F64, cl, c.din[slot][0], cl, c.dout[slot], cl, s);
+      rc = vd_crba(c.dm, VD_F64, cl, c.din[slot][0], chunk, c.dout[slot], chunk, s);
     else
-      rc = vd_aba(c.dm, VD_F64, cl, c.din[slot][0], c.din[slot][1], c.din[slot][2], cl, g3, nullptr, c.dout[slot], cl,
-                  c.dst[slot], s);
+      rc = vd_aba(c.dm, VD_F64, cl, c.din[slot][0], c.din[slot][1], c.din[slot][2], chunk, g3, nullptr, c.dout[slot],
+                  chunk, c.dst[slot], s);
     if (rc) return rc;
     double* dst = pinned ? out + lo : c.pin_out[slot];
     const size_t dpitch = pinned ? sizeof(double) * N : sizeof(double) * cl;
-    ce = cudaMemcpy2DAsync(dst, dpitch, c.dout[slot], sizeof(double) * cl, sizeof(double) * cl, width,
+    ce = cudaMemcpy2DAsync(dst, dpitch, c.dout[slot], sizeof(double) * chunk, sizeof(double) * cl, width,
                            cudaMemcpyDeviceToHost, s);
     if (ce == cudaSuccess && op.kind == 2)
       ce = cudaMemcpyAsync(st_direct ? st_dst + lo : c.pin_st[slot], c.dst[slot], sizeof(int32_t) * cl,

@@ -304,20 +304,22 @@ __global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_osc(const __grid_cons
 
 // ---------------------------------------------------------------- TMA-staged persistent driver (static views)
 // Same math as the plain kernels; inputs arrive through the two-stage
-// bulk-copy pipeline of vd_tma.cuh.  Full tiles only; the N % kBlock tail is
-// done by CTA 0 with direct loads.  Requires 16-byte aligned planes (checked
+// bulk-copy pipeline of vd_tma.cuh.  Requires 16-byte aligned planes (checked
 // on the host) and 2 stages x Op::kGroups x n planes x kBlock of shared memory.
 template <class V, class Op>
 __global__ void __launch_bounds__(kBlock, Op::kMinBlocks) k_tiled(const __grid_constant__ V mv,
                                                                  const __grid_constant__ Op op, int64_t N,
-                                                                 tma::Inputs<typename V::Real> in, int64_t ldi) {
+                                                                 tma::Inputs<typename V::Real> in, int64_t ldi,
+                                                                 bool use_tma) {
   using T = typename V::Real;
   constexpr int n = V::kMax;
   constexpr int G = Op::kGroups;
   __shared__ __align__(128) T buf[2][G * n * kBlock];
   __shared__ __align__(8) uint64_t bar[2];
   const int tid = threadIdx.x;
-  const int64_t full = N / kBlock;
+  // tiles [0, full) arrive by TMA; any other tile (the N % kBlock tail, or all
+  // of them when the planes are not 16-byte aligned) is staged with plain loads
+  const int64_t full = use_tma ? N / kBlock : 0;
   if (tid == 0) {
     tma::mbar_init(&bar[0], 1);
     tma::mbar_init(&bar[1], 1);
@@ -329,22 +331,32 @@ __global__ void __launch_bounds__(kBlock, Op::kMinBlocks) k_tiled(const __grid_c
     if (t0 < full) tma::issue_tile<T, kBlock>(buf[0], in, n, ldi, t0, &bar[0]);
     if (t0 + step < full) tma::issue_tile<T, kBlock>(buf[1], in, n, ldi, t0 + step, &bar[1]);
   }
+  // The N % kBlock tail is the globally last tile: the CTA that reaches it
+  // stages it with plain loads and runs the SAME call site, so every
+  // instance is computed by identical instructions (results do not depend on
+  // where an instance falls in the batch).
+  const int64_t tiles = (N + kBlock - 1) / kBlock;
   int it = 0;
-  for (int64_t t = t0; t < full; t += step, ++it) {
+  for (int64_t t = t0; t < tiles; t += step, ++it) {
     const int st = it & 1;
-    tma::mbar_wait(&bar[st], (it >> 1) & 1);
+    const int64_t i = t * kBlock + tid;
+    if (t < full) {
+      tma::mbar_wait(&bar[st], (it >> 1) & 1);
+    } else {
+      for (int gk = 0; gk < G * n; ++gk) {
+        const int g = gk / n, k = gk - g * n;
+        buf[st][gk * kBlock + tid] = i < N ? in.p[g][(int64_t)k * ldi + i] : T(0);
+      }
+    }
     const T* b = buf[st] + tid;
-    op.run(mv, SmemRow<T, kBlock>{b}, SmemRow<T, kBlock>{b + (G > 1 ? n : 0) * kBlock},
-           SmemRow<T, kBlock>{b + (G > 2 ? 2 * n : 0) * kBlock}, t * kBlock + tid);
+    if (i < N)
+      op.run(mv, SmemRow<T, kBlock>{b}, SmemRow<T, kBlock>{b + (G > 1 ? n : 0) * kBlock},
+             SmemRow<T, kBlock>{b + (G > 2 ? 2 * n : 0) * kBlock}, i);
     __syncthreads();  // every thread is done reading stage st
     if (tid == 0 && t + 2 * step < full) {
       tma::fence_proxy_async();
       tma::issue_tile<T, kBlock>(buf[st], in, n, ldi, t + 2 * step, &bar[st]);
     }
-  }
-  if (blockIdx.x == 0) {  // tail
-    const int64_t i = full * kBlock + tid;
-    if (i < N) op.run(mv, cols(in.p[0], ldi, i), cols(in.p[1], ldi, i), cols(in.p[2], ldi, i), i);
   }
 }
 

@@ -8,9 +8,9 @@
 
 namespace vdk {
 
-// Launch the TMA-staged persistent kernel when the view is compile-time, the
-// two shared-memory stages fit the 48 KB static limit and every input plane
-// is 16-byte aligned; returns -1 when not eligible (caller uses the plain kernel).
+// Launch the staged persistent kernel when the view is compile-time and the
+// two shared-memory stages fit the 48 KB static limit; returns -1 when not
+// eligible (caller uses the plain kernel).
 template <class V, class Op>
 int try_tiled(const V& mv, const Launch& L, const Op& op, const void* a, const void* b, const void* c) {
   using T = typename V::Real;
@@ -21,10 +21,12 @@ int try_tiled(const V& mv, const Launch& L, const Op& op, const void* a, const v
     if constexpr (smem > 48 * 1024) {
       return -1;
     } else {
+      // Compile-time views always run this kernel (one instruction stream for
+      // every instance, whatever N, ld or alignment); TMA is used when every
+      // input plane is 16-byte aligned, otherwise tiles are staged by plain loads.
       const void* ptrs[3] = {a, b, c};
-      bool ok = L.N >= kBlock && (L.ld_in * (int64_t)sizeof(T)) % 16 == 0;
-      for (int g = 0; g < Op::kGroups; ++g) ok = ok && ptrs[g] && ((uintptr_t)ptrs[g] % 16 == 0);
-      if (!ok) return -1;
+      bool aligned = (L.ld_in * (int64_t)sizeof(T)) % 16 == 0;
+      for (int g = 0; g < Op::kGroups; ++g) aligned = aligned && ptrs[g] && ((uintptr_t)ptrs[g] % 16 == 0);
       static int blocks_per_sm = 0, sms = 0;
       if (!blocks_per_sm) {
         int dev = 0;
@@ -33,10 +35,10 @@ int try_tiled(const V& mv, const Launch& L, const Op& op, const void* a, const v
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_tiled<V, Op>, kBlock, 0);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
       }
-      const int64_t tiles = L.N / kBlock;
+      const int64_t tiles = (L.N + kBlock - 1) / kBlock;
       const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * blocks_per_sm);
       tma::Inputs<T> in{{(const T*)a, (const T*)b, (const T*)c}, Op::kGroups};
-      k_tiled<V, Op><<<grid, kBlock, 0, stream_of(L)>>>(mv, op, L.N, in, L.ld_in);
+      k_tiled<V, Op><<<grid, kBlock, 0, stream_of(L)>>>(mv, op, L.N, in, L.ld_in, aligned);
       return (int)cudaGetLastError();
     }
   }

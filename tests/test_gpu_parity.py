@@ -422,3 +422,33 @@ def test_host_batch_api(vd, cuda, omodels):
     got = vd.batch_forward_dynamics(m, b2)
     cosb = np.abs(np.cos(q[:, 4]))
     assert rel_err(got, qdd, axis=1)[cosb > 0.05].max() <= 1e-8
+
+
+def test_results_independent_of_batch_position(vd, cuda, omodels):
+    """Every instance is computed by the same instruction stream whatever N,
+    ld or pointer alignment (TMA tiles, tail tile, plain-staged tiles): shards
+    of a batch concatenate bit-identically (batch.hpp:77-81 determinism)."""
+    om = omodels["chain7"]
+    m, dm = _dm(vd, "chain7")
+    N = 4099
+    q, qd, _, tau = _states(om, N, 91)
+    full = vd.forward_dynamics(dm, _t(q), _t(qd), _t(tau))
+    pieces = []
+    for lo, hi in ((0, 1), (1, 2050), (2050, 2051), (2051, 4099)):
+        pieces.append(vd.forward_dynamics(dm, _t(q[lo:hi]), _t(qd[lo:hi]), _t(tau[lo:hi])))
+    assert torch.equal(torch.cat(pieces), full)
+    # misaligned planes (odd ld through the raw C-ABI) use the plain-staged path
+    lib = vd._lib.load()
+    ld = N + 1
+    pad = lambda a: torch.nn.functional.pad(_t(a).t().contiguous(), (0, 1))  # noqa: E731
+    Q, QD, TA = pad(q), pad(qd), pad(tau)
+    out = torch.zeros((7, ld), dtype=torch.float64, device="cuda")
+    rc = lib.vd_aba(dm.handle, 0, N, Q.data_ptr(), QD.data_ptr(), TA.data_ptr(), ld, None, None, out.data_ptr(), ld,
+                    None, None)
+    torch.cuda.synchronize()
+    assert rc == 0
+    assert torch.equal(out[:, :N].t(), full)
+    # same for RNEA
+    full_r = vd.rnea(dm, _t(q), _t(qd), _t(tau))
+    part_r = torch.cat([vd.rnea(dm, _t(q[a:b]), _t(qd[a:b]), _t(tau[a:b])) for a, b in ((0, 77), (77, 4099))])
+    assert torch.equal(part_r, full_r)
