@@ -147,6 +147,56 @@ __device__ __forceinline__ void crba_one(const V& mv, const JM<typename V::S>* j
   }
 }
 
+// ------------------------------------------------------------------ plain storage
+// Per-joint values that are always runtime numbers are stored without the sp
+// flag: when such an array spills to local memory under a compile-time view,
+// a stored flag would become a runtime value and every select built on it
+// would survive to SASS.  Loading rebuilds a "non-zero" sp.
+template <class S>
+struct PV {  // plain spatial vector
+  decltype(S::v) a[3], l[3];
+  __device__ __forceinline__ void set(const SV<S>& x) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      a[k] = x.a[k].v;
+      l[k] = x.l[k].v;
+    }
+  }
+  __device__ __forceinline__ SV<S> get() const {
+    SV<S> x;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      x.a[k] = S(a[k]);
+      x.l[k] = S(l[k]);
+    }
+    return x;
+  }
+};
+template <class S>
+struct PI {  // plain articulated inertia
+  decltype(S::v) A[6], B[9], C[6];
+  __device__ __forceinline__ void set(const AI<S>& x) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      A[k] = x.A[k].v;
+      C[k] = x.C[k].v;
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) B[k] = x.B[k].v;
+  }
+  __device__ __forceinline__ AI<S> get() const {
+    AI<S> x;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      x.A[k] = S(A[k]);
+      x.C[k] = S(C[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) x.B[k] = S(B[k]);
+    return x;
+  }
+};
+
 // ------------------------------------------------------------------ ABA
 // Articulated-body forward dynamics (Featherstone RBDA Table 7.1).  Not in the
 // reference; its oracle is forward_dynamics (dynamics.hpp:421-444,
@@ -170,8 +220,8 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
   using S = typename V::S;
   using T = typename V::Real;
   constexpr int NM = V::kMax;
-  SV<S> U[NM], vkeep[NM];
-  S u[NM], dinv[NM];
+  PV<S> U[NM], vkeep[NM];
+  T u[NM], dinv[NM];
   SV<S> fl[kFext ? NM : 1];
   WX<S> W[kFext ? NM : 1];
   bool ok = true;
@@ -190,12 +240,12 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
       const JAxis<V> ax(mv, i);
       SV<S> v;
       if (p >= 0) {
-        v = x.motion_to_child(p == i - 1 ? vprev : vkeep[p]);
+        v = x.motion_to_child(p == i - 1 ? vprev : vkeep[p].get());
         ax.add(v, S(qd[i]));
       } else {
         v = ax.scaled(S(qd[i]));
       }
-      if (mv.flags(i) & (kFlagLeaf | kFlagBranch)) vkeep[i] = v;
+      if (mv.flags(i) & (kFlagLeaf | kFlagBranch)) vkeep[i].set(v);
       vprev = v;
       if constexpr (kFext) {
         W[i] = world_of(x, p < 0 ? nullptr : &W[p]);
@@ -211,15 +261,17 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
   }
   // pass 2: articulated inertias leaf -> root
   {
-    AI<S> carryI, slotI[NM];
-    SV<S> carryP = zero, slotP[NM], vrec = zero;
+    AI<S> carryI;
+    PI<S> slotI[NM];
+    SV<S> carryP = zero, vrec = zero;
+    PV<S> slotP[NM];
     uint64_t used = 0;
     int carry_to = -1;
 #pragma unroll
     for (int i = mv.n() - 1; i >= 0; --i) {
       const JAxis<V> ax(mv, i);
       const S qdi = S(qd[i]);
-      const SV<S> v = (mv.flags(i) & kFlagLeaf) ? vkeep[i] : vrec;
+      const SV<S> v = (mv.flags(i) & kFlagLeaf) ? vkeep[i].get() : vrec;
       AI<S> IA;
       SV<S> pA;
       if (mv.oflags(i) & kMassless) {
@@ -239,22 +291,25 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
         pA = pA + carryP;
       }
       if ((used >> i) & 1ull) {
-        ai_add(IA, slotI[i]);
-        pA = pA + slotP[i];
+        ai_add(IA, slotI[i].get());
+        pA = pA + slotP[i].get();
       }
-      U[i] = ai_axis(ax, IA);
-      const S D = ax.dot(U[i]);
+      const SV<S> Ui = ai_axis(ax, IA);
+      U[i].set(Ui);
+      const S D = ax.dot(Ui);
       ok = ok && (D.v > T(0));
-      dinv[i] = S(T(1) / D.v);
-      u[i] = S(tau[i]) - ax.dot(pA);
+      const S di = S(T(1) / D.v);
+      const S ui = S(tau[i]) - ax.dot(pA);
+      dinv[i] = di.v;
+      u[i] = ui.v;
       const int p = mv.parent(i);
       if (p >= 0) {
         JointX<V> x;
         x.load(mv, i, jm[i]);
         const SV<S> c = ax.crm(v, qdi);
         AI<S> Ia = IA;
-        ai_sub_outer(Ia, U[i], dinv[i]);
-        const SV<S> pa = pA + ai_apply(Ia, c) + scale(U[i], u[i] * dinv[i]);
+        ai_sub_outer(Ia, Ui, di);
+        const SV<S> pa = pA + ai_apply(Ia, c) + scale(Ui, ui * di);
         const AI<S> IAp = ai_to_parent(x, Ia);
         const SV<S> pAp = x.force_to_parent(pa);
         if (p == i - 1) {
@@ -265,11 +320,13 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
           ax.add(vmj, -qdi);
           vrec = x.motion_to_parent(vmj);  // v_{i-1}
         } else if ((used >> p) & 1ull) {
-          ai_add(slotI[p], IAp);
-          slotP[p] = slotP[p] + pAp;
+          AI<S> acc = slotI[p].get();
+          ai_add(acc, IAp);
+          slotI[p].set(acc);
+          slotP[p].set(slotP[p].get() + pAp);
         } else {
-          slotI[p] = IAp;
-          slotP[p] = pAp;
+          slotI[p].set(IAp);
+          slotP[p].set(pAp);
           used |= 1ull << p;
         }
       }
@@ -278,7 +335,8 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
   // pass 3: accelerations root -> leaf
   {
     const SV<S> ag = gravity_accel<V>(g3);
-    SV<S> aprev = zero, vprev = zero, akeep[NM];
+    SV<S> aprev = zero, vprev = zero;
+    PV<S> akeep[NM];
 #pragma unroll
     for (int i = 0; i < mv.n(); ++i) {
       JointX<V> x;
@@ -292,15 +350,15 @@ __device__ __forceinline__ bool aba_one(const V& mv, const JM<typename V::S>* jm
         ap = x.motion_to_child(ag);
       } else {
         const bool adj = p == i - 1;
-        v = x.motion_to_child(adj ? vprev : vkeep[p]);
+        v = x.motion_to_child(adj ? vprev : vkeep[p].get());
         ax.add(v, qdi);
-        ap = x.motion_to_child(adj ? aprev : akeep[p]) + ax.crm(v, qdi);
+        ap = x.motion_to_child(adj ? aprev : akeep[p].get()) + ax.crm(v, qdi);
       }
-      qdd[i] = (u[i] - sdot(U[i], ap)) * dinv[i];
+      qdd[i] = (S(u[i]) - sdot(U[i].get(), ap)) * S(dinv[i]);
       ok = ok && isfinite(qdd[i].v);
       SV<S> a = ap;
       ax.add(a, qdd[i]);
-      if (mv.flags(i) & kFlagBranch) akeep[i] = a;
+      if (mv.flags(i) & kFlagBranch) akeep[i].set(a);
       aprev = a;
       vprev = v;
     }
