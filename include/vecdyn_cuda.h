@@ -174,6 +174,23 @@ int vd_osc(vd_device_model dm, int dtype, int64_t N, const void* q, const void* 
            const vd_osc_params* params, void* tau_out, void* Lambda_out, int64_t ld_out, int32_t* status_out,
            void* stream);
 
+/* diff_ik_step, control.hpp:79-97: q̇ = Jᵀ (J Jᵀ + λ² I)⁻¹ (kp ⊙ err + twist_ff).
+ * damping must be > 0 and gains nonnegative (control.hpp:82-86, 32-36). */
+typedef struct vd_task_params {
+  int frame;           /* vd_model_frame_index */
+  double target[12];   /* TaskTarget::pose, R column-major + p */
+  double kp[6];        /* TaskGains::kp (angular first) */
+  double twist_ff[6];  /* TaskTarget::twist_ff */
+  double damping;      /* λ */
+} vd_task_params;
+/* qdot_out n planes; err_out (6 planes, pose_error, control.hpp:73-77) may be NULL. */
+int vd_diff_ik(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, const vd_task_params* params,
+               void* qdot_out, void* err_out, int64_t ld_out, int32_t* status_out, void* stream);
+/* manipulability(geometric_jacobian(frame)), kinematics.hpp:138-153: one plane,
+ * sqrt(det(J Jᵀ)) as a Cholesky pivot product, 0 where the factorization fails. */
+int vd_manipulability(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, int frame,
+                      void* w_out, void* stream);
+
 /* ------------------------------------------------------------------ host batch (drop-in for batch.hpp)
  * batch_rnea / batch_crba / batch_forward_dynamics (batch.hpp:128-165) with
  * HOST column-major N x n inputs and N x K outputs, fp64.  `workers` becomes a

@@ -345,6 +345,62 @@ int orc_batch_osc(void* h, int64_t N, const double* q, const double* qd, const c
   }
 }
 
+// diff_ik_step per instance (control.hpp:79-97); err (6 planes, may be NULL) = pose_error.
+int orc_batch_diffik(void* h, int64_t N, const double* q, const char* frame, const double* target12,
+                     const double* kp, const double* twist_ff, double damping, double* qdot, double* err,
+                     int threads) {
+  try {
+    const Model& m = M(h);
+    const int n = m.dof();
+    TaskTarget t;
+    t.frame = frame;
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) t.pose.R(r, c) = target12[r * 3 + c];
+      t.pose.p[r] = target12[9 + r];
+    }
+    for (int k = 0; k < 6; ++k) {
+      t.gains.kp[k] = kp[k];
+      t.twist_ff.at(k) = twist_ff ? twist_ff[k] : 0.0;
+    }
+    (void)m.frame(frame);
+    (void)diff_ik_step(m, std::vector<double>((size_t)n, 0.0), t, damping);  // argument checks up front
+    batch_eval((int)N,
+               [&](int i) {
+                 const auto a = plane_row<double>(q, N, n, i);
+                 const std::vector<double> v = diff_ik_step(m, a, t, damping);
+                 for (int j = 0; j < n; ++j) qdot[j * N + i] = v[(size_t)j];
+                 if (err) {
+                   const Frames<double> w = forward_kinematics(m, a);
+                   const Motion<double> e = pose_error(t.pose, frame_transform(m, w, t.frame));
+                   for (int k = 0; k < 6; ++k) err[k * N + i] = e[k];
+                 }
+               },
+               threads);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// manipulability(geometric_jacobian(frame)) per instance (kinematics.hpp:138-153).
+int orc_batch_manip(void* h, int64_t N, const double* q, const char* frame, double* w_out, int threads) {
+  try {
+    const Model& m = M(h);
+    const int n = m.dof();
+    (void)m.frame(frame);
+    const std::string f = frame;
+    batch_eval((int)N,
+               [&](int i) {
+                 const Frames<double> w = forward_kinematics(m, plane_row<double>(q, N, n, i));
+                 w_out[i] = manipulability(geometric_jacobian(m, w, f));
+               },
+               threads);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // Frozen algorithmic op counts per evaluation (orc_count.hpp).  algo:
 // 0 rnea_loop, 1 crba_loop, 2 aba_loop, 3 forward_kinematics, 4 rnea (mask
 // form), 5 forward_dynamics (CRBA + bias + LLT), 6 crba (mask form).

@@ -34,7 +34,7 @@ __all__ = [
     "UnsupportedStructureError", "SingularInertiaError", "CudaError", "RobotModel", "DeviceModel", "GravitySpec",
     "TaskGains", "TaskTarget", "PostureGains", "StateBatch", "robots", "urdf", "floating_base", "random_states",
     "rnea", "bias_forces", "gravity_vector", "coriolis_vector", "crba", "forward_dynamics", "dynamics",
-    "forward_kinematics", "forward_kinematics_scan", "frame_transform", "geometric_jacobian", "osc_step", "batch_rnea", "batch_crba",
+    "forward_kinematics", "forward_kinematics_scan", "frame_transform", "geometric_jacobian", "manipulability", "diff_ik_step", "osc_step", "batch_rnea", "batch_crba",
     "batch_forward_dynamics", "shard_range",
 ]
 
@@ -517,6 +517,40 @@ def geometric_jacobian(dm, q, frame):
     _check(_lib.load().vd_jacobian(dm.handle, _dtype_code(qs), N, _p(qs), N, _frame_id(dm, frame), None, _p(out), N,
                                    _stream(dev)))
     return out.t().reshape(N, n, 6).transpose(1, 2)
+
+
+def manipulability(dm, q, frame):
+    """manipulability(geometric_jacobian(frame)) (kinematics.hpp:138-153): (N,),
+    0 at singular configurations."""
+    qs, _, N, dev = _prep(dm, q)
+    out = _out(dev, qs.dtype, 1, N)
+    _check(_lib.load().vd_manipulability(dm.handle, _dtype_code(qs), N, _p(qs), N, _frame_id(dm, frame), _p(out),
+                                         _stream(dev)))
+    return out.reshape(N)
+
+
+def diff_ik_step(dm, q, target, damping, return_error=False):
+    """diff_ik_step (control.hpp:79-97) for a batch sharing one target: (N, n) q̇;
+    with return_error also the (N, 6) pose error."""
+    qs, _, N, dev = _prep(dm, q)
+    n = dm.dof()
+    P = _lib.TaskParams()
+    P.frame = _frame_id(dm, target.frame)
+    R, p = target.pose
+    for c in range(3):
+        for r in range(3):
+            P.target[c * 3 + r] = float(R[r][c])
+    for k in range(3):
+        P.target[9 + k] = float(p[k])
+    for k in range(6):
+        P.kp[k] = target.gains.kp[k]
+        P.twist_ff[k] = target.twist_ff[k]
+    P.damping = float(damping)
+    qdot = _out(dev, qs.dtype, n, N)
+    err = _out(dev, qs.dtype, 6, N) if return_error else None
+    _check(_lib.load().vd_diff_ik(dm.handle, _dtype_code(qs), N, _p(qs), N, ctypes.byref(P), _p(qdot), _p(err), N,
+                                  None, _stream(dev)))
+    return (qdot.t(), err.t()) if return_error else qdot.t()
 
 
 def osc_step(dm, q, qd, target, posture, posture_gains, gravity=None, epsilon=1e-6, return_lambda=False,

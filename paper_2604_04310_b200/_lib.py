@@ -38,6 +38,11 @@ class OscParams(ctypes.Structure):
                 ("gravity", c_double * 3), ("epsilon", c_double)]
 
 
+class TaskParams(ctypes.Structure):
+    _fields_ = [("frame", c_int), ("target", c_double * 12), ("kp", c_double * 6), ("twist_ff", c_double * 6),
+                ("damping", c_double)]
+
+
 # name -> (restype, argtypes); mirrors include/vecdyn_cuda.h one for one.
 SIGNATURES = {
     "vd_last_error": (c_char_p, []),
@@ -81,6 +86,8 @@ SIGNATURES = {
     "vd_aba": (c_int, [P, c_int, c_int64, P, P, P, c_int64, Pd, P, P, c_int64, P, P]),
     "vd_dynamics": (c_int, [P, c_int, c_int64, P, P, P, c_int64, Pd, P, P, P, c_int64, P, P]),
     "vd_osc": (c_int, [P, c_int, c_int64, P, P, c_int64, ctypes.POINTER(OscParams), P, P, c_int64, P, P]),
+    "vd_diff_ik": (c_int, [P, c_int, c_int64, P, c_int64, ctypes.POINTER(TaskParams), P, P, c_int64, P, P]),
+    "vd_manipulability": (c_int, [P, c_int, c_int64, P, c_int64, c_int, P, P]),
     "vd_batch_rnea_host": (c_int, [P, c_int64, P, P, P, Pd, P, Pi, c_int]),
     "vd_batch_crba_host": (c_int, [P, c_int64, P, P, Pi, c_int]),
     "vd_batch_forward_dynamics_host": (c_int, [P, c_int64, P, P, P, Pd, P, P, Pi, c_int]),

@@ -462,6 +462,53 @@ int vd_osc(vd_device_model dm, int dtype, int64_t N, const void* q, const void* 
                 "vd_osc");
 }
 
+namespace {
+void task_frame(const vd_device_model dm, int f, vdk::TaskShared& S) {
+  std::memset(&S, 0, sizeof S);
+  S.frame_joint = dm->pm.frame_joint[f];
+  for (int k = 0; k < 9; ++k) S.frame_R[k] = dm->pm.frame_R[f][k];
+  for (int k = 0; k < 3; ++k) S.frame_p[k] = dm->pm.frame_p[f][k];
+}
+}  // namespace
+
+int vd_diff_ik(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, const vd_task_params* P,
+               void* qdot, void* err, int64_t ld_out, int32_t* status, void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  if (!P) return set_error(VD_ERR_INVALID_ARGUMENT, "null task parameters");
+  if (!(P->damping > 0.0)) return set_error(VD_ERR_GENERIC, "diff_ik_step: damping must be positive");
+  for (int k = 0; k < 6; ++k)
+    if (P->kp[k] < 0.0) return set_error(VD_ERR_GENERIC, "task gains must be nonnegative");
+  if (P->frame < 0 || P->frame >= dm->pm.nframes) return set_error(VD_ERR_UNKNOWN_FRAME, "frame index out of range");
+  VD_NEED(q, "q");
+  VD_NEED(qdot, "qdot");
+  vdk::TaskShared S;
+  task_frame(dm, P->frame, S);
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) S.target_R[r * 3 + c] = P->target[c * 3 + r];
+  for (int k = 0; k < 3; ++k) S.target_p[k] = P->target[9 + k];
+  for (int k = 0; k < 6; ++k) {
+    S.kp[k] = P->kp[k];
+    S.twist_ff[k] = P->twist_ff[k];
+  }
+  S.damping = P->damping;
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_task(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, S, 0, qdot, err, status),
+                "vd_diff_ik");
+}
+
+int vd_manipulability(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, int frame, void* w,
+                      void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_in)) return rc;
+  if (frame < 0 || frame >= dm->pm.nframes) return set_error(VD_ERR_UNKNOWN_FRAME, "frame index out of range");
+  VD_NEED(q, "q");
+  VD_NEED(w, "w");
+  vdk::TaskShared S;
+  task_frame(dm, frame, S);
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_task(make_launch(dm, dtype, N, ld_in, ld_in, stream), q, S, 1, w, nullptr, nullptr),
+                "vd_manipulability");
+}
+
 // ---- internal (not in the public header): packed tables for the robot-table generator
 uint64_t vdi_model_fingerprint(vd_model m) { return m ? vdh::fingerprint(vdh::pack(m->m)) : 0; }
 int vdi_model_packed(vd_model m, int* n, int* parent, int* kind, int* axis_code, double* axis, double* R, double* p,

@@ -405,6 +405,85 @@ __device__ __forceinline__ void rotation_log(const T* R, T* w) {
   for (int k = 0; k < 3; ++k) w[k] = f * anti[k];
 }
 
+// frame_transform + geometric_jacobian (kinematics.hpp:89-129) of frame
+// (joint fj, offset R_f/p_f): world pose of the frame and the 6 x n Jacobian
+// (angular rows first; exact zeros off the ancestor path).
+template <class V>
+__device__ __forceinline__ void frame_pose_jacobian(const V& mv, const JM<typename V::S>* jm, int fj,
+                                                    const double* frame_R, const double* frame_p,
+                                                    typename V::Real* pose_R, typename V::Real* pose_p,
+                                                    typename V::Real (*J)[V::kMax]) {
+  using S = typename V::S;
+  using T = typename V::Real;
+  WX<S> W[V::kMax];
+  fk_world(mv, jm, W);
+  T WR[9], Wp[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) WR[k] = (k % 4 == 0) ? T(1) : T(0);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) Wp[k] = T(0);
+  if (fj >= 0) {
+#pragma unroll
+    for (int i = 0; i < mv.n(); ++i)
+      if (i == fj) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) WR[k] = W[i].R[k].v;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) Wp[k] = W[i].p[k].v;
+      }
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      pose_R[r * 3 + c] =
+          WR[r * 3] * T(frame_R[c]) + WR[r * 3 + 1] * T(frame_R[3 + c]) + WR[r * 3 + 2] * T(frame_R[6 + c]);
+    pose_p[r] = WR[r * 3] * T(frame_p[0]) + WR[r * 3 + 1] * T(frame_p[1]) + WR[r * 3 + 2] * T(frame_p[2]) + Wp[r];
+  }
+  const uint64_t fmask = fj >= 0 ? mv.anc(fj) : 0ull;
+#pragma unroll
+  for (int j = 0; j < mv.n(); ++j) {
+    const bool on = (fmask >> j) & 1ull;
+    T ax[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+      ax[r] = (W[j].R[r * 3] * mv.axis(j, 0) + W[j].R[r * 3 + 1] * mv.axis(j, 1) + W[j].R[r * 3 + 2] * mv.axis(j, 2)).v;
+    if (!on) {
+#pragma unroll
+      for (int r = 0; r < 6; ++r) J[r][j] = T(0);
+    } else if (mv.kind(j) == 0) {
+      const T d[3] = {pose_p[0] - W[j].p[0].v, pose_p[1] - W[j].p[1].v, pose_p[2] - W[j].p[2].v};
+      J[0][j] = ax[0];
+      J[1][j] = ax[1];
+      J[2][j] = ax[2];
+      J[3][j] = ax[1] * d[2] - ax[2] * d[1];
+      J[4][j] = ax[2] * d[0] - ax[0] * d[2];
+      J[5][j] = ax[0] * d[1] - ax[1] * d[0];
+    } else {
+      J[0][j] = J[1][j] = J[2][j] = T(0);
+      J[3][j] = ax[0];
+      J[4][j] = ax[1];
+      J[5][j] = ax[2];
+    }
+  }
+}
+
+// pose_error (control.hpp:73-77): (log(R_t R_cᵀ), p_t − p_c); target R row-major.
+template <class T>
+__device__ __forceinline__ void pose_error(const double* target_R, const double* target_p, const T* pose_R,
+                                           const T* pose_p, T* err) {
+  T Rrel[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      Rrel[r * 3 + c] = T(target_R[r * 3]) * pose_R[c * 3] + T(target_R[r * 3 + 1]) * pose_R[c * 3 + 1] +
+                        T(target_R[r * 3 + 2]) * pose_R[c * 3 + 2];
+  rotation_log(Rrel, err);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) err[3 + k] = T(target_p[k]) - pose_p[k];
+}
+
 // In-place Cholesky of a 6x6 SPD (lower, row-major), Eigen's LLT criterion.
 template <class T>
 __device__ __forceinline__ bool chol6(T* L) {
@@ -446,7 +525,67 @@ __device__ __forceinline__ void chol6_solve(const T* L, T* b) {
   }
 }
 
+// G = J Jᵀ + d·I, lower triangle, row-major 6x6.
+template <class T, int NM>
+__device__ __forceinline__ void gram6(int n, const T (*J)[NM], T d, T* G) {
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) {
+      T s = r == c ? d : T(0);
+#pragma unroll
+      for (int k = 0; k < n; ++k) s += J[r][k] * J[c][k];
+      G[r * 6 + c] = s;
+    }
+}
 
+// diff_ik_step (control.hpp:79-97): q̇ = Jᵀ (J Jᵀ + λ² I)⁻¹ (kp ⊙ err + twist_ff).
+// Returns false when the damped Gram matrix does not factor (non-finite input).
+template <class V>
+__device__ __forceinline__ bool diffik_one(const V& mv, const JM<typename V::S>* jm, const TaskShared& P,
+                                           typename V::Real* qdot, typename V::Real* err_out) {
+  using T = typename V::Real;
+  constexpr int NM = V::kMax;
+  T pose_R[9], pose_p[3], J[6][NM];
+  frame_pose_jacobian(mv, jm, P.frame_joint, P.frame_R, P.frame_p, pose_R, pose_p, J);
+  T err[6];
+  pose_error(P.target_R, P.target_p, pose_R, pose_p, err);
+  T rhs[6], G[36];
+#pragma unroll
+  for (int r = 0; r < 6; ++r) rhs[r] = T(P.kp[r]) * err[r] + T(P.twist_ff[r]);
+  gram6(mv.n(), J, T(P.damping) * T(P.damping), G);
+  const bool ok = chol6(G);
+  chol6_solve(G, rhs);
+#pragma unroll
+  for (int j = 0; j < mv.n(); ++j) {
+    T s = T(0);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) s += J[r][j] * rhs[r];
+    qdot[j] = s;
+  }
+  if (err_out) {
+#pragma unroll
+    for (int r = 0; r < 6; ++r) err_out[r] = err[r];
+  }
+  return ok;
+}
+
+// manipulability (kinematics.hpp:138-153): sqrt(det(J Jᵀ)) as the pivot
+// product of the Cholesky factor; 0 when the factorization fails.
+template <class V>
+__device__ __forceinline__ typename V::Real manip_one(const V& mv, const JM<typename V::S>* jm, const TaskShared& P) {
+  using T = typename V::Real;
+  constexpr int NM = V::kMax;
+  T pose_R[9], pose_p[3], J[6][NM];
+  frame_pose_jacobian(mv, jm, P.frame_joint, P.frame_R, P.frame_p, pose_R, pose_p, J);
+  T G[36];
+  gram6(mv.n(), J, T(0), G);
+  if (!chol6(G)) return T(0);
+  T d = T(1);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) d = d * G[i * 6 + i];
+  return d;
+}
 
 // osc_step (control.hpp:108-155).  The mass matrix is factorised with the
 // branch-sparse LTL of RBDA §6.5 (M = Lᵀ L, L with the ancestor sparsity of
@@ -473,77 +612,11 @@ __device__ __forceinline__ bool osc_one(const V& mv, const JM<typename V::S>* jm
     rnea_one<V, false, QA, QA>(mv, jm, qd, static_cast<const QA*>(nullptr), g3, nullptr, bias);
   }
   // --- frame pose and Jacobian (kinematics.hpp:89-129)
-  WX<S> W[NM];
-  fk_world(mv, jm, W);
-  const int fj = P.frame_joint;
-  T pose_R[9], pose_p[3];
-  {
-    T WR[9], Wp[3];
-    if (fj >= 0) {
-#pragma unroll
-      for (int i = 0; i < mv.n(); ++i)
-        if (i == fj) {
-#pragma unroll
-          for (int k = 0; k < 9; ++k) WR[k] = W[i].R[k].v;
-#pragma unroll
-          for (int k = 0; k < 3; ++k) Wp[k] = W[i].p[k].v;
-        }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 9; ++k) WR[k] = (k % 4 == 0) ? T(1) : T(0);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) Wp[k] = T(0);
-    }
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-        pose_R[r * 3 + c] = WR[r * 3] * T(P.frame_R[c]) + WR[r * 3 + 1] * T(P.frame_R[3 + c]) +
-                            WR[r * 3 + 2] * T(P.frame_R[6 + c]);
-      pose_p[r] = WR[r * 3] * T(P.frame_p[0]) + WR[r * 3 + 1] * T(P.frame_p[1]) + WR[r * 3 + 2] * T(P.frame_p[2]) + Wp[r];
-    }
-  }
-  const uint64_t fmask = fj >= 0 ? mv.anc(fj) : 0ull;
-  T J[6][NM];
-#pragma unroll
-  for (int j = 0; j < mv.n(); ++j) {
-    const bool on = (fmask >> j) & 1ull;
-    T ax[3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-      ax[r] = (W[j].R[r * 3] * mv.axis(j, 0) + W[j].R[r * 3 + 1] * mv.axis(j, 1) + W[j].R[r * 3 + 2] * mv.axis(j, 2)).v;
-    if (!on) {
-#pragma unroll
-      for (int r = 0; r < 6; ++r) J[r][j] = T(0);
-    } else if (mv.kind(j) == 0) {
-      const T d[3] = {pose_p[0] - W[j].p[0].v, pose_p[1] - W[j].p[1].v, pose_p[2] - W[j].p[2].v};
-      J[0][j] = ax[0];
-      J[1][j] = ax[1];
-      J[2][j] = ax[2];
-      J[3][j] = ax[1] * d[2] - ax[2] * d[1];
-      J[4][j] = ax[2] * d[0] - ax[0] * d[2];
-      J[5][j] = ax[0] * d[1] - ax[1] * d[0];
-    } else {
-      J[0][j] = J[1][j] = J[2][j] = T(0);
-      J[3][j] = ax[0];
-      J[4][j] = ax[1];
-      J[5][j] = ax[2];
-    }
-  }
+  T pose_R[9], pose_p[3], J[6][NM];
+  frame_pose_jacobian(mv, jm, P.frame_joint, P.frame_R, P.frame_p, pose_R, pose_p, J);
   // --- pose error (control.hpp:73-77): log(R_t R_cᵀ), p_t − p_c
   T err[6];
-  {
-    T Rrel[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-        Rrel[r * 3 + c] = T(P.target_R[r * 3]) * pose_R[c * 3] + T(P.target_R[r * 3 + 1]) * pose_R[c * 3 + 1] +
-                          T(P.target_R[r * 3 + 2]) * pose_R[c * 3 + 2];
-    rotation_log(Rrel, err);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) err[3 + k] = T(P.target_p[k]) - pose_p[k];
-  }
+  pose_error(P.target_R, P.target_p, pose_R, pose_p, err);
   // --- LTL factorisation in place (RBDA Table 6.3)
 #pragma unroll
   for (int k = mv.n() - 1; k >= 0; --k) {

@@ -79,6 +79,12 @@ int launch_osc(const Launch& L, const void* q, const void* qd, const OscShared& 
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::osc(mv, L, q, qd, P, tau, lambda, status); });
 }
 
+int launch_task(const Launch& L, const void* q, const TaskShared& P, int mode, void* out, void* aux,
+                int32_t* status) {
+  if (L.N == 0) return 0;
+  return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::task(mv, L, q, P, mode, out, aux, status); });
+}
+
 }  // namespace vdk
 
 // ---------------------------------------------------------------- forward_kinematics_scan

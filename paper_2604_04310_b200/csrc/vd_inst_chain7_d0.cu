@@ -5,4 +5,5 @@ namespace vdk {
 template int Launcher<Chain7D>::fk(const Chain7D&, const Launch&, const void*, void*);
 template int Launcher<Chain7D>::jac(const Chain7D&, const Launch&, const void*, const FrameArg&, void*, void*);
 template int Launcher<Chain7D>::crba(const Chain7D&, const Launch&, const void*, void*);
+template int Launcher<Chain7D>::task(const Chain7D&, const Launch&, const void*, const TaskShared&, int, void*, void*, int32_t*);
 }  // namespace vdk

@@ -5,4 +5,5 @@ namespace vdk {
 template int Launcher<Chain7F>::fk(const Chain7F&, const Launch&, const void*, void*);
 template int Launcher<Chain7F>::jac(const Chain7F&, const Launch&, const void*, const FrameArg&, void*, void*);
 template int Launcher<Chain7F>::crba(const Chain7F&, const Launch&, const void*, void*);
+template int Launcher<Chain7F>::task(const Chain7F&, const Launch&, const void*, const TaskShared&, int, void*, void*, int32_t*);
 }  // namespace vdk

@@ -302,6 +302,39 @@ __global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_osc(const __grid_cons
   osc_body(mv, cols(q, ldi, i), cols(qd, ldi, i), i, P, tau, lam, ldo, status);
 }
 
+// ---------------------------------------------------------------- task-space kinematics
+// mode 0: diff_ik_step → out = q̇ (n rows), aux = pose error (6 rows, optional)
+// mode 1: manipulability → out = w (1 row)
+template <class V>
+__global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_task(const __grid_constant__ V mv, int64_t N,
+                                                                const typename V::Real* __restrict__ q, int64_t ldi,
+                                                                const __grid_constant__ TaskShared P, int mode,
+                                                                typename V::Real* __restrict__ out,
+                                                                typename V::Real* __restrict__ aux, int64_t ldo,
+                                                                int32_t* __restrict__ status) {
+  using T = typename V::Real;
+  using S = typename V::S;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  JM<S> jm[V::kMax];
+  load_motion(mv, cols(q, ldi, i), jm);
+  if (mode == 0) {
+    T qd[V::kMax], err[6];
+    const bool ok = diffik_one(mv, jm, P, qd, aux ? err : nullptr);
+    OutCols<T> o{out, ldo, i};
+#pragma unroll
+    for (int j = 0; j < mv.n(); ++j) o.put(j, ok ? qd[j] : T(0));
+    if (aux) {
+      OutCols<T> oe{aux, ldo, i};
+#pragma unroll
+      for (int r = 0; r < 6; ++r) oe.put(r, err[r]);
+    }
+    if (status) status[i] = ok ? 0 : 7;
+  } else {
+    out[i] = manip_one(mv, jm, P);
+  }
+}
+
 // ---------------------------------------------------------------- TMA-staged persistent driver (static views)
 // Same math as the plain kernels; inputs arrive through the two-stage
 // bulk-copy pipeline of vd_tma.cuh.  Requires 16-byte aligned planes (checked
@@ -505,6 +538,8 @@ struct Launcher {
                  void* bias, void* qdd, int32_t* status);
   static int osc(const V& mv, const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau,
                  void* lambda, int32_t* status);
+  static int task(const V& mv, const Launch& L, const void* q, const TaskShared& P, int mode, void* out, void* aux,
+                  int32_t* status);
 };
 
 using GenericD = RuntimeView<double>;

@@ -20,6 +20,7 @@ struct Launch {
 };
 
 struct OscShared;
+struct TaskShared;
 
 // Compile-time robot whose packed-model fingerprint matches (0 = none).
 int match_spec(uint64_t fingerprint, int n);
@@ -40,5 +41,8 @@ int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* 
                     void* bias, void* qdd, int32_t* status);
 int launch_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
                int32_t* status);
+// mode 0: diff_ik_step (out = q̇, aux = pose error); mode 1: manipulability (out = w)
+int launch_task(const Launch& L, const void* q, const TaskShared& P, int mode, void* out, void* aux,
+                int32_t* status);
 
 }  // namespace vdk

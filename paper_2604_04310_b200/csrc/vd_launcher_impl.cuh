@@ -133,4 +133,13 @@ int Launcher<V>::osc(const V& mv, const Launch& L, const void* q, const void* qd
   return (int)cudaGetLastError();
 }
 
+template <class V>
+int Launcher<V>::task(const V& mv, const Launch& L, const void* q, const TaskShared& P, int mode, void* out, void* aux,
+                      int32_t* status) {
+  using T = typename V::Real;
+  k_task<V><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, L.ld_in, P, mode, (T*)out, (T*)aux,
+                                                         L.ld_out, status);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace vdk

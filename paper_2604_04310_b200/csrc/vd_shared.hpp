@@ -42,4 +42,14 @@ struct OscShared {
   double epsilon;
 };
 
+// Per-launch task constants for diff_ik_step / manipulability
+// (vd_task_params, control.hpp:25-37, 79-97; kinematics.hpp:138-153).
+struct TaskShared {
+  int frame_joint;
+  double frame_R[9], frame_p[3];    // frame offset, row-major R
+  double target_R[9], target_p[3];  // row-major
+  double kp[6], twist_ff[6];
+  double damping;
+};
+
 }  // namespace vdk

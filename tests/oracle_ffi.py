@@ -55,6 +55,8 @@ def lib():
         L.orc_batch_fk.argtypes = [vp, i64, vp, vp, ci, ci]
         L.orc_batch_jacobian.argtypes = [vp, i64, vp, cc, vp, vp, ci]
         L.orc_batch_osc.argtypes = [vp, i64, vp, vp, cc, vp, vp, vp, vp, vp, cd, cd, vp, cd, vp, vp, vp, ci]
+        L.orc_batch_diffik.argtypes = [vp, i64, vp, cc, vp, vp, vp, cd, vp, vp, ci]
+        L.orc_batch_manip.argtypes = [vp, i64, vp, cc, vp, ci]
         _lib = L
     return _lib
 
@@ -208,6 +210,23 @@ class Model:
         _chk(lib().orc_batch_osc(self.h, N, _ptr(q), _ptr(qd), frame.encode(), _ptr(t12), _ptr(kp), _ptr(kd),
                                  _ptr(ff), _ptr(post), pkp, pkd, _ptr(g), eps, _ptr(tau), _ptr(lam), _ptr(st), threads))
         return tau, lam.reshape(N, 6, 6).transpose(0, 2, 1), st
+
+    def diff_ik(self, q, frame, target_R, target_p, kp, twist_ff, damping, threads=0):
+        q = _F(q)
+        N, n = q.shape[0], self.n
+        t12 = np.concatenate([np.asarray(target_R, dtype=np.float64).reshape(9), np.asarray(target_p, dtype=np.float64)])
+        kp, ff = (np.asarray(x, dtype=np.float64) for x in (kp, twist_ff))
+        qdot = np.empty((N, n), order="F")
+        err = np.empty((N, 6), order="F")
+        _chk(lib().orc_batch_diffik(self.h, N, _ptr(q), frame.encode(), _ptr(t12), _ptr(kp), _ptr(ff), float(damping),
+                                    _ptr(qdot), _ptr(err), threads))
+        return qdot, err
+
+    def manipulability(self, q, frame, threads=0):
+        q = _F(q)
+        w = np.empty(q.shape[0])
+        _chk(lib().orc_batch_manip(self.h, q.shape[0], _ptr(q), frame.encode(), _ptr(w), threads))
+        return w
 
 
 def rel_err(a, b, axis=None):
