@@ -191,6 +191,25 @@ int vd_diff_ik(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t 
 int vd_manipulability(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, int frame,
                       void* w_out, void* stream);
 
+/* ------------------------------------------------------------------ forward-mode JVPs
+ * jvp(fn, x, v) of autodiff.hpp:41-52 applied to the library's own functions
+ * (the reference runs them on the Dual scalar of dual.hpp:14-196): one pass on
+ * dual numbers returns fn(x) and D fn(x)·v.  Tangent inputs (dq, dqd, ...) may
+ * be NULL (zero tangent); value or tangent outputs may be NULL (not both).
+ * Output layouts are those of the primal functions.  fext is a constant
+ * (zero-tangent) input. */
+int vd_fk_jvp(vd_device_model dm, int dtype, int64_t N, const void* q, const void* dq, int64_t ld_in,
+              void* frames_out, void* dframes_out, int64_t ld_out, void* stream);
+int vd_rnea_jvp(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* qdd,
+                const void* dq, const void* dqd, const void* dqdd, int64_t ld_in, const double* gravity3,
+                const void* fext, void* tau_out, void* dtau_out, int64_t ld_out, void* stream);
+int vd_crba_jvp(vd_device_model dm, int dtype, int64_t N, const void* q, const void* dq, int64_t ld_in, void* M_out,
+                void* dM_out, int64_t ld_out, void* stream);
+/* forward dynamics by ABA on duals: q̈ and its directional derivative along (dq, dq̇, dτ). */
+int vd_aba_jvp(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau,
+               const void* dq, const void* dqd, const void* dtau, int64_t ld_in, const double* gravity3,
+               const void* fext, void* qdd_out, void* dqdd_out, int64_t ld_out, int32_t* status_out, void* stream);
+
 /* ------------------------------------------------------------------ host batch (drop-in for batch.hpp)
  * batch_rnea / batch_crba / batch_forward_dynamics (batch.hpp:128-165) with
  * HOST column-major N x n inputs and N x K outputs, fp64.  `workers` becomes a

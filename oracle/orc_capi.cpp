@@ -10,6 +10,7 @@
 
 #include "orc_batch.hpp"
 #include "orc_count.hpp"
+#include "orc_dual.hpp"
 
 using namespace orc;
 
@@ -337,6 +338,66 @@ int orc_batch_osc(void* h, int64_t N, const double* q, const double* qd, const c
                  if (lambda)
                    for (int k = 0; k < 36; ++k) lambda[k * N + i] = r.Lambda[k];
                  if (status) status[i] = st;
+               },
+               threads);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// Forward-mode JVP (autodiff.hpp:41-52: the algorithm run on the Dual scalar
+// of dual.hpp) of op 0 forward_kinematics (all frames, fk layout), 1 rnea,
+// 2 crba, 3 forward dynamics, on inputs seeded with tangents (NULL = 0).
+// variant: 0 the reference's vectorized / LLT path, 1 the loop path
+// (rnea_loop, crba_loop, aba_loop).  out / dout: values / tangents.
+int orc_batch_jvp(void* h, int op, int64_t N, const double* q, const double* qd, const double* x2, const double* dq,
+                  const double* dqd, const double* dx2, const double* g3, const double* fext, double* out,
+                  double* dout, int* status, int threads, int variant) {
+  try {
+    const Model& m = M(h);
+    const int n = m.dof();
+    const Gravity g = grav(g3);
+    auto seed = [&](const double* x, const double* dx, int64_t i) {
+      std::vector<Dual> r((size_t)n);
+      for (int j = 0; j < n; ++j) r[(size_t)j] = Dual(x ? x[j * N + i] : 0.0, dx ? dx[j * N + i] : 0.0);
+      return r;
+    };
+    auto put = [&](int k, int64_t i, const Dual& v) {
+      if (out) out[k * N + i] = v.value;
+      if (dout) dout[k * N + i] = v.tangent;
+    };
+    batch_eval((int)N,
+               [&](int i) {
+                 const std::vector<Dual> a = seed(q, dq, i);
+                 if (op == 0) {
+                   const Frames<Dual> w = forward_kinematics<Dual>(m, a);
+                   for (int j = 0; j < n; ++j) {
+                     for (int c = 0; c < 3; ++c)
+                       for (int r = 0; r < 3; ++r) put(j * 12 + c * 3 + r, i, w[(size_t)j].R(r, c));
+                     for (int r = 0; r < 3; ++r) put(j * 12 + 9 + r, i, w[(size_t)j].p[r]);
+                   }
+                 } else if (op == 2) {
+                   const Dense<Dual> mm = variant ? crba_loop<Dual>(m, a) : crba<Dual>(m, a);
+                   for (int k = 0; k < n * n; ++k) put(k, i, mm.d[(size_t)k]);
+                 } else {
+                   const std::vector<Dual> b = seed(qd, dqd, i), c = seed(x2, dx2, i);
+                   const ExtForces<Dual> f = fext_row<Dual>(fext, N, n, i);
+                   std::vector<Dual> r((size_t)n, Dual(0.0));
+                   int st = 0;
+                   if (op == 1) {
+                     r = variant ? rnea_loop<Dual>(m, a, b, c, g, f) : rnea<Dual>(m, a, b, c, g, f);
+                   } else {
+                     try {
+                       r = variant ? aba_loop<Dual>(m, a, b, c, g, f) : forward_dynamics<Dual>(m, a, b, c, g, f);
+                     } catch (const SingularInertiaError&) {
+                       st = 7;
+                       r.assign((size_t)n, Dual(0.0));
+                     }
+                     if (status) status[i] = st;
+                   }
+                   for (int j = 0; j < n; ++j) put(j, i, r[(size_t)j]);
+                 }
                },
                threads);
     return 0;

@@ -35,6 +35,7 @@ __all__ = [
     "TaskGains", "TaskTarget", "PostureGains", "StateBatch", "robots", "urdf", "floating_base", "random_states",
     "rnea", "bias_forces", "gravity_vector", "coriolis_vector", "crba", "forward_dynamics", "dynamics",
     "forward_kinematics", "forward_kinematics_scan", "frame_transform", "geometric_jacobian", "manipulability", "diff_ik_step", "osc_step", "batch_rnea", "batch_crba",
+    "forward_kinematics_jvp", "rnea_jvp", "crba_jvp", "forward_dynamics_jvp",
     "batch_forward_dynamics", "shard_range",
 ]
 
@@ -109,7 +110,7 @@ class RobotModel:
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
             self._lib.vd_model_destroy(self._h)
-            self._h = ctypes.c_void_p()
+            self._h = None
 
     @property
     def handle(self):
@@ -309,7 +310,7 @@ class DeviceModel:
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
             self._lib.vd_device_model_destroy(self._h)
-            self._h = ctypes.c_void_p()
+            self._h = None
 
     @property
     def handle(self):
@@ -517,6 +518,65 @@ def geometric_jacobian(dm, q, frame):
     _check(_lib.load().vd_jacobian(dm.handle, _dtype_code(qs), N, _p(qs), N, _frame_id(dm, frame), None, _p(out), N,
                                    _stream(dev)))
     return out.t().reshape(N, n, 6).transpose(1, 2)
+
+
+# ------------------------------------------------------------------ forward-mode JVPs (autodiff.hpp:41-56)
+# jvp(fn, x, v) of the reference, for fn in the library's own batched
+# functions: one device pass on dual numbers returns (fn(x), D fn(x)·v).
+# Tangent arguments default to zero.
+def forward_kinematics_jvp(dm, q, dq):
+    """(frames, d frames), both (N, n, 12) like forward_kinematics."""
+    qs, (dqs,), N, dev = _prep(dm, q, (dq, "dq"))
+    n = dm.dof()
+    out, dout = _out(dev, qs.dtype, 12 * n, N), _out(dev, qs.dtype, 12 * n, N)
+    _check(_lib.load().vd_fk_jvp(dm.handle, _dtype_code(qs), N, _p(qs), _p(dqs), N, _p(out), _p(dout), N,
+                                 _stream(dev)))
+    return out.t().reshape(N, n, 12), dout.t().reshape(N, n, 12)
+
+
+def rnea_jvp(dm, q, qd, qdd, dq=None, dqd=None, dqdd=None, gravity=None, fext=None):
+    """(τ, dτ) with dτ = ∂τ/∂q·dq + ∂τ/∂q̇·dq̇ + ∂τ/∂q̈·dq̈ (fext held constant)."""
+    qs, (qds, qdds, dqs, dqds, dqdds), N, dev = _prep(dm, q, (qd, "qd"), (qdd, "qdd"), (dq, "dq"), (dqd, "dqd"),
+                                                        (dqdd, "dqdd"))
+    n = dm.dof()
+    out, dout = _out(dev, qs.dtype, n, N), _out(dev, qs.dtype, n, N)
+    fx = _fext_planes(fext, N, n, qs.dtype, dev)
+    g = (gravity or GravitySpec.standard()).c()
+    _check(_lib.load().vd_rnea_jvp(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(qdds), _p(dqs), _p(dqds),
+                                   _p(dqdds), N, g, _p(fx), _p(out), _p(dout), N, _stream(dev)))
+    return out.t(), dout.t()
+
+
+def crba_jvp(dm, q, dq):
+    """(M, dM) with dM = Σ_k ∂M/∂q_k dq_k, both (N, n, n)."""
+    qs, (dqs,), N, dev = _prep(dm, q, (dq, "dq"))
+    n = dm.dof()
+    out, dout = _out(dev, qs.dtype, n * n, N), _out(dev, qs.dtype, n * n, N)
+    _check(_lib.load().vd_crba_jvp(dm.handle, _dtype_code(qs), N, _p(qs), _p(dqs), N, _p(out), _p(dout), N,
+                                   _stream(dev)))
+    return (out.t().reshape(N, n, n).transpose(1, 2), dout.t().reshape(N, n, n).transpose(1, 2))
+
+
+def forward_dynamics_jvp(dm, q, qd, tau, dq=None, dqd=None, dtau=None, gravity=None, fext=None,
+                         return_status=False):
+    """(q̈, dq̈) by the articulated-body algorithm on duals; SingularInertiaError
+    as forward_dynamics unless return_status."""
+    torch = _torch()
+    qs, (qds, taus, dqs, dqds, dtaus), N, dev = _prep(dm, q, (qd, "qd"), (tau, "tau"), (dq, "dq"), (dqd, "dqd"),
+                                                        (dtau, "dtau"))
+    n = dm.dof()
+    out, dout = _out(dev, qs.dtype, n, N), _out(dev, qs.dtype, n, N)
+    status = torch.zeros(N, dtype=torch.int32, device=dev)
+    fx = _fext_planes(fext, N, n, qs.dtype, dev)
+    g = (gravity or GravitySpec.standard()).c()
+    _check(_lib.load().vd_aba_jvp(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(taus), _p(dqs), _p(dqds),
+                                  _p(dtaus), N, g, _p(fx), _p(out), _p(dout), N, _p(status), _stream(dev)))
+    if return_status:
+        return out.t(), dout.t(), status
+    if N and int(status.max().item()) != 0:
+        raise SingularInertiaError(
+            "forward_dynamics: mass matrix is not positive definite (zero-inertia degree of freedom?)")
+    return out.t(), dout.t()
 
 
 def manipulability(dm, q, frame):

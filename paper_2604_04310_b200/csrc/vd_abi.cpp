@@ -509,6 +509,59 @@ int vd_manipulability(vd_device_model dm, int dtype, int64_t N, const void* q, i
                 "vd_manipulability");
 }
 
+// ---- forward-mode JVPs (autodiff.hpp:41-56 applied to the library's own functions)
+// gravity3 is a host array (NULL = GravitySpec::standard()); it travels by value.
+static double gcomp(const double* g3, int k) { return g3 ? g3[k] : (k == 2 ? 9.81 : 0.0); }
+static int jvp_launch(vd_device_model dm, int dtype, int64_t N, int64_t ld_in, int64_t ld_out, void* stream,
+                      const vdk::JvpArgs& a, const char* what) {
+  if (N > 0 && dm->n > 0 && !a.out && !a.dout) return set_error(VD_ERR_INVALID_ARGUMENT, "null output buffers");
+  if (dm->n == 0) {
+    if (a.status && N > 0 && cudaMemsetAsync(a.status, 0, sizeof(int32_t) * N, (cudaStream_t)stream) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), what);
+    return VD_OK;
+  }
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_jvp(make_launch(dm, dtype, N, ld_in, ld_out, stream), a), what);
+}
+
+int vd_fk_jvp(vd_device_model dm, int dtype, int64_t N, const void* q, const void* dq, int64_t ld_in, void* frames,
+              void* dframes, int64_t ld_out, void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  VD_NEED(q, "q");
+  vdk::JvpArgs a{vdk::kJvpFK, {q, nullptr, nullptr}, {dq, nullptr, nullptr}, {0.0, 0.0, 0.0}, nullptr, frames, dframes, nullptr};
+  return jvp_launch(dm, dtype, N, ld_in, ld_out, stream, a, "vd_fk_jvp");
+}
+
+int vd_rnea_jvp(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* qdd,
+                const void* dq, const void* dqd, const void* dqdd, int64_t ld_in, const double* g3, const void* fext,
+                void* tau, void* dtau, int64_t ld_out, void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  VD_NEED(q, "q");
+  VD_NEED(qd, "qd");
+  VD_NEED(qdd, "qdd");
+  vdk::JvpArgs a{vdk::kJvpRNEA, {q, qd, qdd}, {dq, dqd, dqdd}, {gcomp(g3, 0), gcomp(g3, 1), gcomp(g3, 2)}, fext, tau, dtau, nullptr};
+  return jvp_launch(dm, dtype, N, ld_in, ld_out, stream, a, "vd_rnea_jvp");
+}
+
+int vd_crba_jvp(vd_device_model dm, int dtype, int64_t N, const void* q, const void* dq, int64_t ld_in, void* M,
+                void* dM, int64_t ld_out, void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  VD_NEED(q, "q");
+  vdk::JvpArgs a{vdk::kJvpCRBA, {q, nullptr, nullptr}, {dq, nullptr, nullptr}, {0.0, 0.0, 0.0}, nullptr, M, dM, nullptr};
+  return jvp_launch(dm, dtype, N, ld_in, ld_out, stream, a, "vd_crba_jvp");
+}
+
+int vd_aba_jvp(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau,
+               const void* dq, const void* dqd, const void* dtau, int64_t ld_in, const double* g3, const void* fext,
+               void* qdd, void* dqdd, int64_t ld_out, int32_t* status, void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  VD_NEED(q, "q");
+  VD_NEED(qd, "qd");
+  VD_NEED(tau, "tau");
+  vdk::JvpArgs a{vdk::kJvpABA, {q, qd, tau}, {dq, dqd, dtau}, {gcomp(g3, 0), gcomp(g3, 1), gcomp(g3, 2)}, fext, qdd, dqdd, status};
+  return jvp_launch(dm, dtype, N, ld_in, ld_out, stream, a, "vd_aba_jvp");
+}
+
 // ---- internal (not in the public header): packed tables for the robot-table generator
 uint64_t vdi_model_fingerprint(vd_model m) { return m ? vdh::fingerprint(vdh::pack(m->m)) : 0; }
 int vdi_model_packed(vd_model m, int* n, int* parent, int* kind, int* axis_code, double* axis, double* R, double* p,

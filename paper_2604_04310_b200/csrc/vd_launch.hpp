@@ -41,6 +41,20 @@ int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* 
                     void* bias, void* qdd, int32_t* status);
 int launch_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
                int32_t* status);
+// Forward-mode JVPs (vd_jvp.cuh): one launch of FK / RNEA / CRBA / ABA on dual numbers.
+enum JvpOp : int { kJvpFK = 0, kJvpRNEA = 1, kJvpCRBA = 2, kJvpABA = 3 };
+struct JvpArgs {
+  int op;             // JvpOp
+  const void* x[3];   // primal inputs (q, q̇, q̈ | τ)
+  const void* dx[3];  // tangents (NULL = 0)
+  double g[3];        // gravity a_g (rnea / aba), by value
+  const void* fext;   // constant external wrenches (rnea / aba), NULL = none
+  void* out;          // values (may be NULL)
+  void* dout;         // tangents (may be NULL)
+  int32_t* status;    // aba
+};
+int launch_jvp(const Launch& L, const JvpArgs& a);
+
 // mode 0: diff_ik_step (out = q̇, aux = pose error); mode 1: manipulability (out = w)
 int launch_task(const Launch& L, const void* q, const TaskShared& P, int mode, void* out, void* aux,
                 int32_t* status);

@@ -57,6 +57,7 @@ def lib():
         L.orc_batch_osc.argtypes = [vp, i64, vp, vp, cc, vp, vp, vp, vp, vp, cd, cd, vp, cd, vp, vp, vp, ci]
         L.orc_batch_diffik.argtypes = [vp, i64, vp, cc, vp, vp, vp, cd, vp, vp, ci]
         L.orc_batch_manip.argtypes = [vp, i64, vp, cc, vp, ci]
+        L.orc_batch_jvp.argtypes = [vp, ci, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ci, ci]
         _lib = L
     return _lib
 
@@ -221,6 +222,29 @@ class Model:
         _chk(lib().orc_batch_diffik(self.h, N, _ptr(q), frame.encode(), _ptr(t12), _ptr(kp), _ptr(ff), float(damping),
                                     _ptr(qdot), _ptr(err), threads))
         return qdot, err
+
+    JVP_OPS = {"fk": (0, 12), "rnea": (1, 1), "crba": (2, None), "fd": (3, 1)}
+
+    def jvp(self, op, x, dx, gravity=(0, 0, 9.81), fext=None, variant=0, threads=0):
+        """(values, tangents[, status]) of op in {fk, rnea, crba, fd} run on duals.
+        x / dx: tuples of (N, n) arrays (q[, qd, qdd|tau]); a None tangent is 0."""
+        code, per = self.JVP_OPS[op]
+        x = [_F(a) for a in x] + [None] * (3 - len(x))
+        dx = [_F(a) for a in dx] + [None] * (3 - len(dx))
+        N, n = x[0].shape[0], self.n
+        K = n * n if per is None else n * per
+        out = np.empty((N, K), order="F")
+        dout = np.empty((N, K), order="F")
+        st = np.zeros(N, dtype=np.int32)
+        g = np.asarray(gravity, dtype=np.float64)
+        fx = None if fext is None else np.asfortranarray(np.asarray(fext, dtype=np.float64).reshape(N, n * 6))
+        _chk(lib().orc_batch_jvp(self.h, code, N, _ptr(x[0]), _ptr(x[1]), _ptr(x[2]), _ptr(dx[0]), _ptr(dx[1]),
+                                 _ptr(dx[2]), _ptr(g), _ptr(fx), _ptr(out), _ptr(dout), _ptr(st), threads, variant))
+        if op == "crba":
+            out, dout = (a.reshape(N, n, n).transpose(0, 2, 1) for a in (out, dout))
+        if op == "fd":
+            return out, dout, st
+        return out, dout
 
     def manipulability(self, q, frame, threads=0):
         q = _F(q)

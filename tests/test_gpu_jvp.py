@@ -1,0 +1,180 @@
+"""GPU parity of the forward-mode JVP kernels (vd_*_jvp)
+against the oracle's dual-number evaluation of the reference algorithms
+(oracle/orc_dual.hpp, pinned by finite differences in test_oracle_jvp.py).
+Values and tangents are both checked: fp64 ≤ 1e-10, fp32 ≤ 1e-4 (vs the fp64
+oracle at the fp32-rounded inputs), rel_err of helpers.hpp:67-72.  Forward
+dynamics tangents carry M⁻¹ twice (dq̈ = M⁻¹(dτ − dc − dM q̈)), so their bound
+scales with κ(M)²; well-conditioned instances meet the flat bar."""
+import numpy as np
+import pytest
+import torch
+
+from oracle_ffi import Model as OModel
+from oracle_ffi import rel_err
+from urdf_gen import random_urdf
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-10
+TOL32 = 1e-4
+ROBOTS = ["chain7", "tree29", "humanoid23"]
+
+
+def _t(a, dtype=torch.float64):
+    return None if a is None else torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+def _np(t):
+    return t.double().cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def omodels(oracle):
+    return {n: OModel.builtin(n) for n in ROBOTS}
+
+
+def _case(om, N, seed):
+    q, qd, qdd, tau = om.random_states(N, seed, True, True)
+    rng = np.random.default_rng(seed)
+    return q, qd, qdd, tau, [rng.standard_normal(q.shape) for _ in range(3)]
+
+
+def _flat(a):
+    return np.asarray(a).reshape(a.shape[0], -1)
+
+
+@pytest.mark.parametrize("name", ROBOTS)
+@pytest.mark.parametrize("generic", [False, True])
+def test_kinematics_dynamics_jvp_fp64(vd, cuda, omodels, name, generic):
+    om = omodels[name]
+    dm = vd.DeviceModel(vd.robots.by_name(name), 0, generic=generic)
+    q, qd, qdd, tau, (vq, vqd, vqdd) = _case(om, 1031, 11)
+    # FK
+    val, tan = vd.forward_kinematics_jvp(dm, _t(q), _t(vq))
+    rv, rt = om.jvp("fk", (q,), (vq,))
+    assert rel_err(_flat(_np(val)), rv, axis=1).max() <= TOL64
+    assert rel_err(_flat(_np(tan)), rt, axis=1).max() <= TOL64
+    # RNEA along (q, q̇, q̈)
+    val, tan = vd.rnea_jvp(dm, _t(q), _t(qd), _t(qdd), _t(vq), _t(vqd), _t(vqdd))
+    rv, rt = om.jvp("rnea", (q, qd, qdd), (vq, vqd, vqdd))
+    assert rel_err(_np(val), rv, axis=1).max() <= TOL64
+    assert rel_err(_np(tan), rt, axis=1).max() <= TOL64
+    # CRBA along q
+    val, tan = vd.crba_jvp(dm, _t(q), _t(vq))
+    rv, rt = om.jvp("crba", (q,), (vq,))
+    assert rel_err(_np(val), rv, axis=1).max() <= TOL64
+    assert rel_err(_np(tan), rt, axis=1).max() <= TOL64
+
+
+@pytest.mark.parametrize("name", ROBOTS)
+@pytest.mark.parametrize("generic", [False, True])
+def test_forward_dynamics_jvp_fp64(vd, cuda, omodels, name, generic):
+    om = omodels[name]
+    dm = vd.DeviceModel(vd.robots.by_name(name), 0, generic=generic)
+    q, qd, _, tau, (vq, vqd, vtau) = _case(om, 1031, 12)
+    val, tan, st = vd.forward_dynamics_jvp(dm, _t(q), _t(qd), _t(tau), _t(vq), _t(vqd), _t(vtau),
+                                           return_status=True)
+    assert int(st.max()) == 0
+    rv, rt, rst = om.jvp("fd", (q, qd, tau), (vq, vqd, vtau))
+    assert np.all(rst == 0)
+    cond = np.linalg.cond(om.crba(q))
+    ev = rel_err(_np(val), rv, axis=1)
+    et = rel_err(_np(tan), rt, axis=1)
+    assert np.all(ev <= np.maximum(TOL64, 1e-15 * cond)), float(ev.max())
+    bound = np.maximum(TOL64, 1e-15 * cond * cond)
+    w = int(np.argmax(et / bound))
+    assert np.all(et <= bound), (float(et[w]), float(cond[w]))
+    well = cond < 1e3
+    assert et[well].max(initial=0) <= TOL64
+
+
+@pytest.mark.parametrize("name", ["chain7", "tree29"])
+def test_jvp_fp32(vd, cuda, omodels, name):
+    om = omodels[name]
+    dm = vd.DeviceModel(vd.robots.by_name(name), 0)
+    q, qd, qdd, tau, (vq, vqd, vqdd) = _case(om, 1024, 13)
+    r32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    q, qd, qdd, vq, vqd, vqdd = map(r32, (q, qd, qdd, vq, vqd, vqdd))
+    f = torch.float32
+    val, tan = vd.rnea_jvp(dm, _t(q, f), _t(qd, f), _t(qdd, f), _t(vq, f), _t(vqd, f), _t(vqdd, f))
+    rv, rt = om.jvp("rnea", (q, qd, qdd), (vq, vqd, vqdd))
+    assert rel_err(_np(val), rv, axis=1).max() <= TOL32
+    assert rel_err(_np(tan), rt, axis=1).max() <= TOL32
+    val, tan = vd.crba_jvp(dm, _t(q, f), _t(vq, f))
+    rv, rt = om.jvp("crba", (q,), (vq,))
+    assert rel_err(_np(val), rv, axis=1).max() <= TOL32
+    assert rel_err(_np(tan), rt, axis=1).max() <= TOL32
+    val, tan = vd.forward_kinematics_jvp(dm, _t(q, f), _t(vq, f))
+    rv, rt = om.jvp("fk", (q,), (vq,))
+    assert rel_err(_flat(_np(tan)), rt, axis=1).max() <= TOL32
+
+
+def test_jvp_partial_tangents_fext_gravity(vd, cuda, omodels):
+    """NULL tangents are zero; f_ext is a constant input; gravity is honoured."""
+    om = omodels["tree29"]
+    dm = vd.DeviceModel(vd.robots.tree29(), 0)
+    N, n = 257, om.n
+    q, qd, qdd, tau, (vq, vqd, _) = _case(om, N, 14)
+    rng = np.random.default_rng(3)
+    fext = rng.uniform(-3, 3, (N, n, 6))
+    g = (0.5, -0.2, 9.5)
+    val, tan = vd.rnea_jvp(dm, _t(q), _t(qd), _t(qdd), dqd=_t(vqd), gravity=vd.GravitySpec(g), fext=_t(fext))
+    rv, rt = om.jvp("rnea", (q, qd, qdd), (None, vqd, None), gravity=g, fext=fext)
+    assert rel_err(_np(val), rv, axis=1).max() <= TOL64
+    assert rel_err(_np(tan), rt, axis=1).max() <= TOL64
+    # the primal output equals the plain kernel bit for bit in value terms
+    assert rel_err(_np(val), _np(vd.rnea(dm, _t(q), _t(qd), _t(qdd), vd.GravitySpec(g), _t(fext))),
+                   axis=1).max() <= 1e-13
+    val, tan = vd.forward_dynamics_jvp(dm, _t(q), _t(qd), _t(tau), dq=_t(vq), gravity=vd.GravitySpec(g),
+                                       fext=_t(fext))
+    rv, rt, _ = om.jvp("fd", (q, qd, tau), (vq, None, None), gravity=g, fext=fext)
+    cond = np.linalg.cond(om.crba(q))
+    assert np.all(rel_err(_np(tan), rt, axis=1) <= np.maximum(TOL64, 1e-15 * cond * cond))
+    # zero tangent -> zero output tangent
+    _, tz = vd.rnea_jvp(dm, _t(q), _t(qd), _t(qdd))
+    assert float(tz.abs().max()) == 0.0
+
+
+def test_jvp_linearity_and_finite_differences(vd, cuda, omodels):
+    om = omodels["chain7"]
+    dm = vd.DeviceModel(vd.robots.chain7(), 0)
+    q, qd, qdd, tau, (v1, v2, v3) = _case(om, 500, 15)
+    a, b = 0.7, -1.3
+    _, t1 = vd.crba_jvp(dm, _t(q), _t(v1))
+    _, t2 = vd.crba_jvp(dm, _t(q), _t(v2))
+    _, t12 = vd.crba_jvp(dm, _t(q), _t(a * v1 + b * v2))
+    assert rel_err(_np(t12), a * _np(t1) + b * _np(t2), axis=1).max() <= 1e-12
+    # central differences of the device's own ABA (step 1e-6, 1e-5)
+    h = 1e-6
+    _, tan = vd.forward_dynamics_jvp(dm, _t(q), _t(qd), _t(tau), _t(v1), _t(v2), _t(v3))
+    fp = _np(vd.forward_dynamics(dm, _t(q + h * v1), _t(qd + h * v2), _t(tau + h * v3)))
+    fm = _np(vd.forward_dynamics(dm, _t(q - h * v1), _t(qd - h * v2), _t(tau - h * v3)))
+    cond = np.linalg.cond(om.crba(q))
+    e = rel_err(_np(tan), (fp - fm) / (2 * h), axis=1)
+    assert np.all(e <= np.maximum(1e-5, 1e-9 * cond))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_jvp_random_trees(vd, cuda, oracle, seed):
+    text = random_urdf(seed, n=12, branchiness=0.5)
+    om = OModel.from_urdf(text)
+    dm = vd.DeviceModel(vd.urdf.load_model_from_string(text), 0)
+    q, qd, qdd, tau, (vq, vqd, vqdd) = _case(om, 300, 400 + seed)
+    _, tan = vd.rnea_jvp(dm, _t(q), _t(qd), _t(qdd), _t(vq), _t(vqd), _t(vqdd))
+    assert rel_err(_np(tan), om.jvp("rnea", (q, qd, qdd), (vq, vqd, vqdd))[1], axis=1).max() <= TOL64
+    _, tan = vd.crba_jvp(dm, _t(q), _t(vq))
+    assert rel_err(_np(tan), om.jvp("crba", (q,), (vq,))[1], axis=1).max() <= TOL64
+
+
+def test_jvp_errors_and_empty(vd, cuda):
+    dm = vd.DeviceModel(vd.robots.chain7(), 0)
+    e = torch.empty((0, 7), dtype=torch.float64, device="cuda")
+    v, t = vd.rnea_jvp(dm, e, e, e)
+    assert v.shape == (0, 7) and t.shape == (0, 7)
+    lib = vd._lib.load()
+    q = torch.zeros((4, 7), dtype=torch.float64, device="cuda")
+    # both outputs NULL
+    assert lib.vd_crba_jvp(dm.handle, 0, 4, q.data_ptr(), None, 4, None, None, 4, None) == vd._lib.VD_ERR_INVALID_ARGUMENT
+    # ld < N
+    assert lib.vd_fk_jvp(dm.handle, 0, 4, q.data_ptr(), None, 2, q.data_ptr(), None, 4,
+                         None) == vd._lib.VD_ERR_DIMENSION
