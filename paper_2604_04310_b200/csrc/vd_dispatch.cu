@@ -63,6 +63,10 @@ int launch_crba(const Launch& L, const void* q, void* M) {
 int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, const void* fext,
                void* qdd, int32_t* status) {
   if (L.N == 0) return 0;
+  if (!fext) {
+    const int rc = launch_gen_aba(L, q, qd, tau, g3, qdd, status);
+    if (rc >= 0) return rc;
+  }
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::aba(mv, L, q, qd, tau, g3, fext, qdd, status); });
 }
 

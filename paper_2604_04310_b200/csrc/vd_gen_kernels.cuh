@@ -1,0 +1,148 @@
+// Kernels around the generated straight-line per-robot routines
+// (vd_gen_robots.cuh, tools/gen_tree_kernels.py).
+//
+// One thread = one robot state, persistent grid (one wave of resident CTAs,
+// each thread strides over the batch).  The generated ABA hands its
+// pass-2 -> pass-3 state (per joint U/D, u/D and cos/sin or q) to the context
+// by slot number; slot k lives
+//   * in registers     when k >= kSlots - kReg  (stored last, read first: the
+//                       root chain of the tree),
+//   * in shared memory when k <  kSmem           ([k][thread] layout),
+//   * otherwise in a global scratch slab [k - kSmem][thread slot] that a
+//     persistent grid re-uses for every state it processes, so it stays
+//     resident in L2 (footprint = resident threads x slots).
+// Loads/stores are SoA-coalesced (element (i, k) at k*ld + i).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "vd_gen_robots.cuh"
+
+namespace vdk {
+
+constexpr int kGenBlock = 128;
+
+// Opaque state ops: a value written through st() must really go to its slot
+// (plain C++ stores would be forwarded to the matching loads, keeping every
+// value live in registers).  Inputs are read once each (prologue / pass 2), so
+// they are plain read-only loads the scheduler may hoist.
+template <class T>
+struct GenMem;
+template <>
+struct GenMem<double> {
+  static __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+  static __device__ __forceinline__ void stg(double* p, double v) {
+    asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v));
+  }
+  static __device__ __forceinline__ double ldgs(const double* p) {
+    double v;
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+  }
+  static __device__ __forceinline__ void sts(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
+  static __device__ __forceinline__ double lds(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+  }
+};
+template <>
+struct GenMem<float> {
+  static __device__ __forceinline__ float ldg(const float* p) { return __ldg(p); }
+  static __device__ __forceinline__ void stg(float* p, float v) { asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v)); }
+  static __device__ __forceinline__ float ldgs(const float* p) {
+    float v;
+    asm volatile("ld.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+  }
+  static __device__ __forceinline__ void sts(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v)); }
+  static __device__ __forceinline__ float lds(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+  }
+};
+
+template <class T, int kSlots, int kReg, int kSmem, int BS, bool kSync>
+struct GenAbaCx {
+  static constexpr int kGlobal = kSlots - kReg - kSmem > 0 ? kSlots - kReg - kSmem : 0;
+  const T* q_;   // &q[i]; element (i, j) at q_[j * ld]
+  const T* qd_;
+  const T* tau_;
+  T* out_;
+  T* sb;         // this thread's scratch: slot k at sb[(k - kSmem) * 32] (warp-interleaved)
+  uint32_t sm;   // shared address of slot 0 for this thread ([k][threadIdx.x])
+  int64_t ld, ldo;
+  bool active;   // false on the padding lanes of the last round (they compute, but write nothing)
+  T g3[3];
+  T reg[kReg > 0 ? kReg : 1];
+  __device__ __forceinline__ T q(int j) const { return GenMem<T>::ldg(q_ + j * ld); }
+  __device__ __forceinline__ T qd(int j) const { return GenMem<T>::ldg(qd_ + j * ld); }
+  __device__ __forceinline__ T tau(int j) const { return GenMem<T>::ldg(tau_ + j * ld); }
+  __device__ __forceinline__ T g(int k) const { return g3[k]; }
+  __device__ __forceinline__ void st(int k, T v) {
+    if (k >= kSlots - kReg) reg[k - (kSlots - kReg)] = v;
+    else if (k < kSmem) GenMem<T>::sts(sm + (uint32_t)(k * BS * sizeof(T)), v);
+    else GenMem<T>::stg(sb + (k - kSmem) * 32, v);
+  }
+  __device__ __forceinline__ T get(int k) const {
+    if (k >= kSlots - kReg) return reg[k - (kSlots - kReg)];
+    if (k < kSmem) return GenMem<T>::lds(sm + (uint32_t)(k * BS * sizeof(T)));
+    return GenMem<T>::ldgs(sb + (k - kSmem) * 32);
+  }
+  __device__ __forceinline__ void qdd(int j, T v) const {
+    if (active) out_[j * ldo] = v;
+  }
+  __device__ __forceinline__ void sync() const {
+    if constexpr (kSync) __syncthreads();
+  }
+};
+
+// Scratch elements per resident thread (0 when every slot is on chip).
+template <class R, class T, int kReg, int kSmem>
+constexpr int64_t gen_aba_scratch_per_thread() {
+  return GenAbaCx<T, R::kAbaSlots, kReg, kSmem, 32, false>::kGlobal;
+}
+
+template <class R, class T, int kReg, int kSmem, int kMinB, int BS = kGenBlock, bool kSync = false>
+__global__ void __launch_bounds__(BS, kMinB)
+    k_gen_aba(int64_t N, const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau, int64_t ldi,
+              T g0, T g1, T g2, T* __restrict__ qdd, int64_t ldo, int32_t* __restrict__ status,
+              T* __restrict__ scratch) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenAbaCx<T, R::kAbaSlots, kReg, kSmem, BS, kSync>;
+  Cx cx;
+  const int64_t slot = (int64_t)blockIdx.x * BS + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * BS;
+  cx.sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  cx.sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  cx.g3[0] = g0;
+  cx.g3[1] = g1;
+  cx.g3[2] = g2;
+  // every thread of a block runs the same number of rounds (barriers inside)
+  for (int64_t base = (int64_t)blockIdx.x * BS; base < N; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    cx.active = i0 < N;
+    const int64_t i = cx.active ? i0 : N - 1;
+    // launder the strides each round so the per-column addresses are not
+    // hoisted out of the loop (29 x 3 live 64-bit addresses otherwise spill)
+    int64_t ld, lo;
+    asm volatile("mov.b64 %0, %1;" : "=l"(ld) : "l"(ldi));
+    asm volatile("mov.b64 %0, %1;" : "=l"(lo) : "l"(ldo));
+    cx.ld = ld;
+    cx.ldo = lo;
+    cx.q_ = q + i;
+    cx.qd_ = qd + i;
+    cx.tau_ = tau + i;
+    cx.out_ = qdd + i;
+    const bool ok = R::template aba<T>(cx);
+    if (cx.active) {
+      if (!ok) {
+        for (int j = 0; j < R::kN; ++j) qdd[(int64_t)j * ldo + i] = T(0);
+      }
+      if (status) status[i] = ok ? 0 : 7;
+    }
+  }
+}
+
+}  // namespace vdk

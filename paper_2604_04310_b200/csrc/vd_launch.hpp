@@ -37,6 +37,10 @@ int launch_rnea(const Launch& L, int mode, const void* q, const void* qd, const 
 int launch_crba(const Launch& L, const void* q, void* M);
 int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, const void* fext,
                void* qdd, int32_t* status);
+// Generated straight-line kernel (vd_inst_gen.cu) when one exists for L.spec;
+// -1 when not applicable.
+int launch_gen_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* qdd,
+                   int32_t* status);
 int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
                     void* bias, void* qdd, int32_t* status);
 int launch_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,

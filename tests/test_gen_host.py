@@ -1,0 +1,85 @@
+"""The generated straight-line robot routines (tools/gen_tree_kernels.py ->
+vd_gen_robots.cuh), compiled for the host, against the oracle's LLT forward
+dynamics (dynamics.hpp:421-444) and ABA restatement.  Runs without a GPU: it
+checks the generator's symbolic algebra and structural-zero folding; the GPU
+parity tests then check the same code on the device."""
+import ctypes
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle_ffi import Model, rel_err
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CSRC = os.path.join(ROOT, "paper_2604_04310_b200", "csrc")
+
+
+@pytest.fixture(scope="module")
+def genlib(tmp_path_factory):
+    so = str(tmp_path_factory.mktemp("gen") / "gen_host.so")
+    # FMA contraction as on the device (nvcc contracts mul+add by default)
+    subprocess.run(["g++", "-O1", "-march=x86-64-v3", "-ffp-contract=fast", "-std=c++20", "-shared", "-fPIC", "-I", CSRC,
+                    os.path.join(ROOT, "tests", "cpp", "gen_host.cpp"), "-o", so], check=True)
+    L = ctypes.CDLL(so)
+    L.gen_aba_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 6
+    L.gen_fingerprint.restype = ctypes.c_ulonglong
+    return L
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def test_generated_tables_are_current():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_tree_kernels.py"), "--check"],
+                       capture_output=True, text=True)
+    if "No such file" in r.stderr or "OSError" in r.stderr:
+        pytest.skip("product library not built")
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("name,code", [("chain7", 1), ("tree29", 2)])
+@pytest.mark.parametrize("f32", [False, True])
+def test_generated_aba_matches_oracle(genlib, name, code, f32):
+    om = Model.builtin(name)
+    N = 2048
+    q, qd, _, tau = om.random_states(N, 2604 + code, True, True)
+    dt = np.float32 if f32 else np.float64
+    Q, QD, TA = (np.asfortranarray(a.astype(dt)) for a in (q, qd, tau))
+    out = np.zeros_like(Q, order="F")
+    st = np.zeros(N, dtype=np.int32)
+    g = np.array([0.0, 0.0, 9.81])
+    bad = genlib.gen_aba_host(code, int(f32), N, _p(Q), _p(QD), _p(TA), _p(g), _p(out), _p(st))
+    assert bad == 0
+    ref, rst = om.forward_dynamics(q, qd, tau)
+    assert np.all(rst == 0)
+    err = rel_err(out.astype(np.float64), ref, axis=1)
+    cond = np.linalg.cond(om.crba(q))
+    # flat bar where the problem is well conditioned for the precision
+    # (DESIGN.md §Parity policy): κ < 1e5 in fp64, κ < 1e4 in fp32
+    well = cond < (1e4 if f32 else 1e5)
+    tol = 1e-4 if f32 else 1e-10
+    assert err[well].max(initial=0) <= tol
+    # ill-conditioned instances (tree29 near base gimbal lock): forward-error
+    # bound of a backward-stable solve, n·ε·κ(M) (DESIGN.md §Parity policy)
+    eps = np.finfo(np.float32 if f32 else np.float64).eps
+    bound = np.maximum(tol, om.n * eps * cond)
+    assert np.all(err <= bound)
+
+
+def test_generated_aba_with_gravity_roundtrip(genlib):
+    """FD∘ID (test_dynamics.cpp:335-351) with non-standard gravity."""
+    om = Model.builtin("tree29")
+    N = 512
+    q, qd, qdd, _ = om.random_states(N, 77, True, False)
+    g = np.array([0.3, -0.4, 9.0])
+    tau = om.rnea(q, qd, qdd, gravity=tuple(g))
+    out = np.zeros_like(q, order="F")
+    st = np.zeros(N, dtype=np.int32)
+    Q, QD, TA = (np.asfortranarray(a) for a in (q, qd, tau))
+    assert genlib.gen_aba_host(2, 0, N, _p(Q), _p(QD), _p(TA), _p(g), _p(out), _p(st)) == 0
+    cosb = np.abs(np.cos(q[:, 4]))
+    assert rel_err(out, qdd, axis=1)[cosb > 0.05].max() <= 1e-8

@@ -1,0 +1,537 @@
+#!/usr/bin/env python3
+"""Generate straight-line, structure-folded per-robot dynamics routines.
+
+Why: the template kernels (vd_algos.cuh) carry per-value "may be non-zero"
+flags through arrays; for a 29-joint tree those arrays stay in local memory,
+the flags become runtime values and the compiled ABA is ~30 K SASS
+instructions of which only ~4.6 K are FP64 (the rest select/flag traffic).
+Here the recursion is unrolled in Python over a symbolic scalar instead:
+every product with a structural 0 / ±1 of the model (axis-aligned joints,
+identity offset rotations, zero offsets, sparse and massless inertias) is
+folded at generation time, and the emitted C++ is plain SSA arithmetic on T.
+
+The math mirrors vd_device.cuh / vd_algos.cuh term by term (same spatial
+algebra, same transform stages X = X_off ∘ X_J, kinematics.hpp:35-38), so the
+generated routine computes what `aba_one` computes:
+
+  ABA (Featherstone RBDA Table 7.1; oracle: forward_dynamics,
+  dynamics.hpp:421-444).  Pass 1 and pass 2 are fused as a DFS: a joint's
+  velocity is computed on the way down and consumed by its pass-2 step on the
+  way up, so only the velocities on the current root->leaf path are live.
+  Pass-2 -> pass-3 state per joint (U/D, u/D and the joint's cos/sin or q) is
+  written through `cx.st(k, v)` / read back with `cx.get(k)`: the kernel
+  decides where slot k lives (registers, shared memory or an L2-resident
+  scratch), because for a 29-joint tree it does not fit in registers.
+
+Model constants come from the library's own packer (tools/gen_robot_tables.py
+`packed`), so the generated code is the packed device model frozen into code.
+
+Usage: python tools/gen_tree_kernels.py [--check]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import gen_robot_tables as grt  # noqa: E402
+
+ROOT = grt.ROOT
+OUT = os.path.join(ROOT, "paper_2604_04310_b200", "csrc", "vd_gen_robots.cuh")
+ROBOTS = [("tree29", "Tree29"), ("chain7", "Chain7")]
+
+
+class Ex:
+    """Symbolic scalar: a compile-time constant (c) or a named SSA value (s)."""
+
+    __slots__ = ("c", "s")
+
+    def __init__(self, c=None, s=None):
+        self.c = c
+        self.s = s
+
+    def is0(self):
+        return self.c is not None and self.c == 0.0
+
+
+def K(x):
+    return Ex(c=float(x))
+
+
+ZERO = K(0.0)
+ONE = K(1.0)
+
+
+class Gen:
+    def __init__(self):
+        self.lines = []
+        self.n = 0
+        self.flops = 0
+
+    # ---------------------------------------------------------------- emission
+    def lit(self, c):
+        if c == 0.0:
+            return "T(0)"
+        if c == 1.0:
+            return "T(1)"
+        if c == -1.0:
+            return "T(-1)"
+        return f"T({float.hex(c)})"
+
+    def o(self, a):
+        return a.s if a.c is None else self.lit(a.c)
+
+    def tmp(self, expr, prefix="t"):
+        name = f"{prefix}{self.n}"
+        self.n += 1
+        self.lines.append(f"  const T {name} = {expr};")
+        return Ex(s=name)
+
+    def raw(self, line):
+        self.lines.append("  " + line)
+
+    # ---------------------------------------------------------------- scalar ops (folding)
+    def add(self, a, b):
+        if a.c is not None and b.c is not None:
+            return K(a.c + b.c)
+        if a.is0():
+            return b
+        if b.is0():
+            return a
+        self.flops += 1
+        return self.tmp(f"{self.o(a)} + {self.o(b)}")
+
+    def sub(self, a, b):
+        if a.c is not None and b.c is not None:
+            return K(a.c - b.c)
+        if b.is0():
+            return a
+        if a.is0():
+            return self.neg(b)
+        self.flops += 1
+        return self.tmp(f"{self.o(a)} - {self.o(b)}")
+
+    def neg(self, a):
+        if a.c is not None:
+            return K(-a.c)
+        return self.tmp(f"-{a.s}")
+
+    def mul(self, a, b):
+        if a.c is not None and b.c is not None:
+            return K(a.c * b.c)
+        if a.is0() or b.is0():
+            return ZERO
+        if a.c == 1.0:
+            return b
+        if b.c == 1.0:
+            return a
+        if a.c == -1.0:
+            return self.neg(b)
+        if b.c == -1.0:
+            return self.neg(a)
+        self.flops += 1
+        return self.tmp(f"{self.o(a)} * {self.o(b)}")
+
+    def sum(self, xs):
+        acc = ZERO
+        for x in xs:
+            acc = self.add(acc, x)
+        return acc
+
+    def dot(self, xs, ys):
+        return self.sum([self.mul(x, y) for x, y in zip(xs, ys)])
+
+    # ---------------------------------------------------------------- 3-vectors / 3x3 (row-major)
+    def cross3(self, x, y):
+        return [self.sub(self.mul(x[1], y[2]), self.mul(x[2], y[1])),
+                self.sub(self.mul(x[2], y[0]), self.mul(x[0], y[2])),
+                self.sub(self.mul(x[0], y[1]), self.mul(x[1], y[0]))]
+
+    def matvec(self, Q, x):
+        return [self.dot(Q[3 * r:3 * r + 3], x) for r in range(3)]
+
+    def matTvec(self, Q, x):
+        return [self.dot([Q[r], Q[3 + r], Q[6 + r]], x) for r in range(3)]
+
+    def vadd(self, x, y):
+        return [self.add(a, b) for a, b in zip(x, y)]
+
+    def vsub(self, x, y):
+        return [self.sub(a, b) for a, b in zip(x, y)]
+
+    # ---------------------------------------------------------------- spatial (angular first: [a0 a1 a2 l0 l1 l2])
+    def motion_in(self, Q, t, m):  # inverse_transform_motion (spatial.hpp:233-238)
+        a = self.matTvec(Q, m[:3])
+        d = self.vsub(m[3:], self.cross3(t, m[:3]))
+        return a + self.matTvec(Q, d)
+
+    def motion_out(self, Q, t, m):  # transform_motion (spatial.hpp:225-230)
+        a = self.matvec(Q, m[:3])
+        l = self.vadd(self.matvec(Q, m[3:]), self.cross3(t, a))
+        return a + l
+
+    def force_out(self, Q, t, f):  # transform_force (spatial.hpp:241-246)
+        l = self.matvec(Q, f[3:])
+        a = self.vadd(self.matvec(Q, f[:3]), self.cross3(t, l))
+        return a + l
+
+    def crm(self, v, m):  # spatial.hpp:204-208
+        a = self.cross3(v[:3], m[:3])
+        l = self.vadd(self.cross3(v[:3], m[3:]), self.cross3(v[3:], m[:3]))
+        return a + l
+
+    def crf(self, v, f):  # spatial.hpp:212-216
+        a = self.vadd(self.cross3(v[:3], f[:3]), self.cross3(v[3:], f[3:]))
+        l = self.cross3(v[:3], f[3:])
+        return a + l
+
+    def sdot(self, f, m):
+        return self.add(self.dot(f[:3], m[:3]), self.dot(f[3:], m[3:]))
+
+    # rigid-body inertia, 10 params: m, h[3], I = xx yy zz xy xz yz (about the origin)
+    def rb_apply(self, b, v):
+        m, h, I = b
+        hv = self.cross3(h, v[3:])
+        hw = self.cross3(h, v[:3])
+        Im = [[I[0], I[3], I[4]], [I[3], I[1], I[5]], [I[4], I[5], I[2]]]
+        a = [self.add(self.dot(Im[r], v[:3]), hv[r]) for r in range(3)]
+        l = [self.sub(self.mul(m, v[3 + k]), hw[k]) for k in range(3)]
+        return a + l
+
+    # articulated inertia: dict A (sym 6: xx yy zz xy xz yz), B (3x3 row-major), C (sym 6)
+    @staticmethod
+    def sym(s6, r, c):
+        return s6[r] if r == c else s6[r + c + 2]
+
+    def ai_from_rb(self, b):
+        m, h, I = b
+        B = [ZERO, self.neg(h[2]), h[1], h[2], ZERO, self.neg(h[0]), self.neg(h[1]), h[0], ZERO]
+        return {"A": list(I), "B": B, "C": [m, m, m, ZERO, ZERO, ZERO]}
+
+    def ai_add(self, x, y):
+        return {k: [self.add(a, b) for a, b in zip(x[k], y[k])] for k in ("A", "B", "C")}
+
+    def ai_apply(self, I, v):
+        A, B, C = I["A"], I["B"], I["C"]
+        a = [self.add(self.dot([self.sym(A, r, 0), self.sym(A, r, 1), self.sym(A, r, 2)], v[:3]),
+                      self.dot(B[3 * r:3 * r + 3], v[3:])) for r in range(3)]
+        l = [self.add(self.dot([B[r], B[3 + r], B[6 + r]], v[:3]),
+                      self.dot([self.sym(C, r, 0), self.sym(C, r, 1), self.sym(C, r, 2)], v[3:])) for r in range(3)]
+        return a + l
+
+    def sym_rotate(self, Q, s6):  # Q S Qᵀ
+        s = [[self.sym(s6, r, c) for c in range(3)] for r in range(3)]
+        t = [[self.dot(Q[3 * r:3 * r + 3], [s[0][c], s[1][c], s[2][c]]) for c in range(3)] for r in range(3)]
+        ir, ic = (0, 1, 2, 0, 0, 1), (0, 1, 2, 1, 2, 2)
+        return [self.dot(t[ir[k]], Q[3 * ic[k]:3 * ic[k] + 3]) for k in range(6)]
+
+    def full_rotate(self, Q, B):  # Q B Qᵀ
+        t = [[self.dot(Q[3 * r:3 * r + 3], [B[c], B[3 + c], B[6 + c]]) for c in range(3)] for r in range(3)]
+        return [self.dot(t[r], Q[3 * c:3 * c + 3]) for r in range(3) for c in range(3)]
+
+    def ai_out(self, I, Q, t):
+        """X* IA X*ᵀ for X = (Q, t) (vd_device.cuh ai_out)."""
+        o = {"A": self.sym_rotate(Q, I["A"]), "C": self.sym_rotate(Q, I["C"]), "B": self.full_rotate(Q, I["B"])}
+        if all(x.is0() for x in t):
+            return o
+        C1 = [[self.sym(o["C"], r, c) for c in range(3)] for r in range(3)]
+        B1 = o["B"]
+        PC = [[None] * 3 for _ in range(3)]
+        W = [[None] * 3 for _ in range(3)]
+        Z = [[None] * 3 for _ in range(3)]
+        for c in range(3):
+            PC[0][c] = self.sub(self.mul(t[1], C1[2][c]), self.mul(t[2], C1[1][c]))
+            PC[1][c] = self.sub(self.mul(t[2], C1[0][c]), self.mul(t[0], C1[2][c]))
+            PC[2][c] = self.sub(self.mul(t[0], C1[1][c]), self.mul(t[1], C1[0][c]))
+        for c in range(3):
+            W[0][c] = self.sub(self.mul(t[1], B1[c * 3 + 2]), self.mul(t[2], B1[c * 3 + 1]))
+            W[1][c] = self.sub(self.mul(t[2], B1[c * 3 + 0]), self.mul(t[0], B1[c * 3 + 2]))
+            W[2][c] = self.sub(self.mul(t[0], B1[c * 3 + 1]), self.mul(t[1], B1[c * 3 + 0]))
+        for r in range(3):
+            Z[r][0] = self.sub(self.mul(PC[r][1], t[2]), self.mul(PC[r][2], t[1]))
+            Z[r][1] = self.sub(self.mul(PC[r][2], t[0]), self.mul(PC[r][0], t[2]))
+            Z[r][2] = self.sub(self.mul(PC[r][0], t[1]), self.mul(PC[r][1], t[0]))
+        ir, ic = (0, 1, 2, 0, 0, 1), (0, 1, 2, 1, 2, 2)
+        A = [self.add(o["A"][k], self.sub(self.add(W[ir[k]][ic[k]], W[ic[k]][ir[k]]), Z[ir[k]][ic[k]])) for k in range(6)]
+        B = [self.add(B1[3 * r + c], PC[r][c]) for r in range(3) for c in range(3)]
+        return {"A": A, "B": B, "C": o["C"]}
+
+
+class Robot:
+    def __init__(self, d):
+        self.d = d
+        self.n = d["n"]
+        self.parent = d["parent"]
+        self.kind = d["kind"]
+        self.children = [[] for _ in range(self.n)]
+        self.roots = []
+        for i, p in enumerate(self.parent):
+            (self.children[p] if p >= 0 else self.roots).append(i)
+
+    def axis(self, i):
+        return [K(v) for v in self.d["axis"][3 * i:3 * i + 3]]
+
+    def QO(self, i):
+        return [K(v) for v in self.d["R"][9 * i:9 * i + 9]]
+
+    def tO(self, i):
+        return [K(v) for v in self.d["p"][3 * i:3 * i + 3]]
+
+    def rb(self, i):
+        I = self.d["inertia"][10 * i:10 * i + 10]
+        return (K(I[0]), [K(v) for v in I[1:4]], [K(v) for v in I[4:10]])
+
+
+class Joint:
+    """X_i = X_off ∘ X_J(q) for one joint, built from its motion values
+    (c, s) (revolute) or q (prismatic)."""
+
+    def __init__(self, g, rb, i, cs=None, q=None):
+        self.g = g
+        self.i = i
+        self.prismatic = rb.kind[i] == 1
+        ax = rb.axis(i)
+        self.ax = ax
+        self.QO, self.tO = rb.QO(i), rb.tO(i)
+        if self.prismatic:
+            self.QJ = [ONE if k % 4 == 0 else ZERO for k in range(9)]
+            self.tJ = [g.mul(a, q) for a in ax]
+        else:
+            c, s = cs
+            self.tJ = [ZERO, ZERO, ZERO]
+            unit = [k for k in range(3) if not ax[k].is0()]
+            if len(unit) == 1 and abs(ax[unit[0]].c) == 1.0:
+                k = unit[0]
+                k1, k2 = (k + 1) % 3, (k + 2) % 3
+                sg = s if ax[k].c > 0 else g.neg(s)
+                Q = [ZERO] * 9
+                Q[k * 3 + k] = ONE
+                Q[k1 * 3 + k1] = c
+                Q[k2 * 3 + k2] = c
+                Q[k1 * 3 + k2] = g.neg(sg)
+                Q[k2 * 3 + k1] = sg
+                self.QJ = Q
+            else:  # Rodrigues (spatial.hpp:302-308)
+                omc = g.sub(ONE, c)
+                Q = [g.add(g.mul(g.mul(ax[r], ax[cc]), omc), c if r == cc else ZERO) for r in range(3) for cc in range(3)]
+                Q[1] = g.sub(Q[1], g.mul(ax[2], s))
+                Q[2] = g.add(Q[2], g.mul(ax[1], s))
+                Q[3] = g.add(Q[3], g.mul(ax[2], s))
+                Q[5] = g.sub(Q[5], g.mul(ax[0], s))
+                Q[6] = g.sub(Q[6], g.mul(ax[1], s))
+                Q[7] = g.add(Q[7], g.mul(ax[0], s))
+                self.QJ = Q
+
+    def motion_to_child(self, m):
+        g = self.g
+        return g.motion_in(self.QJ, self.tJ, g.motion_in(self.QO, self.tO, m))
+
+    def motion_to_parent(self, m):
+        g = self.g
+        return g.motion_out(self.QO, self.tO, g.motion_out(self.QJ, self.tJ, m))
+
+    def force_to_parent(self, f):
+        g = self.g
+        return g.force_out(self.QO, self.tO, g.force_out(self.QJ, self.tJ, f))
+
+    def ai_to_parent(self, I):
+        g = self.g
+        return g.ai_out(g.ai_out(I, self.QJ, self.tJ), self.QO, self.tO)
+
+    # motion subspace S: (axis, 0) revolute / (0, axis) prismatic
+    def S(self, x):
+        m = [self.g.mul(a, x) for a in self.ax]
+        return ([ZERO] * 3 + m) if self.prismatic else (m + [ZERO] * 3)
+
+    def Svec(self):
+        return ([ZERO] * 3 + self.ax) if self.prismatic else (self.ax + [ZERO] * 3)
+
+    def Sdot(self, f):
+        return self.g.dot(self.ax, f[3:] if self.prismatic else f[:3])
+
+
+def gen_aba(rb):
+    """Emit the ABA body.  Context cx provides q(i), qd(i), tau(i), g(k),
+    st(k, v) / get(k) for the pass-2 -> pass-3 state, qdd(i, v) for the
+    outputs and sync() at every joint step (kernels may keep the warps of a
+    block in lockstep there so they share instruction-cache lines)."""
+    g = Gen()
+    n = rb.n
+    nslot_box = [0]
+    layout = {}  # joint -> (slot of ud, slots of Ud[6], slots of motion)
+    mrefs, qdrefs, nonlocal_counts = {}, {}, {}
+
+    def joint_from(i, mref):
+        if mref[0] == "q":
+            return Joint(g, rb, i, q=load(mref[1]))
+        return Joint(g, rb, i, cs=(load(mref[1]), load(mref[2])))
+
+    def motion_vals(i):
+        qi = g.tmp(f"cx.q({i})", "q")
+        if rb.kind[i] == 1:
+            return None, qi
+        s = Ex(s=f"s{i}")
+        c = Ex(s=f"c{i}")
+        g.raw(f"T s{i}, c{i};")
+        g.raw(f"vd_sincos({qi.s}, &s{i}, &c{i});")
+        return (c, s), qi
+
+    def store(v):
+        if v.c is not None:
+            return ("k", v.c)
+        k = nslot_box[0]
+        nslot_box[0] += 1
+        g.raw(f"cx.st({k}, {v.s});")
+        return ("s", k)
+
+    def load(ref):
+        if ref[0] == "k":
+            return K(ref[1])
+        return g.tmp(f"cx.get({ref[1]})", "r")
+
+    def down_up(i, vp):
+        """Pass 1 at i, recursion into the children, pass 2 at i.  Returns
+        (contribution to the parent, v_parent reconstructed from v_i)."""
+        g.raw("cx.sync();")
+        mref = mrefs[i]
+        X = joint_from(i, mref)
+        qdi = load(qdrefs[i])
+        v = X.S(qdi) if vp is None else g.vadd(X.motion_to_child(vp), X.S(qdi))
+        # nothing of joint i but v stays live across its subtree: the motion
+        # values and q̇ are re-read from their slots for the pass-2 step
+        # children: contributions are summed as they arrive; v_i is not kept
+        # live across a child's subtree but rebuilt from the child's v
+        # (v_i = X_c (v_c − S_c q̇_c)), so only the current path velocity is live.
+        acc = None
+        for c in rb.children[i]:
+            (Ic, pc), v = down_up(c, v)
+            acc = (Ic, pc) if acc is None else (g.ai_add(acc[0], Ic), g.vadd(acc[1], pc))
+        if rb.children[i]:
+            g.raw("cx.sync();")
+            X = joint_from(i, mref)
+            qdi = load(qdrefs[i])
+        b = rb.rb(i)
+        IA = g.ai_from_rb(b)
+        pA = g.crf(v, g.rb_apply(b, v))
+        if acc is not None:
+            IA = g.ai_add(IA, acc[0])
+            pA = g.vadd(pA, acc[1])
+        U = g.ai_apply(IA, X.Svec())
+        D = X.Sdot(U)
+        g.raw(f"ok = ok && ({g.o(D)} > T(0));")
+        dinv = g.tmp(f"T(1) / {g.o(D)}", "di")
+        taui = g.tmp(f"cx.tau({i})", "ta")
+        u = g.sub(taui, X.Sdot(pA))
+        Ud = [g.mul(x, dinv) for x in U]
+        ud = g.mul(u, dinv)
+        layout[i] = (store(ud), [store(x) for x in Ud], mref)
+        if vp is None:
+            return None, None
+        c = g.crm(v, X.S(qdi))
+        # Ia = IA − U Udᵀ
+        ir, ic = (0, 1, 2, 0, 0, 1), (0, 1, 2, 1, 2, 2)
+        Ia = {"A": [g.sub(IA["A"][k], g.mul(U[ir[k]], Ud[ic[k]])) for k in range(6)],
+              "C": [g.sub(IA["C"][k], g.mul(U[3 + ir[k]], Ud[3 + ic[k]])) for k in range(6)],
+              "B": [g.sub(IA["B"][3 * r + cc], g.mul(U[r], Ud[3 + cc])) for r in range(3) for cc in range(3)]}
+        pa = g.vadd(g.vadd(pA, g.ai_apply(Ia, c)), [g.mul(x, u_) for x, u_ in zip(U, [ud] * 6)])
+        vpar = X.motion_to_parent(g.vsub(v, X.S(qdi)))
+        return (X.ai_to_parent(Ia), X.force_to_parent(pa)), vpar
+
+    g.raw("bool ok = true;")
+    # prologue: every joint's motion values (cos/sin or q) and q̇ are computed
+    # up front — n independent load -> sincos chains instead of n serialised
+    # ones — and parked in the first slots (the kernel keeps those on chip).
+    for i in range(n):
+        cs, qi = motion_vals(i)
+        mrefs[i] = ("q", store(qi)) if cs is None else ("cs", store(cs[0]), store(cs[1]))
+    for i in range(n):
+        qdrefs[i] = store(g.tmp(f"cx.qd({i})", "qd"))
+    nonlocal_counts["prologue"] = nslot_box[0]
+    for r in rb.roots:
+        down_up(r, None)
+
+    gvec = [ZERO, ZERO, ZERO, Ex(s="ga0"), Ex(s="ga1"), Ex(s="ga2")]
+    g.raw("const T ga0 = cx.g(0), ga1 = cx.g(1), ga2 = cx.g(2);")
+
+    def down(i, vp, ap):
+        g.raw("cx.sync();")
+        udr, Udr, mref = layout[i]
+        X = joint_from(i, mref)
+        qdi = load(qdrefs[i])
+        if vp is None:
+            v = X.S(qdi)
+            a1 = X.motion_to_child(gvec)
+        else:
+            v = g.vadd(X.motion_to_child(vp), X.S(qdi))
+            a1 = g.vadd(X.motion_to_child(ap), g.crm(v, X.S(qdi)))
+        ud = load(udr)
+        Ud = [load(r) for r in Udr]
+        qdd = g.sub(ud, g.sdot(Ud, a1))
+        g.raw(f"cx.qdd({i}, {g.o(qdd)});")
+        g.raw(f"ok = ok && vd_isfinite({g.o(qdd)});")
+        if rb.children[i]:
+            a = g.vadd(a1, X.S(qdd))
+            for c in rb.children[i]:
+                down(c, v, a)
+
+    for r in rb.roots:
+        down(r, None, None)
+    g.raw("return ok;")
+    return g, nslot_box[0], nonlocal_counts["prologue"]
+
+
+def emit(name, cls, rb):
+    g, nslot, npro = gen_aba(rb)
+    out = [f"// ---- {name}: ABA, {g.flops} flops (mul/add after folding), {nslot} state slots",
+           f"struct Gen{cls} {{",
+           f"  static constexpr int kN = {rb.n};",
+           f"  static constexpr int kAbaSlots = {nslot};",
+           f"  // slots [0, kAbaPrologue): cos/sin|q and q̇ of every joint, read in all three passes",
+           f"  static constexpr int kAbaPrologue = {npro};",
+           f"  static constexpr int kAbaFlops = {g.flops};",
+           f"  static constexpr uint64_t kFingerprint = {rb.d['fp']:#x}ull;",
+           "  template <class T, class Cx>",
+           "  VD_HD static bool aba(Cx& cx) {"]
+    out += ["  " + ln for ln in g.lines]
+    out += ["  }", "};", ""]
+    return out
+
+
+def generate(lib):
+    s = ["// GENERATED by tools/gen_tree_kernels.py from the library's own packed models",
+         "// (assets/*.urdf via vdi_model_packed).  Do not edit.  Straight-line, structure-folded",
+         "// per-robot routines; see the generator's docstring for the algorithm and its",
+         "// reference lines.",
+         "#pragma once", "", "#include <cmath>", "#include <cstdint>", "",
+         "#ifndef VD_HD", "#if defined(__CUDACC__)", "#define VD_HD __host__ __device__ __forceinline__",
+         "#else", "#define VD_HD inline", "#endif", "#endif", "",
+         "namespace vdk {", "",
+         "#if defined(__CUDA_ARCH__)",
+         "__device__ __forceinline__ void vd_sincos(double x, double* s, double* c) { sincos(x, s, c); }",
+         "__device__ __forceinline__ void vd_sincos(float x, float* s, float* c) { sincosf(x, s, c); }",
+         "template <class T> __device__ __forceinline__ bool vd_isfinite(T x) { return isfinite(x); }",
+         "#else",
+         "template <class T> inline void vd_sincos(T x, T* s, T* c) { *s = std::sin(x); *c = std::cos(x); }",
+         "template <class T> inline bool vd_isfinite(T x) { return std::isfinite(x); }",
+         "#endif", ""]
+    for name, cls in ROBOTS:
+        s += emit(name, cls, Robot(grt.packed(lib, name)))
+    s += ["}  // namespace vdk", ""]
+    return "\n".join(s)
+
+
+def main():
+    text = generate(grt.load_lib())
+    if "--check" in sys.argv:
+        cur = open(OUT).read() if os.path.exists(OUT) else ""
+        if cur != text:
+            print("vd_gen_robots.cuh is stale; run tools/gen_tree_kernels.py")
+            return 1
+        print("vd_gen_robots.cuh is up to date")
+        return 0
+    with open(OUT, "w") as f:
+        f.write(text)
+    print("wrote", OUT)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
