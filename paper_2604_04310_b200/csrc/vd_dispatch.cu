@@ -32,6 +32,7 @@ int match_spec(uint64_t fp, int n) { return match_spec_tables(fp, n); }
 
 int launch_fk(const Launch& L, const void* q, void* out) {
   if (L.N == 0) return 0;
+  if (const int rc = launch_gen_fk(L, q, out); rc >= 0) return rc;
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::fk(mv, L, q, out); });
 }
 
@@ -52,11 +53,15 @@ int launch_rnea(const Launch& L, int mode, const void* q, const void* qd, const 
   const double* g = (mode == 3) ? zero3 : g3;
   const void* qd_ = (mode == 2) ? nullptr : qd;
   const void* qdd_ = (mode == 0) ? qdd : nullptr;
+  if (!fext) {
+    if (const int rc = launch_gen_rnea(L, mode, q, qd, qdd, g3, tau); rc >= 0) return rc;
+  }
   return with_view<true>(L, [&](auto mv) { return Launcher<decltype(mv)>::rnea(mv, L, q, qd_, qdd_, g, fext, tau); });
 }
 
 int launch_crba(const Launch& L, const void* q, void* M) {
   if (L.N == 0) return 0;
+  if (const int rc = launch_gen_crba(L, q, M); rc >= 0) return rc;
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::crba(mv, L, q, M); });
 }
 
@@ -73,6 +78,15 @@ int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, 
 int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
                     void* bias, void* qdd, int32_t* status) {
   if (L.N == 0) return 0;
+  if (L.spec == kTree29) {
+    // generated kernels, one per output (each re-derives the joint
+    // transforms; cheaper than the fused loop kernel's local-memory state)
+    int rc = 0;
+    if (M && (rc = launch_gen_crba(L, q, M)) != 0) return rc;
+    if (bias && (rc = launch_gen_rnea(L, 1, q, qd, nullptr, g3, bias)) != 0) return rc;
+    if (qdd && (rc = launch_gen_aba(L, q, qd, tau, g3, qdd, status)) != 0) return rc;
+    return 0;
+  }
   return with_view(L,
                    [&](auto mv) { return Launcher<decltype(mv)>::dyn(mv, L, q, qd, tau, g3, M, bias, qdd, status); });
 }

@@ -63,82 +63,75 @@ struct GenMem<float> {
   }
 };
 
-template <class T, int kSlots, int kReg, int kSmem, int BS, bool kSync>
-struct GenAbaCx {
+template <class T, int kSlots, int kReg, int kSmem>
+struct GenCx {
   static constexpr int kGlobal = kSlots - kReg - kSmem > 0 ? kSlots - kReg - kSmem : 0;
-  const T* q_;   // &q[i]; element (i, j) at q_[j * ld]
-  const T* qd_;
-  const T* tau_;
-  T* out_;
-  T* sb;         // this thread's scratch: slot k at sb[(k - kSmem) * 32] (warp-interleaved)
-  uint32_t sm;   // shared address of slot 0 for this thread ([k][threadIdx.x])
+  const T* in_[3];  // &x_g[i]; element (i, j) of input g at in_[g][j * ld]
+  T* out_;          // &y[i]; element (i, k) at out_[k * ldo]
+  T* sb;            // this thread's scratch: slot k at sb[(k - kSmem) * 32] (warp-interleaved)
+  uint32_t sm;      // shared address of slot 0 for this thread ([k][threadIdx.x])
   int64_t ld, ldo;
-  bool active;   // false on the padding lanes of the last round (they compute, but write nothing)
+  bool active;      // false on the padding lanes of the last round (they compute, but write nothing)
   T g3[3];
   T reg[kReg > 0 ? kReg : 1];
-  __device__ __forceinline__ T q(int j) const { return GenMem<T>::ldg(q_ + j * ld); }
-  __device__ __forceinline__ T qd(int j) const { return GenMem<T>::ldg(qd_ + j * ld); }
-  __device__ __forceinline__ T tau(int j) const { return GenMem<T>::ldg(tau_ + j * ld); }
+  __device__ __forceinline__ T x(int g, int j) const { return GenMem<T>::ldg(in_[g] + j * ld); }
   __device__ __forceinline__ T g(int k) const { return g3[k]; }
   __device__ __forceinline__ void st(int k, T v) {
     if (k >= kSlots - kReg) reg[k - (kSlots - kReg)] = v;
-    else if (k < kSmem) GenMem<T>::sts(sm + (uint32_t)(k * BS * sizeof(T)), v);
+    else if (k < kSmem) GenMem<T>::sts(sm + (uint32_t)(k * kGenBlock * sizeof(T)), v);
     else GenMem<T>::stg(sb + (k - kSmem) * 32, v);
   }
   __device__ __forceinline__ T get(int k) const {
     if (k >= kSlots - kReg) return reg[k - (kSlots - kReg)];
-    if (k < kSmem) return GenMem<T>::lds(sm + (uint32_t)(k * BS * sizeof(T)));
+    if (k < kSmem) return GenMem<T>::lds(sm + (uint32_t)(k * kGenBlock * sizeof(T)));
     return GenMem<T>::ldgs(sb + (k - kSmem) * 32);
   }
-  __device__ __forceinline__ void qdd(int j, T v) const {
-    if (active) out_[j * ldo] = v;
-  }
-  __device__ __forceinline__ void sync() const {
-    if constexpr (kSync) __syncthreads();
+  __device__ __forceinline__ void y(int, int k, T v) const {
+    if (active) out_[k * ldo] = v;
   }
 };
 
 // Scratch elements per resident thread (0 when every slot is on chip).
-template <class R, class T, int kReg, int kSmem>
-constexpr int64_t gen_aba_scratch_per_thread() {
-  return GenAbaCx<T, R::kAbaSlots, kReg, kSmem, 32, false>::kGlobal;
+template <class Op, class T, int kReg, int kSmem>
+constexpr int64_t gen_scratch_per_thread() {
+  return GenCx<T, Op::kSlots, kReg, kSmem>::kGlobal;
 }
 
-template <class R, class T, int kReg, int kSmem, int kMinB, int BS = kGenBlock, bool kSync = false>
-__global__ void __launch_bounds__(BS, kMinB)
-    k_gen_aba(int64_t N, const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau, int64_t ldi,
-              T g0, T g1, T g2, T* __restrict__ qdd, int64_t ldo, int32_t* __restrict__ status,
-              T* __restrict__ scratch) {
+// One generated routine (Op = GenRobot::Aba / Rnea / RneaBias / RneaGrav /
+// Crba / Fk) over a persistent grid: every thread strides over the batch.
+template <class Op, class T, int kReg, int kSmem, int kMinB>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
+          T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status, T* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
-  using Cx = GenAbaCx<T, R::kAbaSlots, kReg, kSmem, BS, kSync>;
+  using Cx = GenCx<T, Op::kSlots, kReg, kSmem>;
   Cx cx;
-  const int64_t slot = (int64_t)blockIdx.x * BS + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * BS;
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
   cx.sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
   cx.sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
   cx.g3[0] = g0;
   cx.g3[1] = g1;
   cx.g3[2] = g2;
-  // every thread of a block runs the same number of rounds (barriers inside)
-  for (int64_t base = (int64_t)blockIdx.x * BS; base < N; base += stride) {
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride) {
     const int64_t i0 = base + threadIdx.x;
     cx.active = i0 < N;
     const int64_t i = cx.active ? i0 : N - 1;
     // launder the strides each round so the per-column addresses are not
-    // hoisted out of the loop (29 x 3 live 64-bit addresses otherwise spill)
+    // hoisted out of the loop (n x 3 live 64-bit addresses otherwise spill)
     int64_t ld, lo;
     asm volatile("mov.b64 %0, %1;" : "=l"(ld) : "l"(ldi));
     asm volatile("mov.b64 %0, %1;" : "=l"(lo) : "l"(ldo));
     cx.ld = ld;
     cx.ldo = lo;
-    cx.q_ = q + i;
-    cx.qd_ = qd + i;
-    cx.tau_ = tau + i;
-    cx.out_ = qdd + i;
-    const bool ok = R::template aba<T>(cx);
+    cx.in_[0] = x0 + i;
+    cx.in_[1] = (Op::kIn > 1 ? x1 : x0) + i;
+    cx.in_[2] = (Op::kIn > 2 ? x2 : x0) + i;
+    cx.out_ = y + i;
+    const bool ok = Op::template run<T>(cx);
     if (cx.active) {
       if (!ok) {
-        for (int j = 0; j < R::kN; ++j) qdd[(int64_t)j * ldo + i] = T(0);
+        for (int j = 0; j < Op::kOut; ++j) y[(int64_t)j * ldo + i] = T(0);
       }
       if (status) status[i] = ok ? 0 : 7;
     }

@@ -1,7 +1,8 @@
-// Launchers for the generated straight-line robot kernels (vd_gen_kernels.cuh).
-// tree29 (G1) ABA runs here: the fully unrolled template kernel is dominated
-// by flag/select overhead and the loop kernel by local-memory state (see
-// DESIGN.md "Generated kernels").
+// Launchers for the generated straight-line robot kernels (vd_gen_kernels.cuh,
+// tools/gen_tree_kernels.py).  tree29 (G1) ABA, RNEA (+ bias / gravity /
+// Coriolis), CRBA and FK run here: the fully unrolled template kernels are
+// dominated by flag/select overhead and the loop kernels by local-memory
+// state.
 #include <algorithm>
 #include <mutex>
 
@@ -11,42 +12,46 @@
 namespace vdk {
 namespace {
 
-// Per-dtype placement of the 267 pass-2 -> pass-3 state slots (ablib/gen_sweep.cu
-// on B200): fp64 keeps the last 40 slots in registers and the first 110 (the
-// prologue's cos/sin/q̇ of every joint + the first leg) in shared memory at 2
-// CTAs/SM; fp32 puts 110 slots in shared memory at 4 CTAs/SM.
-template <class T>
-struct GenAbaCfg;
+// Slot placement and CTAs/SM per (op, dtype), from ablib/gen_sweep*.cu on a
+// B200 (kReg: last slots kept in registers; kSmem: first slots in shared
+// memory; the rest in the L2-resident scratch slab).
+template <class Op, class T>
+struct Cfg {
+  static constexpr int kReg = 0, kSmem = Op::kSlots < 55 ? Op::kSlots : 55, kMinB = sizeof(T) == 8 ? 3 : 4;
+};
 template <>
-struct GenAbaCfg<double> {
+struct Cfg<GenTree29::Aba, double> {
   static constexpr int kReg = 40, kSmem = 110, kMinB = 2;
 };
 template <>
-struct GenAbaCfg<float> {
+struct Cfg<GenTree29::Aba, float> {
   static constexpr int kReg = 0, kSmem = 110, kMinB = 4;
+};
+template <>
+struct Cfg<GenTree29::Crba, double> {
+  static constexpr int kReg = 0, kSmem = 40, kMinB = 4;
 };
 
 struct Occ {
   int blocks_per_sm = 0, sms = 0;
 };
 
-template <class R, class T>
-int launch_gen_aba_t(const Launch& L, const T* q, const T* qd, const T* tau, const double* g3, T* qdd,
-                     int32_t* status) {
-  using C = GenAbaCfg<T>;
-  auto kern = k_gen_aba<R, T, C::kReg, C::kSmem, C::kMinB>;
+template <class Op, class T>
+int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
+             int32_t* status) {
+  using C = Cfg<Op, T>;
+  auto kern = k_gen<Op, T, C::kReg, C::kSmem, C::kMinB>;
   constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
-  static std::once_flag once;
-  static Occ occ[64];
   static std::mutex mu;
+  static Occ occ[64];
   int dev = 0;
   cudaGetDevice(&dev);
-  std::call_once(once, [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
   Occ o;
   {
     std::lock_guard<std::mutex> lk(mu);
     Occ& c = occ[dev & 63];
     if (!c.blocks_per_sm) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.blocks_per_sm, kern, kGenBlock, smem);
       if (c.blocks_per_sm < 1) c.blocks_per_sm = 1;
@@ -58,7 +63,7 @@ int launch_gen_aba_t(const Launch& L, const T* q, const T* qd, const T* tau, con
   // L2-resident scratch for the slots that are neither in registers nor in
   // shared memory: one slab per resident thread, stream-ordered from the
   // device's memory pool (no synchronisation, safe for concurrent streams).
-  const size_t scratch_bytes = (size_t)blocks * kGenBlock * gen_aba_scratch_per_thread<R, T, C::kReg, C::kSmem>() * sizeof(T);
+  const size_t scratch_bytes = (size_t)blocks * kGenBlock * gen_scratch_per_thread<Op, T, C::kReg, C::kSmem>() * sizeof(T);
   T* scratch = nullptr;
   if (scratch_bytes) {
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_bytes, s);
@@ -66,10 +71,18 @@ int launch_gen_aba_t(const Launch& L, const T* q, const T* qd, const T* tau, con
   }
   // gravity3 == NULL: GravitySpec::standard() (dynamics.hpp:39-50), as g3_of
   const T g0 = g3 ? T(g3[0]) : T(0), g1 = g3 ? T(g3[1]) : T(0), g2 = g3 ? T(g3[2]) : T(9.81);
-  kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, q, qd, tau, L.ld_in, g0, g1, g2, qdd, L.ld_out, status, scratch);
+  kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, (const T*)x0, (const T*)x1, (const T*)x2, L.ld_in, g0, g1, g2,
+                                                 (T*)y, L.ld_out, status, scratch);
   cudaError_t e = cudaGetLastError();
   if (scratch) cudaFreeAsync(scratch, s);
   return (int)e;
+}
+
+template <class Op>
+int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
+              int32_t* status) {
+  return L.dtype == 0 ? launch_t<Op, double>(L, x0, x1, x2, g3, y, status)
+                      : launch_t<Op, float>(L, x0, x1, x2, g3, y, status);
 }
 
 }  // namespace
@@ -77,11 +90,31 @@ int launch_gen_aba_t(const Launch& L, const T* q, const T* qd, const T* tau, con
 int launch_gen_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* qdd,
                    int32_t* status) {
   if (L.spec != kTree29) return -1;
-  if (L.dtype == 0)
-    return launch_gen_aba_t<GenTree29, double>(L, (const double*)q, (const double*)qd, (const double*)tau, g3,
-                                               (double*)qdd, status);
-  return launch_gen_aba_t<GenTree29, float>(L, (const float*)q, (const float*)qd, (const float*)tau, g3, (float*)qdd,
-                                            status);
+  return launch_op<GenTree29::Aba>(L, q, qd, tau, g3, qdd, status);
+}
+
+int launch_gen_rnea(const Launch& L, int mode, const void* q, const void* qd, const void* qdd, const double* g3,
+                    void* tau) {
+  if (L.spec != kTree29) return -1;
+  // mode 0 full, 1 bias (q̈ = 0), 2 gravity (q̇ = q̈ = 0), 3 Coriolis (q̈ = 0, g = 0);
+  // a NULL q̇ / q̈ means zeros, as in the template kernels
+  static const double zero3[3] = {0, 0, 0};
+  const bool has_qd = mode != 2 && qd, has_qdd = mode == 0 && qdd;
+  const double* g = mode == 3 ? zero3 : g3;
+  if (has_qd && has_qdd) return launch_op<GenTree29::Rnea>(L, q, qd, qdd, g, tau, nullptr);
+  if (has_qd) return launch_op<GenTree29::RneaBias>(L, q, qd, nullptr, g, tau, nullptr);
+  if (!has_qdd) return launch_op<GenTree29::RneaGrav>(L, q, nullptr, nullptr, g, tau, nullptr);
+  return -1;  // q̇ = 0 with q̈: no generated variant, template kernel
+}
+
+int launch_gen_crba(const Launch& L, const void* q, void* M) {
+  if (L.spec != kTree29) return -1;
+  return launch_op<GenTree29::Crba>(L, q, nullptr, nullptr, nullptr, M, nullptr);
+}
+
+int launch_gen_fk(const Launch& L, const void* q, void* frames) {
+  if (L.spec != kTree29) return -1;
+  return launch_op<GenTree29::Fk>(L, q, nullptr, nullptr, nullptr, frames, nullptr);
 }
 
 }  // namespace vdk

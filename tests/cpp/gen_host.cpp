@@ -9,48 +9,49 @@
 namespace {
 template <class T>
 struct HostCx {
-  const T *Q, *QD, *TAU;
+  const T* X[3];
   const double* G;
-  T* OUT;
+  T* Y;
   long ld, i;
   T* slots;
-  T q(int j) const { return Q[j * ld + i]; }
-  T qd(int j) const { return QD[j * ld + i]; }
-  T tau(int j) const { return TAU[j * ld + i]; }
+  T x(int g, int j) const { return X[g][j * ld + i]; }
   T g(int k) const { return T(G[k]); }
   void st(int k, T v) { slots[k] = v; }
   T get(int k) const { return slots[k]; }
-  void qdd(int j, T v) const { OUT[j * ld + i] = v; }
-  void sync() const {}
+  void y(int, int k, T v) const { Y[k * ld + i] = v; }
 };
-template <class R, class T>
-int run(long N, const T* q, const T* qd, const T* tau, const double* g, T* out, int* status) {
-  std::vector<T> slots(R::kAbaSlots + 1);
+template <class Op, class T>
+int run(long N, const void* const* x, const double* g, void* y, int* status) {
+  std::vector<T> slots(Op::kSlots + 1);
   int bad = 0;
   for (long i = 0; i < N; ++i) {
-    HostCx<T> cx{q, qd, tau, g, out, N, i, slots.data()};
-    const bool ok = R::template aba<T>(cx);
+    HostCx<T> cx{{(const T*)x[0], (const T*)x[1], (const T*)x[2]}, g, (T*)y, N, i, slots.data()};
+    const bool ok = Op::template run<T>(cx);
     status[i] = ok ? 0 : 7;
     bad += !ok;
   }
   return bad;
 }
+template <class R, class T>
+int run_op(int op, long N, const void* const* x, const double* g, void* y, int* status) {
+  switch (op) {
+    case 0: return run<typename R::Aba, T>(N, x, g, y, status);
+    case 1: return run<typename R::Rnea, T>(N, x, g, y, status);
+    case 2: return run<typename R::RneaBias, T>(N, x, g, y, status);
+    case 3: return run<typename R::RneaGrav, T>(N, x, g, y, status);
+    case 4: return run<typename R::Crba, T>(N, x, g, y, status);
+    default: return run<typename R::Fk, T>(N, x, g, y, status);
+  }
+}
 }  // namespace
 
-extern "C" int gen_aba_host(int robot, int f32, long N, const void* q, const void* qd, const void* tau,
-                            const double* g, void* out, int* status) {
-  if (f32) {
-    auto f = [&](auto r) {
-      return run<decltype(r), float>(N, (const float*)q, (const float*)qd, (const float*)tau, g, (float*)out, status);
-    };
-    return robot == 2 ? f(vdk::GenTree29{}) : f(vdk::GenChain7{});
-  }
-  auto d = [&](auto r) {
-    return run<decltype(r), double>(N, (const double*)q, (const double*)qd, (const double*)tau, g, (double*)out,
-                                    status);
-  };
-  return robot == 2 ? d(vdk::GenTree29{}) : d(vdk::GenChain7{});
-}
-extern "C" unsigned long long gen_fingerprint(int robot) {
-  return robot == 2 ? vdk::GenTree29::kFingerprint : vdk::GenChain7::kFingerprint;
+// op: 0 aba, 1 rnea, 2 bias, 3 gravity, 4 crba, 5 fk; robot: 1 chain7, 2 tree29
+extern "C" int gen_run_host(int robot, int op, int f32, long N, const void* x0, const void* x1, const void* x2,
+                            const double* g, void* y, int* status) {
+  const void* x[3] = {x0, x1 ? x1 : x0, x2 ? x2 : x0};
+  if (robot == 2)
+    return f32 ? run_op<vdk::GenTree29, float>(op, N, x, g, y, status)
+               : run_op<vdk::GenTree29, double>(op, N, x, g, y, status);
+  return f32 ? run_op<vdk::GenChain7, float>(op, N, x, g, y, status)
+             : run_op<vdk::GenChain7, double>(op, N, x, g, y, status);
 }

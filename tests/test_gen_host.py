@@ -24,9 +24,21 @@ def genlib(tmp_path_factory):
     subprocess.run(["g++", "-O1", "-march=x86-64-v3", "-ffp-contract=fast", "-std=c++20", "-shared", "-fPIC", "-I", CSRC,
                     os.path.join(ROOT, "tests", "cpp", "gen_host.cpp"), "-o", so], check=True)
     L = ctypes.CDLL(so)
-    L.gen_aba_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 6
-    L.gen_fingerprint.restype = ctypes.c_ulonglong
+    L.gen_run_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 6
     return L
+
+
+def _run(L, robot, op, xs, nout, g=(0.0, 0.0, 9.81), f32=False):
+    """op: 0 aba, 1 rnea, 2 bias, 3 gravity, 4 crba, 5 fk (gen_host.cpp)."""
+    dt = np.float32 if f32 else np.float64
+    X = [np.asfortranarray(a.astype(dt)) for a in xs]
+    N = X[0].shape[0]
+    Y = np.zeros((N, nout), dtype=dt, order="F")
+    st = np.zeros(N, dtype=np.int32)
+    ptrs = [_p(a) for a in X] + [None] * (3 - len(X))
+    ga = np.asarray(g, dtype=np.float64)
+    bad = L.gen_run_host(robot, op, int(f32), N, *ptrs, _p(ga), _p(Y), _p(st))
+    return Y.astype(np.float64), st, bad
 
 
 def _p(a):
@@ -47,12 +59,7 @@ def test_generated_aba_matches_oracle(genlib, name, code, f32):
     om = Model.builtin(name)
     N = 2048
     q, qd, _, tau = om.random_states(N, 2604 + code, True, True)
-    dt = np.float32 if f32 else np.float64
-    Q, QD, TA = (np.asfortranarray(a.astype(dt)) for a in (q, qd, tau))
-    out = np.zeros_like(Q, order="F")
-    st = np.zeros(N, dtype=np.int32)
-    g = np.array([0.0, 0.0, 9.81])
-    bad = genlib.gen_aba_host(code, int(f32), N, _p(Q), _p(QD), _p(TA), _p(g), _p(out), _p(st))
+    out, st, bad = _run(genlib, code, 0, (q, qd, tau), om.n, f32=f32)
     assert bad == 0
     ref, rst = om.forward_dynamics(q, qd, tau)
     assert np.all(rst == 0)
@@ -77,9 +84,40 @@ def test_generated_aba_with_gravity_roundtrip(genlib):
     q, qd, qdd, _ = om.random_states(N, 77, True, False)
     g = np.array([0.3, -0.4, 9.0])
     tau = om.rnea(q, qd, qdd, gravity=tuple(g))
-    out = np.zeros_like(q, order="F")
-    st = np.zeros(N, dtype=np.int32)
-    Q, QD, TA = (np.asfortranarray(a) for a in (q, qd, tau))
-    assert genlib.gen_aba_host(2, 0, N, _p(Q), _p(QD), _p(TA), _p(g), _p(out), _p(st)) == 0
+    out, st, bad = _run(genlib, 2, 0, (q, qd, tau), om.n, g=g)
+    assert bad == 0
     cosb = np.abs(np.cos(q[:, 4]))
     assert rel_err(out, qdd, axis=1)[cosb > 0.05].max() <= 1e-8
+
+
+@pytest.mark.parametrize("name,code", [("chain7", 1), ("tree29", 2)])
+@pytest.mark.parametrize("f32", [False, True])
+def test_generated_rnea_family(genlib, name, code, f32):
+    """rnea / bias / gravity (dynamics.hpp:222-267, 403-416, 434-435)."""
+    om = Model.builtin(name)
+    q, qd, qdd, _ = om.random_states(1024, 11 + code, True, False)
+    tol = 1e-4 if f32 else 1e-10
+    g = (0.3, -0.4, 9.0)
+    got, _, _ = _run(genlib, code, 1, (q, qd, qdd), om.n, g=g, f32=f32)
+    assert rel_err(got, om.rnea(q, qd, qdd, gravity=g), axis=1).max() <= tol
+    z = np.zeros_like(q)
+    got, _, _ = _run(genlib, code, 2, (q, qd), om.n, f32=f32)
+    assert rel_err(got, om.rnea(q, qd, z), axis=1).max() <= tol
+    got, _, _ = _run(genlib, code, 3, (q,), om.n, f32=f32)
+    assert rel_err(got, om.rnea(q, z, z), axis=1).max() <= tol
+
+
+@pytest.mark.parametrize("name,code", [("chain7", 1), ("tree29", 2)])
+def test_generated_crba_and_fk(genlib, name, code):
+    """crba (dynamics.hpp:341-365; exact zeros between branches) and
+    forward_kinematics (kinematics.hpp:43-56)."""
+    om = Model.builtin(name)
+    n = om.n
+    q, _, _, _ = om.random_states(1024, 21 + code, True, False)
+    M, _, _ = _run(genlib, code, 4, (q,), n * n)
+    ref = om.crba(q).transpose(0, 2, 1).reshape(len(q), -1)  # plane c·n + r = M(r, c)
+    assert rel_err(M, ref, axis=1).max() <= 1e-10
+    structural = np.all(ref == 0, axis=0)  # off-branch entries: zero for every state
+    assert np.all(M[:, structural] == 0)  # exact zeros between branches, as in the reference
+    F, _, _ = _run(genlib, code, 5, (q,), 12 * n)
+    assert rel_err(F, om.fk(q).reshape(len(q), -1), axis=1).max() <= 1e-10

@@ -1,0 +1,87 @@
+// Placement/occupancy sweep of the generated kernels (tools/gen_tree_kernels.py) on one GPU.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr -Ipaper_2604_04310_b200/csrc tools/gen_sweep.cu -o ablib/gen_sweep
+#include <cstdio>
+#include <cstring>
+#include <vector>
+#include <cmath>
+#include "vd_gen_kernels.cuh"
+using namespace vdk;
+static const char* g_filter = nullptr;
+template <class T>
+__global__ void k_fill(T* p, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t x = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 31;
+    p[i] = T((double)(x >> 11) * (1.0 / 9007199254740992.0) * 6.283185307179586 - 3.141592653589793);
+  }
+}
+template <class Op, class T, int kReg, int kSmem, int kMinB>
+void run(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, int n) {
+  if (g_filter && !strstr(name, g_filter)) return;
+  auto kern = k_gen<Op, T, kReg, kSmem, kMinB>;
+  size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int bps = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int64_t grid = (int64_t)sms * bps;
+  if ((size_t)(grid * kGenBlock * gen_scratch_per_thread<Op, T, kReg, kSmem>() * sizeof(T)) > cap) { printf("%s scratch\n", name); return; }
+  cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  const T* x0 = x; const T* x1 = x + N * n; const T* x2 = x + 2 * N * n;
+  for (int w = 0; w < 3; ++w) kern<<<grid, kGenBlock, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch);
+  cudaEventRecord(a);
+  const int reps = 20;
+  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch);
+  cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms = 0; cudaEventElapsedTime(&ms, a, b); ms /= reps;
+  double bytes = (double)N * (Op::kIn * n + Op::kOut) * sizeof(T);
+  printf("%-26s regs %3d lmem %4zu smem %6zu b/SM %d  %.4f ms  %.3e evals/s  %6.2f TF(gen)  %6.0f GB/s  %s\n", name, fa.numRegs,
+         fa.localSizeBytes, smem, bps, ms, N / (ms * 1e-3), (double)Op::kFlops * N / (ms * 1e-3) / 1e12, bytes / (ms * 1e-3) / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
+}
+int main(int argc, char** argv) {
+  if (argc > 1) g_filter = argv[1];
+  size_t cap = 1ull << 31;
+  const int64_t N = 262144; const int n = 29;
+  double *xd, *yd, *sd; float *xf, *yf, *sf; int32_t* st;
+  cudaMalloc(&xd, 3 * N * n * 8); cudaMalloc(&yd, N * n * n * 8); cudaMalloc(&sd, cap); cudaMalloc(&st, N * 4);
+  k_fill<<<1024, 256>>>(xd, 3 * N * n, 1);
+  using R = GenTree29;
+  run<R::Rnea, double, 0, 55, 2>("t29 rnea f64 s55 b2", N, xd, yd, st, sd, cap, n);
+  run<R::Rnea, double, 0, 55, 3>("t29 rnea f64 s55 b3", N, xd, yd, st, sd, cap, n);
+  run<R::Rnea, double, 0, 0, 3>("t29 rnea f64 s0 b3", N, xd, yd, st, sd, cap, n);
+  run<R::Rnea, double, 0, 0, 4>("t29 rnea f64 s0 b4", N, xd, yd, st, sd, cap, n);
+  run<R::Rnea, double, 0, 40, 4>("t29 rnea f64 s40 b4", N, xd, yd, st, sd, cap, n);
+  run<R::RneaBias, double, 0, 55, 3>("t29 bias f64 s55 b3", N, xd, yd, st, sd, cap, n);
+  run<R::RneaGrav, double, 0, 55, 3>("t29 grav f64 s55 b3", N, xd, yd, st, sd, cap, n);
+  run<R::Crba, double, 0, 55, 2>("t29 crba f64 s55 b2", N, xd, yd, st, sd, cap, n);
+  run<R::Crba, double, 0, 55, 3>("t29 crba f64 s55 b3", N, xd, yd, st, sd, cap, n);
+  run<R::Crba, double, 0, 0, 4>("t29 crba f64 s0 b4", N, xd, yd, st, sd, cap, n);
+  run<R::Crba, double, 0, 40, 4>("t29 crba f64 s40 b4", N, xd, yd, st, sd, cap, n);
+  run<R::Fk, double, 0, 55, 3>("t29 fk f64 s55 b3", N, xd, yd, st, sd, cap, n);
+  run<R::Fk, double, 0, 0, 4>("t29 fk f64 s0 b4", N, xd, yd, st, sd, cap, n);
+  run<R::Fk, double, 0, 40, 4>("t29 fk f64 s40 b4", N, xd, yd, st, sd, cap, n);
+  run<R::Fk, double, 55, 0, 3>("t29 fk f64 r55 b3", N, xd, yd, st, sd, cap, n);
+  cudaMalloc(&xf, 3 * N * n * 4); cudaMalloc(&yf, N * n * n * 4); cudaMalloc(&sf, cap);
+  k_fill<<<1024, 256>>>(xf, 3 * N * n, 1);
+  run<R::Rnea, float, 0, 55, 3>("t29 rnea f32 s55 b3", N, xf, yf, st, sf, cap, n);
+  run<R::Rnea, float, 0, 55, 4>("t29 rnea f32 s55 b4", N, xf, yf, st, sf, cap, n);
+  run<R::Rnea, float, 55, 0, 3>("t29 rnea f32 r55 b3", N, xf, yf, st, sf, cap, n);
+  run<R::Crba, float, 0, 55, 4>("t29 crba f32 s55 b4", N, xf, yf, st, sf, cap, n);
+  run<R::Crba, float, 55, 0, 3>("t29 crba f32 r55 b3", N, xf, yf, st, sf, cap, n);
+  run<R::Fk, float, 0, 55, 4>("t29 fk f32 s55 b4", N, xf, yf, st, sf, cap, n);
+  run<R::Fk, float, 55, 0, 4>("t29 fk f32 r55 b4", N, xf, yf, st, sf, cap, n);
+  // chain7 (N = 4M) vs the template kernels
+  const int64_t N7 = 4194304;
+  double *x7, *y7; cudaMalloc(&x7, 3 * N7 * 7 * 8); cudaMalloc(&y7, N7 * 49 * 8);
+  cudaFree(st); cudaMalloc(&st, N7 * 4);
+  k_fill<<<1024, 256>>>(x7, 3 * N7 * 7, 2);
+  using C = GenChain7;
+  run<C::Aba, double, C::Aba::kSlots, 0, 3>("c7 aba f64 allreg b3", N7, x7, y7, st, sd, cap, 7);
+  run<C::Rnea, double, 14, 0, 3>("c7 rnea f64 r14 b3", N7, x7, y7, st, sd, cap, 7);
+  run<C::Rnea, double, 14, 0, 4>("c7 rnea f64 r14 b4", N7, x7, y7, st, sd, cap, 7);
+  run<C::Crba, double, 14, 0, 4>("c7 crba f64 r14 b4", N7, x7, y7, st, sd, cap, 7);
+  run<C::Fk, double, 14, 0, 4>("c7 fk f64 r14 b4", N7, x7, y7, st, sd, cap, 7);
+  return 0;
+}

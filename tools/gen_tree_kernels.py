@@ -348,66 +348,83 @@ class Joint:
         return self.g.dot(self.ax, f[3:] if self.prismatic else f[:3])
 
 
-def gen_aba(rb):
-    """Emit the ABA body.  Context cx provides q(i), qd(i), tau(i), g(k),
-    st(k, v) / get(k) for the pass-2 -> pass-3 state, qdd(i, v) for the
-    outputs and sync() at every joint step (kernels may keep the warps of a
-    block in lockstep there so they share instruction-cache lines)."""
-    g = Gen()
-    n = rb.n
-    nslot_box = [0]
-    layout = {}  # joint -> (slot of ud, slots of Ud[6], slots of motion)
-    mrefs, qdrefs, nonlocal_counts = {}, {}, {}
+class Algo:
+    """Shared emission state of one generated routine: the symbolic
+    generator, slot allocation (cx.st / cx.get) and the prologue that parks
+    every joint's motion values (cos/sin, or q for prismatic joints) and,
+    optionally, q̇ in the first slots."""
 
-    def joint_from(i, mref):
-        if mref[0] == "q":
-            return Joint(g, rb, i, q=load(mref[1]))
-        return Joint(g, rb, i, cs=(load(mref[1]), load(mref[2])))
+    def __init__(self, rb, with_qd_slots):
+        self.rb = rb
+        self.g = Gen()
+        self.nslot = 0
+        self.mrefs, self.qdrefs = {}, {}
+        g = self.g
+        g.raw("bool ok = true;")
+        # n independent load -> sincos chains instead of n serialised ones
+        for i in range(rb.n):
+            qi = g.tmp(f"cx.x(0, {i})", "q")
+            if rb.kind[i] == 1:
+                self.mrefs[i] = ("q", self.store(qi))
+            else:
+                g.raw(f"T s{i}, c{i};")
+                g.raw(f"vd_sincos({qi.s}, &s{i}, &c{i});")
+                self.mrefs[i] = ("cs", self.store(Ex(s=f"c{i}")), self.store(Ex(s=f"s{i}")))
+        if with_qd_slots:
+            for i in range(rb.n):
+                self.qdrefs[i] = self.store(g.tmp(f"cx.x(1, {i})", "qd"))
+        self.nprologue = self.nslot
 
-    def motion_vals(i):
-        qi = g.tmp(f"cx.q({i})", "q")
-        if rb.kind[i] == 1:
-            return None, qi
-        s = Ex(s=f"s{i}")
-        c = Ex(s=f"c{i}")
-        g.raw(f"T s{i}, c{i};")
-        g.raw(f"vd_sincos({qi.s}, &s{i}, &c{i});")
-        return (c, s), qi
-
-    def store(v):
+    def store(self, v):
         if v.c is not None:
             return ("k", v.c)
-        k = nslot_box[0]
-        nslot_box[0] += 1
-        g.raw(f"cx.st({k}, {v.s});")
+        k = self.nslot
+        self.nslot += 1
+        self.g.raw(f"cx.st({k}, {v.s});")
         return ("s", k)
 
-    def load(ref):
+    def load(self, ref):
         if ref[0] == "k":
             return K(ref[1])
-        return g.tmp(f"cx.get({ref[1]})", "r")
+        return self.g.tmp(f"cx.get({ref[1]})", "r")
+
+    def joint(self, i):
+        m = self.mrefs[i]
+        if m[0] == "q":
+            return Joint(self.g, self.rb, i, q=self.load(m[1]))
+        return Joint(self.g, self.rb, i, cs=(self.load(m[1]), self.load(m[2])))
+
+    def gravity(self):
+        self.g.raw("const T ga0 = cx.g(0), ga1 = cx.g(1), ga2 = cx.g(2);")
+        return [ZERO, ZERO, ZERO, Ex(s="ga0"), Ex(s="ga1"), Ex(s="ga2")]
+
+    def finish(self):
+        self.g.raw("return ok;")
+        return self
+
+
+def gen_aba(rb):
+    """ABA (Featherstone RBDA Table 7.1; oracle forward_dynamics,
+    dynamics.hpp:421-444).  x(0) = q, x(1) = q̇, x(2) = τ; y(0, i) = q̈_i.
+
+    Pass 1 and pass 2 run as one DFS (only the current root->leaf velocity is
+    live; a parent's velocity is rebuilt from its child, v_p = X(v − S q̇));
+    the pass-2 -> pass-3 state per joint (U/D, u/D) goes to slots."""
+    A = Algo(rb, True)
+    g = A.g
+    layout = {}
 
     def down_up(i, vp):
-        """Pass 1 at i, recursion into the children, pass 2 at i.  Returns
-        (contribution to the parent, v_parent reconstructed from v_i)."""
-        g.raw("cx.sync();")
-        mref = mrefs[i]
-        X = joint_from(i, mref)
-        qdi = load(qdrefs[i])
+        X = A.joint(i)
+        qdi = A.load(A.qdrefs[i])
         v = X.S(qdi) if vp is None else g.vadd(X.motion_to_child(vp), X.S(qdi))
-        # nothing of joint i but v stays live across its subtree: the motion
-        # values and q̇ are re-read from their slots for the pass-2 step
-        # children: contributions are summed as they arrive; v_i is not kept
-        # live across a child's subtree but rebuilt from the child's v
-        # (v_i = X_c (v_c − S_c q̇_c)), so only the current path velocity is live.
         acc = None
         for c in rb.children[i]:
             (Ic, pc), v = down_up(c, v)
             acc = (Ic, pc) if acc is None else (g.ai_add(acc[0], Ic), g.vadd(acc[1], pc))
-        if rb.children[i]:
-            g.raw("cx.sync();")
-            X = joint_from(i, mref)
-            qdi = load(qdrefs[i])
+        if rb.children[i]:  # re-read instead of keeping them live across the subtree
+            X = A.joint(i)
+            qdi = A.load(A.qdrefs[i])
         b = rb.rb(i)
         IA = g.ai_from_rb(b)
         pA = g.crf(v, g.rb_apply(b, v))
@@ -418,54 +435,38 @@ def gen_aba(rb):
         D = X.Sdot(U)
         g.raw(f"ok = ok && ({g.o(D)} > T(0));")
         dinv = g.tmp(f"T(1) / {g.o(D)}", "di")
-        taui = g.tmp(f"cx.tau({i})", "ta")
+        taui = g.tmp(f"cx.x(2, {i})", "ta")
         u = g.sub(taui, X.Sdot(pA))
         Ud = [g.mul(x, dinv) for x in U]
         ud = g.mul(u, dinv)
-        layout[i] = (store(ud), [store(x) for x in Ud], mref)
+        layout[i] = (A.store(ud), [A.store(x) for x in Ud])
         if vp is None:
             return None, None
         c = g.crm(v, X.S(qdi))
-        # Ia = IA − U Udᵀ
-        ir, ic = (0, 1, 2, 0, 0, 1), (0, 1, 2, 1, 2, 2)
+        ir, ic = (0, 1, 2, 0, 0, 1), (0, 1, 2, 1, 2, 2)  # Ia = IA − U Udᵀ
         Ia = {"A": [g.sub(IA["A"][k], g.mul(U[ir[k]], Ud[ic[k]])) for k in range(6)],
               "C": [g.sub(IA["C"][k], g.mul(U[3 + ir[k]], Ud[3 + ic[k]])) for k in range(6)],
               "B": [g.sub(IA["B"][3 * r + cc], g.mul(U[r], Ud[3 + cc])) for r in range(3) for cc in range(3)]}
-        pa = g.vadd(g.vadd(pA, g.ai_apply(Ia, c)), [g.mul(x, u_) for x, u_ in zip(U, [ud] * 6)])
+        pa = g.vadd(g.vadd(pA, g.ai_apply(Ia, c)), [g.mul(x, ud) for x in U])
         vpar = X.motion_to_parent(g.vsub(v, X.S(qdi)))
         return (X.ai_to_parent(Ia), X.force_to_parent(pa)), vpar
 
-    g.raw("bool ok = true;")
-    # prologue: every joint's motion values (cos/sin or q) and q̇ are computed
-    # up front — n independent load -> sincos chains instead of n serialised
-    # ones — and parked in the first slots (the kernel keeps those on chip).
-    for i in range(n):
-        cs, qi = motion_vals(i)
-        mrefs[i] = ("q", store(qi)) if cs is None else ("cs", store(cs[0]), store(cs[1]))
-    for i in range(n):
-        qdrefs[i] = store(g.tmp(f"cx.qd({i})", "qd"))
-    nonlocal_counts["prologue"] = nslot_box[0]
     for r in rb.roots:
         down_up(r, None)
-
-    gvec = [ZERO, ZERO, ZERO, Ex(s="ga0"), Ex(s="ga1"), Ex(s="ga2")]
-    g.raw("const T ga0 = cx.g(0), ga1 = cx.g(1), ga2 = cx.g(2);")
+    gvec = A.gravity()
 
     def down(i, vp, ap):
-        g.raw("cx.sync();")
-        udr, Udr, mref = layout[i]
-        X = joint_from(i, mref)
-        qdi = load(qdrefs[i])
+        udr, Udr = layout[i]
+        X = A.joint(i)
+        qdi = A.load(A.qdrefs[i])
         if vp is None:
             v = X.S(qdi)
             a1 = X.motion_to_child(gvec)
         else:
             v = g.vadd(X.motion_to_child(vp), X.S(qdi))
             a1 = g.vadd(X.motion_to_child(ap), g.crm(v, X.S(qdi)))
-        ud = load(udr)
-        Ud = [load(r) for r in Udr]
-        qdd = g.sub(ud, g.sdot(Ud, a1))
-        g.raw(f"cx.qdd({i}, {g.o(qdd)});")
+        qdd = g.sub(A.load(udr), g.sdot([A.load(r) for r in Udr], a1))
+        g.raw(f"cx.y(0, {i}, {g.o(qdd)});")
         g.raw(f"ok = ok && vd_isfinite({g.o(qdd)});")
         if rb.children[i]:
             a = g.vadd(a1, X.S(qdd))
@@ -474,24 +475,171 @@ def gen_aba(rb):
 
     for r in rb.roots:
         down(r, None, None)
-    g.raw("return ok;")
-    return g, nslot_box[0], nonlocal_counts["prologue"]
+    return A.finish()
+
+
+def gen_rnea(rb, with_qd, with_qdd):
+    """RNEA (rnea_loop, dynamics.hpp:272-327; Alg. 1 of PAPER.md:141-151):
+    x(0) = q, x(1) = q̇ (if with_qd), x(2) = q̈ (if with_qdd); y(0, i) = τ_i.
+    with_qdd = False is the bias term c + g (dynamics.hpp:434-435), with_qd =
+    False as well the gravity term (dynamics.hpp:403-408).  One DFS: v, a and
+    the body's own force on the way down, Σ child forces and τ on the way up."""
+    A = Algo(rb, False)
+    g = A.g
+    gvec = A.gravity()
+
+    def rec(i, vp, ap):
+        X = A.joint(i)
+        qdi = g.tmp(f"cx.x(1, {i})", "qd") if with_qd else ZERO
+        qddi = g.tmp(f"cx.x(2, {i})", "qa") if with_qdd else ZERO
+        if vp is None:
+            v = X.S(qdi)
+            a = g.vadd(X.motion_to_child(gvec), X.S(qddi))
+        else:
+            v = g.vadd(X.motion_to_child(vp), X.S(qdi))
+            a = g.vadd(g.vadd(X.motion_to_child(ap), g.crm(v, X.S(qdi))), X.S(qddi))
+        b = rb.rb(i)
+        f = g.vadd(g.rb_apply(b, a), g.crf(v, g.rb_apply(b, v)))
+        for c in rb.children[i]:
+            f = g.vadd(f, rec(c, v, a))
+        if rb.children[i]:
+            X = A.joint(i)
+        tau = X.Sdot(f)
+        g.raw(f"cx.y(0, {i}, {g.o(tau)});")
+        return X.force_to_parent(f) if vp is not None else None
+
+    for r in rb.roots:
+        rec(r, None, None)
+    return A.finish()
+
+
+def gen_crba(rb):
+    """CRBA (crba_loop, dynamics.hpp:369-400; Alg. 2 of PAPER.md:156-165):
+    x(0) = q; y(0, c·n + r) = M(r, c), dense, with exact zeros between
+    branches (dynamics.hpp:330-335, test_dynamics.cpp:200-216).  Composite
+    inertias (10-parameter form) are summed leaf -> root in one DFS; each
+    column is emitted as soon as its composite is complete, walking the force
+    F = Ic S up the ancestor chain."""
+    A = Algo(rb, False)
+    g = A.g
+    n = rb.n
+    related = [[False] * n for _ in range(n)]
+
+    def emit(r, c, val):
+        related[r][c] = related[c][r] = True
+        g.raw(f"cx.y(0, {c * n + r}, {g.o(val)});")
+        if r != c:
+            g.raw(f"cx.y(0, {r * n + c}, {g.o(val)});")
+
+    def rec(i):
+        Ic = rb.rb(i)
+        for c in rb.children[i]:
+            cm, ch, cI = rec(c)
+            Ic = (g.add(Ic[0], cm), g.vadd(Ic[1], ch), g.vadd(Ic[2], cI))
+        X = A.joint(i)
+        F = g.rb_apply(Ic, X.Svec())
+        emit(i, i, X.Sdot(F))
+        j = i
+        while rb.parent[j] >= 0:
+            F = A.joint(j).force_to_parent(F)
+            j = rb.parent[j]
+            emit(i, j, Joint_Sdot(g, rb, j, F))
+        if rb.parent[i] < 0:
+            return None
+        return rb_to_parent(g, X, Ic)
+
+    for r in rb.roots:
+        rec(r)
+    for c in range(n):
+        for r in range(n):
+            if not related[r][c]:
+                g.raw(f"cx.y(0, {c * n + r}, T(0));")
+    return A.finish()
+
+
+def Joint_Sdot(g, rb, j, f):
+    ax = rb.axis(j)
+    return g.dot(ax, f[3:] if rb.kind[j] == 1 else f[:3])
+
+
+def rb_out(g, b, Q, t):
+    """transform_inertia (spatial.hpp:259-267) on the 10-parameter form
+    (vd_device.cuh rb_out): h' = Q h + m t, I' = Q I Qᵀ + (2 g·t + m|t|²) 1 − t uᵀ − g tᵀ."""
+    m, h, I = b
+    gq = g.matvec(Q, h)
+    Ir = g.sym_rotate(Q, I)
+    if all(x.is0() for x in t):
+        return (m, gq, Ir)
+    u = [g.add(gq[k], g.mul(m, t[k])) for k in range(3)]
+    diag = g.add(g.dot(gq, t), g.dot(u, t))
+    I2 = [g.add(Ir[k], g.sub(g.sub(diag, g.mul(t[k], u[k])), g.mul(gq[k], t[k]))) for k in range(3)]
+    I2 += [g.sub(Ir[3], g.add(g.mul(t[0], u[1]), g.mul(gq[0], t[1]))),
+           g.sub(Ir[4], g.add(g.mul(t[0], u[2]), g.mul(gq[0], t[2]))),
+           g.sub(Ir[5], g.add(g.mul(t[1], u[2]), g.mul(gq[1], t[2])))]
+    return (m, u, I2)
+
+
+def rb_to_parent(g, X, b):
+    return rb_out(g, rb_out(g, b, X.QJ, X.tJ), X.QO, X.tO)
+
+
+def gen_fk(rb):
+    """forward_kinematics (kinematics.hpp:43-56): x(0) = q; y(0, 12 j + 3 c + r)
+    = ⁰R_j(r, c) (column-major), y(0, 12 j + 9 + r) = ⁰p_j(r)."""
+    A = Algo(rb, False)
+    g = A.g
+
+    def rec(i, Wp):
+        X = A.joint(i)
+        Rl = [g.dot(X.QO[3 * r:3 * r + 3], [X.QJ[c], X.QJ[3 + c], X.QJ[6 + c]]) for r in range(3) for c in range(3)]
+        pl = g.vadd(X.tO, g.matvec(X.QO, X.tJ))
+        if Wp is None:
+            R, p = Rl, pl
+        else:
+            WR, Wpp = Wp
+            R = [g.dot(WR[3 * r:3 * r + 3], [Rl[c], Rl[3 + c], Rl[6 + c]]) for r in range(3) for c in range(3)]
+            p = g.vadd(g.matvec(WR, pl), Wpp)
+        for c in range(3):
+            for r in range(3):
+                g.raw(f"cx.y(0, {12 * i + 3 * c + r}, {g.o(R[3 * r + c])});")
+        for r in range(3):
+            g.raw(f"cx.y(0, {12 * i + 9 + r}, {g.o(p[r])});")
+        for c in rb.children[i]:
+            rec(c, (R, p))
+
+    for r in rb.roots:
+        rec(r, None)
+    return A.finish()
+
+
+# (struct name, generator, output planes as a function of n, input groups)
+OPS = [("Aba", gen_aba, lambda n: n, 3),
+       ("Rnea", lambda rb: gen_rnea(rb, True, True), lambda n: n, 3),
+       ("RneaBias", lambda rb: gen_rnea(rb, True, False), lambda n: n, 2),
+       ("RneaGrav", lambda rb: gen_rnea(rb, False, False), lambda n: n, 1),
+       ("Crba", gen_crba, lambda n: n * n, 1),
+       ("Fk", gen_fk, lambda n: 12 * n, 1)]
 
 
 def emit(name, cls, rb):
-    g, nslot, npro = gen_aba(rb)
-    out = [f"// ---- {name}: ABA, {g.flops} flops (mul/add after folding), {nslot} state slots",
+    out = [f"// ---- {name}",
            f"struct Gen{cls} {{",
            f"  static constexpr int kN = {rb.n};",
-           f"  static constexpr int kAbaSlots = {nslot};",
-           f"  // slots [0, kAbaPrologue): cos/sin|q and q̇ of every joint, read in all three passes",
-           f"  static constexpr int kAbaPrologue = {npro};",
-           f"  static constexpr int kAbaFlops = {g.flops};",
-           f"  static constexpr uint64_t kFingerprint = {rb.d['fp']:#x}ull;",
-           "  template <class T, class Cx>",
-           "  VD_HD static bool aba(Cx& cx) {"]
-    out += ["  " + ln for ln in g.lines]
-    out += ["  }", "};", ""]
+           f"  static constexpr uint64_t kFingerprint = {rb.d['fp']:#x}ull;"]
+    for op, fn, nout, nin in OPS:
+        A = fn(rb)
+        out += [f"  // {op}: {A.g.flops} mul/add after folding; {A.nslot} slots, the first {A.nprologue} written by the prologue",
+                f"  struct {op} {{",
+                f"    static constexpr int kSlots = {A.nslot};",
+                f"    static constexpr int kPrologue = {A.nprologue};",
+                f"    static constexpr int kFlops = {A.g.flops};",
+                f"    static constexpr int kIn = {nin};",
+                f"    static constexpr int kOut = {nout(rb.n)};",
+                "    template <class T, class Cx>",
+                "    VD_HD static bool run(Cx& cx) {"]
+        out += ["    " + ln for ln in A.g.lines]
+        out += ["    }", "  };"]
+    out += ["};", ""]
     return out
 
 
