@@ -94,6 +94,7 @@ int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* 
 int launch_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
                int32_t* status) {
   if (L.N == 0) return 0;
+  if (const int rc = launch_gen_osc(L, q, qd, P, tau, lambda, status); rc >= 0) return rc;
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::osc(mv, L, q, qd, P, tau, lambda, status); });
 }
 

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include "vd_gen_robots.cuh"
+#include "vd_shared.hpp"
 
 namespace vdk {
 
@@ -132,6 +133,69 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
     if (cx.active) {
       if (!ok) {
         for (int j = 0; j < Op::kOut; ++j) y[(int64_t)j * ldo + i] = T(0);
+      }
+      if (status) status[i] = ok ? 0 : 7;
+    }
+  }
+}
+
+// osc_step context: task parameters (OscShared, kernel parameter space) and
+// a second output (Λ, 36 planes, optional).
+template <class T, int kSlots, int kReg, int kSmem>
+struct GenOscCx : GenCx<T, kSlots, kReg, kSmem> {
+  const OscShared* P;
+  T* out1_;  // &Λ[i] or nullptr
+  __device__ __forceinline__ T g(int k) const { return T(P->gravity[k]); }
+  __device__ __forceinline__ T fR(int k) const { return T(P->frame_R[k]); }
+  __device__ __forceinline__ T fp(int k) const { return T(P->frame_p[k]); }
+  __device__ __forceinline__ T tR(int k) const { return T(P->target_R[k]); }
+  __device__ __forceinline__ T tp(int k) const { return T(P->target_p[k]); }
+  __device__ __forceinline__ T kp(int k) const { return T(P->kp[k]); }
+  __device__ __forceinline__ T kd(int k) const { return T(P->kd[k]); }
+  __device__ __forceinline__ T aff(int k) const { return T(P->accel_ff[k]); }
+  __device__ __forceinline__ T pkp() const { return T(P->posture_kp); }
+  __device__ __forceinline__ T pkd() const { return T(P->posture_kd); }
+  __device__ __forceinline__ T eps() const { return T(P->epsilon); }
+  __device__ __forceinline__ T post(int k) const { return T(P->posture[k]); }
+  __device__ __forceinline__ bool want_lambda() const { return out1_ != nullptr; }
+  __device__ __forceinline__ void y(int o, int k, T v) const {
+    if (this->active) (o == 0 ? this->out_ : out1_)[k * this->ldo] = v;
+  }
+};
+
+template <class Op, class T, int kReg, int kSmem, int kMinB>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen_osc(int64_t N, const T* __restrict__ q, const T* __restrict__ qd, int64_t ldi,
+              const __grid_constant__ OscShared P, T* __restrict__ tau, T* __restrict__ lam, int64_t ldo,
+              int32_t* __restrict__ status, T* __restrict__ scratch) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenOscCx<T, Op::kSlots, kReg, kSmem>;
+  Cx cx;
+  cx.P = &P;
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  cx.sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  cx.sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    cx.active = i0 < N;
+    const int64_t i = cx.active ? i0 : N - 1;
+    int64_t ld, lo;
+    asm volatile("mov.b64 %0, %1;" : "=l"(ld) : "l"(ldi));
+    asm volatile("mov.b64 %0, %1;" : "=l"(lo) : "l"(ldo));
+    cx.ld = ld;
+    cx.ldo = lo;
+    cx.in_[0] = q + i;
+    cx.in_[1] = qd + i;
+    cx.in_[2] = q + i;
+    cx.out_ = tau + i;
+    cx.out1_ = lam ? lam + i : nullptr;
+    const bool ok = Op::template run<T>(cx);
+    if (cx.active) {
+      if (!ok) {
+        for (int j = 0; j < Op::kOut; ++j) tau[(int64_t)j * ldo + i] = T(0);
+        if (lam)
+          for (int j = 0; j < 36; ++j) lam[(int64_t)j * ldo + i] = T(0);
       }
       if (status) status[i] = ok ? 0 : 7;
     }

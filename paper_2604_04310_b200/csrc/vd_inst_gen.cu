@@ -78,6 +78,53 @@ int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, co
   return (int)e;
 }
 
+// Occupancy (and the dynamic shared-memory opt-in) once per device for each
+// kernel instantiation; keyed by <Op, T>, not by the kernel's function type
+// (all variants of one dtype share it).
+template <class Op, class T, class Kern>
+Occ occupancy(Kern kern, size_t smem) {
+  static std::mutex mu;
+  static Occ occ[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  Occ& c = occ[dev & 63];
+  if (!c.blocks_per_sm) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.blocks_per_sm, kern, kGenBlock, smem);
+    if (c.blocks_per_sm < 1) c.blocks_per_sm = 1;
+  }
+  return c;
+}
+
+template <class Op, class T>
+struct OscCfg {
+  static constexpr int kReg = 0, kSmem = 110, kMinB = sizeof(T) == 8 ? 2 : 3;
+};
+
+template <class Op, class T>
+int launch_osc_t(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lam,
+                 int32_t* status) {
+  using C = OscCfg<Op, T>;
+  auto kern = k_gen_osc<Op, T, C::kReg, C::kSmem, C::kMinB>;
+  constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
+  const Occ o = occupancy<Op, T>(kern, smem);
+  const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
+  cudaStream_t s = static_cast<cudaStream_t>(L.stream);
+  const size_t scratch_bytes = (size_t)blocks * kGenBlock * gen_scratch_per_thread<Op, T, C::kReg, C::kSmem>() * sizeof(T);
+  T* scratch = nullptr;
+  if (scratch_bytes) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_bytes, s);
+    if (e != cudaSuccess) return (int)e;
+  }
+  kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, (const T*)q, (const T*)qd, L.ld_in, P, (T*)tau, (T*)lam,
+                                                 L.ld_out, status, scratch);
+  cudaError_t e = cudaGetLastError();
+  if (scratch) cudaFreeAsync(scratch, s);
+  return (int)e;
+}
+
 template <class Op>
 int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
               int32_t* status) {
@@ -105,6 +152,18 @@ int launch_gen_rnea(const Launch& L, int mode, const void* q, const void* qd, co
   if (has_qd) return launch_op<GenTree29::RneaBias>(L, q, qd, nullptr, g, tau, nullptr);
   if (!has_qdd) return launch_op<GenTree29::RneaGrav>(L, q, nullptr, nullptr, g, tau, nullptr);
   return -1;  // q̇ = 0 with q̈: no generated variant, template kernel
+}
+
+int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
+                   int32_t* status) {
+  if (L.spec != kTree29) return -1;
+  int rc = -1;
+  GenTree29::with_osc(P.frame_joint, [&](auto op) {
+    using Op = decltype(op);
+    rc = L.dtype == 0 ? launch_osc_t<Op, double>(L, q, qd, P, tau, lambda, status)
+                      : launch_osc_t<Op, float>(L, q, qd, P, tau, lambda, status);
+  });
+  return rc;
 }
 
 int launch_gen_crba(const Launch& L, const void* q, void* M) {

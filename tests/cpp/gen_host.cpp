@@ -14,11 +14,26 @@ struct HostCx {
   T* Y;
   long ld, i;
   T* slots;
+  // OSC parameters (gen_osc_host layout): fR 9, fp 3, tR 9, tp 3, kp 6, kd 6, aff 6, pkp, pkd, eps, posture n
+  const double* P = nullptr;
+  T* Y1 = nullptr;
   T x(int g, int j) const { return X[g][j * ld + i]; }
   T g(int k) const { return T(G[k]); }
   void st(int k, T v) { slots[k] = v; }
   T get(int k) const { return slots[k]; }
-  void y(int, int k, T v) const { Y[k * ld + i] = v; }
+  void y(int o, int k, T v) const { (o == 0 ? Y : Y1)[k * ld + i] = v; }
+  T fR(int k) const { return T(P[k]); }
+  T fp(int k) const { return T(P[9 + k]); }
+  T tR(int k) const { return T(P[12 + k]); }
+  T tp(int k) const { return T(P[21 + k]); }
+  T kp(int k) const { return T(P[24 + k]); }
+  T kd(int k) const { return T(P[30 + k]); }
+  T aff(int k) const { return T(P[36 + k]); }
+  T pkp() const { return T(P[42]); }
+  T pkd() const { return T(P[43]); }
+  T eps() const { return T(P[44]); }
+  T post(int k) const { return T(P[45 + k]); }
+  bool want_lambda() const { return Y1 != nullptr; }
 };
 template <class Op, class T>
 int run(long N, const void* const* x, const double* g, void* y, int* status) {
@@ -43,8 +58,34 @@ int run_op(int op, long N, const void* const* x, const double* g, void* y, int* 
     default: return run<typename R::Fk, T>(N, x, g, y, status);
   }
 }
+
+template <class R>
+int osc(int fj, long N, const double* q, const double* qd, const double* g, const double* P, double* tau,
+        double* lam, int* status) {
+  int bad = -1;
+  R::with_osc(fj, [&](auto op) {
+    using Op = decltype(op);
+    std::vector<double> slots(Op::kSlots + 1);
+    bad = 0;
+    for (long i = 0; i < N; ++i) {
+      HostCx<double> cx{{q, qd, q}, g, tau, N, i, slots.data()};
+      cx.P = P;
+      cx.Y1 = lam;
+      const bool ok = Op::template run<double>(cx);
+      status[i] = ok ? 0 : 7;
+      bad += !ok;
+    }
+  });
+  return bad;
+}
 }  // namespace
 
+// generated osc_step on frame joint fj (fp64); -1 when no variant exists for fj
+extern "C" int gen_osc_host(int robot, int fj, long N, const double* q, const double* qd, const double* g,
+                            const double* P, double* tau, double* lam, int* status) {
+  return robot == 2 ? osc<vdk::GenTree29>(fj, N, q, qd, g, P, tau, lam, status)
+                    : osc<vdk::GenChain7>(fj, N, q, qd, g, P, tau, lam, status);
+}
 // op: 0 aba, 1 rnea, 2 bias, 3 gravity, 4 crba, 5 fk; robot: 1 chain7, 2 tree29
 extern "C" int gen_run_host(int robot, int op, int f32, long N, const void* x0, const void* x1, const void* x2,
                             const double* g, void* y, int* status) {

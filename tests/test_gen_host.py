@@ -121,3 +121,40 @@ def test_generated_crba_and_fk(genlib, name, code):
     assert np.all(M[:, structural] == 0)  # exact zeros between branches, as in the reference
     F, _, _ = _run(genlib, code, 5, (q,), 12 * n)
     assert rel_err(F, om.fk(q).reshape(len(q), -1), axis=1).max() <= 1e-10
+
+
+@pytest.mark.parametrize("name,code,frame", [("chain7", 1, "ee"), ("tree29", 2, "l_palm"), ("tree29", 2, "head"),
+                                              ("tree29", 2, "r_foot")])
+def test_generated_osc_matches_oracle(genlib, name, code, frame):
+    """osc_step (control.hpp:108-155): τ and Λ against the oracle, with the
+    conditioning-aware bound of test_gpu_parity.test_osc_fp64."""
+    om = Model.builtin(name)
+    N = 512
+    q, qd, _, _ = om.random_states(N, 61, True, False)
+    fid = {f[0]: f for f in om.frames()}[frame]
+    fj, off = fid[1], fid[2]
+    q0 = np.zeros((1, om.n))
+    pose0, _ = om.jacobian(q0, frame)
+    R0 = pose0[0, :9].reshape(3, 3, order="F")
+    p0 = pose0[0, 9:]
+    kp, kd, aff = [100.0] * 6, [20.0] * 6, [0.0] * 6
+    posture = np.linspace(-0.3, 0.3, om.n)
+    tau_ref, lam_ref, st_ref = om.osc(q, qd, frame, R0, p0, kp, kd, aff, posture, 10.0, 2.0)
+    fR = off[:9].reshape(3, 3, order="F")  # frame offset, column-major R
+    P = np.concatenate([fR.reshape(-1), off[9:], R0.reshape(-1), p0, kp, kd, aff, [10.0, 2.0, 1e-6], posture])
+    genlib.gen_osc_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 7
+    Q, QD = np.asfortranarray(q), np.asfortranarray(qd)
+    tau = np.zeros_like(Q, order="F")
+    lam = np.zeros((N, 36), order="F")
+    st = np.zeros(N, dtype=np.int32)
+    g = np.array([0.0, 0.0, 9.81])
+    bad = genlib.gen_osc_host(code, fj, N, _p(Q), _p(QD), _p(g), _p(P), _p(tau), _p(lam), _p(st))
+    assert bad >= 0, "no generated variant for this frame joint"
+    assert np.all(st == st_ref)
+    ok = st == 0
+    kappa = np.linalg.cond(om.crba(q)) * np.linalg.cond(lam_ref)
+    bound = np.maximum(1e-10, 1e-16 * kappa)
+    e_tau = rel_err(tau, tau_ref, axis=1)
+    assert np.all(e_tau[ok] <= bound[ok]), float((e_tau / bound).max())
+    e_lam = rel_err(lam, lam_ref.reshape(N, -1), axis=1)
+    assert np.all(e_lam[ok] <= np.maximum(bound[ok], 1e-10)), float(e_lam.max())

@@ -276,8 +276,9 @@ def test_fk_scan(vd, cuda, omodels, oracle):
 
 
 # ---------------------------------------------------------------- OSC
-def _osc_case(vd, om, m, dm, name, N, seed, dtype=torch.float64):
-    frame = "ee" if name == "chain7" else ("l_palm" if name != "humanoid23" else "r_palm")
+def _osc_case(vd, om, m, dm, name, N, seed, dtype=torch.float64, frame=None):
+    if frame is None:
+        frame = "ee" if name == "chain7" else ("l_palm" if name != "humanoid23" else "r_palm")
     q, qd, _, _ = _states(om, N, seed, with_tau=False)
     q0 = np.zeros((1, om.n))
     pose0, _ = om.jacobian(q0, frame)
@@ -487,3 +488,20 @@ def test_tree29_generated_aba_shards_and_ld(vd, cuda, omodels, dtype):
     d = rel_err(_np(full[:4096]), _np(loop), axis=1)
     eps = float(torch.finfo(dtype).eps)
     assert np.all(d <= np.maximum(1e-10 if dtype == torch.float64 else 1e-4, 29 * eps * cond))
+
+
+@pytest.mark.parametrize("frame", ["head", "r_foot", "r_palm", "l_hand"])
+def test_osc_tree29_frames(vd, cuda, omodels, frame):
+    """G1 OSC on other task frames: generated variants (leaf joints and fused
+    frames: head on the torso, r_foot, r_palm) and the loop kernel fallback
+    (l_hand's joint 23 also carries l_palm, so it is generated too) against
+    the oracle's osc_step (control.hpp:108-155)."""
+    om = omodels["tree29"]
+    m, dm = _dm(vd, "tree29")
+    q, tau, lam, st, tau_ref, lam_ref, st_ref = _osc_case(vd, om, m, dm, "tree29", 1024, 63, frame=frame)
+    assert np.all(st == st_ref)
+    ok = st == 0
+    kappa = np.linalg.cond(om.crba(q)) * np.linalg.cond(lam_ref)
+    bound = np.maximum(TOL64, 1e-16 * kappa)
+    assert np.all(rel_err(tau, tau_ref, axis=1)[ok] <= bound[ok])
+    assert np.all(rel_err(lam, lam_ref, axis=1)[ok] <= np.maximum(bound[ok], 1e-10))

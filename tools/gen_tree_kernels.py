@@ -255,9 +255,30 @@ class Gen:
         return {"A": A, "B": B, "C": o["C"]}
 
 
+def frame_joints(lib, name):
+    """Joints carrying a named frame with a non-identity offset (fixed-joint
+    fused frames such as `l_palm`, `head`), from the library's own model."""
+    import ctypes
+    h = ctypes.c_void_p()
+    if lib.vd_model_builtin(name.encode(), ctypes.byref(h)) != 0:
+        raise RuntimeError(lib.vd_last_error().decode())
+    out = set()
+    for k in range(lib.vd_model_frame_count(h)):
+        buf = ctypes.create_string_buffer(256)
+        j = ctypes.c_int()
+        off = (ctypes.c_double * 12)()
+        lib.vd_model_frame(h, k, buf, 256, ctypes.byref(j), off)
+        ident = [1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0]
+        if j.value >= 0 and any(abs(off[t] - ident[t]) > 0 for t in range(12)):
+            out.add(j.value)
+    lib.vd_model_destroy(h)
+    return sorted(out)
+
+
 class Robot:
-    def __init__(self, d):
+    def __init__(self, d, fjoints=()):
         self.d = d
+        self.frame_joints = list(fjoints)
         self.n = d["n"]
         self.parent = d["parent"]
         self.kind = d["kind"]
@@ -612,6 +633,274 @@ def gen_fk(rb):
     return A.finish()
 
 
+class Slots:
+    """Named values kept in context slots (cx.st / cx.get): every write is a
+    store (re-using the key's slot), every read a load.  Structural zeros
+    stay symbolic constants and never touch a slot."""
+
+    def __init__(self, A):
+        self.A = A
+        self.ref = {}
+
+    def set(self, key, v):
+        if v.c is not None:
+            self.ref[key] = ("k", v.c)
+            return
+        old = self.ref.get(key)
+        if old is not None and old[0] == "s":
+            self.A.g.raw(f"cx.st({old[1]}, {v.s});")
+        else:
+            self.ref[key] = self.A.store(v)
+
+    def get(self, key):
+        return self.A.load(self.ref[key])
+
+
+def chol6(g, G):
+    """In-place Cholesky of a symmetric 6x6 (dict (r, c) -> Ex, lower), the
+    same operation order as vd_algos.cuh chol6 / Eigen's LLT.  Returns (L, ok
+    expression)."""
+    L = dict(G)
+    oks = []
+    for k in range(6):
+        x = L[(k, k)]
+        for j in range(k):
+            x = g.sub(x, g.mul(L[(k, j)], L[(k, j)]))
+        oks.append(f"({g.o(x)} > T(0))")
+        x = g.tmp(f"vd_sqrt({g.o(x)})", "sq")
+        L[(k, k)] = x
+        inv = g.tmp(f"T(1) / {x.s}", "iv")
+        for i in range(k + 1, 6):
+            sv = L[(i, k)]
+            for j in range(k):
+                sv = g.sub(sv, g.mul(L[(i, j)], L[(k, j)]))
+            L[(i, k)] = g.mul(sv, inv)
+    return L, " && ".join(oks)
+
+
+def chol6_solve(g, L, b):
+    b = list(b)
+    for i in range(6):
+        sv = b[i]
+        for j in range(i):
+            sv = g.sub(sv, g.mul(L[(i, j)], b[j]))
+        b[i] = g.tmp(f"{g.o(sv)} / {g.o(L[(i, i)])}", "dv") if not sv.is0() else ZERO
+    for i in range(5, -1, -1):
+        sv = b[i]
+        for j in range(i + 1, 6):
+            sv = g.sub(sv, g.mul(L[(j, i)], b[j]))
+        b[i] = g.tmp(f"{g.o(sv)} / {g.o(L[(i, i)])}", "dv") if not sv.is0() else ZERO
+    return b
+
+
+def gen_osc(rb, fj):
+    """osc_step (control.hpp:108-155) for a task frame on joint fj (frame
+    offset, target, gains, posture and ε are runtime parameters), mirroring
+    vd_algos.cuh osc_one: CRBA -> M in compact ancestor rows, branch-sparse
+    LTL (RBDA §6.5, no fill-in), M⁻¹ applied to the 6 Jacobian rows and the
+    posture torque, Λ = (J M⁻¹ Jᵀ + εI)⁻¹ and (J M⁻¹ Jᵀ)⁻¹ by 6x6 Cholesky,
+    τ = Jᵀ(F − z) + τ_post + c + g with the bias from RNEA.  Structural
+    sparsity is symbolic: J is zero off the frame's ancestor path, so the
+    Jacobian-row solves touch only that path.
+    x(0) = q, x(1) = q̇; y(0, k) = τ_k, y(1, 6 c + r) = Λ(r, c)."""
+    A = Algo(rb, True)
+    g = A.g
+    n = rb.n
+    depth = [0] * n
+    for i in range(n):
+        depth[i] = 1 if rb.parent[i] < 0 else depth[rb.parent[i]] + 1
+    path = []
+    j = fj
+    while j >= 0:
+        path.append(j)
+        j = rb.parent[j]
+    path = path[::-1]  # root .. fj
+    onpath = set(path)
+    SL = Slots(A)
+
+    # ---- frame pose along the path (kinematics.hpp:43-56, 89-96) and J (108-129)
+    W = {}
+    Wp = None
+    for i in path:
+        X = A.joint(i)
+        Rl = [g.dot(X.QO[3 * r:3 * r + 3], [X.QJ[c], X.QJ[3 + c], X.QJ[6 + c]]) for r in range(3) for c in range(3)]
+        pl = g.vadd(X.tO, g.matvec(X.QO, X.tJ))
+        if Wp is None:
+            R, p = Rl, pl
+        else:
+            R = [g.dot(Wp[0][3 * r:3 * r + 3], [Rl[c], Rl[3 + c], Rl[6 + c]]) for r in range(3) for c in range(3)]
+            p = g.vadd(g.matvec(Wp[0], pl), Wp[1])
+        W[i] = (R, p)
+        Wp = (R, p)
+    WR, Wpos = W[fj]
+    fR = [g.tmp(f"cx.fR({k})", "pf") for k in range(9)]
+    fpv = [g.tmp(f"cx.fp({k})", "pf") for k in range(3)]
+    pose_R = [g.dot(WR[3 * r:3 * r + 3], [fR[c], fR[3 + c], fR[6 + c]]) for r in range(3) for c in range(3)]
+    pose_p = g.vadd(g.matvec(WR, fpv), Wpos)
+    for i in path:
+        R, p = W[i]
+        ax = g.matvec(R, rb.axis(i))
+        if rb.kind[i] == 0:
+            d = g.vsub(pose_p, p)
+            col = ax + g.cross3(ax, d)
+        else:
+            col = [ZERO] * 3 + ax
+        for r in range(6):
+            SL.set(("J", r, i), col[r])
+    # ---- pose error (control.hpp:73-77): log(R_t R_cᵀ), p_t − p_c
+    tR = [g.tmp(f"cx.tR({k})", "pt") for k in range(9)]
+    Rrel = [g.dot(tR[3 * r:3 * r + 3], pose_R[3 * c:3 * c + 3]) for r in range(3) for c in range(3)]
+    rl = ", ".join(g.o(x) for x in Rrel)
+    g.raw(f"const T Rrel_[9] = {{{rl}}};")
+    g.raw("T lg_[3];")
+    g.raw("vd_rotation_log(Rrel_, lg_);")
+    err = [Ex(s="lg_[0]"), Ex(s="lg_[1]"), Ex(s="lg_[2]")]
+    err += [g.sub(g.tmp(f"cx.tp({k})", "pt"), pose_p[k]) for k in range(3)]
+    for k in range(6):
+        SL.set(("err", k), err[k])
+
+    # ---- CRBA (crba_loop, dynamics.hpp:369-400) into compact rows Mc(i, d) = M(i, anc_d(i))
+    def crba(i):
+        Ic = rb.rb(i)
+        for c in rb.children[i]:
+            cm, ch, cI = crba(c)
+            Ic = (g.add(Ic[0], cm), g.vadd(Ic[1], ch), g.vadd(Ic[2], cI))
+        X = A.joint(i)
+        F = g.rb_apply(Ic, X.Svec())
+        SL.set(("M", i, 0), X.Sdot(F))
+        j, d = i, 0
+        while rb.parent[j] >= 0:
+            F = A.joint(j).force_to_parent(F)
+            j = rb.parent[j]
+            d += 1
+            SL.set(("M", i, d), Joint_Sdot(g, rb, j, F))
+        if rb.parent[i] < 0:
+            return None
+        return rb_to_parent(g, X, Ic)
+
+    for r in rb.roots:
+        crba(r)
+
+    # ---- LTL in place (RBDA Table 6.3), k = n-1 .. 0
+    def anc(i, d):
+        for _ in range(d):
+            i = rb.parent[i]
+        return i
+
+    for k in range(n - 1, -1, -1):
+        dkk = SL.get(("M", k, 0))
+        g.raw(f"ok = ok && ({g.o(dkk)} > T(0));")
+        lkk = g.tmp(f"vd_sqrt({g.o(dkk)})", "sq")
+        SL.set(("M", k, 0), lkk)
+        inv = g.tmp(f"T(1) / {lkk.s}", "iv")
+        row = {0: lkk}
+        for d in range(1, depth[k]):
+            row[d] = g.mul(SL.get(("M", k, d)), inv)
+            SL.set(("M", k, d), row[d])
+        for d in range(1, depth[k]):
+            i = anc(k, d)
+            for e in range(d, depth[k]):
+                SL.set(("M", i, e - d), g.sub(SL.get(("M", i, e - d)), g.mul(row[d], row[e])))
+
+    # ---- 7 right-hand sides: rows of J and τ_post = kp_p (q_post − q) − kd_p q̇
+    pkp, pkd = g.tmp("cx.pkp()", "pp"), g.tmp("cx.pkd()", "pp")
+
+    def tpost(k):
+        qk = g.tmp(f"cx.x(0, {k})", "q")
+        return g.sub(g.mul(pkp, g.sub(g.tmp(f"cx.post({k})", "pp"), qk)), g.mul(pkd, A.load(A.qdrefs[k])))
+
+    for k in range(n):
+        for r in range(6):
+            SL.set(("X", r, k), SL.get(("J", r, k)) if k in onpath else ZERO)
+        SL.set(("X", 6, k), tpost(k))
+    # Lᵀ y = b (leaf -> root), then L x = y (root -> leaf); only path entries of
+    # x are needed (J is zero elsewhere)
+    for i in range(n - 1, -1, -1):
+        inv = g.tmp(f"T(1) / {g.o(SL.get(('M', i, 0)))}", "iv")
+        xi = {}
+        for r in range(7):
+            v = SL.get(("X", r, i)) if SL.ref[("X", r, i)][0] == "s" else K(SL.ref[("X", r, i)][1])
+            xi[r] = g.mul(v, inv)
+            SL.set(("X", r, i), xi[r])
+        for d in range(1, depth[i]):
+            j = anc(i, d)
+            lij = None
+            for r in range(7):
+                if xi[r].is0():
+                    continue
+                if lij is None:
+                    lij = SL.get(("M", i, d))
+                cur = SL.get(("X", r, j)) if SL.ref[("X", r, j)][0] == "s" else K(SL.ref[("X", r, j)][1])
+                SL.set(("X", r, j), g.sub(cur, g.mul(lij, xi[r])))
+    xs = {}
+    for i in path:
+        acc = {r: (SL.get(("X", r, i)) if SL.ref[("X", r, i)][0] == "s" else K(SL.ref[("X", r, i)][1])) for r in range(7)}
+        for d in range(1, depth[i]):
+            j = anc(i, d)
+            lij = SL.get(("M", i, d))
+            for r in range(7):
+                acc[r] = g.sub(acc[r], g.mul(lij, xs[(r, j)]))
+        inv = g.tmp(f"T(1) / {g.o(SL.get(('M', i, 0)))}", "iv")
+        for r in range(7):
+            xs[(r, i)] = g.mul(acc[r], inv)
+    # ---- gram = J M⁻¹ Jᵀ, w = J M⁻¹ τ_post, J q̇
+    Jp = {(r, k): SL.get(("J", r, k)) for r in range(6) for k in path}
+    gram = {}
+    for r in range(6):
+        for c in range(r + 1):
+            gram[(r, c)] = g.sum([g.mul(Jp[(r, k)], xs[(c, k)]) for k in path])
+    w = [g.sum([g.mul(Jp[(r, k)], xs[(6, k)]) for k in path]) for r in range(6)]
+    jqd = [g.sum([g.mul(Jp[(r, k)], A.load(A.qdrefs[k])) for k in path]) for r in range(6)]
+    eps = g.tmp("cx.eps()", "pe")
+    Gr = {key: (g.add(v, eps) if key[0] == key[1] else v) for key, v in gram.items()}
+    Lr, _ = chol6(g, Gr)
+    Lg, gok = chol6(g, gram)
+    g.raw(f"const bool gok_ = {gok};")
+    F = [g.add(g.sub(g.mul(g.tmp(f"cx.kp({r})", "pg"), SL.get(("err", r))), g.mul(g.tmp(f"cx.kd({r})", "pg"), jqd[r])),
+               g.tmp(f"cx.aff({r})", "pg")) for r in range(6)]
+    F = chol6_solve(g, Lr, F)
+    zg = chol6_solve(g, Lg, w)
+    zr = chol6_solve(g, Lr, w)
+    z = [g.tmp(f"gok_ ? {g.o(a)} : {g.o(b)}", "z") for a, b in zip(zg, zr)]
+    fz = [g.sub(a, b) for a, b in zip(F, z)]
+    jt = {k: g.sum([g.mul(Jp[(r, k)], fz[r]) for r in range(6)]) for k in path}
+    for k in path:
+        SL.set(("jt", k), jt[k])
+    # ---- Λ = (J M⁻¹ Jᵀ + εI)⁻¹, column by column
+    g.raw("if (cx.want_lambda()) {")
+    for c in range(6):
+        e = chol6_solve(g, Lr, [ONE if r == c else ZERO for r in range(6)])
+        for r in range(6):
+            g.raw(f"cx.y(1, {6 * c + r}, {g.o(e[r])});")
+    g.raw("}")
+    # ---- bias c + g (RNEA with q̈ = 0, dynamics.hpp:434-435) and τ
+    gvec = A.gravity()
+
+    def rec(i, vp, ap):
+        X = A.joint(i)
+        qdi = A.load(A.qdrefs[i])
+        if vp is None:
+            v = X.S(qdi)
+            a = X.motion_to_child(gvec)
+        else:
+            v = g.vadd(X.motion_to_child(vp), X.S(qdi))
+            a = g.vadd(X.motion_to_child(ap), g.crm(v, X.S(qdi)))
+        b = rb.rb(i)
+        f = g.vadd(g.rb_apply(b, a), g.crf(v, g.rb_apply(b, v)))
+        for c in rb.children[i]:
+            f = g.vadd(f, rec(c, v, a))
+        if rb.children[i]:
+            X = A.joint(i)
+        tau = g.add(g.add(tpost(i), X.Sdot(f)), SL.get(("jt", i)) if i in onpath else ZERO)
+        g.raw(f"cx.y(0, {i}, {g.o(tau)});")
+        g.raw(f"ok = ok && vd_isfinite({g.o(tau)});")
+        return X.force_to_parent(f) if vp is not None else None
+
+    for r in rb.roots:
+        rec(r, None, None)
+    return A.finish()
+
+
 # (struct name, generator, output planes as a function of n, input groups)
 OPS = [("Aba", gen_aba, lambda n: n, 3),
        ("Rnea", lambda rb: gen_rnea(rb, True, True), lambda n: n, 3),
@@ -639,6 +928,33 @@ def emit(name, cls, rb):
                 "    VD_HD static bool run(Cx& cx) {"]
         out += ["    " + ln for ln in A.g.lines]
         out += ["    }", "  };"]
+    # OSC per task-frame joint (the frame offset stays a runtime parameter):
+    # one variant for every leaf joint (end effectors) and the joints that
+    # carry a named frame of the model
+    osc_joints = sorted(set(i for i in range(rb.n) if not rb.children[i]) | set(rb.frame_joints))
+    for fj in osc_joints:
+        A = gen_osc(rb, fj)
+        out += [f"  // Osc on joint {fj}: {A.g.flops} mul/add after folding; {A.nslot} slots",
+                f"  struct Osc{fj} {{",
+                f"    static constexpr int kSlots = {A.nslot};",
+                f"    static constexpr int kPrologue = {A.nprologue};",
+                f"    static constexpr int kFlops = {A.g.flops};",
+                "    static constexpr int kIn = 2;",
+                f"    static constexpr int kOut = {rb.n};",
+                "    template <class T, class Cx>",
+                "    VD_HD static bool run(Cx& cx) {"]
+        out += ["    " + ln for ln in A.g.lines]
+        out += ["    }", "  };"]
+    out.append(f"  static constexpr int kOscJoints[] = {{{', '.join(str(j) for j in osc_joints)}}};")
+    out.append("  // calls f(Osc<fj>{}) for the generated variant of joint fj; false if none")
+    out.append("  template <class F>")
+    out.append("  static bool with_osc(int fj, F&& f) {")
+    out.append("    switch (fj) {")
+    for fj in osc_joints:
+        out.append(f"      case {fj}: f(Osc{fj}{{}}); return true;")
+    out.append("      default: return false;")
+    out.append("    }")
+    out.append("  }")
     out += ["};", ""]
     return out
 
@@ -652,6 +968,39 @@ def generate(lib):
          "#ifndef VD_HD", "#if defined(__CUDACC__)", "#define VD_HD __host__ __device__ __forceinline__",
          "#else", "#define VD_HD inline", "#endif", "#endif", "",
          "namespace vdk {", "",
+         "template <class T> VD_HD T vd_sqrt(T x) { using std::sqrt; return sqrt(x); }",
+         "// rotation_log (control.hpp:45-68), the reference acos form and branches",
+         "template <class T>",
+         "VD_HD void vd_rotation_log(const T* R, T* w) {",
+         "  using std::acos; using std::sin; using std::sqrt;",
+         "  const T tr = R[0] + R[4] + R[8];",
+         "  const T anti[3] = {R[7] - R[5], R[2] - R[6], R[3] - R[1]};",
+         "  T ca = T(0.5) * (tr - T(1));",
+         "  ca = ca < T(-1) ? T(-1) : (ca > T(1) ? T(1) : ca);",
+         "  const T ang = acos(ca);",
+         "  const T pi = T(3.14159265358979323846);",
+         "  if (ang < T(1e-9)) {",
+         "    for (int k = 0; k < 3; ++k) w[k] = T(0.5) * anti[k];",
+         "    return;",
+         "  }",
+         "  if (ang > pi - T(1e-6)) {",
+         "    const T sd[3] = {T(0.5) * (R[0] + T(1)), T(0.5) * (R[4] + T(1)), T(0.5) * (R[8] + T(1))};",
+         "    int k = 0;",
+         "    if (sd[1] > sd[k]) k = 1;",
+         "    if (sd[2] > sd[k]) k = 2;",
+         "    T ax[3];",
+         "    for (int r = 0; r < 3; ++r) ax[r] = (r == k) ? sd[k] : T(0.5) * R[r * 3 + k];",
+         "    const T inv = T(1) / sqrt(sd[k] > T(1e-12) ? sd[k] : T(1e-12));",
+         "    for (int r = 0; r < 3; ++r) ax[r] *= inv;",
+         "    const T nrm = sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);",
+         "    for (int r = 0; r < 3; ++r) ax[r] /= nrm;",
+         "    const T sgn = (anti[0] * ax[0] + anti[1] * ax[1] + anti[2] * ax[2]) < T(0) ? T(-1) : T(1);",
+         "    for (int r = 0; r < 3; ++r) w[r] = ang * sgn * ax[r];",
+         "    return;",
+         "  }",
+         "  const T f = T(0.5) * ang / sin(ang);",
+         "  for (int k = 0; k < 3; ++k) w[k] = f * anti[k];",
+         "}", "",
          "#if defined(__CUDA_ARCH__)",
          "__device__ __forceinline__ void vd_sincos(double x, double* s, double* c) { sincos(x, s, c); }",
          "__device__ __forceinline__ void vd_sincos(float x, float* s, float* c) { sincosf(x, s, c); }",
@@ -661,7 +1010,7 @@ def generate(lib):
          "template <class T> inline bool vd_isfinite(T x) { return std::isfinite(x); }",
          "#endif", ""]
     for name, cls in ROBOTS:
-        s += emit(name, cls, Robot(grt.packed(lib, name)))
+        s += emit(name, cls, Robot(grt.packed(lib, name), frame_joints(lib, name)))
     s += ["}  // namespace vdk", ""]
     return "\n".join(s)
 
