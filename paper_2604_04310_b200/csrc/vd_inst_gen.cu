@@ -36,28 +36,45 @@ struct Occ {
   int blocks_per_sm = 0, sms = 0;
 };
 
+// The scratch slabs come from the device's default stream-ordered pool; by
+// default the pool hands memory back to the driver at every synchronisation,
+// which turns each launch's cudaMallocAsync into a real allocation.  Keep it.
+inline void keep_pool_memory(int dev) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
+// Occupancy (and the dynamic shared-memory opt-in) once per device for each
+// kernel instantiation; keyed by <Op, T>, not by the kernel's function type
+// (all variants of one dtype share it).
+template <class Op, class T, class Kern>
+Occ occupancy(Kern kern, size_t smem) {
+  static std::mutex mu;
+  static Occ occ[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  Occ& c = occ[dev & 63];
+  if (!c.blocks_per_sm) {
+    keep_pool_memory(dev);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.blocks_per_sm, kern, kGenBlock, smem);
+    if (c.blocks_per_sm < 1) c.blocks_per_sm = 1;
+  }
+  return c;
+}
+
 template <class Op, class T>
 int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
              int32_t* status) {
   using C = Cfg<Op, T>;
   auto kern = k_gen<Op, T, C::kReg, C::kSmem, C::kMinB>;
   constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
-  static std::mutex mu;
-  static Occ occ[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  Occ o;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    Occ& c = occ[dev & 63];
-    if (!c.blocks_per_sm) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.blocks_per_sm, kern, kGenBlock, smem);
-      if (c.blocks_per_sm < 1) c.blocks_per_sm = 1;
-    }
-    o = c;
-  }
+  const Occ o = occupancy<Op, T>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
   cudaStream_t s = static_cast<cudaStream_t>(L.stream);
   // L2-resident scratch for the slots that are neither in registers nor in
@@ -78,29 +95,11 @@ int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, co
   return (int)e;
 }
 
-// Occupancy (and the dynamic shared-memory opt-in) once per device for each
-// kernel instantiation; keyed by <Op, T>, not by the kernel's function type
-// (all variants of one dtype share it).
-template <class Op, class T, class Kern>
-Occ occupancy(Kern kern, size_t smem) {
-  static std::mutex mu;
-  static Occ occ[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  Occ& c = occ[dev & 63];
-  if (!c.blocks_per_sm) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.blocks_per_sm, kern, kGenBlock, smem);
-    if (c.blocks_per_sm < 1) c.blocks_per_sm = 1;
-  }
-  return c;
-}
-
+// OSC (tools/gen_sweep.cu): fp64 55 slots in shared memory at 3 CTAs/SM,
+// fp32 220 slots at 2 CTAs/SM.
 template <class Op, class T>
 struct OscCfg {
-  static constexpr int kReg = 0, kSmem = 110, kMinB = sizeof(T) == 8 ? 2 : 3;
+  static constexpr int kReg = 0, kSmem = sizeof(T) == 8 ? 55 : 220, kMinB = sizeof(T) == 8 ? 3 : 2;
 };
 
 template <class Op, class T>

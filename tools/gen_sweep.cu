@@ -40,6 +40,35 @@ void run(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_
          fa.localSizeBytes, smem, bps, ms, N / (ms * 1e-3), (double)Op::kFlops * N / (ms * 1e-3) / 1e12, bytes / (ms * 1e-3) / 1e9,
          cudaGetErrorString(cudaGetLastError()));
 }
+template <class Op, class T, int kReg, int kSmem, int kMinB>
+void run_osc(const char* name, int64_t N, T* x, T* y, T* lam, int32_t* st, T* scratch, size_t cap, int n) {
+  if (g_filter && !strstr(name, g_filter)) return;
+  auto kern = k_gen_osc<Op, T, kReg, kSmem, kMinB>;
+  size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int bps = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int64_t grid = (int64_t)sms * bps;
+  if ((size_t)(grid * kGenBlock * gen_scratch_per_thread<Op, T, kReg, kSmem>() * sizeof(T)) > cap) { printf("%s scratch\n", name); return; }
+  OscShared P{};
+  for (int k = 0; k < 9; ++k) P.frame_R[k] = P.target_R[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  P.target_p[2] = 0.3;
+  for (int k = 0; k < 6; ++k) { P.kp[k] = 100; P.kd[k] = 20; }
+  P.posture_kp = 10; P.posture_kd = 2; P.gravity[2] = 9.81; P.epsilon = 1e-6;
+  cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int w = 0; w < 2; ++w) kern<<<grid, kGenBlock, smem>>>(N, x, x + N * n, N, P, y, lam, N, st, scratch);
+  cudaEventRecord(a);
+  const int reps = 5;
+  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, x, x + N * n, N, P, y, lam, N, st, scratch);
+  cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms = 0; cudaEventElapsedTime(&ms, a, b); ms /= reps;
+  printf("%-26s regs %3d lmem %4zu smem %6zu b/SM %d scratch %5.0f MB  %.4f ms  %.3e evals/s  %6.2f TF(gen)  %s\n", name, fa.numRegs,
+         fa.localSizeBytes, smem, bps, grid * kGenBlock * gen_scratch_per_thread<Op, T, kReg, kSmem>() * sizeof(T) / 1e6, ms,
+         N / (ms * 1e-3), (double)Op::kFlops * N / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+}
+
 int main(int argc, char** argv) {
   if (argc > 1) g_filter = argv[1];
   size_t cap = 1ull << 31;
@@ -48,6 +77,21 @@ int main(int argc, char** argv) {
   cudaMalloc(&xd, 3 * N * n * 8); cudaMalloc(&yd, N * n * n * 8); cudaMalloc(&sd, cap); cudaMalloc(&st, N * 4);
   k_fill<<<1024, 256>>>(xd, 3 * N * n, 1);
   using R = GenTree29;
+  {
+    double* lam; cudaMalloc(&lam, 36 * N * 8);
+    run_osc<R::Osc23, double, 0, 110, 2>("t29 osc f64 s110 b2", N, xd, yd, lam, st, sd, cap, n);
+    run_osc<R::Osc23, double, 0, 110, 1>("t29 osc f64 s110 b1", N, xd, yd, lam, st, sd, cap, n);
+    run_osc<R::Osc23, double, 0, 220, 1>("t29 osc f64 s220 b1", N, xd, yd, lam, st, sd, cap, n);
+    run_osc<R::Osc23, double, 0, 55, 3>("t29 osc f64 s55 b3", N, xd, yd, lam, st, sd, cap, n);
+    run_osc<R::Osc23, double, 0, 0, 2>("t29 osc f64 s0 b2", N, xd, yd, lam, st, sd, cap, n);
+    float* lf; cudaMalloc(&lf, 36 * N * 4);
+    float *xf0, *yf0; cudaMalloc(&xf0, 3 * N * n * 4); cudaMalloc(&yf0, N * n * 4);
+    k_fill<<<1024, 256>>>(xf0, 3 * N * n, 1);
+    run_osc<R::Osc23, float, 0, 110, 3>("t29 osc f32 s110 b3", N, xf0, yf0, lf, st, (float*)sd, cap, n);
+    run_osc<R::Osc23, float, 0, 220, 2>("t29 osc f32 s220 b2", N, xf0, yf0, lf, st, (float*)sd, cap, n);
+    run_osc<R::Osc23, float, 0, 110, 2>("t29 osc f32 s110 b2", N, xf0, yf0, lf, st, (float*)sd, cap, n);
+    run_osc<R::Osc23, float, 0, 0, 4>("t29 osc f32 s0 b4", N, xf0, yf0, lf, st, (float*)sd, cap, n);
+  }
   run<R::Rnea, double, 0, 55, 2>("t29 rnea f64 s55 b2", N, xd, yd, st, sd, cap, n);
   run<R::Rnea, double, 0, 55, 3>("t29 rnea f64 s55 b3", N, xd, yd, st, sd, cap, n);
   run<R::Rnea, double, 0, 0, 3>("t29 rnea f64 s0 b3", N, xd, yd, st, sd, cap, n);

@@ -42,6 +42,24 @@ def main():
             rc = lib.vd_crba(dm.handle, code, N, x[0].data_ptr(), N, out.data_ptr(), N, s)
         elif op == "fk":
             rc = lib.vd_fk(dm.handle, code, N, x[0].data_ptr(), N, out.data_ptr(), N, s)
+        elif op == "osc":
+            if _ == 0:
+                frame = "ee" if robot == "chain7" else "l_palm"
+                P = vd._lib.OscParams()
+                P.frame = m.frame_index(frame)
+                pose = vd.frame_transform(dm, torch.zeros((1, n), dtype=torch.float64, device="cuda"), frame)
+                pose = pose.cpu().numpy()[0]
+                for k in range(12):
+                    P.target[k] = float(pose[k])
+                for k in range(6):
+                    P.kp[k], P.kd[k], P.accel_ff[k] = 100.0, 20.0, 0.0
+                post = (ctypes.c_double * n)(*([0.0] * n))
+                P.posture = ctypes.cast(post, vd._lib.Pd)
+                P.posture_kp, P.posture_kd, P.epsilon = 10.0, 2.0, 1e-6
+                P.gravity[0], P.gravity[1], P.gravity[2] = 0.0, 0.0, 9.81
+                lam = torch.empty((36, N), dtype=tdt, device="cuda")
+            rc = lib.vd_osc(dm.handle, code, N, x[0].data_ptr(), x[1].data_ptr(), N, ctypes.byref(P), out.data_ptr(),
+                            lam.data_ptr(), N, None, s)
         else:
             raise SystemExit("unknown op " + op)
         assert rc == 0, lib.vd_last_error()
