@@ -119,9 +119,16 @@ def main():
     import bench
 
     out = {}
-    specs = [("chain7_aba_f64", "k_aba<StaticView<RobotChain7,double>>", 4194304, bench.flops_per_eval("chain7", "aba"), 224),
-             ("tree29_aba_f64", "k_aba<RuntimeView<double>> (tree29)", 262144, bench.flops_per_eval("tree29", "aba"), 928),
-             ("tree29_rnea_f64", "k_rnea<StaticView<RobotTree29,double>>", 262144, bench.flops_per_eval("tree29", "rnea"), 928)]
+    # (key, kernel, states per launch, algorithmic flops / state, algorithmic bytes / state)
+    specs = [("chain7_aba_f64", "k_tiled<StaticView<RobotChain7,double>, OpABA> (TMA-staged)", 4194304,
+              bench.flops_per_eval("chain7", "aba"), 224),
+             ("tree29_aba_f64", "k_gen<GenTree29::Aba, double> (generated)", 262144, bench.flops_per_eval("tree29", "aba"), 928),
+             ("tree29_rnea_f64", "k_gen<GenTree29::Rnea, double> (generated)", 262144,
+              bench.flops_per_eval("tree29", "rnea"), 928),
+             ("tree29_crba_f64", "k_gen<GenTree29::Crba, double> (generated)", 262144,
+              bench.flops_per_eval("tree29", "crba"), 232 + 6728),
+             ("tree29_osc_f64", "k_gen_osc<GenTree29::Osc23, double> (generated, frame l_palm)", 262144, None,
+              464 + 232 + 288)]
     for key, name, states, fl, bps in specs:
         rep = os.path.join(OUT, f"{r}_{key}.ncu-rep")
         if os.path.exists(rep):
