@@ -56,7 +56,7 @@ struct Dual {
 template <>
 __device__ __forceinline__ void sincos_t<Dual<double>>(Dual<double> x, Dual<double>* s, Dual<double>* c) {
   double sv, cv;
-  sincos(x.value, &sv, &cv);
+  vd_sincos_f64(x.value, &sv, &cv);
   *s = Dual<double>(sv, cv * x.tangent);
   *c = Dual<double>(cv, -sv * x.tangent);
 }

@@ -19,10 +19,10 @@ struct G3 {
   T g[3];
 };
 
-template <class V, class A>
+template <bool kFastTrig = false, class V, class A>
 __device__ __forceinline__ void load_motion(const V& mv, const A& q, JM<typename V::S>* jm) {
 #pragma unroll
-  for (int j = 0; j < mv.n(); ++j) jm[j] = joint_motion(mv, j, q[j]);
+  for (int j = 0; j < mv.n(); ++j) jm[j] = joint_motion<V, typename V::Real, kFastTrig>(mv, j, q[j]);
 }
 
 template <class T>
@@ -406,7 +406,7 @@ struct OpABA {
   __device__ __forceinline__ void run(const V& mv, const A& q, const A& qd, const A& tau, int64_t i) const {
     using S = typename V::S;
     JM<S> jm[V::kMax];
-    load_motion(mv, q, jm);
+    load_motion<true>(mv, q, jm);
     S out[V::kMax];
     const bool ok = aba_one<V, false>(mv, jm, qd, tau, g.g, nullptr, out);
     OutCols<T> o{qdd, ldo, i};

@@ -60,6 +60,20 @@ ZERO = K(0.0)
 ONE = K(1.0)
 
 
+# Model constants shared by every routine of the robot being generated.  An
+# fp64 literal costs two UMOVs per use in SASS; a __constant__ table entry
+# would be a c[bank][offset] operand instead, but inside the persistent loop
+# the compiler hoists those loads into registers and spills them (measured:
+# tree29 RNEA 0.14 -> 0.20 ms), so literals are the default (USE_POOL).
+POOL = {}
+USE_POOL = False
+
+
+def _low32_zero(c):
+    import struct
+    return struct.unpack("<Q", struct.pack("<d", c))[0] & 0xFFFFFFFF == 0
+
+
 class Gen:
     def __init__(self):
         self.lines = []
@@ -74,7 +88,11 @@ class Gen:
             return "T(1)"
         if c == -1.0:
             return "T(-1)"
-        return f"T({float.hex(c)})"
+        if _low32_zero(c) or not USE_POOL:  # immediate / literal
+            return f"T({float.hex(c)})"
+        if c not in POOL:
+            POOL[c] = len(POOL)
+        return f"kc<T>({POOL[c]})"
 
     def o(self, a):
         return a.s if a.c is None else self.lit(a.c)
@@ -911,6 +929,32 @@ OPS = [("Aba", gen_aba, lambda n: n, 3),
 
 
 def emit(name, cls, rb):
+    POOL.clear()
+    body = emit_body(name, cls, rb)
+    import struct
+    vals = sorted(POOL, key=lambda c: POOL[c])
+    dv = ", ".join(float.hex(c) for c in vals) or "0.0"
+    fv = ", ".join(float.hex(struct.unpack("<f", struct.pack("<f", c))[0]) + "f" for c in vals) or "0.0f"
+    n = max(1, len(vals))
+    pre = [f"// ---- {name}: {len(vals)} model constants",
+           "#if defined(__CUDACC__)",
+           f"static __constant__ double vd_kd_{name}[{n}] = {{{dv}}};",
+           f"static __constant__ float vd_kf_{name}[{n}] = {{{fv}}};",
+           "#endif",
+           f"static const double vd_hkd_{name}[{n}] = {{{dv}}};",
+           f"static const float vd_hkf_{name}[{n}] = {{{fv}}};"]
+    kc = ["  template <class T>",
+          "  VD_HD static T kc(int i) {",
+          "#if defined(__CUDA_ARCH__)",
+          f"    if constexpr (sizeof(T) == 8) return vd_kd_{name}[i]; else return vd_kf_{name}[i];",
+          "#else",
+          f"    if constexpr (sizeof(T) == 8) return vd_hkd_{name}[i]; else return vd_hkf_{name}[i];",
+          "#endif",
+          "  }"]
+    return pre + body[:4] + kc + body[4:]
+
+
+def emit_body(name, cls, rb):
     out = [f"// ---- {name}",
            f"struct Gen{cls} {{",
            f"  static constexpr int kN = {rb.n};",
@@ -1002,6 +1046,8 @@ def generate(lib):
          "  for (int k = 0; k < 3; ++k) w[k] = f * anti[k];",
          "}", "",
          "#if defined(__CUDA_ARCH__)",
+         "// library sincos here: vd_sincos_f64's __constant__ coefficients get hoisted out of the persistent",
+         "// loop into registers and spilled in these 168/255-register kernels (measured slower)",
          "__device__ __forceinline__ void vd_sincos(double x, double* s, double* c) { sincos(x, s, c); }",
          "__device__ __forceinline__ void vd_sincos(float x, float* s, float* c) { sincosf(x, s, c); }",
          "template <class T> __device__ __forceinline__ bool vd_isfinite(T x) { return isfinite(x); }",
