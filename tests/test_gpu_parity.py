@@ -505,3 +505,19 @@ def test_osc_tree29_frames(vd, cuda, omodels, frame):
     bound = np.maximum(TOL64, 1e-16 * kappa)
     assert np.all(rel_err(tau, tau_ref, axis=1)[ok] <= bound[ok])
     assert np.all(rel_err(lam, lam_ref, axis=1)[ok] <= np.maximum(bound[ok], 1e-10))
+
+
+@pytest.mark.parametrize("wrap", [0.0, 1e3, 1e7])
+def test_aba_large_joint_angles(vd, cuda, omodels, wrap):
+    """The ABA path's fp64 sin/cos (vd_sincos.cuh): Cody-Waite reduction for
+    |q| ≤ 1e6, library fallback above.  Joint angles shifted by 2π·k must give
+    the oracle's result on the same (shifted, rounded) inputs."""
+    om = omodels["chain7"]
+    m, dm = _dm(vd, "chain7")
+    q, qd, _, tau = _states(om, 2048, 71)
+    rng = np.random.default_rng(3)
+    qs = q + 2 * np.pi * np.round(rng.uniform(-wrap, wrap, q.shape))
+    ref, st = om.forward_dynamics(qs, qd, tau)
+    got = _np(vd.forward_dynamics(dm, _t(qs), _t(qd), _t(tau)))
+    cond = np.linalg.cond(om.crba(qs))
+    assert np.all(rel_err(got, ref, axis=1) <= np.maximum(TOL64, 7 * np.finfo(np.float64).eps * cond))
