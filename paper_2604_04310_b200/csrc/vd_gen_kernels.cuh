@@ -87,6 +87,20 @@ struct GenCx {
     if (k < kSmem) return GenMem<T>::lds(sm + (uint32_t)(k * kGenBlock * sizeof(T)));
     return GenMem<T>::ldgs(sb + (k - kSmem) * 32);
   }
+  // a double in slots k, k + 1 (mixed-precision joints of the fp32 routines;
+  // one slot when T is double)
+  __device__ __forceinline__ void st2(int k, double v) {
+    if constexpr (sizeof(T) == 8) {
+      st(k, v);
+    } else {
+      st(k, __int_as_float(__double2loint(v)));
+      st(k + 1, __int_as_float(__double2hiint(v)));
+    }
+  }
+  __device__ __forceinline__ double get2(int k) const {
+    if constexpr (sizeof(T) == 8) return get(k);
+    else return __hiloint2double(__float_as_int(get(k + 1)), __float_as_int(get(k)));
+  }
   __device__ __forceinline__ void y(int, int k, T v) const {
     if (active) out_[k * ldo] = v;
   }

@@ -24,7 +24,7 @@ struct Cfg<GenTree29::Aba, double> {
   static constexpr int kReg = 40, kSmem = 110, kMinB = 2;
 };
 template <>
-struct Cfg<GenTree29::Aba, float> {
+struct Cfg<GenTree29::AbaMixed, float> {
   static constexpr int kReg = 0, kSmem = 110, kMinB = 4;
 };
 template <>
@@ -136,7 +136,9 @@ int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, c
 int launch_gen_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* qdd,
                    int32_t* status) {
   if (L.spec != kTree29) return -1;
-  return launch_op<GenTree29::Aba>(L, q, qd, tau, g3, qdd, status);
+  // fp32: the mixed-precision routine (floating-base trunk in fp64)
+  return L.dtype == 0 ? launch_t<GenTree29::Aba, double>(L, q, qd, tau, g3, qdd, status)
+                      : launch_t<GenTree29::AbaMixed, float>(L, q, qd, tau, g3, qdd, status);
 }
 
 int launch_gen_rnea(const Launch& L, int mode, const void* q, const void* qd, const void* qdd, const double* g3,

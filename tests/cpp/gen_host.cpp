@@ -2,6 +2,7 @@
 // (paper_2604_04310_b200/csrc/vd_gen_robots.cuh) for the CPU test suite:
 // the same generated arithmetic the sm_100a kernels run, checked here against
 // the oracle (tests/test_gen_host.py).  Test infrastructure only.
+#include <cstring>
 #include <vector>
 
 #include "vd_gen_robots.cuh"
@@ -21,6 +22,12 @@ struct HostCx {
   T g(int k) const { return T(G[k]); }
   void st(int k, T v) { slots[k] = v; }
   T get(int k) const { return slots[k]; }
+  void st2(int k, double v) { std::memcpy(&slots[k], &v, sizeof(double)); }  // slots k (and k + 1 for float)
+  double get2(int k) const {
+    double v;
+    std::memcpy(&v, &slots[k], sizeof(double));
+    return v;
+  }
   void y(int o, int k, T v) const { (o == 0 ? Y : Y1)[k * ld + i] = v; }
   T fR(int k) const { return T(P[k]); }
   T fp(int k) const { return T(P[9 + k]); }
@@ -50,7 +57,10 @@ int run(long N, const void* const* x, const double* g, void* y, int* status) {
 template <class R, class T>
 int run_op(int op, long N, const void* const* x, const double* g, void* y, int* status) {
   switch (op) {
-    case 0: return run<typename R::Aba, T>(N, x, g, y, status);
+    case 0:  // fp32: the mixed-precision routine the device uses
+      if constexpr (sizeof(T) == 4) return run<typename R::AbaMixed, T>(N, x, g, y, status);
+      else return run<typename R::Aba, T>(N, x, g, y, status);
+    case 6: return run<typename R::Aba, T>(N, x, g, y, status);  // plain fp32 ABA (comparison)
     case 1: return run<typename R::Rnea, T>(N, x, g, y, status);
     case 2: return run<typename R::RneaBias, T>(N, x, g, y, status);
     case 3: return run<typename R::RneaGrav, T>(N, x, g, y, status);

@@ -79,17 +79,21 @@ class Gen:
         self.lines = []
         self.n = 0
         self.flops = 0
+        # scalar type of emitted temporaries: "T" (the kernel's dtype) or "TD"
+        # (double) for the high-precision joints of a mixed-precision routine
+        self.ty = "T"
 
     # ---------------------------------------------------------------- emission
     def lit(self, c):
+        t = self.ty
         if c == 0.0:
-            return "T(0)"
+            return f"{t}(0)"
         if c == 1.0:
-            return "T(1)"
+            return f"{t}(1)"
         if c == -1.0:
-            return "T(-1)"
-        if _low32_zero(c) or not USE_POOL:  # immediate / literal
-            return f"T({float.hex(c)})"
+            return f"{t}(-1)"
+        if _low32_zero(c) or not USE_POOL or t != "T":  # immediate / literal
+            return f"{t}({float.hex(c)})"
         if c not in POOL:
             POOL[c] = len(POOL)
         return f"kc<T>({POOL[c]})"
@@ -97,10 +101,10 @@ class Gen:
     def o(self, a):
         return a.s if a.c is None else self.lit(a.c)
 
-    def tmp(self, expr, prefix="t"):
+    def tmp(self, expr, prefix="t", ty=None):
         name = f"{prefix}{self.n}"
         self.n += 1
-        self.lines.append(f"  const T {name} = {expr};")
+        self.lines.append(f"  const {ty or self.ty} {name} = {expr};")
         return Ex(s=name)
 
     def raw(self, line):
@@ -393,22 +397,26 @@ class Algo:
     every joint's motion values (cos/sin, or q for prismatic joints) and,
     optionally, q̇ in the first slots."""
 
-    def __init__(self, rb, with_qd_slots):
+    def __init__(self, rb, with_qd_slots, hp=()):
         self.rb = rb
         self.g = Gen()
         self.nslot = 0
+        self.hp = set(hp)  # joints computed in double when T is float
         self.mrefs, self.qdrefs = {}, {}
         g = self.g
+        g.raw("using TD = double;")
         g.raw("bool ok = true;")
         # n independent load -> sincos chains instead of n serialised ones
         for i in range(rb.n):
-            qi = g.tmp(f"cx.x(0, {i})", "q")
+            g.ty = "TD" if i in self.hp else "T"
+            qi = g.tmp(f"cx.x(0, {i})", "q", ty="T")
             if rb.kind[i] == 1:
                 self.mrefs[i] = ("q", self.store(qi))
             else:
-                g.raw(f"T s{i}, c{i};")
-                g.raw(f"vd_sincos({qi.s}, &s{i}, &c{i});")
+                g.raw(f"{g.ty} s{i}, c{i};")
+                g.raw(f"vd_sincos({g.ty}({qi.s}), &s{i}, &c{i});")
                 self.mrefs[i] = ("cs", self.store(Ex(s=f"c{i}")), self.store(Ex(s=f"s{i}")))
+        g.ty = "T"
         if with_qd_slots:
             for i in range(rb.n):
                 self.qdrefs[i] = self.store(g.tmp(f"cx.x(1, {i})", "qd"))
@@ -418,6 +426,10 @@ class Algo:
         if v.c is not None:
             return ("k", v.c)
         k = self.nslot
+        if self.g.ty == "TD":  # a double in two consecutive slots (one when T is double)
+            self.nslot += 2
+            self.g.raw(f"cx.st2({k}, {v.s});")
+            return ("h", k)
         self.nslot += 1
         self.g.raw(f"cx.st({k}, {v.s});")
         return ("s", k)
@@ -425,7 +437,9 @@ class Algo:
     def load(self, ref):
         if ref[0] == "k":
             return K(ref[1])
-        return self.g.tmp(f"cx.get({ref[1]})", "r")
+        if ref[0] == "h":
+            return self.g.tmp(f"cx.get2({ref[1]})", "r", ty="TD")
+        return self.g.tmp(f"cx.get({ref[1]})", "r", ty="T")
 
     def joint(self, i):
         m = self.mrefs[i]
@@ -434,7 +448,7 @@ class Algo:
         return Joint(self.g, self.rb, i, cs=(self.load(m[1]), self.load(m[2])))
 
     def gravity(self):
-        self.g.raw("const T ga0 = cx.g(0), ga1 = cx.g(1), ga2 = cx.g(2);")
+        self.g.raw(f"const {self.g.ty} ga0 = cx.g(0), ga1 = cx.g(1), ga2 = cx.g(2);")
         return [ZERO, ZERO, ZERO, Ex(s="ga0"), Ex(s="ga1"), Ex(s="ga2")]
 
     def finish(self):
@@ -442,18 +456,26 @@ class Algo:
         return self
 
 
-def gen_aba(rb):
+def gen_aba(rb, hp=()):
     """ABA (Featherstone RBDA Table 7.1; oracle forward_dynamics,
     dynamics.hpp:421-444).  x(0) = q, x(1) = q̇, x(2) = τ; y(0, i) = q̈_i.
 
     Pass 1 and pass 2 run as one DFS (only the current root->leaf velocity is
     live; a parent's velocity is rebuilt from its child, v_p = X(v − S q̇));
-    the pass-2 -> pass-3 state per joint (U/D, u/D) goes to slots."""
-    A = Algo(rb, True)
+    the pass-2 -> pass-3 state per joint (U/D, u/D) goes to slots.
+
+    hp: joints whose steps are computed (and whose slots are stored) in double
+    when T is float — mixed precision for the floating-base trunk, where the
+    whole tree's articulated inertia is projected."""
+    A = Algo(rb, True, hp)
     g = A.g
     layout = {}
 
+    def ty(i):
+        g.ty = "TD" if i in A.hp else "T"
+
     def down_up(i, vp):
+        ty(i)
         X = A.joint(i)
         qdi = A.load(A.qdrefs[i])
         v = X.S(qdi) if vp is None else g.vadd(X.motion_to_child(vp), X.S(qdi))
@@ -461,6 +483,7 @@ def gen_aba(rb):
         for c in rb.children[i]:
             (Ic, pc), v = down_up(c, v)
             acc = (Ic, pc) if acc is None else (g.ai_add(acc[0], Ic), g.vadd(acc[1], pc))
+        ty(i)
         if rb.children[i]:  # re-read instead of keeping them live across the subtree
             X = A.joint(i)
             qdi = A.load(A.qdrefs[i])
@@ -472,9 +495,9 @@ def gen_aba(rb):
             pA = g.vadd(pA, acc[1])
         U = g.ai_apply(IA, X.Svec())
         D = X.Sdot(U)
-        g.raw(f"ok = ok && ({g.o(D)} > T(0));")
-        dinv = g.tmp(f"T(1) / {g.o(D)}", "di")
-        taui = g.tmp(f"cx.x(2, {i})", "ta")
+        g.raw(f"ok = ok && ({g.o(D)} > {g.ty}(0));")
+        dinv = g.tmp(f"{g.ty}(1) / {g.o(D)}", "di")
+        taui = g.tmp(f"cx.x(2, {i})", "ta", ty="T")
         u = g.sub(taui, X.Sdot(pA))
         Ud = [g.mul(x, dinv) for x in U]
         ud = g.mul(u, dinv)
@@ -492,9 +515,11 @@ def gen_aba(rb):
 
     for r in rb.roots:
         down_up(r, None)
+    ty(rb.roots[0])
     gvec = A.gravity()
 
     def down(i, vp, ap):
+        ty(i)
         udr, Udr = layout[i]
         X = A.joint(i)
         qdi = A.load(A.qdrefs[i])
@@ -920,7 +945,21 @@ def gen_osc(rb, fj):
 
 
 # (struct name, generator, output planes as a function of n, input groups)
+def trunk(rb):
+    """Root chain up to and including the first joint with several children
+    (tree29: the six floating-base joints); empty for serial chains."""
+    out, i = [], rb.roots[0] if rb.roots else -1
+    while i >= 0:
+        out.append(i)
+        if len(rb.children[i]) != 1:
+            break
+        i = rb.children[i][0]
+    return out if i >= 0 and len(rb.children[i]) > 1 else []
+
+
 OPS = [("Aba", gen_aba, lambda n: n, 3),
+       # fp32 kernels: the floating-base trunk in fp64 (DESIGN.md §Parity policy)
+       ("AbaMixed", lambda rb: gen_aba(rb, trunk(rb)), lambda n: n, 3),
        ("Rnea", lambda rb: gen_rnea(rb, True, True), lambda n: n, 3),
        ("RneaBias", lambda rb: gen_rnea(rb, True, False), lambda n: n, 2),
        ("RneaGrav", lambda rb: gen_rnea(rb, False, False), lambda n: n, 1),
