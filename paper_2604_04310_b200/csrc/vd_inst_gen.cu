@@ -24,8 +24,8 @@ struct Cfg<GenTree29::Aba, double> {
   static constexpr int kReg = 40, kSmem = 110, kMinB = 2;
 };
 template <>
-struct Cfg<GenTree29::AbaMixed, float> {
-  static constexpr int kReg = 0, kSmem = 110, kMinB = 4;
+struct Cfg<GenTree29::AbaMixed, float> {  // the trunk's fp64 slots (stored last) in registers
+  static constexpr int kReg = 40, kSmem = 110, kMinB = 3;
 };
 template <>
 struct Cfg<GenTree29::Crba, double> {

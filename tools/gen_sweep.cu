@@ -109,6 +109,12 @@ int main(int argc, char** argv) {
   run<R::Fk, double, 55, 0, 3>("t29 fk f64 r55 b3", N, xd, yd, st, sd, cap, n);
   cudaMalloc(&xf, 3 * N * n * 4); cudaMalloc(&yf, N * n * n * 4); cudaMalloc(&sf, cap);
   k_fill<<<1024, 256>>>(xf, 3 * N * n, 1);
+  run<R::AbaMixed, float, 0, 110, 4>("t29 abamix f32 s110 b4", N, xf, yf, st, sf, cap, n);
+  run<R::AbaMixed, float, 0, 160, 3>("t29 abamix f32 s160 b3", N, xf, yf, st, sf, cap, n);
+  run<R::AbaMixed, float, 0, 220, 2>("t29 abamix f32 s220 b2", N, xf, yf, st, sf, cap, n);
+  run<R::AbaMixed, float, 0, 0, 4>("t29 abamix f32 s0 b4", N, xf, yf, st, sf, cap, n);
+  run<R::AbaMixed, float, 40, 110, 3>("t29 abamix f32 r40 s110 b3", N, xf, yf, st, sf, cap, n);
+  run<R::Aba, float, 0, 110, 4>("t29 aba(plain) f32 s110 b4", N, xf, yf, st, sf, cap, n);
   run<R::Rnea, float, 0, 55, 3>("t29 rnea f32 s55 b3", N, xf, yf, st, sf, cap, n);
   run<R::Rnea, float, 0, 55, 4>("t29 rnea f32 s55 b4", N, xf, yf, st, sf, cap, n);
   run<R::Rnea, float, 55, 0, 3>("t29 rnea f32 r55 b3", N, xf, yf, st, sf, cap, n);
