@@ -309,6 +309,17 @@ def run_ours(args):
         "hbm_gbs_achieved": round(bytes_per_eval * N / (ms_local * 1e-3) / 1e9, 1), "hbm_gbs_peak": hbm,
         "hbm_frac": round(bytes_per_eval * N / (ms_local * 1e-3) / 1e9 / hbm, 4),
     }
+    # DRAM traffic per launch of this kernel at this N from the committed
+    # `ncu --set full` capture (tools/capture_profiles.sh; ncu cannot run
+    # inside the timed bench)
+    prof = os.path.join(ROOT, "profiles", "r01_chain7_aba_f64.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            pj = json.load(f)
+        if int(pj.get("states_per_launch", 0)) == N:
+            roofline["traffic"] = pj["dram_bytes_per_launch"]
+            roofline["traffic_over_algorithmic"] = pj["traffic_over_algorithmic"]
+            roofline["traffic_source"] = "profiles/r01_chain7_aba_f64.json (ncu --set full, dram__bytes_read+write)"
 
     # ---------------- e2e through the public host API (pinned buffers)
     e2e = None
