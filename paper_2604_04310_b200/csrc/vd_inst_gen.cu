@@ -25,11 +25,23 @@ struct Cfg<GenTree29::Aba, double> {
 };
 template <>
 struct Cfg<GenTree29::AbaMixed, float> {  // the trunk's fp64 slots (stored last) in registers
-  static constexpr int kReg = 40, kSmem = 110, kMinB = 3;
+  static constexpr int kReg = 40, kSmem = 122, kMinB = 3;
 };
 template <>
 struct Cfg<GenTree29::Crba, double> {
   static constexpr int kReg = 0, kSmem = 40, kMinB = 4;
+};
+template <>
+struct Cfg<GenTree29::Rnea, double> {  // prologue: cos/sin, q̇, q̈ of every joint
+  static constexpr int kReg = 58, kSmem = 55, kMinB = 2;
+};
+template <>
+struct Cfg<GenTree29::Rnea, float> {
+  static constexpr int kReg = 55, kSmem = 0, kMinB = 3;
+};
+template <>
+struct Cfg<GenTree29::RneaBias, double> {
+  static constexpr int kReg = 0, kSmem = 72, kMinB = 3;
 };
 
 struct Occ {

@@ -92,13 +92,17 @@ int main(int argc, char** argv) {
     run_osc<R::Osc23, float, 0, 110, 2>("t29 osc f32 s110 b2", N, xf0, yf0, lf, st, (float*)sd, cap, n);
     run_osc<R::Osc23, float, 0, 0, 4>("t29 osc f32 s0 b4", N, xf0, yf0, lf, st, (float*)sd, cap, n);
   }
-  run<R::Rnea, double, 0, 55, 2>("t29 rnea f64 s55 b2", N, xd, yd, st, sd, cap, n);
   run<R::Rnea, double, 0, 55, 3>("t29 rnea f64 s55 b3", N, xd, yd, st, sd, cap, n);
+  run<R::Rnea, double, 0, 113, 2>("t29 rnea f64 s113 b2", N, xd, yd, st, sd, cap, n);
   run<R::Rnea, double, 0, 0, 3>("t29 rnea f64 s0 b3", N, xd, yd, st, sd, cap, n);
-  run<R::Rnea, double, 0, 0, 4>("t29 rnea f64 s0 b4", N, xd, yd, st, sd, cap, n);
-  run<R::Rnea, double, 0, 40, 4>("t29 rnea f64 s40 b4", N, xd, yd, st, sd, cap, n);
+  run<R::Rnea, double, 58, 55, 2>("t29 rnea f64 r58 s55 b2", N, xd, yd, st, sd, cap, n);
+  run<R::Rnea, double, 0, 72, 3>("t29 rnea f64 s72 b3", N, xd, yd, st, sd, cap, n);
   run<R::RneaBias, double, 0, 55, 3>("t29 bias f64 s55 b3", N, xd, yd, st, sd, cap, n);
+  run<R::RneaBias, double, 0, 72, 3>("t29 bias f64 s72 b3", N, xd, yd, st, sd, cap, n);
   run<R::RneaGrav, double, 0, 55, 3>("t29 grav f64 s55 b3", N, xd, yd, st, sd, cap, n);
+  run<R::Aba, double, 40, 110, 2>("t29 aba f64 r40 s110 b2", N, xd, yd, st, sd, cap, n);
+  run<R::Aba, double, 40, 113, 2>("t29 aba f64 r40 s113 b2", N, xd, yd, st, sd, cap, n);
+  run<R::Aba, double, 40, 72, 3>("t29 aba f64 r40 s72 b3", N, xd, yd, st, sd, cap, n);
   run<R::Crba, double, 0, 55, 2>("t29 crba f64 s55 b2", N, xd, yd, st, sd, cap, n);
   run<R::Crba, double, 0, 55, 3>("t29 crba f64 s55 b3", N, xd, yd, st, sd, cap, n);
   run<R::Crba, double, 0, 0, 4>("t29 crba f64 s0 b4", N, xd, yd, st, sd, cap, n);
@@ -109,14 +113,12 @@ int main(int argc, char** argv) {
   run<R::Fk, double, 55, 0, 3>("t29 fk f64 r55 b3", N, xd, yd, st, sd, cap, n);
   cudaMalloc(&xf, 3 * N * n * 4); cudaMalloc(&yf, N * n * n * 4); cudaMalloc(&sf, cap);
   k_fill<<<1024, 256>>>(xf, 3 * N * n, 1);
-  run<R::AbaMixed, float, 0, 110, 4>("t29 abamix f32 s110 b4", N, xf, yf, st, sf, cap, n);
-  run<R::AbaMixed, float, 0, 160, 3>("t29 abamix f32 s160 b3", N, xf, yf, st, sf, cap, n);
-  run<R::AbaMixed, float, 0, 220, 2>("t29 abamix f32 s220 b2", N, xf, yf, st, sf, cap, n);
-  run<R::AbaMixed, float, 0, 0, 4>("t29 abamix f32 s0 b4", N, xf, yf, st, sf, cap, n);
   run<R::AbaMixed, float, 40, 110, 3>("t29 abamix f32 r40 s110 b3", N, xf, yf, st, sf, cap, n);
-  run<R::Aba, float, 0, 110, 4>("t29 aba(plain) f32 s110 b4", N, xf, yf, st, sf, cap, n);
-  run<R::Rnea, float, 0, 55, 3>("t29 rnea f32 s55 b3", N, xf, yf, st, sf, cap, n);
+  run<R::AbaMixed, float, 40, 122, 3>("t29 abamix f32 r40 s122 b3", N, xf, yf, st, sf, cap, n);
+  run<R::AbaMixed, float, 40, 160, 3>("t29 abamix f32 r40 s160 b3", N, xf, yf, st, sf, cap, n);
   run<R::Rnea, float, 0, 55, 4>("t29 rnea f32 s55 b4", N, xf, yf, st, sf, cap, n);
+  run<R::Rnea, float, 0, 113, 4>("t29 rnea f32 s113 b4", N, xf, yf, st, sf, cap, n);
+  run<R::Rnea, float, 0, 113, 3>("t29 rnea f32 s113 b3", N, xf, yf, st, sf, cap, n);
   run<R::Rnea, float, 55, 0, 3>("t29 rnea f32 r55 b3", N, xf, yf, st, sf, cap, n);
   run<R::Crba, float, 0, 55, 4>("t29 crba f32 s55 b4", N, xf, yf, st, sf, cap, n);
   run<R::Crba, float, 55, 0, 3>("t29 crba f32 r55 b3", N, xf, yf, st, sf, cap, n);

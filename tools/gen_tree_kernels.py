@@ -397,19 +397,25 @@ class Algo:
     every joint's motion values (cos/sin, or q for prismatic joints) and,
     optionally, q̇ in the first slots."""
 
-    def __init__(self, rb, with_qd_slots, hp=()):
+    def __init__(self, rb, with_qd_slots, hp=(), extra=()):
+        """extra: further input groups (2 = q̈ or τ) loaded by the prologue
+        into slots (self.xrefs[(g, i)])."""
         self.rb = rb
         self.g = Gen()
         self.nslot = 0
         self.hp = set(hp)  # joints computed in double when T is float
-        self.mrefs, self.qdrefs = {}, {}
+        self.mrefs, self.qdrefs, self.xrefs = {}, {}, {}
         g = self.g
         g.raw("using TD = double;")
         g.raw("bool ok = true;")
-        # n independent load -> sincos chains instead of n serialised ones
+        # every input load of the state is issued first (all in flight at
+        # once), then n independent sincos chains
+        qv = [g.tmp(f"cx.x(0, {i})", "q", ty="T") for i in range(rb.n)]
+        qdv = [g.tmp(f"cx.x(1, {i})", "qd", ty="T") for i in range(rb.n)] if with_qd_slots else []
+        xv = {(gi, i): g.tmp(f"cx.x({gi}, {i})", "xa", ty="T") for gi in extra for i in range(rb.n)}
         for i in range(rb.n):
             g.ty = "TD" if i in self.hp else "T"
-            qi = g.tmp(f"cx.x(0, {i})", "q", ty="T")
+            qi = qv[i]
             if rb.kind[i] == 1:
                 self.mrefs[i] = ("q", self.store(qi))
             else:
@@ -417,9 +423,10 @@ class Algo:
                 g.raw(f"vd_sincos({g.ty}({qi.s}), &s{i}, &c{i});")
                 self.mrefs[i] = ("cs", self.store(Ex(s=f"c{i}")), self.store(Ex(s=f"s{i}")))
         g.ty = "T"
-        if with_qd_slots:
-            for i in range(rb.n):
-                self.qdrefs[i] = self.store(g.tmp(f"cx.x(1, {i})", "qd"))
+        for i, v in enumerate(qdv):
+            self.qdrefs[i] = self.store(v)
+        for key, v in xv.items():
+            self.xrefs[key] = self.store(v)
         self.nprologue = self.nslot
 
     def store(self, v):
@@ -456,7 +463,7 @@ class Algo:
         return self
 
 
-def gen_aba(rb, hp=()):
+def gen_aba(rb, hp=(), tau_prologue=False):
     """ABA (Featherstone RBDA Table 7.1; oracle forward_dynamics,
     dynamics.hpp:421-444).  x(0) = q, x(1) = q̇, x(2) = τ; y(0, i) = q̈_i.
 
@@ -467,7 +474,10 @@ def gen_aba(rb, hp=()):
     hp: joints whose steps are computed (and whose slots are stored) in double
     when T is float — mixed precision for the floating-base trunk, where the
     whole tree's articulated inertia is projected."""
-    A = Algo(rb, True, hp)
+    # tau_prologue: τ loaded with q, q̇ up front into slots (faster for the
+    # fp32 routine; for fp64 those 29 slots displace pass-2 state from shared
+    # memory and it measured slower, so τ is read at each joint's pass-2 step)
+    A = Algo(rb, True, hp, extra=(2,) if tau_prologue else ())
     g = A.g
     layout = {}
 
@@ -497,7 +507,7 @@ def gen_aba(rb, hp=()):
         D = X.Sdot(U)
         g.raw(f"ok = ok && ({g.o(D)} > {g.ty}(0));")
         dinv = g.tmp(f"{g.ty}(1) / {g.o(D)}", "di")
-        taui = g.tmp(f"cx.x(2, {i})", "ta", ty="T")
+        taui = A.load(A.xrefs[(2, i)]) if tau_prologue else g.tmp(f"cx.x(2, {i})", "ta", ty="T")
         u = g.sub(taui, X.Sdot(pA))
         Ud = [g.mul(x, dinv) for x in U]
         ud = g.mul(u, dinv)
@@ -548,14 +558,14 @@ def gen_rnea(rb, with_qd, with_qdd):
     with_qdd = False is the bias term c + g (dynamics.hpp:434-435), with_qd =
     False as well the gravity term (dynamics.hpp:403-408).  One DFS: v, a and
     the body's own force on the way down, Σ child forces and τ on the way up."""
-    A = Algo(rb, False)
+    A = Algo(rb, with_qd, extra=(2,) if with_qdd else ())
     g = A.g
     gvec = A.gravity()
 
     def rec(i, vp, ap):
         X = A.joint(i)
-        qdi = g.tmp(f"cx.x(1, {i})", "qd") if with_qd else ZERO
-        qddi = g.tmp(f"cx.x(2, {i})", "qa") if with_qdd else ZERO
+        qdi = A.load(A.qdrefs[i]) if with_qd else ZERO
+        qddi = A.load(A.xrefs[(2, i)]) if with_qdd else ZERO
         if vp is None:
             v = X.S(qdi)
             a = g.vadd(X.motion_to_child(gvec), X.S(qddi))
@@ -959,7 +969,7 @@ def trunk(rb):
 
 OPS = [("Aba", gen_aba, lambda n: n, 3),
        # fp32 kernels: the floating-base trunk in fp64 (DESIGN.md §Parity policy)
-       ("AbaMixed", lambda rb: gen_aba(rb, trunk(rb)), lambda n: n, 3),
+       ("AbaMixed", lambda rb: gen_aba(rb, trunk(rb), tau_prologue=True), lambda n: n, 3),
        ("Rnea", lambda rb: gen_rnea(rb, True, True), lambda n: n, 3),
        ("RneaBias", lambda rb: gen_rnea(rb, True, False), lambda n: n, 2),
        ("RneaGrav", lambda rb: gen_rnea(rb, False, False), lambda n: n, 1),
