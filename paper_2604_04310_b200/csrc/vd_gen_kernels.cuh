@@ -64,8 +64,9 @@ struct GenMem<float> {
   }
 };
 
-template <class T, int kSlots, int kReg, int kSmem>
+template <class T, int kSlots, int kReg, int kSmem, bool kFast = false>
 struct GenCx {
+  static constexpr bool kFastTrig = kFast;  // fp64 sin/cos by vd_sincos_f64
   static constexpr int kGlobal = kSlots - kReg - kSmem > 0 ? kSlots - kReg - kSmem : 0;
   const T* in_[3];  // &x_g[i]; element (i, j) of input g at in_[g][j * ld]
   T* out_;          // &y[i]; element (i, k) at out_[k * ldo]
@@ -76,6 +77,9 @@ struct GenCx {
   T g3[3];
   T reg[kReg > 0 ? kReg : 1];
   __device__ __forceinline__ T x(int g, int j) const { return GenMem<T>::ldg(in_[g] + j * ld); }
+  __device__ __forceinline__ void prefetch(int g, int j) const {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(in_[g] + j * ld));
+  }
   __device__ __forceinline__ T g(int k) const { return g3[k]; }
   __device__ __forceinline__ void st(int k, T v) {
     if (k >= kSlots - kReg) reg[k - (kSlots - kReg)] = v;
@@ -114,12 +118,12 @@ constexpr int64_t gen_scratch_per_thread() {
 
 // One generated routine (Op = GenRobot::Aba / Rnea / RneaBias / RneaGrav /
 // Crba / Fk) over a persistent grid: every thread strides over the batch.
-template <class Op, class T, int kReg, int kSmem, int kMinB>
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false>
 __global__ void __launch_bounds__(kGenBlock, kMinB)
     k_gen(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
           T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status, T* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
-  using Cx = GenCx<T, Op::kSlots, kReg, kSmem>;
+  using Cx = GenCx<T, Op::kSlots, kReg, kSmem, kFast>;
   Cx cx;
   const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * kGenBlock;

@@ -10,6 +10,7 @@
 namespace {
 template <class T>
 struct HostCx {
+  static constexpr bool kFastTrig = false;
   const T* X[3];
   const double* G;
   T* Y;
@@ -19,6 +20,7 @@ struct HostCx {
   const double* P = nullptr;
   T* Y1 = nullptr;
   T x(int g, int j) const { return X[g][j * ld + i]; }
+  void prefetch(int, int) const {}
   T g(int k) const { return T(G[k]); }
   void st(int k, T v) { slots[k] = v; }
   T get(int k) const { return slots[k]; }

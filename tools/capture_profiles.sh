@@ -8,7 +8,7 @@ cap() {  # key op robot dtype N kernel-regex
   ncu --set full --clock-control none --import-source on -k regex:"$6" -s 1 -c 1 -o gpurun_out/${R}_$1 \
       python tools/prof_kernel.py $2 $3 $4 $5 3 > gpurun_out/${R}_$1.ncu.log 2>&1
 }
-cap chain7_aba_f64 aba chain7 f64 4194304 'k_tiled|k_aba'
+cap chain7_aba_f64 aba chain7 f64 4194304 'k_gen|k_tiled|k_aba'
 cap tree29_aba_f64 aba tree29 f64 262144 'k_gen'
 cap tree29_rnea_f64 rnea tree29 f64 262144 'k_gen'
 cap tree29_crba_f64 crba tree29 f64 262144 'k_gen'

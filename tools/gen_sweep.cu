@@ -15,10 +15,10 @@ __global__ void k_fill(T* p, int64_t n, uint64_t seed) {
     p[i] = T((double)(x >> 11) * (1.0 / 9007199254740992.0) * 6.283185307179586 - 3.141592653589793);
   }
 }
-template <class Op, class T, int kReg, int kSmem, int kMinB>
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false>
 void run(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, int n) {
   if (g_filter && !strstr(name, g_filter)) return;
-  auto kern = k_gen<Op, T, kReg, kSmem, kMinB>;
+  auto kern = k_gen<Op, T, kReg, kSmem, kMinB, kFast>;
   size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int bps = 0, sms = 0;
@@ -131,6 +131,13 @@ int main(int argc, char** argv) {
   k_fill<<<1024, 256>>>(x7, 3 * N7 * 7, 2);
   using C = GenChain7;
   run<C::Aba, double, C::Aba::kSlots, 0, 3>("c7 aba f64 allreg b3", N7, x7, y7, st, sd, cap, 7);
+  run<C::Aba, double, C::Aba::kSlots, 0, 4>("c7 aba f64 allreg b4", N7, x7, y7, st, sd, cap, 7);
+  run<C::Aba, double, 44, 28, 3>("c7 aba f64 r44 s28 b3", N7, x7, y7, st, sd, cap, 7);
+  run<C::Aba, double, 44, 28, 4>("c7 aba f64 r44 s28 b4", N7, x7, y7, st, sd, cap, 7);
+  run<C::Aba, double, 44, 28, 4, true>("c7 aba f64 r44 s28 b4 fast", N7, x7, y7, st, sd, cap, 7);
+  run<C::Aba, double, 44, 28, 3, true>("c7 aba f64 r44 s28 b3 fast", N7, x7, y7, st, sd, cap, 7);
+  run<C::Aba, double, 72, 0, 4, true>("c7 aba f64 allreg b4 fast", N7, x7, y7, st, sd, cap, 7);
+  run<C::Aba, double, 0, 28, 4>("c7 aba f64 s28 b4", N7, x7, y7, st, sd, cap, 7);
   run<C::Rnea, double, 14, 0, 3>("c7 rnea f64 r14 b3", N7, x7, y7, st, sd, cap, 7);
   run<C::Rnea, double, 14, 0, 4>("c7 rnea f64 r14 b4", N7, x7, y7, st, sd, cap, 7);
   run<C::Crba, double, 14, 0, 4>("c7 crba f64 r14 b4", N7, x7, y7, st, sd, cap, 7);

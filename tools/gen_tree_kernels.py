@@ -420,7 +420,7 @@ class Algo:
                 self.mrefs[i] = ("q", self.store(qi))
             else:
                 g.raw(f"{g.ty} s{i}, c{i};")
-                g.raw(f"vd_sincos({g.ty}({qi.s}), &s{i}, &c{i});")
+                g.raw(f"vd_sincos_cx<Cx>({g.ty}({qi.s}), &s{i}, &c{i});")
                 self.mrefs[i] = ("cs", self.store(Ex(s=f"c{i}")), self.store(Ex(s=f"s{i}")))
         g.ty = "T"
         for i, v in enumerate(qdv):
@@ -480,6 +480,7 @@ def gen_aba(rb, hp=(), tau_prologue=False):
     A = Algo(rb, True, hp, extra=(2,) if tau_prologue else ())
     g = A.g
     layout = {}
+
 
     def ty(i):
         g.ty = "TD" if i in A.hp else "T"
@@ -1057,7 +1058,7 @@ def generate(lib):
          "// (assets/*.urdf via vdi_model_packed).  Do not edit.  Straight-line, structure-folded",
          "// per-robot routines; see the generator's docstring for the algorithm and its",
          "// reference lines.",
-         "#pragma once", "", "#include <cmath>", "#include <cstdint>", "",
+         "#pragma once", "", "#include <cmath>", "#include <cstdint>", "", "#include \"vd_sincos.cuh\"", "",
          "#ifndef VD_HD", "#if defined(__CUDACC__)", "#define VD_HD __host__ __device__ __forceinline__",
          "#else", "#define VD_HD inline", "#endif", "#endif", "",
          "namespace vdk {", "",
@@ -1103,7 +1104,15 @@ def generate(lib):
          "#else",
          "template <class T> inline void vd_sincos(T x, T* s, T* c) { *s = std::sin(x); *c = std::cos(x); }",
          "template <class T> inline bool vd_isfinite(T x) { return std::isfinite(x); }",
-         "#endif", ""]
+         "#endif",
+         "// Cx::kFastTrig selects vd_sincos_f64 (vd_sincos.cuh) for fp64 on the device",
+         "template <class Cx, class T>",
+         "VD_HD void vd_sincos_cx(T x, T* s, T* c) {",
+         "#if defined(__CUDA_ARCH__)",
+         "  if constexpr (Cx::kFastTrig && sizeof(T) == 8) { vd_sincos_f64(x, s, c); return; }",
+         "#endif",
+         "  vd_sincos(x, s, c);",
+         "}", ""]
     for name, cls in ROBOTS:
         s += emit(name, cls, Robot(grt.packed(lib, name), frame_joints(lib, name)))
     s += ["}  // namespace vdk", ""]

@@ -120,7 +120,7 @@ def main():
 
     out = {}
     # (key, kernel, states per launch, algorithmic flops / state, algorithmic bytes / state)
-    specs = [("chain7_aba_f64", "k_tiled<StaticView<RobotChain7,double>, OpABA> (TMA-staged)", 4194304,
+    specs = [("chain7_aba_f64", "k_gen<GenChain7::Aba, double> (generated, fast fp64 sincos)", 4194304,
               bench.flops_per_eval("chain7", "aba"), 224),
              ("tree29_aba_f64", "k_gen<GenTree29::Aba, double> (generated)", 262144, bench.flops_per_eval("tree29", "aba"), 928),
              ("tree29_rnea_f64", "k_gen<GenTree29::Rnea, double> (generated)", 262144,
