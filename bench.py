@@ -481,7 +481,39 @@ def run_configs(vd, lib, dev, stream, sptr, args, rank, world):
             None, {"note": "tau + Lambda outputs"})
         del q, qd, tau, lam
         torch.cuda.empty_cache()
+    out["batch_sweep"] = batch_sweep(vd, lib, dev, stream, sptr, dc, dt_)
     return out
+
+
+def batch_sweep(vd, lib, dev, stream, sptr, dc, dt_):
+    """evals/s vs batch size (BASELINE.json: "... vs batch"), fp64, device-timed:
+    Panda and G1, ABA and RNEA, from 1 K states (launch/latency bound) to the
+    full configurations (compute bound)."""
+    import torch
+
+    res = {}
+    gen = torch.Generator(device=dev).manual_seed(SEED + 11)
+    for robot, dmod, n, Nmax in (("panda", dc, 7, 4194304), ("g1", dt_, 29, 1048576)):
+        x = [((torch.rand((n, Nmax), generator=gen, device=dev, dtype=torch.float64) * 2 - 1) * np.pi)
+             for _ in range(3)]
+        y = torch.empty((n, Nmax), dtype=torch.float64, device=dev)
+        for op in ("aba", "rnea"):
+            row = {}
+            N = 1024
+            while N <= Nmax:
+                if op == "aba":
+                    fn = lambda N=N: lib.vd_aba(dmod.handle, 0, N, x[0].data_ptr(), x[1].data_ptr(),  # noqa
+                                                x[2].data_ptr(), Nmax, None, None, y.data_ptr(), Nmax, None, sptr)
+                else:
+                    fn = lambda N=N: lib.vd_rnea(dmod.handle, 0, N, x[0].data_ptr(), x[1].data_ptr(),  # noqa
+                                                 x[2].data_ptr(), Nmax, None, None, y.data_ptr(), Nmax, sptr)
+                ms = event_time(fn, 20 if N < 65536 else 10, 3, stream)
+                row[str(N)] = round(N / (ms * 1e-3), 1)
+                N *= 4
+            res[f"{robot}_{op}_f64_evals_per_s"] = row
+        del x, y
+        torch.cuda.empty_cache()
+    return res
 
 
 def main():
