@@ -27,7 +27,7 @@ struct Cfg<GenChain7::Aba, double> {  // the headline kernel: 0.60 ms / 4M state
 };
 template <>
 struct Cfg<GenTree29::Aba, double> {
-  static constexpr int kReg = 40, kSmem = 110, kMinB = 2;
+  static constexpr int kReg = 40, kSmem = 113, kMinB = 2;
   static constexpr bool kFast = false;
 };
 template <>

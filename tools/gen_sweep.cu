@@ -101,6 +101,11 @@ int main(int argc, char** argv) {
   run<R::RneaBias, double, 0, 72, 3>("t29 bias f64 s72 b3", N, xd, yd, st, sd, cap, n);
   run<R::RneaGrav, double, 0, 55, 3>("t29 grav f64 s55 b3", N, xd, yd, st, sd, cap, n);
   run<R::Aba, double, 40, 110, 2>("t29 aba f64 r40 s110 b2", N, xd, yd, st, sd, cap, n);
+  run<R::Aba, double, 20, 110, 2>("t29 aba f64 r20 s110 b2", N, xd, yd, st, sd, cap, n);
+  run<R::Aba, double, 60, 110, 2>("t29 aba f64 r60 s110 b2", N, xd, yd, st, sd, cap, n);
+  run<R::Aba, double, 80, 100, 2>("t29 aba f64 r80 s100 b2", N, xd, yd, st, sd, cap, n);
+  run<R::Aba, double, 40, 84, 2>("t29 aba f64 r40 s84 b2", N, xd, yd, st, sd, cap, n);
+  run<R::Aba, double, 40, 200, 1>("t29 aba f64 r40 s200 b1", N, xd, yd, st, sd, cap, n);
   run<R::Aba, double, 40, 113, 2>("t29 aba f64 r40 s113 b2", N, xd, yd, st, sd, cap, n);
   run<R::Aba, double, 40, 72, 3>("t29 aba f64 r40 s72 b3", N, xd, yd, st, sd, cap, n);
   run<R::Crba, double, 0, 55, 2>("t29 crba f64 s55 b2", N, xd, yd, st, sd, cap, n);
