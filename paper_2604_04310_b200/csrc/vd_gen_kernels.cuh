@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include "vd_gen_robots.cuh"
+#include "vd_launch.hpp"
 #include "vd_shared.hpp"
 
 namespace vdk {
@@ -216,6 +217,66 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
           for (int j = 0; j < 36; ++j) lam[(int64_t)j * ldo + i] = T(0);
       }
       if (status) status[i] = ok ? 0 : 7;
+    }
+  }
+}
+
+// Forward-mode JVP context (JvpArgs): NULL primal inputs read as 0, NULL
+// tangents as 0; output group 0 = values, 1 = tangents (either may be NULL).
+template <class T, int kSlots, int kReg, int kSmem>
+struct GenJvpCx : GenCx<T, kSlots, kReg, kSmem> {
+  const T* din_[3];
+  T* dout_;
+  __device__ __forceinline__ T x(int g, int j) const {
+    return this->in_[g] ? GenMem<T>::ldg(this->in_[g] + j * this->ld) : T(0);
+  }
+  __device__ __forceinline__ T dx(int g, int j) const {
+    return din_[g] ? GenMem<T>::ldg(din_[g] + j * this->ld) : T(0);
+  }
+  __device__ __forceinline__ T g(int k) const { return this->g3[k]; }
+  __device__ __forceinline__ void y(int o, int k, T v) const {
+    T* p = o == 0 ? this->out_ : dout_;
+    if (this->active && p) p[k * this->ldo] = v;
+  }
+};
+
+template <class Op, class T, int kReg, int kSmem, int kMinB>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen_jvp(int64_t N, const __grid_constant__ JvpArgs a, int64_t ldi, int64_t ldo, T* __restrict__ scratch) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenJvpCx<T, Op::kSlots, kReg, kSmem>;
+  Cx cx;
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  cx.sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  cx.sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  for (int k = 0; k < 3; ++k) cx.g3[k] = T(a.g[k]);
+  T* out = (T*)a.out;
+  T* dout = (T*)a.dout;
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    cx.active = i0 < N;
+    const int64_t i = cx.active ? i0 : N - 1;
+    int64_t ld, lo;
+    asm volatile("mov.b64 %0, %1;" : "=l"(ld) : "l"(ldi));
+    asm volatile("mov.b64 %0, %1;" : "=l"(lo) : "l"(ldo));
+    cx.ld = ld;
+    cx.ldo = lo;
+    for (int k = 0; k < 3; ++k) {
+      cx.in_[k] = a.x[k] ? (const T*)a.x[k] + i : nullptr;
+      cx.din_[k] = a.dx[k] ? (const T*)a.dx[k] + i : nullptr;
+    }
+    cx.out_ = out ? out + i : nullptr;
+    cx.dout_ = dout ? dout + i : nullptr;
+    const bool ok = Op::template run<T>(cx);
+    if (cx.active) {
+      if (!ok) {
+        for (int j = 0; j < Op::kOut; ++j) {
+          if (out) out[(int64_t)j * ldo + i] = T(0);
+          if (dout) dout[(int64_t)j * ldo + i] = T(0);
+        }
+      }
+      if (a.status) a.status[i] = ok ? 0 : 7;
     }
   }
 }

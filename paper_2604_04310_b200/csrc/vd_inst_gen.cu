@@ -148,6 +148,31 @@ int launch_osc_t(const Launch& L, const void* q, const void* qd, const OscShared
   return (int)e;
 }
 
+template <class Op, class T>
+struct JvpCfg {
+  static constexpr int kReg = sizeof(T) == 8 ? 40 : 0, kSmem = sizeof(T) == 8 ? 110 : 220, kMinB = 2;
+};
+
+template <class Op, class T>
+int launch_jvp_t(const Launch& L, const JvpArgs& a) {
+  using C = JvpCfg<Op, T>;
+  auto kern = k_gen_jvp<Op, T, C::kReg, C::kSmem, C::kMinB>;
+  constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
+  const Occ o = occupancy<Op, T>(kern, smem);
+  const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
+  cudaStream_t s = static_cast<cudaStream_t>(L.stream);
+  const size_t scratch_bytes = (size_t)blocks * kGenBlock * gen_scratch_per_thread<Op, T, C::kReg, C::kSmem>() * sizeof(T);
+  T* scratch = nullptr;
+  if (scratch_bytes) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_bytes, s);
+    if (e != cudaSuccess) return (int)e;
+  }
+  kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, a, L.ld_in, L.ld_out, scratch);
+  cudaError_t e = cudaGetLastError();
+  if (scratch) cudaFreeAsync(scratch, s);
+  return (int)e;
+}
+
 template <class Op>
 int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
               int32_t* status) {
@@ -191,6 +216,16 @@ int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShar
                       : launch_osc_t<Op, float>(L, q, qd, P, tau, lambda, status);
   });
   return rc;
+}
+
+int launch_gen_jvp(const Launch& L, const JvpArgs& a) {
+  if (L.spec != kTree29 || a.fext) return -1;
+  if (a.op == kJvpABA)
+    return L.dtype == 0 ? launch_jvp_t<GenTree29::AbaJvp, double>(L, a) : launch_jvp_t<GenTree29::AbaJvp, float>(L, a);
+  if (a.op == kJvpRNEA)
+    return L.dtype == 0 ? launch_jvp_t<GenTree29::RneaJvp, double>(L, a)
+                        : launch_jvp_t<GenTree29::RneaJvp, float>(L, a);
+  return -1;
 }
 
 int launch_gen_crba(const Launch& L, const void* q, void* M) {

@@ -64,6 +64,8 @@ struct JvpArgs {
   int32_t* status;    // aba
 };
 int launch_jvp(const Launch& L, const JvpArgs& a);
+// generated dual-number kernels (tree29 ABA / RNEA without f_ext); -1 otherwise
+int launch_gen_jvp(const Launch& L, const JvpArgs& a);
 
 // mode 0: diff_ik_step (out = q̇, aux = pose error); mode 1: manipulability (out = w)
 int launch_task(const Launch& L, const void* q, const TaskShared& P, int mode, void* out, void* aux,

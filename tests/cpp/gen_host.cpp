@@ -19,7 +19,9 @@ struct HostCx {
   // OSC parameters (gen_osc_host layout): fR 9, fp 3, tR 9, tp 3, kp 6, kd 6, aff 6, pkp, pkd, eps, posture n
   const double* P = nullptr;
   T* Y1 = nullptr;
-  T x(int g, int j) const { return X[g][j * ld + i]; }
+  const T* DX[3] = {nullptr, nullptr, nullptr};  // JVP tangents (NULL = 0)
+  T x(int g, int j) const { return X[g] ? X[g][j * ld + i] : T(0); }
+  T dx(int g, int j) const { return DX[g] ? DX[g][j * ld + i] : T(0); }
   void prefetch(int, int) const {}
   T g(int k) const { return T(G[k]); }
   void st(int k, T v) { slots[k] = v; }
@@ -98,6 +100,35 @@ extern "C" int gen_osc_host(int robot, int fj, long N, const double* q, const do
   return robot == 2 ? osc<vdk::GenTree29>(fj, N, q, qd, g, P, tau, lam, status)
                     : osc<vdk::GenChain7>(fj, N, q, qd, g, P, tau, lam, status);
 }
+template <class Op>
+int jvp(long N, const double* const* x, const double* const* dx, const double* g, double* y, double* dy,
+        int* status) {
+  std::vector<double> slots(Op::kSlots + 1);
+  int bad = 0;
+  for (long i = 0; i < N; ++i) {
+    HostCx<double> cx{{x[0], x[1], x[2]}, g, y, N, i, slots.data()};
+    cx.Y1 = dy;
+    for (int k = 0; k < 3; ++k) cx.DX[k] = dx[k];
+    const bool ok = Op::template run<double>(cx);
+    status[i] = ok ? 0 : 7;
+    bad += !ok;
+  }
+  return bad;
+}
+
+// generated forward-mode JVP, fp64: op 0 forward dynamics (ABA), 1 RNEA
+extern "C" int gen_jvp_host(int robot, int op, long N, const double* x0, const double* x1, const double* x2,
+                            const double* dx0, const double* dx1, const double* dx2, const double* g, double* y,
+                            double* dy, int* status) {
+  const double* x[3] = {x0, x1, x2};
+  const double* dx[3] = {dx0, dx1, dx2};
+  if (robot == 2)
+    return op == 0 ? jvp<vdk::GenTree29::AbaJvp>(N, x, dx, g, y, dy, status)
+                   : jvp<vdk::GenTree29::RneaJvp>(N, x, dx, g, y, dy, status);
+  return op == 0 ? jvp<vdk::GenChain7::AbaJvp>(N, x, dx, g, y, dy, status)
+                 : jvp<vdk::GenChain7::RneaJvp>(N, x, dx, g, y, dy, status);
+}
+
 // op: 0 aba, 1 rnea, 2 bias, 3 gravity, 4 crba, 5 fk; robot: 1 chain7, 2 tree29
 extern "C" int gen_run_host(int robot, int op, int f32, long N, const void* x0, const void* x1, const void* x2,
                             const double* g, void* y, int* status) {

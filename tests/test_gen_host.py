@@ -158,3 +158,35 @@ def test_generated_osc_matches_oracle(genlib, name, code, frame):
     assert np.all(e_tau[ok] <= bound[ok]), float((e_tau / bound).max())
     e_lam = rel_err(lam, lam_ref.reshape(N, -1), axis=1)
     assert np.all(e_lam[ok] <= np.maximum(bound[ok], 1e-10)), float(e_lam.max())
+
+
+@pytest.mark.parametrize("name,code", [("chain7", 1), ("tree29", 2)])
+def test_generated_jvp_matches_oracle(genlib, name, code):
+    """Generated dual-number ABA and RNEA against the oracle's Dual
+    restatement (dual.hpp / autodiff.hpp): values and tangents."""
+    om = Model.builtin(name)
+    N = 512
+    q, qd, qdd, tau = om.random_states(N, 81 + code, True, True)
+    rng = np.random.default_rng(5)
+    dq, dqd, dx2 = (rng.uniform(-1, 1, q.shape) for _ in range(3))
+    genlib.gen_jvp_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 10
+    g = np.array([0.0, 0.0, 9.81])
+    F = np.asfortranarray
+    for op, x2, key in ((0, tau, "fd"), (1, qdd, "rnea")):
+        X = [F(q), F(qd), F(x2)]
+        DX = [F(dq), F(dqd), F(dx2)]
+        y = np.zeros_like(X[0], order="F")
+        dy = np.zeros_like(X[0], order="F")
+        st = np.zeros(N, dtype=np.int32)
+        bad = genlib.gen_jvp_host(code, op, N, *[_p(a) for a in X], *[_p(a) for a in DX], _p(g), _p(y), _p(dy), _p(st))
+        assert bad == 0
+        ref = om.jvp(key, (q, qd, x2), (dq, dqd, dx2))
+        rv, rt = ref[0], ref[1]
+        if key == "fd":
+            cond = np.linalg.cond(om.crba(q))
+            ok = cond < 1e5  # tangents of a solve inherit its conditioning twice
+            assert rel_err(y, rv, axis=1)[ok].max() <= 1e-10
+            assert rel_err(dy, rt, axis=1)[ok].max() <= 1e-9
+        else:
+            assert rel_err(y, rv, axis=1).max() <= 1e-10
+            assert rel_err(dy, rt, axis=1).max() <= 1e-10

@@ -110,6 +110,28 @@ class Gen:
     def raw(self, line):
         self.lines.append("  " + line)
 
+    # ---------------------------------------------------------------- hooks (overridden by DGen for JVPs)
+    def input(self, gi, i):
+        return self.tmp(f"cx.x({gi}, {i})", "x", ty="T")
+
+    def sincos(self, q, i):
+        """(cos q, sin q) of joint i's angle, in the current precision."""
+        self.raw(f"{self.ty} s{i}, c{i};")
+        self.raw(f"vd_sincos_cx<Cx>({self.ty}({q.s}), &s{i}, &c{i});")
+        return Ex(s=f"c{i}"), Ex(s=f"s{i}")
+
+    def recip(self, d):
+        return self.tmp(f"{self.ty}(1) / {self.o(d)}", "di")
+
+    def check_pos(self, d):
+        self.raw(f"ok = ok && ({self.o(d)} > {self.ty}(0));")
+
+    def check_finite(self, v):
+        self.raw(f"ok = ok && vd_isfinite({self.o(v)});")
+
+    def output(self, o, k, v):
+        self.raw(f"cx.y({o}, {k}, {self.o(v)});")
+
     # ---------------------------------------------------------------- scalar ops (folding)
     def add(self, a, b):
         if a.c is not None and b.c is not None:
@@ -277,6 +299,84 @@ class Gen:
         return {"A": A, "B": B, "C": o["C"]}
 
 
+class DualEx:
+    """Forward-mode dual scalar (dual.hpp:14-42): value and tangent, each a
+    symbolic Ex (structural zeros fold in both)."""
+
+    __slots__ = ("v", "t")
+
+    def __init__(self, v, t):
+        self.v = v
+        self.t = t
+
+    @property
+    def c(self):  # a constant only when the tangent is exactly zero
+        return self.v.c if (self.v.c is not None and self.t.is0()) else None
+
+    @property
+    def s(self):
+        return None
+
+    def is0(self):
+        return self.v.is0() and self.t.is0()
+
+
+def _lift(x):
+    return x if isinstance(x, DualEx) else DualEx(x, ZERO)
+
+
+class DGen(Gen):
+    """Gen over dual numbers: every spatial-algebra routine of Gen runs
+    unchanged (it is written with add / sub / mul / neg); the hooks load
+    tangents (cx.dx), differentiate sin/cos and 1/x, and write the tangent
+    outputs to output group 1 (the JVP of the same routine)."""
+
+    def add(self, a, b):
+        a, b = _lift(a), _lift(b)
+        return DualEx(Gen.add(self, a.v, b.v), Gen.add(self, a.t, b.t))
+
+    def sub(self, a, b):
+        a, b = _lift(a), _lift(b)
+        return DualEx(Gen.sub(self, a.v, b.v), Gen.sub(self, a.t, b.t))
+
+    def neg(self, a):
+        a = _lift(a)
+        return DualEx(Gen.neg(self, a.v), Gen.neg(self, a.t))
+
+    def mul(self, a, b):
+        a, b = _lift(a), _lift(b)
+        v = Gen.mul(self, a.v, b.v)
+        t = Gen.add(self, Gen.mul(self, a.v, b.t), Gen.mul(self, a.t, b.v))
+        return DualEx(v, t)
+
+    def o(self, a):
+        return Gen.o(self, a.v if isinstance(a, DualEx) else a)
+
+    def input(self, gi, i):
+        return DualEx(self.tmp(f"cx.x({gi}, {i})", "x", ty="T"), self.tmp(f"cx.dx({gi}, {i})", "dx", ty="T"))
+
+    def sincos(self, q, i):
+        c, sn = Gen.sincos(self, q.v, i)
+        # d sin = cos dq, d cos = −sin dq (dual.hpp:97-102)
+        return DualEx(c, Gen.neg(self, Gen.mul(self, sn, q.t))), DualEx(sn, Gen.mul(self, c, q.t))
+
+    def recip(self, d):
+        r = Gen.recip(self, d.v)
+        return DualEx(r, Gen.neg(self, Gen.mul(self, d.t, Gen.mul(self, r, r))))
+
+    def check_pos(self, d):
+        Gen.check_pos(self, d.v)
+
+    def check_finite(self, v):
+        Gen.check_finite(self, v.v)
+        Gen.check_finite(self, v.t)
+
+    def output(self, o, k, v):
+        v = _lift(v)
+        Gen.output(self, 0, k, v.v)
+        Gen.output(self, 1, k, v.t)
+
+
 def frame_joints(lib, name):
     """Joints carrying a named frame with a non-identity offset (fixed-joint
     fused frames such as `l_palm`, `head`), from the library's own model."""
@@ -397,11 +497,11 @@ class Algo:
     every joint's motion values (cos/sin, or q for prismatic joints) and,
     optionally, q̇ in the first slots."""
 
-    def __init__(self, rb, with_qd_slots, hp=(), extra=()):
+    def __init__(self, rb, with_qd_slots, hp=(), extra=(), dual=False):
         """extra: further input groups (2 = q̈ or τ) loaded by the prologue
-        into slots (self.xrefs[(g, i)])."""
+        into slots (self.xrefs[(g, i)]); dual: emit the forward-mode JVP."""
         self.rb = rb
-        self.g = Gen()
+        self.g = DGen() if dual else Gen()
         self.nslot = 0
         self.hp = set(hp)  # joints computed in double when T is float
         self.mrefs, self.qdrefs, self.xrefs = {}, {}, {}
@@ -410,18 +510,17 @@ class Algo:
         g.raw("bool ok = true;")
         # every input load of the state is issued first (all in flight at
         # once), then n independent sincos chains
-        qv = [g.tmp(f"cx.x(0, {i})", "q", ty="T") for i in range(rb.n)]
-        qdv = [g.tmp(f"cx.x(1, {i})", "qd", ty="T") for i in range(rb.n)] if with_qd_slots else []
-        xv = {(gi, i): g.tmp(f"cx.x({gi}, {i})", "xa", ty="T") for gi in extra for i in range(rb.n)}
+        qv = [g.input(0, i) for i in range(rb.n)]
+        qdv = [g.input(1, i) for i in range(rb.n)] if with_qd_slots else []
+        xv = {(gi, i): g.input(gi, i) for gi in extra for i in range(rb.n)}
         for i in range(rb.n):
             g.ty = "TD" if i in self.hp else "T"
             qi = qv[i]
             if rb.kind[i] == 1:
                 self.mrefs[i] = ("q", self.store(qi))
             else:
-                g.raw(f"{g.ty} s{i}, c{i};")
-                g.raw(f"vd_sincos_cx<Cx>({g.ty}({qi.s}), &s{i}, &c{i});")
-                self.mrefs[i] = ("cs", self.store(Ex(s=f"c{i}")), self.store(Ex(s=f"s{i}")))
+                c, sn = g.sincos(qi, i)
+                self.mrefs[i] = ("cs", self.store(c), self.store(sn))
         g.ty = "T"
         for i, v in enumerate(qdv):
             self.qdrefs[i] = self.store(v)
@@ -430,6 +529,8 @@ class Algo:
         self.nprologue = self.nslot
 
     def store(self, v):
+        if isinstance(v, DualEx):  # value and tangent in their own slots
+            return ("d", self.store(v.v), self.store(v.t))
         if v.c is not None:
             return ("k", v.c)
         k = self.nslot
@@ -442,6 +543,8 @@ class Algo:
         return ("s", k)
 
     def load(self, ref):
+        if ref[0] == "d":
+            return DualEx(self.load(ref[1]), self.load(ref[2]))
         if ref[0] == "k":
             return K(ref[1])
         if ref[0] == "h":
@@ -463,7 +566,7 @@ class Algo:
         return self
 
 
-def gen_aba(rb, hp=(), tau_prologue=False):
+def gen_aba(rb, hp=(), tau_prologue=False, dual=False):
     """ABA (Featherstone RBDA Table 7.1; oracle forward_dynamics,
     dynamics.hpp:421-444).  x(0) = q, x(1) = q̇, x(2) = τ; y(0, i) = q̈_i.
 
@@ -477,7 +580,7 @@ def gen_aba(rb, hp=(), tau_prologue=False):
     # tau_prologue: τ loaded with q, q̇ up front into slots (faster for the
     # fp32 routine; for fp64 those 29 slots displace pass-2 state from shared
     # memory and it measured slower, so τ is read at each joint's pass-2 step)
-    A = Algo(rb, True, hp, extra=(2,) if tau_prologue else ())
+    A = Algo(rb, True, hp, extra=(2,) if tau_prologue else (), dual=dual)
     g = A.g
     layout = {}
 
@@ -506,9 +609,9 @@ def gen_aba(rb, hp=(), tau_prologue=False):
             pA = g.vadd(pA, acc[1])
         U = g.ai_apply(IA, X.Svec())
         D = X.Sdot(U)
-        g.raw(f"ok = ok && ({g.o(D)} > {g.ty}(0));")
-        dinv = g.tmp(f"{g.ty}(1) / {g.o(D)}", "di")
-        taui = A.load(A.xrefs[(2, i)]) if tau_prologue else g.tmp(f"cx.x(2, {i})", "ta", ty="T")
+        g.check_pos(D)
+        dinv = g.recip(D)
+        taui = A.load(A.xrefs[(2, i)]) if tau_prologue else g.input(2, i)
         u = g.sub(taui, X.Sdot(pA))
         Ud = [g.mul(x, dinv) for x in U]
         ud = g.mul(u, dinv)
@@ -541,8 +644,8 @@ def gen_aba(rb, hp=(), tau_prologue=False):
             v = g.vadd(X.motion_to_child(vp), X.S(qdi))
             a1 = g.vadd(X.motion_to_child(ap), g.crm(v, X.S(qdi)))
         qdd = g.sub(A.load(udr), g.sdot([A.load(r) for r in Udr], a1))
-        g.raw(f"cx.y(0, {i}, {g.o(qdd)});")
-        g.raw(f"ok = ok && vd_isfinite({g.o(qdd)});")
+        g.output(0, i, qdd)
+        g.check_finite(qdd)
         if rb.children[i]:
             a = g.vadd(a1, X.S(qdd))
             for c in rb.children[i]:
@@ -553,13 +656,13 @@ def gen_aba(rb, hp=(), tau_prologue=False):
     return A.finish()
 
 
-def gen_rnea(rb, with_qd, with_qdd):
+def gen_rnea(rb, with_qd, with_qdd, dual=False):
     """RNEA (rnea_loop, dynamics.hpp:272-327; Alg. 1 of PAPER.md:141-151):
     x(0) = q, x(1) = q̇ (if with_qd), x(2) = q̈ (if with_qdd); y(0, i) = τ_i.
     with_qdd = False is the bias term c + g (dynamics.hpp:434-435), with_qd =
     False as well the gravity term (dynamics.hpp:403-408).  One DFS: v, a and
     the body's own force on the way down, Σ child forces and τ on the way up."""
-    A = Algo(rb, with_qd, extra=(2,) if with_qdd else ())
+    A = Algo(rb, with_qd, extra=(2,) if with_qdd else (), dual=dual)
     g = A.g
     gvec = A.gravity()
 
@@ -580,7 +683,7 @@ def gen_rnea(rb, with_qd, with_qdd):
         if rb.children[i]:
             X = A.joint(i)
         tau = X.Sdot(f)
-        g.raw(f"cx.y(0, {i}, {g.o(tau)});")
+        g.output(0, i, tau)
         return X.force_to_parent(f) if vp is not None else None
 
     for r in rb.roots:
@@ -975,6 +1078,10 @@ OPS = [("Aba", gen_aba, lambda n: n, 3),
        ("RneaBias", lambda rb: gen_rnea(rb, True, False), lambda n: n, 2),
        ("RneaGrav", lambda rb: gen_rnea(rb, False, False), lambda n: n, 1),
        ("Crba", gen_crba, lambda n: n * n, 1),
+       # forward-mode JVPs (autodiff.hpp:41-50 on dual.hpp scalars): value in
+       # output group 0, tangent in group 1
+       ("AbaJvp", lambda rb: gen_aba(rb, dual=True), lambda n: n, 3),
+       ("RneaJvp", lambda rb: gen_rnea(rb, True, True, dual=True), lambda n: n, 3),
        ("Fk", gen_fk, lambda n: 12 * n, 1)]
 
 
