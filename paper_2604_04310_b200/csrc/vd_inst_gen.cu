@@ -219,13 +219,16 @@ int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShar
 }
 
 int launch_gen_jvp(const Launch& L, const JvpArgs& a) {
-  if (L.spec != kTree29 || a.fext) return -1;
+  if (L.spec != kTree29 || (a.fext && (a.op == kJvpABA || a.op == kJvpRNEA))) return -1;
   if (a.op == kJvpABA)
     return L.dtype == 0 ? launch_jvp_t<GenTree29::AbaJvp, double>(L, a) : launch_jvp_t<GenTree29::AbaJvp, float>(L, a);
   if (a.op == kJvpRNEA)
     return L.dtype == 0 ? launch_jvp_t<GenTree29::RneaJvp, double>(L, a)
                         : launch_jvp_t<GenTree29::RneaJvp, float>(L, a);
-  return -1;
+  if (a.op == kJvpCRBA)
+    return L.dtype == 0 ? launch_jvp_t<GenTree29::CrbaJvp, double>(L, a)
+                        : launch_jvp_t<GenTree29::CrbaJvp, float>(L, a);
+  return L.dtype == 0 ? launch_jvp_t<GenTree29::FkJvp, double>(L, a) : launch_jvp_t<GenTree29::FkJvp, float>(L, a);
 }
 
 int launch_gen_crba(const Launch& L, const void* q, void* M) {

@@ -116,15 +116,20 @@ int jvp(long N, const double* const* x, const double* const* dx, const double* g
   return bad;
 }
 
-// generated forward-mode JVP, fp64: op 0 forward dynamics (ABA), 1 RNEA
+// generated forward-mode JVP, fp64: op 0 forward dynamics (ABA), 1 RNEA, 2 CRBA, 3 FK (tree29)
 extern "C" int gen_jvp_host(int robot, int op, long N, const double* x0, const double* x1, const double* x2,
                             const double* dx0, const double* dx1, const double* dx2, const double* g, double* y,
                             double* dy, int* status) {
   const double* x[3] = {x0, x1, x2};
   const double* dx[3] = {dx0, dx1, dx2};
-  if (robot == 2)
-    return op == 0 ? jvp<vdk::GenTree29::AbaJvp>(N, x, dx, g, y, dy, status)
-                   : jvp<vdk::GenTree29::RneaJvp>(N, x, dx, g, y, dy, status);
+  if (robot == 2) {
+    switch (op) {
+      case 0: return jvp<vdk::GenTree29::AbaJvp>(N, x, dx, g, y, dy, status);
+      case 1: return jvp<vdk::GenTree29::RneaJvp>(N, x, dx, g, y, dy, status);
+      case 2: return jvp<vdk::GenTree29::CrbaJvp>(N, x, dx, g, y, dy, status);
+      default: return jvp<vdk::GenTree29::FkJvp>(N, x, dx, g, y, dy, status);
+    }
+  }
   return op == 0 ? jvp<vdk::GenChain7::AbaJvp>(N, x, dx, g, y, dy, status)
                  : jvp<vdk::GenChain7::RneaJvp>(N, x, dx, g, y, dy, status);
 }

@@ -190,3 +190,26 @@ def test_generated_jvp_matches_oracle(genlib, name, code):
         else:
             assert rel_err(y, rv, axis=1).max() <= 1e-10
             assert rel_err(dy, rt, axis=1).max() <= 1e-10
+
+
+def test_generated_crba_fk_jvp_matches_oracle(genlib):
+    """Generated dual-number CRBA and FK (tree29) against the oracle."""
+    om = Model.builtin("tree29")
+    N, n = 256, om.n
+    q, _, _, _ = om.random_states(N, 91, True, False)
+    dq = np.random.default_rng(6).uniform(-1, 1, q.shape)
+    genlib.gen_jvp_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 10
+    g = np.array([0.0, 0.0, 9.81])
+    Q, DQ = np.asfortranarray(q), np.asfortranarray(dq)
+    for op, key, K in ((2, "crba", n * n), (3, "fk", 12 * n)):
+        y = np.zeros((N, K), order="F")
+        dy = np.zeros((N, K), order="F")
+        st = np.zeros(N, dtype=np.int32)
+        genlib.gen_jvp_host(2, op, N, _p(Q), None, None, _p(DQ), None, None, _p(g), _p(y), _p(dy), _p(st))
+        rv, rt = om.jvp(key, (q,), (dq,))
+        if key == "crba":
+            rv, rt = (a.transpose(0, 2, 1).reshape(N, -1) for a in (rv, rt))
+        else:
+            rv, rt = rv.reshape(N, -1), rt.reshape(N, -1)
+        assert rel_err(y, rv, axis=1).max() <= 1e-10
+        assert rel_err(dy, rt, axis=1).max() <= 1e-10

@@ -691,23 +691,23 @@ def gen_rnea(rb, with_qd, with_qdd, dual=False):
     return A.finish()
 
 
-def gen_crba(rb):
+def gen_crba(rb, dual=False):
     """CRBA (crba_loop, dynamics.hpp:369-400; Alg. 2 of PAPER.md:156-165):
     x(0) = q; y(0, c·n + r) = M(r, c), dense, with exact zeros between
     branches (dynamics.hpp:330-335, test_dynamics.cpp:200-216).  Composite
     inertias (10-parameter form) are summed leaf -> root in one DFS; each
     column is emitted as soon as its composite is complete, walking the force
     F = Ic S up the ancestor chain."""
-    A = Algo(rb, False)
+    A = Algo(rb, False, dual=dual)
     g = A.g
     n = rb.n
     related = [[False] * n for _ in range(n)]
 
     def emit(r, c, val):
         related[r][c] = related[c][r] = True
-        g.raw(f"cx.y(0, {c * n + r}, {g.o(val)});")
+        g.output(0, c * n + r, val)
         if r != c:
-            g.raw(f"cx.y(0, {r * n + c}, {g.o(val)});")
+            g.output(0, r * n + c, val)
 
     def rec(i):
         Ic = rb.rb(i)
@@ -731,7 +731,7 @@ def gen_crba(rb):
     for c in range(n):
         for r in range(n):
             if not related[r][c]:
-                g.raw(f"cx.y(0, {c * n + r}, T(0));")
+                g.output(0, c * n + r, ZERO)
     return A.finish()
 
 
@@ -761,10 +761,10 @@ def rb_to_parent(g, X, b):
     return rb_out(g, rb_out(g, b, X.QJ, X.tJ), X.QO, X.tO)
 
 
-def gen_fk(rb):
+def gen_fk(rb, dual=False):
     """forward_kinematics (kinematics.hpp:43-56): x(0) = q; y(0, 12 j + 3 c + r)
     = ⁰R_j(r, c) (column-major), y(0, 12 j + 9 + r) = ⁰p_j(r)."""
-    A = Algo(rb, False)
+    A = Algo(rb, False, dual=dual)
     g = A.g
 
     def rec(i, Wp):
@@ -779,9 +779,9 @@ def gen_fk(rb):
             p = g.vadd(g.matvec(WR, pl), Wpp)
         for c in range(3):
             for r in range(3):
-                g.raw(f"cx.y(0, {12 * i + 3 * c + r}, {g.o(R[3 * r + c])});")
+                g.output(0, 12 * i + 3 * c + r, R[3 * r + c])
         for r in range(3):
-            g.raw(f"cx.y(0, {12 * i + 9 + r}, {g.o(p[r])});")
+            g.output(0, 12 * i + 9 + r, p[r])
         for c in rb.children[i]:
             rec(c, (R, p))
 
@@ -1082,6 +1082,8 @@ OPS = [("Aba", gen_aba, lambda n: n, 3),
        # output group 0, tangent in group 1
        ("AbaJvp", lambda rb: gen_aba(rb, dual=True), lambda n: n, 3),
        ("RneaJvp", lambda rb: gen_rnea(rb, True, True, dual=True), lambda n: n, 3),
+       ("CrbaJvp", lambda rb: gen_crba(rb, dual=True), lambda n: n * n, 1),
+       ("FkJvp", lambda rb: gen_fk(rb, dual=True), lambda n: 12 * n, 1),
        ("Fk", gen_fk, lambda n: 12 * n, 1)]
 
 
