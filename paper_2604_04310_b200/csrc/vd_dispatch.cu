@@ -39,6 +39,12 @@ int launch_fk(const Launch& L, const void* q, void* out) {
 int launch_jacobian(const Launch& L, const void* q, int frame_joint, const double* frame_R, const double* frame_p,
                     void* pose, void* J) {
   if (L.N == 0) return 0;
+  if (L.spec == kTree29) {
+    TaskShared P{};
+    for (int k = 0; k < 9; ++k) P.frame_R[k] = frame_R[k];
+    for (int k = 0; k < 3; ++k) P.frame_p[k] = frame_p[k];
+    if (const int rc = launch_gen_task(L, 0, frame_joint, P, q, pose, J, nullptr); rc >= 0) return rc;
+  }
   FrameArg fr;
   fr.joint = frame_joint;
   for (int k = 0; k < 9; ++k) fr.R[k] = frame_R[k];
@@ -101,6 +107,10 @@ int launch_osc(const Launch& L, const void* q, const void* qd, const OscShared& 
 int launch_task(const Launch& L, const void* q, const TaskShared& P, int mode, void* out, void* aux,
                 int32_t* status) {
   if (L.N == 0) return 0;
+  if (const int rc = launch_gen_task(L, mode == 0 ? 1 : 2, P.frame_joint, P, q, out, mode == 0 ? aux : nullptr,
+                                     mode == 0 ? status : nullptr);
+      rc >= 0)
+    return rc;
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::task(mv, L, q, P, mode, out, aux, status); });
 }
 

@@ -281,4 +281,57 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
   }
 }
 
+// Task-space context (Jacobian / diff-IK / manipulability): TaskShared in
+// kernel parameter space, two nullable output groups.
+template <class T, int kSlots, int kReg, int kSmem>
+struct GenTaskCx : GenCx<T, kSlots, kReg, kSmem> {
+  const TaskShared* P;
+  T* out1_;
+  __device__ __forceinline__ T fR(int k) const { return T(P->frame_R[k]); }
+  __device__ __forceinline__ T fp(int k) const { return T(P->frame_p[k]); }
+  __device__ __forceinline__ T tR(int k) const { return T(P->target_R[k]); }
+  __device__ __forceinline__ T tp(int k) const { return T(P->target_p[k]); }
+  __device__ __forceinline__ T kp(int k) const { return T(P->kp[k]); }
+  __device__ __forceinline__ T tw(int k) const { return T(P->twist_ff[k]); }
+  __device__ __forceinline__ T damp() const { return T(P->damping); }
+  __device__ __forceinline__ void y(int o, int k, T v) const {
+    T* p = o == 0 ? this->out_ : out1_;
+    if (this->active && p) p[k * this->ldo] = v;
+  }
+};
+
+template <class Op, class T, int kReg, int kSmem, int kMinB>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen_task(int64_t N, const T* __restrict__ q, int64_t ldi, const __grid_constant__ TaskShared P,
+               T* __restrict__ y0, T* __restrict__ y1, int64_t ldo, int32_t* __restrict__ status,
+               T* __restrict__ scratch) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenTaskCx<T, Op::kSlots, kReg, kSmem>;
+  Cx cx;
+  cx.P = &P;
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  cx.sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  cx.sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    cx.active = i0 < N;
+    const int64_t i = cx.active ? i0 : N - 1;
+    int64_t ld, lo;
+    asm volatile("mov.b64 %0, %1;" : "=l"(ld) : "l"(ldi));
+    asm volatile("mov.b64 %0, %1;" : "=l"(lo) : "l"(ldo));
+    cx.ld = ld;
+    cx.ldo = lo;
+    cx.in_[0] = cx.in_[1] = cx.in_[2] = q + i;
+    cx.out_ = y0 ? y0 + i : nullptr;
+    cx.out1_ = y1 ? y1 + i : nullptr;
+    const bool ok = Op::template run<T>(cx);
+    if (cx.active) {
+      if (!ok && y0)
+        for (int j = 0; j < Op::kOut; ++j) y0[(int64_t)j * ldo + i] = T(0);
+      if (status) status[i] = ok ? 0 : 7;
+    }
+  }
+}
+
 }  // namespace vdk

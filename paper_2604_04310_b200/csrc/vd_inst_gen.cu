@@ -173,6 +173,18 @@ int launch_jvp_t(const Launch& L, const JvpArgs& a) {
   return (int)e;
 }
 
+template <class Op, class T>
+int launch_task_t(const Launch& L, const void* q, const TaskShared& P, void* y0, void* y1, int32_t* status) {
+  constexpr int kReg = 0, kSmem = Op::kSlots, kMinB = sizeof(T) == 8 ? 3 : 4;  // path-only state: all on chip
+  auto kern = k_gen_task<Op, T, kReg, kSmem, kMinB>;
+  constexpr size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  const Occ o = occupancy<Op, T>(kern, smem);
+  const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
+  kern<<<(unsigned)blocks, kGenBlock, smem, static_cast<cudaStream_t>(L.stream)>>>(
+      L.N, (const T*)q, L.ld_in, P, (T*)y0, (T*)y1, L.ld_out, status, nullptr);
+  return (int)cudaGetLastError();
+}
+
 template <class Op>
 int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
               int32_t* status) {
@@ -229,6 +241,24 @@ int launch_gen_jvp(const Launch& L, const JvpArgs& a) {
     return L.dtype == 0 ? launch_jvp_t<GenTree29::CrbaJvp, double>(L, a)
                         : launch_jvp_t<GenTree29::CrbaJvp, float>(L, a);
   return L.dtype == 0 ? launch_jvp_t<GenTree29::FkJvp, double>(L, a) : launch_jvp_t<GenTree29::FkJvp, float>(L, a);
+}
+
+// which: 0 Jacobian (y0 pose, y1 J), 1 diff-IK (y0 q̇, y1 err), 2 manipulability (y0 w)
+int launch_gen_task(const Launch& L, int which, int frame_joint, const TaskShared& P, const void* q, void* y0,
+                    void* y1, int32_t* status) {
+  if (L.spec != kTree29) return -1;
+  int rc = -1;
+  GenTree29::with_task(frame_joint, [&](auto jac, auto dik, auto man) {
+    auto go = [&](auto op) {
+      using Op = decltype(op);
+      rc = L.dtype == 0 ? launch_task_t<Op, double>(L, q, P, y0, y1, status)
+                        : launch_task_t<Op, float>(L, q, P, y0, y1, status);
+    };
+    if (which == 0) go(jac);
+    else if (which == 1) go(dik);
+    else go(man);
+  });
+  return rc;
 }
 
 int launch_gen_crba(const Launch& L, const void* q, void* M) {

@@ -45,6 +45,8 @@ int launch_gen_rnea(const Launch& L, int mode, const void* q, const void* qd, co
                     void* tau);
 int launch_gen_crba(const Launch& L, const void* q, void* M);
 int launch_gen_fk(const Launch& L, const void* q, void* frames);
+int launch_gen_task(const Launch& L, int which, int frame_joint, const TaskShared& P, const void* q, void* y0,
+                    void* y1, int32_t* status);
 int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
                    int32_t* status);
 int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,

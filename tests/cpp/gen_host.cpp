@@ -44,6 +44,8 @@ struct HostCx {
   T pkd() const { return T(P[43]); }
   T eps() const { return T(P[44]); }
   T post(int k) const { return T(P[45 + k]); }
+  T tw(int k) const { return T(P[30 + k]); }  // diff-IK: twist_ff in the kd slots, damping in eps
+  T damp() const { return T(P[44]); }
   bool want_lambda() const { return Y1 != nullptr; }
 };
 template <class Op, class T>
@@ -132,6 +134,32 @@ extern "C" int gen_jvp_host(int robot, int op, long N, const double* x0, const d
   }
   return op == 0 ? jvp<vdk::GenChain7::AbaJvp>(N, x, dx, g, y, dy, status)
                  : jvp<vdk::GenChain7::RneaJvp>(N, x, dx, g, y, dy, status);
+}
+
+// generated task-space routine on frame joint fj (fp64): which 0 Jacobian (y0 pose 12, y1 J 6n),
+// 1 diff-IK (y0 q̇, y1 err), 2 manipulability (y0); -1 when no variant exists for fj
+extern "C" int gen_task_host(int which, int fj, long N, const double* q, const double* P, double* y0, double* y1,
+                             int* status) {
+  int bad = -1;
+  vdk::GenTree29::with_task(fj, [&](auto jac, auto dik, auto man) {
+    auto go = [&](auto op) {
+      using Op = decltype(op);
+      std::vector<double> slots(Op::kSlots + 1);
+      bad = 0;
+      for (long i = 0; i < N; ++i) {
+        HostCx<double> cx{{q, q, q}, nullptr, y0, N, i, slots.data()};
+        cx.P = P;
+        cx.Y1 = y1;
+        const bool ok = Op::template run<double>(cx);
+        status[i] = ok ? 0 : 7;
+        bad += !ok;
+      }
+    };
+    if (which == 0) go(jac);
+    else if (which == 1) go(dik);
+    else go(man);
+  });
+  return bad;
 }
 
 // op: 0 aba, 1 rnea, 2 bias, 3 gravity, 4 crba, 5 fk; robot: 1 chain7, 2 tree29

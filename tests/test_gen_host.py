@@ -213,3 +213,40 @@ def test_generated_crba_fk_jvp_matches_oracle(genlib):
             rv, rt = rv.reshape(N, -1), rt.reshape(N, -1)
         assert rel_err(y, rv, axis=1).max() <= 1e-10
         assert rel_err(dy, rt, axis=1).max() <= 1e-10
+
+
+@pytest.mark.parametrize("frame", ["l_palm", "head", "r_foot"])
+def test_generated_task_routines_match_oracle(genlib, frame):
+    """Generated Jacobian / diff-IK / manipulability (kinematics.hpp:89-153,
+    control.hpp:79-97) for G1 task frames against the oracle."""
+    om = Model.builtin("tree29")
+    N = 512
+    q, _, _, _ = om.random_states(N, 93, True, False)
+    fid = {f[0]: f for f in om.frames()}[frame]
+    fj, off = fid[1], fid[2]
+    fR = off[:9].reshape(3, 3, order="F")
+    q0 = np.zeros((1, om.n))
+    pose0, _ = om.jacobian(q0, frame)
+    R0, p0 = pose0[0, :9].reshape(3, 3, order="F"), pose0[0, 9:]
+    kp, tw, damp = [2.0, 2.0, 2.0, 1.0, 1.0, 1.0], [0.1, 0.0, -0.1, 0.0, 0.2, 0.0], 0.05
+    P = np.zeros(45 + om.n)
+    P[:9], P[9:12], P[12:21], P[21:24] = fR.reshape(-1), off[9:], R0.reshape(-1), p0
+    P[24:30], P[30:36], P[44] = kp, tw, damp
+    genlib.gen_task_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 5
+    Q = np.asfortranarray(q)
+    st = np.zeros(N, dtype=np.int32)
+    pose = np.zeros((N, 12), order="F")
+    J = np.zeros((N, 6 * om.n), order="F")
+    assert genlib.gen_task_host(0, fj, N, _p(Q), _p(P), _p(pose), _p(J), _p(st)) == 0
+    rpose, rJ = om.jacobian(q, frame)
+    assert rel_err(pose, rpose, axis=1).max() <= 1e-12
+    assert rel_err(J, rJ.transpose(0, 2, 1).reshape(N, -1), axis=1).max() <= 1e-12  # plane 6 c + r
+    qd = np.zeros((N, om.n), order="F")
+    err = np.zeros((N, 6), order="F")
+    assert genlib.gen_task_host(1, fj, N, _p(Q), _p(P), _p(qd), _p(err), _p(st)) == 0
+    rqd, rerr = om.diff_ik(q, frame, R0, p0, kp, tw, damp)
+    assert rel_err(qd, rqd, axis=1).max() <= 1e-10
+    assert rel_err(err, rerr, axis=1).max() <= 1e-10
+    w = np.zeros((N, 1), order="F")
+    assert genlib.gen_task_host(2, fj, N, _p(Q), _p(P), _p(w), None, _p(st)) == 0
+    assert rel_err(w[:, 0], om.manipulability(q, frame)) <= 1e-10

@@ -497,7 +497,7 @@ class Algo:
     every joint's motion values (cos/sin, or q for prismatic joints) and,
     optionally, q̇ in the first slots."""
 
-    def __init__(self, rb, with_qd_slots, hp=(), extra=(), dual=False):
+    def __init__(self, rb, with_qd_slots, hp=(), extra=(), dual=False, only=None):
         """extra: further input groups (2 = q̈ or τ) loaded by the prologue
         into slots (self.xrefs[(g, i)]); dual: emit the forward-mode JVP."""
         self.rb = rb
@@ -510,10 +510,11 @@ class Algo:
         g.raw("bool ok = true;")
         # every input load of the state is issued first (all in flight at
         # once), then n independent sincos chains
-        qv = [g.input(0, i) for i in range(rb.n)]
+        joints = [i for i in range(rb.n) if only is None or i in only]  # prologue subset
+        qv = {i: g.input(0, i) for i in joints}
         qdv = [g.input(1, i) for i in range(rb.n)] if with_qd_slots else []
         xv = {(gi, i): g.input(gi, i) for gi in extra for i in range(rb.n)}
-        for i in range(rb.n):
+        for i in joints:
             g.ty = "TD" if i in self.hp else "T"
             qi = qv[i]
             if rb.kind[i] == 1:
@@ -1058,6 +1059,120 @@ def gen_osc(rb, fj):
     return A.finish()
 
 
+def frame_pose_J(A, fj):
+    """frame_transform + geometric_jacobian (kinematics.hpp:89-129) of the
+    task frame on joint fj (offset cx.fR / cx.fp, row-major): pose (R
+    row-major 9, p 3) and the Jacobian columns of the path joints (angular
+    rows first; every other column is an exact zero)."""
+    g, rb = A.g, A.rb
+    path = []
+    j = fj
+    while j >= 0:
+        path.append(j)
+        j = rb.parent[j]
+    path = path[::-1]
+    W, Wp = {}, None
+    for i in path:
+        X = A.joint(i)
+        Rl = [g.dot(X.QO[3 * r:3 * r + 3], [X.QJ[c], X.QJ[3 + c], X.QJ[6 + c]]) for r in range(3) for c in range(3)]
+        pl = g.vadd(X.tO, g.matvec(X.QO, X.tJ))
+        if Wp is None:
+            R, p = Rl, pl
+        else:
+            R = [g.dot(Wp[0][3 * r:3 * r + 3], [Rl[c], Rl[3 + c], Rl[6 + c]]) for r in range(3) for c in range(3)]
+            p = g.vadd(g.matvec(Wp[0], pl), Wp[1])
+        W[i] = (R, p)
+        Wp = (R, p)
+    WR, Wpos = W[fj]
+    fR = [g.tmp(f"cx.fR({k})", "pf") for k in range(9)]
+    fpv = [g.tmp(f"cx.fp({k})", "pf") for k in range(3)]
+    pose_R = [g.dot(WR[3 * r:3 * r + 3], [fR[c], fR[3 + c], fR[6 + c]]) for r in range(3) for c in range(3)]
+    pose_p = g.vadd(g.matvec(WR, fpv), Wpos)
+    J = {}
+    for i in path:
+        R, p = W[i]
+        ax = g.matvec(R, rb.axis(i))
+        col = (ax + g.cross3(ax, g.vsub(pose_p, p))) if rb.kind[i] == 0 else ([ZERO] * 3 + ax)
+        for r in range(6):
+            J[(r, i)] = col[r]
+    return pose_R, pose_p, J, path
+
+
+def _path(rb, fj):
+    out = []
+    while fj >= 0:
+        out.append(fj)
+        fj = rb.parent[fj]
+    return set(out)
+
+
+def gen_jac(rb, fj):
+    """x(0) = q; y(0, ·) = frame pose (R column-major, p), y(1, 6 c + r) = J(r, c)."""
+    A = Algo(rb, False, only=_path(rb, fj))
+    g = A.g
+    pose_R, pose_p, J, path = frame_pose_J(A, fj)
+    for c in range(3):
+        for r in range(3):
+            g.raw(f"cx.y(0, {3 * c + r}, {g.o(pose_R[3 * r + c])});")
+    for r in range(3):
+        g.raw(f"cx.y(0, {9 + r}, {g.o(pose_p[r])});")
+    for c in range(rb.n):
+        for r in range(6):
+            g.raw(f"cx.y(1, {6 * c + r}, {g.o(J.get((r, c), ZERO))});")
+    return A.finish()
+
+
+def _gram6(g, J, path, d):
+    G = {}
+    for r in range(6):
+        for c in range(r + 1):
+            v = g.sum([g.mul(J[(r, k)], J[(c, k)]) for k in path])
+            G[(r, c)] = g.add(v, d) if (r == c and d is not None) else v
+    return G
+
+
+def gen_diffik(rb, fj):
+    """diff_ik_step (control.hpp:79-97; vd_algos.cuh diffik_one): q̇ = Jᵀ (J Jᵀ
+    + λ² I)⁻¹ (kp ⊙ err + twist_ff).  y(0, j) = q̇_j (zeroed by the kernel when
+    the damped Gram matrix does not factor), y(1, r) = pose error."""
+    A = Algo(rb, False, only=_path(rb, fj))
+    g = A.g
+    pose_R, pose_p, J, path = frame_pose_J(A, fj)
+    tR = [g.tmp(f"cx.tR({k})", "pt") for k in range(9)]
+    Rrel = [g.dot(tR[3 * r:3 * r + 3], pose_R[3 * c:3 * c + 3]) for r in range(3) for c in range(3)]
+    g.raw(f"const T Rrel_[9] = {{{', '.join(g.o(x) for x in Rrel)}}};")
+    g.raw("T lg_[3];")
+    g.raw("vd_rotation_log(Rrel_, lg_);")
+    err = [Ex(s="lg_[0]"), Ex(s="lg_[1]"), Ex(s="lg_[2]")]
+    err += [g.sub(g.tmp(f"cx.tp({k})", "pt"), pose_p[k]) for k in range(3)]
+    for r in range(6):
+        g.raw(f"cx.y(1, {r}, {g.o(err[r])});")
+    rhs = [g.add(g.mul(g.tmp(f"cx.kp({r})", "pg"), err[r]), g.tmp(f"cx.tw({r})", "pg")) for r in range(6)]
+    lam = g.tmp("cx.damp()", "pd")
+    L, okx = chol6(g, _gram6(g, J, path, g.mul(lam, lam)))
+    g.raw(f"ok = ok && {okx};")
+    x = chol6_solve(g, L, rhs)
+    for j in range(rb.n):
+        v = g.sum([g.mul(J[(r, j)], x[r]) for r in range(6)]) if j in path else ZERO
+        g.raw(f"cx.y(0, {j}, {g.o(v)});")
+    return A.finish()
+
+
+def gen_manip(rb, fj):
+    """manipulability (kinematics.hpp:138-153; vd_algos.cuh manip_one):
+    sqrt(det(J Jᵀ)) as the product of the Cholesky pivots, 0 when it does not
+    factor.  y(0, 0) = w."""
+    A = Algo(rb, False, only=_path(rb, fj))
+    g = A.g
+    _, _, J, path = frame_pose_J(A, fj)
+    L, okx = chol6(g, _gram6(g, J, path, None))
+    d = L[(0, 0)]
+    for i in range(1, 6):
+        d = g.mul(d, L[(i, i)])
+    g.raw(f"cx.y(0, 0, ({okx}) ? {g.o(d)} : T(0));")
+    return A.finish()
+
+
 # (struct name, generator, output planes as a function of n, input groups)
 def trunk(rb):
     """Root chain up to and including the first joint with several children
@@ -1148,7 +1263,30 @@ def emit_body(name, cls, rb):
                 "    VD_HD static bool run(Cx& cx) {"]
         out += ["    " + ln for ln in A.g.lines]
         out += ["    }", "  };"]
+    for fj in osc_joints:
+        for nm, fn, nout in (("Jac", gen_jac, 12), ("DiffIk", gen_diffik, rb.n), ("Manip", gen_manip, 1)):
+            A = fn(rb, fj)
+            out += [f"  // {nm} on joint {fj}: {A.g.flops} mul/add after folding; {A.nslot} slots",
+                    f"  struct {nm}{fj} {{",
+                    f"    static constexpr int kSlots = {A.nslot};",
+                    f"    static constexpr int kPrologue = {A.nprologue};",
+                    f"    static constexpr int kFlops = {A.g.flops};",
+                    "    static constexpr int kIn = 1;",
+                    f"    static constexpr int kOut = {nout};",
+                    "    template <class T, class Cx>",
+                    "    VD_HD static bool run(Cx& cx) {"]
+            out += ["    " + ln for ln in A.g.lines]
+            out += ["    }", "  };"]
     out.append(f"  static constexpr int kOscJoints[] = {{{', '.join(str(j) for j in osc_joints)}}};")
+    out.append("  // calls f(Jac<fj>{}, DiffIk<fj>{}, Manip<fj>{}) for a generated frame joint; false if none")
+    out.append("  template <class F>")
+    out.append("  static bool with_task(int fj, F&& f) {")
+    out.append("    switch (fj) {")
+    for fj in osc_joints:
+        out.append(f"      case {fj}: f(Jac{fj}{{}}, DiffIk{fj}{{}}, Manip{fj}{{}}); return true;")
+    out.append("      default: return false;")
+    out.append("    }")
+    out.append("  }")
     out.append("  // calls f(Osc<fj>{}) for the generated variant of joint fj; false if none")
     out.append("  template <class F>")
     out.append("  static bool with_osc(int fj, F&& f) {")
