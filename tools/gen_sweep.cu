@@ -143,9 +143,23 @@ int main(int argc, char** argv) {
   run<C::Aba, double, 44, 28, 3, true>("c7 aba f64 r44 s28 b3 fast", N7, x7, y7, st, sd, cap, 7);
   run<C::Aba, double, 72, 0, 4, true>("c7 aba f64 allreg b4 fast", N7, x7, y7, st, sd, cap, 7);
   run<C::Aba, double, 0, 28, 4>("c7 aba f64 s28 b4", N7, x7, y7, st, sd, cap, 7);
-  run<C::Rnea, double, 14, 0, 3>("c7 rnea f64 r14 b3", N7, x7, y7, st, sd, cap, 7);
-  run<C::Rnea, double, 14, 0, 4>("c7 rnea f64 r14 b4", N7, x7, y7, st, sd, cap, 7);
-  run<C::Crba, double, 14, 0, 4>("c7 crba f64 r14 b4", N7, x7, y7, st, sd, cap, 7);
-  run<C::Fk, double, 14, 0, 4>("c7 fk f64 r14 b4", N7, x7, y7, st, sd, cap, 7);
+  run<C::Rnea, double, 28, 0, 4, true>("c7 rnea f64 r28 b4 fast", N7, x7, y7, st, sd, cap, 7);
+  run<C::Rnea, double, 28, 0, 3, true>("c7 rnea f64 r28 b3 fast", N7, x7, y7, st, sd, cap, 7);
+  run<C::Rnea, double, 0, 28, 4, true>("c7 rnea f64 s28 b4 fast", N7, x7, y7, st, sd, cap, 7);
+  run<C::Crba, double, 14, 0, 4, true>("c7 crba f64 r14 b4 fast", N7, x7, y7, st, sd, cap, 7);
+  run<C::Fk, double, 14, 0, 4, true>("c7 fk f64 r14 b4 fast", N7, x7, y7, st, sd, cap, 7);
+  {
+    float *x7f, *y7f; cudaMalloc(&x7f, 3 * N7 * 7 * 4); cudaMalloc(&y7f, N7 * 49 * 4);
+    k_fill<<<1024, 256>>>(x7f, 3 * N7 * 7, 2);
+    run<C::Aba, float, C::Aba::kSlots, 0, 4>("c7 aba f32 allreg b4", N7, x7f, y7f, st, (float*)sd, cap, 7);
+    run<C::Aba, float, 44, 28, 4>("c7 aba f32 r44 s28 b4", N7, x7f, y7f, st, (float*)sd, cap, 7);
+    run<C::Aba, float, 44, 28, 6>("c7 aba f32 r44 s28 b6", N7, x7f, y7f, st, (float*)sd, cap, 7);
+    run<C::Rnea, float, 28, 0, 6>("c7 rnea f32 r28 b6", N7, x7f, y7f, st, (float*)sd, cap, 7);
+    double* lam7; cudaMalloc(&lam7, 36 * N7 * 8);
+    run_osc<C::Osc6, double, 0, 55, 3>("c7 osc f64 s55 b3", N7, x7, y7, lam7, st, sd, cap, 7);
+    run_osc<C::Osc6, double, 60, 55, 2>("c7 osc f64 r60 s55 b2", N7, x7, y7, lam7, st, sd, cap, 7);
+    run_osc<C::Osc6, double, 0, 147, 2>("c7 osc f64 s147 b2", N7, x7, y7, lam7, st, sd, cap, 7);
+  }
+
   return 0;
 }
