@@ -140,6 +140,39 @@ def event_time(fn, steps, warmup, stream):
     return e0.elapsed_time(e1) / steps
 
 
+def graph_time(fn_s, steps, warmup, per_graph=20):
+    """Average ms per call of fn_s(stream_ptr), replayed from a CUDA graph of
+    per_graph back-to-back calls on a side stream: for small batches, where
+    one host call per step would time the host launch path instead of the GPU.
+    Falls back to None when capture is not possible."""
+    import torch
+
+    s = torch.cuda.Stream()
+    sp = ctypes.c_void_p(s.cuda_stream)
+    try:
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                fn_s(sp)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(per_graph):
+                fn_s(sp)
+        torch.cuda.synchronize()
+    except Exception:  # noqa: BLE001
+        return None
+    reps = max(2, steps // per_graph)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        g.replay()
+        e0.record(s)
+        for _ in range(reps):
+            g.replay()
+        e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / (reps * per_graph)
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -427,9 +460,14 @@ def run_configs(vd, lib, dev, stream, sptr, args, rank, world):
         pose = torch.empty((12, N), dtype=dt, device=dev)
         J = torch.empty((42, N), dtype=dt, device=dev)
         fid = chain.frame_index("ee")
-        fn = lambda: lib.vd_jacobian(dc.handle, code, N, q.data_ptr(), N, fid, pose.data_ptr(), J.data_ptr(), N, sptr)  # noqa
-        rec(f"2_panda_fk_jacobian_b4096_{'f64' if code == 0 else 'f32'}", N, event_time(fn, 200, 20, stream),
-            flops_per_eval("chain7", "fk"))
+        fn_s = lambda sp: lib.vd_jacobian(dc.handle, code, N, q.data_ptr(), N, fid, pose.data_ptr(),  # noqa
+                                          J.data_ptr(), N, sp)
+        key = f"2_panda_fk_jacobian_b4096_{'f64' if code == 0 else 'f32'}"
+        rec(key, N, event_time(lambda: fn_s(sptr), 200, 20, stream), flops_per_eval("chain7", "fk"))
+        gms = graph_time(fn_s, 400, 20)
+        if gms:  # the per-call loop above is host-launch bound at this size
+            out[key].update({"ms_graph": round(gms, 5), "evals_per_s_graph": N / (gms * 1e-3),
+                             "note": "ms: one host call per step; ms_graph: CUDA-graph replay of the same calls"})
     # config 3: Panda M + bias + ABA (fused), batch 65536, fp32 and fp64
     for dt, code in ((torch.float64, 0), (torch.float32, 1)):
         N = 65536
@@ -488,7 +526,8 @@ def run_configs(vd, lib, dev, stream, sptr, args, rank, world):
 def batch_sweep(vd, lib, dev, stream, sptr, dc, dt_):
     """evals/s vs batch size (BASELINE.json: "... vs batch"), fp64, device-timed:
     Panda and G1, ABA and RNEA, from 1 K states (launch/latency bound) to the
-    full configurations (compute bound)."""
+    full configurations (compute bound).  Sizes ≤ 64 K are also timed as CUDA
+    graph replays (no host launch path per call); the faster figure is kept."""
     import torch
 
     res = {}
@@ -508,6 +547,16 @@ def batch_sweep(vd, lib, dev, stream, sptr, dc, dt_):
                     fn = lambda N=N: lib.vd_rnea(dmod.handle, 0, N, x[0].data_ptr(), x[1].data_ptr(),  # noqa
                                                  x[2].data_ptr(), Nmax, None, None, y.data_ptr(), Nmax, sptr)
                 ms = event_time(fn, 20 if N < 65536 else 10, 3, stream)
+                if N <= 65536:  # launch-bound sizes: time graph replays of the same call
+                    if op == "aba":
+                        fs = lambda sp, N=N: lib.vd_aba(dmod.handle, 0, N, x[0].data_ptr(), x[1].data_ptr(),  # noqa
+                                                        x[2].data_ptr(), Nmax, None, None, y.data_ptr(), Nmax, None,
+                                                        sp)
+                    else:
+                        fs = lambda sp, N=N: lib.vd_rnea(dmod.handle, 0, N, x[0].data_ptr(), x[1].data_ptr(),  # noqa
+                                                         x[2].data_ptr(), Nmax, None, None, y.data_ptr(), Nmax, sp)
+                    gms = graph_time(fs, 100, 3)
+                    ms = min(ms, gms) if gms else ms
                 row[str(N)] = round(N / (ms * 1e-3), 1)
                 N *= 4
             res[f"{robot}_{op}_f64_evals_per_s"] = row

@@ -143,6 +143,8 @@ vdk::Launch make_launch(vd_device_model dm, int dtype, int64_t N, int64_t ldi, i
   L.ld_in = ldi;
   L.ld_out = ldo;
   L.stream = stream;
+  L.serial = true;
+  for (int i = 0; i < dm->n; ++i) L.serial = L.serial && dm->pm.parent[i] == i - 1;
   return L;
 }
 int finish(int rc, const char* where) {

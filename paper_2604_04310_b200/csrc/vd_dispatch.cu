@@ -29,6 +29,7 @@ int with_view(const Launch& L, Fn&& fn) {
 }  // namespace
 
 int match_spec(uint64_t fp, int n) { return match_spec_tables(fp, n); }
+int launch_jac_scan(const Launch& L, const void* q, const FrameArg& fr, void* pose, void* J);
 
 int launch_fk(const Launch& L, const void* q, void* out) {
   if (L.N == 0) return 0;
@@ -49,6 +50,9 @@ int launch_jacobian(const Launch& L, const void* q, int frame_joint, const doubl
   fr.joint = frame_joint;
   for (int k = 0; k < 9; ++k) fr.R[k] = frame_R[k];
   for (int k = 0; k < 3; ++k) fr.p[k] = frame_p[k];
+  // serial chains at batches below one wave of thread-per-state CTAs: 8 lanes
+  // per state (config 2, Panda at N = 4096)
+  if (L.serial && L.n <= 32 && L.N <= 32768) return launch_jac_scan(L, q, fr, pose, J);
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::jac(mv, L, q, fr, pose, J); });
 }
 
@@ -181,6 +185,144 @@ __global__ void __launch_bounds__(128) k_fk_scan(const __grid_constant__ DevMode
   }
 }
 }  // namespace
+
+// frame pose + geometric Jacobian (kinematics.hpp:89-136) for serial chains
+// at small batches: the scan above gives lane j its world transform W_j; the
+// frame's lane composes the frame offset and broadcasts the frame point; lane
+// j writes Jacobian column j (zero off the ancestor path).  8 lanes per state
+// instead of one thread: a 4096-state batch fills 256 CTAs instead of 32.
+// model accessors for the scan kernel: the packed model by value (any serial
+// chain) or a robot's compile-time tables (no kernel-parameter payload)
+template <class T>
+struct ScanDev {
+  DevModel<T> m;
+  __device__ __forceinline__ int n() const { return m.n; }
+  __device__ __forceinline__ int kind(int j) const { return m.kind[j]; }
+  __device__ __forceinline__ T axis(int j, int k) const { return m.axis[j][k]; }
+  __device__ __forceinline__ T R(int j, int k) const { return m.R[j][k]; }
+  __device__ __forceinline__ T p(int j, int k) const { return m.p[j][k]; }
+  __device__ __forceinline__ uint64_t anc(int j) const { return m.anc[j]; }
+};
+template <class Robot, class T>
+struct ScanStatic {
+  __device__ __forceinline__ int n() const { return Robot::kN; }
+  __device__ __forceinline__ int kind(int j) const { return Robot::kind()[j]; }
+  __device__ __forceinline__ T axis(int j, int k) const { return T(Robot::axis()[j * 3 + k]); }
+  __device__ __forceinline__ T R(int j, int k) const { return T(Robot::rot()[j * 9 + k]); }
+  __device__ __forceinline__ T p(int j, int k) const { return T(Robot::pos()[j * 3 + k]); }
+  __device__ __forceinline__ uint64_t anc(int j) const { return Robot::anc()[j]; }
+};
+
+template <class T, class M>
+__global__ void __launch_bounds__(128) k_jac_scan(const __grid_constant__ M m, int seg, int64_t N,
+                                                  const T* __restrict__ q, int64_t ldi, int fj,
+                                                  const __grid_constant__ FrameArg fr, T* __restrict__ pose,
+                                                  T* __restrict__ J, int64_t ldo) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % seg;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t i = warp * (32 / seg) + lane / seg;
+  const bool active = i < N && sub < m.n();
+  const int64_t ii = i < N ? i : N - 1;
+  T R[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)}, p[3] = {T(0), T(0), T(0)};
+  if (sub < m.n()) {
+    const T qi = q[(int64_t)sub * ldi + ii];
+    T QJ[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)}, tJ[3] = {T(0), T(0), T(0)};
+    const T a[3] = {m.axis(sub, 0), m.axis(sub, 1), m.axis(sub, 2)};
+    if (m.kind(sub) == 0) {  // Rodrigues, spatial.hpp:302-308
+      T s, c;
+      sincos_t<T>(qi, &s, &c);
+      const T omc = T(1) - c;
+      for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) QJ[r * 3 + k] = a[r] * a[k] * omc + (r == k ? c : T(0));
+      QJ[1] -= a[2] * s;
+      QJ[2] += a[1] * s;
+      QJ[3] += a[2] * s;
+      QJ[5] -= a[0] * s;
+      QJ[6] -= a[1] * s;
+      QJ[7] += a[0] * s;
+    } else {
+      for (int k = 0; k < 3; ++k) tJ[k] = a[k] * qi;
+    }
+    for (int r = 0; r < 3; ++r) {  // X_off ∘ X_J
+      for (int k = 0; k < 3; ++k)
+        R[r * 3 + k] = m.R(sub, r * 3) * QJ[k] + m.R(sub, r * 3 + 1) * QJ[3 + k] + m.R(sub, r * 3 + 2) * QJ[6 + k];
+      p[r] = m.R(sub, r * 3) * tJ[0] + m.R(sub, r * 3 + 1) * tJ[1] + m.R(sub, r * 3 + 2) * tJ[2] + m.p(sub, r);
+    }
+  }
+  for (int d = 1; d < seg; d <<= 1) {
+    T Rn[9], pn[3];
+    for (int k = 0; k < 9; ++k) Rn[k] = __shfl_up_sync(0xffffffffu, R[k], d, seg);
+    for (int k = 0; k < 3; ++k) pn[k] = __shfl_up_sync(0xffffffffu, p[k], d, seg);
+    if (sub >= d) {
+      T R2[9], p2[3];
+      for (int r = 0; r < 3; ++r) {
+        for (int k = 0; k < 3; ++k) R2[r * 3 + k] = Rn[r * 3] * R[k] + Rn[r * 3 + 1] * R[3 + k] + Rn[r * 3 + 2] * R[6 + k];
+        p2[r] = Rn[r * 3] * p[0] + Rn[r * 3 + 1] * p[1] + Rn[r * 3 + 2] * p[2] + pn[r];
+      }
+      for (int k = 0; k < 9; ++k) R[k] = R2[k];
+      for (int k = 0; k < 3; ++k) p[k] = p2[k];
+    }
+  }
+  // frame pose on lane fj (frame_transform, kinematics.hpp:89-96), broadcast the frame point
+  T PR[9], Pp[3];
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c)
+      PR[r * 3 + c] = R[r * 3] * T(fr.R[c]) + R[r * 3 + 1] * T(fr.R[3 + c]) + R[r * 3 + 2] * T(fr.R[6 + c]);
+    Pp[r] = R[r * 3] * T(fr.p[0]) + R[r * 3 + 1] * T(fr.p[1]) + R[r * 3 + 2] * T(fr.p[2]) + p[r];
+  }
+  const int src = fj >= 0 ? fj : 0;
+  T Pf[3];
+  for (int k = 0; k < 3; ++k) Pf[k] = __shfl_sync(0xffffffffu, Pp[k], src, seg);
+  if (!active) return;
+  if (pose && sub == src) {
+    for (int c = 0; c < 3; ++c)
+      for (int r = 0; r < 3; ++r) pose[(int64_t)(c * 3 + r) * ldo + i] = fj >= 0 ? PR[r * 3 + c] : T(r == c);
+    for (int r = 0; r < 3; ++r) pose[(int64_t)(9 + r) * ldo + i] = fj >= 0 ? Pp[r] : T(fr.p[r]);
+  }
+  if (J) {  // geometric_jacobian (kinematics.hpp:108-129)
+    T col[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
+    if (fj >= 0 && ((m.anc(fj) >> sub) & 1ull)) {
+      T ax[3];
+      for (int r = 0; r < 3; ++r) ax[r] = R[r * 3] * m.axis(sub, 0) + R[r * 3 + 1] * m.axis(sub, 1) + R[r * 3 + 2] * m.axis(sub, 2);
+      if (m.kind(sub) == 0) {
+        const T d[3] = {Pf[0] - p[0], Pf[1] - p[1], Pf[2] - p[2]};
+        col[0] = ax[0];
+        col[1] = ax[1];
+        col[2] = ax[2];
+        col[3] = ax[1] * d[2] - ax[2] * d[1];
+        col[4] = ax[2] * d[0] - ax[0] * d[2];
+        col[5] = ax[0] * d[1] - ax[1] * d[0];
+      } else {
+        col[3] = ax[0];
+        col[4] = ax[1];
+        col[5] = ax[2];
+      }
+    }
+    for (int r = 0; r < 6; ++r) J[(int64_t)(sub * 6 + r) * ldo + i] = col[r];
+  }
+}
+
+int launch_jac_scan(const Launch& L, const void* q, const FrameArg& fr, void* pose, void* J) {
+  int seg = 1;
+  while (seg < L.n) seg <<= 1;
+  const int64_t threads = ((L.N + (32 / seg) - 1) / (32 / seg)) * 32;
+  const unsigned grid = (unsigned)((threads + 127) / 128);
+  cudaStream_t s = static_cast<cudaStream_t>(L.stream);
+  auto go = [&](auto m, auto tag) {
+    using T = decltype(tag);
+    k_jac_scan<T><<<grid, 128, 0, s>>>(m, seg, L.N, (const T*)q, L.ld_in, fr.joint, fr, (T*)pose, (T*)J, L.ld_out);
+  };
+  if (L.spec == kChain7) {
+    if (L.dtype == 0) go(ScanStatic<RobotChain7, double>{}, double());
+    else go(ScanStatic<RobotChain7, float>{}, float());
+  } else if (L.dtype == 0) {
+    go(ScanDev<double>{*static_cast<const DevModel<double>*>(L.model)}, double());
+  } else {
+    go(ScanDev<float>{*static_cast<const DevModel<float>*>(L.model)}, float());
+  }
+  return (int)cudaGetLastError();
+}
 
 int launch_fk_scan(const Launch& L, const void* q, void* out) {
   if (L.N == 0) return 0;

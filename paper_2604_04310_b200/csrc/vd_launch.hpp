@@ -17,6 +17,7 @@ struct Launch {
   const void* model;        // host DevModel<T>* (matching dtype), passed by value to the kernels
   int64_t N, ld_in, ld_out;
   void* stream;
+  bool serial = false;      // every joint's parent is its predecessor
 };
 
 struct OscShared;
