@@ -4,6 +4,8 @@
 // dominated by flag/select overhead and the loop kernels by local-memory
 // state.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "vd_gen_kernels.cuh"
@@ -73,6 +75,11 @@ struct Occ {
   int blocks_per_sm = 0, sms = 0;
 };
 
+inline bool debug_launches() {
+  static const bool on = std::getenv("VD_DEBUG_LAUNCH") != nullptr;
+  return on;
+}
+
 // The scratch slabs come from the device's default stream-ordered pool; by
 // default the pool hands memory back to the driver at every synchronisation,
 // which turns each launch's cudaMallocAsync into a real allocation.  Keep it.
@@ -114,6 +121,9 @@ int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, co
   const Occ o = occupancy<Op, T>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
   cudaStream_t s = static_cast<cudaStream_t>(L.stream);
+  if (debug_launches())
+    std::fprintf(stderr, "[vd] k_gen slots %d reg %d smem %d: %d CTAs/SM x %d SMs, grid %lld, smem %zu B\n", Op::kSlots,
+                 C::kReg, C::kSmem, o.blocks_per_sm, o.sms, (long long)blocks, smem);
   // L2-resident scratch for the slots that are neither in registers nor in
   // shared memory: one slab per resident thread, stream-ordered from the
   // device's memory pool (no synchronisation, safe for concurrent streams).
