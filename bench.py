@@ -492,11 +492,27 @@ def run_configs(vd, lib, dev, stream, sptr, args, rank, world):
         sfx = "f64" if code == 0 else "f32"
         rec(f"4_g1_rnea_b262144_{sfx}", N, event_time(f_r, steps, warm, stream), flops_per_eval("tree29", "rnea"))
         rec(f"4_g1_aba_b262144_{sfx}", N, event_time(f_a, steps, warm, stream), flops_per_eval("tree29", "aba"))
+    # config 4': G1 CRBA, batch 262144 fp64: dense M (841 planes, the reference's
+    # output) vs the branch-sparse packed lower triangle (242 planes); both HBM bound
+    N = 262144
+    q, _, _ = states(29, N, torch.float64)
+    nnz = len(tree.crba_pattern()[0])
+    Md = torch.empty((29 * 29, N), dtype=torch.float64, device=dev)
+    Mp = torch.empty((nnz, N), dtype=torch.float64, device=dev)
+    f_d = lambda: lib.vd_crba(dt_.handle, 0, N, q.data_ptr(), N, Md.data_ptr(), N, sptr)  # noqa
+    f_p = lambda: lib.vd_crba_packed(dt_.handle, 0, N, q.data_ptr(), N, Mp.data_ptr(), N, sptr)  # noqa
+    for key, fn, planes in (("4p_g1_crba_dense_b262144_f64", f_d, 29 * 29), ("4p_g1_crba_packed_b262144_f64", f_p, nnz)):
+        ms = event_time(fn, steps, warm, stream)
+        byts = (29 + planes) * 8 * N
+        rec(key, N, ms, flops_per_eval("tree29", "crba"),
+            {"out_planes": planes, "hbm_gbs": round(byts / (ms * 1e-3) / 1e9, 1),
+             "hbm_frac": round(byts / (ms * 1e-3) / 1e9 / measured_peaks().get("hbm_gbs", 6650.0), 4)})
+    del Md, Mp, q
     # config 5: OSC terms, batch 4M (per GPU), Panda and G1
     for robot, dmod, frame in (("chain7", dc, "ee"), ("tree29", dt_, "l_palm")):
         m = chain if robot == "chain7" else tree
         n = m.dof()
-        N = 4194304 if robot == "chain7" else 1048576
+        N = 4194304  # config 5: batch 4M per GPU for both robots
         q, qd, _ = states(n, N, torch.float64)
         P = vd._lib.OscParams()
         P.frame = m.frame_index(frame)

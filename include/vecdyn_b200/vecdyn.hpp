@@ -7,7 +7,7 @@
 //   vecdyn::urdf::load_model(path) urdf.hpp:70         vecdyn::urdf::load_model(path)
 //   vecdyn::floating_base(model)   model.hpp:163       vecdyn::floating_base(model)
 //   vecdyn::RobotModel             model.hpp:90-149    vecdyn::RobotModel (dof, joint_names, frame, ...)
-//   vecdyn::GravitySpec            dynamics.hpp:194    vecdyn::GravitySpec
+//   vecdyn::GravitySpec            dynamics.hpp:39     vecdyn::GravitySpec
 //   vecdyn::StateBatch / random_states   batch.hpp:15-75   same (column-major N x n, std::vector)
 //   vecdyn::batch_rnea / batch_crba / batch_forward_dynamics  batch.hpp:128-165
 //                                                   same, `workers` replaced by a device list
@@ -24,6 +24,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <utility>
 #include <vector>
 
 #include "../vecdyn_cuda.h"
@@ -107,13 +108,21 @@ class RobotModel {
     if (!p.empty()) detail::check(vd_model_parents(handle(), p.data()));
     return p;
   }
+  // (rows, cols) of crba_packed's planes (vd_model_crba_pattern)
+  std::pair<std::vector<int32_t>, std::vector<int32_t>> crba_pattern() const {
+    int nnz = 0;
+    detail::check(vd_model_crba_pattern(handle(), nullptr, nullptr, &nnz));
+    std::vector<int32_t> r((size_t)nnz), c((size_t)nnz);
+    if (nnz) detail::check(vd_model_crba_pattern(handle(), r.data(), c.data(), &nnz));
+    return {r, c};
+  }
   std::string joint_name(int i) const {
     char b[256];
     detail::check(vd_model_joint_name(handle(), i, b, sizeof b));
     return b;
   }
   int joint_index(std::string_view name) const { return vd_model_joint_index(handle(), std::string(name).c_str()); }
-  int frame_index(std::string_view name) const {  // RobotModel::frame, model.cpp:512-518
+  int frame_index(std::string_view name) const {  // RobotModel::frame, model.cpp:337-343
     int k = -1;
     detail::check(vd_model_frame_index(handle(), std::string(name).c_str(), &k));
     return k;
@@ -166,7 +175,7 @@ inline RobotModel floating_base(const RobotModel& m) {
   return RobotModel(h);
 }
 
-struct GravitySpec {  // dynamics.hpp:194-205
+struct GravitySpec {  // dynamics.hpp:35-50
   double accel[3] = {0.0, 0.0, 9.81};
   static GravitySpec standard() { return GravitySpec(); }
   static GravitySpec zero() { return GravitySpec{{0.0, 0.0, 0.0}}; }
@@ -262,6 +271,11 @@ inline void rnea(const DeviceModel& dm, DType t, int64_t N, const void* q, const
 }
 inline void crba(const DeviceModel& dm, DType t, int64_t N, const void* q, void* M, void* stream = nullptr) {
   detail::check(vd_crba(dm.handle(), (int)t, N, q, N, M, N, stream));
+}
+// M's branch-sparse lower triangle; plane k = M(rows[k], cols[k]) of crba_pattern
+inline void crba_packed(const DeviceModel& dm, DType t, int64_t N, const void* q, void* M_packed,
+                        void* stream = nullptr) {
+  detail::check(vd_crba_packed(dm.handle(), (int)t, N, q, N, M_packed, N, stream));
 }
 inline void forward_dynamics(const DeviceModel& dm, DType t, int64_t N, const void* q, const void* qd,
                              const void* tau, void* qdd, int32_t* status = nullptr,

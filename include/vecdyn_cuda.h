@@ -36,13 +36,13 @@ extern "C" {
 #endif
 
 #define VD_OK 0
-#define VD_ERR_DIMENSION 1              /* DimensionError            errors.hpp:25-28 */
-#define VD_ERR_PARSE 2                  /* ParseError(line, column)  errors.hpp:43-53 */
-#define VD_ERR_MODEL 3                  /* ModelError                errors.hpp:31-34 */
-#define VD_ERR_UNKNOWN_FRAME 4          /* UnknownFrameError         errors.hpp:37-40 */
-#define VD_ERR_UNSUPPORTED_FEATURE 5    /* UnsupportedFeatureError   errors.hpp:56-59 */
-#define VD_ERR_UNSUPPORTED_STRUCTURE 6  /* UnsupportedStructureError errors.hpp:62-65 */
-#define VD_ERR_SINGULAR_INERTIA 7       /* SingularInertiaError      errors.hpp:68-71 */
+#define VD_ERR_DIMENSION 1              /* DimensionError            errors.hpp:14-18 */
+#define VD_ERR_PARSE 2                  /* ParseError(line, column)  errors.hpp:32-43 */
+#define VD_ERR_MODEL 3                  /* ModelError                errors.hpp:20-24 */
+#define VD_ERR_UNKNOWN_FRAME 4          /* UnknownFrameError         errors.hpp:26-30 */
+#define VD_ERR_UNSUPPORTED_FEATURE 5    /* UnsupportedFeatureError   errors.hpp:45-49 */
+#define VD_ERR_UNSUPPORTED_STRUCTURE 6  /* UnsupportedStructureError errors.hpp:51-55 */
+#define VD_ERR_SINGULAR_INERTIA 7       /* SingularInertiaError      errors.hpp:57-61 */
 #define VD_ERR_CUDA 8                   /* CUDA runtime failure (no reference analogue) */
 #define VD_ERR_INVALID_ARGUMENT 9       /* null pointer, ld < N, bad dtype, ... */
 #define VD_ERR_IO 10                    /* Error("cannot open URDF file ...") urdf.cpp:277-281 */
@@ -90,9 +90,15 @@ int vd_model_joint_index(vd_model m, const char* name); /* -1 if absent (model.c
  * inertia: 6x6 row-major about the joint frame origin, angular first. */
 int vd_model_joint(vd_model m, int i, int* type, double axis[3], double offset[12], double inertia[36]);
 int vd_model_ancestor_mask(vd_model m, double* mask_out); /* n*n, column-major (Eigen MatrixXd) */
+/* Branch-sparse lower triangle of M (the reference's M_lower = U ⊙ (SᵀCS),
+ * dynamics.hpp:337-350; every other entry is an exact zero,
+ * test_dynamics.cpp:200-216): the pairs (r, c), r >= c, c an ancestor of r or
+ * r itself, in compressed-column order (c ascending, then r).  *nnz_out
+ * receives the count (chain7 28, tree29 242); rows / cols may be NULL. */
+int vd_model_crba_pattern(vd_model m, int32_t* rows_out, int32_t* cols_out, int* nnz_out);
 int vd_model_frame_count(vd_model m);
 int vd_model_frame(vd_model m, int k, char* name, size_t len, int* joint, double offset[12]);
-/* RobotModel::frame(name) index; VD_ERR_UNKNOWN_FRAME when absent (model.cpp:512-518) */
+/* RobotModel::frame(name) index; VD_ERR_UNKNOWN_FRAME when absent (model.cpp:337-343) */
 int vd_model_frame_index(vd_model m, const char* name, int* out);
 
 /* StateBatch random_states(model, count, seed, with_qdd, with_tau), batch.hpp:48-75:
@@ -116,9 +122,9 @@ int vd_device_model_set_generic(vd_device_model dm, int generic);
 
 /* ------------------------------------------------------------------ batched kernels
  * gravity3: the base acceleration a_g = −field (GravitySpec::accel.linear,
- * dynamics.hpp:194-205); NULL means GravitySpec::standard() = (0, 0, +9.81).
+ * dynamics.hpp:35-50); NULL means GravitySpec::standard() = (0, 0, +9.81).
  * fext: NULL or 6n planes, plane j*6 + k = component k (angular first) of
- * the world-frame Plücker wrench on joint j (ExternalForcesT, dynamics.hpp:210-236). */
+ * the world-frame Plücker wrench on joint j (ExternalForcesT, dynamics.hpp:52-81). */
 
 /* forward_kinematics, kinematics.hpp:43-56: plane j*12 + k (k < 9: R column-major, 9..11: p) */
 int vd_fk(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* frames_out,
@@ -132,22 +138,27 @@ int vd_fk_scan(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t 
  * J 6 x n column-major (plane c*6 + r).  Either output may be NULL. */
 int vd_jacobian(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, int frame, void* pose_out,
                 void* J_out, int64_t ld_out, void* stream);
-/* rnea(model, q, qd, qdd, gravity, fext), dynamics.hpp:405-422 */
+/* rnea(model, q, qd, qdd, gravity, fext), dynamics.hpp:250-267 */
 int vd_rnea(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* qdd, int64_t ld_in,
             const double* gravity3, const void* fext, void* tau_out, int64_t ld_out, void* stream);
 /* c + g (− Σ Jᵀ f_ext): rnea(q, qd, 0, gravity, fext), dynamics.hpp:434-435 */
 int vd_bias(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in,
             const double* gravity3, const void* fext, void* out, int64_t ld_out, void* stream);
-/* gravity_vector, dynamics.hpp:557-563 */
+/* gravity_vector, dynamics.hpp:402-408 */
 int vd_gravity(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, const double* gravity3,
                void* out, int64_t ld_out, void* stream);
-/* coriolis_vector, dynamics.hpp:565-571 */
+/* coriolis_vector, dynamics.hpp:410-416 */
 int vd_coriolis(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in, void* out,
                 int64_t ld_out, void* stream);
-/* crba, dynamics.hpp:507-520: M n x n column-major, plane c*n + r */
+/* crba, dynamics.hpp:352-365: M n x n column-major, plane c*n + r */
 int vd_crba(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* M_out, int64_t ld_out,
             void* stream);
-/* forward_dynamics, dynamics.hpp:576-599, computed by the articulated-body
+/* crba in packed form (no reference analogue; the reference returns dense M,
+ * dynamics.hpp:352-365): plane k = M(rows[k], cols[k]) of vd_model_crba_pattern.
+ * Output planes 242 instead of 841 for tree29 (the dense output is HBM-bound). */
+int vd_crba_packed(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* M_packed_out,
+                   int64_t ld_out, void* stream);
+/* forward_dynamics, dynamics.hpp:418-444, computed by the articulated-body
  * algorithm (absent from the reference).  status_out (int32 x N)
  * may be NULL. */
 int vd_aba(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau, int64_t ld_in,

@@ -73,7 +73,7 @@ void llt_solve(const Dense<T>& L, Dense<T>& B) {
 }
 
 // ---------------------------------------------------------------- gravity / fext
-// GravitySpec, dynamics.hpp:194-205: a_g = -field, default (0,0,0, 0,0,+9.81).
+// GravitySpec, dynamics.hpp:35-50: a_g = -field, default (0,0,0, 0,0,+9.81).
 struct Gravity {
   V3<double> lin{0, 0, 9.81};
   static Gravity standard() { return Gravity(); }
@@ -81,7 +81,7 @@ struct Gravity {
   static Gravity from_field(const V3<double>& f) { return Gravity{-f}; }
 };
 
-// ExternalForcesT, dynamics.hpp:210-236: per-joint world Plücker wrenches.
+// ExternalForcesT, dynamics.hpp:52-81: per-joint world Plücker wrenches.
 template <class T>
 struct ExtForces {
   std::vector<Force<T>> w;  // empty = none
@@ -118,7 +118,7 @@ Xform<T> local_transform(const Joint& j, const T& q) {
   }
   return j.offset.as<T>() * motion;
 }
-// dynamics.hpp:324-330
+// dynamics.hpp:169-175
 template <class T>
 Motion<T> local_axis(const Joint& j) {
   Motion<T> s;
@@ -216,7 +216,7 @@ struct Workspace {
   std::vector<Mat6<T>> I, C;
 };
 
-// dynamics.hpp:337-359
+// dynamics.hpp:182-213
 template <class T>
 void prepare_world_arrays(const Model& m, const Frames<T>& w, Workspace<T>& ws) {
   const int n = m.dof();
@@ -236,7 +236,7 @@ void prepare_world_arrays(const Model& m, const Frames<T>& w, Workspace<T>& ws) 
   }
 }
 
-// dynamics.hpp:377-403: mask-product form
+// dynamics.hpp:222-248: mask-product form
 //   V = U (S∘q̇) ; A = a_g + U (S∘q̈ + V × S∘q̇) ; F = Uᵀ (I A + V ×* I V − F_ext) ; τ = S·F
 template <class T>
 std::vector<T> rnea_from_workspace(const Model& m, Workspace<T>& ws, const std::vector<T>& qd,
@@ -287,7 +287,7 @@ std::vector<T> rnea(const Model& m, const std::vector<T>& q, const std::vector<T
   return rnea_from_workspace(m, ws, qd, qdd, g, fext);
 }
 
-// dynamics.hpp:427-482: local-frame two-pass recursion.
+// dynamics.hpp:272-327: local-frame two-pass recursion.
 template <class T>
 std::vector<T> rnea_loop(const Model& m, const std::vector<T>& q, const std::vector<T>& qd,
                          const std::vector<T>& qdd, const Gravity& g = Gravity::standard(),
@@ -327,7 +327,7 @@ std::vector<T> rnea_loop(const Model& m, const std::vector<T>& q, const std::vec
   return tau;
 }
 
-// dynamics.hpp:485-505: C = Uᵀ I ; lower = U ⊙ (C S)·Sᵀ ; M = L + Lᵀ − diag L.
+// dynamics.hpp:337-350: C = Uᵀ I ; lower = U ⊙ (C S)·Sᵀ ; M = L + Lᵀ − diag L.
 template <class T>
 Dense<T> crba_from_workspace(const Model& m, Workspace<T>& ws) {
   const int n = m.dof();
@@ -356,7 +356,7 @@ Dense<T> crba(const Model& m, const std::vector<T>& q, Workspace<T>* wsp = nullp
   return crba_from_workspace(m, ws);
 }
 
-// dynamics.hpp:524-555
+// dynamics.hpp:369-400
 template <class T>
 Dense<T> crba_loop(const Model& m, const std::vector<T>& q) {
   detail::check_size(m, q.size(), "configuration vector");
@@ -388,7 +388,7 @@ Dense<T> crba_loop(const Model& m, const std::vector<T>& q) {
   return M;
 }
 
-// dynamics.hpp:557-571
+// dynamics.hpp:402-416
 template <class T>
 std::vector<T> gravity_vector(const Model& m, const std::vector<T>& q, const Gravity& g = Gravity::standard()) {
   const std::vector<T> z((size_t)m.dof(), T(0));
@@ -400,7 +400,7 @@ std::vector<T> coriolis_vector(const Model& m, const std::vector<T>& q, const st
   return rnea<T>(m, q, qd, z, Gravity::zero());
 }
 
-// dynamics.hpp:576-599: q̈ = M⁻¹(τ − bias) via LLT; SingularInertiaError if not PD.
+// dynamics.hpp:418-444: q̈ = M⁻¹(τ − bias) via LLT; SingularInertiaError if not PD.
 template <class T>
 std::vector<T> forward_dynamics(const Model& m, const std::vector<T>& q, const std::vector<T>& qd,
                                 const std::vector<T>& tau, const Gravity& g = Gravity::standard(),

@@ -171,7 +171,7 @@ void orc_random_states(void* h, int64_t N, uint64_t seed, double* q, double* qd,
   if (tau) std::memcpy(tau, b.tau.data(), b.tau.size() * sizeof(double));
 }
 
-// variant 0: vectorized mask form (dynamics.hpp:405-414); 1: rnea_loop.
+// variant 0: vectorized mask form (dynamics.hpp:222-248); 1: rnea_loop.
 // f32 != 0 evaluates in single precision (inputs rounded to float).
 int orc_batch_rnea(void* h, int64_t N, const double* q, const double* qd, const double* qdd, const double* g3,
                    const double* fext, double* tau, int threads, int variant, int f32) {

@@ -8,7 +8,7 @@ follow the reference:
   urdf.load_model(path) / load_model_from_string(text)       urdf.cpp:384-390
   RobotModel (dof, joints, frames, ancestor_mask, ...)        model.hpp:90-149
   floating_base(model)                                       model.cpp:289-331
-  GravitySpec.standard() / zero() / from_field()              dynamics.hpp:194-205
+  GravitySpec.standard() / zero() / from_field()              dynamics.hpp:35-50
   rnea, crba, gravity_vector, coriolis_vector,
   forward_dynamics (ABA), forward_kinematics,
   frame_transform, geometric_jacobian, osc_step               kinematics/dynamics/control.hpp
@@ -33,7 +33,7 @@ __all__ = [
     "Error", "DimensionError", "ModelError", "UnknownFrameError", "ParseError", "UnsupportedFeatureError",
     "UnsupportedStructureError", "SingularInertiaError", "CudaError", "RobotModel", "DeviceModel", "GravitySpec",
     "TaskGains", "TaskTarget", "PostureGains", "StateBatch", "robots", "urdf", "floating_base", "random_states",
-    "rnea", "bias_forces", "gravity_vector", "coriolis_vector", "crba", "forward_dynamics", "dynamics",
+    "rnea", "bias_forces", "gravity_vector", "coriolis_vector", "crba", "crba_packed", "unpack_crba", "forward_dynamics", "dynamics",
     "forward_kinematics", "forward_kinematics_scan", "frame_transform", "geometric_jacobian", "manipulability", "diff_ik_step", "osc_step", "batch_rnea", "batch_crba",
     "forward_kinematics_jvp", "rnea_jvp", "crba_jvp", "forward_dynamics_jvp",
     "batch_forward_dynamics", "shard_range",
@@ -174,6 +174,17 @@ class RobotModel:
         _check(self._lib.vd_model_ancestor_mask(self._h, m))
         return np.array(m[: n * n]).reshape(n, n, order="F")
 
+    def crba_pattern(self):
+        """(rows, cols) of the branch-sparse lower triangle of M in
+        compressed-column order (vd_model_crba_pattern); the layout of
+        crba_packed's planes."""
+        nnz = ctypes.c_int(0)
+        _check(self._lib.vd_model_crba_pattern(self._h, None, None, ctypes.byref(nnz)))
+        r = (ctypes.c_int32 * max(nnz.value, 1))()
+        c = (ctypes.c_int32 * max(nnz.value, 1))()
+        _check(self._lib.vd_model_crba_pattern(self._h, r, c, ctypes.byref(nnz)))
+        return np.array(r[: nnz.value], dtype=np.int64), np.array(c[: nnz.value], dtype=np.int64)
+
     def frames(self):
         out = []
         for k in range(self._lib.vd_model_frame_count(self._h)):
@@ -242,7 +253,7 @@ def floating_base(model):
 
 # ------------------------------------------------------------------ gravity / control structs
 class GravitySpec:
-    """a_g = −field; default (0, 0, +9.81) (dynamics.hpp:194-205)."""
+    """a_g = −field; default (0, 0, +9.81) (dynamics.hpp:35-50)."""
 
     def __init__(self, linear_accel=(0.0, 0.0, 9.81)):
         self.accel = tuple(float(x) for x in linear_accel)
@@ -395,7 +406,7 @@ def _p(t):
 
 
 def rnea(dm, q, qd, qdd, gravity=None, fext=None):
-    """rnea(model, q, qd, qdd, gravity, fext) — dynamics.hpp:405-422; (N, n) torques."""
+    """rnea(model, q, qd, qdd, gravity, fext) — dynamics.hpp:250-267; (N, n) torques."""
     qs, (qds, qdds), N, dev = _prep(dm, q, (qd, "qd"), (qdd, "qdd"))
     n = dm.dof()
     out = _out(dev, qs.dtype, n, N)
@@ -418,7 +429,7 @@ def bias_forces(dm, q, qd, gravity=None, fext=None):
 
 
 def gravity_vector(dm, q, gravity=None):
-    """dynamics.hpp:557-563."""
+    """dynamics.hpp:402-408."""
     qs, _, N, dev = _prep(dm, q)
     out = _out(dev, qs.dtype, dm.dof(), N)
     g = (gravity or GravitySpec.standard()).c()
@@ -427,7 +438,7 @@ def gravity_vector(dm, q, gravity=None):
 
 
 def coriolis_vector(dm, q, qd):
-    """dynamics.hpp:565-571."""
+    """dynamics.hpp:410-416."""
     qs, (qds,), N, dev = _prep(dm, q, (qd, "qd"))
     out = _out(dev, qs.dtype, dm.dof(), N)
     _check(_lib.load().vd_coriolis(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), N, _p(out), N, _stream(dev)))
@@ -435,12 +446,38 @@ def coriolis_vector(dm, q, qd):
 
 
 def crba(dm, q):
-    """crba(model, q) — dynamics.hpp:507-520; returns (N, n, n)."""
+    """crba(model, q) — dynamics.hpp:352-365; returns (N, n, n)."""
     qs, _, N, dev = _prep(dm, q)
     n = dm.dof()
     out = _out(dev, qs.dtype, n * n, N)
     _check(_lib.load().vd_crba(dm.handle, _dtype_code(qs), N, _p(qs), N, _p(out), N, _stream(dev)))
     return out.t().reshape(N, n, n).transpose(1, 2)
+
+
+def crba_packed(dm, q):
+    """M(q) as its branch-sparse lower triangle: (N, nnz), column k =
+    M[rows[k], cols[k]] for (rows, cols) = dm.model.crba_pattern().  Every
+    other entry of the reference's dense M is an exact zero or the mirror of a
+    packed one (dynamics.hpp:331-350); see unpack_crba."""
+    qs, _, N, dev = _prep(dm, q)
+    nnz = len(dm.model.crba_pattern()[0])
+    out = _out(dev, qs.dtype, nnz, N)
+    _check(_lib.load().vd_crba_packed(dm.handle, _dtype_code(qs), N, _p(qs), N, _p(out), N, _stream(dev)))
+    return out.t()
+
+
+def unpack_crba(model, Mp):
+    """Dense symmetric (N, n, n) M from crba_packed's (N, nnz) output
+    (symmetrize_lower, dynamics.hpp:331-335)."""
+    torch = _torch()
+    rows, cols = model.crba_pattern()
+    n = model.dof()
+    M = torch.zeros(Mp.shape[0], n, n, dtype=Mp.dtype, device=Mp.device)
+    r = torch.as_tensor(rows, device=Mp.device)
+    c = torch.as_tensor(cols, device=Mp.device)
+    M[:, r, c] = Mp
+    M[:, c, r] = Mp
+    return M
 
 
 def forward_dynamics(dm, q, qd, tau, gravity=None, fext=None, return_status=False):

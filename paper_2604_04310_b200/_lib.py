@@ -66,6 +66,7 @@ SIGNATURES = {
     "vd_model_joint_index": (c_int, [P, c_char_p]),
     "vd_model_joint": (c_int, [P, c_int, Pi, Pd, Pd, Pd]),
     "vd_model_ancestor_mask": (c_int, [P, Pd]),
+    "vd_model_crba_pattern": (c_int, [P, P, P, P]),
     "vd_model_frame_count": (c_int, [P]),
     "vd_model_frame": (c_int, [P, c_int, ctypes.c_char_p, c_size_t, Pi, Pd]),
     "vd_model_frame_index": (c_int, [P, c_char_p, Pi]),
@@ -83,6 +84,7 @@ SIGNATURES = {
     "vd_gravity": (c_int, [P, c_int, c_int64, P, c_int64, Pd, P, c_int64, P]),
     "vd_coriolis": (c_int, [P, c_int, c_int64, P, P, c_int64, P, c_int64, P]),
     "vd_crba": (c_int, [P, c_int, c_int64, P, c_int64, P, c_int64, P]),
+    "vd_crba_packed": (c_int, [P, c_int, c_int64, P, c_int64, P, c_int64, P]),
     "vd_aba": (c_int, [P, c_int, c_int64, P, P, P, c_int64, Pd, P, P, c_int64, P, P]),
     "vd_dynamics": (c_int, [P, c_int, c_int64, P, P, P, c_int64, Pd, P, P, P, c_int64, P, P]),
     "vd_osc": (c_int, [P, c_int, c_int64, P, P, c_int64, ctypes.POINTER(OscParams), P, P, c_int64, P, P]),

@@ -245,6 +245,22 @@ int vd_model_ancestor_mask(vd_model m, double* mask) {
     }
   return VD_OK;
 }
+int vd_model_crba_pattern(vd_model m, int32_t* rows, int32_t* cols, int* nnz) {
+  if (!m || !nnz) return set_error(VD_ERR_INVALID_ARGUMENT, "null argument");
+  const int n = m->m.dof();
+  int k = 0;
+  for (int c = 0; c < n; ++c)
+    for (int r = c; r < n; ++r) {
+      int j = r;
+      while (j >= 0 && j != c) j = m->m.bodies[(size_t)j].parent;
+      if (j != c) continue;
+      if (rows) rows[k] = r;
+      if (cols) cols[k] = c;
+      ++k;
+    }
+  *nnz = k;
+  return VD_OK;
+}
 int vd_model_frame_count(vd_model m) { return m ? (int)m->m.frames.size() : -1; }
 int vd_model_frame(vd_model m, int k, char* name, size_t len, int* joint, double offset[12]) {
   if (!m || k < 0 || k >= (int)m->m.frames.size()) return set_error(VD_ERR_INVALID_ARGUMENT, "bad frame index");
@@ -395,6 +411,26 @@ int vd_crba(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_
   if (dm->n == 0) return VD_OK;
   DeviceGuard g(dm->device);
   return finish(vdk::launch_crba(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, M), "vd_crba");
+}
+
+int vd_crba_packed(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, void* Mp, int64_t ld_out,
+                   void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  VD_NEED(q, "q");
+  VD_NEED(Mp, "M_packed");
+  if (dm->n == 0) return VD_OK;
+  // vd_model_crba_pattern's order, from the packed parents (same topology)
+  vdk::PackTable tab{};
+  const int n = dm->n;
+  for (int c = 0; c < n; ++c)
+    for (int r = c; r < n; ++r) {
+      int j = r;
+      while (j >= 0 && j != c) j = dm->pm.parent[j];
+      if (j == c) tab.src[tab.nnz++] = (uint16_t)(c * n + r);
+    }
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_crba_packed(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, Mp, tab),
+                "vd_crba_packed");
 }
 
 int vd_aba(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau, int64_t ld_in,

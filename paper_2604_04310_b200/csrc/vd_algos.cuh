@@ -54,7 +54,7 @@ __device__ __forceinline__ void fk_world(const V& mv, const JM<typename V::S>* j
 }
 
 // ------------------------------------------------------------------ RNEA
-// rnea_loop (dynamics.hpp:427-482): two-pass recursion in local coordinates.
+// rnea_loop (dynamics.hpp:272-327): two-pass recursion in local coordinates.
 // qdd == nullptr means q̈ = 0 (bias forces, dynamics.hpp:434-435).
 template <class V, bool kFext, class QdA, class QddA>
 __device__ __forceinline__ void rnea_one(const V& mv, const JM<typename V::S>* jm, const QdA& qd, const QddA* qdd,
@@ -111,7 +111,7 @@ __device__ __forceinline__ void rnea_one(const V& mv, const JM<typename V::S>* j
 }
 
 // ------------------------------------------------------------------ CRBA
-// crba_loop (dynamics.hpp:524-555): composite inertias leaf -> root, then
+// crba_loop (dynamics.hpp:369-400): composite inertias leaf -> root, then
 // one force propagation up the ancestor chain per column.  emit(i, j, value)
 // receives M(i, j) for j = i and every ancestor j of i.
 template <class V, class Emit>

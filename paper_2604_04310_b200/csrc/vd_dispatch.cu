@@ -75,6 +75,44 @@ int launch_crba(const Launch& L, const void* q, void* M) {
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::crba(mv, L, q, M); });
 }
 
+namespace {
+// Gather of the packed planes from a dense M (models without a generated
+// kernel): blockIdx.y = packed plane, x strides over the batch (coalesced).
+template <class T>
+__global__ void k_pack_lower(int64_t N, const T* __restrict__ M, int64_t ld_m, const __grid_constant__ PackTable tab,
+                             T* __restrict__ out, int64_t ld_out) {
+  const int k = blockIdx.y;
+  const T* src = M + (int64_t)tab.src[k] * ld_m;
+  T* dst = out + (int64_t)k * ld_out;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+}  // namespace
+
+int launch_crba_packed(const Launch& L, const void* q, void* Mp, const PackTable& tab) {
+  if (L.N == 0 || tab.nnz == 0) return 0;
+  if (const int rc = launch_gen_crba_packed(L, q, Mp); rc >= 0) return rc;
+  // dense M into stream-ordered scratch, then gather
+  cudaStream_t s = static_cast<cudaStream_t>(L.stream);
+  const size_t es = L.dtype == 0 ? sizeof(double) : sizeof(float);
+  void* dense = nullptr;
+  cudaError_t e = cudaMallocAsync(&dense, (size_t)L.N * L.n * L.n * es, s);
+  if (e != cudaSuccess) return (int)e;
+  Launch Ld = L;
+  Ld.ld_out = L.N;
+  int rc = launch_crba(Ld, q, dense);
+  if (rc == 0) {
+    const dim3 grid((unsigned)std::min<int64_t>((L.N + 255) / 256, 1184), (unsigned)tab.nnz);
+    if (L.dtype == 0)
+      k_pack_lower<double><<<grid, 256, 0, s>>>(L.N, (const double*)dense, L.N, tab, (double*)Mp, L.ld_out);
+    else
+      k_pack_lower<float><<<grid, 256, 0, s>>>(L.N, (const float*)dense, L.N, tab, (float*)Mp, L.ld_out);
+    rc = (int)cudaGetLastError();
+  }
+  cudaFreeAsync(dense, s);
+  return rc;
+}
+
 int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, const void* fext,
                void* qdd, int32_t* status) {
   if (L.N == 0) return 0;

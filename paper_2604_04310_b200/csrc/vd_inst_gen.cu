@@ -55,6 +55,25 @@ struct Cfg<GenTree29::Crba, double> {
   static constexpr int kReg = 0, kSmem = 40, kMinB = 4;
   static constexpr bool kFast = false;
 };
+// packed CRBA (gen_sweep, N = 262144 / 4M): tree29 fp64 all 55 slots in
+// registers at 3 CTAs/SM 0.112 ms (vs 0.133 with the dense routine's
+// placement); fp32 in shared memory at 6 CTAs/SM 0.061 ms; chain7 fp64 all in
+// registers 0.21 ms at 4M states (85 % of HBM)
+template <>
+struct Cfg<GenTree29::CrbaPacked, double> {
+  static constexpr int kReg = GenTree29::CrbaPacked::kSlots, kSmem = 0, kMinB = 3;
+  static constexpr bool kFast = false;
+};
+template <>
+struct Cfg<GenTree29::CrbaPacked, float> {
+  static constexpr int kReg = 0, kSmem = GenTree29::CrbaPacked::kSlots, kMinB = 6;
+  static constexpr bool kFast = false;
+};
+template <class T>
+struct Cfg<GenChain7::CrbaPacked, T> {
+  static constexpr int kReg = GenChain7::CrbaPacked::kSlots, kSmem = 0, kMinB = 4;
+  static constexpr bool kFast = false;
+};
 template <>
 struct Cfg<GenTree29::Rnea, double> {  // prologue: cos/sin, q̇, q̈ of every joint
   static constexpr int kReg = 58, kSmem = 55, kMinB = 2;
@@ -294,6 +313,12 @@ int launch_gen_task(const Launch& L, int which, int frame_joint, const TaskShare
 int launch_gen_crba(const Launch& L, const void* q, void* M) {
   if (L.spec != kTree29) return -1;
   return launch_op<GenTree29::Crba>(L, q, nullptr, nullptr, nullptr, M, nullptr);
+}
+
+int launch_gen_crba_packed(const Launch& L, const void* q, void* Mp) {
+  if (L.spec == kTree29) return launch_op<GenTree29::CrbaPacked>(L, q, nullptr, nullptr, nullptr, Mp, nullptr);
+  if (L.spec == kChain7) return launch_op<GenChain7::CrbaPacked>(L, q, nullptr, nullptr, nullptr, Mp, nullptr);
+  return -1;
 }
 
 int launch_gen_fk(const Launch& L, const void* q, void* frames) {

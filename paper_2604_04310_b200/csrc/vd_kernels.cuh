@@ -178,7 +178,7 @@ __device__ __forceinline__ void store_mass(const V& mv, const JM<typename V::S>*
     o.put(c * n + r, val.v);
     if (r != c) o.put(r * n + c, val.v);
   });
-  // exact zeros between branches (dynamics.hpp:503, test_dynamics.cpp:352-368)
+  // exact zeros between branches (dynamics.hpp:331-335, test_dynamics.cpp:200-216)
 #pragma unroll
   for (int r = 0; r < mv.n(); ++r)
 #pragma unroll

@@ -36,6 +36,13 @@ int launch_jacobian(const Launch& L, const void* q, int frame_joint, const doubl
 int launch_rnea(const Launch& L, int mode, const void* q, const void* qd, const void* qdd, const double* g3,
                 const void* fext, void* tau);
 int launch_crba(const Launch& L, const void* q, void* M);
+// Branch-sparse lower triangle of M (vd_model_crba_pattern order): plane k of
+// the output is dense plane src[k] (= c·n + r) of M.  At most 64·65/2 pairs.
+struct PackTable {
+  int nnz;
+  uint16_t src[2080];
+};
+int launch_crba_packed(const Launch& L, const void* q, void* Mp, const PackTable& tab);
 int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, const void* fext,
                void* qdd, int32_t* status);
 // Generated straight-line kernel (vd_inst_gen.cu) when one exists for L.spec;
@@ -45,6 +52,7 @@ int launch_gen_aba(const Launch& L, const void* q, const void* qd, const void* t
 int launch_gen_rnea(const Launch& L, int mode, const void* q, const void* qd, const void* qdd, const double* g3,
                     void* tau);
 int launch_gen_crba(const Launch& L, const void* q, void* M);
+int launch_gen_crba_packed(const Launch& L, const void* q, void* Mp);
 int launch_gen_fk(const Launch& L, const void* q, void* frames);
 int launch_gen_task(const Launch& L, int which, int frame_joint, const TaskShared& P, const void* q, void* y0,
                     void* y1, int32_t* status);

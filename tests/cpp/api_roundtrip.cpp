@@ -35,6 +35,14 @@ int main() {
     for (int64_t i = 0; i < b.N; i += 97)
       for (int r = 0; r < n; ++r)
         for (int c = 0; c < n; ++c) asym = std::max(asym, std::abs(M[(c * n + r) * b.N + i] - M[(r * n + c) * b.N + i]));
+    // crba_pattern: every entry outside it (and its mirror) is an exact zero of M
+    const auto [rows, cols] = model.crba_pattern();
+    std::vector<char> keep((size_t)n * n, 0);
+    for (size_t k = 0; k < rows.size(); ++k) keep[(size_t)cols[k] * n + rows[k]] = keep[(size_t)rows[k] * n + cols[k]] = 1;
+    for (int64_t i = 0; i < b.N; i += 97)
+      for (int e = 0; e < n * n; ++e)
+        if (!keep[(size_t)e] && M[(size_t)e * b.N + i] != 0.0) ++bad;
+    if (rows.size() != (n == 7 ? 28u : 242u)) ++bad;
     std::printf("%s: FD(ID) roundtrip max rel err %.3e over %d states, CRBA asymmetry %.1e\n", name, worst, counted, asym);
     if (!(worst <= 1e-8) || asym != 0.0) ++bad;
   }

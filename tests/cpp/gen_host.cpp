@@ -71,6 +71,7 @@ int run_op(int op, long N, const void* const* x, const double* g, void* y, int* 
     case 2: return run<typename R::RneaBias, T>(N, x, g, y, status);
     case 3: return run<typename R::RneaGrav, T>(N, x, g, y, status);
     case 4: return run<typename R::Crba, T>(N, x, g, y, status);
+    case 7: return run<typename R::CrbaPacked, T>(N, x, g, y, status);
     default: return run<typename R::Fk, T>(N, x, g, y, status);
   }
 }

@@ -109,7 +109,7 @@ def test_generated_rnea_family(genlib, name, code, f32):
 
 @pytest.mark.parametrize("name,code", [("chain7", 1), ("tree29", 2)])
 def test_generated_crba_and_fk(genlib, name, code):
-    """crba (dynamics.hpp:341-365; exact zeros between branches) and
+    """crba (dynamics.hpp:337-365; exact zeros between branches) and
     forward_kinematics (kinematics.hpp:43-56)."""
     om = Model.builtin(name)
     n = om.n
@@ -121,6 +121,35 @@ def test_generated_crba_and_fk(genlib, name, code):
     assert np.all(M[:, structural] == 0)  # exact zeros between branches, as in the reference
     F, _, _ = _run(genlib, code, 5, (q,), 12 * n)
     assert rel_err(F, om.fk(q).reshape(len(q), -1), axis=1).max() <= 1e-10
+
+
+def _lower_pattern(om):
+    """Branch-sparse lower triangle in compressed-column order, from the
+    oracle's ancestor mask U (U[r, c] = 1 iff c is r or an ancestor of r)."""
+    U = om.arrays()["mask"]
+    return [(r, c) for c in range(om.n) for r in range(c, om.n) if U[r, c] != 0]
+
+
+@pytest.mark.parametrize("name,code,nnz", [("chain7", 1, 28), ("tree29", 2, 242)])
+@pytest.mark.parametrize("f32", [False, True])
+def test_generated_packed_crba(genlib, name, code, nnz, f32):
+    """The packed CRBA routine emits exactly the branch-sparse lower
+    triangle of the reference's M (dynamics.hpp:331-350), and every entry it
+    drops is an exact zero of the reference (test_dynamics.cpp:200-216)."""
+    om = Model.builtin(name)
+    pat = _lower_pattern(om)
+    assert len(pat) == nnz
+    q, _, _, _ = om.random_states(1024, 31 + code, True, False)
+    Mp, _, _ = _run(genlib, code, 7, (q,), nnz, f32=f32)
+    ref = om.crba(q)
+    rows, cols = np.array(pat).T
+    assert rel_err(Mp, ref[:, rows, cols], axis=1).max() <= (1e-4 if f32 else 1e-10)
+    keep = np.zeros((om.n, om.n), bool)
+    keep[rows, cols] = keep[cols, rows] = True
+    assert np.all(ref[:, ~keep] == 0)
+    if not f32:  # same generated arithmetic as the dense routine: bitwise equal
+        Md, _, _ = _run(genlib, code, 4, (q,), om.n * om.n)
+        assert np.array_equal(Mp, Md[:, cols * om.n + rows])
 
 
 @pytest.mark.parametrize("name,code,frame", [("chain7", 1, "ee"), ("tree29", 2, "l_palm"), ("tree29", 2, "head"),

@@ -64,7 +64,7 @@ def test_rnea_fp64(vd, cuda, omodels, name, generic):
     ref = om.rnea(q, qd, qdd)
     got = _np(vd.rnea(dm, _t(q), _t(qd), _t(qdd)))
     assert rel_err(got, ref, axis=1).max() <= TOL64
-    # bias, gravity, coriolis (dynamics.hpp:557-571)
+    # bias, gravity, coriolis (dynamics.hpp:402-416)
     z = np.zeros_like(q)
     assert rel_err(_np(vd.bias_forces(dm, _t(q), _t(qd))), om.rnea(q, qd, z), axis=1).max() <= TOL64
     assert rel_err(_np(vd.gravity_vector(dm, _t(q))), om.rnea(q, z, z), axis=1).max() <= TOL64
@@ -106,7 +106,7 @@ def test_crba_fp64(vd, cuda, omodels, name, generic):
     ref = om.crba(q)
     got = _np(vd.crba(dm, _t(q)))
     assert rel_err(got, ref, axis=1).max() <= TOL64
-    # exact zeros between branches (test_dynamics.cpp:352-368)
+    # exact zeros between branches (test_dynamics.cpp:200-216)
     mask = m.ancestor_mask()
     off = (mask == 0) & (mask.T == 0)
     assert np.all(got[:, off] == 0.0)
@@ -120,6 +120,46 @@ def test_crba_fp32(vd, cuda, omodels, name):
     q, _, _, _ = _states(om, 2048, 22, with_tau=False)
     got = _np(vd.crba(dm, _t(q, torch.float32)))
     assert rel_err(got, om.crba(q), axis=1).max() <= TOL32
+
+
+@pytest.mark.parametrize("name", ROBOTS)
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_crba_packed(vd, cuda, omodels, name, generic, dtype):
+    """vd_crba_packed: the branch-sparse lower triangle of M (dynamics.hpp:
+    331-350) against the oracle, and bitwise equal to the dense vd_crba output
+    at the packed positions (same generated arithmetic / a gather of it)."""
+    om = omodels[name]
+    m, dm = _dm(vd, name, generic)
+    rows, cols = m.crba_pattern()
+    mask = m.ancestor_mask()
+    assert len(rows) == int(np.tril(mask).sum())
+    q, _, _, _ = _states(om, 3001, 23, with_tau=False)  # ragged batch (not a multiple of the CTA)
+    qt = _t(q, dtype)
+    Mp = vd.crba_packed(dm, qt)
+    assert Mp.shape == (3001, len(rows))
+    ref = om.crba(q)
+    tol = TOL64 if dtype == torch.float64 else TOL32
+    assert rel_err(_np(Mp), ref[:, rows, cols], axis=1).max() <= tol
+    dense = vd.crba(dm, qt)
+    if generic or name == "tree29":  # both from the same generated routine / a gather of the dense M
+        assert torch.equal(Mp, dense[:, rows, cols])
+        assert torch.equal(vd.unpack_crba(m, Mp), dense)
+    else:  # chain7 dense M runs the template kernel, packed the generated routine
+        assert rel_err(_np(vd.unpack_crba(m, Mp)), _np(dense), axis=1).max() <= tol
+        assert torch.equal(vd.unpack_crba(m, Mp) == 0, dense == 0)
+    # ld_out > N through the C-ABI (strided planes), and N = 0
+    N, nnz = 1000, len(rows)
+    out = torch.full((nnz, N + 37), -1.0, dtype=dtype, device="cuda")
+    qs = qt[:N].t().contiguous()
+    lib = vd._lib.load()
+    rc = lib.vd_crba_packed(dm.handle, 0 if dtype == torch.float64 else 1, N, qs.data_ptr(), N, out.data_ptr(), N + 37,
+                            None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert torch.equal(out[:, :N].t(), Mp[:N])
+    assert torch.all(out[:, N:] == -1.0)
+    assert lib.vd_crba_packed(dm.handle, 0, 0, qs.data_ptr(), 0, out.data_ptr(), 0, None) == 0
 
 
 # ---------------------------------------------------------------- forward dynamics (ABA vs LLT oracle)
@@ -200,7 +240,7 @@ def test_dynamics_fused(vd, cuda, omodels):
 
 
 def test_singular_model_reports_status(vd, cuda):
-    # test_dynamics.cpp:524-534: a zero-inertia dof -> SingularInertiaError
+    # test_dynamics.cpp:372-382: a zero-inertia dof -> SingularInertiaError
     text = """<robot name="g"><link name="base"/>
       <link name="ghost"><inertial><mass value="0"/><inertia ixx="0" ixy="0" ixz="0" iyy="0" iyz="0" izz="0"/>
       </inertial></link>
@@ -375,7 +415,7 @@ def test_edge_cases(vd, cuda, omodels):
         vd.rnea(dm, _t(np.zeros((3, 6))), _t(np.zeros((3, 6))), _t(np.zeros((3, 6))))
     with pytest.raises(vd.UnknownFrameError):
         vd.geometric_jacobian(dm, _t(q), "nope")
-    # 0-dof model yields empty results (test_dynamics.cpp:567-576)
+    # 0-dof model yields empty results (test_dynamics.cpp:415-424)
     m0 = vd.urdf.load_model_from_string(
         '<robot name="z"><link name="base"/><link name="tool"/>'
         '<joint name="mount" type="fixed"><parent link="base"/><child link="tool"/></joint></robot>')
@@ -387,7 +427,7 @@ def test_edge_cases(vd, cuda, omodels):
 # ---------------------------------------------------------------- full-size properties
 def test_full_size_properties(vd, cuda):
     """BASELINE configs at full size: FD∘ID roundtrip (test_dynamics.cpp:335-351)
-    and CRBA column = RNEA(e_i) (test_dynamics.cpp:305-321) on the device."""
+    and CRBA column = RNEA(e_i) (test_dynamics.cpp:153-166) on the device."""
     for name, N in (("chain7", 65536), ("tree29", 262144)):
         m, dm = _dm(vd, name)
         g = torch.Generator(device="cuda").manual_seed(9)

@@ -12,6 +12,7 @@ cap chain7_aba_f64 aba chain7 f64 4194304 'k_gen|k_tiled|k_aba'
 cap tree29_aba_f64 aba tree29 f64 262144 'k_gen'
 cap tree29_rnea_f64 rnea tree29 f64 262144 'k_gen'
 cap tree29_crba_f64 crba tree29 f64 262144 'k_gen'
+cap tree29_crba_packed_f64 crbap tree29 f64 262144 'k_gen'
 cap tree29_osc_f64 osc tree29 f64 262144 'k_gen_osc'
 python bench.py --steps 3 --warmup 3 --no-configs --no-cpu > gpurun_out/${R}_bench_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv \

@@ -112,6 +112,15 @@ int main(int argc, char** argv) {
   run<R::Crba, double, 0, 55, 3>("t29 crba f64 s55 b3", N, xd, yd, st, sd, cap, n);
   run<R::Crba, double, 0, 0, 4>("t29 crba f64 s0 b4", N, xd, yd, st, sd, cap, n);
   run<R::Crba, double, 0, 40, 4>("t29 crba f64 s40 b4", N, xd, yd, st, sd, cap, n);
+  run<R::CrbaPacked, double, 0, 40, 4>("t29 crbap f64 s40 b4", N, xd, yd, st, sd, cap, n);
+  run<R::CrbaPacked, double, 0, 55, 4>("t29 crbap f64 s55 b4", N, xd, yd, st, sd, cap, n);
+  run<R::CrbaPacked, double, 0, 28, 6>("t29 crbap f64 s28 b6", N, xd, yd, st, sd, cap, n);
+  run<R::CrbaPacked, double, 0, 24, 6>("t29 crbap f64 s24 b6", N, xd, yd, st, sd, cap, n);
+  run<R::CrbaPacked, double, 0, 20, 8>("t29 crbap f64 s20 b8", N, xd, yd, st, sd, cap, n);
+  run<R::CrbaPacked, double, 0, 0, 8>("t29 crbap f64 s0 b8", N, xd, yd, st, sd, cap, n);
+  run<R::CrbaPacked, double, 0, 0, 6>("t29 crbap f64 s0 b6", N, xd, yd, st, sd, cap, n);
+  run<R::CrbaPacked, double, 55, 0, 3>("t29 crbap f64 r55 b3", N, xd, yd, st, sd, cap, n);
+  run<R::CrbaPacked, double, 55, 0, 4>("t29 crbap f64 r55 b4", N, xd, yd, st, sd, cap, n);
   run<R::Fk, double, 0, 55, 3>("t29 fk f64 s55 b3", N, xd, yd, st, sd, cap, n);
   run<R::Fk, double, 0, 0, 4>("t29 fk f64 s0 b4", N, xd, yd, st, sd, cap, n);
   run<R::Fk, double, 0, 40, 4>("t29 fk f64 s40 b4", N, xd, yd, st, sd, cap, n);
@@ -127,6 +136,11 @@ int main(int argc, char** argv) {
   run<R::Rnea, float, 55, 0, 3>("t29 rnea f32 r55 b3", N, xf, yf, st, sf, cap, n);
   run<R::Crba, float, 0, 55, 4>("t29 crba f32 s55 b4", N, xf, yf, st, sf, cap, n);
   run<R::Crba, float, 55, 0, 3>("t29 crba f32 r55 b3", N, xf, yf, st, sf, cap, n);
+  run<R::CrbaPacked, float, 0, 55, 4>("t29 crbap f32 s55 b4", N, xf, yf, st, sf, cap, n);
+  run<R::CrbaPacked, float, 0, 55, 6>("t29 crbap f32 s55 b6", N, xf, yf, st, sf, cap, n);
+  run<R::CrbaPacked, float, 0, 40, 8>("t29 crbap f32 s40 b8", N, xf, yf, st, sf, cap, n);
+  run<R::CrbaPacked, float, 0, 0, 8>("t29 crbap f32 s0 b8", N, xf, yf, st, sf, cap, n);
+  run<R::CrbaPacked, float, 55, 0, 4>("t29 crbap f32 r55 b4", N, xf, yf, st, sf, cap, n);
   run<R::Fk, float, 0, 55, 4>("t29 fk f32 s55 b4", N, xf, yf, st, sf, cap, n);
   run<R::Fk, float, 55, 0, 4>("t29 fk f32 r55 b4", N, xf, yf, st, sf, cap, n);
   // chain7 (N = 4M) vs the template kernels
@@ -135,6 +149,11 @@ int main(int argc, char** argv) {
   cudaFree(st); cudaMalloc(&st, N7 * 4);
   k_fill<<<1024, 256>>>(x7, 3 * N7 * 7, 2);
   using C = GenChain7;
+  run<C::CrbaPacked, double, 14, 0, 4>("c7 crbap f64 allreg b4", N7, x7, y7, st, sd, cap, 7);
+  run<C::CrbaPacked, double, 14, 0, 6>("c7 crbap f64 allreg b6", N7, x7, y7, st, sd, cap, 7);
+  run<C::CrbaPacked, double, 14, 0, 8>("c7 crbap f64 allreg b8", N7, x7, y7, st, sd, cap, 7);
+  run<C::CrbaPacked, double, 0, 14, 8>("c7 crbap f64 s14 b8", N7, x7, y7, st, sd, cap, 7);
+  run<C::Crba, double, 14, 0, 4>("c7 crba f64 allreg b4", N7, x7, y7, st, sd, cap, 7);
   run<C::Aba, double, C::Aba::kSlots, 0, 3>("c7 aba f64 allreg b3", N7, x7, y7, st, sd, cap, 7);
   run<C::Aba, double, C::Aba::kSlots, 0, 4>("c7 aba f64 allreg b4", N7, x7, y7, st, sd, cap, 7);
   run<C::Aba, double, 44, 28, 3>("c7 aba f64 r44 s28 b3", N7, x7, y7, st, sd, cap, 7);

@@ -409,6 +409,21 @@ class Robot:
         for i, p in enumerate(self.parent):
             (self.children[p] if p >= 0 else self.roots).append(i)
 
+    def lower_pattern(self):
+        """Branch-sparse lower triangle of M in compressed-column order: (r, c)
+        for c ascending, r ascending, c an ancestor of r or r itself.  Every
+        other entry of M is an exact zero (dynamics.hpp:330-335,
+        test_dynamics.cpp:200-216).  Same order as vd_model_crba_pattern."""
+        out = []
+        for c in range(self.n):
+            for r in range(c, self.n):
+                j = r
+                while j >= 0 and j != c:
+                    j = self.parent[j]
+                if j == c:
+                    out.append((r, c))
+        return out
+
     def axis(self, i):
         return [K(v) for v in self.d["axis"][3 * i:3 * i + 3]]
 
@@ -692,10 +707,12 @@ def gen_rnea(rb, with_qd, with_qdd, dual=False):
     return A.finish()
 
 
-def gen_crba(rb, dual=False):
+def gen_crba(rb, dual=False, packed=False):
     """CRBA (crba_loop, dynamics.hpp:369-400; Alg. 2 of PAPER.md:156-165):
     x(0) = q; y(0, c·n + r) = M(r, c), dense, with exact zeros between
-    branches (dynamics.hpp:330-335, test_dynamics.cpp:200-216).  Composite
+    branches (dynamics.hpp:330-335, test_dynamics.cpp:200-216).  packed: only
+    the branch-sparse lower triangle, y(0, k) = M(r_k, c_k) for the k-th pair
+    of Robot.lower_pattern() (G1: 242 of 841 values).  Composite
     inertias (10-parameter form) are summed leaf -> root in one DFS; each
     column is emitted as soon as its composite is complete, walking the force
     F = Ic S up the ancestor chain."""
@@ -703,9 +720,13 @@ def gen_crba(rb, dual=False):
     g = A.g
     n = rb.n
     related = [[False] * n for _ in range(n)]
+    pidx = {rc: k for k, rc in enumerate(rb.lower_pattern())}
 
     def emit(r, c, val):
         related[r][c] = related[c][r] = True
+        if packed:
+            g.output(0, pidx[(r, c)], val)
+            return
         g.output(0, c * n + r, val)
         if r != c:
             g.output(0, r * n + c, val)
@@ -729,7 +750,7 @@ def gen_crba(rb, dual=False):
 
     for r in rb.roots:
         rec(r)
-    for c in range(n):
+    for c in range(n if not packed else 0):
         for r in range(n):
             if not related[r][c]:
                 g.output(0, c * n + r, ZERO)
@@ -1186,20 +1207,21 @@ def trunk(rb):
     return out if i >= 0 and len(rb.children[i]) > 1 else []
 
 
-OPS = [("Aba", gen_aba, lambda n: n, 3),
+OPS = [("Aba", gen_aba, lambda rb: rb.n, 3),
        # fp32 kernels: the floating-base trunk in fp64 (DESIGN.md §Parity policy)
-       ("AbaMixed", lambda rb: gen_aba(rb, trunk(rb), tau_prologue=True), lambda n: n, 3),
-       ("Rnea", lambda rb: gen_rnea(rb, True, True), lambda n: n, 3),
-       ("RneaBias", lambda rb: gen_rnea(rb, True, False), lambda n: n, 2),
-       ("RneaGrav", lambda rb: gen_rnea(rb, False, False), lambda n: n, 1),
-       ("Crba", gen_crba, lambda n: n * n, 1),
+       ("AbaMixed", lambda rb: gen_aba(rb, trunk(rb), tau_prologue=True), lambda rb: rb.n, 3),
+       ("Rnea", lambda rb: gen_rnea(rb, True, True), lambda rb: rb.n, 3),
+       ("RneaBias", lambda rb: gen_rnea(rb, True, False), lambda rb: rb.n, 2),
+       ("RneaGrav", lambda rb: gen_rnea(rb, False, False), lambda rb: rb.n, 1),
+       ("Crba", gen_crba, lambda rb: rb.n * rb.n, 1),
+       ("CrbaPacked", lambda rb: gen_crba(rb, packed=True), lambda rb: len(rb.lower_pattern()), 1),
        # forward-mode JVPs (autodiff.hpp:41-50 on dual.hpp scalars): value in
        # output group 0, tangent in group 1
-       ("AbaJvp", lambda rb: gen_aba(rb, dual=True), lambda n: n, 3),
-       ("RneaJvp", lambda rb: gen_rnea(rb, True, True, dual=True), lambda n: n, 3),
-       ("CrbaJvp", lambda rb: gen_crba(rb, dual=True), lambda n: n * n, 1),
-       ("FkJvp", lambda rb: gen_fk(rb, dual=True), lambda n: 12 * n, 1),
-       ("Fk", gen_fk, lambda n: 12 * n, 1)]
+       ("AbaJvp", lambda rb: gen_aba(rb, dual=True), lambda rb: rb.n, 3),
+       ("RneaJvp", lambda rb: gen_rnea(rb, True, True, dual=True), lambda rb: rb.n, 3),
+       ("CrbaJvp", lambda rb: gen_crba(rb, dual=True), lambda rb: rb.n * rb.n, 1),
+       ("FkJvp", lambda rb: gen_fk(rb, dual=True), lambda rb: 12 * rb.n, 1),
+       ("Fk", gen_fk, lambda rb: 12 * rb.n, 1)]
 
 
 def emit(name, cls, rb):
@@ -1241,7 +1263,7 @@ def emit_body(name, cls, rb):
                 f"    static constexpr int kPrologue = {A.nprologue};",
                 f"    static constexpr int kFlops = {A.g.flops};",
                 f"    static constexpr int kIn = {nin};",
-                f"    static constexpr int kOut = {nout(rb.n)};",
+                f"    static constexpr int kOut = {nout(rb)};",
                 "    template <class T, class Cx>",
                 "    VD_HD static bool run(Cx& cx) {"]
         out += ["    " + ln for ln in A.g.lines]

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Minimal driver for ncu captures: a few launches of one hot-path kernel.
 
-Usage: python tools/prof_kernel.py [aba|rnea|crba|dyn|osc|fk] [chain7|tree29] [f64|f32] [N] [launches]
+Usage: python tools/prof_kernel.py [aba|rnea|crba|crbap|dyn|osc|fk] [chain7|tree29] [f64|f32] [N] [launches]
 """
 import ctypes
 import os
@@ -40,6 +40,8 @@ def main():
                              out.data_ptr(), N, s)
         elif op == "crba":
             rc = lib.vd_crba(dm.handle, code, N, x[0].data_ptr(), N, out.data_ptr(), N, s)
+        elif op == "crbap":
+            rc = lib.vd_crba_packed(dm.handle, code, N, x[0].data_ptr(), N, out.data_ptr(), N, s)
         elif op == "fk":
             rc = lib.vd_fk(dm.handle, code, N, x[0].data_ptr(), N, out.data_ptr(), N, s)
         elif op == "osc":

@@ -127,6 +127,8 @@ def main():
               bench.flops_per_eval("tree29", "rnea"), 928),
              ("tree29_crba_f64", "k_gen<GenTree29::Crba, double> (generated)", 262144,
               bench.flops_per_eval("tree29", "crba"), 232 + 6728),
+             ("tree29_crba_packed_f64", "k_gen<GenTree29::CrbaPacked, double> (generated, 242 packed planes)", 262144,
+              bench.flops_per_eval("tree29", "crba"), 232 + 242 * 8),
              ("tree29_osc_f64", "k_gen_osc<GenTree29::Osc23, double> (generated, frame l_palm)", 262144, None,
               464 + 232 + 288)]
     for key, name, states, fl, bps in specs:
