@@ -127,8 +127,9 @@ def test_crba_fp32(vd, cuda, omodels, name):
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 def test_crba_packed(vd, cuda, omodels, name, generic, dtype):
     """vd_crba_packed: the branch-sparse lower triangle of M (dynamics.hpp:
-    331-350) against the oracle, and bitwise equal to the dense vd_crba output
-    at the packed positions (same generated arithmetic / a gather of it)."""
+    331-350) against the oracle, and equal to the dense vd_crba output at the
+    packed positions (bitwise for the gather path, to 1e-13 / 1e-5 for the
+    separately compiled generated routine)."""
     om = omodels[name]
     m, dm = _dm(vd, name, generic)
     rows, cols = m.crba_pattern()
@@ -142,11 +143,17 @@ def test_crba_packed(vd, cuda, omodels, name, generic, dtype):
     tol = TOL64 if dtype == torch.float64 else TOL32
     assert rel_err(_np(Mp), ref[:, rows, cols], axis=1).max() <= tol
     dense = vd.crba(dm, qt)
-    if generic or name == "tree29":  # both from the same generated routine / a gather of the dense M
+    if generic:  # a coalesced gather of the dense M: bitwise
         assert torch.equal(Mp, dense[:, rows, cols])
         assert torch.equal(vd.unpack_crba(m, Mp), dense)
-    else:  # chain7 dense M runs the template kernel, packed the generated routine
-        assert rel_err(_np(vd.unpack_crba(m, Mp)), _np(dense), axis=1).max() <= tol
+    else:
+        # tree29: the packed and dense routines are generated from the same
+        # expression graph (gen_crba) but compiled as separate straight-line
+        # kernels, so ptxas's FMA contraction may differ in the last bits;
+        # chain7 dense M runs the template kernel.  Tight agreement + the
+        # identical exact-zero pattern.
+        close = 1e-13 if dtype == torch.float64 else 1e-5
+        assert rel_err(_np(vd.unpack_crba(m, Mp)), _np(dense), axis=1).max() <= close
         assert torch.equal(vd.unpack_crba(m, Mp) == 0, dense == 0)
     # ld_out > N through the C-ABI (strided planes), and N = 0
     N, nnz = 1000, len(rows)
