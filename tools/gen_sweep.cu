@@ -4,6 +4,8 @@
 #include <cstring>
 #include <vector>
 #include <cmath>
+#include <cstdlib>
+#include <algorithm>
 #include "vd_gen_kernels.cuh"
 using namespace vdk;
 static const char* g_filter = nullptr;
@@ -49,6 +51,9 @@ void run_osc(const char* name, int64_t N, T* x, T* y, T* lam, int32_t* st, T* sc
   int bps = 0, sms = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  // SWEEP_CTAS_PER_SM caps the persistent grid below the occupancy limit so
+  // the per-thread L2 scratch slab can be sized to fit L2.
+  if (const char* e = getenv("SWEEP_CTAS_PER_SM")) bps = std::min(bps, atoi(e));
   int64_t grid = (int64_t)sms * bps;
   if ((size_t)(grid * kGenBlock * gen_scratch_per_thread<Op, T, kReg, kSmem>() * sizeof(T)) > cap) { printf("%s scratch\n", name); return; }
   OscShared P{};
