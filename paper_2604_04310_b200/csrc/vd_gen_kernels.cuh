@@ -65,7 +65,11 @@ struct GenMem<float> {
   }
 };
 
-template <class T, int kSlots, int kReg, int kSmem, bool kFast = false>
+// kStream: state inputs are read and outputs written with the evict-first
+// (.cs) cache operator, so the streamed batch does not push the per-thread
+// scratch slab out of L2 (gen_sweep: G1 ABA fp64 0.31-0.42 -> 0.29 ms, dense
+// CRBA 1.1-1.8x; it slows the OSC routines, which keep the default).
+template <class T, int kSlots, int kReg, int kSmem, bool kFast = false, bool kStream = false>
 struct GenCx {
   static constexpr bool kFastTrig = kFast;  // fp64 sin/cos by vd_sincos_f64
   static constexpr int kGlobal = kSlots - kReg - kSmem > 0 ? kSlots - kReg - kSmem : 0;
@@ -77,7 +81,10 @@ struct GenCx {
   bool active;      // false on the padding lanes of the last round (they compute, but write nothing)
   T g3[3];
   T reg[kReg > 0 ? kReg : 1];
-  __device__ __forceinline__ T x(int g, int j) const { return GenMem<T>::ldg(in_[g] + j * ld); }
+  __device__ __forceinline__ T x(int g, int j) const {
+    if constexpr (kStream) return __ldcs(in_[g] + j * ld);
+    else return GenMem<T>::ldg(in_[g] + j * ld);
+  }
   __device__ __forceinline__ void prefetch(int g, int j) const {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(in_[g] + j * ld));
   }
@@ -107,7 +114,11 @@ struct GenCx {
     else return __hiloint2double(__float_as_int(get(k + 1)), __float_as_int(get(k)));
   }
   __device__ __forceinline__ void y(int, int k, T v) const {
-    if (active) out_[k * ldo] = v;
+    if constexpr (kStream) {
+      if (active) __stcs(out_ + k * ldo, v);
+    } else {
+      if (active) out_[k * ldo] = v;
+    }
   }
 };
 
@@ -119,12 +130,12 @@ constexpr int64_t gen_scratch_per_thread() {
 
 // One generated routine (Op = GenRobot::Aba / Rnea / RneaBias / RneaGrav /
 // Crba / Fk) over a persistent grid: every thread strides over the batch.
-template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false>
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false, bool kStream = false>
 __global__ void __launch_bounds__(kGenBlock, kMinB)
     k_gen(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
           T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status, T* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
-  using Cx = GenCx<T, Op::kSlots, kReg, kSmem, kFast>;
+  using Cx = GenCx<T, Op::kSlots, kReg, kSmem, kFast, kStream>;
   Cx cx;
   const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * kGenBlock;

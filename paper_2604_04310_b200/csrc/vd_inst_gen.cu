@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "vd_gen_kernels.cuh"
 #include "vd_launch.hpp"
@@ -22,6 +23,11 @@ struct Cfg {
   static constexpr int kReg = 0, kSmem = Op::kSlots < 55 ? Op::kSlots : 55, kMinB = sizeof(T) == 8 ? 3 : 4;
   static constexpr bool kFast = false;  // vd_sincos_f64 instead of the library sincos
 };
+// kStream (GenCx): evict-first state I/O; false unless a Cfg sets it
+template <class C, class = void>
+struct StreamIo : std::false_type {};
+template <class C>
+struct StreamIo<C, std::void_t<decltype(C::kStream)>> : std::bool_constant<C::kStream> {};
 template <>
 struct Cfg<GenChain7::Aba, double> {  // the headline kernel: 0.60 ms / 4M states vs 0.61 templated
   static constexpr int kReg = 44, kSmem = 28, kMinB = 4;
@@ -40,20 +46,28 @@ template <class T>
 struct Cfg<GenChain7::RneaBias, T> : Chain7RneaCfg<T, GenChain7::RneaBias::kSlots> {};
 template <class T>
 struct Cfg<GenChain7::RneaGrav, T> : Chain7RneaCfg<T, GenChain7::RneaGrav::kSlots> {};
+// G1 ABA / dense CRBA with evict-first state I/O (gen_sweep, two runs each,
+// N = 262144): ABA fp64 0.31-0.42 -> 0.29 ms, mixed fp32 0.19 -> 0.17 ms,
+// CRBA fp64 0.39 (s40 b4) -> 0.30 ms (s55 b3), fp32 0.30 -> 0.16 ms
 template <>
 struct Cfg<GenTree29::Aba, double> {
   static constexpr int kReg = 40, kSmem = 113, kMinB = 2;
-  static constexpr bool kFast = false;
+  static constexpr bool kFast = false, kStream = true;
 };
 template <>
 struct Cfg<GenTree29::AbaMixed, float> {  // the trunk's fp64 slots (stored last) in registers
   static constexpr int kReg = 40, kSmem = 122, kMinB = 3;
-  static constexpr bool kFast = false;
+  static constexpr bool kFast = false, kStream = true;
 };
 template <>
 struct Cfg<GenTree29::Crba, double> {
-  static constexpr int kReg = 0, kSmem = 40, kMinB = 4;
-  static constexpr bool kFast = false;
+  static constexpr int kReg = 0, kSmem = 55, kMinB = 3;
+  static constexpr bool kFast = false, kStream = true;
+};
+template <>
+struct Cfg<GenTree29::Crba, float> {
+  static constexpr int kReg = 0, kSmem = 55, kMinB = 4;
+  static constexpr bool kFast = false, kStream = true;
 };
 // packed CRBA (gen_sweep, N = 262144 / 4M): tree29 fp64 all 55 slots in
 // registers at 3 CTAs/SM 0.112 ms (vs 0.133 with the dense routine's
@@ -135,7 +149,7 @@ template <class Op, class T>
 int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
              int32_t* status) {
   using C = Cfg<Op, T>;
-  auto kern = k_gen<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast>;
+  auto kern = k_gen<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
   constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
   const Occ o = occupancy<Op, T>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);

@@ -1,5 +1,5 @@
 // Placement/occupancy sweep of the generated kernels (tools/gen_tree_kernels.py) on one GPU.
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr -Ipaper_2604_04310_b200/csrc tools/gen_sweep.cu -o ablib/gen_sweep
+// Build: nvcc [-DSWEEP_STREAM=true] -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr -Ipaper_2604_04310_b200/csrc tools/gen_sweep.cu -o ablib/gen_sweep
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -8,6 +8,10 @@
 #include <algorithm>
 #include "vd_gen_kernels.cuh"
 using namespace vdk;
+// -DSWEEP_STREAM=true: evict-first state I/O (GenCx kStream) for every k_gen entry
+#ifndef SWEEP_STREAM
+#define SWEEP_STREAM false
+#endif
 static const char* g_filter = nullptr;
 template <class T>
 __global__ void k_fill(T* p, int64_t n, uint64_t seed) {
@@ -20,7 +24,7 @@ __global__ void k_fill(T* p, int64_t n, uint64_t seed) {
 template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false>
 void run(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, int n) {
   if (g_filter && !strstr(name, g_filter)) return;
-  auto kern = k_gen<Op, T, kReg, kSmem, kMinB, kFast>;
+  auto kern = k_gen<Op, T, kReg, kSmem, kMinB, kFast, SWEEP_STREAM>;
   size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int bps = 0, sms = 0;
