@@ -234,28 +234,31 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
 
 // Forward-mode JVP context (JvpArgs): NULL primal inputs read as 0, NULL
 // tangents as 0; output group 0 = values, 1 = tangents (either may be NULL).
-template <class T, int kSlots, int kReg, int kSmem>
+template <class T, int kSlots, int kReg, int kSmem, bool kStream = false>
 struct GenJvpCx : GenCx<T, kSlots, kReg, kSmem> {
   const T* din_[3];
   T* dout_;
-  __device__ __forceinline__ T x(int g, int j) const {
-    return this->in_[g] ? GenMem<T>::ldg(this->in_[g] + j * this->ld) : T(0);
+  static __device__ __forceinline__ T ld_(const T* p) {
+    if constexpr (kStream) return __ldcs(p);
+    else return GenMem<T>::ldg(p);
   }
-  __device__ __forceinline__ T dx(int g, int j) const {
-    return din_[g] ? GenMem<T>::ldg(din_[g] + j * this->ld) : T(0);
-  }
+  __device__ __forceinline__ T x(int g, int j) const { return this->in_[g] ? ld_(this->in_[g] + j * this->ld) : T(0); }
+  __device__ __forceinline__ T dx(int g, int j) const { return din_[g] ? ld_(din_[g] + j * this->ld) : T(0); }
   __device__ __forceinline__ T g(int k) const { return this->g3[k]; }
   __device__ __forceinline__ void y(int o, int k, T v) const {
     T* p = o == 0 ? this->out_ : dout_;
-    if (this->active && p) p[k * this->ldo] = v;
+    if (this->active && p) {
+      if constexpr (kStream) __stcs(p + k * this->ldo, v);
+      else p[k * this->ldo] = v;
+    }
   }
 };
 
-template <class Op, class T, int kReg, int kSmem, int kMinB>
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kStream = false>
 __global__ void __launch_bounds__(kGenBlock, kMinB)
     k_gen_jvp(int64_t N, const __grid_constant__ JvpArgs a, int64_t ldi, int64_t ldo, T* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
-  using Cx = GenJvpCx<T, Op::kSlots, kReg, kSmem>;
+  using Cx = GenJvpCx<T, Op::kSlots, kReg, kSmem, kStream>;
   Cx cx;
   const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * kGenBlock;

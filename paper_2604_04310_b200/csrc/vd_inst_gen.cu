@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <type_traits>
+#include <utility>
 
 #include "vd_gen_kernels.cuh"
 #include "vd_launch.hpp"
@@ -209,12 +210,12 @@ struct JvpCfg {
   static constexpr int kReg = sizeof(T) == 8 ? 40 : 0, kSmem = sizeof(T) == 8 ? 110 : 220, kMinB = 2;
 };
 
-template <class Op, class T>
-int launch_jvp_t(const Launch& L, const JvpArgs& a) {
+template <class Op, class T, bool kStream>
+int launch_jvp_v(const Launch& L, const JvpArgs& a) {
   using C = JvpCfg<Op, T>;
-  auto kern = k_gen_jvp<Op, T, C::kReg, C::kSmem, C::kMinB>;
+  auto kern = k_gen_jvp<Op, T, C::kReg, C::kSmem, C::kMinB, kStream>;
   constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
-  const Occ o = occupancy<Op, T>(kern, smem);
+  const Occ o = occupancy<std::pair<Op, std::bool_constant<kStream>>, T>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
   cudaStream_t s = static_cast<cudaStream_t>(L.stream);
   const size_t scratch_bytes = (size_t)blocks * kGenBlock * gen_scratch_per_thread<Op, T, C::kReg, C::kSmem>() * sizeof(T);
@@ -227,6 +228,16 @@ int launch_jvp_t(const Launch& L, const JvpArgs& a) {
   cudaError_t e = cudaGetLastError();
   if (scratch) cudaFreeAsync(scratch, s);
   return (int)e;
+}
+
+// The JVPs read and write every value/tangent plane once: evict-first I/O
+// throughout (tools/jvp_time.py, G1, N = 262144, plain -> .cs): fp64 FK-JVP
+// 0.46 -> 0.37 ms, RNEA-JVP 1.03 -> 0.82, CRBA-JVP 1.33 -> 0.80, ABA-JVP
+// 1.81 -> 1.80; fp32 FK-JVP 0.40 -> 0.27, CRBA-JVP 1.12 -> 0.59, ABA-JVP
+// 1.20 -> 0.93, RNEA-JVP 0.47 -> 0.47.
+template <class Op, class T>
+int launch_jvp_t(const Launch& L, const JvpArgs& a) {
+  return launch_jvp_v<Op, T, true>(L, a);
 }
 
 template <class Op, class T>
