@@ -361,6 +361,10 @@ def _soa(x, n, name, dtype=None, device=None):
     if dtype is not None and x.dtype != dtype:
         x = x.to(dtype)
     if device is not None and x.device != device:
+        if x.is_cuda:
+            # The C-ABI call runs under the model's device and stream; a tensor on
+            # another GPU would be read with no ordering against its producer.
+            raise CudaError(f"{name} is on {x.device}, the device model is on {device}")
         x = x.to(device)
     if not x.is_cuda:
         raise CudaError(f"{name} must be a CUDA tensor (no CPU fallback)")
@@ -377,7 +381,7 @@ def _prep(dm, q, *others):
     n = dm.dof()
     if not torch.is_tensor(q):
         q = torch.as_tensor(np.asarray(q))
-    dev = torch.device("cuda", dm.device) if not q.is_cuda else q.device
+    dev = torch.device("cuda", dm.device)
     qs = _soa(q, n, "q", device=dev)
     rest = [None if o is None else _soa(o, n, nm, dtype=qs.dtype, device=dev) for o, nm in others]
     return qs, rest, qs.shape[1], dev
@@ -393,6 +397,8 @@ def _fext_planes(fext, N, n, dtype, dev):
     if fext is None:
         return None
     torch = _torch()
+    if torch.is_tensor(fext) and fext.is_cuda and fext.device != dev:
+        raise CudaError(f"external forces are on {fext.device}, the device model is on {dev}")
     f = torch.as_tensor(fext, dtype=dtype, device=dev)
     if f.dim() == 2:
         f = f.unsqueeze(0).expand(N, -1, -1)

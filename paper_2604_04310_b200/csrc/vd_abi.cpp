@@ -13,6 +13,7 @@
 #include <random>
 #include <string>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "../../include/vecdyn_cuda.h"
@@ -704,10 +705,15 @@ int prepare_ctx(DevCtx& c, vd_model m, int n, int64_t chunk, int width, bool sta
   }
   const int64_t need_out = chunk * width;
   if (chunk * n > c.cap_in || need_out > c.cap_out || c.cap < chunk) {
+    // Release everything and zero the capacities first: a failed cudaMalloc
+    // below must leave the context empty, never holding freed pointers.
     for (int b = 0; b < 2; ++b) {
-      for (int k = 0; k < 3; ++k) cudaFree(c.din[b][k]);
-      cudaFree(c.dout[b]);
-      cudaFree(c.dst[b]);
+      for (int k = 0; k < 3; ++k) cudaFree(std::exchange(c.din[b][k], nullptr));
+      cudaFree(std::exchange(c.dout[b], nullptr));
+      cudaFree(std::exchange(c.dst[b], nullptr));
+    }
+    c.cap = c.cap_in = c.cap_out = 0;
+    for (int b = 0; b < 2; ++b) {
       for (int k = 0; k < 3; ++k)
         if ((e = cudaMalloc(&c.din[b][k], sizeof(double) * n * chunk)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
       if ((e = cudaMalloc(&c.dout[b], sizeof(double) * need_out)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
@@ -719,9 +725,12 @@ int prepare_ctx(DevCtx& c, vd_model m, int n, int64_t chunk, int width, bool sta
   }
   if (staging && c.cap_pin < chunk * std::max(n, width)) {
     for (int b = 0; b < 2; ++b) {
-      for (int k = 0; k < 3; ++k) cudaFreeHost(c.pin_in[b][k]);
-      cudaFreeHost(c.pin_out[b]);
-      cudaFreeHost(c.pin_st[b]);
+      for (int k = 0; k < 3; ++k) cudaFreeHost(std::exchange(c.pin_in[b][k], nullptr));
+      cudaFreeHost(std::exchange(c.pin_out[b], nullptr));
+      cudaFreeHost(std::exchange(c.pin_st[b], nullptr));
+    }
+    c.cap_pin = 0;
+    for (int b = 0; b < 2; ++b) {
       const int64_t cnt = chunk * std::max(n, width);
       for (int k = 0; k < 3; ++k)
         if ((e = cudaMallocHost(&c.pin_in[b][k], sizeof(double) * cnt)) != cudaSuccess) return cuda_fail(e, "pinned");

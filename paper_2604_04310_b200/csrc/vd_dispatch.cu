@@ -1,4 +1,6 @@
 // Host-side dispatch from a Launch descriptor to the per-view launchers.
+#include <mutex>
+
 #include "vd_kernels.cuh"
 
 namespace vdk {
@@ -29,6 +31,34 @@ int with_view(const Launch& L, Fn&& fn) {
 }  // namespace
 
 int match_spec(uint64_t fp, int n) { return match_spec_tables(fp, n); }
+
+int scratch_alloc(void** p, size_t bytes, void* stream) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev & 63]) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      cudaError_t e = cudaMemPoolCreate(&pools[dev & 63], &props);
+      if (e != cudaSuccess) return (int)e;
+      uint64_t thr = kScratchKeepBytes;
+      cudaMemPoolSetAttribute(pools[dev & 63], cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool = pools[dev & 63];
+  }
+  *p = nullptr;
+  return (int)cudaMallocFromPoolAsync(p, bytes, pool, static_cast<cudaStream_t>(stream));
+}
+
+void scratch_free(void* p, void* stream) {
+  if (p) cudaFreeAsync(p, static_cast<cudaStream_t>(stream));
+}
 int launch_jac_scan(const Launch& L, const void* q, const FrameArg& fr, void* pose, void* J);
 
 int launch_fk(const Launch& L, const void* q, void* out) {
@@ -92,24 +122,31 @@ __global__ void k_pack_lower(int64_t N, const T* __restrict__ M, int64_t ld_m, c
 int launch_crba_packed(const Launch& L, const void* q, void* Mp, const PackTable& tab) {
   if (L.N == 0 || tab.nnz == 0) return 0;
   if (const int rc = launch_gen_crba_packed(L, q, Mp); rc >= 0) return rc;
-  // dense M into stream-ordered scratch, then gather
+  // Dense M of a chunk of states into pool scratch, then gather.  Chunked so
+  // the scratch stays bounded (a 64-dof model at 4M states would otherwise
+  // need n²·N·8 B ≈ 137 GB): at most ~256 MB of dense planes per chunk.
   cudaStream_t s = static_cast<cudaStream_t>(L.stream);
   const size_t es = L.dtype == 0 ? sizeof(double) : sizeof(float);
+  const size_t plane_set = (size_t)L.n * L.n * es;
+  const int64_t chunk = std::min<int64_t>(L.N, std::max<int64_t>(1024, (int64_t)((256ull << 20) / plane_set)) / 128 * 128);
   void* dense = nullptr;
-  cudaError_t e = cudaMallocAsync(&dense, (size_t)L.N * L.n * L.n * es, s);
-  if (e != cudaSuccess) return (int)e;
-  Launch Ld = L;
-  Ld.ld_out = L.N;
-  int rc = launch_crba(Ld, q, dense);
-  if (rc == 0) {
-    const dim3 grid((unsigned)std::min<int64_t>((L.N + 255) / 256, 1184), (unsigned)tab.nnz);
+  if (int rc = scratch_alloc(&dense, (size_t)chunk * plane_set, L.stream)) return rc;
+  const size_t tsz = L.dtype == 0 ? sizeof(double) : sizeof(float);
+  int rc = 0;
+  for (int64_t b = 0; b < L.N && rc == 0; b += chunk) {
+    Launch Ld = L;
+    Ld.N = std::min<int64_t>(chunk, L.N - b);
+    Ld.ld_out = chunk;
+    rc = launch_crba(Ld, static_cast<const char*>(q) + b * tsz, dense);
+    if (rc != 0) break;
+    const dim3 grid((unsigned)std::min<int64_t>((Ld.N + 255) / 256, 1184), (unsigned)tab.nnz);
     if (L.dtype == 0)
-      k_pack_lower<double><<<grid, 256, 0, s>>>(L.N, (const double*)dense, L.N, tab, (double*)Mp, L.ld_out);
+      k_pack_lower<double><<<grid, 256, 0, s>>>(Ld.N, (const double*)dense, chunk, tab, (double*)Mp + b, L.ld_out);
     else
-      k_pack_lower<float><<<grid, 256, 0, s>>>(L.N, (const float*)dense, L.N, tab, (float*)Mp, L.ld_out);
+      k_pack_lower<float><<<grid, 256, 0, s>>>(Ld.N, (const float*)dense, chunk, tab, (float*)Mp + b, L.ld_out);
     rc = (int)cudaGetLastError();
   }
-  cudaFreeAsync(dense, s);
+  scratch_free(dense, L.stream);
   return rc;
 }
 

@@ -114,17 +114,6 @@ inline bool debug_launches() {
   return on;
 }
 
-// The scratch slabs come from the device's default stream-ordered pool; by
-// default the pool hands memory back to the driver at every synchronisation,
-// which turns each launch's cudaMallocAsync into a real allocation.  Keep it.
-inline void keep_pool_memory(int dev) {
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-}
-
 // Occupancy (and the dynamic shared-memory opt-in) once per device for each
 // kernel instantiation; keyed by <Op, T>, not by the kernel's function type
 // (all variants of one dtype share it).
@@ -137,7 +126,6 @@ Occ occupancy(Kern kern, size_t smem) {
   std::lock_guard<std::mutex> lk(mu);
   Occ& c = occ[dev & 63];
   if (!c.blocks_per_sm) {
-    keep_pool_memory(dev);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.blocks_per_sm, kern, kGenBlock, smem);
@@ -160,19 +148,19 @@ int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, co
                  C::kReg, C::kSmem, o.blocks_per_sm, o.sms, (long long)blocks, smem);
   // L2-resident scratch for the slots that are neither in registers nor in
   // shared memory: one slab per resident thread, stream-ordered from the
-  // device's memory pool (no synchronisation, safe for concurrent streams).
+  // library's private pool (scratch_alloc: no synchronisation, safe for
+  // concurrent streams, bounded caching).
   const size_t scratch_bytes = (size_t)blocks * kGenBlock * gen_scratch_per_thread<Op, T, C::kReg, C::kSmem>() * sizeof(T);
   T* scratch = nullptr;
   if (scratch_bytes) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_bytes, s);
-    if (e != cudaSuccess) return (int)e;
+    if (int rc = scratch_alloc(reinterpret_cast<void**>(&scratch), scratch_bytes, s)) return rc;
   }
   // gravity3 == NULL: GravitySpec::standard() (dynamics.hpp:39-50), as g3_of
   const T g0 = g3 ? T(g3[0]) : T(0), g1 = g3 ? T(g3[1]) : T(0), g2 = g3 ? T(g3[2]) : T(9.81);
   kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, (const T*)x0, (const T*)x1, (const T*)x2, L.ld_in, g0, g1, g2,
                                                  (T*)y, L.ld_out, status, scratch);
   cudaError_t e = cudaGetLastError();
-  if (scratch) cudaFreeAsync(scratch, s);
+  scratch_free(scratch, s);
   return (int)e;
 }
 
@@ -195,19 +183,24 @@ int launch_osc_t(const Launch& L, const void* q, const void* qd, const OscShared
   const size_t scratch_bytes = (size_t)blocks * kGenBlock * gen_scratch_per_thread<Op, T, C::kReg, C::kSmem>() * sizeof(T);
   T* scratch = nullptr;
   if (scratch_bytes) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_bytes, s);
-    if (e != cudaSuccess) return (int)e;
+    if (int rc = scratch_alloc(reinterpret_cast<void**>(&scratch), scratch_bytes, s)) return rc;
   }
   kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, (const T*)q, (const T*)qd, L.ld_in, P, (T*)tau, (T*)lam,
                                                  L.ld_out, status, scratch);
   cudaError_t e = cudaGetLastError();
-  if (scratch) cudaFreeAsync(scratch, s);
+  scratch_free(scratch, s);
   return (int)e;
 }
 
+// Placement caps, clamped to the routine's own slot count so a small routine
+// (FK-JVP, CRBA-JVP) does not reserve shared memory it never touches and is
+// not held at the occupancy of the largest one (ABA-JVP).
 template <class Op, class T>
 struct JvpCfg {
-  static constexpr int kReg = sizeof(T) == 8 ? 40 : 0, kSmem = sizeof(T) == 8 ? 110 : 220, kMinB = 2;
+  static constexpr int kRegCap = sizeof(T) == 8 ? 40 : 0, kSmemCap = sizeof(T) == 8 ? 110 : 220;
+  static constexpr int kReg = kRegCap < Op::kSlots ? kRegCap : Op::kSlots;
+  static constexpr int kSmem = kSmemCap < Op::kSlots - kReg ? kSmemCap : Op::kSlots - kReg;
+  static constexpr int kMinB = 2;
 };
 
 template <class Op, class T, bool kStream>
@@ -221,12 +214,11 @@ int launch_jvp_v(const Launch& L, const JvpArgs& a) {
   const size_t scratch_bytes = (size_t)blocks * kGenBlock * gen_scratch_per_thread<Op, T, C::kReg, C::kSmem>() * sizeof(T);
   T* scratch = nullptr;
   if (scratch_bytes) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_bytes, s);
-    if (e != cudaSuccess) return (int)e;
+    if (int rc = scratch_alloc(reinterpret_cast<void**>(&scratch), scratch_bytes, s)) return rc;
   }
   kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, a, L.ld_in, L.ld_out, scratch);
   cudaError_t e = cudaGetLastError();
-  if (scratch) cudaFreeAsync(scratch, s);
+  scratch_free(scratch, s);
   return (int)e;
 }
 

@@ -2,10 +2,19 @@
 // kernels (vd_kernels.cu).  Not part of the public boundary.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 namespace vdk {
 
+
+// Stream-ordered scratch from a private per-device pool (vd_dispatch.cu).
+// The pool keeps up to kScratchKeepBytes cached across synchronisations so a
+// per-launch slab is not a real allocation every time; it never touches the
+// device's default pool, whose release policy belongs to the application.
+constexpr uint64_t kScratchKeepBytes = 512ull << 20;
+int scratch_alloc(void** p, size_t bytes, void* stream);
+void scratch_free(void* p, void* stream);
 
 // Which compile-time robot a device model matched (0 = generic kernels).
 enum Spec : int { kGeneric = 0, kChain7 = 1, kTree29 = 2, kHumanoid23 = 3 };

@@ -3,10 +3,36 @@
 #pragma once
 
 #include <algorithm>
+#include <mutex>
 
 #include "vd_kernels.cuh"
 
 namespace vdk {
+
+// Persistent-grid size of one kernel, cached per device.  host_batch drives
+// several devices from concurrent threads, so the cache is mutex-protected
+// and keyed by the calling thread's current device.
+struct TiledOcc {
+  int blocks_per_sm = 0, sms = 0;
+};
+
+template <class K>
+TiledOcc tiled_occupancy(K kern) {
+  static std::mutex mu;
+  static TiledOcc occ[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  TiledOcc& c = occ[dev & 63];
+  if (!c.blocks_per_sm) {
+    int sms = 0, bps = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kBlock, 0);
+    c.sms = sms;
+    c.blocks_per_sm = bps < 1 ? 1 : bps;
+  }
+  return c;
+}
 
 // Launch the staged persistent kernel when the view is compile-time and the
 // two shared-memory stages fit the 48 KB static limit; returns -1 when not
@@ -27,16 +53,9 @@ int try_tiled(const V& mv, const Launch& L, const Op& op, const void* a, const v
       const void* ptrs[3] = {a, b, c};
       bool aligned = (L.ld_in * (int64_t)sizeof(T)) % 16 == 0;
       for (int g = 0; g < Op::kGroups; ++g) aligned = aligned && ptrs[g] && ((uintptr_t)ptrs[g] % 16 == 0);
-      static int blocks_per_sm = 0, sms = 0;
-      if (!blocks_per_sm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_tiled<V, Op>, kBlock, 0);
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-      }
+      const TiledOcc o = tiled_occupancy(k_tiled<V, Op>);
       const int64_t tiles = (L.N + kBlock - 1) / kBlock;
-      const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * blocks_per_sm);
+      const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)o.sms * o.blocks_per_sm);
       tma::Inputs<T> in{{(const T*)a, (const T*)b, (const T*)c}, Op::kGroups};
       k_tiled<V, Op><<<grid, kBlock, 0, stream_of(L)>>>(mv, op, L.N, in, L.ld_in, aligned);
       return (int)cudaGetLastError();

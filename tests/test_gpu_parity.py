@@ -169,6 +169,34 @@ def test_crba_packed(vd, cuda, omodels, name, generic, dtype):
     assert lib.vd_crba_packed(dm.handle, 0, 0, qs.data_ptr(), 0, out.data_ptr(), 0, None) == 0
 
 
+def test_crba_packed_gather_chunks(vd, cuda, omodels):
+    """Models without a generated packed routine build dense M in bounded
+    pool scratch chunk by chunk (~256 MB of dense planes per chunk) and gather;
+    a batch spanning several chunks, written with ld_out > N, equals the dense
+    vd_crba output at the packed positions bitwise."""
+    m, dm = _dm(vd, "tree29", generic=True)
+    rows, cols = m.crba_pattern()
+    N, nnz = 90001, len(rows)  # 3 chunks of 39808 states for 29 dof (fp64)
+    q = (torch.rand((N, m.dof()), dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(7))
+         * 2 - 1) * np.pi
+    dense = vd.crba(dm, q)
+    out = torch.full((nnz, N + 5), -1.0, dtype=torch.float64, device="cuda")
+    qs = q.t().contiguous()
+    lib = vd._lib.load()
+    assert lib.vd_crba_packed(dm.handle, 0, N, qs.data_ptr(), N, out.data_ptr(), N + 5, None) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(out[:, :N].t(), dense[:, rows, cols])
+    assert torch.all(out[:, N:] == -1.0)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_inputs_on_another_device_rejected(vd, cuda):
+    m, dm = _dm(vd, "chain7")
+    q = torch.zeros((4, 7), dtype=torch.float64, device="cuda:1")
+    with pytest.raises(vd.CudaError):
+        vd.rnea(dm, q, q, q)
+
+
 # ---------------------------------------------------------------- forward dynamics (ABA vs LLT oracle)
 def _fd_check(om, q, qd, tau, got, tol, name):
     ref, st = om.forward_dynamics(q, qd, tau)
