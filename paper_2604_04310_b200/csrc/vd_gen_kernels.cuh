@@ -69,7 +69,10 @@ struct GenMem<float> {
 // (.cs) cache operator, so the streamed batch does not push the per-thread
 // scratch slab out of L2 (gen_sweep: G1 ABA fp64 0.31-0.42 -> 0.29 ms, dense
 // CRBA 1.1-1.8x; it slows the OSC routines, which keep the default).
-template <class T, int kSlots, int kReg, int kSmem, bool kFast = false, bool kStream = false>
+// kSyncEvery > 0: a CTA barrier at every kSyncEvery-th phase point of the
+// generated routine (one per joint step), so the CTA's warps walk the
+// straight-line code together and share its instruction-cache lines.
+template <class T, int kSlots, int kReg, int kSmem, bool kFast = false, bool kStream = false, int kSyncEvery = 0>
 struct GenCx {
   static constexpr bool kFastTrig = kFast;  // fp64 sin/cos by vd_sincos_f64
   static constexpr int kGlobal = kSlots - kReg - kSmem > 0 ? kSlots - kReg - kSmem : 0;
@@ -87,6 +90,14 @@ struct GenCx {
   }
   __device__ __forceinline__ void prefetch(int g, int j) const {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(in_[g] + j * ld));
+  }
+  // every read of input group g for this state is done (GenAsyncCx overrides)
+  __device__ __forceinline__ void fetch_next(int) const {}
+  template <int K>
+  __device__ __forceinline__ void phase() const {
+    if constexpr (kSyncEvery > 0) {
+      if constexpr (K % kSyncEvery == 0) __syncthreads();
+    }
   }
   __device__ __forceinline__ T g(int k) const { return g3[k]; }
   __device__ __forceinline__ void st(int k, T v) {
@@ -130,12 +141,13 @@ constexpr int64_t gen_scratch_per_thread() {
 
 // One generated routine (Op = GenRobot::Aba / Rnea / RneaBias / RneaGrav /
 // Crba / Fk) over a persistent grid: every thread strides over the batch.
-template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false, bool kStream = false>
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false, bool kStream = false,
+          int kSyncEvery = 0>
 __global__ void __launch_bounds__(kGenBlock, kMinB)
     k_gen(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
           T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status, T* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
-  using Cx = GenCx<T, Op::kSlots, kReg, kSmem, kFast, kStream>;
+  using Cx = GenCx<T, Op::kSlots, kReg, kSmem, kFast, kStream, kSyncEvery>;
   Cx cx;
   const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * kGenBlock;
@@ -167,6 +179,105 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
       if (status) status[i] = ok ? 0 : 7;
     }
   }
+}
+
+// Asynchronous state input.  The inputs of the state a thread processes next
+// are copied global -> shared memory with per-thread cp.async (no CTA barrier:
+// each thread reads only the elements it copied) while it computes the current
+// state.  A generated routine calls fetch_next(g) once its reads of group g are
+// done, so the copy of the next state's group g overlaps the rest of the
+// routine: the next state starts with q and q̇ on chip, and the ABA's τ (read
+// in pass 2, released before pass 3) is never waited for.  ncu of the plain
+// kernel (chain7 ABA fp64): 30 % of the warp-stall samples were long-scoreboard
+// waits on exactly these loads (profiles/README.md).
+// Shared memory per thread: kSmem slots, then kIn × kDof input elements
+// ([k][thread] layout, conflict-free).
+// kStream: the copies carry an L2 evict-first policy (as GenCx's .cs loads).
+template <bool kStream, class T>
+__device__ __forceinline__ void vd_cp_async(uint32_t dst, const T* src, uint64_t pol) {
+  if constexpr (kStream)
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], %2, %3;" ::"r"(dst), "l"(src), "n"(sizeof(T)),
+                 "l"(pol)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(src), "n"(sizeof(T)) : "memory");
+}
+
+template <class T, int kSlots, int kReg, int kSmem, bool kFast, bool kStream, int kDof, int kSyncEvery = 0>
+struct GenAsyncCx : GenCx<T, kSlots, kReg, kSmem, kFast, kStream, kSyncEvery> {
+  uint32_t ib;     // shared address of this thread's input element (0, 0)
+  const T* nx[3];  // &x_g[next state]
+  uint64_t pol;    // L2 evict-first policy (kStream)
+  static __device__ __forceinline__ uint32_t off(int g, int j) {
+    return (uint32_t)((g * kDof + j) * kGenBlock * (int)sizeof(T));
+  }
+  __device__ __forceinline__ T x(int g, int j) const { return GenMem<T>::lds(ib + off(g, j)); }
+  __device__ __forceinline__ void fetch_next(int g) const { fetch(ib, nx[g], this->ld, g, pol); }
+  static __device__ __forceinline__ void fetch(uint32_t ib, const T* src, int64_t ld, int g, uint64_t pol) {
+#pragma unroll
+    for (int j = 0; j < kDof; ++j) vd_cp_async<kStream>(ib + off(g, j), src + j * ld, pol);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+};
+
+template <class Op, class T, int kReg, int kSmem>
+constexpr size_t gen_async_smem() {
+  return (size_t)(kSmem + Op::kIn * Op::kDof) * kGenBlock * sizeof(T);
+}
+
+// k_gen with asynchronous state input (same arguments, same results).
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false, bool kStream = false,
+          int kSyncEvery = 0>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen_async(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
+                T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status,
+                T* __restrict__ scratch) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenAsyncCx<T, Op::kSlots, kReg, kSmem, kFast, kStream, Op::kDof, kSyncEvery>;
+  Cx cx;
+  cx.pol = 0;
+  if constexpr (kStream) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(cx.pol));
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  cx.sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  cx.sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  cx.ib = cx.sm + (uint32_t)(kSmem * kGenBlock * sizeof(T));
+  cx.g3[0] = g0;
+  cx.g3[1] = g1;
+  cx.g3[2] = g2;
+  const T* xs[3] = {x0, Op::kIn > 1 ? x1 : x0, Op::kIn > 2 ? x2 : x0};
+  // the first state's inputs (padding lanes of the last round read state N-1)
+  {
+    const int64_t i = slot < N ? slot : N - 1;
+#pragma unroll
+    for (int g = 0; g < Op::kIn; ++g) Cx::fetch(cx.ib, xs[g] + i, ldi, g, cx.pol);
+  }
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    cx.active = i0 < N;
+    const int64_t i = cx.active ? i0 : N - 1;
+    const int64_t inext = i0 + stride < N ? i0 + stride : N - 1;
+    int64_t ld, lo;
+    asm volatile("mov.b64 %0, %1;" : "=l"(ld) : "l"(ldi));
+    asm volatile("mov.b64 %0, %1;" : "=l"(lo) : "l"(ldo));
+    cx.ld = ld;
+    cx.ldo = lo;
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {
+      cx.in_[g] = xs[g] + i;
+      cx.nx[g] = xs[g] + inext;
+    }
+    cx.out_ = y + i;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    const bool ok = Op::template run<T>(cx);
+    if (cx.active) {
+      if (!ok) {
+        for (int j = 0; j < Op::kOut; ++j) y[(int64_t)j * ldo + i] = T(0);
+      }
+      if (status) status[i] = ok ? 0 : 7;
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");  // no copy outlives the CTA
 }
 
 // osc_step context: task parameters (OscShared, kernel parameter space) and

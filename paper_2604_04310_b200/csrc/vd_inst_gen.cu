@@ -29,10 +29,27 @@ template <class C, class = void>
 struct StreamIo : std::false_type {};
 template <class C>
 struct StreamIo<C, std::void_t<decltype(C::kStream)>> : std::bool_constant<C::kStream> {};
+// kAsync (k_gen_async): the next state's inputs are prefetched into shared
+// memory with cp.async while the current one is computed; false unless a Cfg
+// sets it
+template <class C, class = void>
+struct AsyncIo : std::false_type {};
+template <class C>
+struct AsyncIo<C, std::void_t<decltype(C::kAsync)>> : std::bool_constant<C::kAsync> {};
+// The headline kernel, N = 4M states (tools/async_sweep.cu, one B200):
+// plain k_gen r44 s28 b4 0.599 ms; async r30 s35 b4 0.555, + evict-first
+// 0.548, r24 s41 (3 CTAs/SM) 0.543 ms; the templated TMA kernel 0.61 ms.
 template <>
-struct Cfg<GenChain7::Aba, double> {  // the headline kernel: 0.60 ms / 4M states vs 0.61 templated
-  static constexpr int kReg = 44, kSmem = 28, kMinB = 4;
-  static constexpr bool kFast = true;
+struct Cfg<GenChain7::Aba, double> {
+  static constexpr int kReg = 24, kSmem = 41, kMinB = 3;
+  static constexpr bool kFast = true, kStream = true, kAsync = true;
+};
+// chain7 fp32 ABA: generated + async r40 s25 (6 CTAs/SM) 0.299 ms at 4M
+// states vs 0.41 ms for the templated TMA kernel
+template <>
+struct Cfg<GenChain7::Aba, float> {
+  static constexpr int kReg = 40, kSmem = 25, kMinB = 6;
+  static constexpr bool kFast = false, kAsync = true;
 };
 // chain7 RNEA family: all slots in registers, fast fp64 sincos (gen_sweep:
 // fp64 0.252 vs 0.261 ms templated, fp32 0.142 vs 0.153 ms at 4M states)
@@ -134,12 +151,22 @@ Occ occupancy(Kern kern, size_t smem) {
   return c;
 }
 
+// The kernel a Cfg selects (only that one is instantiated).
+template <class Op, class T, class C>
+constexpr auto gen_kernel() {
+  if constexpr (AsyncIo<C>::value)
+    return k_gen_async<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
+  else
+    return k_gen<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
+}
+
 template <class Op, class T>
 int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
              int32_t* status) {
   using C = Cfg<Op, T>;
-  auto kern = k_gen<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
-  constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
+  constexpr bool kAsync = AsyncIo<C>::value;
+  auto kern = gen_kernel<Op, T, C>();
+  constexpr size_t smem = kAsync ? gen_async_smem<Op, T, C::kReg, C::kSmem>() : (size_t)C::kSmem * kGenBlock * sizeof(T);
   const Occ o = occupancy<Op, T>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
   cudaStream_t s = static_cast<cudaStream_t>(L.stream);
@@ -255,8 +282,9 @@ int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, c
 
 int launch_gen_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* qdd,
                    int32_t* status) {
-  if (L.spec == kChain7)  // fp64 only; fp32 stays on the TMA-staged template kernel
-    return L.dtype == 0 ? launch_t<GenChain7::Aba, double>(L, q, qd, tau, g3, qdd, status) : -1;
+  if (L.spec == kChain7)
+    return L.dtype == 0 ? launch_t<GenChain7::Aba, double>(L, q, qd, tau, g3, qdd, status)
+                        : launch_t<GenChain7::Aba, float>(L, q, qd, tau, g3, qdd, status);
   if (L.spec != kTree29) return -1;
   // fp32: the mixed-precision routine (floating-base trunk in fp64)
   return L.dtype == 0 ? launch_t<GenTree29::Aba, double>(L, q, qd, tau, g3, qdd, status)

@@ -23,6 +23,9 @@ struct HostCx {
   T x(int g, int j) const { return X[g] ? X[g][j * ld + i] : T(0); }
   T dx(int g, int j) const { return DX[g] ? DX[g][j * ld + i] : T(0); }
   void prefetch(int, int) const {}
+  void fetch_next(int) const {}
+  template <int K>
+  void phase() const {}
   T g(int k) const { return T(G[k]); }
   void st(int k, T v) { slots[k] = v; }
   T get(int k) const { return slots[k]; }

@@ -1,0 +1,156 @@
+// A/B of k_gen (plain state loads) against k_gen_async (cp.async prefetch of
+// the next state's inputs) for the generated ABA routines, on one GPU.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr
+//        -Ipaper_2604_04310_b200/csrc tools/async_sweep.cu -o ablib/async_sweep
+// Prints time per launch and the max |difference| of each variant's output
+// against the plain kernel's (the same generated arithmetic: expected 0).
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <vector>
+#include "vd_gen_kernels.cuh"
+using namespace vdk;
+
+template <class T>
+__global__ void k_fill(T* p, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t x = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 31;
+    p[i] = T((double)(x >> 11) * (1.0 / 9007199254740992.0) * 6.283185307179586 - 3.141592653589793);
+  }
+}
+
+static std::vector<double> g_ref;
+
+template <class T, class K>
+void time_kernel(const char* name, K kern, size_t smem, size_t scratch_per_thread, int64_t N, int n, int nout, T* x,
+                 T* y, int32_t* st, T* scratch, size_t cap, bool is_ref) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int bps = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (bps < 1) { printf("%-40s does not fit\n", name); return; }
+  const int64_t grid = std::min<int64_t>((int64_t)sms * bps, (N + kGenBlock - 1) / kGenBlock);
+  if ((size_t)grid * kGenBlock * scratch_per_thread * sizeof(T) > cap) { printf("%s scratch\n", name); return; }
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, kern);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const T *x0 = x, *x1 = x + N * n, *x2 = x + 2 * N * n;
+  cudaMemset(y, 0, sizeof(T) * N * nout);
+  for (int w = 0; w < 3; ++w) kern<<<grid, kGenBlock, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch);
+  cudaEventRecord(a);
+  const int reps = 20;
+  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  ms /= reps;
+  std::vector<T> h((size_t)N * nout);
+  cudaMemcpy(h.data(), y, sizeof(T) * h.size(), cudaMemcpyDeviceToHost);
+  double md = 0;
+  if (is_ref) {
+    g_ref.assign(h.begin(), h.end());
+  } else {
+    for (size_t k = 0; k < h.size(); ++k) md = std::max(md, std::fabs((double)h[k] - g_ref[k]) / std::max(1.0, std::fabs(g_ref[k])));
+  }
+  printf("%-40s regs %3d lmem %4zu smem %6zu b/SM %d  %.4f ms  %.3e evals/s  maxdiff %.2e  %s\n", name, fa.numRegs,
+         fa.localSizeBytes, smem, bps, ms, N / (ms * 1e-3), md, cudaGetErrorString(cudaGetLastError()));
+}
+
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast, bool kStream, int kSync = 0>
+void plain(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, bool ref = false) {
+  time_kernel<T>(name, k_gen<Op, T, kReg, kSmem, kMinB, kFast, kStream, kSync>, (size_t)kSmem * kGenBlock * sizeof(T),
+                 gen_scratch_per_thread<Op, T, kReg, kSmem>(), N, Op::kDof, Op::kOut, x, y, st, scratch, cap, ref);
+}
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast, bool kStream = false, int kSync = 0>
+void async(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, bool ref = false) {
+  time_kernel<T>(name, k_gen_async<Op, T, kReg, kSmem, kMinB, kFast, kStream, kSync>, gen_async_smem<Op, T, kReg, kSmem>(),
+                 gen_scratch_per_thread<Op, T, kReg, kSmem>(), N, Op::kDof, Op::kOut, x, y, st, scratch, cap, ref);
+}
+
+#define ON(k) (!strcmp(which, "all") || !strcmp(which, k))
+int main(int argc, char** argv) {
+  const char* which = argc > 1 ? argv[1] : "all";
+  const size_t cap = 1ull << 30;
+  double *x, *y, *scratch;
+  int32_t* st;
+  const int64_t Nmax = 4194304;
+  cudaMalloc(&x, sizeof(double) * Nmax * 7 * 3);
+  cudaMalloc(&y, sizeof(double) * 262144 * 841);
+  cudaMalloc(&scratch, cap);
+  cudaMalloc(&st, sizeof(int32_t) * Nmax);
+  float* xf = (float*)x;
+  float* yf = (float*)y;
+  float* sf = (float*)scratch;
+  const int64_t N7 = 4194304, N29 = 262144;
+  if (ON("c7")) {
+    k_fill<<<1184, 256>>>(x, N7 * 21, 1);
+    plain<GenChain7::Aba, double, 44, 28, 4, true, false>("c7 aba f64 plain r44 s28 b4", N7, x, y, st, scratch, cap, true);
+    async<GenChain7::Aba, double, 30, 35, 4, true>("c7 aba f64 async r30 s35 b4", N7, x, y, st, scratch, cap);
+    async<GenChain7::Aba, double, 24, 41, 4, true>("c7 aba f64 async r24 s41 b4", N7, x, y, st, scratch, cap);
+    async<GenChain7::Aba, double, 36, 29, 4, true>("c7 aba f64 async r36 s29 b4", N7, x, y, st, scratch, cap);
+    async<GenChain7::Aba, double, 16, 49, 4, true>("c7 aba f64 async r16 s49 b4", N7, x, y, st, scratch, cap);
+    async<GenChain7::Aba, double, 30, 35, 4, true, true>("c7 aba f64 async r30 s35 b4 cs", N7, x, y, st, scratch, cap);
+  }
+  if (ON("sync")) {
+    k_fill<<<1184, 256>>>(x, N7 * 21, 1);
+    async<GenChain7::Aba, double, 24, 41, 3, true, true>("c7 aba f64 async r24 s41 cs", N7, x, y, st, scratch, cap, true);
+    async<GenChain7::Aba, double, 24, 41, 3, true, true, 1>("c7 aba f64 async r24 s41 cs sync1", N7, x, y, st, scratch, cap);
+    async<GenChain7::Aba, double, 24, 41, 3, true, true, 3>("c7 aba f64 async r24 s41 cs sync3", N7, x, y, st, scratch, cap);
+    async<GenChain7::Aba, double, 24, 41, 3, true, true, 7>("c7 aba f64 async r24 s41 cs sync7", N7, x, y, st, scratch, cap);
+    k_fill<<<1184, 256>>>(x, N29 * 87, 2);
+    plain<GenTree29::Aba, double, 40, 113, 2, false, true>("t29 aba f64 plain", N29, x, y, st, scratch, cap, true);
+    plain<GenTree29::Aba, double, 40, 113, 2, false, true, 1>("t29 aba f64 plain sync1", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Aba, double, 40, 113, 2, false, true, 2>("t29 aba f64 plain sync2", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Aba, double, 40, 113, 2, false, true, 4>("t29 aba f64 plain sync4", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Aba, double, 40, 113, 2, false, true, 8>("t29 aba f64 plain sync8", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Aba, double, 40, 60, 3, false, true, 2>("t29 aba f64 r40 s60 b3 sync2", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Rnea, double, 58, 55, 2, false, false>("t29 rnea f64 plain", N29, x, y, st, scratch, cap, true);
+    plain<GenTree29::Rnea, double, 58, 55, 2, false, false, 2>("t29 rnea f64 plain sync2", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Rnea, double, 58, 55, 2, false, false, 4>("t29 rnea f64 plain sync4", N29, x, y, st, scratch, cap);
+  }
+  if (ON("c7f")) {
+    k_fill<<<1184, 256>>>(xf, N7 * 21, 1);
+    async<GenChain7::Aba, float, 20, 45, 4, false>("c7 aba f32 async r20 s45 b4", N7, xf, yf, st, sf, cap, true);
+    async<GenChain7::Aba, float, 30, 35, 5, false>("c7 aba f32 async r30 s35 b5", N7, xf, yf, st, sf, cap);
+    async<GenChain7::Aba, float, 40, 25, 6, false>("c7 aba f32 async r40 s25 b6", N7, xf, yf, st, sf, cap);
+    async<GenChain7::Aba, float, 65, 0, 6, false>("c7 aba f32 async r65 s0 b6", N7, xf, yf, st, sf, cap);
+    async<GenChain7::AbaMixed, float, 20, 52, 4, false>("c7 abamixed f32 async r20 s52 b4", N7, xf, yf, st, sf, cap);
+  }
+  if (ON("c7r")) {
+    k_fill<<<1184, 256>>>(x, N7 * 21, 1);
+    constexpr int S = GenChain7::Rnea::kSlots;
+    plain<GenChain7::Rnea, double, S, 0, 4, true, false>("c7 rnea f64 plain", N7, x, y, st, scratch, cap, true);
+    async<GenChain7::Rnea, double, S, 0, 4, true>("c7 rnea f64 async rall b4", N7, x, y, st, scratch, cap);
+    async<GenChain7::Rnea, double, 0, S, 4, true>("c7 rnea f64 async sall b4", N7, x, y, st, scratch, cap);
+    async<GenChain7::Rnea, double, S - 14, 14, 4, true>("c7 rnea f64 async r-14 s14 b4", N7, x, y, st, scratch, cap);
+    k_fill<<<1184, 256>>>(xf, N7 * 21, 1);
+    plain<GenChain7::Rnea, float, S, 0, 6, true, false>("c7 rnea f32 plain", N7, xf, yf, st, sf, cap, true);
+    async<GenChain7::Rnea, float, S, 0, 6, true>("c7 rnea f32 async rall b6", N7, xf, yf, st, sf, cap);
+    async<GenChain7::Rnea, float, 0, S, 6, true>("c7 rnea f32 async sall b6", N7, xf, yf, st, sf, cap);
+  }
+  if (ON("c7c")) {
+    k_fill<<<1184, 256>>>(x, N7 * 21, 1);
+    constexpr int S = GenChain7::Crba::kSlots;
+    plain<GenChain7::Crba, double, S, 0, 4, true, false>("c7 crba f64 plain rall b4", N7, x, y, st, scratch, cap, true);
+    plain<GenChain7::Crba, double, S, 0, 4, true, true>("c7 crba f64 plain rall b4 cs", N7, x, y, st, scratch, cap);
+    async<GenChain7::Crba, double, S, 0, 4, true>("c7 crba f64 async rall b4", N7, x, y, st, scratch, cap);
+    async<GenChain7::Crba, double, S, 0, 4, true, true>("c7 crba f64 async rall b4 cs", N7, x, y, st, scratch, cap);
+    async<GenChain7::Crba, double, S, 0, 6, true, true>("c7 crba f64 async rall b6 cs", N7, x, y, st, scratch, cap);
+  }
+  if (ON("t29")) {
+    k_fill<<<1184, 256>>>(x, N29 * 87, 2);
+    plain<GenTree29::Aba, double, 40, 113, 2, false, true>("t29 aba f64 plain r40 s113 b2 cs", N29, x, y, st, scratch, cap, true);
+    plain<GenTree29::Rnea, double, 58, 55, 2, false, false>("t29 rnea f64 plain r58 s55 b2", N29, x, y, st, scratch, cap, true);
+    async<GenTree29::Rnea, double, 58, 20, 2, false>("t29 rnea f64 async r58 s20 b2", N29, x, y, st, scratch, cap);
+    async<GenTree29::Rnea, double, 58, 20, 2, false, true>("t29 rnea f64 async r58 s20 b2 cs", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Crba, double, 0, 55, 3, false, true>("t29 crba f64 plain s55 b3 cs", N29, x, y, st, scratch, cap, true);
+    async<GenTree29::Crba, double, 0, 44, 3, false, true>("t29 crba f64 async s44 b3 cs", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Fk, double, 0, GenTree29::Fk::kSlots < 55 ? GenTree29::Fk::kSlots : 55, 3, false, false>("t29 fk f64 plain", N29, x, y, st, scratch, cap, true);
+    async<GenTree29::Fk, double, 0, GenTree29::Fk::kSlots < 40 ? GenTree29::Fk::kSlots : 40, 3, false, true>("t29 fk f64 async cs", N29, x, y, st, scratch, cap);
+  }
+  return 0;
+}

@@ -82,6 +82,7 @@ class Gen:
         # scalar type of emitted temporaries: "T" (the kernel's dtype) or "TD"
         # (double) for the high-precision joints of a mixed-precision routine
         self.ty = "T"
+        self.groups_read = set()  # input groups read through cx.x (see Algo.release)
 
     # ---------------------------------------------------------------- emission
     def lit(self, c):
@@ -112,6 +113,7 @@ class Gen:
 
     # ---------------------------------------------------------------- hooks (overridden by DGen for JVPs)
     def input(self, gi, i):
+        self.groups_read.add(gi)
         return self.tmp(f"cx.x({gi}, {i})", "x", ty="T")
 
     def sincos(self, q, i):
@@ -353,6 +355,7 @@ class DGen(Gen):
         return Gen.o(self, a.v if isinstance(a, DualEx) else a)
 
     def input(self, gi, i):
+        self.groups_read.add(gi)
         return DualEx(self.tmp(f"cx.x({gi}, {i})", "x", ty="T"), self.tmp(f"cx.dx({gi}, {i})", "dx", ty="T"))
 
     def sincos(self, q, i):
@@ -543,6 +546,19 @@ class Algo:
         for key, v in xv.items():
             self.xrefs[key] = self.store(v)
         self.nprologue = self.nslot
+        self.released = set()
+        self.nphase = 0
+        for gi in sorted(g.groups_read):
+            self.release(gi)
+
+    def release(self, gi):
+        """Every read of input group gi has been emitted: cx.fetch_next(gi)
+        lets an asynchronous context start copying the next state's group gi
+        into the buffer these reads came from (a no-op for the others).
+        Emitted once per group; finish() releases whatever is left."""
+        if gi in self.g.groups_read and gi not in self.released:
+            self.released.add(gi)
+            self.g.raw(f"cx.fetch_next({gi});")
 
     def store(self, v):
         if isinstance(v, DualEx):  # value and tangent in their own slots
@@ -568,6 +584,10 @@ class Algo:
         return self.g.tmp(f"cx.get({ref[1]})", "r", ty="T")
 
     def joint(self, i):
+        # a numbered phase point at every joint step: a kernel may barrier its
+        # warps here so they walk the straight-line code together (I-cache reuse)
+        self.g.raw(f"cx.template phase<{self.nphase}>();")
+        self.nphase += 1
         m = self.mrefs[i]
         if m[0] == "q":
             return Joint(self.g, self.rb, i, q=self.load(m[1]))
@@ -578,6 +598,8 @@ class Algo:
         return [ZERO, ZERO, ZERO, Ex(s="ga0"), Ex(s="ga1"), Ex(s="ga2")]
 
     def finish(self):
+        for gi in sorted(self.g.groups_read):
+            self.release(gi)
         self.g.raw("return ok;")
         return self
 
@@ -645,6 +667,7 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False):
 
     for r in rb.roots:
         down_up(r, None)
+    A.release(2)  # τ is read only in pass 2
     ty(rb.roots[0])
     gvec = A.gravity()
 
@@ -1260,6 +1283,7 @@ def emit_body(name, cls, rb):
         out += [f"  // {op}: {A.g.flops} mul/add after folding; {A.nslot} slots, the first {A.nprologue} written by the prologue",
                 f"  struct {op} {{",
                 f"    static constexpr int kSlots = {A.nslot};",
+                f"    static constexpr int kDof = {rb.n};",
                 f"    static constexpr int kPrologue = {A.nprologue};",
                 f"    static constexpr int kFlops = {A.g.flops};",
                 f"    static constexpr int kIn = {nin};",
@@ -1277,6 +1301,7 @@ def emit_body(name, cls, rb):
         out += [f"  // Osc on joint {fj}: {A.g.flops} mul/add after folding; {A.nslot} slots",
                 f"  struct Osc{fj} {{",
                 f"    static constexpr int kSlots = {A.nslot};",
+                f"    static constexpr int kDof = {rb.n};",
                 f"    static constexpr int kPrologue = {A.nprologue};",
                 f"    static constexpr int kFlops = {A.g.flops};",
                 "    static constexpr int kIn = 2;",
@@ -1291,6 +1316,7 @@ def emit_body(name, cls, rb):
             out += [f"  // {nm} on joint {fj}: {A.g.flops} mul/add after folding; {A.nslot} slots",
                     f"  struct {nm}{fj} {{",
                     f"    static constexpr int kSlots = {A.nslot};",
+                    f"    static constexpr int kDof = {rb.n};",
                     f"    static constexpr int kPrologue = {A.nprologue};",
                     f"    static constexpr int kFlops = {A.g.flops};",
                     "    static constexpr int kIn = 1;",
