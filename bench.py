@@ -354,14 +354,16 @@ def run_ours(args):
     # DRAM traffic per launch of this kernel at this N from the committed
     # `ncu --set full` capture (tools/capture_profiles.sh; ncu cannot run
     # inside the timed bench)
-    prof = os.path.join(ROOT, "profiles", "r01_chain7_aba_f64.json")
-    if os.path.exists(prof):
+    prof = next((os.path.join(ROOT, "profiles", f"{r}_chain7_aba_f64.json") for r in ("r02", "r01")
+                 if os.path.exists(os.path.join(ROOT, "profiles", f"{r}_chain7_aba_f64.json"))), "")
+    if prof:
         with open(prof) as f:
             pj = json.load(f)
         if int(pj.get("states_per_launch", 0)) == N:
             roofline["traffic"] = pj["dram_bytes_per_launch"]
             roofline["traffic_over_algorithmic"] = pj["traffic_over_algorithmic"]
-            roofline["traffic_source"] = "profiles/r01_chain7_aba_f64.json (ncu --set full, dram__bytes_read+write)"
+            roofline["traffic_source"] = (f"profiles/{os.path.basename(prof)} (ncu --set full, "
+                                          "dram__bytes_read+write)")
 
     # ---------------- e2e through the public host API (pinned buffers)
     e2e = None

@@ -72,7 +72,8 @@ struct GenMem<float> {
 // kSyncEvery > 0: a CTA barrier at every kSyncEvery-th phase point of the
 // generated routine (one per joint step), so the CTA's warps walk the
 // straight-line code together and share its instruction-cache lines.
-template <class T, int kSlots, int kReg, int kSmem, bool kFast = false, bool kStream = false, int kSyncEvery = 0>
+template <class T, int kSlots, int kReg, int kSmem, bool kFast = false, bool kStream = false, int kSyncEvery = 0,
+          int kBlk = kGenBlock>
 struct GenCx {
   static constexpr bool kFastTrig = kFast;  // fp64 sin/cos by vd_sincos_f64
   static constexpr int kGlobal = kSlots - kReg - kSmem > 0 ? kSlots - kReg - kSmem : 0;
@@ -102,12 +103,12 @@ struct GenCx {
   __device__ __forceinline__ T g(int k) const { return g3[k]; }
   __device__ __forceinline__ void st(int k, T v) {
     if (k >= kSlots - kReg) reg[k - (kSlots - kReg)] = v;
-    else if (k < kSmem) GenMem<T>::sts(sm + (uint32_t)(k * kGenBlock * sizeof(T)), v);
+    else if (k < kSmem) GenMem<T>::sts(sm + (uint32_t)(k * kBlk * sizeof(T)), v);
     else GenMem<T>::stg(sb + (k - kSmem) * 32, v);
   }
   __device__ __forceinline__ T get(int k) const {
     if (k >= kSlots - kReg) return reg[k - (kSlots - kReg)];
-    if (k < kSmem) return GenMem<T>::lds(sm + (uint32_t)(k * kGenBlock * sizeof(T)));
+    if (k < kSmem) return GenMem<T>::lds(sm + (uint32_t)(k * kBlk * sizeof(T)));
     return GenMem<T>::ldgs(sb + (k - kSmem) * 32);
   }
   // a double in slots k, k + 1 (mixed-precision joints of the fp32 routines;
@@ -142,21 +143,21 @@ constexpr int64_t gen_scratch_per_thread() {
 // One generated routine (Op = GenRobot::Aba / Rnea / RneaBias / RneaGrav /
 // Crba / Fk) over a persistent grid: every thread strides over the batch.
 template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false, bool kStream = false,
-          int kSyncEvery = 0>
-__global__ void __launch_bounds__(kGenBlock, kMinB)
+          int kSyncEvery = 0, int kBlk = kGenBlock>
+__global__ void __launch_bounds__(kBlk, kMinB)
     k_gen(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
           T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status, T* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
-  using Cx = GenCx<T, Op::kSlots, kReg, kSmem, kFast, kStream, kSyncEvery>;
+  using Cx = GenCx<T, Op::kSlots, kReg, kSmem, kFast, kStream, kSyncEvery, kBlk>;
   Cx cx;
-  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  const int64_t slot = (int64_t)blockIdx.x * kBlk + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kBlk;
   cx.sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
   cx.sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
   cx.g3[0] = g0;
   cx.g3[1] = g1;
   cx.g3[2] = g2;
-  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride) {
+  for (int64_t base = (int64_t)blockIdx.x * kBlk; base < N; base += stride) {
     const int64_t i0 = base + threadIdx.x;
     cx.active = i0 < N;
     const int64_t i = cx.active ? i0 : N - 1;

@@ -24,14 +24,14 @@ static std::vector<double> g_ref;
 
 template <class T, class K>
 void time_kernel(const char* name, K kern, size_t smem, size_t scratch_per_thread, int64_t N, int n, int nout, T* x,
-                 T* y, int32_t* st, T* scratch, size_t cap, bool is_ref) {
+                 T* y, int32_t* st, T* scratch, size_t cap, bool is_ref, int blk = kGenBlock) {
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int bps = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, blk, smem);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   if (bps < 1) { printf("%-40s does not fit\n", name); return; }
-  const int64_t grid = std::min<int64_t>((int64_t)sms * bps, (N + kGenBlock - 1) / kGenBlock);
-  if ((size_t)grid * kGenBlock * scratch_per_thread * sizeof(T) > cap) { printf("%s scratch\n", name); return; }
+  const int64_t grid = std::min<int64_t>((int64_t)sms * bps, (N + blk - 1) / blk);
+  if ((size_t)grid * blk * scratch_per_thread * sizeof(T) > cap) { printf("%s scratch\n", name); return; }
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, kern);
   cudaEvent_t a, b;
@@ -39,10 +39,10 @@ void time_kernel(const char* name, K kern, size_t smem, size_t scratch_per_threa
   cudaEventCreate(&b);
   const T *x0 = x, *x1 = x + N * n, *x2 = x + 2 * N * n;
   cudaMemset(y, 0, sizeof(T) * N * nout);
-  for (int w = 0; w < 3; ++w) kern<<<grid, kGenBlock, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch);
+  for (int w = 0; w < 3; ++w) kern<<<grid, blk, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch);
   cudaEventRecord(a);
   const int reps = 20;
-  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch);
+  for (int r = 0; r < reps; ++r) kern<<<grid, blk, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms = 0;
@@ -64,6 +64,11 @@ template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast, bool kS
 void plain(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, bool ref = false) {
   time_kernel<T>(name, k_gen<Op, T, kReg, kSmem, kMinB, kFast, kStream, kSync>, (size_t)kSmem * kGenBlock * sizeof(T),
                  gen_scratch_per_thread<Op, T, kReg, kSmem>(), N, Op::kDof, Op::kOut, x, y, st, scratch, cap, ref);
+}
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast, bool kStream, int kSync, int kBlk>
+void plainb(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, bool ref = false) {
+  time_kernel<T>(name, k_gen<Op, T, kReg, kSmem, kMinB, kFast, kStream, kSync, kBlk>, (size_t)kSmem * kBlk * sizeof(T),
+                 gen_scratch_per_thread<Op, T, kReg, kSmem>(), N, Op::kDof, Op::kOut, x, y, st, scratch, cap, ref, kBlk);
 }
 template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast, bool kStream = false, int kSync = 0>
 void async(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, bool ref = false) {
@@ -111,6 +116,19 @@ int main(int argc, char** argv) {
     plain<GenTree29::Rnea, double, 58, 55, 2, false, false>("t29 rnea f64 plain", N29, x, y, st, scratch, cap, true);
     plain<GenTree29::Rnea, double, 58, 55, 2, false, false, 2>("t29 rnea f64 plain sync2", N29, x, y, st, scratch, cap);
     plain<GenTree29::Rnea, double, 58, 55, 2, false, false, 4>("t29 rnea f64 plain sync4", N29, x, y, st, scratch, cap);
+  }
+  if (ON("blk")) {
+    k_fill<<<1184, 256>>>(x, N29 * 87, 2);
+    plain<GenTree29::Aba, double, 40, 113, 2, false, true>("t29 aba f64 plain", N29, x, y, st, scratch, cap, true);
+    plainb<GenTree29::Aba, double, 40, 110, 1, false, true, 0, 256>("t29 aba blk256 s110", N29, x, y, st, scratch, cap);
+    plainb<GenTree29::Aba, double, 40, 110, 1, false, true, 1, 256>("t29 aba blk256 s110 sync1", N29, x, y, st, scratch, cap);
+    plainb<GenTree29::Aba, double, 40, 110, 1, false, true, 2, 256>("t29 aba blk256 s110 sync2", N29, x, y, st, scratch, cap);
+    plainb<GenTree29::Aba, double, 40, 110, 1, false, true, 4, 256>("t29 aba blk256 s110 sync4", N29, x, y, st, scratch, cap);
+    plainb<GenTree29::Aba, double, 40, 54, 1, false, true, 2, 512>("t29 aba blk512 s54 sync2", N29, x, y, st, scratch, cap);
+    plainb<GenTree29::Aba, double, 40, 54, 1, false, true, 0, 512>("t29 aba blk512 s54", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Rnea, double, 58, 55, 2, false, false>("t29 rnea f64 plain", N29, x, y, st, scratch, cap, true);
+    plainb<GenTree29::Rnea, double, 58, 55, 1, false, false, 2, 256>("t29 rnea blk256 sync2", N29, x, y, st, scratch, cap);
+    plainb<GenTree29::Rnea, double, 58, 55, 1, false, false, 0, 256>("t29 rnea blk256", N29, x, y, st, scratch, cap);
   }
   if (ON("c7f")) {
     k_fill<<<1184, 256>>>(xf, N7 * 21, 1);

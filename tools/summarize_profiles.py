@@ -2,7 +2,9 @@
 """Summarise ncu captures (gpurun_out/*.ncu-rep, launch-list CSVs) into
 profiles/<round>_*.{json,txt} — the evidence committed with each round.
 
-Usage: python tools/summarize_profiles.py r01
+Usage: python tools/summarize_profiles.py r01 [REPS_DIR [OUT_DIR]]
+(defaults gpurun_out/ and profiles/; on the GPU box the reports stay in /tmp
+and only the summaries travel back through gpurun_out/).
 """
 import collections
 import csv
@@ -113,14 +115,20 @@ def launches(path):
 
 
 def main():
+    global OUT, PROF
     r = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    if len(sys.argv) > 2:
+        OUT = sys.argv[2]
+    if len(sys.argv) > 3:
+        PROF = sys.argv[3]
     os.makedirs(PROF, exist_ok=True)
     sys.path.insert(0, os.path.join(ROOT))
     import bench
 
     out = {}
     # (key, kernel, states per launch, algorithmic flops / state, algorithmic bytes / state)
-    specs = [("chain7_aba_f64", "k_gen<GenChain7::Aba, double> (generated, fast fp64 sincos)", 4194304,
+    specs = [("chain7_aba_f64", "k_gen_async<GenChain7::Aba, double> (generated, cp.async state prefetch, fast fp64 "
+                                "sincos)", 4194304,
               bench.flops_per_eval("chain7", "aba"), 224),
              ("tree29_aba_f64", "k_gen<GenTree29::Aba, double> (generated)", 262144, bench.flops_per_eval("tree29", "aba"), 928),
              ("tree29_rnea_f64", "k_gen<GenTree29::Rnea, double> (generated)", 262144,
