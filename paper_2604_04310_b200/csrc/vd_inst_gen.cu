@@ -197,6 +197,13 @@ template <class Op, class T>
 struct OscCfg {
   static constexpr int kReg = 0, kSmem = sizeof(T) == 8 ? 55 : 220, kMinB = sizeof(T) == 8 ? 3 : 2;
 };
+// chain7 (Panda `ee`), N = 4M, tools/async_sweep.cu "more": every slot on
+// chip.  fp64 r80 s67 b2 1.45 ms, fp32 r60 s87 1.56 -> 0.70 ms, against the
+// templated osc_one kernel 2.35 / 1.57 ms.
+template <class T>
+struct OscCfg<GenChain7::Osc6, T> {
+  static constexpr int kReg = sizeof(T) == 8 ? 80 : 60, kSmem = sizeof(T) == 8 ? 67 : 87, kMinB = 2;
+};
 
 template <class Op, class T>
 int launch_osc_t(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lam,
@@ -312,16 +319,23 @@ int launch_gen_rnea(const Launch& L, int mode, const void* q, const void* qd, co
   return -1;
 }
 
-int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
-                   int32_t* status) {
-  if (L.spec != kTree29) return -1;
+template <class R>
+int gen_osc_t(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
+              int32_t* status) {
   int rc = -1;
-  GenTree29::with_osc(P.frame_joint, [&](auto op) {
+  R::with_osc(P.frame_joint, [&](auto op) {
     using Op = decltype(op);
     rc = L.dtype == 0 ? launch_osc_t<Op, double>(L, q, qd, P, tau, lambda, status)
                       : launch_osc_t<Op, float>(L, q, qd, P, tau, lambda, status);
   });
   return rc;
+}
+
+int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
+                   int32_t* status) {
+  if (L.spec == kTree29) return gen_osc_t<GenTree29>(L, q, qd, P, tau, lambda, status);
+  if (L.spec == kChain7) return gen_osc_t<GenChain7>(L, q, qd, P, tau, lambda, status);
+  return -1;
 }
 
 int launch_gen_jvp(const Launch& L, const JvpArgs& a) {

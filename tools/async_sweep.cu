@@ -76,6 +76,33 @@ void async(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, siz
                  gen_scratch_per_thread<Op, T, kReg, kSmem>(), N, Op::kDof, Op::kOut, x, y, st, scratch, cap, ref);
 }
 
+template <class Op, class T, int kReg, int kSmem, int kMinB>
+void osc(const char* name, int64_t N, T* x, T* y, T* lam, int32_t* st, T* scratch, size_t cap, int n, bool ref = false) {
+  auto kern = k_gen_osc<Op, T, kReg, kSmem, kMinB>;
+  const size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int bps = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t grid = std::min<int64_t>((int64_t)sms * bps, (N + kGenBlock - 1) / kGenBlock);
+  if ((size_t)(grid * kGenBlock * gen_scratch_per_thread<Op, T, kReg, kSmem>() * sizeof(T)) > cap) { printf("%s scratch\n", name); return; }
+  OscShared P{};
+  for (int k = 0; k < 9; ++k) P.frame_R[k] = P.target_R[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  P.target_p[2] = 0.3;
+  for (int k = 0; k < 6; ++k) { P.kp[k] = 100; P.kd[k] = 20; }
+  P.posture_kp = 10; P.posture_kd = 2; P.gravity[2] = 9.81; P.epsilon = 1e-6;
+  cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int w = 0; w < 2; ++w) kern<<<grid, kGenBlock, smem>>>(N, x, x + N * n, N, P, y, lam, N, st, scratch);
+  cudaEventRecord(a);
+  const int reps = 10;
+  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, x, x + N * n, N, P, y, lam, N, st, scratch);
+  cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms = 0; cudaEventElapsedTime(&ms, a, b); ms /= reps;
+  printf("%-40s regs %3d lmem %4zu smem %6zu b/SM %d  %.4f ms  %.3e evals/s  %s\n", name, fa.numRegs, fa.localSizeBytes,
+         smem, bps, ms, N / (ms * 1e-3), cudaGetErrorString(cudaGetLastError()));
+}
+
 #define ON(k) (!strcmp(which, "all") || !strcmp(which, k))
 int main(int argc, char** argv) {
   const char* which = argc > 1 ? argv[1] : "all";
@@ -129,6 +156,38 @@ int main(int argc, char** argv) {
     plain<GenTree29::Rnea, double, 58, 55, 2, false, false>("t29 rnea f64 plain", N29, x, y, st, scratch, cap, true);
     plainb<GenTree29::Rnea, double, 58, 55, 1, false, false, 2, 256>("t29 rnea blk256 sync2", N29, x, y, st, scratch, cap);
     plainb<GenTree29::Rnea, double, 58, 55, 1, false, false, 0, 256>("t29 rnea blk256", N29, x, y, st, scratch, cap);
+  }
+  if (ON("more")) {
+    k_fill<<<1184, 256>>>(x, N7 * 21, 1);
+    constexpr int S7 = GenChain7::Osc6::kSlots;
+    double* lam = nullptr;
+    cudaMalloc(&lam, sizeof(double) * 36 * N7);
+    osc<GenChain7::Osc6, double, 0, 55, 3>("c7 osc f64 s55 b3", N7, x, y, lam, st, scratch, cap, 7);
+    osc<GenChain7::Osc6, double, 60, 55, 2>("c7 osc f64 r60 s55 b2", N7, x, y, lam, st, scratch, cap, 7);
+    osc<GenChain7::Osc6, double, 0, S7 < 100 ? S7 : 100, 2>("c7 osc f64 s100 b2", N7, x, y, lam, st, scratch, cap, 7);
+    osc<GenChain7::Osc6, double, 40, 70, 2>("c7 osc f64 r40 s70 b2", N7, x, y, lam, st, scratch, cap, 7);
+    osc<GenChain7::Osc6, double, 60, 87, 2>("c7 osc f64 r60 s87 b2", N7, x, y, lam, st, scratch, cap, 7);
+    osc<GenChain7::Osc6, double, 80, 67, 2>("c7 osc f64 r80 s67 b2", N7, x, y, lam, st, scratch, cap, 7);
+    osc<GenChain7::Osc6, double, 40, 55, 2>("c7 osc f64 r40 s55 b2", N7, x, y, lam, st, scratch, cap, 7);
+    k_fill<<<1184, 256>>>(xf, N7 * 21, 1);
+    osc<GenChain7::Osc6, float, 0, 147, 3>("c7 osc f32 s147 b3", N7, xf, yf, (float*)lam, st, sf, cap, 7);
+    osc<GenChain7::Osc6, float, 60, 87, 3>("c7 osc f32 r60 s87 b3", N7, xf, yf, (float*)lam, st, sf, cap, 7);
+    osc<GenChain7::Osc6, float, 60, 87, 2>("c7 osc f32 r60 s87 b2", N7, xf, yf, (float*)lam, st, sf, cap, 7);
+    osc<GenChain7::Osc6, float, 40, 107, 4>("c7 osc f32 r40 s107 b4", N7, xf, yf, (float*)lam, st, sf, cap, 7);
+    cudaFree(lam);
+    cudaMalloc(&lam, sizeof(double) * 36 * N29);
+    k_fill<<<1184, 256>>>(x, N29 * 87, 2);
+    osc<GenTree29::Osc23, double, 0, 55, 3>("t29 osc23 f64 s55 b3", N29, x, y, lam, st, scratch, cap, 29);
+    osc<GenTree29::Osc23, float, 0, 220, 2>("t29 osc23 f32 s220 b2", N29, xf, yf, (float*)lam, st, sf, cap, 29);
+    cudaFree(lam);
+    constexpr int SP = GenTree29::CrbaPacked::kSlots;
+    plain<GenTree29::CrbaPacked, double, SP, 0, 3, false, false>("t29 crbap f64 plain rall b3", N29, x, y, st, scratch, cap, true);
+    plain<GenTree29::CrbaPacked, double, SP, 0, 3, false, true>("t29 crbap f64 plain rall b3 cs", N29, x, y, st, scratch, cap);
+    async<GenTree29::CrbaPacked, double, SP, 0, 3, false, true>("t29 crbap f64 async rall b3 cs", N29, x, y, st, scratch, cap);
+    async<GenTree29::CrbaPacked, double, SP, 0, 4, false, true>("t29 crbap f64 async rall b4 cs", N29, x, y, st, scratch, cap);
+    async<GenTree29::CrbaPacked, double, 0, SP, 4, false, true>("t29 crbap f64 async sall b4 cs", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Fk, double, 0, 55, 3, false, true>("t29 fk f64 plain s55 b3 cs", N29, x, y, st, scratch, cap, true);
+    plain<GenTree29::Rnea, double, 58, 55, 2, false, true>("t29 rnea f64 plain r58 s55 b2 cs", N29, x, y, st, scratch, cap, true);
   }
   if (ON("c7f")) {
     k_fill<<<1184, 256>>>(xf, N7 * 21, 1);

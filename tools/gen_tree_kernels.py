@@ -861,37 +861,43 @@ class Slots:
 def chol6(g, G):
     """In-place Cholesky of a symmetric 6x6 (dict (r, c) -> Ex, lower), the
     same operation order as vd_algos.cuh chol6 / Eigen's LLT.  Returns (L, ok
-    expression)."""
+    expression, pivots l_kk); L[(k, k)] holds the reciprocal 1 / l_kk, which
+    is all the substitutions need (a multiply instead of an fp64 division per
+    use: the divide is a ~10-instruction Newton sequence with a slow-path
+    branch)."""
     L = dict(G)
     oks = []
+    piv = []
     for k in range(6):
         x = L[(k, k)]
         for j in range(k):
             x = g.sub(x, g.mul(L[(k, j)], L[(k, j)]))
         oks.append(f"({g.o(x)} > T(0))")
         x = g.tmp(f"vd_sqrt({g.o(x)})", "sq")
-        L[(k, k)] = x
+        piv.append(x)
         inv = g.tmp(f"T(1) / {x.s}", "iv")
+        L[(k, k)] = inv
         for i in range(k + 1, 6):
             sv = L[(i, k)]
             for j in range(k):
                 sv = g.sub(sv, g.mul(L[(i, j)], L[(k, j)]))
             L[(i, k)] = g.mul(sv, inv)
-    return L, " && ".join(oks)
+    return L, " && ".join(oks), piv
 
 
 def chol6_solve(g, L, b):
+    """L Lᵀ x = b with L from chol6 (reciprocal diagonal)."""
     b = list(b)
     for i in range(6):
         sv = b[i]
         for j in range(i):
             sv = g.sub(sv, g.mul(L[(i, j)], b[j]))
-        b[i] = g.tmp(f"{g.o(sv)} / {g.o(L[(i, i)])}", "dv") if not sv.is0() else ZERO
+        b[i] = g.mul(sv, L[(i, i)])
     for i in range(5, -1, -1):
         sv = b[i]
         for j in range(i + 1, 6):
             sv = g.sub(sv, g.mul(L[(j, i)], b[j]))
-        b[i] = g.tmp(f"{g.o(sv)} / {g.o(L[(i, i)])}", "dv") if not sv.is0() else ZERO
+        b[i] = g.mul(sv, L[(i, i)])
     return b
 
 
@@ -993,8 +999,8 @@ def gen_osc(rb, fj):
         dkk = SL.get(("M", k, 0))
         g.raw(f"ok = ok && ({g.o(dkk)} > T(0));")
         lkk = g.tmp(f"vd_sqrt({g.o(dkk)})", "sq")
-        SL.set(("M", k, 0), lkk)
         inv = g.tmp(f"T(1) / {lkk.s}", "iv")
+        SL.set(("M", k, 0), inv)  # the substitutions below only need 1 / l_kk
         row = {0: lkk}
         for d in range(1, depth[k]):
             row[d] = g.mul(SL.get(("M", k, d)), inv)
@@ -1018,7 +1024,7 @@ def gen_osc(rb, fj):
     # Lᵀ y = b (leaf -> root), then L x = y (root -> leaf); only path entries of
     # x are needed (J is zero elsewhere)
     for i in range(n - 1, -1, -1):
-        inv = g.tmp(f"T(1) / {g.o(SL.get(('M', i, 0)))}", "iv")
+        inv = SL.get(("M", i, 0))
         xi = {}
         for r in range(7):
             v = SL.get(("X", r, i)) if SL.ref[("X", r, i)][0] == "s" else K(SL.ref[("X", r, i)][1])
@@ -1042,7 +1048,7 @@ def gen_osc(rb, fj):
             lij = SL.get(("M", i, d))
             for r in range(7):
                 acc[r] = g.sub(acc[r], g.mul(lij, xs[(r, j)]))
-        inv = g.tmp(f"T(1) / {g.o(SL.get(('M', i, 0)))}", "iv")
+        inv = SL.get(("M", i, 0))
         for r in range(7):
             xs[(r, i)] = g.mul(acc[r], inv)
     # ---- gram = J M⁻¹ Jᵀ, w = J M⁻¹ τ_post, J q̇
@@ -1055,8 +1061,8 @@ def gen_osc(rb, fj):
     jqd = [g.sum([g.mul(Jp[(r, k)], A.load(A.qdrefs[k])) for k in path]) for r in range(6)]
     eps = g.tmp("cx.eps()", "pe")
     Gr = {key: (g.add(v, eps) if key[0] == key[1] else v) for key, v in gram.items()}
-    Lr, _ = chol6(g, Gr)
-    Lg, gok = chol6(g, gram)
+    Lr, _, _ = chol6(g, Gr)
+    Lg, gok, _ = chol6(g, gram)
     g.raw(f"const bool gok_ = {gok};")
     F = [g.add(g.sub(g.mul(g.tmp(f"cx.kp({r})", "pg"), SL.get(("err", r))), g.mul(g.tmp(f"cx.kd({r})", "pg"), jqd[r])),
                g.tmp(f"cx.aff({r})", "pg")) for r in range(6)]
@@ -1193,7 +1199,7 @@ def gen_diffik(rb, fj):
         g.raw(f"cx.y(1, {r}, {g.o(err[r])});")
     rhs = [g.add(g.mul(g.tmp(f"cx.kp({r})", "pg"), err[r]), g.tmp(f"cx.tw({r})", "pg")) for r in range(6)]
     lam = g.tmp("cx.damp()", "pd")
-    L, okx = chol6(g, _gram6(g, J, path, g.mul(lam, lam)))
+    L, okx, _ = chol6(g, _gram6(g, J, path, g.mul(lam, lam)))
     g.raw(f"ok = ok && {okx};")
     x = chol6_solve(g, L, rhs)
     for j in range(rb.n):
@@ -1209,10 +1215,10 @@ def gen_manip(rb, fj):
     A = Algo(rb, False, only=_path(rb, fj))
     g = A.g
     _, _, J, path = frame_pose_J(A, fj)
-    L, okx = chol6(g, _gram6(g, J, path, None))
-    d = L[(0, 0)]
+    L, okx, piv = chol6(g, _gram6(g, J, path, None))
+    d = piv[0]
     for i in range(1, 6):
-        d = g.mul(d, L[(i, i)])
+        d = g.mul(d, piv[i])
     g.raw(f"cx.y(0, 0, ({okx}) ? {g.o(d)} : T(0));")
     return A.finish()
 
