@@ -70,12 +70,6 @@ int launch_fk(const Launch& L, const void* q, void* out) {
 int launch_jacobian(const Launch& L, const void* q, int frame_joint, const double* frame_R, const double* frame_p,
                     void* pose, void* J) {
   if (L.N == 0) return 0;
-  if (L.spec == kTree29) {
-    TaskShared P{};
-    for (int k = 0; k < 9; ++k) P.frame_R[k] = frame_R[k];
-    for (int k = 0; k < 3; ++k) P.frame_p[k] = frame_p[k];
-    if (const int rc = launch_gen_task(L, 0, frame_joint, P, q, pose, J, nullptr); rc >= 0) return rc;
-  }
   FrameArg fr;
   fr.joint = frame_joint;
   for (int k = 0; k < 9; ++k) fr.R[k] = frame_R[k];
@@ -83,6 +77,12 @@ int launch_jacobian(const Launch& L, const void* q, int frame_joint, const doubl
   // serial chains at batches below one wave of thread-per-state CTAs: 8 lanes
   // per state (config 2, Panda at N = 4096)
   if (L.serial && L.n <= 32 && L.N <= 32768) return launch_jac_scan(L, q, fr, pose, J);
+  if (L.spec == kTree29 || L.spec == kChain7) {
+    TaskShared P{};
+    for (int k = 0; k < 9; ++k) P.frame_R[k] = frame_R[k];
+    for (int k = 0; k < 3; ++k) P.frame_p[k] = frame_p[k];
+    if (const int rc = launch_gen_task(L, 0, frame_joint, P, q, pose, J, nullptr); rc >= 0) return rc;
+  }
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::jac(mv, L, q, fr, pose, J); });
 }
 

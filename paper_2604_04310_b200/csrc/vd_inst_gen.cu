@@ -352,11 +352,11 @@ int launch_gen_jvp(const Launch& L, const JvpArgs& a) {
 }
 
 // which: 0 Jacobian (y0 pose, y1 J), 1 diff-IK (y0 q̇, y1 err), 2 manipulability (y0 w)
-int launch_gen_task(const Launch& L, int which, int frame_joint, const TaskShared& P, const void* q, void* y0,
-                    void* y1, int32_t* status) {
-  if (L.spec != kTree29) return -1;
+template <class R>
+int gen_task_t(const Launch& L, int which, int frame_joint, const TaskShared& P, const void* q, void* y0, void* y1,
+               int32_t* status) {
   int rc = -1;
-  GenTree29::with_task(frame_joint, [&](auto jac, auto dik, auto man) {
+  R::with_task(frame_joint, [&](auto jac, auto dik, auto man) {
     auto go = [&](auto op) {
       using Op = decltype(op);
       rc = L.dtype == 0 ? launch_task_t<Op, double>(L, q, P, y0, y1, status)
@@ -367,6 +367,16 @@ int launch_gen_task(const Launch& L, int which, int frame_joint, const TaskShare
     else go(man);
   });
   return rc;
+}
+
+// Jacobian / diff-IK / manipulability on a generated frame joint.  chain7
+// `ee` (tools/async_sweep.cu "jac", 4M states): geometric Jacobian + pose
+// fp64 1.55 -> 0.39 ms, fp32 1.13 -> 0.37 ms against the template kernel.
+int launch_gen_task(const Launch& L, int which, int frame_joint, const TaskShared& P, const void* q, void* y0,
+                    void* y1, int32_t* status) {
+  if (L.spec == kTree29) return gen_task_t<GenTree29>(L, which, frame_joint, P, q, y0, y1, status);
+  if (L.spec == kChain7) return gen_task_t<GenChain7>(L, which, frame_joint, P, q, y0, y1, status);
+  return -1;
 }
 
 int launch_gen_crba(const Launch& L, const void* q, void* M) {

@@ -103,6 +103,30 @@ void osc(const char* name, int64_t N, T* x, T* y, T* lam, int32_t* st, T* scratc
          smem, bps, ms, N / (ms * 1e-3), cudaGetErrorString(cudaGetLastError()));
 }
 
+template <class Op, class T, int kReg, int kSmem, int kMinB>
+void task(const char* name, int64_t N, T* x, T* y0, T* y1, int32_t* st) {
+  auto kern = k_gen_task<Op, T, kReg, kSmem, kMinB>;
+  const size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int bps = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t grid = std::min<int64_t>((int64_t)sms * bps, (N + kGenBlock - 1) / kGenBlock);
+  TaskShared P{};
+  for (int k = 0; k < 9; ++k) P.frame_R[k] = P.target_R[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  P.frame_p[2] = 0.1;
+  cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int w = 0; w < 2; ++w) kern<<<grid, kGenBlock, smem>>>(N, x, N, P, y0, y1, N, st, nullptr);
+  cudaEventRecord(a);
+  const int reps = 10;
+  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, x, N, P, y0, y1, N, st, nullptr);
+  cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms = 0; cudaEventElapsedTime(&ms, a, b); ms /= reps;
+  printf("%-40s regs %3d lmem %4zu smem %6zu b/SM %d  %.4f ms  %.3e evals/s  %s\n", name, fa.numRegs, fa.localSizeBytes,
+         smem, bps, ms, N / (ms * 1e-3), cudaGetErrorString(cudaGetLastError()));
+}
+
 #define ON(k) (!strcmp(which, "all") || !strcmp(which, k))
 int main(int argc, char** argv) {
   const char* which = argc > 1 ? argv[1] : "all";
@@ -111,7 +135,7 @@ int main(int argc, char** argv) {
   int32_t* st;
   const int64_t Nmax = 4194304;
   cudaMalloc(&x, sizeof(double) * Nmax * 7 * 3);
-  cudaMalloc(&y, sizeof(double) * 262144 * 841);
+  cudaMalloc(&y, sizeof(double) * 4194304 * 84);
   cudaMalloc(&scratch, cap);
   cudaMalloc(&st, sizeof(int32_t) * Nmax);
   float* xf = (float*)x;
@@ -188,6 +212,22 @@ int main(int argc, char** argv) {
     async<GenTree29::CrbaPacked, double, 0, SP, 4, false, true>("t29 crbap f64 async sall b4 cs", N29, x, y, st, scratch, cap);
     plain<GenTree29::Fk, double, 0, 55, 3, false, true>("t29 fk f64 plain s55 b3 cs", N29, x, y, st, scratch, cap, true);
     plain<GenTree29::Rnea, double, 58, 55, 2, false, true>("t29 rnea f64 plain r58 s55 b2 cs", N29, x, y, st, scratch, cap, true);
+  }
+  if (ON("jac")) {
+    k_fill<<<1184, 256>>>(x, N7 * 21, 1);
+    double* J = nullptr;
+    cudaMalloc(&J, sizeof(double) * 42 * N7);
+    constexpr int SJ = GenChain7::Jac6::kSlots;
+    task<GenChain7::Jac6, double, 0, SJ, 3>("c7 jac6 f64 sall b3", N7, x, y, J, st);
+    task<GenChain7::Jac6, double, 0, SJ, 4>("c7 jac6 f64 sall b4", N7, x, y, J, st);
+    task<GenChain7::Jac6, double, 0, SJ, 5>("c7 jac6 f64 sall b5", N7, x, y, J, st);
+    task<GenChain7::Jac6, float, 0, SJ, 6>("c7 jac6 f32 sall b6", N7, xf, yf, (float*)J, st);
+    constexpr int SF = GenChain7::Fk::kSlots;
+    plain<GenChain7::Fk, double, SF, 0, 4, true, false>("c7 fk f64 plain rall b4", N7, x, y, st, scratch, cap, true);
+    plain<GenChain7::Fk, double, SF, 0, 4, true, true>("c7 fk f64 plain rall b4 cs", N7, x, y, st, scratch, cap);
+    async<GenChain7::Fk, double, SF, 0, 4, true, true>("c7 fk f64 async rall b4 cs", N7, x, y, st, scratch, cap);
+    async<GenChain7::Fk, double, SF, 0, 6, true, true>("c7 fk f64 async rall b6 cs", N7, x, y, st, scratch, cap);
+    cudaFree(J);
   }
   if (ON("c7f")) {
     k_fill<<<1184, 256>>>(xf, N7 * 21, 1);
