@@ -234,7 +234,10 @@ struct JvpCfg {
   static constexpr int kRegCap = sizeof(T) == 8 ? 40 : 0, kSmemCap = sizeof(T) == 8 ? 110 : 220;
   static constexpr int kReg = kRegCap < Op::kSlots ? kRegCap : Op::kSlots;
   static constexpr int kSmem = kSmemCap < Op::kSlots - kReg ? kSmemCap : Op::kSlots - kReg;
-  static constexpr int kMinB = 2;
+  // fp32 routines up to 110 slots at 3 CTAs/SM (async_sweep "jvp", G1 at
+  // 262144: CRBA-JVP 0.50 -> 0.43 ms, FK-JVP 0.25 -> 0.20 ms); fp64 and the
+  // larger routines measured best at 2 (255 registers)
+  static constexpr int kMinB = sizeof(T) == 4 && Op::kSlots <= 110 ? 3 : 2;
 };
 
 template <class Op, class T, bool kStream>
@@ -338,17 +341,27 @@ int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShar
   return -1;
 }
 
-int launch_gen_jvp(const Launch& L, const JvpArgs& a) {
-  if (L.spec != kTree29 || (a.fext && (a.op == kJvpABA || a.op == kJvpRNEA))) return -1;
+template <class R>
+int gen_jvp_t(const Launch& L, const JvpArgs& a) {
   if (a.op == kJvpABA)
-    return L.dtype == 0 ? launch_jvp_t<GenTree29::AbaJvp, double>(L, a) : launch_jvp_t<GenTree29::AbaJvp, float>(L, a);
+    return L.dtype == 0 ? launch_jvp_t<typename R::AbaJvp, double>(L, a) : launch_jvp_t<typename R::AbaJvp, float>(L, a);
   if (a.op == kJvpRNEA)
-    return L.dtype == 0 ? launch_jvp_t<GenTree29::RneaJvp, double>(L, a)
-                        : launch_jvp_t<GenTree29::RneaJvp, float>(L, a);
+    return L.dtype == 0 ? launch_jvp_t<typename R::RneaJvp, double>(L, a)
+                        : launch_jvp_t<typename R::RneaJvp, float>(L, a);
   if (a.op == kJvpCRBA)
-    return L.dtype == 0 ? launch_jvp_t<GenTree29::CrbaJvp, double>(L, a)
-                        : launch_jvp_t<GenTree29::CrbaJvp, float>(L, a);
-  return L.dtype == 0 ? launch_jvp_t<GenTree29::FkJvp, double>(L, a) : launch_jvp_t<GenTree29::FkJvp, float>(L, a);
+    return L.dtype == 0 ? launch_jvp_t<typename R::CrbaJvp, double>(L, a)
+                        : launch_jvp_t<typename R::CrbaJvp, float>(L, a);
+  return L.dtype == 0 ? launch_jvp_t<typename R::FkJvp, double>(L, a) : launch_jvp_t<typename R::FkJvp, float>(L, a);
+}
+
+int launch_gen_jvp(const Launch& L, const JvpArgs& a) {
+  if (a.fext && (a.op == kJvpABA || a.op == kJvpRNEA)) return -1;
+  if (L.spec == kTree29) return gen_jvp_t<GenTree29>(L, a);
+  // chain7 (tools/jvp_time.py, 1M states, Python API, template -> generated):
+  // fp64 FK-JVP 0.39 -> 0.37, RNEA-JVP 0.55 -> 0.36, CRBA-JVP 0.35 -> 0.25,
+  // ABA-JVP 0.84 -> 0.66 ms; fp32 0.22/0.34/0.17/0.56 -> 0.21/0.23/0.16/0.43 ms
+  if (L.spec == kChain7) return gen_jvp_t<GenChain7>(L, a);
+  return -1;
 }
 
 // which: 0 Jacobian (y0 pose, y1 J), 1 diff-IK (y0 q̇, y1 err), 2 manipulability (y0 w)

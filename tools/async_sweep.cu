@@ -127,6 +127,34 @@ void task(const char* name, int64_t N, T* x, T* y0, T* y1, int32_t* st) {
          smem, bps, ms, N / (ms * 1e-3), cudaGetErrorString(cudaGetLastError()));
 }
 
+template <class Op, class T, int kReg, int kSmem, int kMinB>
+void jvp(const char* name, int64_t N, T* x, T* y, T* scratch, size_t cap) {
+  auto kern = k_gen_jvp<Op, T, kReg, kSmem, kMinB, true>;
+  const size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int bps = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t grid = std::min<int64_t>((int64_t)sms * bps, (N + kGenBlock - 1) / kGenBlock);
+  if ((size_t)(grid * kGenBlock * gen_scratch_per_thread<Op, T, kReg, kSmem>() * sizeof(T)) > cap) { printf("%s scratch\n", name); return; }
+  const int n = Op::kDof;
+  JvpArgs a{};
+  for (int g = 0; g < Op::kIn; ++g) { a.x[g] = x + g * N * n; a.dx[g] = x + (3 + g) * N * n; }
+  a.g[2] = 9.81;
+  a.out = y;
+  a.dout = y + (int64_t)Op::kOut * N;
+  cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int w = 0; w < 2; ++w) kern<<<grid, kGenBlock, smem>>>(N, a, N, N, scratch);
+  cudaEventRecord(e0);
+  const int reps = 10;
+  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, a, N, N, scratch);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms = 0; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
+  printf("%-40s regs %3d lmem %4zu smem %6zu b/SM %d  %.4f ms  %.3e evals/s  %s\n", name, fa.numRegs, fa.localSizeBytes,
+         smem, bps, ms, N / (ms * 1e-3), cudaGetErrorString(cudaGetLastError()));
+}
+
 #define ON(k) (!strcmp(which, "all") || !strcmp(which, k))
 int main(int argc, char** argv) {
   const char* which = argc > 1 ? argv[1] : "all";
@@ -228,6 +256,33 @@ int main(int argc, char** argv) {
     async<GenChain7::Fk, double, SF, 0, 4, true, true>("c7 fk f64 async rall b4 cs", N7, x, y, st, scratch, cap);
     async<GenChain7::Fk, double, SF, 0, 6, true, true>("c7 fk f64 async rall b6 cs", N7, x, y, st, scratch, cap);
     cudaFree(J);
+  }
+  if (ON("jvp")) {
+    // 6 input planes of N29 x 29 doubles, outputs value + tangent
+    double *xj = nullptr, *yj = nullptr;
+    cudaMalloc(&xj, sizeof(double) * 6 * 29 * N29);
+    cudaMalloc(&yj, sizeof(double) * 2 * 841 * N29);
+    k_fill<<<1184, 256>>>(xj, 6 * 29 * N29, 5);
+    jvp<GenTree29::CrbaJvp, double, 40, 70, 2>("t29 crbajvp f64 r40 s70 b2", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::CrbaJvp, double, 40, 70, 3>("t29 crbajvp f64 r40 s70 b3", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::CrbaJvp, double, 0, 55, 3>("t29 crbajvp f64 r0 s55 b3", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::CrbaJvp, double, 40, 110, 2>("t29 crbajvp f64 r40 s110 b2 (r1)", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::FkJvp, double, 40, 70, 2>("t29 fkjvp f64 r40 s70 b2", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::FkJvp, double, 40, 70, 3>("t29 fkjvp f64 r40 s70 b3", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::FkJvp, double, 0, 55, 3>("t29 fkjvp f64 r0 s55 b3", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::FkJvp, double, 40, 110, 2>("t29 fkjvp f64 r40 s110 b2 (r1)", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::CrbaJvp, float, 0, 110, 2>("t29 crbajvp f32 s110 b2", N29, (float*)xj, (float*)yj, sf, cap);
+    jvp<GenTree29::CrbaJvp, float, 0, 110, 3>("t29 crbajvp f32 s110 b3", N29, (float*)xj, (float*)yj, sf, cap);
+    jvp<GenTree29::FkJvp, float, 0, 110, 2>("t29 fkjvp f32 s110 b2", N29, (float*)xj, (float*)yj, sf, cap);
+    jvp<GenTree29::FkJvp, float, 0, 110, 3>("t29 fkjvp f32 s110 b3", N29, (float*)xj, (float*)yj, sf, cap);
+    jvp<GenChain7::AbaJvp, double, 40, 89, 2>("c7 abajvp f64 r40 s89 b2", 1048576, xj, yj, scratch, cap);
+    jvp<GenChain7::AbaJvp, double, 40, 40, 3>("c7 abajvp f64 r40 s40 b3", 1048576, xj, yj, scratch, cap);
+    jvp<GenChain7::AbaJvp, double, 64, 65, 2>("c7 abajvp f64 r64 s65 b2", 1048576, xj, yj, scratch, cap);
+    jvp<GenChain7::RneaJvp, double, 40, 16, 2>("c7 rneajvp f64 r40 s16 b2", 1048576, xj, yj, scratch, cap);
+    jvp<GenChain7::RneaJvp, double, 56, 0, 3>("c7 rneajvp f64 r56 b3", 1048576, xj, yj, scratch, cap);
+    jvp<GenChain7::RneaJvp, double, 56, 0, 4>("c7 rneajvp f64 r56 b4", 1048576, xj, yj, scratch, cap);
+    cudaFree(xj);
+    cudaFree(yj);
   }
   if (ON("c7f")) {
     k_fill<<<1184, 256>>>(xf, N7 * 21, 1);
