@@ -191,11 +191,14 @@ int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, co
   return (int)e;
 }
 
-// OSC (tools/gen_sweep.cu): fp64 55 slots in shared memory at 3 CTAs/SM,
-// fp32 220 slots at 2 CTAs/SM.
+// OSC on branched trees: the articulated-body form (gen_osc_aba, ~255 slots
+// for a G1 hand/foot frame instead of the 486 of the M-based form).
+// tools/async_sweep.cu "more", G1 `l_palm`, N = 262144: fp64 r40 s110 (2
+// CTAs/SM) 0.61 ms, s55 b3 0.69 ms (the M-based routine: 1.23 ms); fp32
+// r40 s144 (3 CTAs/SM) 0.27 ms (M-based: 0.50 ms).
 template <class Op, class T>
 struct OscCfg {
-  static constexpr int kReg = 0, kSmem = sizeof(T) == 8 ? 55 : 220, kMinB = sizeof(T) == 8 ? 3 : 2;
+  static constexpr int kReg = 40, kSmem = sizeof(T) == 8 ? 110 : 144, kMinB = sizeof(T) == 8 ? 2 : 3;
 };
 // chain7 (Panda `ee`), N = 4M, tools/async_sweep.cu "more": every slot on
 // chip.  fp64 r80 s67 b2 1.45 ms, fp32 r60 s87 1.56 -> 0.70 ms, against the

@@ -230,7 +230,15 @@ int main(int argc, char** argv) {
     cudaMalloc(&lam, sizeof(double) * 36 * N29);
     k_fill<<<1184, 256>>>(x, N29 * 87, 2);
     osc<GenTree29::Osc23, double, 0, 55, 3>("t29 osc23 f64 s55 b3", N29, x, y, lam, st, scratch, cap, 29);
+    osc<GenTree29::Osc23, double, 0, 110, 2>("t29 osc23 f64 s110 b2", N29, x, y, lam, st, scratch, cap, 29);
+    osc<GenTree29::Osc23, double, 40, 55, 3>("t29 osc23 f64 r40 s55 b3", N29, x, y, lam, st, scratch, cap, 29);
+    osc<GenTree29::Osc23, double, 40, 110, 2>("t29 osc23 f64 r40 s110 b2", N29, x, y, lam, st, scratch, cap, 29);
+    osc<GenTree29::Osc23, double, 0, 72, 3>("t29 osc23 f64 s72 b3", N29, x, y, lam, st, scratch, cap, 29);
+    osc<GenTree29::Osc23, double, 0, 40, 4>("t29 osc23 f64 s40 b4", N29, x, y, lam, st, scratch, cap, 29);
     osc<GenTree29::Osc23, float, 0, 220, 2>("t29 osc23 f32 s220 b2", N29, xf, yf, (float*)lam, st, sf, cap, 29);
+    osc<GenTree29::Osc23, float, 0, 144, 3>("t29 osc23 f32 s144 b3", N29, xf, yf, (float*)lam, st, sf, cap, 29);
+    osc<GenTree29::Osc23, float, 40, 144, 3>("t29 osc23 f32 r40 s144 b3", N29, xf, yf, (float*)lam, st, sf, cap, 29);
+    osc<GenTree29::Osc23, float, 0, 110, 4>("t29 osc23 f32 s110 b4", N29, xf, yf, (float*)lam, st, sf, cap, 29);
     cudaFree(lam);
     constexpr int SP = GenTree29::CrbaPacked::kSlots;
     plain<GenTree29::CrbaPacked, double, SP, 0, 3, false, false>("t29 crbap f64 plain rall b3", N29, x, y, st, scratch, cap, true);

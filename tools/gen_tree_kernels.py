@@ -1109,6 +1109,220 @@ def gen_osc(rb, fj):
     return A.finish()
 
 
+def gen_osc_aba(rb, fj):
+    """osc_step (control.hpp:108-155) for a task frame on joint fj through the
+    articulated-body factorisation instead of M: the same quantities as
+    gen_osc (Λ = (J M⁻¹ Jᵀ + εI)⁻¹, J M⁻¹ τ_post, c + g, τ) but M is never
+    formed.  One ABA pass 2 at zero velocity and gravity over all joints
+    (articulated inertias, with τ_post as the joint force) keeps U/D, 1/D
+    and u/D of the path joints only; M⁻¹ τ_post and the six columns of the
+    body-frame inverse task inertia G_b = J_b M⁻¹ J_bᵀ (a unit wrench at the
+    frame body, propagated up the path and the accelerations back down it)
+    are path-only sweeps; J never materialises: J = T J_b with
+    T = [[R, 0], [−R [r_f]×, R]] (R the frame body's world rotation, r_f the
+    frame point in body coordinates), so J M⁻¹ Jᵀ = T G_b Tᵀ, J q̇ = T v_b,
+    and Jᵀ F is the body wrench Tᵀ F pushed up the path.  Per-state slot
+    state is the prologue plus ~9 values per path joint, against the
+    branch-sparse M of gen_osc (G1 `l_palm`: 486 -> ~220 slots), which is
+    what bounds the G1 OSC (its L2 scratch slab spills to DRAM).
+    Featherstone RBDA Table 7.1 (ABA with external forces: p^A = −f^x);
+    the reference's LLT of M (control.hpp:131-149) is the oracle.
+    x(0) = q, x(1) = q̇; y(0, k) = τ_k, y(1, 6 c + r) = Λ(r, c)."""
+    A = Algo(rb, True)
+    g = A.g
+    path = []
+    j = fj
+    while j >= 0:
+        path.append(j)
+        j = rb.parent[j]
+    path = path[::-1]  # root .. fj
+    onpath = set(path)
+    SL = Slots(A)
+
+    # ---- world pose of the frame body (kinematics.hpp:43-56, 89-96)
+    Wp = None
+    for i in path:
+        X = A.joint(i)
+        Rl = [g.dot(X.QO[3 * r:3 * r + 3], [X.QJ[c], X.QJ[3 + c], X.QJ[6 + c]]) for r in range(3) for c in range(3)]
+        pl = g.vadd(X.tO, g.matvec(X.QO, X.tJ))
+        if Wp is None:
+            Wp = (Rl, pl)
+        else:
+            Wp = ([g.dot(Wp[0][3 * r:3 * r + 3], [Rl[c], Rl[3 + c], Rl[6 + c]]) for r in range(3) for c in range(3)],
+                  g.vadd(g.matvec(Wp[0], pl), Wp[1]))
+    WR, Wpos = Wp
+    fR = [g.tmp(f"cx.fR({k})", "pf") for k in range(9)]
+    fpv = [g.tmp(f"cx.fp({k})", "pf") for k in range(3)]
+    pose_R = [g.dot(WR[3 * r:3 * r + 3], [fR[c], fR[3 + c], fR[6 + c]]) for r in range(3) for c in range(3)]
+    pose_p = g.vadd(g.matvec(WR, fpv), Wpos)
+    for k in range(9):
+        SL.set(("R", k), WR[k])
+    # ---- pose error (control.hpp:73-77): log(R_t R_cᵀ), p_t − p_c
+    tR = [g.tmp(f"cx.tR({k})", "pt") for k in range(9)]
+    Rrel = [g.dot(tR[3 * r:3 * r + 3], pose_R[3 * c:3 * c + 3]) for r in range(3) for c in range(3)]
+    g.raw(f"const T Rrel_[9] = {{{', '.join(g.o(x) for x in Rrel)}}};")
+    g.raw("T lg_[3];")
+    g.raw("vd_rotation_log(Rrel_, lg_);")
+    err = [Ex(s="lg_[0]"), Ex(s="lg_[1]"), Ex(s="lg_[2]")]
+    err += [g.sub(g.tmp(f"cx.tp({k})", "pt"), pose_p[k]) for k in range(3)]
+    for k in range(6):
+        SL.set(("err", k), err[k])
+
+    pkp, pkd = g.tmp("cx.pkp()", "pp"), g.tmp("cx.pkd()", "pp")
+
+    def tpost(k):  # τ_post = kp_p (q_post − q) − kd_p q̇ (control.hpp:150-151)
+        qk = g.tmp(f"cx.x(0, {k})", "q")
+        return g.sub(g.mul(pkp, g.sub(g.tmp(f"cx.post({k})", "pp"), qk)), g.mul(pkd, A.load(A.qdrefs[k])))
+
+    # ---- ABA pass 2 at q̇ = 0, a_g = 0 with τ = τ_post (RBDA Table 7.1)
+    def up(i):
+        acc = None
+        for c in rb.children[i]:
+            Ic, pc = up(c)
+            acc = (Ic, pc) if acc is None else (g.ai_add(acc[0], Ic), g.vadd(acc[1], pc))
+        X = A.joint(i)
+        IA = g.ai_from_rb(rb.rb(i))
+        pA = [ZERO] * 6
+        if acc is not None:
+            IA = g.ai_add(IA, acc[0])
+            pA = acc[1]
+        U = g.ai_apply(IA, X.Svec())
+        D = X.Sdot(U)
+        g.check_pos(D)
+        dinv = g.recip(D)
+        u = g.sub(tpost(i), X.Sdot(pA))
+        Ud = [g.mul(x, dinv) for x in U]
+        ud = g.mul(u, dinv)
+        if i in onpath:
+            for k in range(6):
+                SL.set(("Ud", i, k), Ud[k])
+            SL.set(("dinv", i), dinv)
+            SL.set(("ud", i), ud)
+        if rb.parent[i] < 0:
+            return None
+        ir, ic = (0, 1, 2, 0, 0, 1), (0, 1, 2, 1, 2, 2)  # Ia = IA − U Udᵀ
+        Ia = {"A": [g.sub(IA["A"][k], g.mul(U[ir[k]], Ud[ic[k]])) for k in range(6)],
+              "C": [g.sub(IA["C"][k], g.mul(U[3 + ir[k]], Ud[3 + ic[k]])) for k in range(6)],
+              "B": [g.sub(IA["B"][3 * r + cc], g.mul(U[r], Ud[3 + cc])) for r in range(3) for cc in range(3)]}
+        pa = g.vadd(pA, [g.mul(x, ud) for x in U])
+        return X.ai_to_parent(Ia), X.force_to_parent(pa)
+
+    for r in rb.roots:
+        up(r)
+
+    def down_path(urefs):
+        """Pass 3 down the path at zero velocity and gravity; urefs(i) -> u_i
+        (or None: use the stored u/D).  Returns the frame body's acceleration."""
+        a = None
+        for i in path:
+            X = A.joint(i)
+            Ud = [SL.get(("Ud", i, k)) for k in range(6)]
+            if a is not None:
+                a = X.motion_to_child(a)
+            u = urefs(i)
+            qdd = SL.get(("ud", i)) if u is None else g.mul(u, SL.get(("dinv", i)))
+            if a is not None:
+                qdd = g.sub(qdd, g.sdot(Ud, a))
+            a = X.S(qdd) if a is None else g.vadd(a, X.S(qdd))
+        return a
+
+    a_post = down_path(lambda i: None)  # M⁻¹ τ_post seen at the frame body
+    apost = [g.tmp(g.o(x), "ap") if x.c is None else x for x in a_post]
+    for k in range(6):
+        SL.set(("apost", k), apost[k])
+
+    # ---- G_b = J_b M⁻¹ J_bᵀ: unit wrench e_r at the frame body (p^A = −e_r)
+    Gb = {}
+    for r in range(6):
+        pA = [K(-1.0) if k == r else ZERO for k in range(6)]
+        for i in reversed(path):
+            X = A.joint(i)
+            u = g.neg(X.Sdot(pA))
+            SL.set(("u", i), u)
+            if rb.parent[i] >= 0:
+                Ud = [SL.get(("Ud", i, k)) for k in range(6)]
+                pA = X.force_to_parent(g.vadd(pA, [g.mul(x, u) for x in Ud]))
+        col = down_path(lambda i: SL.get(("u", i)) if SL.ref[("u", i)][0] == "s" else K(SL.ref[("u", i)][1]))
+        for k in range(6):
+            Gb[(k, r)] = col[k]
+            SL.set(("Gb", k, r), col[k])
+
+    # ---- T = [[R, 0], [−R [r_f]×, R]]: body spatial vector -> world (ω, v at the frame point)
+    R = [SL.get(("R", k)) for k in range(9)]
+    rf = [g.tmp(f"cx.fp({k})", "pf") for k in range(3)]
+
+    def Tm(m):
+        return g.matvec(R, m[:3]) + g.matvec(R, g.vadd(m[3:], g.cross3(m[:3], rf)))
+
+    TG = [Tm([SL.get(("Gb", k, c)) for k in range(6)]) for c in range(6)]  # TG[c] = column c of T G_b
+    gram = {}
+    for rr in range(6):
+        row = Tm([TG[c][rr] for c in range(6)])  # row rr of T G_b Tᵀ
+        for c in range(rr + 1):
+            gram[(rr, c)] = row[c]
+    w = Tm([SL.get(("apost", k)) for k in range(6)])
+    # J q̇ = T v_b, v_b from the velocity pass down the path
+    v = None
+    for i in path:
+        X = A.joint(i)
+        qdi = A.load(A.qdrefs[i])
+        v = X.S(qdi) if v is None else g.vadd(X.motion_to_child(v), X.S(qdi))
+    jqd = Tm(v)
+    eps = g.tmp("cx.eps()", "pe")
+    Gr = {key: (g.add(val, eps) if key[0] == key[1] else val) for key, val in gram.items()}
+    Lr, _, _ = chol6(g, Gr)
+    Lg, gok, _ = chol6(g, gram)
+    g.raw(f"const bool gok_ = {gok};")
+    F = [g.add(g.sub(g.mul(g.tmp(f"cx.kp({r})", "pg"), SL.get(("err", r))), g.mul(g.tmp(f"cx.kd({r})", "pg"), jqd[r])),
+               g.tmp(f"cx.aff({r})", "pg")) for r in range(6)]
+    F = chol6_solve(g, Lr, F)
+    zg = chol6_solve(g, Lg, w)
+    zr = chol6_solve(g, Lr, w)
+    z = [g.tmp(f"gok_ ? {g.o(a)} : {g.o(b)}", "z") for a, b in zip(zg, zr)]
+    fz = [g.sub(a, b) for a, b in zip(F, z)]
+    # ---- Jᵀ (F − z): body wrench Tᵀ fz = (Rᵀ n + r_f × Rᵀ f, Rᵀ f), pushed up the path
+    fl = g.matTvec(R, fz[3:])
+    fb = g.vadd(g.matTvec(R, fz[:3]), g.cross3(rf, fl)) + fl
+    for i in reversed(path):
+        X = A.joint(i)
+        SL.set(("jt", i), X.Sdot(fb))
+        if rb.parent[i] >= 0:
+            fb = X.force_to_parent(fb)
+    # ---- Λ = (J M⁻¹ Jᵀ + εI)⁻¹, column by column
+    g.raw("if (cx.want_lambda()) {")
+    for c in range(6):
+        e = chol6_solve(g, Lr, [ONE if r == c else ZERO for r in range(6)])
+        for r in range(6):
+            g.raw(f"cx.y(1, {6 * c + r}, {g.o(e[r])});")
+    g.raw("}")
+    # ---- bias c + g (RNEA with q̈ = 0, dynamics.hpp:434-435) and τ
+    gvec = A.gravity()
+
+    def rec(i, vp, ap):
+        X = A.joint(i)
+        qdi = A.load(A.qdrefs[i])
+        if vp is None:
+            v = X.S(qdi)
+            a = X.motion_to_child(gvec)
+        else:
+            v = g.vadd(X.motion_to_child(vp), X.S(qdi))
+            a = g.vadd(X.motion_to_child(ap), g.crm(v, X.S(qdi)))
+        b = rb.rb(i)
+        f = g.vadd(g.rb_apply(b, a), g.crf(v, g.rb_apply(b, v)))
+        for c in rb.children[i]:
+            f = g.vadd(f, rec(c, v, a))
+        if rb.children[i]:
+            X = A.joint(i)
+        tau = g.add(g.add(tpost(i), X.Sdot(f)), SL.get(("jt", i)) if i in onpath else ZERO)
+        g.raw(f"cx.y(0, {i}, {g.o(tau)});")
+        g.raw(f"ok = ok && vd_isfinite({g.o(tau)});")
+        return X.force_to_parent(f) if vp is not None else None
+
+    for r in rb.roots:
+        rec(r, None, None)
+    return A.finish()
+
+
 def frame_pose_J(A, fj):
     """frame_transform + geometric_jacobian (kinematics.hpp:89-129) of the
     task frame on joint fj (offset cx.fR / cx.fp, row-major): pose (R
@@ -1302,8 +1516,11 @@ def emit_body(name, cls, rb):
     # one variant for every leaf joint (end effectors) and the joints that
     # carry a named frame of the model
     osc_joints = sorted(set(i for i in range(rb.n) if not rb.children[i]) | set(rb.frame_joints))
+    # branched trees: the articulated-body OSC (no M in per-state slots);
+    # serial chains: M is small, the branch-sparse LTL form costs fewer flops
+    serial = all(p == i - 1 for i, p in enumerate(rb.parent))
     for fj in osc_joints:
-        A = gen_osc(rb, fj)
+        A = gen_osc(rb, fj) if serial else gen_osc_aba(rb, fj)
         out += [f"  // Osc on joint {fj}: {A.g.flops} mul/add after folding; {A.nslot} slots",
                 f"  struct Osc{fj} {{",
                 f"    static constexpr int kSlots = {A.nslot};",
