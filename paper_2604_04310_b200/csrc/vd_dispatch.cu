@@ -93,9 +93,7 @@ int launch_rnea(const Launch& L, int mode, const void* q, const void* qd, const 
   const double* g = (mode == 3) ? zero3 : g3;
   const void* qd_ = (mode == 2) ? nullptr : qd;
   const void* qdd_ = (mode == 0) ? qdd : nullptr;
-  if (!fext) {
-    if (const int rc = launch_gen_rnea(L, mode, q, qd, qdd, g3, tau); rc >= 0) return rc;
-  }
+  if (const int rc = launch_gen_rnea(L, mode, q, qd, qdd, g3, fext, tau); rc >= 0) return rc;
   return with_view<true>(L, [&](auto mv) { return Launcher<decltype(mv)>::rnea(mv, L, q, qd_, qdd_, g, fext, tau); });
 }
 
@@ -153,10 +151,7 @@ int launch_crba_packed(const Launch& L, const void* q, void* Mp, const PackTable
 int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, const void* fext,
                void* qdd, int32_t* status) {
   if (L.N == 0) return 0;
-  if (!fext) {
-    const int rc = launch_gen_aba(L, q, qd, tau, g3, qdd, status);
-    if (rc >= 0) return rc;
-  }
+  if (const int rc = launch_gen_aba(L, q, qd, tau, g3, fext, qdd, status); rc >= 0) return rc;
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::aba(mv, L, q, qd, tau, g3, fext, qdd, status); });
 }
 
@@ -168,8 +163,8 @@ int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* 
     // transforms; cheaper than the fused loop kernel's local-memory state)
     int rc = 0;
     if (M && (rc = launch_gen_crba(L, q, M)) != 0) return rc;
-    if (bias && (rc = launch_gen_rnea(L, 1, q, qd, nullptr, g3, bias)) != 0) return rc;
-    if (qdd && (rc = launch_gen_aba(L, q, qd, tau, g3, qdd, status)) != 0) return rc;
+    if (bias && (rc = launch_gen_rnea(L, 1, q, qd, nullptr, g3, nullptr, bias)) != 0) return rc;
+    if (qdd && (rc = launch_gen_aba(L, q, qd, tau, g3, nullptr, qdd, status)) != 0) return rc;
     return 0;
   }
   return with_view(L,

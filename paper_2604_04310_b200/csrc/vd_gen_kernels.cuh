@@ -79,6 +79,7 @@ struct GenCx {
   static constexpr int kGlobal = kSlots - kReg - kSmem > 0 ? kSlots - kReg - kSmem : 0;
   const T* in_[3];  // &x_g[i]; element (i, j) of input g at in_[g][j * ld]
   T* out_;          // &y[i]; element (i, k) at out_[k * ldo]
+  const T* fx_;     // &fext[i] (NULL: no external wrenches); plane 6 j + k at fx_[(6 j + k) * ld]
   T* sb;            // this thread's scratch: slot k at sb[(k - kSmem) * 32] (warp-interleaved)
   uint32_t sm;      // shared address of slot 0 for this thread ([k][threadIdx.x])
   int64_t ld, ldo;
@@ -88,6 +89,10 @@ struct GenCx {
   __device__ __forceinline__ T x(int g, int j) const {
     if constexpr (kStream) return __ldcs(in_[g] + j * ld);
     else return GenMem<T>::ldg(in_[g] + j * ld);
+  }
+  __device__ __forceinline__ T fx(int k) const {
+    if constexpr (kStream) return __ldcs(fx_ + k * ld);
+    else return GenMem<T>::ldg(fx_ + k * ld);
   }
   __device__ __forceinline__ void prefetch(int g, int j) const {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(in_[g] + j * ld));
@@ -146,7 +151,8 @@ template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false,
           int kSyncEvery = 0, int kBlk = kGenBlock>
 __global__ void __launch_bounds__(kBlk, kMinB)
     k_gen(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
-          T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status, T* __restrict__ scratch) {
+          T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status, T* __restrict__ scratch,
+          const T* __restrict__ fext) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
   using Cx = GenCx<T, Op::kSlots, kReg, kSmem, kFast, kStream, kSyncEvery, kBlk>;
   Cx cx;
@@ -172,6 +178,7 @@ __global__ void __launch_bounds__(kBlk, kMinB)
     cx.in_[1] = (Op::kIn > 1 ? x1 : x0) + i;
     cx.in_[2] = (Op::kIn > 2 ? x2 : x0) + i;
     cx.out_ = y + i;
+    cx.fx_ = fext ? fext + i : nullptr;
     const bool ok = Op::template run<T>(cx);
     if (cx.active) {
       if (!ok) {
@@ -232,7 +239,7 @@ template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false,
 __global__ void __launch_bounds__(kGenBlock, kMinB)
     k_gen_async(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
                 T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status,
-                T* __restrict__ scratch) {
+                T* __restrict__ scratch, const T* __restrict__ fext) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
   using Cx = GenAsyncCx<T, Op::kSlots, kReg, kSmem, kFast, kStream, Op::kDof, kSyncEvery>;
   Cx cx;
@@ -269,6 +276,7 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
       cx.nx[g] = xs[g] + inext;
     }
     cx.out_ = y + i;
+    cx.fx_ = fext ? fext + i : nullptr;
     asm volatile("cp.async.wait_all;" ::: "memory");
     const bool ok = Op::template run<T>(cx);
     if (cx.active) {

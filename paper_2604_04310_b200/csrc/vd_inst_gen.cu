@@ -67,6 +67,13 @@ struct Cfg<GenChain7::RneaGrav, T> : Chain7RneaCfg<T, GenChain7::RneaGrav::kSlot
 // G1 ABA / dense CRBA with evict-first state I/O (gen_sweep, two runs each,
 // N = 262144): ABA fp64 0.31-0.42 -> 0.29 ms, mixed fp32 0.19 -> 0.17 ms,
 // CRBA fp64 0.39 (s40 b4) -> 0.30 ms (s55 b3), fp32 0.30 -> 0.16 ms
+// f_ext routines: the placement of their plain counterparts
+template <class T>
+struct Cfg<GenChain7::RneaFext, T> : Chain7RneaCfg<T, GenChain7::RneaFext::kSlots> {};
+template <class T>
+struct Cfg<GenChain7::RneaBiasFext, T> : Chain7RneaCfg<T, GenChain7::RneaBiasFext::kSlots> {};
+template <class T>
+struct Cfg<GenChain7::AbaFext, T> : Cfg<GenChain7::Aba, T> {};
 template <>
 struct Cfg<GenTree29::Aba, double> {
   static constexpr int kReg = 40, kSmem = 113, kMinB = 2;
@@ -121,6 +128,14 @@ struct Cfg<GenTree29::RneaBias, double> {
   static constexpr int kReg = 0, kSmem = 72, kMinB = 3;
   static constexpr bool kFast = false;
 };
+template <class T>
+struct Cfg<GenTree29::RneaFext, T> : Cfg<GenTree29::Rnea, T> {};
+template <>
+struct Cfg<GenTree29::RneaBiasFext, double> : Cfg<GenTree29::RneaBias, double> {};
+template <>
+struct Cfg<GenTree29::AbaFext, double> : Cfg<GenTree29::Aba, double> {};
+template <>
+struct Cfg<GenTree29::AbaMixedFext, float> : Cfg<GenTree29::AbaMixed, float> {};
 
 struct Occ {
   int blocks_per_sm = 0, sms = 0;
@@ -162,7 +177,7 @@ constexpr auto gen_kernel() {
 
 template <class Op, class T>
 int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
-             int32_t* status) {
+             int32_t* status, const void* fext = nullptr) {
   using C = Cfg<Op, T>;
   constexpr bool kAsync = AsyncIo<C>::value;
   auto kern = gen_kernel<Op, T, C>();
@@ -185,7 +200,7 @@ int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, co
   // gravity3 == NULL: GravitySpec::standard() (dynamics.hpp:39-50), as g3_of
   const T g0 = g3 ? T(g3[0]) : T(0), g1 = g3 ? T(g3[1]) : T(0), g2 = g3 ? T(g3[2]) : T(9.81);
   kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, (const T*)x0, (const T*)x1, (const T*)x2, L.ld_in, g0, g1, g2,
-                                                 (T*)y, L.ld_out, status, scratch);
+                                                 (T*)y, L.ld_out, status, scratch, (const T*)fext);
   cudaError_t e = cudaGetLastError();
   scratch_free(scratch, s);
   return (int)e;
@@ -286,32 +301,44 @@ int launch_task_t(const Launch& L, const void* q, const TaskShared& P, void* y0,
 
 template <class Op>
 int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
-              int32_t* status) {
-  return L.dtype == 0 ? launch_t<Op, double>(L, x0, x1, x2, g3, y, status)
-                      : launch_t<Op, float>(L, x0, x1, x2, g3, y, status);
+              int32_t* status, const void* fext = nullptr) {
+  return L.dtype == 0 ? launch_t<Op, double>(L, x0, x1, x2, g3, y, status, fext)
+                      : launch_t<Op, float>(L, x0, x1, x2, g3, y, status, fext);
 }
 
 }  // namespace
 
-int launch_gen_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* qdd,
-                   int32_t* status) {
-  if (L.spec == kChain7)
+int launch_gen_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3,
+                   const void* fext, void* qdd, int32_t* status) {
+  if (L.spec == kChain7) {
+    if (fext)
+      return L.dtype == 0 ? launch_t<GenChain7::AbaFext, double>(L, q, qd, tau, g3, qdd, status, fext)
+                          : launch_t<GenChain7::AbaFext, float>(L, q, qd, tau, g3, qdd, status, fext);
     return L.dtype == 0 ? launch_t<GenChain7::Aba, double>(L, q, qd, tau, g3, qdd, status)
                         : launch_t<GenChain7::Aba, float>(L, q, qd, tau, g3, qdd, status);
+  }
   if (L.spec != kTree29) return -1;
   // fp32: the mixed-precision routine (floating-base trunk in fp64)
+  if (fext)
+    return L.dtype == 0 ? launch_t<GenTree29::AbaFext, double>(L, q, qd, tau, g3, qdd, status, fext)
+                        : launch_t<GenTree29::AbaMixedFext, float>(L, q, qd, tau, g3, qdd, status, fext);
   return L.dtype == 0 ? launch_t<GenTree29::Aba, double>(L, q, qd, tau, g3, qdd, status)
                       : launch_t<GenTree29::AbaMixed, float>(L, q, qd, tau, g3, qdd, status);
 }
 
 template <class R>
 int gen_rnea_t(const Launch& L, int mode, const void* q, const void* qd, const void* qdd, const double* g3,
-               void* tau) {
+               const void* fext, void* tau) {
   // mode 0 full, 1 bias (q̈ = 0), 2 gravity (q̇ = q̈ = 0), 3 Coriolis (q̈ = 0, g = 0);
   // a NULL q̇ / q̈ means zeros, as in the template kernels
   static const double zero3[3] = {0, 0, 0};
   const bool has_qd = mode != 2 && qd, has_qdd = mode == 0 && qdd;
   const double* g = mode == 3 ? zero3 : g3;
+  if (fext) {  // f_ext variants: full RNEA and the bias term
+    if (has_qd && has_qdd) return launch_op<typename R::RneaFext>(L, q, qd, qdd, g, tau, nullptr, fext);
+    if (has_qd && mode == 1) return launch_op<typename R::RneaBiasFext>(L, q, qd, nullptr, g, tau, nullptr, fext);
+    return -1;
+  }
   if (has_qd && has_qdd) return launch_op<typename R::Rnea>(L, q, qd, qdd, g, tau, nullptr);
   if (has_qd) return launch_op<typename R::RneaBias>(L, q, qd, nullptr, g, tau, nullptr);
   if (!has_qdd) return launch_op<typename R::RneaGrav>(L, q, nullptr, nullptr, g, tau, nullptr);
@@ -319,9 +346,9 @@ int gen_rnea_t(const Launch& L, int mode, const void* q, const void* qd, const v
 }
 
 int launch_gen_rnea(const Launch& L, int mode, const void* q, const void* qd, const void* qdd, const double* g3,
-                    void* tau) {
-  if (L.spec == kTree29) return gen_rnea_t<GenTree29>(L, mode, q, qd, qdd, g3, tau);
-  if (L.spec == kChain7) return gen_rnea_t<GenChain7>(L, mode, q, qd, qdd, g3, tau);
+                    const void* fext, void* tau) {
+  if (L.spec == kTree29) return gen_rnea_t<GenTree29>(L, mode, q, qd, qdd, g3, fext, tau);
+  if (L.spec == kChain7) return gen_rnea_t<GenChain7>(L, mode, q, qd, qdd, g3, fext, tau);
   return -1;
 }
 

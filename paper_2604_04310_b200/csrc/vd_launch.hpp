@@ -56,10 +56,10 @@ int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, 
                void* qdd, int32_t* status);
 // Generated straight-line kernel (vd_inst_gen.cu) when one exists for L.spec;
 // -1 when not applicable.
-int launch_gen_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* qdd,
-                   int32_t* status);
+int launch_gen_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3,
+                   const void* fext, void* qdd, int32_t* status);
 int launch_gen_rnea(const Launch& L, int mode, const void* q, const void* qd, const void* qdd, const double* g3,
-                    void* tau);
+                    const void* fext, void* tau);
 int launch_gen_crba(const Launch& L, const void* q, void* M);
 int launch_gen_crba_packed(const Launch& L, const void* q, void* Mp);
 int launch_gen_fk(const Launch& L, const void* q, void* frames);

@@ -20,8 +20,10 @@ struct HostCx {
   const double* P = nullptr;
   T* Y1 = nullptr;
   const T* DX[3] = {nullptr, nullptr, nullptr};  // JVP tangents (NULL = 0)
+  const T* FX = nullptr;                         // external wrenches, plane 6 j + k
   T x(int g, int j) const { return X[g] ? X[g][j * ld + i] : T(0); }
   T dx(int g, int j) const { return DX[g] ? DX[g][j * ld + i] : T(0); }
+  T fx(int k) const { return FX[k * ld + i]; }
   void prefetch(int, int) const {}
   void fetch_next(int) const {}
   template <int K>
@@ -52,11 +54,12 @@ struct HostCx {
   bool want_lambda() const { return Y1 != nullptr; }
 };
 template <class Op, class T>
-int run(long N, const void* const* x, const double* g, void* y, int* status) {
+int run(long N, const void* const* x, const double* g, void* y, int* status, const void* fext = nullptr) {
   std::vector<T> slots(Op::kSlots + 1);
   int bad = 0;
   for (long i = 0; i < N; ++i) {
     HostCx<T> cx{{(const T*)x[0], (const T*)x[1], (const T*)x[2]}, g, (T*)y, N, i, slots.data()};
+    cx.FX = (const T*)fext;
     const bool ok = Op::template run<T>(cx);
     status[i] = ok ? 0 : 7;
     bad += !ok;
@@ -64,8 +67,13 @@ int run(long N, const void* const* x, const double* g, void* y, int* status) {
   return bad;
 }
 template <class R, class T>
-int run_op(int op, long N, const void* const* x, const double* g, void* y, int* status) {
+int run_op(int op, long N, const void* const* x, const double* g, void* y, int* status, const void* fext = nullptr) {
   switch (op) {
+    case 8: return run<typename R::RneaFext, T>(N, x, g, y, status, fext);
+    case 9: return run<typename R::RneaBiasFext, T>(N, x, g, y, status, fext);
+    case 10:
+      if constexpr (sizeof(T) == 4) return run<typename R::AbaMixedFext, T>(N, x, g, y, status, fext);
+      else return run<typename R::AbaFext, T>(N, x, g, y, status, fext);
     case 0:  // fp32: the mixed-precision routine the device uses
       if constexpr (sizeof(T) == 4) return run<typename R::AbaMixed, T>(N, x, g, y, status);
       else return run<typename R::Aba, T>(N, x, g, y, status);
@@ -175,4 +183,15 @@ extern "C" int gen_run_host(int robot, int op, int f32, long N, const void* x0, 
                : run_op<vdk::GenTree29, double>(op, N, x, g, y, status);
   return f32 ? run_op<vdk::GenChain7, float>(op, N, x, g, y, status)
              : run_op<vdk::GenChain7, double>(op, N, x, g, y, status);
+}
+
+// op: 8 rnea + f_ext, 9 bias + f_ext, 10 aba + f_ext (fp32: the mixed-precision routine); fext: 6n planes
+extern "C" int gen_run_fext_host(int robot, int op, int f32, long N, const void* x0, const void* x1, const void* x2,
+                                 const void* fext, const double* g, void* y, int* status) {
+  const void* x[3] = {x0, x1 ? x1 : x0, x2 ? x2 : x0};
+  if (robot == 2)
+    return f32 ? run_op<vdk::GenTree29, float>(op, N, x, g, y, status, fext)
+               : run_op<vdk::GenTree29, double>(op, N, x, g, y, status, fext);
+  return f32 ? run_op<vdk::GenChain7, float>(op, N, x, g, y, status, fext)
+             : run_op<vdk::GenChain7, double>(op, N, x, g, y, status, fext);
 }

@@ -279,3 +279,47 @@ def test_generated_task_routines_match_oracle(genlib, frame):
     w = np.zeros((N, 1), order="F")
     assert genlib.gen_task_host(2, fj, N, _p(Q), _p(P), _p(w), None, _p(st)) == 0
     assert rel_err(w[:, 0], om.manipulability(q, frame)) <= 1e-10
+
+
+def _run_fext(L, robot, op, xs, fext, nout, g=(0.0, 0.0, 9.81), f32=False):
+    """op: 8 rnea + f_ext, 9 bias + f_ext, 10 aba + f_ext (gen_host.cpp); fext (N, n, 6)."""
+    dt = np.float32 if f32 else np.float64
+    X = [np.asfortranarray(a.astype(dt)) for a in xs]
+    N, n = X[0].shape
+    F = np.asfortranarray(fext.reshape(N, 6 * n).astype(dt))  # plane 6 j + k
+    Y = np.zeros((N, nout), dtype=dt, order="F")
+    st = np.zeros(N, dtype=np.int32)
+    ptrs = [_p(a) for a in X] + [None] * (3 - len(X))
+    ga = np.asarray(g, dtype=np.float64)
+    L.gen_run_fext_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 7
+    bad = L.gen_run_fext_host(robot, op, int(f32), N, *ptrs, _p(F), _p(ga), _p(Y), _p(st))
+    return Y.astype(np.float64), st, bad
+
+
+@pytest.mark.parametrize("name,code", [("chain7", 1), ("tree29", 2)])
+@pytest.mark.parametrize("f32", [False, True])
+def test_generated_fext_routines_match_oracle(genlib, name, code, f32):
+    """External wrenches (ExternalForcesT, dynamics.hpp:52-81, subtracted at
+    243-245) in the generated RNEA, bias and ABA routines against the
+    oracle on random world-frame wrenches and a non-standard gravity."""
+    om = Model.builtin(name)
+    N = 1024
+    q, qd, qdd, tau = om.random_states(N, 4040 + code, True, True)
+    rng = np.random.default_rng(7 + code)
+    fext = rng.uniform(-5.0, 5.0, size=(N, om.n, 6))
+    g = (0.2, -0.1, 9.5)
+    tol = 1e-4 if f32 else 1e-10
+    got, _, bad = _run_fext(genlib, code, 8, (q, qd, qdd), fext, om.n, g=g, f32=f32)
+    assert bad == 0
+    assert rel_err(got, om.rnea(q, qd, qdd, gravity=g, fext=fext), axis=1).max() <= tol
+    got, _, _ = _run_fext(genlib, code, 9, (q, qd), fext, om.n, g=g, f32=f32)
+    assert rel_err(got, om.rnea(q, qd, np.zeros_like(q), gravity=g, fext=fext), axis=1).max() <= tol
+    got, st, bad = _run_fext(genlib, code, 10, (q, qd, tau), fext, om.n, g=g, f32=f32)
+    assert bad == 0
+    ref, rst = om.forward_dynamics(q, qd, tau, gravity=g, fext=fext)
+    assert np.all(rst == 0)
+    err = rel_err(got, ref, axis=1)
+    cond = np.linalg.cond(om.crba(q))
+    eps = np.finfo(np.float32 if f32 else np.float64).eps
+    assert err[cond < 1e5].max(initial=0) <= tol
+    assert np.all(err <= np.maximum(tol, om.n * eps * cond))

@@ -604,7 +604,37 @@ class Algo:
         return self
 
 
-def gen_aba(rb, hp=(), tau_prologue=False, dual=False):
+def world_of(g, X, Wp):
+    """World transform (R row-major 9, p 3) of joint X's body from its
+    parent's (kinematics.hpp:43-56): local R = QO·QJ, p = tO + QO·tJ."""
+    Rl = [g.dot(X.QO[3 * r:3 * r + 3], [X.QJ[c], X.QJ[3 + c], X.QJ[6 + c]]) for r in range(3) for c in range(3)]
+    pl = g.vadd(X.tO, g.matvec(X.QO, X.tJ))
+    if Wp is None:
+        return Rl, pl
+    R = [g.dot(Wp[0][3 * r:3 * r + 3], [Rl[c], Rl[3 + c], Rl[6 + c]]) for r in range(3) for c in range(3)]
+    return R, g.vadd(g.matvec(Wp[0], pl), Wp[1])
+
+
+def world_of_parent(g, X, W):
+    """The parent's world transform rebuilt from the child's (W_p = W ∘ X⁻¹),
+    so a DFS keeps only the current root->leaf transform live (as the
+    velocities: v_p = X(v − S q̇))."""
+    Rl = [g.dot(X.QO[3 * r:3 * r + 3], [X.QJ[c], X.QJ[3 + c], X.QJ[6 + c]]) for r in range(3) for c in range(3)]
+    pl = g.vadd(X.tO, g.matvec(X.QO, X.tJ))
+    Rp = [g.dot(W[0][3 * r:3 * r + 3], Rl[3 * c:3 * c + 3]) for r in range(3) for c in range(3)]  # R Rlᵀ
+    return Rp, g.vsub(W[1], g.matvec(Rp, pl))
+
+
+def fext_body(g, W, i):
+    """External wrench on joint i (world Plücker about the origin, fext plane
+    6i + k, ExternalForcesT dynamics.hpp:52-81) in body i coordinates:
+    inverse_transform_force (spatial.hpp:249-254), n_b = Rᵀ(n − p × f), f_b = Rᵀ f."""
+    fw = [g.tmp(f"cx.fx({6 * i + k})", "fx") for k in range(6)]
+    R, p = W
+    return g.matTvec(R, g.vsub(fw[:3], g.cross3(p, fw[3:]))) + g.matTvec(R, fw[3:])
+
+
+def gen_aba(rb, hp=(), tau_prologue=False, dual=False, fext=False):
     """ABA (Featherstone RBDA Table 7.1; oracle forward_dynamics,
     dynamics.hpp:421-444).  x(0) = q, x(1) = q̇, x(2) = τ; y(0, i) = q̈_i.
 
@@ -614,7 +644,12 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False):
 
     hp: joints whose steps are computed (and whose slots are stored) in double
     when T is float — mixed precision for the floating-base trunk, where the
-    whole tree's articulated inertia is projected."""
+    whole tree's articulated inertia is projected.
+
+    fext: external wrenches (cx.fx, world Plücker, ExternalForcesT), applied
+    as p^A_i = v×*Iv − ⁱX₀* f_i (RBDA Table 7.1; oracle aba_loop, subtracted
+    like dynamics.hpp:243-245); the world transform rides the DFS like the
+    velocity (forward on the way down, rebuilt from the child on the way up)."""
     # tau_prologue: τ loaded with q, q̇ up front into slots (faster for the
     # fp32 routine; for fp64 those 29 slots displace pass-2 state from shared
     # memory and it measured slower, so τ is read at each joint's pass-2 step)
@@ -626,14 +661,15 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False):
     def ty(i):
         g.ty = "TD" if i in A.hp else "T"
 
-    def down_up(i, vp):
+    def down_up(i, vp, Wp=None):
         ty(i)
         X = A.joint(i)
         qdi = A.load(A.qdrefs[i])
         v = X.S(qdi) if vp is None else g.vadd(X.motion_to_child(vp), X.S(qdi))
+        W = world_of(g, X, Wp) if fext else None
         acc = None
         for c in rb.children[i]:
-            (Ic, pc), v = down_up(c, v)
+            (Ic, pc), v, W = down_up(c, v, W)
             acc = (Ic, pc) if acc is None else (g.ai_add(acc[0], Ic), g.vadd(acc[1], pc))
         ty(i)
         if rb.children[i]:  # re-read instead of keeping them live across the subtree
@@ -642,6 +678,8 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False):
         b = rb.rb(i)
         IA = g.ai_from_rb(b)
         pA = g.crf(v, g.rb_apply(b, v))
+        if fext:
+            pA = g.vsub(pA, fext_body(g, W, i))
         if acc is not None:
             IA = g.ai_add(IA, acc[0])
             pA = g.vadd(pA, acc[1])
@@ -655,7 +693,7 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False):
         ud = g.mul(u, dinv)
         layout[i] = (A.store(ud), [A.store(x) for x in Ud])
         if vp is None:
-            return None, None
+            return None, None, None
         c = g.crm(v, X.S(qdi))
         ir, ic = (0, 1, 2, 0, 0, 1), (0, 1, 2, 1, 2, 2)  # Ia = IA − U Udᵀ
         Ia = {"A": [g.sub(IA["A"][k], g.mul(U[ir[k]], Ud[ic[k]])) for k in range(6)],
@@ -663,7 +701,8 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False):
               "B": [g.sub(IA["B"][3 * r + cc], g.mul(U[r], Ud[3 + cc])) for r in range(3) for cc in range(3)]}
         pa = g.vadd(g.vadd(pA, g.ai_apply(Ia, c)), [g.mul(x, ud) for x in U])
         vpar = X.motion_to_parent(g.vsub(v, X.S(qdi)))
-        return (X.ai_to_parent(Ia), X.force_to_parent(pa)), vpar
+        Wpar = world_of_parent(g, X, W) if fext else None
+        return (X.ai_to_parent(Ia), X.force_to_parent(pa)), vpar, Wpar
 
     for r in rb.roots:
         down_up(r, None)
@@ -695,17 +734,20 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False):
     return A.finish()
 
 
-def gen_rnea(rb, with_qd, with_qdd, dual=False):
+def gen_rnea(rb, with_qd, with_qdd, dual=False, fext=False):
     """RNEA (rnea_loop, dynamics.hpp:272-327; Alg. 1 of PAPER.md:141-151):
     x(0) = q, x(1) = q̇ (if with_qd), x(2) = q̈ (if with_qdd); y(0, i) = τ_i.
     with_qdd = False is the bias term c + g (dynamics.hpp:434-435), with_qd =
     False as well the gravity term (dynamics.hpp:403-408).  One DFS: v, a and
-    the body's own force on the way down, Σ child forces and τ on the way up."""
+    the body's own force on the way down, Σ child forces and τ on the way up.
+    fext: f_i −= ⁱX₀* f_ext,i (dynamics.hpp:243-245, rnea_loop 316-318), the
+    world transform carried down the DFS and rebuilt from the child between
+    siblings."""
     A = Algo(rb, with_qd, extra=(2,) if with_qdd else (), dual=dual)
     g = A.g
     gvec = A.gravity()
 
-    def rec(i, vp, ap):
+    def rec(i, vp, ap, Wp=None):
         X = A.joint(i)
         qdi = A.load(A.qdrefs[i]) if with_qd else ZERO
         qddi = A.load(A.xrefs[(2, i)]) if with_qdd else ZERO
@@ -717,13 +759,20 @@ def gen_rnea(rb, with_qd, with_qdd, dual=False):
             a = g.vadd(g.vadd(X.motion_to_child(ap), g.crm(v, X.S(qdi))), X.S(qddi))
         b = rb.rb(i)
         f = g.vadd(g.rb_apply(b, a), g.crf(v, g.rb_apply(b, v)))
+        W = None
+        if fext:
+            W = world_of(g, X, Wp)
+            f = g.vsub(f, fext_body(g, W, i))
         for c in rb.children[i]:
-            f = g.vadd(f, rec(c, v, a))
+            fc, W = rec(c, v, a, W)
+            f = g.vadd(f, fc)
         if rb.children[i]:
             X = A.joint(i)
         tau = X.Sdot(f)
         g.output(0, i, tau)
-        return X.force_to_parent(f) if vp is not None else None
+        if vp is None:
+            return None, None
+        return X.force_to_parent(f), (world_of_parent(g, X, W) if fext else None)
 
     for r in rb.roots:
         rec(r, None, None)
@@ -1456,6 +1505,11 @@ OPS = [("Aba", gen_aba, lambda rb: rb.n, 3),
        ("Rnea", lambda rb: gen_rnea(rb, True, True), lambda rb: rb.n, 3),
        ("RneaBias", lambda rb: gen_rnea(rb, True, False), lambda rb: rb.n, 2),
        ("RneaGrav", lambda rb: gen_rnea(rb, False, False), lambda rb: rb.n, 1),
+       # external wrenches (cx.fx planes): τ, bias and q̈ with f_ext (§8(f)3)
+       ("RneaFext", lambda rb: gen_rnea(rb, True, True, fext=True), lambda rb: rb.n, 3),
+       ("RneaBiasFext", lambda rb: gen_rnea(rb, True, False, fext=True), lambda rb: rb.n, 2),
+       ("AbaFext", lambda rb: gen_aba(rb, fext=True), lambda rb: rb.n, 3),
+       ("AbaMixedFext", lambda rb: gen_aba(rb, trunk(rb), tau_prologue=True, fext=True), lambda rb: rb.n, 3),
        ("Crba", gen_crba, lambda rb: rb.n * rb.n, 1),
        ("CrbaPacked", lambda rb: gen_crba(rb, packed=True), lambda rb: len(rb.lower_pattern()), 1),
        # forward-mode JVPs (autodiff.hpp:41-50 on dual.hpp scalars): value in
