@@ -61,12 +61,15 @@ ONE = K(1.0)
 
 
 # Model constants shared by every routine of the robot being generated.  An
-# fp64 literal costs two UMOVs per use in SASS; a __constant__ table entry
-# would be a c[bank][offset] operand instead, but inside the persistent loop
-# the compiler hoists those loads into registers and spills them (measured:
-# tree29 RNEA 0.14 -> 0.20 ms), so literals are the default (USE_POOL).
+# fp64 literal costs up to two UMOVs per use in SASS (12 % of the G1 ABA's
+# instructions); a __constant__ table read in C++ is hoisted out of the
+# persistent loop into registers and spilled (round 1: tree29 RNEA 0.14 ->
+# 0.20 ms).  VD_GEN_POOL=asm emits one opaque `ld.const` per use instead
+# (LDCU.128 into uniform registers, two constants per instruction); round 2,
+# tools/async_sweep.cu: G1 ABA 0.294 -> 0.290 ms, G1 RNEA 0.099 -> 0.116,
+# Panda ABA 0.539 -> 0.571, G1 OSC 0.61 -> 0.67 ms.  Literals stay the default.
 POOL = {}
-USE_POOL = False
+USE_POOL = os.environ.get("VD_GEN_POOL", "") == "asm"
 
 
 def _low32_zero(c):
@@ -97,7 +100,7 @@ class Gen:
             return f"{t}({float.hex(c)})"
         if c not in POOL:
             POOL[c] = len(POOL)
-        return f"kc<T>({POOL[c]})"
+        return f"kc<T, {POOL[c]}>()"
 
     def o(self, a):
         return a.s if a.c is None else self.lit(a.c)
@@ -1529,19 +1532,29 @@ def emit(name, cls, rb):
     dv = ", ".join(float.hex(c) for c in vals) or "0.0"
     fv = ", ".join(float.hex(struct.unpack("<f", struct.pack("<f", c))[0]) + "f" for c in vals) or "0.0f"
     n = max(1, len(vals))
+    # Constant pool (USE_POOL): one __constant__ table per robot, read with an
+    # opaque ld.const per use so the compiler cannot hoist every constant of
+    # the routine out of the persistent loop into registers.  C linkage: the
+    # asm names the table; the header is included by one translation unit
+    # per binary.
     pre = [f"// ---- {name}: {len(vals)} model constants",
            "#if defined(__CUDACC__)",
-           f"static __constant__ double vd_kd_{name}[{n}] = {{{dv}}};",
-           f"static __constant__ float vd_kf_{name}[{n}] = {{{fv}}};",
+           f'extern "C" {{ __constant__ double vd_kd_{name}[{n}] = {{{dv}}}; }}',
+           f'extern "C" {{ __constant__ float vd_kf_{name}[{n}] = {{{fv}}}; }}',
            "#endif",
            f"static const double vd_hkd_{name}[{n}] = {{{dv}}};",
            f"static const float vd_hkf_{name}[{n}] = {{{fv}}};"]
-    kc = ["  template <class T>",
-          "  VD_HD static T kc(int i) {",
+    kc = ["  template <class T, int I>",
+          "  VD_HD static T kc() {",
           "#if defined(__CUDA_ARCH__)",
-          f"    if constexpr (sizeof(T) == 8) return vd_kd_{name}[i]; else return vd_kf_{name}[i];",
+          "    T v;",
+          "    if constexpr (sizeof(T) == 8)",
+          f'      asm volatile("ld.const.f64 %0, [vd_kd_{name}+%1];" : "=d"(v) : "n"(I * 8));',
+          "    else",
+          f'      asm volatile("ld.const.f32 %0, [vd_kf_{name}+%1];" : "=f"(v) : "n"(I * 4));',
+          "    return v;",
           "#else",
-          f"    if constexpr (sizeof(T) == 8) return vd_hkd_{name}[i]; else return vd_hkf_{name}[i];",
+          f"    if constexpr (sizeof(T) == 8) return vd_hkd_{name}[I]; else return vd_hkf_{name}[I];",
           "#endif",
           "  }"]
     return pre + body[:4] + kc + body[4:]
