@@ -1557,6 +1557,8 @@ def emit(name, cls, rb):
           f"    if constexpr (sizeof(T) == 8) return vd_hkd_{name}[I]; else return vd_hkf_{name}[I];",
           "#endif",
           "  }"]
+    if not USE_POOL:  # literals only: no table, no accessor
+        return body
     return pre + body[:4] + kc + body[4:]
 
 
