@@ -258,6 +258,19 @@ struct JvpCfg {
   static constexpr int kMinB = sizeof(T) == 4 && Op::kSlots <= 110 ? 3 : 2;
 };
 
+// G1 ABA-JVP (526 slots): one CTA/SM with 220 shared slots keeps the scratch
+// slab in L2 (async_sweep "jvp", 262144 states: fp64 r40 s110 b2 1.50 ->
+// r40 s220 b1 1.24 ms; fp32 s220 b2 0.72 -> r40 s220 b2 0.64 ms); G1 fp32
+// RNEA-JVP s220 b2 0.27 -> s144 b3 0.25 ms.
+template <class T>
+struct JvpCfg<GenTree29::AbaJvp, T> {
+  static constexpr int kReg = 40, kSmem = 220, kMinB = sizeof(T) == 8 ? 1 : 2;
+};
+template <>
+struct JvpCfg<GenTree29::RneaJvp, float> {
+  static constexpr int kReg = 0, kSmem = 144, kMinB = 3;
+};
+
 template <class Op, class T, bool kStream>
 int launch_jvp_v(const Launch& L, const JvpArgs& a) {
   using C = JvpCfg<Op, T>;

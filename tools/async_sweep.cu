@@ -283,6 +283,17 @@ int main(int argc, char** argv) {
     jvp<GenTree29::CrbaJvp, float, 0, 110, 3>("t29 crbajvp f32 s110 b3", N29, (float*)xj, (float*)yj, sf, cap);
     jvp<GenTree29::FkJvp, float, 0, 110, 2>("t29 fkjvp f32 s110 b2", N29, (float*)xj, (float*)yj, sf, cap);
     jvp<GenTree29::FkJvp, float, 0, 110, 3>("t29 fkjvp f32 s110 b3", N29, (float*)xj, (float*)yj, sf, cap);
+    jvp<GenTree29::AbaJvp, double, 40, 110, 2>("t29 abajvp f64 r40 s110 b2", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::AbaJvp, double, 40, 220, 1>("t29 abajvp f64 r40 s220 b1", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::AbaJvp, double, 60, 110, 2>("t29 abajvp f64 r60 s110 b2", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::AbaJvp, double, 0, 55, 3>("t29 abajvp f64 r0 s55 b3", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::AbaJvp, float, 0, 220, 2>("t29 abajvp f32 s220 b2", N29, (float*)xj, (float*)yj, sf, cap);
+    jvp<GenTree29::AbaJvp, float, 40, 220, 2>("t29 abajvp f32 r40 s220 b2", N29, (float*)xj, (float*)yj, sf, cap);
+    jvp<GenTree29::AbaJvp, float, 0, 144, 3>("t29 abajvp f32 s144 b3", N29, (float*)xj, (float*)yj, sf, cap);
+    jvp<GenTree29::RneaJvp, double, 40, 110, 2>("t29 rneajvp f64 r40 s110 b2", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::RneaJvp, double, 40, 55, 3>("t29 rneajvp f64 r40 s55 b3", N29, xj, yj, scratch, cap);
+    jvp<GenTree29::RneaJvp, float, 0, 220, 2>("t29 rneajvp f32 s220 b2", N29, (float*)xj, (float*)yj, sf, cap);
+    jvp<GenTree29::RneaJvp, float, 0, 144, 3>("t29 rneajvp f32 s144 b3", N29, (float*)xj, (float*)yj, sf, cap);
     jvp<GenChain7::AbaJvp, double, 40, 89, 2>("c7 abajvp f64 r40 s89 b2", 1048576, xj, yj, scratch, cap);
     jvp<GenChain7::AbaJvp, double, 40, 40, 3>("c7 abajvp f64 r40 s40 b3", 1048576, xj, yj, scratch, cap);
     jvp<GenChain7::AbaJvp, double, 64, 65, 2>("c7 abajvp f64 r64 s65 b2", 1048576, xj, yj, scratch, cap);
