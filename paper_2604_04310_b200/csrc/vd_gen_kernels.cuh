@@ -16,7 +16,7 @@
 
 #include <cuda_runtime.h>
 
-#include "vd_gen_robots.cuh"
+#include "vd_gen_prelude.cuh"
 #include "vd_launch.hpp"
 #include "vd_shared.hpp"
 

@@ -1,0 +1,75 @@
+// Shared prelude of the generated straight-line routines (vd_gen_robots.cuh
+// and the per-model JIT translation units): scalar helpers the emitted code
+// calls.  Hand-maintained; tools/gen_tree_kernels.py emits only the robot
+// structs.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+#include "vd_sincos.cuh"
+
+#ifndef VD_HD
+#if defined(__CUDACC__)
+#define VD_HD __host__ __device__ __forceinline__
+#else
+#define VD_HD inline
+#endif
+#endif
+
+namespace vdk {
+
+template <class T> VD_HD T vd_sqrt(T x) { using std::sqrt; return sqrt(x); }
+// rotation_log (control.hpp:45-68), the reference acos form and branches
+template <class T>
+VD_HD void vd_rotation_log(const T* R, T* w) {
+  using std::acos; using std::sin; using std::sqrt;
+  const T tr = R[0] + R[4] + R[8];
+  const T anti[3] = {R[7] - R[5], R[2] - R[6], R[3] - R[1]};
+  T ca = T(0.5) * (tr - T(1));
+  ca = ca < T(-1) ? T(-1) : (ca > T(1) ? T(1) : ca);
+  const T ang = acos(ca);
+  const T pi = T(3.14159265358979323846);
+  if (ang < T(1e-9)) {
+    for (int k = 0; k < 3; ++k) w[k] = T(0.5) * anti[k];
+    return;
+  }
+  if (ang > pi - T(1e-6)) {
+    const T sd[3] = {T(0.5) * (R[0] + T(1)), T(0.5) * (R[4] + T(1)), T(0.5) * (R[8] + T(1))};
+    int k = 0;
+    if (sd[1] > sd[k]) k = 1;
+    if (sd[2] > sd[k]) k = 2;
+    T ax[3];
+    for (int r = 0; r < 3; ++r) ax[r] = (r == k) ? sd[k] : T(0.5) * R[r * 3 + k];
+    const T inv = T(1) / sqrt(sd[k] > T(1e-12) ? sd[k] : T(1e-12));
+    for (int r = 0; r < 3; ++r) ax[r] *= inv;
+    const T nrm = sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+    for (int r = 0; r < 3; ++r) ax[r] /= nrm;
+    const T sgn = (anti[0] * ax[0] + anti[1] * ax[1] + anti[2] * ax[2]) < T(0) ? T(-1) : T(1);
+    for (int r = 0; r < 3; ++r) w[r] = ang * sgn * ax[r];
+    return;
+  }
+  const T f = T(0.5) * ang / sin(ang);
+  for (int k = 0; k < 3; ++k) w[k] = f * anti[k];
+}
+
+#if defined(__CUDA_ARCH__)
+// library sincos here: vd_sincos_f64's __constant__ coefficients get hoisted out of the persistent
+// loop into registers and spilled in these 168/255-register kernels (measured slower)
+__device__ __forceinline__ void vd_sincos(double x, double* s, double* c) { sincos(x, s, c); }
+__device__ __forceinline__ void vd_sincos(float x, float* s, float* c) { sincosf(x, s, c); }
+template <class T> __device__ __forceinline__ bool vd_isfinite(T x) { return isfinite(x); }
+#else
+template <class T> inline void vd_sincos(T x, T* s, T* c) { *s = std::sin(x); *c = std::cos(x); }
+template <class T> inline bool vd_isfinite(T x) { return std::isfinite(x); }
+#endif
+// Cx::kFastTrig selects vd_sincos_f64 (vd_sincos.cuh) for fp64 on the device
+template <class Cx, class T>
+VD_HD void vd_sincos_cx(T x, T* s, T* c) {
+#if defined(__CUDA_ARCH__)
+  if constexpr (Cx::kFastTrig && sizeof(T) == 8) { vd_sincos_f64(x, s, c); return; }
+#endif
+  vd_sincos(x, s, c);
+}
+
+}  // namespace vdk

@@ -10,32 +10,11 @@
 #include <type_traits>
 #include <utility>
 
-#include "vd_gen_kernels.cuh"
-#include "vd_launch.hpp"
+#include "vd_gen_robots.cuh"
+#include "vd_gen_launch.cuh"
 
 namespace vdk {
-namespace {
 
-// Slot placement and CTAs/SM per (op, dtype), from ablib/gen_sweep*.cu on a
-// B200 (kReg: last slots kept in registers; kSmem: first slots in shared
-// memory; the rest in the L2-resident scratch slab).
-template <class Op, class T>
-struct Cfg {
-  static constexpr int kReg = 0, kSmem = Op::kSlots < 55 ? Op::kSlots : 55, kMinB = sizeof(T) == 8 ? 3 : 4;
-  static constexpr bool kFast = false;  // vd_sincos_f64 instead of the library sincos
-};
-// kStream (GenCx): evict-first state I/O; false unless a Cfg sets it
-template <class C, class = void>
-struct StreamIo : std::false_type {};
-template <class C>
-struct StreamIo<C, std::void_t<decltype(C::kStream)>> : std::bool_constant<C::kStream> {};
-// kAsync (k_gen_async): the next state's inputs are prefetched into shared
-// memory with cp.async while the current one is computed; false unless a Cfg
-// sets it
-template <class C, class = void>
-struct AsyncIo : std::false_type {};
-template <class C>
-struct AsyncIo<C, std::void_t<decltype(C::kAsync)>> : std::bool_constant<C::kAsync> {};
 // The headline kernel, N = 4M states (tools/async_sweep.cu, one B200):
 // plain k_gen r44 s28 b4 0.599 ms; async r30 s35 b4 0.555, + evict-first
 // 0.548, r24 s41 (3 CTAs/SM) 0.543 ms; the templated TMA kernel 0.61 ms.
@@ -137,74 +116,7 @@ struct Cfg<GenTree29::AbaFext, double> : Cfg<GenTree29::Aba, double> {};
 template <>
 struct Cfg<GenTree29::AbaMixedFext, float> : Cfg<GenTree29::AbaMixed, float> {};
 
-struct Occ {
-  int blocks_per_sm = 0, sms = 0;
-};
-
-inline bool debug_launches() {
-  static const bool on = std::getenv("VD_DEBUG_LAUNCH") != nullptr;
-  return on;
-}
-
-// Occupancy (and the dynamic shared-memory opt-in) once per device for each
-// kernel instantiation; keyed by <Op, T>, not by the kernel's function type
-// (all variants of one dtype share it).
-template <class Op, class T, class Kern>
-Occ occupancy(Kern kern, size_t smem) {
-  static std::mutex mu;
-  static Occ occ[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  Occ& c = occ[dev & 63];
-  if (!c.blocks_per_sm) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.blocks_per_sm, kern, kGenBlock, smem);
-    if (c.blocks_per_sm < 1) c.blocks_per_sm = 1;
-  }
-  return c;
-}
-
-// The kernel a Cfg selects (only that one is instantiated).
-template <class Op, class T, class C>
-constexpr auto gen_kernel() {
-  if constexpr (AsyncIo<C>::value)
-    return k_gen_async<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
-  else
-    return k_gen<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
-}
-
-template <class Op, class T>
-int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
-             int32_t* status, const void* fext = nullptr) {
-  using C = Cfg<Op, T>;
-  constexpr bool kAsync = AsyncIo<C>::value;
-  auto kern = gen_kernel<Op, T, C>();
-  constexpr size_t smem = kAsync ? gen_async_smem<Op, T, C::kReg, C::kSmem>() : (size_t)C::kSmem * kGenBlock * sizeof(T);
-  const Occ o = occupancy<Op, T>(kern, smem);
-  const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
-  cudaStream_t s = static_cast<cudaStream_t>(L.stream);
-  if (debug_launches())
-    std::fprintf(stderr, "[vd] k_gen slots %d reg %d smem %d: %d CTAs/SM x %d SMs, grid %lld, smem %zu B\n", Op::kSlots,
-                 C::kReg, C::kSmem, o.blocks_per_sm, o.sms, (long long)blocks, smem);
-  // L2-resident scratch for the slots that are neither in registers nor in
-  // shared memory: one slab per resident thread, stream-ordered from the
-  // library's private pool (scratch_alloc: no synchronisation, safe for
-  // concurrent streams, bounded caching).
-  const size_t scratch_bytes = (size_t)blocks * kGenBlock * gen_scratch_per_thread<Op, T, C::kReg, C::kSmem>() * sizeof(T);
-  T* scratch = nullptr;
-  if (scratch_bytes) {
-    if (int rc = scratch_alloc(reinterpret_cast<void**>(&scratch), scratch_bytes, s)) return rc;
-  }
-  // gravity3 == NULL: GravitySpec::standard() (dynamics.hpp:39-50), as g3_of
-  const T g0 = g3 ? T(g3[0]) : T(0), g1 = g3 ? T(g3[1]) : T(0), g2 = g3 ? T(g3[2]) : T(9.81);
-  kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, (const T*)x0, (const T*)x1, (const T*)x2, L.ld_in, g0, g1, g2,
-                                                 (T*)y, L.ld_out, status, scratch, (const T*)fext);
-  cudaError_t e = cudaGetLastError();
-  scratch_free(scratch, s);
-  return (int)e;
-}
+namespace {
 
 // OSC on branched trees: the articulated-body form (gen_osc_aba, ~255 slots
 // for a G1 hand/foot frame instead of the 486 of the M-based form).
@@ -310,13 +222,6 @@ int launch_task_t(const Launch& L, const void* q, const TaskShared& P, void* y0,
   kern<<<(unsigned)blocks, kGenBlock, smem, static_cast<cudaStream_t>(L.stream)>>>(
       L.N, (const T*)q, L.ld_in, P, (T*)y0, (T*)y1, L.ld_out, status, nullptr);
   return (int)cudaGetLastError();
-}
-
-template <class Op>
-int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
-              int32_t* status, const void* fext = nullptr) {
-  return L.dtype == 0 ? launch_t<Op, double>(L, x0, x1, x2, g3, y, status, fext)
-                      : launch_t<Op, float>(L, x0, x1, x2, g3, y, status, fext);
 }
 
 }  // namespace

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <cmath>
 #include <vector>
+#include "vd_gen_robots.cuh"
 #include "vd_gen_kernels.cuh"
 using namespace vdk;
 

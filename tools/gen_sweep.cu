@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <algorithm>
+#include "vd_gen_robots.cuh"
 #include "vd_gen_kernels.cuh"
 using namespace vdk;
 // -DSWEEP_STREAM=true: evict-first state I/O (GenCx kStream) for every k_gen entry
