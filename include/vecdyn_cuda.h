@@ -119,6 +119,16 @@ int vd_device_model_dof(vd_device_model dm);
 int vd_device_model_specialization(vd_device_model dm);
 /* Force the generic kernels even for builtin robots (testing / comparison). */
 int vd_device_model_set_generic(vd_device_model dm, int generic);
+/* Per-model JIT module (no reference analogue: the reference has no device
+ * code).  A model that is not one of the compile-time robots runs the loop
+ * kernels unless a module of its generated straight-line routines (ABA, RNEA,
+ * bias, gravity, Coriolis, CRBA, packed CRBA, FK; built by
+ * paper_2604_04310_b200/jit.py, `python -m paper_2604_04310_b200.jit model.urdf`)
+ * is attached: device models created from m afterwards use it.  Fails with
+ * VD_ERR_INVALID_ARGUMENT if the module was generated for a different model. */
+int vd_model_attach_jit(vd_model m, const char* module_path);
+/* 1 if calls on dm run a JIT module, 0 if not, -1 for a null handle */
+int vd_device_model_jit(vd_device_model dm);
 
 /* ------------------------------------------------------------------ batched kernels
  * gravity3: the base acceleration a_g = −field (GravitySpec::accel.linear,

@@ -306,12 +306,18 @@ class PostureGains:
 # ------------------------------------------------------------------ device model
 class DeviceModel:
     """The model packed and uploaded to one GPU (compile-time specialised when it
-    matches a builtin robot)."""
+    matches a builtin robot).  jit=True: for any other model, build (or reuse
+    the cached) per-model module of generated routines and attach it to the
+    model first (jit.py); ignored for the builtin robots."""
 
-    def __init__(self, model, device=0, generic=False):
+    def __init__(self, model, device=0, generic=False, jit=False):
         self.model = model
         self.device = int(device)
         self._lib = _lib.load()
+        if jit and self._lib.vdi_model_fingerprint(model.handle) not in _builtin_fingerprints():
+            from . import jit as _jit
+
+            _jit.attach(model)
         h = ctypes.c_void_p()
         _check(self._lib.vd_device_model_create(model.handle, self.device, ctypes.byref(h)))
         self._h = h
@@ -332,6 +338,20 @@ class DeviceModel:
 
     def specialization(self):
         return self._lib.vd_device_model_specialization(self._h)
+
+    def uses_jit(self):
+        """True when calls run the model's JIT module (jit.py)."""
+        return self._lib.vd_device_model_jit(self._h) == 1
+
+
+_BUILTIN_FP = None
+
+
+def _builtin_fingerprints():
+    global _BUILTIN_FP
+    if _BUILTIN_FP is None:
+        _BUILTIN_FP = {_lib.load().vdi_model_fingerprint(robots.by_name(n).handle) for n in ("chain7", "tree29")}
+    return _BUILTIN_FP
 
 
 def _torch():

@@ -76,6 +76,8 @@ SIGNATURES = {
     "vd_device_model_dof": (c_int, [P]),
     "vd_device_model_specialization": (c_int, [P]),
     "vd_device_model_set_generic": (c_int, [P, c_int]),
+    "vd_model_attach_jit": (c_int, [P, c_char_p]),
+    "vd_device_model_jit": (c_int, [P]),
     "vd_fk": (c_int, [P, c_int, c_int64, P, c_int64, P, c_int64, P]),
     "vd_fk_scan": (c_int, [P, c_int, c_int64, P, c_int64, P, c_int64, P]),
     "vd_jacobian": (c_int, [P, c_int, c_int64, P, c_int64, c_int, P, P, c_int64, P]),

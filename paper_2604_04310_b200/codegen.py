@@ -1581,12 +1581,20 @@ def emit(name, cls, rb):
     return pre + body[:4] + kc + body[4:]
 
 
-def emit_body(name, cls, rb):
+# the routines a per-model JIT module carries (paper_2604_04310_b200/jit.py):
+# the dynamics hot path; OSC, task-space and JVP calls stay on the loop kernels
+JIT_OPS = ("Aba", "AbaMixed", "Rnea", "RneaBias", "RneaGrav", "RneaFext", "RneaBiasFext", "AbaFext", "AbaMixedFext",
+           "Crba", "CrbaPacked", "Fk")
+
+
+def emit_body(name, cls, rb, ops=None, tasks=True):
     out = [f"// ---- {name}",
            f"struct Gen{cls} {{",
            f"  static constexpr int kN = {rb.n};",
            f"  static constexpr uint64_t kFingerprint = {rb.d['fp']:#x}ull;"]
     for op, fn, nout, nin in OPS:
+        if ops is not None and op not in ops:
+            continue
         A = fn(rb)
         out += [f"  // {op}: {A.g.flops} mul/add after folding; {A.nslot} slots, the first {A.nprologue} written by the prologue",
                 f"  struct {op} {{",
@@ -1600,6 +1608,8 @@ def emit_body(name, cls, rb):
                 "    VD_HD static bool run(Cx& cx) {"]
         out += ["    " + ln for ln in A.g.lines]
         out += ["    }", "  };"]
+    if not tasks:
+        return out + ["};", ""]
     # OSC per task-frame joint (the frame offset stays a runtime parameter):
     # one variant for every leaf joint (end effectors) and the joints that
     # carry a named frame of the model
@@ -1657,3 +1667,15 @@ def emit_body(name, cls, rb):
     out.append("  }")
     out += ["};", ""]
     return out
+
+
+def jit_source(lib, h, cls="Jit"):
+    """Translation unit of a per-model JIT module: the model's generated
+    routines (JIT_OPS) as struct Gen<cls>, then the C entry points of
+    csrc/vd_jit_entry.cuh over them."""
+    rb = Robot(packed_model(lib, h), frame_joints(lib, h))
+    lines = ["// GENERATED at model load by paper_2604_04310_b200/jit.py; do not edit.",
+             "#include \"vd_gen_launch.cuh\"", "", "namespace vdk {", ""]
+    lines += emit_body(f"jit {rb.d['fp']:#x}", cls, rb, ops=JIT_OPS, tasks=False)
+    lines += ["}  // namespace vdk", "", f"#define VD_JIT_ROBOT vdk::Gen{cls}", "#include \"vd_jit_entry.cuh\"", ""]
+    return "\n".join(lines), rb.d["fp"]

@@ -3,6 +3,7 @@
 // host batch path.  No CPU fallback exists: every numeric entry point runs
 // the sm_100a kernels or fails with VD_ERR_CUDA.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <cmath>
 #include <cstdio>
@@ -21,8 +22,18 @@
 #include "vd_host.hpp"
 #include "vd_launch.hpp"
 
+// A per-model JIT module (vd_jit_entry.cuh) loaded with dlopen.  Never
+// unloaded: launches may still be in flight on some stream when the last
+// model referencing it goes away.
+struct JitModule {
+  void* dl = nullptr;
+  uint64_t fp = 0;
+  vdk::JitLaunchFn launch = nullptr;
+};
+
 struct vd_model_s {
   vdh::Model m;
+  std::shared_ptr<JitModule> jit;  // vd_model_attach_jit
 };
 
 struct vd_device_model_s {
@@ -30,6 +41,7 @@ struct vd_device_model_s {
   int n = 0;
   int spec = 0;
   bool force_generic = false;
+  std::shared_ptr<JitModule> jit;  // the model's JIT module (models without compile-time kernels)
   vdh::PackedModel pm;
   // Host copies of the packed model; the generic kernels receive them by
   // value in their parameter space (__grid_constant__), so no device
@@ -146,6 +158,7 @@ vdk::Launch make_launch(vd_device_model dm, int dtype, int64_t N, int64_t ldi, i
   L.stream = stream;
   L.serial = true;
   for (int i = 0; i < dm->n; ++i) L.serial = L.serial && dm->pm.parent[i] == i - 1;
+  L.jit = (!dm->force_generic && dm->jit) ? dm->jit->launch : nullptr;
   return L;
 }
 int finish(int rc, const char* where) {
@@ -305,6 +318,7 @@ int vd_device_model_create(vd_model m, int device, vd_device_model* out) {
     dm->pm = vdh::pack(m->m);
     dm->n = dm->pm.n;
     dm->spec = vdk::match_spec(vdh::fingerprint(dm->pm), dm->pm.n);
+    if (dm->spec == vdk::kGeneric) dm->jit = m->jit;  // builtin robots keep their compiled-in kernels
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
@@ -325,6 +339,32 @@ void vd_device_model_destroy(vd_device_model dm) {
   delete dm;
 }
 int vd_device_model_dof(vd_device_model dm) { return dm ? dm->n : -1; }
+int vd_device_model_jit(vd_device_model dm) { return dm ? ((dm->jit && !dm->force_generic) ? 1 : 0) : -1; }
+
+int vd_model_attach_jit(vd_model m, const char* path) {
+  if (!m || !path) return set_error(VD_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&]() -> int {
+    void* dl = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+    if (!dl) return set_error(VD_ERR_INVALID_ARGUMENT, std::string("vd_model_attach_jit: ") + dlerror());
+    auto abi = reinterpret_cast<int (*)()>(dlsym(dl, "vdj_abi_version"));
+    auto fpf = reinterpret_cast<uint64_t (*)()>(dlsym(dl, "vdj_fingerprint"));
+    auto init = reinterpret_cast<void (*)(int (*)(void**, size_t, void*), void (*)(void*, void*))>(dlsym(dl, "vdj_init"));
+    auto launch = reinterpret_cast<vdk::JitLaunchFn>(dlsym(dl, "vdj_launch"));
+    if (!abi || !fpf || !init || !launch)
+      return set_error(VD_ERR_INVALID_ARGUMENT, "vd_model_attach_jit: not a vecdyn JIT module");
+    if (abi() != vdk::kJitAbi) return set_error(VD_ERR_INVALID_ARGUMENT, "vd_model_attach_jit: JIT ABI mismatch");
+    const uint64_t fp = vdh::fingerprint(vdh::pack(m->m));
+    if (fpf() != fp)
+      return set_error(VD_ERR_INVALID_ARGUMENT, "vd_model_attach_jit: module was generated for another model");
+    init(&vdk::scratch_alloc, &vdk::scratch_free);
+    auto jm = std::make_shared<JitModule>();
+    jm->dl = dl;
+    jm->fp = fp;
+    jm->launch = launch;
+    m->jit = std::move(jm);
+    return VD_OK;
+  });
+}
 int vd_device_model_specialization(vd_device_model dm) { return dm ? (dm->force_generic ? 0 : dm->spec) : -1; }
 int vd_device_model_set_generic(vd_device_model dm, int generic) {
   if (!dm) return set_error(VD_ERR_INVALID_ARGUMENT, "null device model");

@@ -61,8 +61,16 @@ void scratch_free(void* p, void* stream) {
 }
 int launch_jac_scan(const Launch& L, const void* q, const FrameArg& fr, void* pose, void* J);
 
+// The model's JIT module (vd_jit_entry.cuh), when one is attached; -1 when
+// there is none or it has no routine for the call.
+static int jit_call(const Launch& L, JitOp op, const void* x0, const void* x1, const void* x2, const double* g3,
+                    const void* fext, void* y, int32_t* status) {
+  return L.jit ? L.jit(op, &L, x0, x1, x2, g3, fext, y, status) : -1;
+}
+
 int launch_fk(const Launch& L, const void* q, void* out) {
   if (L.N == 0) return 0;
+  if (const int rc = jit_call(L, kJitFk, q, nullptr, nullptr, nullptr, nullptr, out, nullptr); rc >= 0) return rc;
   if (const int rc = launch_gen_fk(L, q, out); rc >= 0) return rc;
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::fk(mv, L, q, out); });
 }
@@ -93,12 +101,17 @@ int launch_rnea(const Launch& L, int mode, const void* q, const void* qd, const 
   const double* g = (mode == 3) ? zero3 : g3;
   const void* qd_ = (mode == 2) ? nullptr : qd;
   const void* qdd_ = (mode == 0) ? qdd : nullptr;
+  {
+    static const JitOp ops[4] = {kJitRnea, kJitBias, kJitGravity, kJitCoriolis};
+    if (const int rc = jit_call(L, ops[mode & 3], q, qd_, qdd_, g3, fext, tau, nullptr); rc >= 0) return rc;
+  }
   if (const int rc = launch_gen_rnea(L, mode, q, qd, qdd, g3, fext, tau); rc >= 0) return rc;
   return with_view<true>(L, [&](auto mv) { return Launcher<decltype(mv)>::rnea(mv, L, q, qd_, qdd_, g, fext, tau); });
 }
 
 int launch_crba(const Launch& L, const void* q, void* M) {
   if (L.N == 0) return 0;
+  if (const int rc = jit_call(L, kJitCrba, q, nullptr, nullptr, nullptr, nullptr, M, nullptr); rc >= 0) return rc;
   if (const int rc = launch_gen_crba(L, q, M); rc >= 0) return rc;
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::crba(mv, L, q, M); });
 }
@@ -119,6 +132,8 @@ __global__ void k_pack_lower(int64_t N, const T* __restrict__ M, int64_t ld_m, c
 
 int launch_crba_packed(const Launch& L, const void* q, void* Mp, const PackTable& tab) {
   if (L.N == 0 || tab.nnz == 0) return 0;
+  if (const int rc = jit_call(L, kJitCrbaPacked, q, nullptr, nullptr, nullptr, nullptr, Mp, nullptr); rc >= 0)
+    return rc;
   if (const int rc = launch_gen_crba_packed(L, q, Mp); rc >= 0) return rc;
   // Dense M of a chunk of states into pool scratch, then gather.  Chunked so
   // the scratch stays bounded (a 64-dof model at 4M states would otherwise
@@ -151,6 +166,7 @@ int launch_crba_packed(const Launch& L, const void* q, void* Mp, const PackTable
 int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, const void* fext,
                void* qdd, int32_t* status) {
   if (L.N == 0) return 0;
+  if (const int rc = jit_call(L, kJitAba, q, qd, tau, g3, fext, qdd, status); rc >= 0) return rc;
   if (const int rc = launch_gen_aba(L, q, qd, tau, g3, fext, qdd, status); rc >= 0) return rc;
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::aba(mv, L, q, qd, tau, g3, fext, qdd, status); });
 }
@@ -158,6 +174,13 @@ int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, 
 int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
                     void* bias, void* qdd, int32_t* status) {
   if (L.N == 0) return 0;
+  if (L.jit) {  // the JIT module's routines, one launch per output (as tree29 below)
+    int rc = 0;
+    if (M && (rc = launch_crba(L, q, M)) != 0) return rc;
+    if (bias && (rc = launch_rnea(L, 1, q, qd, nullptr, g3, nullptr, bias)) != 0) return rc;
+    if (qdd && (rc = launch_aba(L, q, qd, tau, g3, nullptr, qdd, status)) != 0) return rc;
+    return 0;
+  }
   if (L.spec == kTree29) {
     // generated kernels, one per output (each re-derives the joint
     // transforms; cheaper than the fused loop kernel's local-memory state)

@@ -19,6 +19,18 @@ void scratch_free(void* p, void* stream);
 // Which compile-time robot a device model matched (0 = generic kernels).
 enum Spec : int { kGeneric = 0, kChain7 = 1, kTree29 = 2, kHumanoid23 = 3 };
 
+struct Launch;
+// Per-model JIT modules (paper_2604_04310_b200/jit.py, vd_jit_entry.cuh):
+// generated routines of a model without compile-time kernels, loaded at run
+// time.  One entry point; returns -1 when the module has no routine for op.
+enum JitOp : int {
+  kJitAba = 0, kJitRnea = 1, kJitBias = 2, kJitGravity = 3, kJitCoriolis = 4, kJitCrba = 5, kJitCrbaPacked = 6,
+  kJitFk = 7
+};
+constexpr int kJitAbi = 1;
+using JitLaunchFn = int (*)(int op, const Launch* L, const void* x0, const void* x1, const void* x2,
+                            const double* g3, const void* fext, void* y, int32_t* status);
+
 struct Launch {
   int spec;                 // Spec
   int dtype;                // 0 f64, 1 f32
@@ -27,6 +39,7 @@ struct Launch {
   int64_t N, ld_in, ld_out;
   void* stream;
   bool serial = false;      // every joint's parent is its predecessor
+  JitLaunchFn jit = nullptr;  // the model's JIT module, if one is attached
 };
 
 struct OscShared;

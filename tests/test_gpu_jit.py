@@ -1,0 +1,90 @@
+"""GPU parity of per-model JIT modules (jit.py): the generated straight-line
+routines of a model that is not a compile-time robot, against the CPU oracle
+and against the same model on the loop kernels.  Bars as test_gpu_parity.py
+(fp64 1e-10, fp32 1e-4 against the fp64 oracle, rel_err of
+proj/tests/helpers.hpp:67-72; forward dynamics with the conditioning-aware
+bound of DESIGN.md §Parity policy)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle_ffi import Model as OModel
+from oracle_ffi import rel_err
+from urdf_gen import random_urdf
+
+pytestmark = pytest.mark.gpu
+
+TOL64, TOL32 = 1e-10, 1e-4
+CASES = [("random12", lambda: random_urdf(5, n=12)), ("random16", lambda: random_urdf(11, n=16, branchiness=0.6)),
+         ("humanoid23", None)]
+
+
+def _t(a, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+def _np(t):
+    return t.double().cpu().numpy()
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])
+def case(request, vd, oracle):
+    name, make = request.param
+    if make is None:
+        m, om = vd.robots.by_name(name), OModel.builtin(name)
+    else:
+        text = make()
+        m, om = vd.urdf.load_model_from_string(text), OModel.from_urdf(text)
+    dm = vd.DeviceModel(m, 0, jit=True)
+    assert dm.specialization() == 0 and dm.uses_jit()
+    generic = vd.DeviceModel(m, 0, generic=True)
+    assert not generic.uses_jit()
+    return m, om, dm, generic
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_jit_dynamics_match_oracle(vd, cuda, case, dtype):
+    m, om, dm, generic = case
+    n = om.n
+    tol = TOL64 if dtype == torch.float64 else TOL32
+    q, qd, qdd, tau = om.random_states(1537, 31, True, True)
+    rng = np.random.default_rng(3)
+    fext = rng.uniform(-1, 1, (1537, n, 6))
+    g = (0.3, -0.2, 9.5)
+    G = vd.GravitySpec(g)
+    T = lambda a: _t(a, dtype)  # noqa: E731
+    assert rel_err(_np(vd.rnea(dm, T(q), T(qd), T(qdd), G)), om.rnea(q, qd, qdd, gravity=g), axis=1).max() <= tol
+    assert rel_err(_np(vd.rnea(dm, T(q), T(qd), T(qdd), G, T(fext))), om.rnea(q, qd, qdd, gravity=g, fext=fext),
+                   axis=1).max() <= tol
+    z = np.zeros_like(q)
+    assert rel_err(_np(vd.bias_forces(dm, T(q), T(qd), G)), om.rnea(q, qd, z, gravity=g), axis=1).max() <= tol
+    assert rel_err(_np(vd.gravity_vector(dm, T(q), G)), om.rnea(q, z, z, gravity=g), axis=1).max() <= tol
+    assert rel_err(_np(vd.coriolis_vector(dm, T(q), T(qd))), om.rnea(q, qd, z, gravity=(0, 0, 0)),
+                   axis=1).max() <= tol
+    M = om.crba(q)
+    assert rel_err(_np(vd.crba(dm, T(q))), M, axis=1).max() <= tol
+    rows, cols = m.crba_pattern()
+    assert rel_err(_np(vd.crba_packed(dm, T(q))), M[:, rows, cols], axis=1).max() <= tol
+    assert rel_err(_np(vd.forward_kinematics(dm, T(q))), om.fk(q), axis=1).max() <= tol
+    for fx in (None, fext):
+        got = _np(vd.forward_dynamics(dm, T(q), T(qd), T(tau), G, None if fx is None else T(fx)))
+        ref, st = om.forward_dynamics(q, qd, tau, gravity=g, fext=fx)
+        assert np.all(st == 0)
+        err = rel_err(got, ref, axis=1)
+        eps = np.finfo(np.float64 if dtype == torch.float64 else np.float32).eps
+        cond = np.linalg.cond(M)
+        assert np.all(err <= np.maximum(tol, n * eps * cond))
+        assert err[cond < 1e5].max(initial=0) <= tol
+
+
+def test_jit_matches_loop_kernels(vd, cuda, case):
+    """Same model, JIT module vs the loop kernels, fp64: the two are separate
+    evaluations of the same recursions (agreement to rounding)."""
+    m, om, dm, generic = case
+    q, qd, qdd, tau = om.random_states(999, 32, True, True)
+    a = _np(vd.forward_dynamics(dm, _t(q), _t(qd), _t(tau)))
+    b = _np(vd.forward_dynamics(generic, _t(q), _t(qd), _t(tau)))
+    cond = np.linalg.cond(om.crba(q))
+    assert np.all(rel_err(a, b, axis=1) <= np.maximum(1e-10, om.n * 1e-16 * cond))
+    assert rel_err(_np(vd.rnea(dm, _t(q), _t(qd), _t(qdd))), _np(vd.rnea(generic, _t(q), _t(qd), _t(qdd))),
+                   axis=1).max() <= 1e-12
