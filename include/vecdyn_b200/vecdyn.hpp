@@ -122,6 +122,9 @@ class RobotModel {
     return b;
   }
   int joint_index(std::string_view name) const { return vd_model_joint_index(handle(), std::string(name).c_str()); }
+  // Attach this model's JIT module of generated routines (vd_model_attach_jit;
+  // built by `python -m paper_2604_04310_b200.jit model.urdf`).
+  void attach_jit(const std::string& module_path) { detail::check(vd_model_attach_jit(handle(), module_path.c_str())); }
   int frame_index(std::string_view name) const {  // RobotModel::frame, model.cpp:337-343
     int k = -1;
     detail::check(vd_model_frame_index(handle(), std::string(name).c_str(), &k));
