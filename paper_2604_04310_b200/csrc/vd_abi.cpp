@@ -33,8 +33,15 @@ struct JitModule {
 
 struct vd_model_s {
   vdh::Model m;
-  std::shared_ptr<JitModule> jit;  // vd_model_attach_jit
+  std::shared_ptr<JitModule> jit;  // vd_model_attach_jit; read/written under jit_mutex()
 };
+
+// A model is otherwise immutable and shared across threads (model.hpp:86-89);
+// attaching a JIT module is its one mutation.
+static std::mutex& jit_mutex() {
+  static std::mutex mu;
+  return mu;
+}
 
 struct vd_device_model_s {
   int device = 0;
@@ -318,7 +325,10 @@ int vd_device_model_create(vd_model m, int device, vd_device_model* out) {
     dm->pm = vdh::pack(m->m);
     dm->n = dm->pm.n;
     dm->spec = vdk::match_spec(vdh::fingerprint(dm->pm), dm->pm.n);
-    if (dm->spec == vdk::kGeneric) dm->jit = m->jit;  // builtin robots keep their compiled-in kernels
+    if (dm->spec == vdk::kGeneric) {  // builtin robots keep their compiled-in kernels
+      std::lock_guard<std::mutex> lk(jit_mutex());
+      dm->jit = m->jit;
+    }
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
@@ -361,6 +371,7 @@ int vd_model_attach_jit(vd_model m, const char* path) {
     jm->dl = dl;
     jm->fp = fp;
     jm->launch = launch;
+    std::lock_guard<std::mutex> lk(jit_mutex());
     m->jit = std::move(jm);
     return VD_OK;
   });
@@ -692,6 +703,7 @@ struct DevCtx {
   vd_device_model dm = nullptr;
   uint64_t fp = 0;
   int n = -1;
+  const void* jit_id = nullptr;  // the model's JIT module the cached device model was created with
   cudaStream_t st[2] = {nullptr, nullptr};
   cudaEvent_t done[2] = {nullptr, nullptr};
   double* din[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
@@ -730,12 +742,18 @@ bool is_pinned(const void* p) {
 int prepare_ctx(DevCtx& c, vd_model m, int n, int64_t chunk, int width, bool staging) {
   cudaError_t e;
   const uint64_t fp = vdh::fingerprint(vdh::pack(m->m));
-  if (!c.dm || c.fp != fp || c.n != n) {
+  const void* jit_id;
+  {
+    std::lock_guard<std::mutex> lk(jit_mutex());
+    jit_id = m->jit.get();
+  }
+  if (!c.dm || c.fp != fp || c.n != n || c.jit_id != jit_id) {
     if (c.dm) vd_device_model_destroy(c.dm);
     c.dm = nullptr;
     if (int rc = vd_device_model_create(m, c.device, &c.dm)) return rc;
     c.fp = fp;
     c.n = n;
+    c.jit_id = jit_id;
   }
   if (!c.st[0]) {
     for (int k = 0; k < 2; ++k) {

@@ -88,3 +88,15 @@ def test_jit_matches_loop_kernels(vd, cuda, case):
     assert np.all(rel_err(a, b, axis=1) <= np.maximum(1e-10, om.n * 1e-16 * cond))
     assert rel_err(_np(vd.rnea(dm, _t(q), _t(qd), _t(qdd))), _np(vd.rnea(generic, _t(q), _t(qd), _t(qdd))),
                    axis=1).max() <= 1e-12
+
+
+def test_jit_host_batch_api(vd, cuda, case):
+    """batch_* (batch.hpp:128-165) on host buffers through a model with a JIT
+    module attached: the per-device contexts pick the module up."""
+    m, om, dm, generic = case
+    b = vd.random_states(m, 5000, 77, True, True)
+    tau = vd.batch_rnea(m, b)
+    assert rel_err(tau, om.rnea(b.q, b.qd, b.qdd), axis=1).max() <= TOL64
+    b.tau = tau
+    qdd = vd.batch_forward_dynamics(m, b)
+    assert rel_err(qdd, b.qdd, axis=1).max() <= 1e-8  # FD∘ID roundtrip (test_dynamics.cpp:335-351)
