@@ -74,7 +74,10 @@ def build(model, verbose=False):
 
 def attach(model, path=None, verbose=False):
     """Attach a JIT module (built if `path` is None) to `model`; device models
-    created from it afterwards use it.  Returns the module path."""
+    created from it afterwards use it.  Returns the module path (None for a
+    model without joints: every call on it is a no-op already)."""
+    if model.dof() == 0:
+        return None
     path = path or build(model, verbose=verbose)
     lib = _lib.load()
     if lib.vd_model_attach_jit(model.handle, path.encode()) != 0:

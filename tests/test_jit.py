@@ -43,3 +43,13 @@ def test_jit_cache_is_reused(vd, jitmod):
 
     m, path = jitmod
     assert jit.build(m) == path  # same model, same source: the cached module
+
+
+def test_jit_skips_models_without_joints(vd):
+    from paper_2604_04310_b200 import jit
+
+    text = ('<robot name="empty"><link name="base"><inertial><mass value="1.0"/>'
+            '<inertia ixx="1" ixy="0" ixz="0" iyy="1" iyz="0" izz="1"/></inertial></link></robot>')
+    m = vd.urdf.load_model_from_string(text)
+    assert m.dof() == 0
+    assert jit.attach(m) is None
