@@ -463,6 +463,28 @@ def run_configs(vd, lib, dev, stream, sptr, args, rank, world):
     tree = vd.robots.tree29()
     dc, dt_ = vd.DeviceModel(chain, dev.index), vd.DeviceModel(tree, dev.index)
 
+    # config 1: Panda RNEA on one random state.  The reference number is CPU
+    # latency (CLOCK_MONOTONIC, median of 10,000 calls) of the
+    # oracle port's rnea on one host thread; beside it the device time of one
+    # vd_rnea call at N = 1 (host launch included) and its CUDA-graph replay.
+    if True:  # every rank (event_time's barriers)
+        import oracle_ffi
+
+        L = oracle_ffi.lib()
+        L.orc_rnea_latency_ns.restype = ctypes.c_double
+        L.orc_rnea_latency_ns.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64]
+        cpu_ns = L.orc_rnea_latency_ns(oracle_ffi.Model.builtin("chain7").h, 10000, SEED + 1)
+        q1, qd1, qdd1 = states(7, 1, torch.float64)
+        tau1 = torch.empty((7, 1), dtype=torch.float64, device=dev)
+        fn1 = lambda sp: lib.vd_rnea(dc.handle, 0, 1, q1.data_ptr(), qd1.data_ptr(), qdd1.data_ptr(), 1, None,  # noqa
+                                     None, tau1.data_ptr(), 1, sp)
+        g1 = graph_time(fn1, 400, 20)
+        out["1_panda_rnea_single_state_f64"] = {
+            "states": 1, "cpu_reference_median_ns": round(cpu_ns, 1), "cpu_threads": 1,
+            "gpu_ms_one_call": round(event_time(lambda: fn1(sptr), 200, 20, stream), 5),
+            "gpu_ms_graph": round(g1, 5) if g1 else None,
+            "note": "latency, not throughput: a single state is the reference's CPU use case (config 1)"}
+
     # config 2: Panda FK + EE Jacobian, batch 4096
     for dt, code in ((torch.float64, 0), (torch.float32, 1)):
         N = 4096

@@ -5,6 +5,9 @@
 // SoA column-major buffers (element (i, k) at k*N + i, exactly Eigen's
 // column-major N x K used by StateBatch and batch_crba, batch.hpp:15-19,
 // 147-148) and runs through orc::batch_eval (batch.hpp:82-125).
+#include <algorithm>
+#include <ctime>
+#include <vector>
 #include <cstring>
 #include <string>
 
@@ -505,6 +508,30 @@ double orc_count_flops(void* h, int algo, double* out) {
     out[4] = (double)c.trig;
   }
   return (double)c.flops();
+}
+
+// BASELINE config 1: single-state RNEA latency of the reference path (the
+// mask-vectorised rnea, dynamics.hpp:250-267) as PAPER.md:312 measures it —
+// CLOCK_MONOTONIC around each call, `iters` calls on one seeded random state
+// (batch.hpp:48-75 draw order), median in nanoseconds.  Test infrastructure:
+// bench.py's CPU leg only.
+double orc_rnea_latency_ns(void* h, int iters, uint64_t seed) {
+  const Model& m = M(h);
+  const int n = m.dof();
+  std::vector<double> q(n), qd(n), qdd(n);
+  orc_random_states(h, 1, seed, q.data(), qd.data(), qdd.data(), nullptr);
+  std::vector<double> ns((size_t)std::max(iters, 1));
+  volatile double sink = 0;
+  for (size_t k = 0; k < ns.size(); ++k) {
+    timespec a, b;
+    clock_gettime(CLOCK_MONOTONIC, &a);
+    const std::vector<double> t = rnea<double>(m, q, qd, qdd, Gravity::standard(), ExtForces<double>());
+    clock_gettime(CLOCK_MONOTONIC, &b);
+    sink = sink + t[0];
+    ns[k] = (double)(b.tv_sec - a.tv_sec) * 1e9 + (double)(b.tv_nsec - a.tv_nsec);
+  }
+  std::nth_element(ns.begin(), ns.begin() + ns.size() / 2, ns.end());
+  return ns[ns.size() / 2];
 }
 
 }  // extern "C"
