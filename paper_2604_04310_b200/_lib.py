@@ -100,6 +100,8 @@ SIGNATURES = {
     "vd_batch_crba_host": (c_int, [P, c_int64, P, P, Pi, c_int]),
     "vd_batch_forward_dynamics_host": (c_int, [P, c_int64, P, P, P, Pd, P, P, Pi, c_int]),
     "vd_shard_range": (c_int, [c_int64, c_int, c_int, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64)]),
+    "vd_rows_to_planes": (c_int, [c_int, c_int64, c_int, P, c_int64, P, c_int64, P]),
+    "vd_planes_to_rows": (c_int, [c_int, c_int64, c_int, P, c_int64, P, c_int64, P]),
 }
 
 _lib = None

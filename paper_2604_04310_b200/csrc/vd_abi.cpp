@@ -673,6 +673,25 @@ int vdi_model_packed(vd_model m, int* n, int* parent, int* kind, int* axis_code,
   });
 }
 
+static int layout_call(int dtype, bool to_planes, int64_t N, int K, const void* src, int64_t ld_src, void* dst,
+                       int64_t ld_dst, void* stream, const char* where) {
+  if (dtype != VD_F64 && dtype != VD_F32) return set_error(VD_ERR_INVALID_ARGUMENT, "dtype must be VD_F64 or VD_F32");
+  if (N < 0 || K < 0) return set_error(VD_ERR_DIMENSION, "negative size");
+  if (N == 0 || K == 0) return VD_OK;
+  if (!src || !dst) return set_error(VD_ERR_INVALID_ARGUMENT, "null buffer");
+  const int64_t ld_rows = to_planes ? ld_src : ld_dst, ld_planes = to_planes ? ld_dst : ld_src;
+  if (ld_rows < K || ld_planes < N) return set_error(VD_ERR_DIMENSION, "leading dimension too small");
+  return finish(vdk::launch_layout(dtype == VD_F64 ? 0 : 1, to_planes, N, K, src, ld_src, dst, ld_dst, stream), where);
+}
+int vd_rows_to_planes(int dtype, int64_t N, int K, const void* rows, int64_t ld_rows, void* planes, int64_t ld_planes,
+                      void* stream) {
+  return layout_call(dtype, true, N, K, rows, ld_rows, planes, ld_planes, stream, "vd_rows_to_planes");
+}
+int vd_planes_to_rows(int dtype, int64_t N, int K, const void* planes, int64_t ld_planes, void* rows, int64_t ld_rows,
+                      void* stream) {
+  return layout_call(dtype, false, N, K, planes, ld_planes, rows, ld_rows, stream, "vd_planes_to_rows");
+}
+
 int vd_shard_range(int64_t N, int world, int rank, int64_t* begin, int64_t* end) {
   if (world <= 0 || rank < 0 || rank >= world || N < 0 || !begin || !end)
     return set_error(VD_ERR_INVALID_ARGUMENT, "bad shard arguments");

@@ -100,6 +100,10 @@ int launch_jvp(const Launch& L, const JvpArgs& a);
 // generated dual-number kernels (tree29 ABA / RNEA without f_ext); -1 otherwise
 int launch_gen_jvp(const Launch& L, const JvpArgs& a);
 
+// Row-major (N, K) batch <-> K planes (vd_layout.cu); to_planes: rows -> planes.
+int launch_layout(int dtype, bool to_planes, int64_t N, int K, const void* src, int64_t ld_src, void* dst,
+                  int64_t ld_dst, void* stream);
+
 // mode 0: diff_ik_step (out = q̇, aux = pose error); mode 1: manipulability (out = w)
 int launch_task(const Launch& L, const void* q, const TaskShared& P, int mode, void* out, void* aux,
                 int32_t* status);
