@@ -308,16 +308,17 @@ class DeviceModel:
     """The model packed and uploaded to one GPU (compile-time specialised when it
     matches a builtin robot).  jit=True: for any other model, build (or reuse
     the cached) per-model module of generated routines and attach it to the
-    model first (jit.py); ignored for the builtin robots."""
+    model first (jit.py), with the task-space routines of `jit_frames`;
+    ignored for the builtin robots."""
 
-    def __init__(self, model, device=0, generic=False, jit=False):
+    def __init__(self, model, device=0, generic=False, jit=False, jit_frames=()):
         self.model = model
         self.device = int(device)
         self._lib = _lib.load()
         if jit and self._lib.vdi_model_fingerprint(model.handle) not in _builtin_fingerprints():
             from . import jit as _jit
 
-            _jit.attach(model)
+            _jit.attach(model, frames=tuple(jit_frames))
         h = ctypes.c_void_p()
         _check(self._lib.vd_device_model_create(model.handle, self.device, ctypes.byref(h)))
         self._h = h

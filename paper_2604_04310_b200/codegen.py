@@ -1587,7 +1587,7 @@ JIT_OPS = ("Aba", "AbaMixed", "Rnea", "RneaBias", "RneaGrav", "RneaFext", "RneaB
            "Crba", "CrbaPacked", "Fk")
 
 
-def emit_body(name, cls, rb, ops=None, tasks=True):
+def emit_body(name, cls, rb, ops=None, tasks=True, task_joints=None):
     out = [f"// ---- {name}",
            f"struct Gen{cls} {{",
            f"  static constexpr int kN = {rb.n};",
@@ -1614,6 +1614,8 @@ def emit_body(name, cls, rb, ops=None, tasks=True):
     # one variant for every leaf joint (end effectors) and the joints that
     # carry a named frame of the model
     osc_joints = sorted(set(i for i in range(rb.n) if not rb.children[i]) | set(rb.frame_joints))
+    if task_joints is not None:
+        osc_joints = sorted(set(task_joints))
     # branched trees: the articulated-body OSC (no M in per-state slots);
     # serial chains: M is small, the branch-sparse LTL form costs fewer flops
     serial = all(p == i - 1 for i, p in enumerate(rb.parent))
@@ -1669,13 +1671,18 @@ def emit_body(name, cls, rb, ops=None, tasks=True):
     return out
 
 
-def jit_source(lib, h, cls="Jit"):
+def jit_source(lib, h, task_joints=(), cls="Jit"):
     """Translation unit of a per-model JIT module: the model's generated
-    routines (JIT_OPS) as struct Gen<cls>, then the C entry points of
-    csrc/vd_jit_entry.cuh over them."""
+    routines (JIT_OPS; with task_joints also OSC / Jacobian / diff-IK /
+    manipulability on those frame joints) as struct Gen<cls>, then the C
+    entry points of csrc/vd_jit_entry.cuh over them."""
     rb = Robot(packed_model(lib, h), frame_joints(lib, h))
+    tj = sorted(set(task_joints))
     lines = ["// GENERATED at model load by paper_2604_04310_b200/jit.py; do not edit.",
              "#include \"vd_gen_launch.cuh\"", "", "namespace vdk {", ""]
-    lines += emit_body(f"jit {rb.d['fp']:#x}", cls, rb, ops=JIT_OPS, tasks=False)
-    lines += ["}  // namespace vdk", "", f"#define VD_JIT_ROBOT vdk::Gen{cls}", "#include \"vd_jit_entry.cuh\"", ""]
+    lines += emit_body(f"jit {rb.d['fp']:#x}", cls, rb, ops=JIT_OPS, tasks=bool(tj), task_joints=tj)
+    lines += ["}  // namespace vdk", "", f"#define VD_JIT_ROBOT vdk::Gen{cls}"]
+    if tj:
+        lines += ["#define VD_JIT_TASKS 1"]
+    lines += ["#include \"vd_jit_entry.cuh\"", ""]
     return "\n".join(lines), rb.d["fp"]

@@ -29,6 +29,8 @@ struct JitModule {
   void* dl = nullptr;
   uint64_t fp = 0;
   vdk::JitLaunchFn launch = nullptr;
+  vdk::JitTaskFn task_launch = nullptr;  // modules generated with task frames
+  uint64_t task_mask = 0;
 };
 
 struct vd_model_s {
@@ -165,7 +167,11 @@ vdk::Launch make_launch(vd_device_model dm, int dtype, int64_t N, int64_t ldi, i
   L.stream = stream;
   L.serial = true;
   for (int i = 0; i < dm->n; ++i) L.serial = L.serial && dm->pm.parent[i] == i - 1;
-  L.jit = (!dm->force_generic && dm->jit) ? dm->jit->launch : nullptr;
+  if (!dm->force_generic && dm->jit) {
+    L.jit = dm->jit->launch;
+    L.jit_task = dm->jit->task_launch;
+    L.jit_task_mask = dm->jit->task_mask;
+  }
   return L;
 }
 int finish(int rc, const char* where) {
@@ -371,6 +377,9 @@ int vd_model_attach_jit(vd_model m, const char* path) {
     jm->dl = dl;
     jm->fp = fp;
     jm->launch = launch;
+    auto tmask = reinterpret_cast<uint64_t (*)()>(dlsym(dl, "vdj_task_mask"));
+    jm->task_launch = reinterpret_cast<vdk::JitTaskFn>(dlsym(dl, "vdj_task_launch"));
+    jm->task_mask = (tmask && jm->task_launch) ? tmask() : 0;
     std::lock_guard<std::mutex> lk(jit_mutex());
     m->jit = std::move(jm);
     return VD_OK;

@@ -61,6 +61,10 @@ void scratch_free(void* p, void* stream) {
 }
 int launch_jac_scan(const Launch& L, const void* q, const FrameArg& fr, void* pose, void* J);
 
+static bool jit_has_task(const Launch& L, int frame_joint) {
+  return L.jit_task && frame_joint >= 0 && frame_joint < 64 && ((L.jit_task_mask >> frame_joint) & 1);
+}
+
 // The model's JIT module (vd_jit_entry.cuh), when one is attached; -1 when
 // there is none or it has no routine for the call.
 static int jit_call(const Launch& L, JitOp op, const void* x0, const void* x1, const void* x2, const double* g3,
@@ -85,10 +89,13 @@ int launch_jacobian(const Launch& L, const void* q, int frame_joint, const doubl
   // serial chains at batches below one wave of thread-per-state CTAs: 8 lanes
   // per state (config 2, Panda at N = 4096)
   if (L.serial && L.n <= 32 && L.N <= 32768) return launch_jac_scan(L, q, fr, pose, J);
-  if (L.spec == kTree29 || L.spec == kChain7) {
+  if (L.spec == kTree29 || L.spec == kChain7 || jit_has_task(L, frame_joint)) {
     TaskShared P{};
     for (int k = 0; k < 9; ++k) P.frame_R[k] = frame_R[k];
     for (int k = 0; k < 3; ++k) P.frame_p[k] = frame_p[k];
+    if (jit_has_task(L, frame_joint)) {
+      if (const int rc = L.jit_task(0, &L, frame_joint, q, nullptr, &P, pose, J, nullptr); rc >= 0) return rc;
+    }
     if (const int rc = launch_gen_task(L, 0, frame_joint, P, q, pose, J, nullptr); rc >= 0) return rc;
   }
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::jac(mv, L, q, fr, pose, J); });
@@ -197,6 +204,9 @@ int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* 
 int launch_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
                int32_t* status) {
   if (L.N == 0) return 0;
+  if (jit_has_task(L, P.frame_joint)) {
+    if (const int rc = L.jit_task(3, &L, P.frame_joint, q, qd, &P, tau, lambda, status); rc >= 0) return rc;
+  }
   if (const int rc = launch_gen_osc(L, q, qd, P, tau, lambda, status); rc >= 0) return rc;
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::osc(mv, L, q, qd, P, tau, lambda, status); });
 }
@@ -204,6 +214,12 @@ int launch_osc(const Launch& L, const void* q, const void* qd, const OscShared& 
 int launch_task(const Launch& L, const void* q, const TaskShared& P, int mode, void* out, void* aux,
                 int32_t* status) {
   if (L.N == 0) return 0;
+  if (jit_has_task(L, P.frame_joint)) {
+    if (const int rc = L.jit_task(mode == 0 ? 1 : 2, &L, P.frame_joint, q, nullptr, &P, out, mode == 0 ? aux : nullptr,
+                                  mode == 0 ? status : nullptr);
+        rc >= 0)
+      return rc;
+  }
   if (const int rc = launch_gen_task(L, mode == 0 ? 1 : 2, P.frame_joint, P, q, out, mode == 0 ? aux : nullptr,
                                      mode == 0 ? status : nullptr);
       rc >= 0)

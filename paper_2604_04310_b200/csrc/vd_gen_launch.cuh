@@ -112,4 +112,48 @@ int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, c
                       : launch_t<Op, float>(L, x0, x1, x2, g3, y, status, fext);
 }
 
+
+// OSC on branched trees: the articulated-body form (gen_osc_aba, ~255 slots
+// for a G1 hand/foot frame instead of the 486 of the M-based form).
+// tools/async_sweep.cu "more", G1 `l_palm`, N = 262144: fp64 r40 s110 (2
+// CTAs/SM) 0.61 ms, s55 b3 0.69 ms (the M-based routine: 1.23 ms); fp32
+// r40 s144 (3 CTAs/SM) 0.27 ms (M-based: 0.50 ms).
+template <class Op, class T>
+struct OscCfg {
+  static constexpr int kReg = 40, kSmem = sizeof(T) == 8 ? 110 : 144, kMinB = sizeof(T) == 8 ? 2 : 3;
+};
+template <class Op, class T>
+int launch_osc_t(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lam,
+                 int32_t* status) {
+  using C = OscCfg<Op, T>;
+  auto kern = k_gen_osc<Op, T, C::kReg, C::kSmem, C::kMinB>;
+  constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
+  const Occ o = occupancy<Op, T>(kern, smem);
+  const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
+  cudaStream_t s = static_cast<cudaStream_t>(L.stream);
+  const size_t scratch_bytes = (size_t)blocks * kGenBlock * gen_scratch_per_thread<Op, T, C::kReg, C::kSmem>() * sizeof(T);
+  T* scratch = nullptr;
+  if (scratch_bytes) {
+    if (int rc = scratch_alloc(reinterpret_cast<void**>(&scratch), scratch_bytes, s)) return rc;
+  }
+  kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, (const T*)q, (const T*)qd, L.ld_in, P, (T*)tau, (T*)lam,
+                                                 L.ld_out, status, scratch);
+  cudaError_t e = cudaGetLastError();
+  scratch_free(scratch, s);
+  return (int)e;
+}
+
+template <class Op, class T>
+int launch_task_t(const Launch& L, const void* q, const TaskShared& P, void* y0, void* y1, int32_t* status) {
+  constexpr int kReg = 0, kSmem = Op::kSlots, kMinB = sizeof(T) == 8 ? 3 : 4;  // path-only state: all on chip
+  auto kern = k_gen_task<Op, T, kReg, kSmem, kMinB>;
+  constexpr size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  const Occ o = occupancy<Op, T>(kern, smem);
+  const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
+  kern<<<(unsigned)blocks, kGenBlock, smem, static_cast<cudaStream_t>(L.stream)>>>(
+      L.N, (const T*)q, L.ld_in, P, (T*)y0, (T*)y1, L.ld_out, status, nullptr);
+  return (int)cudaGetLastError();
+}
+
+
 }  // namespace vdk

@@ -77,3 +77,43 @@ VD_JIT_API int vdj_launch(int op, const vdk::Launch* L, const void* x0, const vo
       return -1;
   }
 }
+
+#ifdef VD_JIT_TASKS
+// Task-space routines on the frame joints the module was generated for:
+// bit j of the mask = joint j has OSC, Jacobian, diff-IK and manipulability.
+VD_JIT_API uint64_t vdj_task_mask(void) {
+  uint64_t m = 0;
+  for (int j : VD_JIT_ROBOT::kOscJoints) m |= 1ull << j;
+  return m;
+}
+// which: 0 Jacobian (y0 pose, y1 J), 1 diff-IK (y0 q̇, y1 err), 2 manipulability
+// (y0 w); params = vdk::TaskShared.  3: OSC (y0 τ, y1 Λ), params =
+// vdk::OscShared.  Same conventions as vd_inst_gen.cu's gen_task_t / gen_osc_t.
+VD_JIT_API int vdj_task_launch(int which, const vdk::Launch* L, int frame_joint, const void* q, const void* qd,
+                               const void* params, void* y0, void* y1, int32_t* status) {
+  using R = VD_JIT_ROBOT;
+  using namespace vdk;
+  int rc = -1;
+  const bool f64 = L->dtype == 0;
+  if (which == 3) {
+    const OscShared& P = *static_cast<const OscShared*>(params);
+    R::with_osc(frame_joint, [&](auto op) {
+      using Op = decltype(op);
+      rc = f64 ? launch_osc_t<Op, double>(*L, q, qd, P, y0, y1, status)
+               : launch_osc_t<Op, float>(*L, q, qd, P, y0, y1, status);
+    });
+    return rc;
+  }
+  const TaskShared& P = *static_cast<const TaskShared*>(params);
+  R::with_task(frame_joint, [&](auto jac, auto dik, auto man) {
+    auto go = [&](auto op) {
+      using Op = decltype(op);
+      rc = f64 ? launch_task_t<Op, double>(*L, q, P, y0, y1, status) : launch_task_t<Op, float>(*L, q, P, y0, y1, status);
+    };
+    if (which == 0) go(jac);
+    else if (which == 1) go(dik);
+    else go(man);
+  });
+  return rc;
+}
+#endif

@@ -30,6 +30,9 @@ enum JitOp : int {
 constexpr int kJitAbi = 1;
 using JitLaunchFn = int (*)(int op, const Launch* L, const void* x0, const void* x1, const void* x2,
                             const double* g3, const void* fext, void* y, int32_t* status);
+// which: 0 Jacobian, 1 diff-IK, 2 manipulability (params TaskShared*), 3 OSC (params OscShared*)
+using JitTaskFn = int (*)(int which, const Launch* L, int frame_joint, const void* q, const void* qd,
+                          const void* params, void* y0, void* y1, int32_t* status);
 
 struct Launch {
   int spec;                 // Spec
@@ -40,6 +43,8 @@ struct Launch {
   void* stream;
   bool serial = false;      // every joint's parent is its predecessor
   JitLaunchFn jit = nullptr;  // the model's JIT module, if one is attached
+  JitTaskFn jit_task = nullptr;  // its task-space routines, for the frame joints in jit_task_mask
+  uint64_t jit_task_mask = 0;
 };
 
 struct OscShared;

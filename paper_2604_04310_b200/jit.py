@@ -9,9 +9,10 @@ sm_100a into a shared library (csrc/vd_jit_entry.cuh's entry points) and
 caches it by model fingerprint and source hash; `attach(model)` loads it into
 the model (vd_model_attach_jit) so every device model created from it
 afterwards runs ABA, RNEA, bias, gravity, Coriolis, CRBA, packed CRBA and FK
-through it.  Everything else (Jacobian, OSC, JVPs) stays on the loop kernels.
+through it, and OSC / Jacobian / diff-IK / manipulability on the frames the
+module was built for.  JVPs stay on the loop kernels.
 
-    python -m paper_2604_04310_b200.jit robot.urdf     # prints the module path
+    python -m paper_2604_04310_b200.jit robot.urdf [frame ...]   # prints the module path
 
 C++ users attach the printed module with vd_model_attach_jit.
 """
@@ -42,15 +43,37 @@ def _nvcc():
     return "nvcc"
 
 
-def source(model):
-    """(translation unit text, model fingerprint) for `model` (a RobotModel)."""
-    return codegen.jit_source(_lib.load(), model.handle)
+def frame_joints(model, frames):
+    """Joint indices of named frames (vd_model_frame); UnknownFrameError-like
+    RuntimeError for a name the model does not have."""
+    import ctypes
+
+    lib = _lib.load()
+    out = []
+    for name in frames:
+        k = ctypes.c_int()
+        if lib.vd_model_frame_index(model.handle, name.encode(), ctypes.byref(k)) != 0:
+            raise RuntimeError(lib.vd_last_error().decode())
+        j = ctypes.c_int()
+        buf = ctypes.create_string_buffer(256)
+        off = (ctypes.c_double * 12)()
+        lib.vd_model_frame(model.handle, k.value, buf, 256, ctypes.byref(j), off)
+        if j.value >= 0:
+            out.append(j.value)
+    return sorted(set(out))
 
 
-def build(model, verbose=False):
+def source(model, frames=()):
+    """(translation unit text, model fingerprint) for `model` (a RobotModel);
+    `frames`: frame names whose OSC / Jacobian / diff-IK / manipulability
+    routines the module also carries."""
+    return codegen.jit_source(_lib.load(), model.handle, task_joints=frame_joints(model, frames))
+
+
+def build(model, frames=(), verbose=False):
     """Path of the model's JIT module, compiling it if it is not cached.
     Raises RuntimeError with nvcc's output if the compile fails."""
-    src, fp = source(model)
+    src, fp = source(model, frames)
     tag = hashlib.sha1((src + " ".join(NVCC_FLAGS)).encode()).hexdigest()[:12]
     out_dir = cache_dir()
     os.makedirs(out_dir, exist_ok=True)
@@ -72,13 +95,14 @@ def build(model, verbose=False):
     return so
 
 
-def attach(model, path=None, verbose=False):
-    """Attach a JIT module (built if `path` is None) to `model`; device models
-    created from it afterwards use it.  Returns the module path (None for a
-    model without joints: every call on it is a no-op already)."""
+def attach(model, path=None, frames=(), verbose=False):
+    """Attach a JIT module (built if `path` is None, with the task-space
+    routines of `frames`) to `model`; device models created from it
+    afterwards use it.  Returns the module path (None for a model without
+    joints: every call on it is a no-op already)."""
     if model.dof() == 0:
         return None
-    path = path or build(model, verbose=verbose)
+    path = path or build(model, frames=frames, verbose=verbose)
     lib = _lib.load()
     if lib.vd_model_attach_jit(model.handle, path.encode()) != 0:
         raise RuntimeError(lib.vd_last_error().decode())
@@ -88,10 +112,10 @@ def attach(model, path=None, verbose=False):
 def main(argv):
     from . import urdf
 
-    if len(argv) != 1:
-        sys.stderr.write("usage: python -m paper_2604_04310_b200.jit robot.urdf\n")
+    if not argv:
+        sys.stderr.write("usage: python -m paper_2604_04310_b200.jit robot.urdf [frame ...]\n")
         return 2
-    print(build(urdf.load_model(argv[0]), verbose=True))
+    print(build(urdf.load_model(argv[0]), frames=argv[1:], verbose=True))
     return 0
 
 

@@ -100,3 +100,51 @@ def test_jit_host_batch_api(vd, cuda, case):
     b.tau = tau
     qdd = vd.batch_forward_dynamics(m, b)
     assert rel_err(qdd, b.qdd, axis=1).max() <= 1e-8  # FD∘ID roundtrip (test_dynamics.cpp:335-351)
+
+
+@pytest.fixture(scope="module")
+def task_case(vd, oracle):
+    """humanoid23 with a JIT module that also carries its `l_palm` tasks."""
+    m, om = vd.robots.by_name("humanoid23"), OModel.builtin("humanoid23")
+    dm = vd.DeviceModel(m, 0, jit=True, jit_frames=("l_palm",))
+    assert dm.uses_jit()
+    return m, om, dm
+
+
+def test_jit_task_routines_match_oracle(vd, cuda, task_case):
+    """OSC (osc_step, control.hpp:108-155), geometric Jacobian
+    (kinematics.hpp:108-136), diff-IK (control.hpp:79-97) and manipulability
+    (kinematics.hpp:138-153) from the module's generated routines, fp64,
+    against the oracle with the conditioning-aware bounds of
+    test_gpu_parity.test_osc_fp64 / test_gpu_task."""
+    m, om, dm = task_case
+    frame, N = "l_palm", 1024
+    q, qd, _, _ = om.random_states(N, 93, False, False)
+    q0 = np.zeros((1, om.n))
+    pose0, _ = om.jacobian(q0, frame)
+    R0, p0 = pose0[0, :9].reshape(3, 3, order="F"), pose0[0, 9:]
+    tau_ref, lam_ref, st_ref = om.osc(q, qd, frame, R0, p0, [100.0] * 6, [20.0] * 6, [0.0] * 6, np.zeros(om.n),
+                                      10.0, 2.0)
+    tgt = vd.TaskTarget(frame, (R0, p0), vd.TaskGains.uniform(100.0, 20.0))
+    tau, lam, st = vd.osc_step(dm, _t(q), _t(qd), tgt, np.zeros(om.n), vd.PostureGains(10.0, 2.0),
+                               return_lambda=True, return_status=True)
+    st = st.cpu().numpy()
+    assert np.all(st == st_ref)
+    ok = st == 0
+    kappa = np.linalg.cond(om.crba(q)) * np.linalg.cond(lam_ref)
+    bound = np.maximum(TOL64, 1e-16 * kappa)
+    assert np.all(rel_err(_np(tau), tau_ref, axis=1)[ok] <= bound[ok])
+    assert np.all(rel_err(_np(lam).reshape(N, -1), lam_ref.reshape(N, -1), axis=1)[ok] <= np.maximum(bound[ok], 1e-10))
+    pose_ref, J_ref = om.jacobian(q, frame)
+    assert rel_err(_np(vd.geometric_jacobian(dm, _t(q), frame)), J_ref, axis=1).max() <= TOL64
+    assert rel_err(_np(vd.frame_transform(dm, _t(q), frame)), pose_ref, axis=1).max() <= TOL64
+    w = _np(vd.manipulability(dm, _t(q), frame))
+    assert rel_err(w[:, None], om.manipulability(q, frame)[:, None], axis=1).max() <= 1e-9
+    kp, ff, damping = [5.0, 4.0, 3.0, 2.0, 1.5, 1.0], [0.1, -0.2, 0.3, 0.01, 0.02, -0.03], 1e-2
+    qd_ref, err_ref = om.diff_ik(q, frame, R0, p0, kp, ff, damping)
+    qd_got, err = vd.diff_ik_step(dm, _t(q), vd.TaskTarget(frame, (R0, p0), vd.TaskGains(kp=kp), twist_ff=ff),
+                                  damping, return_error=True)
+    G = J_ref @ np.swapaxes(J_ref, 1, 2) + damping * damping * np.eye(6)
+    theta = np.linalg.norm(err_ref[:, :3], axis=1)
+    klog = np.maximum(1.0, 1.0 / np.maximum(np.pi - theta, 1e-6) ** 2)
+    assert np.all(rel_err(_np(qd_got), qd_ref, axis=1) <= np.maximum(TOL64, 1e-16 * np.linalg.cond(G) * klog))
