@@ -74,7 +74,15 @@ def build(model, frames=(), verbose=False):
     """Path of the model's JIT module, compiling it if it is not cached.
     Raises RuntimeError with nvcc's output if the compile fails."""
     src, fp = source(model, frames)
-    tag = hashlib.sha1((src + " ".join(NVCC_FLAGS)).encode()).hexdigest()[:12]
+    # the cache key covers everything the module is compiled from: its source,
+    # the flags and the library headers it includes (launch machinery, kernel
+    # templates, the Launch struct of the library it will be loaded into)
+    h = hashlib.sha1((src + " ".join(NVCC_FLAGS)).encode())
+    for name in sorted(os.listdir(CSRC)):
+        if name.endswith((".cuh", ".hpp", ".h")) and name != "vd_gen_robots.cuh":
+            with open(os.path.join(CSRC, name), "rb") as f:
+                h.update(f.read())
+    tag = h.hexdigest()[:12]
     out_dir = cache_dir()
     os.makedirs(out_dir, exist_ok=True)
     so = os.path.join(out_dir, f"vdj_{fp:016x}_{tag}.so")
