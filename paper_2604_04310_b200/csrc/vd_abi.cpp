@@ -366,12 +366,14 @@ int vd_model_attach_jit(vd_model m, const char* path) {
     auto fpf = reinterpret_cast<uint64_t (*)()>(dlsym(dl, "vdj_fingerprint"));
     auto init = reinterpret_cast<void (*)(int (*)(void**, size_t, void*), void (*)(void*, void*))>(dlsym(dl, "vdj_init"));
     auto launch = reinterpret_cast<vdk::JitLaunchFn>(dlsym(dl, "vdj_launch"));
-    if (!abi || !fpf || !init || !launch)
-      return set_error(VD_ERR_INVALID_ARGUMENT, "vd_model_attach_jit: not a vecdyn JIT module");
-    if (abi() != vdk::kJitAbi) return set_error(VD_ERR_INVALID_ARGUMENT, "vd_model_attach_jit: JIT ABI mismatch");
+    auto refuse = [&](const char* why) {
+      dlclose(dl);  // nothing from a refused module was ever called into
+      return set_error(VD_ERR_INVALID_ARGUMENT, std::string("vd_model_attach_jit: ") + why);
+    };
+    if (!abi || !fpf || !init || !launch) return refuse("not a vecdyn JIT module");
+    if (abi() != vdk::kJitAbi) return refuse("JIT ABI mismatch");
     const uint64_t fp = vdh::fingerprint(vdh::pack(m->m));
-    if (fpf() != fp)
-      return set_error(VD_ERR_INVALID_ARGUMENT, "vd_model_attach_jit: module was generated for another model");
+    if (fpf() != fp) return refuse("module was generated for another model");
     init(&vdk::scratch_alloc, &vdk::scratch_free);
     auto jm = std::make_shared<JitModule>();
     jm->dl = dl;
