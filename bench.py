@@ -540,6 +540,17 @@ def run_configs(vd, lib, dev, stream, sptr, args, rank, world):
             {"out_planes": planes, "hbm_gbs": round(byts / (ms * 1e-3) / 1e9, 1),
              "hbm_frac": round(byts / (ms * 1e-3) / 1e9 / measured_peaks().get("hbm_gbs", 6650.0), 4)})
     del Md, Mp, q
+    # the headline workload in fp32 (the north star's fp32 mode, 1e-4 parity):
+    # Panda ABA, 4M states per GPU, generated kernel with async state input
+    N = N_HEAD
+    q, qd, x = states(7, N, torch.float32)
+    a32 = torch.empty((7, N), dtype=torch.float32, device=dev)
+    f32 = lambda: lib.vd_aba(dc.handle, 1, N, q.data_ptr(), qd.data_ptr(), x.data_ptr(), N, None, None,  # noqa
+                             a32.data_ptr(), N, None, sptr)
+    ms = event_time(f32, steps, warm, stream)
+    rec("headline_panda_aba_b4194304_f32", N, ms, flops_per_eval("chain7", "aba"),
+        {"fp32_peak_frac_note": "algorithmic TFLOP/s against the in-run FP32 FMA peak: see fp32_peak_tflops"})
+    del q, qd, x, a32
     # config 5: OSC terms, batch 4M (per GPU), Panda and G1
     for robot, dmod, frame in (("chain7", dc, "ee"), ("tree29", dt_, "l_palm")):
         m = chain if robot == "chain7" else tree
