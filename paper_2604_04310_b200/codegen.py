@@ -552,8 +552,8 @@ class Algo:
         # once), then n independent sincos chains
         joints = [i for i in range(rb.n) if only is None or i in only]  # prologue subset
         qv = {i: g.input(0, i) for i in joints}
-        qdv = [g.input(1, i) for i in range(rb.n)] if with_qd_slots else []
-        xv = {(gi, i): g.input(gi, i) for gi in extra for i in range(rb.n)}
+        qdv = {i: g.input(1, i) for i in joints} if with_qd_slots else {}
+        xv = {(gi, i): g.input(gi, i) for gi in extra for i in joints}
         for i in joints:
             g.ty = "TD" if i in self.hp else "T"
             qi = qv[i]
@@ -563,7 +563,7 @@ class Algo:
                 c, sn = g.sincos(qi, i)
                 self.mrefs[i] = ("cs", self.store(c), self.store(sn))
         g.ty = "T"
-        for i, v in enumerate(qdv):
+        for i, v in qdv.items():
             self.qdrefs[i] = self.store(v)
         for key, v in xv.items():
             self.xrefs[key] = self.store(v)
@@ -753,6 +753,128 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False, fext=False):
 
     for r in rb.roots:
         down(r, None, None)
+    return A.finish()
+
+
+def subtree(rb, c):
+    out, stack = [], [c]
+    while stack:
+        i = stack.pop()
+        out.append(i)
+        stack.extend(rb.children[i])
+    return sorted(out)
+
+
+def gen_aba_role(rb, r):
+    """One warp role of the branch-parallel ABA (small batches, where one
+    thread's straight-line chain is the latency): the trunk (root .. the
+    first branching joint s) and the subtree under s's child r.  Every role
+    recomputes the trunk velocities, runs passes 1-2 on its subtree and
+    publishes the subtree's articulated inertia and bias force in s's frame
+    (cx.xput, 27 values); after a CTA barrier role 0 sums them, finishes
+    pass 2 and runs pass 3 down the trunk, publishing s's acceleration; after
+    a second barrier every role runs pass 3 on its subtree.  The arithmetic of
+    every joint step is gen_aba's (RBDA Table 7.1)."""
+    tr = trunk(rb)
+    s_ = tr[-1]
+    kids = rb.children[s_]
+    R = len(kids)
+    mine = subtree(rb, kids[r])
+    A = Algo(rb, True, only=set(tr) | set(mine))
+    g = A.g
+    layout = {}
+
+    def finish(i, v, acc):
+        X = A.joint(i)
+        qdi = A.load(A.qdrefs[i])
+        b = rb.rb(i)
+        IA = g.ai_from_rb(b)
+        pA = g.crf(v, g.rb_apply(b, v))
+        if acc is not None:
+            IA = g.ai_add(IA, acc[0])
+            pA = g.vadd(pA, acc[1])
+        U = g.ai_apply(IA, X.Svec())
+        D = X.Sdot(U)
+        g.check_pos(D)
+        dinv = g.recip(D)
+        u = g.sub(g.input(2, i), X.Sdot(pA))
+        Ud = [g.mul(x, dinv) for x in U]
+        ud = g.mul(u, dinv)
+        layout[i] = (A.store(ud), [A.store(x) for x in Ud])
+        if rb.parent[i] < 0:
+            return None, None
+        c = g.crm(v, X.S(qdi))
+        ir, ic = (0, 1, 2, 0, 0, 1), (0, 1, 2, 1, 2, 2)
+        Ia = {"A": [g.sub(IA["A"][k], g.mul(U[ir[k]], Ud[ic[k]])) for k in range(6)],
+              "C": [g.sub(IA["C"][k], g.mul(U[3 + ir[k]], Ud[3 + ic[k]])) for k in range(6)],
+              "B": [g.sub(IA["B"][3 * rr + cc], g.mul(U[rr], Ud[3 + cc])) for rr in range(3) for cc in range(3)]}
+        pa = g.vadd(g.vadd(pA, g.ai_apply(Ia, c)), [g.mul(x, ud) for x in U])
+        vpar = X.motion_to_parent(g.vsub(v, X.S(qdi)))
+        return (X.ai_to_parent(Ia), X.force_to_parent(pa)), vpar
+
+    def down_up(i, vp):
+        X = A.joint(i)
+        qdi = A.load(A.qdrefs[i])
+        v = X.S(qdi) if vp is None else g.vadd(X.motion_to_child(vp), X.S(qdi))
+        acc = None
+        for c in rb.children[i]:
+            (Ic, pc), v = down_up(c, v)
+            acc = (Ic, pc) if acc is None else (g.ai_add(acc[0], Ic), g.vadd(acc[1], pc))
+        return finish(i, v, acc)
+
+    def down(i, vp, ap, gvec=None):
+        udr, Udr = layout[i]
+        X = A.joint(i)
+        qdi = A.load(A.qdrefs[i])
+        if vp is None:
+            v = X.S(qdi)
+            a1 = X.motion_to_child(gvec)
+        else:
+            v = g.vadd(X.motion_to_child(vp), X.S(qdi))
+            a1 = g.vadd(X.motion_to_child(ap), g.crm(v, X.S(qdi)))
+        qdd = g.sub(A.load(udr), g.sdot([A.load(x) for x in Udr], a1))
+        g.output(0, i, qdd)
+        g.check_finite(qdd)
+        return v, g.vadd(a1, X.S(qdd))
+
+    # pass 1 down the trunk (every role)
+    v = None
+    for i in tr:
+        X = A.joint(i)
+        qdi = A.load(A.qdrefs[i])
+        v = X.S(qdi) if v is None else g.vadd(X.motion_to_child(v), X.S(qdi))
+    # passes 1-2 of the subtree, its contribution published in s's frame
+    (Ic, pc), v_s = down_up(kids[r], v)
+    vals = Ic["A"] + Ic["B"] + Ic["C"] + pc
+    for k, x in enumerate(vals):
+        g.raw(f"cx.xput({r * 27 + k}, {g.o(x)});")
+    g.raw("cx.role_sync();")
+    if r == 0:
+        acc = None
+        for rr in range(R):
+            got = [g.tmp(f"cx.xget({rr * 27 + k})", "xg") for k in range(27)]
+            c = ({"A": got[0:6], "B": got[6:15], "C": got[15:21]}, got[21:27])
+            acc = c if acc is None else (g.ai_add(acc[0], c[0]), g.vadd(acc[1], c[1]))
+        ret, vv = finish(s_, v_s, acc)
+        for i in reversed(tr[:-1]):
+            ret, vv = finish(i, vv, ret)
+        A.release(2)
+        gvec = A.gravity()
+        vp = ap = None
+        for i in tr:
+            vp, ap = down(i, vp, ap, gvec)
+        for k in range(6):
+            g.raw(f"cx.xput({R * 27 + k}, {g.o(ap[k])});")
+    A.release(2)
+    g.raw("cx.role_sync();")
+    a_s = [g.tmp(f"cx.xget({R * 27 + k})", "xa") for k in range(6)]
+
+    def down_sub(i, vp, ap):
+        vi, ai = down(i, vp, ap)
+        for c in rb.children[i]:
+            down_sub(c, vi, ai)
+
+    down_sub(kids[r], v_s, a_s)
     return A.finish()
 
 
@@ -1686,3 +1808,29 @@ def jit_source(lib, h, task_joints=(), cls="Jit"):
         lines += ["#define VD_JIT_TASKS 1"]
     lines += ["#include \"vd_jit_entry.cuh\"", ""]
     return "\n".join(lines), rb.d["fp"]
+
+
+def emit_op(name, A, rb, nin, nout):
+    """One generated routine as a struct with run<T>(Cx&)."""
+    out = [f"  // {name}: {A.g.flops} mul/add after folding; {A.nslot} slots",
+           f"  struct {name} {{",
+           f"    static constexpr int kSlots = {A.nslot};",
+           f"    static constexpr int kDof = {rb.n};",
+           f"    static constexpr int kPrologue = {A.nprologue};",
+           f"    static constexpr int kFlops = {A.g.flops};",
+           f"    static constexpr int kIn = {nin};",
+           f"    static constexpr int kOut = {nout};",
+           "    template <class T, class Cx>",
+           "    VD_HD static bool run(Cx& cx) {"]
+    out += ["    " + ln for ln in A.g.lines]
+    out += ["    }", "  };"]
+    return out
+
+
+def emit_roles(cls, rb):
+    """struct Gen<cls>Roles: the branch-parallel ABA's warp roles (gen_aba_role)."""
+    R = len(rb.children[trunk(rb)[-1]])
+    out = [f"struct Gen{cls}Roles {{", f"  static constexpr int kRoles = {R};", f"  static constexpr int kN = {rb.n};"]
+    for r in range(R):
+        out += emit_op(f"Role{r}", gen_aba_role(rb, r), rb, 3, rb.n)
+    return out + ["};", ""]
