@@ -110,6 +110,7 @@ class Gen:
         # (double) for the high-precision joints of a mixed-precision routine
         self.ty = "T"
         self.groups_read = set()  # input groups read through cx.x (see Algo.release)
+        self.on_input = None  # Algo's read-after-release guard
 
     # ---------------------------------------------------------------- emission
     def lit(self, c):
@@ -141,6 +142,8 @@ class Gen:
     # ---------------------------------------------------------------- hooks (overridden by DGen for JVPs)
     def input(self, gi, i):
         self.groups_read.add(gi)
+        if self.on_input:
+            self.on_input(gi)
         return self.tmp(f"cx.x({gi}, {i})", "x", ty="T")
 
     def sincos(self, q, i):
@@ -383,6 +386,8 @@ class DGen(Gen):
 
     def input(self, gi, i):
         self.groups_read.add(gi)
+        if self.on_input:
+            self.on_input(gi)
         return DualEx(self.tmp(f"cx.x({gi}, {i})", "x", ty="T"), self.tmp(f"cx.dx({gi}, {i})", "dx", ty="T"))
 
     def sincos(self, q, i):
@@ -569,7 +574,9 @@ class Algo:
             self.xrefs[key] = self.store(v)
         self.nprologue = self.nslot
         self.released = set()
+        self.release_line = {}
         self.nphase = 0
+        g.on_input = self._read_after_release
         for gi in sorted(g.groups_read):
             self.release(gi)
 
@@ -580,7 +587,16 @@ class Algo:
         Emitted once per group; finish() releases whatever is left."""
         if gi in self.g.groups_read and gi not in self.released:
             self.released.add(gi)
+            self.release_line[gi] = len(self.g.lines)
             self.g.raw(f"cx.fetch_next({gi});")
+
+    def _read_after_release(self, gi):
+        """A routine read group gi again after releasing it (OSC re-reads q
+        for the posture torque): withdraw the early release; finish()
+        releases the group after its last read."""
+        if gi in self.released:
+            self.released.discard(gi)
+            self.g.lines[self.release_line.pop(gi)] = f"  // group {gi} is read again below: released at the end"
 
     def store(self, v):
         if isinstance(v, DualEx):  # value and tangent in their own slots
@@ -1207,7 +1223,7 @@ def gen_osc(rb, fj):
     pkp, pkd = g.tmp("cx.pkp()", "pp"), g.tmp("cx.pkd()", "pp")
 
     def tpost(k):
-        qk = g.tmp(f"cx.x(0, {k})", "q")
+        qk = g.input(0, k)
         return g.sub(g.mul(pkp, g.sub(g.tmp(f"cx.post({k})", "pp"), qk)), g.mul(pkd, A.load(A.qdrefs[k])))
 
     for k in range(n):
@@ -1364,7 +1380,7 @@ def gen_osc_aba(rb, fj):
     pkp, pkd = g.tmp("cx.pkp()", "pp"), g.tmp("cx.pkd()", "pp")
 
     def tpost(k):  # τ_post = kp_p (q_post − q) − kd_p q̇ (control.hpp:150-151)
-        qk = g.tmp(f"cx.x(0, {k})", "q")
+        qk = g.input(0, k)
         return g.sub(g.mul(pkp, g.sub(g.tmp(f"cx.post({k})", "pp"), qk)), g.mul(pkd, A.load(A.qdrefs[k])))
 
     # ---- ABA pass 2 at q̇ = 0, a_g = 0 with τ = τ_post (RBDA Table 7.1)
