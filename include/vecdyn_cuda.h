@@ -254,7 +254,8 @@ int vd_shard_range(int64_t N, int world, int rank, int64_t* begin, int64_t* end)
  * e.g. a C array of per-state records or a torch (N, K) tensor) and the
  * planes every kernel above reads and writes (element (i, k) at
  * k*ld_planes + i, the reference's column-major StateBatch layout,
- * batch.hpp:15-19).  Coalesced on both sides (shared-memory staged). */
+ * batch.hpp:15-19).  Coalesced on both sides (shared-memory staged).  Runs
+ * on the calling thread's current device; both buffers must live on it. */
 int vd_rows_to_planes(int dtype, int64_t N, int K, const void* rows, int64_t ld_rows, void* planes,
                       int64_t ld_planes, void* stream);
 int vd_planes_to_rows(int dtype, int64_t N, int K, const void* planes, int64_t ld_planes, void* rows,

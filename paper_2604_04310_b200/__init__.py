@@ -401,7 +401,8 @@ def _to_planes(x):
     N, K = x.shape
     if N > 1 and K > 1 and x.stride() == (K, 1) and x.dtype in (torch.float64, torch.float32):
         out = torch.empty((K, N), dtype=x.dtype, device=x.device)
-        _check(_lib.load().vd_rows_to_planes(_dtype_code(x), N, K, _p(x), K, _p(out), N, _stream(x.device)))
+        with torch.cuda.device(x.device):  # the layout kernel runs on the current device
+            _check(_lib.load().vd_rows_to_planes(_dtype_code(x), N, K, _p(x), K, _p(out), N, _stream(x.device)))
         return out
     return x.t().contiguous()
 
