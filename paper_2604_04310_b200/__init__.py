@@ -35,7 +35,8 @@ __all__ = [
     "TaskGains", "TaskTarget", "PostureGains", "StateBatch", "robots", "urdf", "floating_base", "random_states",
     "rnea", "bias_forces", "gravity_vector", "coriolis_vector", "crba", "crba_packed", "unpack_crba", "forward_dynamics", "dynamics",
     "forward_kinematics", "forward_kinematics_scan", "frame_transform", "geometric_jacobian", "manipulability", "diff_ik_step", "osc_step", "batch_rnea", "batch_crba",
-    "forward_kinematics_jvp", "rnea_jvp", "crba_jvp", "forward_dynamics_jvp",
+    "forward_kinematics_jvp", "rnea_jvp", "crba_jvp", "forward_dynamics_jvp", "rnea_derivatives",
+    "forward_dynamics_derivatives",
     "batch_forward_dynamics", "shard_range",
 ]
 
@@ -656,6 +657,41 @@ def forward_dynamics_jvp(dm, q, qd, tau, dq=None, dqd=None, dtau=None, gravity=N
         raise SingularInertiaError(
             "forward_dynamics: mass matrix is not positive definite (zero-inertia degree of freedom?)")
     return out.t(), dout.t()
+
+
+def rnea_derivatives(dm, q, qd, qdd, gravity=None):
+    """(∂τ/∂q, ∂τ/∂q̇), each (N, n, n) with column j = the JVP along e_j:
+    jacobian_fwd (autodiff.hpp:67-84) of the batched RNEA, n passes of the
+    dual-number kernel per argument (∂τ/∂q̈ is M, crba)."""
+    return _jac_fwd(dm, q, lambda e, zero: rnea_jvp(dm, q, qd, qdd, e, zero, zero, gravity)[1],
+                    lambda e, zero: rnea_jvp(dm, q, qd, qdd, zero, e, zero, gravity)[1])
+
+
+def forward_dynamics_derivatives(dm, q, qd, tau, gravity=None):
+    """(∂q̈/∂q, ∂q̈/∂q̇, ∂q̈/∂τ), each (N, n, n): jacobian_fwd (autodiff.hpp:67-84)
+    of forward dynamics by the dual-number ABA, n passes per argument
+    (∂q̈/∂τ = M⁻¹).  SingularInertiaError as forward_dynamics."""
+    return _jac_fwd(dm, q, lambda e, zero: forward_dynamics_jvp(dm, q, qd, tau, e, zero, zero, gravity)[1],
+                    lambda e, zero: forward_dynamics_jvp(dm, q, qd, tau, zero, e, zero, gravity)[1],
+                    lambda e, zero: forward_dynamics_jvp(dm, q, qd, tau, zero, zero, e, gravity)[1])
+
+
+def _jac_fwd(dm, q, *tangent_fns):
+    torch = _torch()
+    qs = q if torch.is_tensor(q) else torch.as_tensor(np.asarray(q))
+    N, n = qs.shape[0], dm.dof()
+    dev = torch.device("cuda", dm.device)
+    dtype = qs.dtype if qs.dtype in (torch.float64, torch.float32) else torch.float64
+    zero = torch.zeros((N, n), dtype=dtype, device=dev)
+    outs = []
+    for fn in tangent_fns:
+        J = torch.empty((N, n, n), dtype=dtype, device=dev)
+        for j in range(n):
+            e = torch.zeros((N, n), dtype=dtype, device=dev)
+            e[:, j] = 1
+            J[:, :, j] = fn(e, zero)
+        outs.append(J)
+    return tuple(outs)
 
 
 def manipulability(dm, q, frame):

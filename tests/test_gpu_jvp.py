@@ -178,3 +178,38 @@ def test_jvp_errors_and_empty(vd, cuda):
     # ld < N
     assert lib.vd_fk_jvp(dm.handle, 0, 4, q.data_ptr(), None, 2, q.data_ptr(), None, 4,
                          None) == vd._lib.VD_ERR_DIMENSION
+
+
+@pytest.mark.parametrize("name", ["chain7", "tree29"])
+def test_dynamics_derivatives_identities(vd, cuda, omodels, name):
+    """jacobian_fwd (autodiff.hpp:67-84) of the batched dynamics from n JVP
+    passes: ∂q̈/∂τ = M⁻¹; the implicit-function identity ∂q̈/∂(q, q̇) =
+    −M⁻¹ ∂τ/∂(q, q̇) at q̈ = FD(q, q̇, τ); ∂τ/∂q̇ against central finite
+    differences of the oracle's RNEA."""
+    om = omodels[name]
+    dm = vd.DeviceModel(vd.robots.by_name(name), 0)
+    n = om.n
+    q, qd, _, tau = om.random_states(48, 501, True, True)
+    M = om.crba(q)
+    cond = np.linalg.cond(M)
+    keep = cond < 1e6  # identities through M⁻¹ lose ~κ(M)·ε
+    T = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda")  # noqa: E731
+    dq, dqd, dtau = (x.cpu().numpy() for x in vd.forward_dynamics_derivatives(dm, T(q), T(qd), T(tau)))
+    assert np.abs(np.einsum("nij,njk->nik", dtau, M) - np.eye(n))[keep].max() <= 1e-8
+    qdd = vd.forward_dynamics(dm, T(q), T(qd), T(tau)).cpu().numpy()
+    rq, rqd = (x.cpu().numpy() for x in vd.rnea_derivatives(dm, T(q), T(qd), T(qdd)))
+    Minv = np.linalg.inv(M)
+    scale = np.maximum(1.0, np.abs(dq).max(axis=(1, 2)))
+    assert (np.abs(dq + Minv @ rq).max(axis=(1, 2)) / scale)[keep].max() <= 1e-7
+    scale = np.maximum(1.0, np.abs(dqd).max(axis=(1, 2)))
+    assert (np.abs(dqd + Minv @ rqd).max(axis=(1, 2)) / scale)[keep].max() <= 1e-7
+    # finite differences at a bounded q̈ (at the FD q̈ of an ill-conditioned
+    # state |τ| reaches 1e6 and the difference quotient's rounding ~ε|τ|/h)
+    _, _, qdd_r, _ = om.random_states(48, 502, True, False)
+    _, rqd = (x.cpu().numpy() for x in vd.rnea_derivatives(dm, T(q), T(qd), T(qdd_r)))
+    h = 1e-6
+    for j in range(n):
+        e = np.zeros_like(qd)
+        e[:, j] = h
+        fd = (om.rnea(q, qd + e, qdd_r) - om.rnea(q, qd - e, qdd_r)) / (2 * h)
+        assert np.abs(rqd[:, :, j] - fd).max() / max(1.0, np.abs(fd).max()) <= 1e-6
