@@ -148,3 +148,52 @@ def test_jit_task_routines_match_oracle(vd, cuda, task_case):
     theta = np.linalg.norm(err_ref[:, :3], axis=1)
     klog = np.maximum(1.0, 1.0 / np.maximum(np.pi - theta, 1e-6) ** 2)
     assert np.all(rel_err(_np(qd_got), qd_ref, axis=1) <= np.maximum(TOL64, 1e-16 * np.linalg.cond(G) * klog))
+
+
+def _osc_ref_and_got(vd, om, dm, frame, N, seed, dtype):
+    q, qd, _, _ = om.random_states(N, seed, False, False)
+    pose0, _ = om.jacobian(np.zeros((1, om.n)), frame)
+    R0, p0 = pose0[0, :9].reshape(3, 3, order="F"), pose0[0, 9:]
+    tau_ref, lam_ref, st_ref = om.osc(q, qd, frame, R0, p0, [100.0] * 6, [20.0] * 6, [0.0] * 6, np.zeros(om.n),
+                                      10.0, 2.0)
+    tgt = vd.TaskTarget(frame, (R0, p0), vd.TaskGains.uniform(100.0, 20.0))
+    tau, lam, st = vd.osc_step(dm, _t(q, dtype), _t(qd, dtype), tgt, np.zeros(om.n), vd.PostureGains(10.0, 2.0),
+                               return_lambda=True, return_status=True)
+    return q, _np(tau), st.cpu().numpy(), tau_ref, lam_ref, st_ref
+
+
+def test_jit_task_routines_fp32(vd, cuda, task_case):
+    """fp32 OSC from the JIT module against the fp64 oracle: forward error
+    bounded by ε₃₂·κ(M)·κ(J M⁻¹ Jᵀ + εI), flat 1e-4 where that is small
+    (test_gpu_parity.test_osc_fp32's bound)."""
+    m, om, dm = task_case
+    q, tau, st, tau_ref, lam_ref, st_ref = _osc_ref_and_got(vd, om, dm, "l_palm", 1024, 95, torch.float32)
+    ok = (st == 0) & (st_ref == 0)
+    assert ok.mean() > 0.99
+    kappa = np.linalg.cond(om.crba(q)) * np.linalg.cond(lam_ref)
+    eps = np.finfo(np.float32).eps
+    e = rel_err(tau, tau_ref, axis=1)
+    assert np.all(e[ok] <= np.maximum(TOL32, om.n * eps * kappa[ok]))
+    well = ok & (kappa * eps < 1e-6)
+    assert e[well].max(initial=0) <= TOL32
+
+
+def test_jit_serial_chain_tasks(vd, cuda, oracle):
+    """A serial random chain: its JIT module's OSC is the M-based (LTL) form
+    (codegen picks it for chains), Jacobian and dynamics against the oracle."""
+    text = random_urdf(23, n=9, branchiness=0.0)
+    m, om = vd.urdf.load_model_from_string(text), OModel.from_urdf(text)
+    assert m.is_serial_chain()
+    dm = vd.DeviceModel(m, 0, jit=True, jit_frames=("tool",))
+    assert dm.uses_jit()
+    q, tau, st, tau_ref, lam_ref, st_ref = _osc_ref_and_got(vd, om, dm, "tool", 1024, 97, torch.float64)
+    assert np.all(st == st_ref)
+    ok = st == 0
+    kappa = np.linalg.cond(om.crba(q)) * np.linalg.cond(lam_ref)
+    assert np.all(rel_err(tau, tau_ref, axis=1)[ok] <= np.maximum(TOL64, 1e-16 * kappa[ok]))
+    # above the serial-chain scan threshold (32768 states): the module's Jacobian routine
+    q, _, _, _ = om.random_states(40000, 98, False, False)
+    pose_ref, J_ref = om.jacobian(q, "tool")
+    assert rel_err(_np(vd.geometric_jacobian(dm, _t(q), "tool")), J_ref, axis=1).max() <= TOL64
+    qd = np.zeros_like(q)
+    assert rel_err(_np(vd.rnea(dm, _t(q), _t(qd), _t(q))), om.rnea(q, qd, q), axis=1).max() <= TOL64
