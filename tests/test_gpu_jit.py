@@ -197,3 +197,17 @@ def test_jit_serial_chain_tasks(vd, cuda, oracle):
     assert rel_err(_np(vd.geometric_jacobian(dm, _t(q), "tool")), J_ref, axis=1).max() <= TOL64
     qd = np.zeros_like(q)
     assert rel_err(_np(vd.rnea(dm, _t(q), _t(qd), _t(q))), om.rnea(q, qd, q), axis=1).max() <= TOL64
+
+
+def test_builtin_robots_keep_compiled_in_kernels(vd, cuda):
+    """jit=True is a no-op for the builtin robots (their generated kernels are
+    compiled in), and a forced-generic device model never uses a module."""
+    for name, spec in (("chain7", 1), ("tree29", 2)):
+        dm = vd.DeviceModel(vd.robots.by_name(name), 0, jit=True)
+        assert dm.specialization() == spec and not dm.uses_jit()
+    m = vd.urdf.load_model_from_string(random_urdf(5, n=12))
+    from paper_2604_04310_b200 import jit
+
+    jit.attach(m)
+    assert vd.DeviceModel(m, 0).uses_jit()
+    assert not vd.DeviceModel(m, 0, generic=True).uses_jit()
