@@ -286,6 +286,20 @@ inline void forward_dynamics(const DeviceModel& dm, DType t, int64_t N, const vo
                              void* stream = nullptr) {
   detail::check(vd_aba(dm.handle(), (int)t, N, q, qd, tau, N, g.accel, fext, qdd, N, status, stream));
 }
+// Per-state gravity (no reference analogue): gravity_planes = 3 device planes
+// of a_g (= −field), state i's vector at (gravity_planes[i], [N + i], [2N + i]).
+struct GravityPlanes {
+  const void* planes;
+};
+inline void rnea(const DeviceModel& dm, DType t, int64_t N, const void* q, const void* qd, const void* qdd,
+                 void* tau, GravityPlanes g, const void* fext = nullptr, void* stream = nullptr) {
+  detail::check(vd_rnea_pg(dm.handle(), (int)t, N, q, qd, qdd, N, g.planes, fext, tau, N, stream));
+}
+inline void forward_dynamics(const DeviceModel& dm, DType t, int64_t N, const void* q, const void* qd,
+                             const void* tau, void* qdd, int32_t* status, GravityPlanes g,
+                             const void* fext = nullptr, void* stream = nullptr) {
+  detail::check(vd_aba_pg(dm.handle(), (int)t, N, q, qd, tau, N, g.planes, fext, qdd, N, status, stream));
+}
 inline void forward_kinematics(const DeviceModel& dm, DType t, int64_t N, const void* q, void* frames,
                                void* stream = nullptr) {
   detail::check(vd_fk(dm.handle(), (int)t, N, q, N, frames, N, stream));

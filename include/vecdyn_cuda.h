@@ -179,6 +179,26 @@ int vd_dynamics(vd_device_model dm, int dtype, int64_t N, const void* q, const v
                 int64_t ld_in, const double* gravity3, void* M_out, void* bias_out, void* qdd_out, int64_t ld_out,
                 int32_t* status_out, void* stream);
 
+/* Per-state gravity (no reference analogue: GravitySpec is one
+ * per call, dynamics.hpp:35-50).  The same calls as vd_rnea / vd_bias /
+ * vd_gravity / vd_aba / vd_dynamics, with state i's base acceleration a_g read
+ * from gravity_planes: 3 planes (x, y, z of a_g = −field) of dtype elements
+ * with leading dimension ld_in.  Results equal the per-call entry point run on
+ * state i alone with gravity3 = (its a_g). */
+int vd_rnea_pg(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* qdd,
+               int64_t ld_in, const void* gravity_planes, const void* fext, void* tau_out, int64_t ld_out,
+               void* stream);
+int vd_bias_pg(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in,
+               const void* gravity_planes, const void* fext, void* out, int64_t ld_out, void* stream);
+int vd_gravity_pg(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, const void* gravity_planes,
+                  void* out, int64_t ld_out, void* stream);
+int vd_aba_pg(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau, int64_t ld_in,
+              const void* gravity_planes, const void* fext, void* qdd_out, int64_t ld_out, int32_t* status_out,
+              void* stream);
+int vd_dynamics_pg(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau,
+                   int64_t ld_in, const void* gravity_planes, void* M_out, void* bias_out, void* qdd_out,
+                   int64_t ld_out, int32_t* status_out, void* stream);
+
 /* osc_step, control.hpp:108-155.  Shared task / posture parameters. */
 typedef struct vd_osc_params {
   int frame;              /* vd_model_frame_index */

@@ -448,15 +448,37 @@ def _p(t):
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
 
 
+def _gravity(gravity, N, dtype, dev):
+    """(gravity3 for the per-call entry point, None) for a GravitySpec or None;
+    (None, (3, N) planes) for per-state gravity: an (N, 3) array of a_g = −field
+    (vd_*_pg; the reference's GravitySpec is one per call, dynamics.hpp:35-50)."""
+    if gravity is None or isinstance(gravity, GravitySpec):
+        return (gravity or GravitySpec.standard()).c(), None
+    torch = _torch()
+    if torch.is_tensor(gravity) and gravity.is_cuda and gravity.device != dev:
+        raise CudaError(f"gravity is on {gravity.device}, the device model is on {dev}")
+    g = torch.as_tensor(gravity if torch.is_tensor(gravity) else np.asarray(gravity), dtype=dtype, device=dev)
+    if tuple(g.shape) != (N, 3):
+        raise DimensionError(f"per-state gravity has shape {tuple(g.shape)}, expected ({N}, 3)")
+    if N == 0:
+        return GravitySpec.standard().c(), None
+    return None, _to_planes(g)
+
+
 def rnea(dm, q, qd, qdd, gravity=None, fext=None):
     """rnea(model, q, qd, qdd, gravity, fext) — dynamics.hpp:250-267; (N, n) torques."""
     qs, (qds, qdds), N, dev = _prep(dm, q, (qd, "qd"), (qdd, "qdd"))
     n = dm.dof()
     out = _out(dev, qs.dtype, n, N)
     fx = _fext_planes(fext, N, n, qs.dtype, dev)
-    g = (gravity or GravitySpec.standard()).c()
-    _check(_lib.load().vd_rnea(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(qdds), N, g, _p(fx), _p(out), N,
-                               _stream(dev)))
+    g, gp = _gravity(gravity, N, qs.dtype, dev)
+    lib = _lib.load()
+    if gp is None:
+        _check(lib.vd_rnea(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(qdds), N, g, _p(fx), _p(out), N,
+                           _stream(dev)))
+    else:
+        _check(lib.vd_rnea_pg(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(qdds), N, _p(gp), _p(fx), _p(out), N,
+                              _stream(dev)))
     return out.t()
 
 
@@ -466,8 +488,13 @@ def bias_forces(dm, q, qd, gravity=None, fext=None):
     n = dm.dof()
     out = _out(dev, qs.dtype, n, N)
     fx = _fext_planes(fext, N, n, qs.dtype, dev)
-    g = (gravity or GravitySpec.standard()).c()
-    _check(_lib.load().vd_bias(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), N, g, _p(fx), _p(out), N, _stream(dev)))
+    g, gp = _gravity(gravity, N, qs.dtype, dev)
+    lib = _lib.load()
+    if gp is None:
+        _check(lib.vd_bias(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), N, g, _p(fx), _p(out), N, _stream(dev)))
+    else:
+        _check(lib.vd_bias_pg(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), N, _p(gp), _p(fx), _p(out), N,
+                              _stream(dev)))
     return out.t()
 
 
@@ -475,8 +502,12 @@ def gravity_vector(dm, q, gravity=None):
     """dynamics.hpp:402-408."""
     qs, _, N, dev = _prep(dm, q)
     out = _out(dev, qs.dtype, dm.dof(), N)
-    g = (gravity or GravitySpec.standard()).c()
-    _check(_lib.load().vd_gravity(dm.handle, _dtype_code(qs), N, _p(qs), N, g, _p(out), N, _stream(dev)))
+    g, gp = _gravity(gravity, N, qs.dtype, dev)
+    lib = _lib.load()
+    if gp is None:
+        _check(lib.vd_gravity(dm.handle, _dtype_code(qs), N, _p(qs), N, g, _p(out), N, _stream(dev)))
+    else:
+        _check(lib.vd_gravity_pg(dm.handle, _dtype_code(qs), N, _p(qs), N, _p(gp), _p(out), N, _stream(dev)))
     return out.t()
 
 
@@ -533,9 +564,14 @@ def forward_dynamics(dm, q, qd, tau, gravity=None, fext=None, return_status=Fals
     out = _out(dev, qs.dtype, n, N)
     status = torch.zeros(N, dtype=torch.int32, device=dev)
     fx = _fext_planes(fext, N, n, qs.dtype, dev)
-    g = (gravity or GravitySpec.standard()).c()
-    _check(_lib.load().vd_aba(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(taus), N, g, _p(fx), _p(out), N,
-                              _p(status), _stream(dev)))
+    g, gp = _gravity(gravity, N, qs.dtype, dev)
+    lib = _lib.load()
+    if gp is None:
+        _check(lib.vd_aba(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(taus), N, g, _p(fx), _p(out), N,
+                          _p(status), _stream(dev)))
+    else:
+        _check(lib.vd_aba_pg(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(taus), N, _p(gp), _p(fx), _p(out), N,
+                             _p(status), _stream(dev)))
     if return_status:
         return out.t(), status
     if N and int(status.max().item()) != 0:
@@ -553,9 +589,14 @@ def dynamics(dm, q, qd, tau, gravity=None):
     b = _out(dev, qs.dtype, n, N)
     a = _out(dev, qs.dtype, n, N)
     status = torch.zeros(N, dtype=torch.int32, device=dev)
-    g = (gravity or GravitySpec.standard()).c()
-    _check(_lib.load().vd_dynamics(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(taus), N, g, _p(M), _p(b), _p(a),
-                                   N, _p(status), _stream(dev)))
+    g, gp = _gravity(gravity, N, qs.dtype, dev)
+    lib = _lib.load()
+    if gp is None:
+        _check(lib.vd_dynamics(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(taus), N, g, _p(M), _p(b), _p(a), N,
+                               _p(status), _stream(dev)))
+    else:
+        _check(lib.vd_dynamics_pg(dm.handle, _dtype_code(qs), N, _p(qs), _p(qds), _p(taus), N, _p(gp), _p(M), _p(b),
+                                  _p(a), N, _p(status), _stream(dev)))
     return M.t().reshape(N, n, n).transpose(1, 2), b.t(), a.t(), status
 
 

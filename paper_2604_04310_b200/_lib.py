@@ -89,6 +89,11 @@ SIGNATURES = {
     "vd_crba_packed": (c_int, [P, c_int, c_int64, P, c_int64, P, c_int64, P]),
     "vd_aba": (c_int, [P, c_int, c_int64, P, P, P, c_int64, Pd, P, P, c_int64, P, P]),
     "vd_dynamics": (c_int, [P, c_int, c_int64, P, P, P, c_int64, Pd, P, P, P, c_int64, P, P]),
+    "vd_rnea_pg": (c_int, [P, c_int, c_int64, P, P, P, c_int64, P, P, P, c_int64, P]),
+    "vd_bias_pg": (c_int, [P, c_int, c_int64, P, P, c_int64, P, P, P, c_int64, P]),
+    "vd_gravity_pg": (c_int, [P, c_int, c_int64, P, c_int64, P, P, c_int64, P]),
+    "vd_aba_pg": (c_int, [P, c_int, c_int64, P, P, P, c_int64, P, P, P, c_int64, P, P]),
+    "vd_dynamics_pg": (c_int, [P, c_int, c_int64, P, P, P, c_int64, P, P, P, P, c_int64, P, P]),
     "vd_osc": (c_int, [P, c_int, c_int64, P, P, c_int64, ctypes.POINTER(OscParams), P, P, c_int64, P, P]),
     "vd_diff_ik": (c_int, [P, c_int, c_int64, P, c_int64, ctypes.POINTER(TaskParams), P, P, c_int64, P, P]),
     "vd_manipulability": (c_int, [P, c_int, c_int64, P, c_int64, c_int, P, P]),

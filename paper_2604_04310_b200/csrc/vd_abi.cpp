@@ -438,16 +438,18 @@ int vd_jacobian(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t
 
 static int rnea_mode(vd_device_model dm, int dtype, int mode, int64_t N, const void* q, const void* qd,
                      const void* qdd, int64_t ld_in, const double* g3, const void* fext, void* out, int64_t ld_out,
-                     void* stream) {
+                     void* stream, const void* gravity_planes = nullptr, bool pg = false) {
   if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  if (pg) VD_NEED(gravity_planes, "gravity_planes");
   VD_NEED(q, "q");
   if (mode != 2) VD_NEED(qd, "qd");
   if (mode == 0) VD_NEED(qdd, "qdd");
   VD_NEED(out, "output");
   if (dm->n == 0) return VD_OK;
   DeviceGuard g(dm->device);
-  return finish(vdk::launch_rnea(make_launch(dm, dtype, N, ld_in, ld_out, stream), mode, q, qd, qdd, g3, fext, out),
-                "vd_rnea");
+  vdk::Launch L = make_launch(dm, dtype, N, ld_in, ld_out, stream);
+  L.gravity_planes = gravity_planes;
+  return finish(vdk::launch_rnea(L, mode, q, qd, qdd, g3, fext, out), "vd_rnea");
 }
 int vd_rnea(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* qdd, int64_t ld_in,
             const double* g3, const void* fext, void* tau, int64_t ld_out, void* stream) {
@@ -460,6 +462,20 @@ int vd_bias(vd_device_model dm, int dtype, int64_t N, const void* q, const void*
 int vd_gravity(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, const double* g3, void* out,
                int64_t ld_out, void* stream) {
   return rnea_mode(dm, dtype, 2, N, q, nullptr, nullptr, ld_in, g3, nullptr, out, ld_out, stream);
+}
+// per-state gravity: the same calls with a_g read from 3 planes
+int vd_rnea_pg(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* qdd,
+               int64_t ld_in, const void* gravity_planes, const void* fext, void* tau, int64_t ld_out, void* stream) {
+  return rnea_mode(dm, dtype, 0, N, q, qd, qdd, ld_in, nullptr, fext, tau, ld_out, stream, gravity_planes, true);
+}
+int vd_bias_pg(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in,
+               const void* gravity_planes, const void* fext, void* out, int64_t ld_out, void* stream) {
+  return rnea_mode(dm, dtype, 1, N, q, qd, nullptr, ld_in, nullptr, fext, out, ld_out, stream, gravity_planes, true);
+}
+int vd_gravity_pg(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, const void* gravity_planes,
+                  void* out, int64_t ld_out, void* stream) {
+  return rnea_mode(dm, dtype, 2, N, q, nullptr, nullptr, ld_in, nullptr, nullptr, out, ld_out, stream, gravity_planes,
+                   true);
 }
 int vd_coriolis(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in, void* out,
                 int64_t ld_out, void* stream) {
@@ -496,9 +512,11 @@ int vd_crba_packed(vd_device_model dm, int dtype, int64_t N, const void* q, int6
                 "vd_crba_packed");
 }
 
-int vd_aba(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau, int64_t ld_in,
-           const double* g3, const void* fext, void* qdd, int64_t ld_out, int32_t* status, void* stream) {
+static int aba_call(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau,
+                    int64_t ld_in, const double* g3, const void* gravity_planes, const void* fext, void* qdd,
+                    int64_t ld_out, int32_t* status, void* stream, bool pg = false) {
   if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  if (pg) VD_NEED(gravity_planes, "gravity_planes");
   VD_NEED(q, "q");
   VD_NEED(qd, "qd");
   VD_NEED(tau, "tau");
@@ -509,22 +527,43 @@ int vd_aba(vd_device_model dm, int dtype, int64_t N, const void* q, const void* 
     return VD_OK;
   }
   DeviceGuard g(dm->device);
-  return finish(vdk::launch_aba(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, qd, tau, g3, fext, qdd, status),
-                "vd_aba");
+  vdk::Launch L = make_launch(dm, dtype, N, ld_in, ld_out, stream);
+  L.gravity_planes = gravity_planes;
+  return finish(vdk::launch_aba(L, q, qd, tau, g3, fext, qdd, status), "vd_aba");
+}
+int vd_aba(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau, int64_t ld_in,
+           const double* g3, const void* fext, void* qdd, int64_t ld_out, int32_t* status, void* stream) {
+  return aba_call(dm, dtype, N, q, qd, tau, ld_in, g3, nullptr, fext, qdd, ld_out, status, stream);
+}
+int vd_aba_pg(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau, int64_t ld_in,
+              const void* gravity_planes, const void* fext, void* qdd, int64_t ld_out, int32_t* status, void* stream) {
+  return aba_call(dm, dtype, N, q, qd, tau, ld_in, nullptr, gravity_planes, fext, qdd, ld_out, status, stream, true);
 }
 
-int vd_dynamics(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau,
-                int64_t ld_in, const double* g3, void* M, void* bias, void* qdd, int64_t ld_out, int32_t* status,
-                void* stream) {
+static int dynamics_call(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau,
+                         int64_t ld_in, const double* g3, const void* gravity_planes, void* M, void* bias, void* qdd,
+                         int64_t ld_out, int32_t* status, void* stream, bool pg = false) {
   if (int rc = check_common(dm, dtype, N, ld_in, ld_out)) return rc;
+  if (pg) VD_NEED(gravity_planes, "gravity_planes");
   VD_NEED(q, "q");
   VD_NEED(qd, "qd");
   if (qdd) VD_NEED(tau, "tau");
   if (dm->n == 0) return VD_OK;
   DeviceGuard g(dm->device);
-  return finish(vdk::launch_dynamics(make_launch(dm, dtype, N, ld_in, ld_out, stream), q, qd, tau, g3, M, bias, qdd,
-                                     status),
-                "vd_dynamics");
+  vdk::Launch L = make_launch(dm, dtype, N, ld_in, ld_out, stream);
+  L.gravity_planes = gravity_planes;
+  return finish(vdk::launch_dynamics(L, q, qd, tau, g3, M, bias, qdd, status), "vd_dynamics");
+}
+int vd_dynamics(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau,
+                int64_t ld_in, const double* g3, void* M, void* bias, void* qdd, int64_t ld_out, int32_t* status,
+                void* stream) {
+  return dynamics_call(dm, dtype, N, q, qd, tau, ld_in, g3, nullptr, M, bias, qdd, ld_out, status, stream);
+}
+int vd_dynamics_pg(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, const void* tau,
+                   int64_t ld_in, const void* gravity_planes, void* M, void* bias, void* qdd, int64_t ld_out,
+                   int32_t* status, void* stream) {
+  return dynamics_call(dm, dtype, N, q, qd, tau, ld_in, nullptr, gravity_planes, M, bias, qdd, ld_out, status, stream,
+                       true);
 }
 
 int vd_osc(vd_device_model dm, int dtype, int64_t N, const void* q, const void* qd, int64_t ld_in,

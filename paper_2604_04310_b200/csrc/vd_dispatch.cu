@@ -101,9 +101,11 @@ int launch_jacobian(const Launch& L, const void* q, int frame_joint, const doubl
   return with_view(L, [&](auto mv) { return Launcher<decltype(mv)>::jac(mv, L, q, fr, pose, J); });
 }
 
-int launch_rnea(const Launch& L, int mode, const void* q, const void* qd, const void* qdd, const double* g3,
+int launch_rnea(const Launch& L0, int mode, const void* q, const void* qd, const void* qdd, const double* g3,
                 const void* fext, void* tau) {
-  if (L.N == 0) return 0;
+  if (L0.N == 0) return 0;
+  Launch L = L0;
+  if (mode == 3) L.gravity_planes = nullptr;  // Coriolis: no gravity term at all
   static const double zero3[3] = {0, 0, 0};
   const double* g = (mode == 3) ? zero3 : g3;
   const void* qd_ = (mode == 2) ? nullptr : qd;
@@ -181,7 +183,9 @@ int launch_aba(const Launch& L, const void* q, const void* qd, const void* tau, 
 int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
                     void* bias, void* qdd, int32_t* status) {
   if (L.N == 0) return 0;
-  if (L.jit) {  // the JIT module's routines, one launch per output (as tree29 below)
+  // the JIT module's routines, one launch per output (as tree29 below); per-state
+  // gravity takes the same split (the fused loop kernel reads one a_g)
+  if (L.jit || L.gravity_planes) {
     int rc = 0;
     if (M && (rc = launch_crba(L, q, M)) != 0) return rc;
     if (bias && (rc = launch_rnea(L, 1, q, qd, nullptr, g3, nullptr, bias)) != 0) return rc;

@@ -80,6 +80,7 @@ struct GenCx {
   const T* in_[3];  // &x_g[i]; element (i, j) of input g at in_[g][j * ld]
   T* out_;          // &y[i]; element (i, k) at out_[k * ldo]
   const T* fx_;     // &fext[i] (NULL: no external wrenches); plane 6 j + k at fx_[(6 j + k) * ld]
+  const T* gp_ = nullptr;  // &gravity_planes[i] (NULL: g3); a_g component k at gp_[k * ld]
   T* sb;            // this thread's scratch: slot k at sb[(k - kSmem) * 32] (warp-interleaved)
   uint32_t sm;      // shared address of slot 0 for this thread ([k][threadIdx.x])
   int64_t ld, ldo;
@@ -105,7 +106,13 @@ struct GenCx {
       if constexpr (K % kSyncEvery == 0) __syncthreads();
     }
   }
-  __device__ __forceinline__ T g(int k) const { return g3[k]; }
+  __device__ __forceinline__ T g(int k) const {
+    if (gp_) {
+      if constexpr (kStream) return __ldcs(gp_ + k * ld);
+      else return GenMem<T>::ldg(gp_ + k * ld);
+    }
+    return g3[k];
+  }
   __device__ __forceinline__ void st(int k, T v) {
     if (k >= kSlots - kReg) reg[k - (kSlots - kReg)] = v;
     else if (k < kSmem) GenMem<T>::sts(sm + (uint32_t)(k * kBlk * sizeof(T)), v);
@@ -152,7 +159,7 @@ template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false,
 __global__ void __launch_bounds__(kBlk, kMinB)
     k_gen(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
           T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status, T* __restrict__ scratch,
-          const T* __restrict__ fext) {
+          const T* __restrict__ fext, const T* __restrict__ gpl) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
   using Cx = GenCx<T, Op::kSlots, kReg, kSmem, kFast, kStream, kSyncEvery, kBlk>;
   Cx cx;
@@ -179,6 +186,7 @@ __global__ void __launch_bounds__(kBlk, kMinB)
     cx.in_[2] = (Op::kIn > 2 ? x2 : x0) + i;
     cx.out_ = y + i;
     cx.fx_ = fext ? fext + i : nullptr;
+    cx.gp_ = gpl ? gpl + i : nullptr;
     const bool ok = Op::template run<T>(cx);
     if (cx.active) {
       if (!ok) {
@@ -221,6 +229,8 @@ struct GenAsyncCx : GenCx<T, kSlots, kReg, kSmem, kFast, kStream, kSyncEvery> {
   }
   __device__ __forceinline__ T x(int g, int j) const { return GenMem<T>::lds(ib + off(g, j)); }
   __device__ __forceinline__ void fetch_next(int g) const { fetch(ib, nx[g], this->ld, g, pol); }
+  // the call's a_g only: per-state gravity runs k_gen (launch_t)
+  __device__ __forceinline__ T g(int k) const { return this->g3[k]; }
   static __device__ __forceinline__ void fetch(uint32_t ib, const T* src, int64_t ld, int g, uint64_t pol) {
 #pragma unroll
     for (int j = 0; j < kDof; ++j) vd_cp_async<kStream>(ib + off(g, j), src + j * ld, pol);
@@ -233,13 +243,14 @@ constexpr size_t gen_async_smem() {
   return (size_t)(kSmem + Op::kIn * Op::kDof) * kGenBlock * sizeof(T);
 }
 
-// k_gen with asynchronous state input (same arguments, same results).
+// k_gen with asynchronous state input (same arguments, same results; gpl must
+// be NULL: launch_t sends per-state gravity to k_gen).
 template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false, bool kStream = false,
           int kSyncEvery = 0>
 __global__ void __launch_bounds__(kGenBlock, kMinB)
     k_gen_async(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
                 T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status,
-                T* __restrict__ scratch, const T* __restrict__ fext) {
+                T* __restrict__ scratch, const T* __restrict__ fext, const T* __restrict__ gpl) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
   using Cx = GenAsyncCx<T, Op::kSlots, kReg, kSmem, kFast, kStream, Op::kDof, kSyncEvery>;
   Cx cx;

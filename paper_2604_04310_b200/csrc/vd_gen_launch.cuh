@@ -46,9 +46,9 @@ inline bool debug_launches() {
 }
 
 // Occupancy (and the dynamic shared-memory opt-in) once per device for each
-// kernel instantiation; keyed by <Op, T>, not by the kernel's function type
-// (all variants of one dtype share it).
-template <class Op, class T, class Kern>
+// kernel instantiation; keyed by <Op, T, kVariant>, not by the kernel's
+// function type (all kernels of one dtype share that).
+template <class Op, class T, int kVariant = 0, class Kern>
 Occ occupancy(Kern kern, size_t smem) {
   static std::mutex mu;
   static Occ occ[64];
@@ -65,28 +65,27 @@ Occ occupancy(Kern kern, size_t smem) {
   return c;
 }
 
-// The kernel a Cfg selects (only that one is instantiated).
-template <class Op, class T, class C>
+// The kernel of a Cfg: asynchronous state input when it asks for it.
+template <class Op, class T, class C, bool kAsync>
 constexpr auto gen_kernel() {
-  if constexpr (AsyncIo<C>::value)
+  if constexpr (kAsync)
     return k_gen_async<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
   else
     return k_gen<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
 }
 
-template <class Op, class T>
-int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
-             int32_t* status, const void* fext = nullptr) {
+template <class Op, class T, bool kAsync>
+int launch_gen(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
+               int32_t* status, const void* fext) {
   using C = Cfg<Op, T>;
-  constexpr bool kAsync = AsyncIo<C>::value;
-  auto kern = gen_kernel<Op, T, C>();
+  auto kern = gen_kernel<Op, T, C, kAsync>();
   constexpr size_t smem = kAsync ? gen_async_smem<Op, T, C::kReg, C::kSmem>() : (size_t)C::kSmem * kGenBlock * sizeof(T);
-  const Occ o = occupancy<Op, T>(kern, smem);
+  const Occ o = occupancy<Op, T, kAsync>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
   cudaStream_t s = static_cast<cudaStream_t>(L.stream);
   if (debug_launches())
-    std::fprintf(stderr, "[vd] k_gen slots %d reg %d smem %d: %d CTAs/SM x %d SMs, grid %lld, smem %zu B\n", Op::kSlots,
-                 C::kReg, C::kSmem, o.blocks_per_sm, o.sms, (long long)blocks, smem);
+    std::fprintf(stderr, "[vd] k_gen%s slots %d reg %d smem %d: %d CTAs/SM x %d SMs, grid %lld, smem %zu B\n",
+                 kAsync ? "_async" : "", Op::kSlots, C::kReg, C::kSmem, o.blocks_per_sm, o.sms, (long long)blocks, smem);
   // L2-resident scratch for the slots that are neither in registers nor in
   // shared memory: one slab per resident thread, stream-ordered from the
   // library's private pool (scratch_alloc: no synchronisation, safe for
@@ -99,10 +98,24 @@ int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, co
   // gravity3 == NULL: GravitySpec::standard() (dynamics.hpp:39-50), as g3_of
   const T g0 = g3 ? T(g3[0]) : T(0), g1 = g3 ? T(g3[1]) : T(0), g2 = g3 ? T(g3[2]) : T(9.81);
   kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, (const T*)x0, (const T*)x1, (const T*)x2, L.ld_in, g0, g1, g2,
-                                                 (T*)y, L.ld_out, status, scratch, (const T*)fext);
+                                                 (T*)y, L.ld_out, status, scratch, (const T*)fext,
+                                                 (const T*)L.gravity_planes);
   cudaError_t e = cudaGetLastError();
   scratch_free(scratch, s);
   return (int)e;
+}
+
+// One generated routine over the batch.  Per-state gravity (L.gravity_planes)
+// runs the plain kernel even where the Cfg asks for asynchronous input: the
+// asynchronous kernel (the headline Panda ABA) carries no per-state gravity
+// load at all.
+template <class Op, class T>
+int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
+             int32_t* status, const void* fext = nullptr) {
+  if constexpr (AsyncIo<Cfg<Op, T>>::value) {
+    if (!L.gravity_planes) return launch_gen<Op, T, true>(L, x0, x1, x2, g3, y, status, fext);
+  }
+  return launch_gen<Op, T, false>(L, x0, x1, x2, g3, y, status, fext);
 }
 
 template <class Op>

@@ -18,6 +18,11 @@ template <class T>
 struct G3 {
   T g[3];
 };
+// a_g of state i from the gravity planes (Launch::gravity_planes)
+template <class T>
+__device__ __forceinline__ G3<T> per_state_gravity(const T* __restrict__ gpl, int64_t ld, int64_t i) {
+  return G3<T>{{gpl[i], gpl[ld + i], gpl[2 * ld + i]}};
+}
 
 template <bool kFastTrig = false, class V, class A>
 __device__ __forceinline__ void load_motion(const V& mv, const A& q, JM<typename V::S>* jm) {
@@ -151,11 +156,13 @@ __global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_rnea(const __grid_con
                                                   const typename V::Real* __restrict__ qd,
                                                   const typename V::Real* __restrict__ qdd, int64_t ldi,
                                                   G3<typename V::Real> g, const typename V::Real* __restrict__ fext,
-                                                  typename V::Real* __restrict__ tau, int64_t ldo) {
+                                                  typename V::Real* __restrict__ tau, int64_t ldo,
+                                                  const typename V::Real* __restrict__ gpl) {
   using T = typename V::Real;
   using S = typename V::S;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= N) return;
+  if (gpl) g = per_state_gravity(gpl, ldi, i);
   JM<S> jm[V::kMax];
   load_motion(mv, cols(q, ldi, i), jm);
   const Cols<T> qdc{qd, ldi, i}, qddc{qdd, ldi, i}, fc{fext, ldi, i};
@@ -203,11 +210,12 @@ __global__ void __launch_bounds__(kBlock, V::kMinBlocks) k_aba(const __grid_cons
                                                  const typename V::Real* __restrict__ tau, int64_t ldi,
                                                  G3<typename V::Real> g, const typename V::Real* __restrict__ fext,
                                                  typename V::Real* __restrict__ qdd, int64_t ldo,
-                                                 int32_t* __restrict__ status) {
+                                                 int32_t* __restrict__ status, const typename V::Real* __restrict__ gpl) {
   using T = typename V::Real;
   using S = typename V::S;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= N) return;
+  if (gpl) g = per_state_gravity(gpl, ldi, i);
   JM<S> jm[V::kMax];
   load_motion(mv, cols(q, ldi, i), jm);
   const Cols<T> qdc{qd, ldi, i}, tc{tau, ldi, i}, fc{fext, ldi, i};

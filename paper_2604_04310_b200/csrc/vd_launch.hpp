@@ -27,7 +27,7 @@ enum JitOp : int {
   kJitAba = 0, kJitRnea = 1, kJitBias = 2, kJitGravity = 3, kJitCoriolis = 4, kJitCrba = 5, kJitCrbaPacked = 6,
   kJitFk = 7
 };
-constexpr int kJitAbi = 1;
+constexpr int kJitAbi = 2;  // 2: Launch::gravity_planes
 using JitLaunchFn = int (*)(int op, const Launch* L, const void* x0, const void* x1, const void* x2,
                             const double* g3, const void* fext, void* y, int32_t* status);
 // which: 0 Jacobian, 1 diff-IK, 2 manipulability (params TaskShared*), 3 OSC (params OscShared*)
@@ -45,6 +45,10 @@ struct Launch {
   JitLaunchFn jit = nullptr;  // the model's JIT module, if one is attached
   JitTaskFn jit_task = nullptr;  // its task-space routines, for the frame joints in jit_task_mask
   uint64_t jit_task_mask = 0;
+  // Per-state gravity (vd_*_pg): 3 planes of a_g (= −field) with leading
+  // dimension ld_in, in the call's dtype; NULL = the call's gravity3.  Read by
+  // the RNEA (full / bias / gravity vector) and ABA kernels only.
+  const void* gravity_planes = nullptr;
 };
 
 struct OscShared;

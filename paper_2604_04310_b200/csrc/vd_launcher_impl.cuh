@@ -85,7 +85,8 @@ template <class V>
 int Launcher<V>::rnea(const V& mv, const Launch& L, const void* q, const void* qd, const void* qdd, const double* g,
                       const void* fext, void* tau) {
   using T = typename V::Real;
-  if (!fext) {
+  const T* gpl = static_cast<const T*>(L.gravity_planes);
+  if (!fext && !gpl) {
     int rc;
     if (qdd) rc = try_tiled(mv, L, OpRNEA<T, 3>{g3_of<T>(g), (T*)tau, L.ld_out}, q, qd, qdd);
     else if (qd) rc = try_tiled(mv, L, OpRNEA<T, 2>{g3_of<T>(g), (T*)tau, L.ld_out}, q, qd, nullptr);
@@ -94,10 +95,11 @@ int Launcher<V>::rnea(const V& mv, const Launch& L, const void* q, const void* q
   }
   if (fext)
     k_rnea<V, true><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, (const T*)qd, (const T*)qdd,
-                                                                L.ld_in, g3_of<T>(g), (const T*)fext, (T*)tau, L.ld_out);
+                                                                L.ld_in, g3_of<T>(g), (const T*)fext, (T*)tau, L.ld_out,
+                                                                gpl);
   else
     k_rnea<V, false><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, (const T*)qd, (const T*)qdd,
-                                                                 L.ld_in, g3_of<T>(g), nullptr, (T*)tau, L.ld_out);
+                                                                 L.ld_in, g3_of<T>(g), nullptr, (T*)tau, L.ld_out, gpl);
   return (int)cudaGetLastError();
 }
 
@@ -114,18 +116,19 @@ template <class V>
 int Launcher<V>::aba(const V& mv, const Launch& L, const void* q, const void* qd, const void* tau, const double* g,
                      const void* fext, void* qdd, int32_t* status) {
   using T = typename V::Real;
-  if (!fext) {
+  const T* gpl = static_cast<const T*>(L.gravity_planes);
+  if (!fext && !gpl) {
     const int rc = try_tiled(mv, L, OpABA<T>{g3_of<T>(g), (T*)qdd, L.ld_out, status}, q, qd, tau);
     if (rc >= 0) return rc;
   }
   if (fext)
     k_aba<V, true><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, (const T*)qd, (const T*)tau,
                                                                L.ld_in, g3_of<T>(g), (const T*)fext, (T*)qdd, L.ld_out,
-                                                               status);
+                                                               status, gpl);
   else
     k_aba<V, false><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(mv, L.N, (const T*)q, (const T*)qd, (const T*)tau,
                                                                 L.ld_in, g3_of<T>(g), nullptr, (T*)qdd, L.ld_out,
-                                                                status);
+                                                                status, gpl);
   return (int)cudaGetLastError();
 }
 

@@ -40,10 +40,10 @@ void time_kernel(const char* name, K kern, size_t smem, size_t scratch_per_threa
   cudaEventCreate(&b);
   const T *x0 = x, *x1 = x + N * n, *x2 = x + 2 * N * n;
   cudaMemset(y, 0, sizeof(T) * N * nout);
-  for (int w = 0; w < 3; ++w) kern<<<grid, blk, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch, nullptr);
+  for (int w = 0; w < 3; ++w) kern<<<grid, blk, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch, nullptr, nullptr);
   cudaEventRecord(a);
   const int reps = 20;
-  for (int r = 0; r < reps; ++r) kern<<<grid, blk, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch, nullptr);
+  for (int r = 0; r < reps; ++r) kern<<<grid, blk, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch, nullptr, nullptr);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms = 0;

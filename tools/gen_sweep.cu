@@ -36,10 +36,10 @@ void run(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_
   cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   const T* x0 = x; const T* x1 = x + N * n; const T* x2 = x + 2 * N * n;
-  for (int w = 0; w < 3; ++w) kern<<<grid, kGenBlock, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch, nullptr);
+  for (int w = 0; w < 3; ++w) kern<<<grid, kGenBlock, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch, nullptr, nullptr);
   cudaEventRecord(a);
   const int reps = 20;
-  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch, nullptr);
+  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, x0, x1, x2, N, T(0), T(0), T(9.81), y, N, st, scratch, nullptr, nullptr);
   cudaEventRecord(b); cudaEventSynchronize(b);
   float ms = 0; cudaEventElapsedTime(&ms, a, b); ms /= reps;
   double bytes = (double)N * (Op::kIn * n + Op::kOut) * sizeof(T);

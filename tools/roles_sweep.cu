@@ -151,7 +151,8 @@ int main() {
     cudaFuncSetAttribute(kref, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t grid = std::min<int64_t>((N + 127) / 128, (int64_t)sms * 2);
     float ms = timed(kref, dim3((unsigned)grid), 128, smem, N, (const double*)x, (const double*)(x + N * 29),
-                     (const double*)(x + 2 * N * 29), N, 0.0, 0.0, 9.81, y_ref, N, st, scratch, (const double*)nullptr);
+                     (const double*)(x + 2 * N * 29), N, 0.0, 0.0, 9.81, y_ref, N, st, scratch, (const double*)nullptr,
+                     (const double*)nullptr);
     printf("%-28s N %8lld          %.4f ms  %.3e evals/s\n", "single-thread k_gen", (long long)N, ms, N / (ms * 1e-3));
     run_roles<40, 74, 2>("roles r40 s74 b2", N, x, y, y_ref, st, scratch);
     run_roles<40, 40, 3>("roles r40 s40 b3", N, x, y, y_ref, st, scratch);
