@@ -231,6 +231,12 @@ int vd_diff_ik(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t 
  * sqrt(det(J Jᵀ)) as a Cholesky pivot product, 0 where the factorization fails. */
 int vd_manipulability(vd_device_model dm, int dtype, int64_t N, const void* q, int64_t ld_in, int frame,
                       void* w_out, void* stream);
+/* manipulability and its directional derivative D w(q)·dq (jvp_scalar of
+ * kinematics.hpp:138-153 on dual.hpp scalars; autodiff.hpp:52-62): one plane
+ * each, either may be NULL; dq NULL = zero tangent.  With dq = q̇ this is the
+ * Lie derivative L_f w along the drift f = (q̇, q̈) (control.hpp:157-163). */
+int vd_manipulability_jvp(vd_device_model dm, int dtype, int64_t N, const void* q, const void* dq, int64_t ld_in,
+                          int frame, void* w_out, void* dw_out, void* stream);
 
 /* ------------------------------------------------------------------ forward-mode JVPs
  * jvp(fn, x, v) of autodiff.hpp:41-52 applied to the library's own functions

@@ -465,6 +465,32 @@ int orc_batch_manip(void* h, int64_t N, const double* q, const char* frame, doub
   }
 }
 
+// jvp_scalar (autodiff.hpp:52-62) of manipulability(geometric_jacobian(frame))
+// per instance: the JVP the reference's lie_derivative (control.hpp:157-163)
+// takes of h = manipulability ∘ J along a direction dq.
+int orc_batch_manip_jvp(void* h, int64_t N, const double* q, const double* dq, const char* frame, double* w_out,
+                        double* dw_out, int threads) {
+  try {
+    const Model& m = M(h);
+    const int n = m.dof();
+    (void)m.frame(frame);
+    const std::string f = frame;
+    batch_eval((int)N,
+               [&](int i) {
+                 std::vector<Dual> a((size_t)n);
+                 for (int j = 0; j < n; ++j) a[(size_t)j] = Dual(q[j * N + i], dq ? dq[j * N + i] : 0.0);
+                 const Frames<Dual> w = forward_kinematics<Dual>(m, a);
+                 const Dual v = manipulability(geometric_jacobian(m, w, f));
+                 w_out[i] = v.value;
+                 dw_out[i] = v.tangent;
+               },
+               threads);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // Frozen algorithmic op counts per evaluation (orc_count.hpp).  algo:
 // 0 rnea_loop, 1 crba_loop, 2 aba_loop, 3 forward_kinematics, 4 rnea (mask
 // form), 5 forward_dynamics (CRBA + bias + LLT), 6 crba (mask form).

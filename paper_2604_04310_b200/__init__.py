@@ -36,7 +36,7 @@ __all__ = [
     "rnea", "bias_forces", "gravity_vector", "coriolis_vector", "crba", "crba_packed", "unpack_crba", "forward_dynamics", "dynamics",
     "forward_kinematics", "forward_kinematics_scan", "frame_transform", "geometric_jacobian", "manipulability", "diff_ik_step", "osc_step", "batch_rnea", "batch_crba",
     "forward_kinematics_jvp", "rnea_jvp", "crba_jvp", "forward_dynamics_jvp", "rnea_derivatives",
-    "forward_dynamics_derivatives",
+    "forward_dynamics_derivatives", "manipulability_jvp", "lie_derivative",
     "batch_forward_dynamics", "shard_range",
 ]
 
@@ -743,6 +743,31 @@ def manipulability(dm, q, frame):
     _check(_lib.load().vd_manipulability(dm.handle, _dtype_code(qs), N, _p(qs), N, _frame_id(dm, frame), _p(out),
                                          _stream(dev)))
     return out.reshape(N)
+
+
+def manipulability_jvp(dm, q, dq, frame):
+    """(w, D w(q)·dq), each (N,): jvp_scalar (autodiff.hpp:52-62) of
+    manipulability(geometric_jacobian(frame)) (kinematics.hpp:138-153) on
+    dual numbers; the tangent is 0 where the Gram matrix does not factor."""
+    qs, (dqs,), N, dev = _prep(dm, q, (dq, "dq"))
+    w = _out(dev, qs.dtype, 1, N)
+    dw = _out(dev, qs.dtype, 1, N)
+    _check(_lib.load().vd_manipulability_jvp(dm.handle, _dtype_code(qs), N, _p(qs), _p(dqs), N, _frame_id(dm, frame),
+                                             _p(w), _p(dw), _stream(dev)))
+    return w.reshape(N), dw.reshape(N)
+
+
+def lie_derivative(h, f, z):
+    """L_f h(z) = ⟨∇h(z), f(z)⟩ as one JVP of h along f(z), the gradient never
+    formed (control.hpp:157-163), batched: z is a tensor of N states (any
+    trailing shape), f(z) a vector field of z's shape and h(z, dz) -> (value,
+    tangent) a JVP of the scalar function, e.g. ``lambda z, dz:
+    manipulability_jvp(dm, z[:, :n], dz[:, :n], frame)``.  Returns the (N,)
+    tangents."""
+    direction = f(z)
+    if tuple(direction.shape) != tuple(z.shape):
+        raise DimensionError(f"lie_derivative: f(z) has shape {tuple(direction.shape)}, z has {tuple(z.shape)}")
+    return h(z, direction)[1]
 
 
 def diff_ik_step(dm, q, target, damping, return_error=False):

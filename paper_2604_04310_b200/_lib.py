@@ -97,6 +97,7 @@ SIGNATURES = {
     "vd_osc": (c_int, [P, c_int, c_int64, P, P, c_int64, ctypes.POINTER(OscParams), P, P, c_int64, P, P]),
     "vd_diff_ik": (c_int, [P, c_int, c_int64, P, c_int64, ctypes.POINTER(TaskParams), P, P, c_int64, P, P]),
     "vd_manipulability": (c_int, [P, c_int, c_int64, P, c_int64, c_int, P, P]),
+    "vd_manipulability_jvp": (c_int, [P, c_int, c_int64, P, P, c_int64, c_int, P, P, P]),
     "vd_fk_jvp": (c_int, [P, c_int, c_int64, P, P, c_int64, P, P, c_int64, P]),
     "vd_rnea_jvp": (c_int, [P, c_int, c_int64, P, P, P, P, P, P, c_int64, Pd, P, P, P, c_int64, P]),
     "vd_crba_jvp": (c_int, [P, c_int, c_int64, P, P, c_int64, P, P, c_int64, P]),

@@ -152,8 +152,11 @@ class Gen:
         self.raw(f"vd_sincos_cx<Cx>({self.ty}({q.s}), &s{i}, &c{i});")
         return Ex(s=f"c{i}"), Ex(s=f"s{i}")
 
-    def recip(self, d):
-        return self.tmp(f"{self.ty}(1) / {self.o(d)}", "di")
+    def recip(self, d, prefix="di"):
+        return self.tmp(f"{self.ty}(1) / {self.o(d)}", prefix)
+
+    def sqrt(self, x):
+        return self.tmp(f"vd_sqrt({self.o(x)})", "sq")
 
     def check_pos(self, d):
         self.raw(f"ok = ok && ({self.o(d)} > {self.ty}(0));")
@@ -395,9 +398,15 @@ class DGen(Gen):
         # d sin = cos dq, d cos = −sin dq (dual.hpp:97-102)
         return DualEx(c, Gen.neg(self, Gen.mul(self, sn, q.t))), DualEx(sn, Gen.mul(self, c, q.t))
 
-    def recip(self, d):
-        r = Gen.recip(self, d.v)
+    def recip(self, d, prefix="di"):
+        r = Gen.recip(self, d.v, prefix)
         return DualEx(r, Gen.neg(self, Gen.mul(self, d.t, Gen.mul(self, r, r))))
+
+    def sqrt(self, x):
+        # d √x = dx / (2 √x) (dual.hpp sqrt)
+        x = _lift(x)
+        v = Gen.sqrt(self, x.v)
+        return DualEx(v, Gen.mul(self, x.t, self.tmp(f"T(0.5) / {v.s}", "hs")))
 
     def check_pos(self, d):
         Gen.check_pos(self, d.v)
@@ -1082,9 +1091,9 @@ def chol6(g, G):
         for j in range(k):
             x = g.sub(x, g.mul(L[(k, j)], L[(k, j)]))
         oks.append(f"({g.o(x)} > T(0))")
-        x = g.tmp(f"vd_sqrt({g.o(x)})", "sq")
+        x = g.sqrt(x)
         piv.append(x)
-        inv = g.tmp(f"T(1) / {x.s}", "iv")
+        inv = g.recip(x, "iv")
         L[(k, k)] = inv
         for i in range(k + 1, 6):
             sv = L[(i, k)]
@@ -1631,11 +1640,12 @@ def gen_diffik(rb, fj):
     return A.finish()
 
 
-def gen_manip(rb, fj):
+def gen_manip(rb, fj, dual=False):
     """manipulability (kinematics.hpp:138-153; vd_algos.cuh manip_one):
     sqrt(det(J Jᵀ)) as the product of the Cholesky pivots, 0 when it does not
-    factor.  y(0, 0) = w."""
-    A = Algo(rb, False, only=_path(rb, fj))
+    factor.  y(0, 0) = w.  dual: its JVP along the tangent input cx.dx(0, ·)
+    (jvp_scalar, autodiff.hpp:52-62), y(1, 0) = D w · dq (0 where w is)."""
+    A = Algo(rb, False, dual=dual, only=_path(rb, fj))
     g = A.g
     _, _, J, path = frame_pose_J(A, fj)
     L, okx, piv = chol6(g, _gram6(g, J, path, None))
@@ -1643,6 +1653,8 @@ def gen_manip(rb, fj):
     for i in range(1, 6):
         d = g.mul(d, piv[i])
     g.raw(f"cx.y(0, 0, ({okx}) ? {g.o(d)} : T(0));")
+    if dual:
+        g.raw(f"cx.y(1, 0, ({okx}) ? {Gen.o(g, d.t)} : T(0));")
     return A.finish()
 
 
@@ -1772,7 +1784,8 @@ def emit_body(name, cls, rb, ops=None, tasks=True, task_joints=None):
         out += ["    " + ln for ln in A.g.lines]
         out += ["    }", "  };"]
     for fj in osc_joints:
-        for nm, fn, nout in (("Jac", gen_jac, 12), ("DiffIk", gen_diffik, rb.n), ("Manip", gen_manip, 1)):
+        for nm, fn, nout in (("Jac", gen_jac, 12), ("DiffIk", gen_diffik, rb.n), ("Manip", gen_manip, 1),
+                             ("ManipJvp", lambda rb, fj: gen_manip(rb, fj, dual=True), 1)):
             A = fn(rb, fj)
             out += [f"  // {nm} on joint {fj}: {A.g.flops} mul/add after folding; {A.nslot} slots",
                     f"  struct {nm}{fj} {{",
@@ -1787,12 +1800,13 @@ def emit_body(name, cls, rb, ops=None, tasks=True, task_joints=None):
             out += ["    " + ln for ln in A.g.lines]
             out += ["    }", "  };"]
     out.append(f"  static constexpr int kOscJoints[] = {{{', '.join(str(j) for j in osc_joints)}}};")
-    out.append("  // calls f(Jac<fj>{}, DiffIk<fj>{}, Manip<fj>{}) for a generated frame joint; false if none")
+    out.append("  // calls f(Jac<fj>{}, DiffIk<fj>{}, Manip<fj>{}, ManipJvp<fj>{}) for a generated frame joint;")
+    out.append("  // false if none")
     out.append("  template <class F>")
     out.append("  static bool with_task(int fj, F&& f) {")
     out.append("    switch (fj) {")
     for fj in osc_joints:
-        out.append(f"      case {fj}: f(Jac{fj}{{}}, DiffIk{fj}{{}}, Manip{fj}{{}}); return true;")
+        out.append(f"      case {fj}: f(Jac{fj}{{}}, DiffIk{fj}{{}}, Manip{fj}{{}}, ManipJvp{fj}{{}}); return true;")
     out.append("      default: return false;")
     out.append("    }")
     out.append("  }")

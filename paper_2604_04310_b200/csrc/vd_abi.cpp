@@ -649,6 +649,19 @@ int vd_manipulability(vd_device_model dm, int dtype, int64_t N, const void* q, i
                 "vd_manipulability");
 }
 
+int vd_manipulability_jvp(vd_device_model dm, int dtype, int64_t N, const void* q, const void* dq, int64_t ld_in,
+                          int frame, void* w, void* dw, void* stream) {
+  if (int rc = check_common(dm, dtype, N, ld_in, ld_in)) return rc;
+  if (frame < 0 || frame >= dm->pm.nframes) return set_error(VD_ERR_UNKNOWN_FRAME, "frame index out of range");
+  VD_NEED(q, "q");
+  if (N > 0 && dm->n > 0 && !w && !dw) return set_error(VD_ERR_INVALID_ARGUMENT, "null output buffers");
+  vdk::TaskShared S;
+  task_frame(dm, frame, S);
+  DeviceGuard g(dm->device);
+  return finish(vdk::launch_manip_jvp(make_launch(dm, dtype, N, ld_in, ld_in, stream), q, dq, S, w, dw),
+                "vd_manipulability_jvp");
+}
+
 // ---- forward-mode JVPs (autodiff.hpp:41-56 applied to the library's own functions)
 // gravity3 is a host array (NULL = GravitySpec::standard()); it travels by value.
 static double gcomp(const double* g3, int k) { return g3 ? g3[k] : (k == 2 ? 9.81 : 0.0); }

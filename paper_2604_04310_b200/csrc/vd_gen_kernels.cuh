@@ -432,6 +432,8 @@ template <class T, int kSlots, int kReg, int kSmem>
 struct GenTaskCx : GenCx<T, kSlots, kReg, kSmem> {
   const TaskShared* P;
   T* out1_;
+  const T* din_;  // &dq[i] (the ManipJvp tangent; NULL = 0)
+  __device__ __forceinline__ T dx(int, int j) const { return din_ ? GenMem<T>::ldg(din_ + j * this->ld) : T(0); }
   __device__ __forceinline__ T fR(int k) const { return T(P->frame_R[k]); }
   __device__ __forceinline__ T fp(int k) const { return T(P->frame_p[k]); }
   __device__ __forceinline__ T tR(int k) const { return T(P->target_R[k]); }
@@ -449,7 +451,7 @@ template <class Op, class T, int kReg, int kSmem, int kMinB>
 __global__ void __launch_bounds__(kGenBlock, kMinB)
     k_gen_task(int64_t N, const T* __restrict__ q, int64_t ldi, const __grid_constant__ TaskShared P,
                T* __restrict__ y0, T* __restrict__ y1, int64_t ldo, int32_t* __restrict__ status,
-               T* __restrict__ scratch) {
+               T* __restrict__ scratch, const T* __restrict__ dq) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
   using Cx = GenTaskCx<T, Op::kSlots, kReg, kSmem>;
   Cx cx;
@@ -468,12 +470,16 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
     cx.ld = ld;
     cx.ldo = lo;
     cx.in_[0] = cx.in_[1] = cx.in_[2] = q + i;
+    cx.din_ = dq ? dq + i : nullptr;
     cx.out_ = y0 ? y0 + i : nullptr;
     cx.out1_ = y1 ? y1 + i : nullptr;
     const bool ok = Op::template run<T>(cx);
     if (cx.active) {
-      if (!ok && y0)
-        for (int j = 0; j < Op::kOut; ++j) y0[(int64_t)j * ldo + i] = T(0);
+      if (!ok)
+        for (int j = 0; j < Op::kOut; ++j) {
+          if (y0) y0[(int64_t)j * ldo + i] = T(0);
+          if (dq && y1) y1[(int64_t)j * ldo + i] = T(0);  // ManipJvp: the tangent too
+        }
       if (status) status[i] = ok ? 0 : 7;
     }
   }

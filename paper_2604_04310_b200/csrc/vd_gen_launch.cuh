@@ -157,14 +157,15 @@ int launch_osc_t(const Launch& L, const void* q, const void* qd, const OscShared
 }
 
 template <class Op, class T>
-int launch_task_t(const Launch& L, const void* q, const TaskShared& P, void* y0, void* y1, int32_t* status) {
+int launch_task_t(const Launch& L, const void* q, const TaskShared& P, void* y0, void* y1, int32_t* status,
+                  const void* dq = nullptr) {
   constexpr int kReg = 0, kSmem = Op::kSlots, kMinB = sizeof(T) == 8 ? 3 : 4;  // path-only state: all on chip
   auto kern = k_gen_task<Op, T, kReg, kSmem, kMinB>;
   constexpr size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
   const Occ o = occupancy<Op, T>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
   kern<<<(unsigned)blocks, kGenBlock, smem, static_cast<cudaStream_t>(L.stream)>>>(
-      L.N, (const T*)q, L.ld_in, P, (T*)y0, (T*)y1, L.ld_out, status, nullptr);
+      L.N, (const T*)q, L.ld_in, P, (T*)y0, (T*)y1, L.ld_out, status, nullptr, (const T*)dq);
   return (int)cudaGetLastError();
 }
 

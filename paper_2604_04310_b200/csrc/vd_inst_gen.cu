@@ -273,17 +273,18 @@ int launch_gen_jvp(const Launch& L, const JvpArgs& a) {
 // which: 0 Jacobian (y0 pose, y1 J), 1 diff-IK (y0 q̇, y1 err), 2 manipulability (y0 w)
 template <class R>
 int gen_task_t(const Launch& L, int which, int frame_joint, const TaskShared& P, const void* q, void* y0, void* y1,
-               int32_t* status) {
+               int32_t* status, const void* dq) {
   int rc = -1;
-  R::with_task(frame_joint, [&](auto jac, auto dik, auto man) {
+  R::with_task(frame_joint, [&](auto jac, auto dik, auto man, auto man_jvp) {
     auto go = [&](auto op) {
       using Op = decltype(op);
-      rc = L.dtype == 0 ? launch_task_t<Op, double>(L, q, P, y0, y1, status)
-                        : launch_task_t<Op, float>(L, q, P, y0, y1, status);
+      rc = L.dtype == 0 ? launch_task_t<Op, double>(L, q, P, y0, y1, status, dq)
+                        : launch_task_t<Op, float>(L, q, P, y0, y1, status, dq);
     };
     if (which == 0) go(jac);
     else if (which == 1) go(dik);
-    else go(man);
+    else if (which == 2) go(man);
+    else if (which == 4) go(man_jvp);
   });
   return rc;
 }
@@ -292,9 +293,9 @@ int gen_task_t(const Launch& L, int which, int frame_joint, const TaskShared& P,
 // `ee` (tools/async_sweep.cu "jac", 4M states): geometric Jacobian + pose
 // fp64 1.55 -> 0.39 ms, fp32 1.13 -> 0.37 ms against the template kernel.
 int launch_gen_task(const Launch& L, int which, int frame_joint, const TaskShared& P, const void* q, void* y0,
-                    void* y1, int32_t* status) {
-  if (L.spec == kTree29) return gen_task_t<GenTree29>(L, which, frame_joint, P, q, y0, y1, status);
-  if (L.spec == kChain7) return gen_task_t<GenChain7>(L, which, frame_joint, P, q, y0, y1, status);
+                    void* y1, int32_t* status, const void* dq) {
+  if (L.spec == kTree29) return gen_task_t<GenTree29>(L, which, frame_joint, P, q, y0, y1, status, dq);
+  if (L.spec == kChain7) return gen_task_t<GenChain7>(L, which, frame_joint, P, q, y0, y1, status, dq);
   return -1;
 }
 

@@ -87,7 +87,8 @@ VD_JIT_API uint64_t vdj_task_mask(void) {
   return m;
 }
 // which: 0 Jacobian (y0 pose, y1 J), 1 diff-IK (y0 q̇, y1 err), 2 manipulability
-// (y0 w); params = vdk::TaskShared.  3: OSC (y0 τ, y1 Λ), params =
+// (y0 w), 4 manipulability JVP along qd (y0 w, y1 dw); params =
+// vdk::TaskShared.  3: OSC (y0 τ, y1 Λ), params =
 // vdk::OscShared.  Same conventions as vd_inst_gen.cu's gen_task_t / gen_osc_t.
 VD_JIT_API int vdj_task_launch(int which, const vdk::Launch* L, int frame_joint, const void* q, const void* qd,
                                const void* params, void* y0, void* y1, int32_t* status) {
@@ -105,14 +106,17 @@ VD_JIT_API int vdj_task_launch(int which, const vdk::Launch* L, int frame_joint,
     return rc;
   }
   const TaskShared& P = *static_cast<const TaskShared*>(params);
-  R::with_task(frame_joint, [&](auto jac, auto dik, auto man) {
+  const void* dq = which == 4 ? qd : nullptr;
+  R::with_task(frame_joint, [&](auto jac, auto dik, auto man, auto man_jvp) {
     auto go = [&](auto op) {
       using Op = decltype(op);
-      rc = f64 ? launch_task_t<Op, double>(*L, q, P, y0, y1, status) : launch_task_t<Op, float>(*L, q, P, y0, y1, status);
+      rc = f64 ? launch_task_t<Op, double>(*L, q, P, y0, y1, status, dq)
+               : launch_task_t<Op, float>(*L, q, P, y0, y1, status, dq);
     };
     if (which == 0) go(jac);
     else if (which == 1) go(dik);
-    else go(man);
+    else if (which == 2) go(man);
+    else if (which == 4) go(man_jvp);
   });
   return rc;
 }

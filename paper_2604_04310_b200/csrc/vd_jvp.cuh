@@ -201,6 +201,37 @@ __global__ void __launch_bounds__(kBlock) k_jvp(const __grid_constant__ JV mv, i
   }
 }
 
+// JVP of manipulability(geometric_jacobian(frame)) (kinematics.hpp:138-153 on
+// dual.hpp scalars): w and D w(q)·dq, one plane each (either may be NULL).
+// The building block of lie_derivative for the SPEC's CBF example
+// (control.hpp:157-163: L_f h = JVP of h along f).
+template <class JV>
+__global__ void __launch_bounds__(kBlock) k_manip_jvp(const __grid_constant__ JV mv, int64_t N,
+                                                      const typename JV::Base::Real* __restrict__ q,
+                                                      const typename JV::Base::Real* __restrict__ dq, int64_t ldi,
+                                                      const __grid_constant__ TaskShared P,
+                                                      typename JV::Base::Real* __restrict__ w,
+                                                      typename JV::Base::Real* __restrict__ dw) {
+  using D = typename JV::Real;
+  using S = typename JV::S;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  JM<S> jm[JV::kMax];
+  load_motion(mv, Cols<D>{q, dq, ldi, i}, jm);
+  const D v = manip_one(mv, jm, P);
+  if (w) w[i] = v.value;
+  if (dw) dw[i] = v.tangent;
+}
+
+template <class V>
+int launch_manip_jvp_view(const V& mv, const Launch& L, const void* q, const void* dq, const TaskShared& P, void* w,
+                          void* dw) {
+  using T = typename V::Real;
+  k_manip_jvp<JView<V>><<<grid_for(L.N), kBlock, 0, stream_of(L)>>>(JView<V>{mv}, L.N, (const T*)q, (const T*)dq,
+                                                                     L.ld_in, P, (T*)w, (T*)dw);
+  return (int)cudaGetLastError();
+}
+
 template <class V>
 int launch_jvp_view(const V& mv, const Launch& L, const JvpArgs& a) {
   const JView<V> jv{mv};

@@ -27,10 +27,11 @@ enum JitOp : int {
   kJitAba = 0, kJitRnea = 1, kJitBias = 2, kJitGravity = 3, kJitCoriolis = 4, kJitCrba = 5, kJitCrbaPacked = 6,
   kJitFk = 7
 };
-constexpr int kJitAbi = 2;  // 2: Launch::gravity_planes
+constexpr int kJitAbi = 3;  // 2: Launch::gravity_planes; 3: task routine 4 (manipulability JVP)
 using JitLaunchFn = int (*)(int op, const Launch* L, const void* x0, const void* x1, const void* x2,
                             const double* g3, const void* fext, void* y, int32_t* status);
-// which: 0 Jacobian, 1 diff-IK, 2 manipulability (params TaskShared*), 3 OSC (params OscShared*)
+// which: 0 Jacobian, 1 diff-IK, 2 manipulability (params TaskShared*), 3 OSC (params OscShared*),
+// 4 manipulability JVP (qd = the tangent dq; y0 w, y1 dw)
 using JitTaskFn = int (*)(int which, const Launch* L, int frame_joint, const void* q, const void* qd,
                           const void* params, void* y0, void* y1, int32_t* status);
 
@@ -85,8 +86,9 @@ int launch_gen_rnea(const Launch& L, int mode, const void* q, const void* qd, co
 int launch_gen_crba(const Launch& L, const void* q, void* M);
 int launch_gen_crba_packed(const Launch& L, const void* q, void* Mp);
 int launch_gen_fk(const Launch& L, const void* q, void* frames);
+// which: 0 Jacobian, 1 diff-IK, 2 manipulability, 4 manipulability JVP along dq (y0 w, y1 dw)
 int launch_gen_task(const Launch& L, int which, int frame_joint, const TaskShared& P, const void* q, void* y0,
-                    void* y1, int32_t* status);
+                    void* y1, int32_t* status, const void* dq = nullptr);
 int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
                    int32_t* status);
 int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
@@ -108,6 +110,8 @@ struct JvpArgs {
 int launch_jvp(const Launch& L, const JvpArgs& a);
 // generated dual-number kernels (tree29 ABA / RNEA without f_ext); -1 otherwise
 int launch_gen_jvp(const Launch& L, const JvpArgs& a);
+// manipulability and its JVP along dq (vd_jvp.cuh k_manip_jvp); w / dw one plane each
+int launch_manip_jvp(const Launch& L, const void* q, const void* dq, const TaskShared& P, void* w, void* dw);
 
 // Row-major (N, K) batch <-> K planes (vd_layout.cu); to_planes: rows -> planes.
 int launch_layout(int dtype, bool to_planes, int64_t N, int K, const void* src, int64_t ld_src, void* dst,

@@ -151,9 +151,9 @@ extern "C" int gen_jvp_host(int robot, int op, long N, const double* x0, const d
 // generated task-space routine on frame joint fj (fp64): which 0 Jacobian (y0 pose 12, y1 J 6n),
 // 1 diff-IK (y0 q̇, y1 err), 2 manipulability (y0); -1 when no variant exists for fj
 extern "C" int gen_task_host(int which, int fj, long N, const double* q, const double* P, double* y0, double* y1,
-                             int* status) {
+                             int* status, const double* dq) {
   int bad = -1;
-  vdk::GenTree29::with_task(fj, [&](auto jac, auto dik, auto man) {
+  vdk::GenTree29::with_task(fj, [&](auto jac, auto dik, auto man, auto man_jvp) {
     auto go = [&](auto op) {
       using Op = decltype(op);
       std::vector<double> slots(Op::kSlots + 1);
@@ -162,6 +162,7 @@ extern "C" int gen_task_host(int which, int fj, long N, const double* q, const d
         HostCx<double> cx{{q, q, q}, nullptr, y0, N, i, slots.data()};
         cx.P = P;
         cx.Y1 = y1;
+        cx.DX[0] = dq;
         const bool ok = Op::template run<double>(cx);
         status[i] = ok ? 0 : 7;
         bad += !ok;
@@ -169,7 +170,8 @@ extern "C" int gen_task_host(int which, int fj, long N, const double* q, const d
     };
     if (which == 0) go(jac);
     else if (which == 1) go(dik);
-    else go(man);
+    else if (which == 2) go(man);
+    else go(man_jvp);
   });
   return bad;
 }

@@ -57,6 +57,7 @@ def lib():
         L.orc_batch_osc.argtypes = [vp, i64, vp, vp, cc, vp, vp, vp, vp, vp, cd, cd, vp, cd, vp, vp, vp, ci]
         L.orc_batch_diffik.argtypes = [vp, i64, vp, cc, vp, vp, vp, cd, vp, vp, ci]
         L.orc_batch_manip.argtypes = [vp, i64, vp, cc, vp, ci]
+        L.orc_batch_manip_jvp.argtypes = [vp, i64, vp, vp, cc, vp, vp, ci]
         L.orc_batch_jvp.argtypes = [vp, ci, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ci, ci]
         _lib = L
     return _lib
@@ -251,6 +252,13 @@ class Model:
         w = np.empty(q.shape[0])
         _chk(lib().orc_batch_manip(self.h, q.shape[0], _ptr(q), frame.encode(), _ptr(w), threads))
         return w
+
+    def manipulability_jvp(self, q, dq, frame, threads=0):
+        q, dq = _F(q), _F(dq)
+        w, dw = np.empty(q.shape[0]), np.empty(q.shape[0])
+        _chk(lib().orc_batch_manip_jvp(self.h, q.shape[0], _ptr(q), _ptr(dq), frame.encode(), _ptr(w), _ptr(dw),
+                                       threads))
+        return w, dw
 
 
 def rel_err(a, b, axis=None):

@@ -261,24 +261,36 @@ def test_generated_task_routines_match_oracle(genlib, frame):
     P = np.zeros(45 + om.n)
     P[:9], P[9:12], P[12:21], P[21:24] = fR.reshape(-1), off[9:], R0.reshape(-1), p0
     P[24:30], P[30:36], P[44] = kp, tw, damp
-    genlib.gen_task_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 5
+    genlib.gen_task_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 6
     Q = np.asfortranarray(q)
     st = np.zeros(N, dtype=np.int32)
     pose = np.zeros((N, 12), order="F")
     J = np.zeros((N, 6 * om.n), order="F")
-    assert genlib.gen_task_host(0, fj, N, _p(Q), _p(P), _p(pose), _p(J), _p(st)) == 0
+    assert genlib.gen_task_host(0, fj, N, _p(Q), _p(P), _p(pose), _p(J), _p(st), None) == 0
     rpose, rJ = om.jacobian(q, frame)
     assert rel_err(pose, rpose, axis=1).max() <= 1e-12
     assert rel_err(J, rJ.transpose(0, 2, 1).reshape(N, -1), axis=1).max() <= 1e-12  # plane 6 c + r
     qd = np.zeros((N, om.n), order="F")
     err = np.zeros((N, 6), order="F")
-    assert genlib.gen_task_host(1, fj, N, _p(Q), _p(P), _p(qd), _p(err), _p(st)) == 0
+    assert genlib.gen_task_host(1, fj, N, _p(Q), _p(P), _p(qd), _p(err), _p(st), None) == 0
     rqd, rerr = om.diff_ik(q, frame, R0, p0, kp, tw, damp)
     assert rel_err(qd, rqd, axis=1).max() <= 1e-10
     assert rel_err(err, rerr, axis=1).max() <= 1e-10
     w = np.zeros((N, 1), order="F")
-    assert genlib.gen_task_host(2, fj, N, _p(Q), _p(P), _p(w), None, _p(st)) == 0
+    assert genlib.gen_task_host(2, fj, N, _p(Q), _p(P), _p(w), None, _p(st), None) == 0
     assert rel_err(w[:, 0], om.manipulability(q, frame)) <= 1e-10
+    # ManipJvp: the dual-number routine against the oracle's jvp_scalar, where
+    # J Jᵀ is well conditioned (the derivative amplifies rounding by κ near a
+    # singularity; tests/test_gpu_task.py states the bound)
+    dq = np.asfortranarray(np.random.default_rng(4).standard_normal(q.shape))
+    w2, dw = np.zeros((N, 1), order="F"), np.zeros((N, 1), order="F")
+    assert genlib.gen_task_host(4, fj, N, _p(Q), _p(P), _p(w2), _p(dw), _p(st), _p(dq)) == 0
+    rw, rdw = om.manipulability_jvp(q, dq, frame)
+    assert rel_err(w2[:, 0], rw) <= 1e-10
+    kappa = np.linalg.cond(np.einsum("nrk,nck->nrc", rJ, rJ))
+    well = kappa < 1e3
+    assert well.sum() > N // 4
+    assert rel_err(dw[well, 0][:, None], rdw[well][:, None], axis=1).max() <= 1e-10
 
 
 def _run_fext(L, robot, op, xs, fext, nout, g=(0.0, 0.0, 9.81), f32=False):

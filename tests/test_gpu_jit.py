@@ -148,6 +148,14 @@ def test_jit_task_routines_match_oracle(vd, cuda, task_case):
     theta = np.linalg.norm(err_ref[:, :3], axis=1)
     klog = np.maximum(1.0, 1.0 / np.maximum(np.pi - theta, 1e-6) ** 2)
     assert np.all(rel_err(_np(qd_got), qd_ref, axis=1) <= np.maximum(TOL64, 1e-16 * np.linalg.cond(G) * klog))
+    # manipulability JVP (the module's ManipJvp routine) against the oracle's
+    # jvp_scalar, with test_gpu_task.test_manipulability_jvp's κ(J Jᵀ) bound
+    w2, dw = (_np(t) for t in vd.manipulability_jvp(dm, _t(q), _t(qd), frame))
+    rw, rdw = om.manipulability_jvp(q, qd, frame)
+    kappa_j = np.linalg.cond(J_ref @ np.swapaxes(J_ref, 1, 2))
+    e = rel_err(dw[:, None], rdw[:, None], axis=1)
+    assert rel_err(w2[:, None], rw[:, None], axis=1).max() <= 1e-9
+    assert np.all(e <= np.maximum(TOL64, 32 * 2.2e-16 * kappa_j)) and e[kappa_j < 1e3].max() <= TOL64
 
 
 def _osc_ref_and_got(vd, om, dm, frame, N, seed, dtype):

@@ -192,3 +192,76 @@ def test_task_random_trees(vd, cuda, oracle, seed):
     bound = np.maximum(TOL64, 1e-16 * _gram_cond(J, 0.1) * _log_kappa(om.diff_ik(q, "tool", R, p, [1.0] * 6,
                                                                                [0.0] * 6, 0.1)[1]))
     assert np.all(rel_err(qd, qd_ref, axis=1) <= bound)
+
+
+# ---------------------------------------------------------------- manipulability JVP / lie_derivative
+@pytest.mark.parametrize("name", ROBOTS)
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_manipulability_jvp(vd, cuda, omodels, name, dtype):
+    """vd_manipulability_jvp against the oracle's dual-number jvp_scalar of
+    manipulability (orc_batch_manip_jvp, pinned by finite differences in
+    tests/test_lie.py).  The tangent is compared where w is away from a
+    singularity: w is not differentiable where J loses rank, and near it the
+    pivot derivatives d√x = dx / 2√x amplify rounding, so the bound is
+    32·ε·κ(J Jᵀ) (measured ≤ 0.1·ε·κ on the near-singular states) with the
+    flat bar where κ(J Jᵀ) < 1e3."""
+    om = omodels[name]
+    frame = FRAMES[name]
+    dm = vd.DeviceModel(vd.robots.by_name(name), 0)
+    q, qd, _, _ = om.random_states(4097, 97, True, False)
+    if dtype == torch.float32:
+        q, qd = (a.astype(np.float32).astype(np.float64) for a in (q, qd))
+    w_ref, dw_ref = om.manipulability_jvp(q, qd, frame)
+    w, dw = (_np(t) for t in vd.manipulability_jvp(dm, _t(q, dtype), _t(qd, dtype), frame))
+    tol = TOL64 if dtype == torch.float64 else TOL32
+    eps = np.finfo(np.float64 if dtype == torch.float64 else np.float32).eps
+    _, J = om.jacobian(q, frame)
+    kappa = np.linalg.cond(np.einsum("nrk,nck->nrc", J, J))
+    well = kappa < 1e3
+    assert well.sum() > 1000
+    assert np.all(np.isfinite(dw))
+    assert rel_err(w[:, None], w_ref[:, None], axis=1).max() <= tol
+    err = rel_err(dw[:, None], dw_ref[:, None], axis=1)
+    assert np.all(err <= np.maximum(tol, 32 * eps * kappa))
+    assert err[well].max() <= tol
+    # the value plane is manipulability(); a zero tangent gives a zero derivative
+    e_w = rel_err(w[:, None], _np(vd.manipulability(dm, _t(q, dtype), frame))[:, None], axis=1)
+    assert np.all(e_w <= np.maximum(tol, 32 * eps * kappa)) and e_w[well].max() <= tol
+    lib = vd._lib.load()
+    qs = _t(q, dtype).t().contiguous()
+    w2, dw2 = torch.empty(4097, dtype=dtype, device="cuda"), torch.full((4097,), 7.0, dtype=dtype, device="cuda")
+    assert lib.vd_manipulability_jvp(dm.handle, 0 if dtype == torch.float64 else 1, 4097, qs.data_ptr(), None, 4097,
+                                     dm.model.frame_index(frame), w2.data_ptr(), dw2.data_ptr(), None) == 0
+    assert torch.count_nonzero(dw2).item() == 0
+
+
+@pytest.mark.parametrize("name", ["chain7", "tree29"])
+def test_lie_derivative_spec_example(vd, cuda, omodels, name):
+    """SPEC.md:524 on the GPU: h = manipulability ∘ J(q), f = the forward-
+    dynamics drift (q̇, q̈(q, q̇, τ = 0)) on z = (q, q̇): lie_derivative matches
+    the central finite-difference directional derivative of the device
+    manipulability, rel tol 1e-4."""
+    om = omodels[name]
+    frame = FRAMES[name]
+    dm = vd.DeviceModel(vd.robots.by_name(name), 0)
+    n = om.n
+    q, qd, _, _ = om.random_states(2048, 98, True, False)
+    z = torch.cat([_t(q), _t(qd)], dim=1)
+    zero = torch.zeros((2048, n), dtype=torch.float64, device="cuda")
+
+    def drift(z):
+        return torch.cat([z[:, n:], vd.forward_dynamics(dm, z[:, :n], z[:, n:], zero)], dim=1)
+
+    def h(z, dz):
+        return vd.manipulability_jvp(dm, z[:, :n], dz[:, :n], frame)
+
+    lie = _np(vd.lie_derivative(h, drift, z))
+    eps = 1e-6
+    fd = (_np(vd.manipulability(dm, _t(q + eps * qd), frame)) - _np(vd.manipulability(dm, _t(q - eps * qd), frame))) / (
+        2 * eps)
+    w = om.manipulability(q, frame)
+    ok = w > 1e-4
+    assert ok.sum() > 500
+    assert np.all(np.abs(lie - fd)[ok] <= 1e-4 * np.maximum(np.abs(fd[ok]), 1e-3))
+    _, ref = om.manipulability_jvp(q, qd, frame)
+    assert rel_err(lie[ok, None], ref[ok, None], axis=1).max() <= TOL64

@@ -118,10 +118,10 @@ void task(const char* name, int64_t N, T* x, T* y0, T* y1, int32_t* st) {
   P.frame_p[2] = 0.1;
   cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  for (int w = 0; w < 2; ++w) kern<<<grid, kGenBlock, smem>>>(N, x, N, P, y0, y1, N, st, nullptr);
+  for (int w = 0; w < 2; ++w) kern<<<grid, kGenBlock, smem>>>(N, x, N, P, y0, y1, N, st, nullptr, (const T*)nullptr);
   cudaEventRecord(a);
   const int reps = 10;
-  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, x, N, P, y0, y1, N, st, nullptr);
+  for (int r = 0; r < reps; ++r) kern<<<grid, kGenBlock, smem>>>(N, x, N, P, y0, y1, N, st, nullptr, (const T*)nullptr);
   cudaEventRecord(b); cudaEventSynchronize(b);
   float ms = 0; cudaEventElapsedTime(&ms, a, b); ms /= reps;
   printf("%-40s regs %3d lmem %4zu smem %6zu b/SM %d  %.4f ms  %.3e evals/s  %s\n", name, fa.numRegs, fa.localSizeBytes,

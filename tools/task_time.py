@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""Device-timed Jacobian / diff-IK / manipulability through the Python API.
+"""Device-timed Jacobian / diff-IK / manipulability (and its JVP) through the Python API.
 
 Usage: python tools/task_time.py [N ...]   (chain7 frame `ee`, tree29 `l_palm`)
 """
@@ -43,7 +43,8 @@ def main():
                 q = ((torch.rand((N, n), dtype=torch.float64, device="cuda") * 2 - 1) * np.pi).to(dt)
                 calls = {"jacobian": lambda: vd.geometric_jacobian(dm, q, frame),
                          "diff_ik": lambda: vd.diff_ik_step(dm, q, tgt, 0.01),
-                         "manipulability": lambda: vd.manipulability(dm, q, frame)}
+                         "manipulability": lambda: vd.manipulability(dm, q, frame),
+                         "manipulability_jvp": lambda: vd.manipulability_jvp(dm, q, q, frame)}
                 for op, fn in calls.items():
                     ms = timeit(fn)
                     print(json.dumps({"robot": robot, "op": op, "dtype": str(dt)[6:], "N": N, "ms": round(ms, 4)}),
