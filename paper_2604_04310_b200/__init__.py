@@ -37,7 +37,7 @@ __all__ = [
     "forward_kinematics", "forward_kinematics_scan", "frame_transform", "geometric_jacobian", "manipulability", "diff_ik_step", "osc_step", "batch_rnea", "batch_crba",
     "forward_kinematics_jvp", "rnea_jvp", "crba_jvp", "forward_dynamics_jvp", "rnea_derivatives",
     "forward_dynamics_derivatives", "manipulability_jvp", "lie_derivative",
-    "batch_forward_dynamics", "shard_range",
+    "batch_forward_dynamics", "batch_eval", "shard_range",
 ]
 
 
@@ -913,6 +913,73 @@ def batch_forward_dynamics(model, batch, gravity=None, devices=None):
     _check(_lib.load().vd_batch_forward_dynamics_host(model.handle, N, q.ctypes.data, qd.ctypes.data, tau.ctypes.data,
                                                       g, out.ctypes.data, None, d, nd))
     return out
+
+
+class _ShardStates:
+    """One device's shard of a StateBatch for batch_eval: (N_shard, n) views
+    of plane buffers on the device (None for an absent field), the layout
+    every entry point reads without a copy."""
+
+    def __init__(self, batch, b, e, dev):
+        torch = _torch()
+
+        def up(a):
+            if a is None or not a.size:
+                return None
+            return torch.from_numpy(np.ascontiguousarray(a[b:e].T)).to(dev, non_blocking=False).t()
+
+        self.q, self.qd, self.qdd, self.tau = (up(a) for a in (batch.q, batch.qd, batch.qdd, batch.tau))
+        self.begin, self.end = b, e
+
+
+def batch_eval(model, batch, fn, devices=None):
+    """batch_eval (batch.hpp:76-126) with a device list instead of `workers`:
+    the batch is cut into contiguous shards (shard_range, the reference's
+    chunk rule) and fn(device_model, states) runs once per shard on its
+    device, one host thread per device; `states` holds the shard's q, qd,
+    qdd, tau as (N_shard, n) CUDA tensors, and fn returns an (N_shard, K)
+    tensor (or array).  fn sees whole shards rather than single states (the
+    library's entry points are batched); every state still runs the same code
+    path whatever the partition, so the (N, K) result is bitwise identical
+    for any device list.  N = 0 gives a 0 x 0 array, as the reference."""
+    import threading
+
+    torch = _torch()
+    batch.validate(model)
+    N = batch.size()
+    if N == 0:
+        return np.empty((0, 0), dtype=np.float64, order="F")
+    devices = list(devices) if devices else [0]
+    world = min(len(devices), N)
+    parts, errors = [None] * world, [None] * world
+
+    def work(k):
+        try:
+            b, e = shard_range(N, world, k)
+            dev = torch.device("cuda", devices[k])
+            with torch.cuda.device(dev):
+                dm = DeviceModel(model, devices[k])
+                y = fn(dm, _ShardStates(batch, b, e, dev))
+                y = y.detach().double().cpu().numpy() if torch.is_tensor(y) else np.asarray(y, dtype=np.float64)
+            if y.ndim == 1:
+                y = y[:, None]
+            if y.shape[0] != e - b:
+                raise DimensionError(f"batch_eval: fn returned {y.shape[0]} rows for a shard of {e - b} states")
+            parts[k] = y
+        except BaseException as exc:  # re-raised on the calling thread
+            errors[k] = exc
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for exc in errors:
+        if exc is not None:
+            raise exc
+    if len({p.shape[1] for p in parts}) != 1:
+        raise DimensionError("batch_eval: fn returned different widths on different shards")
+    return np.asfortranarray(np.concatenate(parts, axis=0))
 
 
 def shard_range(N, world, rank):

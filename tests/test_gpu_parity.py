@@ -501,6 +501,28 @@ def test_host_batch_api(vd, cuda, omodels):
     assert rel_err(got, qdd, axis=1)[cosb > 0.05].max() <= 1e-8
 
 
+def test_batch_eval(vd, cuda, omodels):
+    """batch_eval (batch.hpp:76-126): fn runs once per contiguous shard on its
+    device; the concatenation is bitwise identical for any partition (here 1
+    and 3 shards on the one GPU) and equals the oracle; N = 0 gives 0 x 0."""
+    m = vd.robots.tree29()
+    b = vd.random_states(m, 3001, 2605, True, True)
+    om = omodels["tree29"]
+
+    def fn(dm, s):
+        return torch.cat([vd.rnea(dm, s.q, s.qd, s.qdd), vd.forward_dynamics(dm, s.q, s.qd, s.tau)], dim=1)
+
+    one = vd.batch_eval(m, b, fn)
+    three = vd.batch_eval(m, b, fn, devices=[0, 0, 0])
+    assert one.shape == (3001, 58) and np.array_equal(one, three)
+    assert rel_err(one[:, :29], om.rnea(b.q, b.qd, b.qdd), axis=1).max() <= TOL64
+    assert np.array_equal(one[:, :29], vd.batch_rnea(m, b))
+    empty = vd.StateBatch(np.zeros((0, 29), order="F"), np.zeros((0, 29), order="F"))
+    assert vd.batch_eval(m, empty, fn).shape == (0, 0)
+    with pytest.raises(vd.DimensionError):
+        vd.batch_eval(m, b, lambda dm, s: s.q[:5])
+
+
 def test_results_independent_of_batch_position(vd, cuda, omodels):
     """Every instance is computed by the same instruction stream whatever N,
     ld or pointer alignment (TMA tiles, tail tile, plain-staged tiles): shards
