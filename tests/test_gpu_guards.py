@@ -89,6 +89,18 @@ def _ops(vd, lib, name, m, dm, n, dtype):
                                                                     p(x[4]), p(x[5]), li, g3, None, p(y[0]), p(y[1]),
                                                                     lo, st.data_ptr(), s)),
     }
+    # per-state gravity: plane 3's first three rows are the a_g planes (same ld as the inputs)
+    ops["rnea_pg"] = ([n], lambda x, li, y, lo, st: lib.vd_rnea_pg(h, code, N, p(x[0]), p(x[1]), p(x[2]), li, p(x[3]),
+                                                                   None, p(y[0]), lo, s))
+    ops["gravity_pg"] = ([n], lambda x, li, y, lo, st: lib.vd_gravity_pg(h, code, N, p(x[0]), li, p(x[3]), p(y[0]), lo,
+                                                                         s))
+    ops["aba_pg"] = ([n], lambda x, li, y, lo, st: lib.vd_aba_pg(h, code, N, p(x[0]), p(x[1]), p(x[2]), li, p(x[3]),
+                                                                 None, p(y[0]), lo, st.data_ptr(), s))
+    ops["dynamics_pg"] = ([n * n, n, n], lambda x, li, y, lo, st: lib.vd_dynamics_pg(
+        h, code, N, p(x[0]), p(x[1]), p(x[2]), li, p(x[3]), p(y[0]), p(y[1]), p(y[2]), lo, st.data_ptr(), s))
+    # one plane each, no ld_out (as vd_manipulability)
+    ops["manip_jvp"] = ([1, 1], lambda x, li, y, lo, st: lib.vd_manipulability_jvp(h, code, N, p(x[0]), p(x[3]), li,
+                                                                                   frame, p(y[0]), p(y[1]), s))
     if m.is_serial_chain():
         ops["fk_scan"] = ([12 * n], lambda x, li, y, lo, st: lib.vd_fk_scan(h, code, N, p(x[0]), li, p(y[0]), lo, s))
     return ops
