@@ -36,7 +36,7 @@ __all__ = [
     "rnea", "bias_forces", "gravity_vector", "coriolis_vector", "crba", "crba_packed", "unpack_crba", "forward_dynamics", "dynamics",
     "forward_kinematics", "forward_kinematics_scan", "frame_transform", "geometric_jacobian", "manipulability", "diff_ik_step", "osc_step", "batch_rnea", "batch_crba",
     "forward_kinematics_jvp", "rnea_jvp", "crba_jvp", "forward_dynamics_jvp", "rnea_derivatives",
-    "forward_dynamics_derivatives", "manipulability_jvp", "lie_derivative",
+    "forward_dynamics_derivatives", "manipulability_jvp", "jvp", "jvp_scalar", "jacobian_fwd", "lie_derivative",
     "batch_forward_dynamics", "batch_eval", "shard_range",
 ]
 
@@ -755,6 +755,41 @@ def manipulability_jvp(dm, q, dq, frame):
     _check(_lib.load().vd_manipulability_jvp(dm.handle, _dtype_code(qs), N, _p(qs), _p(dqs), N, _frame_id(dm, frame),
                                              _p(w), _p(dw), _stream(dev)))
     return w.reshape(N), dw.reshape(N)
+
+
+def jvp(h, x, v):
+    """jvp (autodiff.hpp:41-50), batched: (h(x), Dh(x)·v) from a JVP function
+    h(x, dx) -> (value, tangent) over N states (the library's *_jvp entry
+    points, e.g. ``lambda q, dq: forward_kinematics_jvp(dm, q, dq)``).
+    DimensionError when v's shape is not x's (autodiff.hpp:44-48)."""
+    if tuple(v.shape) != tuple(x.shape):
+        raise DimensionError(f"jvp: tangent has shape {tuple(v.shape)}, input has {tuple(x.shape)}")
+    return h(x, v)
+
+
+def jvp_scalar(h, x, v):
+    """jvp_scalar (autodiff.hpp:52-62), batched: h returns (N,) values and tangents."""
+    val, tan = jvp(h, x, v)
+    if val.dim() != 1 or tan.dim() != 1:
+        raise DimensionError("jvp_scalar: the function is not scalar-valued per state")
+    return val, tan
+
+
+def jacobian_fwd(h, x):
+    """jacobian_fwd (autodiff.hpp:64-84), batched: the (N, m, d) Jacobian of h
+    at the N states x (N, d), column j from one JVP pass along e_j (an AD
+    Jacobian costs d passes; the reference says the same)."""
+    torch = _torch()
+    N, d = x.shape
+    cols = []
+    for j in range(d):
+        e = torch.zeros_like(x)
+        e[:, j] = 1
+        t = h(x, e)[1]
+        cols.append(t.reshape(N, -1))
+    if not cols:
+        return torch.empty((N, 0, 0), dtype=x.dtype, device=x.device)
+    return torch.stack(cols, dim=2)
 
 
 def lie_derivative(h, f, z):

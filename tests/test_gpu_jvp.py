@@ -213,3 +213,26 @@ def test_dynamics_derivatives_identities(vd, cuda, omodels, name):
         e[:, j] = h
         fd = (om.rnea(q, qd + e, qdd_r) - om.rnea(q, qd - e, qdd_r)) / (2 * h)
         assert np.abs(rqd[:, :, j] - fd).max() / max(1.0, np.abs(fd).max()) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["chain7", "tree29"])
+def test_jacobian_fwd_combinator(vd, cuda, omodels, name):
+    """jacobian_fwd (autodiff.hpp:64-84) over the device JVPs: ∂τ/∂q̈ of the
+    dual RNEA is the mass matrix (dynamics.hpp:352-365, the reference's own
+    CRBA-column = RNEA(e_i) identity), and jvp along v equals J·v."""
+    om = omodels[name]
+    dm = vd.DeviceModel(vd.robots.by_name(name), 0)
+    n = om.n
+    q, qd, qdd, _ = om.random_states(512, 61, True, False)
+    tq, tqd, tqdd = _t(q), _t(qd), _t(qdd)
+    zero = torch.zeros_like(tq)
+
+    def h(x, dx):
+        return vd.rnea_jvp(dm, tq, tqd, x, zero, zero, dx)
+
+    J = vd.jacobian_fwd(h, tqdd)
+    assert J.shape == (512, n, n)
+    assert rel_err(_np(J).reshape(512, -1), om.crba(q).reshape(512, -1), axis=1).max() <= 1e-10
+    v = torch.randn(512, n, dtype=torch.float64, device="cuda")
+    _, t = vd.jvp(h, tqdd, v)
+    assert rel_err(_np(t), _np(torch.einsum("nij,nj->ni", J, v)), axis=1).max() <= 1e-12

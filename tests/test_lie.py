@@ -74,3 +74,27 @@ def test_lie_derivative_combinator_spec_examples(vd):
     # f(z) must have z's shape (DimensionError, autodiff.hpp:56-59)
     with pytest.raises(vd.DimensionError):
         vd.lie_derivative(half_sq, lambda z: z[:, :7], z)
+
+
+def test_jvp_combinators(vd):
+    """jvp / jvp_scalar / jacobian_fwd (autodiff.hpp:41-84) on a torch JVP:
+    h(x) = (x0 x1, sin x2) has the Jacobian [[x1, x0, 0], [0, 0, cos x2]]."""
+    x = torch.randn(64, 3, dtype=torch.float64, generator=torch.Generator().manual_seed(5))
+
+    def h(x, dx):
+        val = torch.stack([x[:, 0] * x[:, 1], torch.sin(x[:, 2])], 1)
+        tan = torch.stack([dx[:, 0] * x[:, 1] + x[:, 0] * dx[:, 1], torch.cos(x[:, 2]) * dx[:, 2]], 1)
+        return val, tan
+
+    J = vd.jacobian_fwd(h, x)
+    ref = torch.zeros(64, 2, 3, dtype=torch.float64)
+    ref[:, 0, 0], ref[:, 0, 1], ref[:, 1, 2] = x[:, 1], x[:, 0], torch.cos(x[:, 2])
+    assert torch.equal(J, ref)
+    v = torch.randn(64, 3, dtype=torch.float64)
+    assert torch.allclose(vd.jvp(h, x, v)[1], torch.einsum("nij,nj->ni", J, v), rtol=1e-15, atol=1e-15)
+    with pytest.raises(vd.DimensionError):
+        vd.jvp(h, x, v[:, :2])
+    with pytest.raises(vd.DimensionError):
+        vd.jvp_scalar(h, x, v)
+    s = lambda x, dx: (h(x, dx)[0][:, 0], h(x, dx)[1][:, 0])  # noqa: E731
+    assert torch.equal(vd.jvp_scalar(s, x, v)[1], h(x, v)[1][:, 0])
