@@ -254,7 +254,10 @@ __device__ __forceinline__ void sincos_t<double>(double x, double* s, double* c)
 }
 template <>
 __device__ __forceinline__ void sincos_t<float>(float x, float* s, float* c) {
-  sincosf(x, s, c);
+  // vd_sincos_f32 in the template / loop kernels (tools/sweep.py fp32 against
+  // sincosf: Panda fused M + bias + q̈ 0.695 -> 0.657 ms, generic OSC 11.7 ->
+  // 8.4 ms, the other loop kernels unchanged to +2.5 %)
+  vd_sincos_f32(x, s, c);
 }
 // kFastTrig: fp64 sin/cos by vd_sincos_f64 (vd_sincos.cuh).  Measured on B200
 // it is 2.5 % faster for the chain7 ABA kernel and 2-5 % slower for RNEA /

@@ -75,7 +75,7 @@ struct GenMem<float> {
 template <class T, int kSlots, int kReg, int kSmem, bool kFast = false, bool kStream = false, int kSyncEvery = 0,
           int kBlk = kGenBlock>
 struct GenCx {
-  static constexpr bool kFastTrig = kFast;  // fp64 sin/cos by vd_sincos_f64
+  static constexpr bool kFastTrig = kFast;  // sin/cos by vd_sincos_f64 / vd_sincos_f32
   static constexpr int kGlobal = kSlots - kReg - kSmem > 0 ? kSlots - kReg - kSmem : 0;
   const T* in_[3];  // &x_g[i]; element (i, j) of input g at in_[g][j * ld]
   T* out_;          // &y[i]; element (i, k) at out_[k * ldo]

@@ -63,11 +63,15 @@ template <class T> __device__ __forceinline__ bool vd_isfinite(T x) { return isf
 template <class T> inline void vd_sincos(T x, T* s, T* c) { *s = std::sin(x); *c = std::cos(x); }
 template <class T> inline bool vd_isfinite(T x) { return std::isfinite(x); }
 #endif
-// Cx::kFastTrig selects vd_sincos_f64 (vd_sincos.cuh) for fp64 on the device
+// Cx::kFastTrig selects vd_sincos_f64 / vd_sincos_f32 (vd_sincos.cuh) on the
+// device.  Per routine (Cfg::kFast): the fp32 version makes the Panda ABA
+// 0.300 -> 0.287 ms at 4 M states but the G1 fp32 routines 5-15 % slower
+// (tools/sweep.py), where sincosf stays.
 template <class Cx, class T>
 VD_HD void vd_sincos_cx(T x, T* s, T* c) {
 #if defined(__CUDA_ARCH__)
   if constexpr (Cx::kFastTrig && sizeof(T) == 8) { vd_sincos_f64(x, s, c); return; }
+  if constexpr (Cx::kFastTrig && sizeof(T) == 4) { vd_sincos_f32(x, s, c); return; }
 #endif
   vd_sincos(x, s, c);
 }

@@ -23,19 +23,20 @@ struct Cfg<GenChain7::Aba, double> {
   static constexpr int kReg = 24, kSmem = 41, kMinB = 3;
   static constexpr bool kFast = true, kStream = true, kAsync = true;
 };
-// chain7 fp32 ABA: generated + async r40 s25 (6 CTAs/SM) 0.299 ms at 4M
-// states vs 0.41 ms for the templated TMA kernel
+// chain7 fp32 ABA: generated + async, 0.41 ms for the templated TMA kernel ->
+// r40 s25 (6 CTAs/SM) 0.299 ms at 4M states with sincosf -> r30 s35 (5
+// CTAs/SM) 0.287 ms with vd_sincos_f32 (async_sweep c7f)
 template <>
 struct Cfg<GenChain7::Aba, float> {
-  static constexpr int kReg = 40, kSmem = 25, kMinB = 6;
-  static constexpr bool kFast = false, kAsync = true;
+  static constexpr int kReg = 30, kSmem = 35, kMinB = 5;
+  static constexpr bool kFast = true, kAsync = true;
 };
 // chain7 RNEA family: all slots in registers, fast fp64 sincos (gen_sweep:
 // fp64 0.252 vs 0.261 ms templated, fp32 0.142 vs 0.153 ms at 4M states)
 template <class T, int kSlotsAll>
 struct Chain7RneaCfg {
   static constexpr int kReg = kSlotsAll, kSmem = 0, kMinB = sizeof(T) == 8 ? 4 : 6;
-  static constexpr bool kFast = true;
+  static constexpr bool kFast = sizeof(T) == 8;  // fp32: sincosf (vd_sincos_f32 measured 4 % slower here)
 };
 template <class T>
 struct Cfg<GenChain7::Rnea, T> : Chain7RneaCfg<T, GenChain7::Rnea::kSlots> {};

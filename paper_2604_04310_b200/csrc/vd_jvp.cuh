@@ -63,7 +63,7 @@ __device__ __forceinline__ void sincos_t<Dual<double>>(Dual<double> x, Dual<doub
 template <>
 __device__ __forceinline__ void sincos_t<Dual<float>>(Dual<float> x, Dual<float>* s, Dual<float>* c) {
   float sv, cv;
-  sincosf(x.value, &sv, &cv);
+  sincos_t<float>(x.value, &sv, &cv);
   *s = Dual<float>(sv, cv * x.tangent);
   *c = Dual<float>(cv, -sv * x.tangent);
 }

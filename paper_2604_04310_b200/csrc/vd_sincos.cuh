@@ -81,6 +81,36 @@ __device__ __forceinline__ void vd_sincos_f64(double x, double* sp, double* cp) 
   *sp = sn;
   *cp = cs;
 }
+
+// fp32: the same structure with float constants.  k by the 1.5·2^23 trick
+// (exact for |x·2/π| < 2^22), a three-part Cody–Waite π/2 (FMA products
+// exact) valid for |x| ≤ 1e4, the Cephes sinf / cosf minimax kernels on
+// [−π/4, π/4] (< 1 ulp there); |x| > 1e4 falls back to sincosf.  CUDA's
+// sincosf carries its Payne–Hanek slow path inline at every call site.
+static __device__ __noinline__ void vd_sincos_f32_slow(float x, float* sp, float* cp) { sincosf(x, sp, cp); }
+
+__device__ __forceinline__ void vd_sincos_f32(float x, float* sp, float* cp) {
+  if (fabsf(x) > 1.0e4f) {
+    vd_sincos_f32_slow(x, sp, cp);
+    return;
+  }
+  const float t = fmaf(x, 0x1.45f306p-1f, 0x1.8p23f);
+  const float kf = t - 0x1.8p23f;
+  const int q = __float_as_int(t);
+  float r = fmaf(-kf, 0x1.921fb6p+0f, x);
+  r = fmaf(-kf, -0x1.777a5cp-25f, r);
+  r = fmaf(-kf, -0x1.ee59dap-50f, r);
+  const float z = r * r;
+  const float s = fmaf(r * z, fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f), r);
+  const float c = fmaf(z * z, fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z, 4.166664568298827e-2f),
+                       fmaf(-0.5f, z, 1.0f));
+  float sn = (q & 1) ? c : s;
+  float cs = (q & 1) ? s : c;
+  if (q & 2) sn = -sn;
+  if ((q + 1) & 2) cs = -cs;
+  *sp = sn;
+  *cp = cs;
+}
 #endif
 
 }  // namespace vdk
