@@ -637,3 +637,22 @@ def test_osc_fp32(vd, cuda, omodels, name, frame):
     assert np.all(e_tau[ok] <= np.maximum(TOL32, om.n * eps * kappa[ok]))
     well = ok & (kappa * eps < 1e-6)
     assert e_tau[well].max(initial=0) <= TOL32
+
+
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("scale", [1.0, 3e3, 5e4])
+def test_fp32_large_joint_angles(vd, cuda, omodels, generic, scale):
+    """fp32 sin/cos of joint angles far outside [−π, π] (continuous joints
+    wind up): vd_sincos_f32's Cody–Waite reduction below |q| = 1e4 and its
+    sincosf fallback above, in the Panda ABA (generated, Cfg::kFast) and the
+    loop kernels, against the oracle at the same float-rounded angles."""
+    om = omodels["chain7"]
+    m, dm = _dm(vd, "chain7", generic)
+    q, qd, qdd, _ = _states(om, 4096, 71)
+    wind = np.random.default_rng(3).integers(-1, 2, q.shape) * np.round(scale / (2 * np.pi)) * 2 * np.pi
+    q32 = (q + wind).astype(np.float32).astype(np.float64)
+    tau = om.rnea(q32, qd, qdd)
+    got = _np(vd.rnea(dm, _t(q32, torch.float32), _t(qd, torch.float32), _t(qdd, torch.float32)))
+    assert rel_err(got, tau, axis=1).max() <= TOL32
+    a = _np(vd.forward_dynamics(dm, _t(q32, torch.float32), _t(qd, torch.float32), _t(tau, torch.float32)))
+    _fd_check(om, q32, qd, tau, a, TOL32, "chain7")
