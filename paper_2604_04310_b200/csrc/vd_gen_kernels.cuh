@@ -72,10 +72,10 @@ struct GenMem<float> {
 // kSyncEvery > 0: a CTA barrier at every kSyncEvery-th phase point of the
 // generated routine (one per joint step), so the CTA's warps walk the
 // straight-line code together and share its instruction-cache lines.
-template <class T, int kSlots, int kReg, int kSmem, bool kFast = false, bool kStream = false, int kSyncEvery = 0,
+template <class T, int kSlots, int kReg, int kSmem, int kFast = kTrigLib, bool kStream = false, int kSyncEvery = 0,
           int kBlk = kGenBlock>
 struct GenCx {
-  static constexpr bool kFastTrig = kFast;  // sin/cos by vd_sincos_f64 / vd_sincos_f32
+  static constexpr int kFastTrig = kFast;  // kTrigLib / kTrigFast / kTrigCall (vd_gen_prelude.cuh)
   static constexpr int kGlobal = kSlots - kReg - kSmem > 0 ? kSlots - kReg - kSmem : 0;
   const T* in_[3];  // &x_g[i]; element (i, j) of input g at in_[g][j * ld]
   T* out_;          // &y[i]; element (i, k) at out_[k * ldo]
@@ -154,7 +154,7 @@ constexpr int64_t gen_scratch_per_thread() {
 
 // One generated routine (Op = GenRobot::Aba / Rnea / RneaBias / RneaGrav /
 // Crba / Fk) over a persistent grid: every thread strides over the batch.
-template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false, bool kStream = false,
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kFast = kTrigLib, bool kStream = false,
           int kSyncEvery = 0, int kBlk = kGenBlock>
 __global__ void __launch_bounds__(kBlk, kMinB)
     k_gen(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
@@ -219,7 +219,7 @@ __device__ __forceinline__ void vd_cp_async(uint32_t dst, const T* src, uint64_t
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(src), "n"(sizeof(T)) : "memory");
 }
 
-template <class T, int kSlots, int kReg, int kSmem, bool kFast, bool kStream, int kDof, int kSyncEvery = 0>
+template <class T, int kSlots, int kReg, int kSmem, int kFast, bool kStream, int kDof, int kSyncEvery = 0>
 struct GenAsyncCx : GenCx<T, kSlots, kReg, kSmem, kFast, kStream, kSyncEvery> {
   uint32_t ib;     // shared address of this thread's input element (0, 0)
   const T* nx[3];  // &x_g[next state]
@@ -245,7 +245,7 @@ constexpr size_t gen_async_smem() {
 
 // k_gen with asynchronous state input (same arguments, same results; gpl must
 // be NULL: launch_t sends per-state gravity to k_gen).
-template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast = false, bool kStream = false,
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kFast = kTrigLib, bool kStream = false,
           int kSyncEvery = 0>
 __global__ void __launch_bounds__(kGenBlock, kMinB)
     k_gen_async(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
@@ -302,8 +302,8 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
 
 // osc_step context: task parameters (OscShared, kernel parameter space) and
 // a second output (Λ, 36 planes, optional).
-template <class T, int kSlots, int kReg, int kSmem>
-struct GenOscCx : GenCx<T, kSlots, kReg, kSmem> {
+template <class T, int kSlots, int kReg, int kSmem, int kTrig = kTrigLib>
+struct GenOscCx : GenCx<T, kSlots, kReg, kSmem, kTrig> {
   const OscShared* P;
   T* out1_;  // &Λ[i] or nullptr
   __device__ __forceinline__ T g(int k) const { return T(P->gravity[k]); }
@@ -324,13 +324,13 @@ struct GenOscCx : GenCx<T, kSlots, kReg, kSmem> {
   }
 };
 
-template <class Op, class T, int kReg, int kSmem, int kMinB>
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig = kTrigLib>
 __global__ void __launch_bounds__(kGenBlock, kMinB)
     k_gen_osc(int64_t N, const T* __restrict__ q, const T* __restrict__ qd, int64_t ldi,
               const __grid_constant__ OscShared P, T* __restrict__ tau, T* __restrict__ lam, int64_t ldo,
               int32_t* __restrict__ status, T* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
-  using Cx = GenOscCx<T, Op::kSlots, kReg, kSmem>;
+  using Cx = GenOscCx<T, Op::kSlots, kReg, kSmem, kTrig>;
   Cx cx;
   cx.P = &P;
   const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
@@ -365,8 +365,8 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
 
 // Forward-mode JVP context (JvpArgs): NULL primal inputs read as 0, NULL
 // tangents as 0; output group 0 = values, 1 = tangents (either may be NULL).
-template <class T, int kSlots, int kReg, int kSmem, bool kStream = false>
-struct GenJvpCx : GenCx<T, kSlots, kReg, kSmem> {
+template <class T, int kSlots, int kReg, int kSmem, bool kStream = false, int kTrig = kTrigLib>
+struct GenJvpCx : GenCx<T, kSlots, kReg, kSmem, kTrig> {
   const T* din_[3];
   T* dout_;
   static __device__ __forceinline__ T ld_(const T* p) {
@@ -385,11 +385,11 @@ struct GenJvpCx : GenCx<T, kSlots, kReg, kSmem> {
   }
 };
 
-template <class Op, class T, int kReg, int kSmem, int kMinB, bool kStream = false>
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kStream = false, int kTrig = kTrigLib>
 __global__ void __launch_bounds__(kGenBlock, kMinB)
     k_gen_jvp(int64_t N, const __grid_constant__ JvpArgs a, int64_t ldi, int64_t ldo, T* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char vd_gen_smem[];
-  using Cx = GenJvpCx<T, Op::kSlots, kReg, kSmem, kStream>;
+  using Cx = GenJvpCx<T, Op::kSlots, kReg, kSmem, kStream, kTrig>;
   Cx cx;
   const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * kGenBlock;

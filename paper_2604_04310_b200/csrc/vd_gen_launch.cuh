@@ -22,7 +22,10 @@ namespace vdk {
 template <class Op, class T>
 struct Cfg {
   static constexpr int kReg = 0, kSmem = Op::kSlots < 55 ? Op::kSlots : 55, kMinB = sizeof(T) == 8 ? 3 : 4;
-  static constexpr bool kFast = false;  // vd_sincos_f64 instead of the library sincos
+  // sin/cos evaluation (vd_gen_prelude.cuh): the large-state routines of
+  // robots with >= 20 joints (ABA / RNEA families of JIT models) call one
+  // out-of-line copy, the measured win for the G1 ABA / RNEA
+  static constexpr int kFast = Op::kDof >= 20 && Op::kSlots >= 80 ? kTrigCall : kTrigLib;
 };
 // kStream (GenCx): evict-first state I/O; false unless a Cfg sets it
 template <class C, class = void>
@@ -131,15 +134,18 @@ int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, c
 // tools/async_sweep.cu "more", G1 `l_palm`, N = 262144: fp64 r40 s110 (2
 // CTAs/SM) 0.61 ms, s55 b3 0.69 ms (the M-based routine: 1.23 ms); fp32
 // r40 s144 (3 CTAs/SM) 0.27 ms (M-based: 0.50 ms).
+// sin/cos: one out-of-line copy in fp32 (G1 `l_palm` 0.238 -> 0.213 ms); the
+// fp64 routine is faster with the inlined library routine (0.593 vs 0.603).
 template <class Op, class T>
 struct OscCfg {
   static constexpr int kReg = 40, kSmem = sizeof(T) == 8 ? 110 : 144, kMinB = sizeof(T) == 8 ? 2 : 3;
+  static constexpr int kFast = sizeof(T) == 4 && Op::kDof >= 20 ? kTrigCall : kTrigLib;
 };
 template <class Op, class T>
 int launch_osc_t(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lam,
                  int32_t* status) {
   using C = OscCfg<Op, T>;
-  auto kern = k_gen_osc<Op, T, C::kReg, C::kSmem, C::kMinB>;
+  auto kern = k_gen_osc<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast>;
   constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
   const Occ o = occupancy<Op, T>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);

@@ -53,25 +53,53 @@ VD_HD void vd_rotation_log(const T* R, T* w) {
   for (int k = 0; k < 3; ++k) w[k] = f * anti[k];
 }
 
+// How a generated routine evaluates sin/cos (Cfg::kFast -> Cx::kFastTrig)
+enum : int {
+  kTrigLib = 0,   // the library sincos / sincosf, inlined at every joint
+  kTrigFast = 1,  // vd_sincos_f64 / vd_sincos_f32 (vd_sincos.cuh), inlined
+  kTrigCall = 2,  // the library routine, one out-of-line copy per kernel
+};
+
 #if defined(__CUDA_ARCH__)
-// library sincos here: vd_sincos_f64's __constant__ coefficients get hoisted out of the persistent
-// loop into registers and spilled in these 168/255-register kernels (measured slower)
+// library sincos by default: vd_sincos_f64's __constant__ coefficients get
+// hoisted out of the persistent loop into registers and spilled in these
+// 168/255-register kernels (measured slower)
 __device__ __forceinline__ void vd_sincos(double x, double* s, double* c) { sincos(x, s, c); }
 __device__ __forceinline__ void vd_sincos(float x, float* s, float* c) { sincosf(x, s, c); }
+// kTrigCall: the G1 routines are instruction-cache bound, and the library
+// sincos inlines ~70 instructions at each of 26 joints; one out-of-line copy
+// (a call per joint, result in registers) makes the G1 ABA fp64 0.294 ->
+// 0.262 ms and RNEA 0.100 -> 0.094 ms (tools/async_sweep.cu t29), while the
+// 168-register CRBA / FK routines get slower (the call's register save)
+static __device__ __noinline__ double2 vd_sincos_call(double x) {
+  double2 r;
+  sincos(x, &r.x, &r.y);
+  return r;
+}
+static __device__ __noinline__ float2 vd_sincos_call(float x) {
+  float2 r;
+  sincosf(x, &r.x, &r.y);
+  return r;
+}
 template <class T> __device__ __forceinline__ bool vd_isfinite(T x) { return isfinite(x); }
 #else
 template <class T> inline void vd_sincos(T x, T* s, T* c) { *s = std::sin(x); *c = std::cos(x); }
 template <class T> inline bool vd_isfinite(T x) { return std::isfinite(x); }
 #endif
-// Cx::kFastTrig selects vd_sincos_f64 / vd_sincos_f32 (vd_sincos.cuh) on the
-// device.  Per routine (Cfg::kFast): the fp32 version makes the Panda ABA
-// 0.300 -> 0.287 ms at 4 M states but the G1 fp32 routines 5-15 % slower
-// (tools/sweep.py), where sincosf stays.
+// Cx::kFastTrig: kTrigLib / kTrigFast / kTrigCall above.  kTrigFast in fp32
+// makes the Panda ABA 0.300 -> 0.287 ms at 4 M states but the G1 fp32
+// routines 5-15 % slower (tools/sweep.py).
 template <class Cx, class T>
 VD_HD void vd_sincos_cx(T x, T* s, T* c) {
 #if defined(__CUDA_ARCH__)
-  if constexpr (Cx::kFastTrig && sizeof(T) == 8) { vd_sincos_f64(x, s, c); return; }
-  if constexpr (Cx::kFastTrig && sizeof(T) == 4) { vd_sincos_f32(x, s, c); return; }
+  if constexpr (int(Cx::kFastTrig) == kTrigFast && sizeof(T) == 8) { vd_sincos_f64(x, s, c); return; }
+  if constexpr (int(Cx::kFastTrig) == kTrigFast && sizeof(T) == 4) { vd_sincos_f32(x, s, c); return; }
+  if constexpr (int(Cx::kFastTrig) == kTrigCall) {
+    const auto r = vd_sincos_call(x);
+    *s = r.x;
+    *c = r.y;
+    return;
+  }
 #endif
   vd_sincos(x, s, c);
 }

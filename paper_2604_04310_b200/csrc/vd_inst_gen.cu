@@ -21,7 +21,8 @@ namespace vdk {
 template <>
 struct Cfg<GenChain7::Aba, double> {
   static constexpr int kReg = 24, kSmem = 41, kMinB = 3;
-  static constexpr bool kFast = true, kStream = true, kAsync = true;
+  static constexpr int kFast = kTrigFast;
+  static constexpr bool kStream = true, kAsync = true;
 };
 // chain7 fp32 ABA: generated + async, 0.41 ms for the templated TMA kernel ->
 // r40 s25 (6 CTAs/SM) 0.299 ms at 4M states with sincosf -> r30 s35 (5
@@ -29,14 +30,15 @@ struct Cfg<GenChain7::Aba, double> {
 template <>
 struct Cfg<GenChain7::Aba, float> {
   static constexpr int kReg = 30, kSmem = 35, kMinB = 5;
-  static constexpr bool kFast = true, kAsync = true;
+  static constexpr int kFast = kTrigFast;
+  static constexpr bool kAsync = true;
 };
 // chain7 RNEA family: all slots in registers, fast fp64 sincos (gen_sweep:
 // fp64 0.252 vs 0.261 ms templated, fp32 0.142 vs 0.153 ms at 4M states)
 template <class T, int kSlotsAll>
 struct Chain7RneaCfg {
   static constexpr int kReg = kSlotsAll, kSmem = 0, kMinB = sizeof(T) == 8 ? 4 : 6;
-  static constexpr bool kFast = sizeof(T) == 8;  // fp32: sincosf (vd_sincos_f32 measured 4 % slower here)
+  static constexpr int kFast = sizeof(T) == 8 ? kTrigFast : kTrigLib;  // fp32: vd_sincos_f32 measured 4 % slower
 };
 template <class T>
 struct Cfg<GenChain7::Rnea, T> : Chain7RneaCfg<T, GenChain7::Rnea::kSlots> {};
@@ -54,25 +56,34 @@ template <class T>
 struct Cfg<GenChain7::RneaBiasFext, T> : Chain7RneaCfg<T, GenChain7::RneaBiasFext::kSlots> {};
 template <class T>
 struct Cfg<GenChain7::AbaFext, T> : Cfg<GenChain7::Aba, T> {};
+// G1 sin/cos: one out-of-line copy of the library routine (kTrigCall) in the
+// ABA / RNEA families, whose straight-line code is instruction-cache bound
+// (async_sweep "t29", sweep.py, 262144 states: ABA fp64 0.295 -> 0.264 ms,
+// mixed fp32 0.170 -> 0.146 ms, RNEA fp64 0.100 -> 0.094 ms); the CRBA, FK
+// and gravity routines stay inlined (the call makes them 1-15 % slower).
 template <>
 struct Cfg<GenTree29::Aba, double> {
   static constexpr int kReg = 40, kSmem = 113, kMinB = 2;
-  static constexpr bool kFast = false, kStream = true;
+  static constexpr int kFast = kTrigCall;
+  static constexpr bool kStream = true;
 };
 template <>
 struct Cfg<GenTree29::AbaMixed, float> {  // the trunk's fp64 slots (stored last) in registers
   static constexpr int kReg = 40, kSmem = 122, kMinB = 3;
-  static constexpr bool kFast = false, kStream = true;
+  static constexpr int kFast = kTrigCall;
+  static constexpr bool kStream = true;
 };
 template <>
 struct Cfg<GenTree29::Crba, double> {
   static constexpr int kReg = 0, kSmem = 55, kMinB = 3;
-  static constexpr bool kFast = false, kStream = true;
+  static constexpr int kFast = kTrigLib;
+  static constexpr bool kStream = true;
 };
 template <>
 struct Cfg<GenTree29::Crba, float> {
   static constexpr int kReg = 0, kSmem = 55, kMinB = 4;
-  static constexpr bool kFast = false, kStream = true;
+  static constexpr int kFast = kTrigLib;
+  static constexpr bool kStream = true;
 };
 // packed CRBA (gen_sweep, N = 262144 / 4M): tree29 fp64 all 55 slots in
 // registers at 3 CTAs/SM 0.112 ms (vs 0.133 with the dense routine's
@@ -81,32 +92,32 @@ struct Cfg<GenTree29::Crba, float> {
 template <>
 struct Cfg<GenTree29::CrbaPacked, double> {
   static constexpr int kReg = GenTree29::CrbaPacked::kSlots, kSmem = 0, kMinB = 3;
-  static constexpr bool kFast = false;
+  static constexpr int kFast = kTrigLib;
 };
 template <>
 struct Cfg<GenTree29::CrbaPacked, float> {
   static constexpr int kReg = 0, kSmem = GenTree29::CrbaPacked::kSlots, kMinB = 6;
-  static constexpr bool kFast = false;
+  static constexpr int kFast = kTrigLib;
 };
 template <class T>
 struct Cfg<GenChain7::CrbaPacked, T> {
   static constexpr int kReg = GenChain7::CrbaPacked::kSlots, kSmem = 0, kMinB = 4;
-  static constexpr bool kFast = false;
+  static constexpr int kFast = kTrigLib;
 };
 template <>
 struct Cfg<GenTree29::Rnea, double> {  // prologue: cos/sin, q̇, q̈ of every joint
   static constexpr int kReg = 58, kSmem = 55, kMinB = 2;
-  static constexpr bool kFast = false;
+  static constexpr int kFast = kTrigCall;
 };
 template <>
 struct Cfg<GenTree29::Rnea, float> {
   static constexpr int kReg = 55, kSmem = 0, kMinB = 3;
-  static constexpr bool kFast = false;
+  static constexpr int kFast = kTrigCall;
 };
 template <>
 struct Cfg<GenTree29::RneaBias, double> {
   static constexpr int kReg = 0, kSmem = 72, kMinB = 3;
-  static constexpr bool kFast = false;
+  static constexpr int kFast = kTrigCall;
 };
 template <class T>
 struct Cfg<GenTree29::RneaFext, T> : Cfg<GenTree29::Rnea, T> {};
@@ -123,6 +134,7 @@ struct Cfg<GenTree29::AbaMixedFext, float> : Cfg<GenTree29::AbaMixed, float> {};
 template <class T>
 struct OscCfg<GenChain7::Osc6, T> {
   static constexpr int kReg = sizeof(T) == 8 ? 80 : 60, kSmem = sizeof(T) == 8 ? 67 : 87, kMinB = 2;
+  static constexpr int kFast = kTrigLib;
 };
 
 namespace {
@@ -139,25 +151,31 @@ struct JvpCfg {
   // 262144: CRBA-JVP 0.50 -> 0.43 ms, FK-JVP 0.25 -> 0.20 ms); fp64 and the
   // larger routines measured best at 2 (255 registers)
   static constexpr int kMinB = sizeof(T) == 4 && Op::kSlots <= 110 ? 3 : 2;
+  static constexpr int kFast = kTrigLib;
 };
 
 // G1 ABA-JVP (526 slots): one CTA/SM with 220 shared slots keeps the scratch
 // slab in L2 (async_sweep "jvp", 262144 states: fp64 r40 s110 b2 1.50 ->
 // r40 s220 b1 1.24 ms; fp32 s220 b2 0.72 -> r40 s220 b2 0.64 ms); G1 fp32
 // RNEA-JVP s220 b2 0.27 -> s144 b3 0.25 ms.
+// sin/cos by one out-of-line copy (kTrigCall; async_sweep "trig"): ABA-JVP
+// fp64 1.244 -> 1.207 ms, fp32 0.590 -> 0.567 ms, RNEA-JVP fp32 0.201 -> 0.172
+// ms (fp64 RNEA-JVP is slower with it: 0.50 -> 0.57 ms).
 template <class T>
 struct JvpCfg<GenTree29::AbaJvp, T> {
   static constexpr int kReg = 40, kSmem = 220, kMinB = sizeof(T) == 8 ? 1 : 2;
+  static constexpr int kFast = kTrigCall;
 };
 template <>
 struct JvpCfg<GenTree29::RneaJvp, float> {
   static constexpr int kReg = 0, kSmem = 144, kMinB = 3;
+  static constexpr int kFast = kTrigCall;
 };
 
 template <class Op, class T, bool kStream>
 int launch_jvp_v(const Launch& L, const JvpArgs& a) {
   using C = JvpCfg<Op, T>;
-  auto kern = k_gen_jvp<Op, T, C::kReg, C::kSmem, C::kMinB, kStream>;
+  auto kern = k_gen_jvp<Op, T, C::kReg, C::kSmem, C::kMinB, kStream, C::kFast>;
   constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
   const Occ o = occupancy<std::pair<Op, std::bool_constant<kStream>>, T>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);

@@ -61,25 +61,25 @@ void time_kernel(const char* name, K kern, size_t smem, size_t scratch_per_threa
          fa.localSizeBytes, smem, bps, ms, N / (ms * 1e-3), md, cudaGetErrorString(cudaGetLastError()));
 }
 
-template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast, bool kStream, int kSync = 0>
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kFast, bool kStream, int kSync = 0>
 void plain(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, bool ref = false) {
   time_kernel<T>(name, k_gen<Op, T, kReg, kSmem, kMinB, kFast, kStream, kSync>, (size_t)kSmem * kGenBlock * sizeof(T),
                  gen_scratch_per_thread<Op, T, kReg, kSmem>(), N, Op::kDof, Op::kOut, x, y, st, scratch, cap, ref);
 }
-template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast, bool kStream, int kSync, int kBlk>
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kFast, bool kStream, int kSync, int kBlk>
 void plainb(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, bool ref = false) {
   time_kernel<T>(name, k_gen<Op, T, kReg, kSmem, kMinB, kFast, kStream, kSync, kBlk>, (size_t)kSmem * kBlk * sizeof(T),
                  gen_scratch_per_thread<Op, T, kReg, kSmem>(), N, Op::kDof, Op::kOut, x, y, st, scratch, cap, ref, kBlk);
 }
-template <class Op, class T, int kReg, int kSmem, int kMinB, bool kFast, bool kStream = false, int kSync = 0>
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kFast, bool kStream = false, int kSync = 0>
 void async(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch, size_t cap, bool ref = false) {
   time_kernel<T>(name, k_gen_async<Op, T, kReg, kSmem, kMinB, kFast, kStream, kSync>, gen_async_smem<Op, T, kReg, kSmem>(),
                  gen_scratch_per_thread<Op, T, kReg, kSmem>(), N, Op::kDof, Op::kOut, x, y, st, scratch, cap, ref);
 }
 
-template <class Op, class T, int kReg, int kSmem, int kMinB>
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig = kTrigLib>
 void osc(const char* name, int64_t N, T* x, T* y, T* lam, int32_t* st, T* scratch, size_t cap, int n, bool ref = false) {
-  auto kern = k_gen_osc<Op, T, kReg, kSmem, kMinB>;
+  auto kern = k_gen_osc<Op, T, kReg, kSmem, kMinB, kTrig>;
   const size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int bps = 0, sms = 0;
@@ -128,9 +128,9 @@ void task(const char* name, int64_t N, T* x, T* y0, T* y1, int32_t* st) {
          smem, bps, ms, N / (ms * 1e-3), cudaGetErrorString(cudaGetLastError()));
 }
 
-template <class Op, class T, int kReg, int kSmem, int kMinB>
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig = kTrigLib>
 void jvp(const char* name, int64_t N, T* x, T* y, T* scratch, size_t cap) {
-  auto kern = k_gen_jvp<Op, T, kReg, kSmem, kMinB, true>;
+  auto kern = k_gen_jvp<Op, T, kReg, kSmem, kMinB, true, kTrig>;
   const size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int bps = 0, sms = 0;
@@ -332,6 +332,30 @@ int main(int argc, char** argv) {
     async<GenChain7::Crba, double, S, 0, 4, true>("c7 crba f64 async rall b4", N7, x, y, st, scratch, cap);
     async<GenChain7::Crba, double, S, 0, 4, true, true>("c7 crba f64 async rall b4 cs", N7, x, y, st, scratch, cap);
     async<GenChain7::Crba, double, S, 0, 6, true, true>("c7 crba f64 async rall b6 cs", N7, x, y, st, scratch, cap);
+  }
+  if (ON("trig")) {  // library sincos inlined (kTrigLib) vs one out-of-line copy (kTrigCall), G1 at 262144
+    double* lam = nullptr;
+    cudaMalloc(&lam, sizeof(double) * 36 * N29);
+    k_fill<<<1184, 256>>>(x, N29 * 87, 2);
+    osc<GenTree29::Osc23, double, 40, 110, 2>("t29 osc23 f64 lib", N29, x, y, lam, st, scratch, cap, 29, true);
+    osc<GenTree29::Osc23, double, 40, 110, 2, kTrigCall>("t29 osc23 f64 call", N29, x, y, lam, st, scratch, cap, 29);
+    k_fill<<<1184, 256>>>(xf, N29 * 87, 2);
+    osc<GenTree29::Osc23, float, 40, 144, 3>("t29 osc23 f32 lib", N29, xf, yf, (float*)lam, st, sf, cap, 29, true);
+    osc<GenTree29::Osc23, float, 40, 144, 3, kTrigCall>("t29 osc23 f32 call", N29, xf, yf, (float*)lam, st, sf, cap, 29);
+    k_fill<<<1184, 256>>>(x, N29 * 29 * 6, 2);
+    jvp<GenTree29::AbaJvp, double, 40, 220, 1>("t29 abajvp f64 r40 s220 b1 lib", N29, x, y, scratch, cap);
+    jvp<GenTree29::AbaJvp, double, 40, 220, 1, kTrigCall>("t29 abajvp f64 r40 s220 b1 call", N29, x, y, scratch, cap);
+    jvp<GenTree29::RneaJvp, double, 40, 110, 2>("t29 rneajvp f64 lib", N29, x, y, scratch, cap);
+    k_fill<<<1184, 256>>>(xf, N29 * 29 * 6, 2);
+    jvp<GenTree29::AbaJvp, float, 40, 220, 2>("t29 abajvp f32 r40 s220 b2 lib", N29, xf, yf, sf, cap);
+    jvp<GenTree29::AbaJvp, float, 40, 220, 2, kTrigCall>("t29 abajvp f32 r40 s220 b2 call", N29, xf, yf, sf, cap);
+    jvp<GenTree29::RneaJvp, float, 0, 144, 3>("t29 rneajvp f32 s144 b3 lib", N29, xf, yf, sf, cap);
+    jvp<GenTree29::RneaJvp, float, 0, 144, 3, kTrigCall>("t29 rneajvp f32 s144 b3 call", N29, xf, yf, sf, cap);
+    k_fill<<<1184, 256>>>(x, N29 * 87, 2);
+    plain<GenTree29::RneaGrav, double, 0, 55, 3, false, false>("t29 rneagrav f64 lib", N29, x, y, st, scratch, cap, true);
+    plain<GenTree29::RneaGrav, double, 0, 55, 3, kTrigCall, false>("t29 rneagrav f64 call", N29, x, y, st, scratch, cap);
+    plain<GenTree29::Crba, double, 0, 55, 3, false, true>("t29 crba f64 lib", N29, x, y, st, scratch, cap, true);
+    plain<GenTree29::Crba, double, 0, 55, 3, kTrigCall, true>("t29 crba f64 call", N29, x, y, st, scratch, cap);
   }
   if (ON("t29")) {
     k_fill<<<1184, 256>>>(x, N29 * 87, 2);
