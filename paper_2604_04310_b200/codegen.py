@@ -92,8 +92,19 @@ ONE = K(1.0)
 # (LDCU.128 into uniform registers, two constants per instruction); round 2,
 # tools/async_sweep.cu: G1 ABA 0.294 -> 0.290 ms, G1 RNEA 0.099 -> 0.116,
 # Panda ABA 0.539 -> 0.571, G1 OSC 0.61 -> 0.67 ms.  Literals stay the default.
+#
+# Per routine (POOL_OPS, round 2): the G1 ABA reads its constants from the
+# robot's __constant__ table with plain C++ reads and runs through k_gen_call,
+# which calls the routine once per state out of line, so there is no loop to
+# hoist the table reads out of and ptxas folds them into the DFMAs as
+# constant-bank operands (tools/call_sweep.cu: 0.261 -> 0.242 ms fp64; the
+# Panda ABA, the G1 RNEA / CRBA / FK and the fp32 routines measured no gain or
+# a loss with it).
 POOL = {}
-USE_POOL = os.environ.get("VD_GEN_POOL", "") == "asm"
+POOL_MODE = os.environ.get("VD_GEN_POOL", "")  # "" literals, "asm" opaque ld.const, "table" plain table reads
+USE_POOL = POOL_MODE in ("asm", "table")
+POOL_OPS = {"tree29": ("Aba", "AbaFext")}
+_POOL_ON = False  # set by emit_body while it generates a POOL_OPS routine
 
 
 def _low32_zero(c):
@@ -121,7 +132,7 @@ class Gen:
             return f"{t}(1)"
         if c == -1.0:
             return f"{t}(-1)"
-        if _low32_zero(c) or not USE_POOL or t != "T":  # immediate / literal
+        if _low32_zero(c) or not (USE_POOL or _POOL_ON) or t != "T":  # immediate / literal
             return f"{t}({float.hex(c)})"
         if c not in POOL:
             POOL[c] = len(POOL)
@@ -1695,7 +1706,7 @@ OPS = [("Aba", gen_aba, lambda rb: rb.n, 3),
 
 def emit(name, cls, rb):
     POOL.clear()
-    body = emit_body(name, cls, rb)
+    body = emit_body(name, cls, rb, pool_ops=POOL_OPS.get(name, ()))
     import struct
     vals = sorted(POOL, key=lambda c: POOL[c])
     dv = ", ".join(float.hex(c) for c in vals) or "0.0"
@@ -1706,27 +1717,34 @@ def emit(name, cls, rb):
     # the routine out of the persistent loop into registers.  C linkage: the
     # asm names the table; the header is included by one translation unit
     # per binary.
+    # (table reads need no symbol name: internal linkage, no extern "C")
+    if POOL_MODE == "asm":
+        dev = [f'extern "C" {{ __constant__ double vd_kd_{name}[{n}] = {{{dv}}}; }}',
+               f'extern "C" {{ __constant__ float vd_kf_{name}[{n}] = {{{fv}}}; }}']
+    else:
+        dev = [f"static __constant__ double vd_kd_{name}[{n}] = {{{dv}}};",
+               f"static __constant__ float vd_kf_{name}[{n}] = {{{fv}}};"]
     pre = [f"// ---- {name}: {len(vals)} model constants",
-           "#if defined(__CUDACC__)",
-           f'extern "C" {{ __constant__ double vd_kd_{name}[{n}] = {{{dv}}}; }}',
-           f'extern "C" {{ __constant__ float vd_kf_{name}[{n}] = {{{fv}}}; }}',
+           "#if defined(__CUDACC__)"] + dev + [
            "#endif",
            f"static const double vd_hkd_{name}[{n}] = {{{dv}}};",
            f"static const float vd_hkf_{name}[{n}] = {{{fv}}};"]
     kc = ["  template <class T, int I>",
           "  VD_HD static T kc() {",
-          "#if defined(__CUDA_ARCH__)",
+          "#if defined(__CUDA_ARCH__)"] + ([
+          f"    if constexpr (sizeof(T) == 8) return vd_kd_{name}[I]; else return vd_kf_{name}[I];"]
+          if POOL_MODE != "asm" else [
           "    T v;",
           "    if constexpr (sizeof(T) == 8)",
           f'      asm volatile("ld.const.f64 %0, [vd_kd_{name}+%1];" : "=d"(v) : "n"(I * 8));',
           "    else",
           f'      asm volatile("ld.const.f32 %0, [vd_kf_{name}+%1];" : "=f"(v) : "n"(I * 4));',
-          "    return v;",
+          "    return v;"]) + [
           "#else",
           f"    if constexpr (sizeof(T) == 8) return vd_hkd_{name}[I]; else return vd_hkf_{name}[I];",
           "#endif",
           "  }"]
-    if not USE_POOL:  # literals only: no table, no accessor
+    if not POOL:  # literals only: no table, no accessor
         return body
     return pre + body[:4] + kc + body[4:]
 
@@ -1737,15 +1755,20 @@ JIT_OPS = ("Aba", "AbaMixed", "Rnea", "RneaBias", "RneaGrav", "RneaFext", "RneaB
            "Crba", "CrbaPacked", "Fk")
 
 
-def emit_body(name, cls, rb, ops=None, tasks=True, task_joints=None):
+def emit_body(name, cls, rb, ops=None, tasks=True, task_joints=None, pool_ops=()):
     out = [f"// ---- {name}",
            f"struct Gen{cls} {{",
            f"  static constexpr int kN = {rb.n};",
            f"  static constexpr uint64_t kFingerprint = {rb.d['fp']:#x}ull;"]
+    global _POOL_ON
     for op, fn, nout, nin in OPS:
         if ops is not None and op not in ops:
             continue
-        A = fn(rb)
+        _POOL_ON = op in pool_ops
+        try:
+            A = fn(rb)
+        finally:
+            _POOL_ON = False
         out += [f"  // {op}: {A.g.flops} mul/add after folding; {A.nslot} slots, the first {A.nprologue} written by the prologue",
                 f"  struct {op} {{",
                 f"    static constexpr int kSlots = {A.nslot};",

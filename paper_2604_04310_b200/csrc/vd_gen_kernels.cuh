@@ -197,6 +197,61 @@ __global__ void __launch_bounds__(kBlk, kMinB)
   }
 }
 
+// k_gen with the routine called out of line once per state (Cfg::kCall).
+// A routine that reads its constants from the robot's __constant__ table
+// (codegen POOL_OPS) needs this: inside the persistent loop the compiler
+// hoists every table read out of the loop into registers (and spills them);
+// in the per-state function there is no loop, so the reads become
+// constant-bank operands of the DFMAs (G1 ABA fp64 0.261 -> 0.242 ms,
+// tools/call_sweep.cu).
+template <class Op, class T, int kReg, int kSmem, int kFast, bool kStream>
+__device__ __noinline__ bool gen_state(const T* x0, const T* x1, const T* x2, const T* fx, const T* gp, int64_t ld,
+                                       T* y, int64_t ldo, bool active, T* sb, uint32_t sm, T g0, T g1, T g2) {
+  GenCx<T, Op::kSlots, kReg, kSmem, kFast, kStream> cx;
+  cx.in_[0] = x0;
+  cx.in_[1] = x1;
+  cx.in_[2] = x2;
+  cx.fx_ = fx;
+  cx.gp_ = gp;
+  cx.out_ = y;
+  cx.ld = ld;
+  cx.ldo = ldo;
+  cx.active = active;
+  cx.sb = sb;
+  cx.sm = sm;
+  cx.g3[0] = g0;
+  cx.g3[1] = g1;
+  cx.g3[2] = g2;
+  return Op::template run<T>(cx);
+}
+
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kFast = kTrigLib, bool kStream = false>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen_call(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
+               T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status,
+               T* __restrict__ scratch, const T* __restrict__ fext, const T* __restrict__ gpl) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenCx<T, Op::kSlots, kReg, kSmem, kFast, kStream>;
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  T* sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  const uint32_t sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    const bool active = i0 < N;
+    const int64_t i = active ? i0 : N - 1;
+    const bool ok = gen_state<Op, T, kReg, kSmem, kFast, kStream>(
+        x0 + i, (Op::kIn > 1 ? x1 : x0) + i, (Op::kIn > 2 ? x2 : x0) + i, fext ? fext + i : nullptr,
+        gpl ? gpl + i : nullptr, ldi, y + i, ldo, active, sb, sm, g0, g1, g2);
+    if (active) {
+      if (!ok) {
+        for (int j = 0; j < Op::kOut; ++j) y[(int64_t)j * ldo + i] = T(0);
+      }
+      if (status) status[i] = ok ? 0 : 7;
+    }
+  }
+}
+
 // Asynchronous state input.  The inputs of the state a thread processes next
 // are copied global -> shared memory with per-thread cp.async (no CTA barrier:
 // each thread reads only the elements it copied) while it computes the current

@@ -68,27 +68,36 @@ Occ occupancy(Kern kern, size_t smem) {
   return c;
 }
 
-// The kernel of a Cfg: asynchronous state input when it asks for it.
-template <class Op, class T, class C, bool kAsync>
+// kCall (k_gen_call): the routine out of line once per state; false unless a Cfg sets it
+template <class C, class = void>
+struct CallIo : std::false_type {};
+template <class C>
+struct CallIo<C, std::void_t<decltype(C::kCall)>> : std::bool_constant<C::kCall> {};
+
+// The kernel of a Cfg (kMode 0 k_gen, 1 k_gen_async, 2 k_gen_call).
+template <class Op, class T, class C, int kMode>
 constexpr auto gen_kernel() {
-  if constexpr (kAsync)
+  if constexpr (kMode == 1)
     return k_gen_async<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
+  else if constexpr (kMode == 2)
+    return k_gen_call<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
   else
     return k_gen<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
 }
 
-template <class Op, class T, bool kAsync>
+template <class Op, class T, int kMode>
 int launch_gen(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
                int32_t* status, const void* fext) {
   using C = Cfg<Op, T>;
-  auto kern = gen_kernel<Op, T, C, kAsync>();
+  constexpr bool kAsync = kMode == 1;
+  auto kern = gen_kernel<Op, T, C, kMode>();
   constexpr size_t smem = kAsync ? gen_async_smem<Op, T, C::kReg, C::kSmem>() : (size_t)C::kSmem * kGenBlock * sizeof(T);
-  const Occ o = occupancy<Op, T, kAsync>(kern, smem);
+  const Occ o = occupancy<Op, T, kMode>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
   cudaStream_t s = static_cast<cudaStream_t>(L.stream);
   if (debug_launches())
     std::fprintf(stderr, "[vd] k_gen%s slots %d reg %d smem %d: %d CTAs/SM x %d SMs, grid %lld, smem %zu B\n",
-                 kAsync ? "_async" : "", Op::kSlots, C::kReg, C::kSmem, o.blocks_per_sm, o.sms, (long long)blocks, smem);
+                 kMode == 1 ? "_async" : (kMode == 2 ? "_call" : ""), Op::kSlots, C::kReg, C::kSmem, o.blocks_per_sm, o.sms, (long long)blocks, smem);
   // L2-resident scratch for the slots that are neither in registers nor in
   // shared memory: one slab per resident thread, stream-ordered from the
   // library's private pool (scratch_alloc: no synchronisation, safe for
@@ -116,9 +125,10 @@ template <class Op, class T>
 int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
              int32_t* status, const void* fext = nullptr) {
   if constexpr (AsyncIo<Cfg<Op, T>>::value) {
-    if (!L.gravity_planes) return launch_gen<Op, T, true>(L, x0, x1, x2, g3, y, status, fext);
+    if (!L.gravity_planes) return launch_gen<Op, T, 1>(L, x0, x1, x2, g3, y, status, fext);
   }
-  return launch_gen<Op, T, false>(L, x0, x1, x2, g3, y, status, fext);
+  if constexpr (CallIo<Cfg<Op, T>>::value) return launch_gen<Op, T, 2>(L, x0, x1, x2, g3, y, status, fext);
+  return launch_gen<Op, T, 0>(L, x0, x1, x2, g3, y, status, fext);
 }
 
 template <class Op>

@@ -61,11 +61,13 @@ struct Cfg<GenChain7::AbaFext, T> : Cfg<GenChain7::Aba, T> {};
 // (async_sweep "t29", sweep.py, 262144 states: ABA fp64 0.295 -> 0.264 ms,
 // mixed fp32 0.170 -> 0.146 ms, RNEA fp64 0.100 -> 0.094 ms); the CRBA, FK
 // and gravity routines stay inlined (the call makes them 1-15 % slower).
+// The G1 ABA reads its constants from the __constant__ table (codegen
+// POOL_OPS) and runs out of line per state (k_gen_call): 0.261 -> 0.242 ms.
 template <>
 struct Cfg<GenTree29::Aba, double> {
   static constexpr int kReg = 40, kSmem = 113, kMinB = 2;
   static constexpr int kFast = kTrigCall;
-  static constexpr bool kStream = true;
+  static constexpr bool kStream = true, kCall = true;
 };
 template <>
 struct Cfg<GenTree29::AbaMixed, float> {  // the trunk's fp64 slots (stored last) in registers
