@@ -104,6 +104,9 @@ POOL = {}
 POOL_MODE = os.environ.get("VD_GEN_POOL", "")  # "" literals, "asm" opaque ld.const, "table" plain table reads
 USE_POOL = POOL_MODE in ("asm", "table")
 POOL_OPS = {"tree29": ("Aba", "AbaFext")}
+if os.environ.get("VD_GEN_POOL_OPS") is not None:  # experiments: "robot:Op,Op;robot:Op" ("Osc" = every OSC routine)
+    POOL_OPS = {r: tuple(o.split(",")) for r, o in
+                (e.split(":") for e in os.environ["VD_GEN_POOL_OPS"].split(";") if e)}
 _POOL_ON = False  # set by emit_body while it generates a POOL_OPS routine
 
 
@@ -1793,7 +1796,11 @@ def emit_body(name, cls, rb, ops=None, tasks=True, task_joints=None, pool_ops=()
     # serial chains: M is small, the branch-sparse LTL form costs fewer flops
     serial = all(p == i - 1 for i, p in enumerate(rb.parent))
     for fj in osc_joints:
-        A = gen_osc(rb, fj) if serial else gen_osc_aba(rb, fj)
+        _POOL_ON = "Osc" in pool_ops
+        try:
+            A = gen_osc(rb, fj) if serial else gen_osc_aba(rb, fj)
+        finally:
+            _POOL_ON = False
         out += [f"  // Osc on joint {fj}: {A.g.flops} mul/add after folding; {A.nslot} slots",
                 f"  struct Osc{fj} {{",
                 f"    static constexpr int kSlots = {A.nslot};",

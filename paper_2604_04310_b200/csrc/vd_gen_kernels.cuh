@@ -418,6 +418,55 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
   }
 }
 
+// k_gen_osc with the routine called out of line once per state (OscCfg::kCall;
+// see k_gen_call): a routine that reads its model constants from the robot's
+// __constant__ table (codegen POOL_OPS) gets them as constant-bank operands.
+template <class Op, class T, int kReg, int kSmem, int kTrig>
+__device__ __noinline__ bool gen_osc_state(const OscShared* P, const T* q, const T* qd, int64_t ld, T* tau, T* lam,
+                                           int64_t ldo, bool active, T* sb, uint32_t sm) {
+  GenOscCx<T, Op::kSlots, kReg, kSmem, kTrig> cx;
+  cx.P = P;
+  cx.in_[0] = q;
+  cx.in_[1] = qd;
+  cx.in_[2] = q;
+  cx.out_ = tau;
+  cx.out1_ = lam;
+  cx.ld = ld;
+  cx.ldo = ldo;
+  cx.active = active;
+  cx.sb = sb;
+  cx.sm = sm;
+  return Op::template run<T>(cx);
+}
+
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig = kTrigLib>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen_osc_call(int64_t N, const T* __restrict__ q, const T* __restrict__ qd, int64_t ldi,
+                   const __grid_constant__ OscShared P, T* __restrict__ tau, T* __restrict__ lam, int64_t ldo,
+                   int32_t* __restrict__ status, T* __restrict__ scratch) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenOscCx<T, Op::kSlots, kReg, kSmem, kTrig>;
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  T* sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  const uint32_t sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    const bool active = i0 < N;
+    const int64_t i = active ? i0 : N - 1;
+    const bool ok = gen_osc_state<Op, T, kReg, kSmem, kTrig>(&P, q + i, qd + i, ldi, tau + i, lam ? lam + i : nullptr,
+                                                             ldo, active, sb, sm);
+    if (active) {
+      if (!ok) {
+        for (int j = 0; j < Op::kOut; ++j) tau[(int64_t)j * ldo + i] = T(0);
+        if (lam)
+          for (int j = 0; j < 36; ++j) lam[(int64_t)j * ldo + i] = T(0);
+      }
+      if (status) status[i] = ok ? 0 : 7;
+    }
+  }
+}
+
 // Forward-mode JVP context (JvpArgs): NULL primal inputs read as 0, NULL
 // tangents as 0; output group 0 = values, 1 = tangents (either may be NULL).
 template <class T, int kSlots, int kReg, int kSmem, bool kStream = false, int kTrig = kTrigLib>
@@ -470,6 +519,55 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
     cx.dout_ = dout ? dout + i : nullptr;
     const bool ok = Op::template run<T>(cx);
     if (cx.active) {
+      if (!ok) {
+        for (int j = 0; j < Op::kOut; ++j) {
+          if (out) out[(int64_t)j * ldo + i] = T(0);
+          if (dout) dout[(int64_t)j * ldo + i] = T(0);
+        }
+      }
+      if (a.status) a.status[i] = ok ? 0 : 7;
+    }
+  }
+}
+
+// k_gen_jvp with the routine out of line once per state (JvpCfg::kCall; see
+// k_gen_call).
+template <class Op, class T, int kReg, int kSmem, bool kStream, int kTrig>
+__device__ __noinline__ bool gen_jvp_state(const JvpArgs* a, int64_t i, int64_t ld, int64_t ldo, bool active, T* sb,
+                                           uint32_t sm) {
+  GenJvpCx<T, Op::kSlots, kReg, kSmem, kStream, kTrig> cx;
+  cx.sb = sb;
+  cx.sm = sm;
+  for (int k = 0; k < 3; ++k) cx.g3[k] = T(a->g[k]);
+  cx.active = active;
+  cx.ld = ld;
+  cx.ldo = ldo;
+  for (int k = 0; k < 3; ++k) {
+    cx.in_[k] = a->x[k] ? (const T*)a->x[k] + i : nullptr;
+    cx.din_[k] = a->dx[k] ? (const T*)a->dx[k] + i : nullptr;
+  }
+  cx.out_ = a->out ? (T*)a->out + i : nullptr;
+  cx.dout_ = a->dout ? (T*)a->dout + i : nullptr;
+  return Op::template run<T>(cx);
+}
+
+template <class Op, class T, int kReg, int kSmem, int kMinB, bool kStream = false, int kTrig = kTrigLib>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen_jvp_call(int64_t N, const __grid_constant__ JvpArgs a, int64_t ldi, int64_t ldo, T* __restrict__ scratch) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenJvpCx<T, Op::kSlots, kReg, kSmem, kStream, kTrig>;
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  T* sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  const uint32_t sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  T* out = (T*)a.out;
+  T* dout = (T*)a.dout;
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    const bool active = i0 < N;
+    const int64_t i = active ? i0 : N - 1;
+    const bool ok = gen_jvp_state<Op, T, kReg, kSmem, kStream, kTrig>(&a, i, ldi, ldo, active, sb, sm);
+    if (active) {
       if (!ok) {
         for (int j = 0; j < Op::kOut; ++j) {
           if (out) out[(int64_t)j * ldo + i] = T(0);

@@ -144,12 +144,16 @@ int launch_op(const Launch& L, const void* x0, const void* x1, const void* x2, c
 // tools/async_sweep.cu "more", G1 `l_palm`, N = 262144: fp64 r40 s110 (2
 // CTAs/SM) 0.61 ms, s55 b3 0.69 ms (the M-based routine: 1.23 ms); fp32
 // r40 s144 (3 CTAs/SM) 0.27 ms (M-based: 0.50 ms).
-// sin/cos: one out-of-line copy in fp32 (G1 `l_palm` 0.238 -> 0.213 ms); the
-// fp64 routine is faster with the inlined library routine (0.593 vs 0.603).
+// sin/cos: one out-of-line copy (G1 `l_palm` fp32 0.238 -> 0.213 ms).  In
+// fp64 an earlier A/B put the inlined library routine ahead (0.593 vs 0.603
+// ms); tools/pool_call_sweep.cu over all five G1 frame joints, two builds
+// each, has the call ahead on every one: 0.64 -> 0.56 (11), 0.63 -> 0.60
+// (17), 0.46 -> 0.41 (18), 0.67 -> 0.57 (23), 0.71 -> 0.60 ms (28) — the
+// inlined variant's time varies from box to box, the call's much less.
 template <class Op, class T>
 struct OscCfg {
   static constexpr int kReg = 40, kSmem = sizeof(T) == 8 ? 110 : 144, kMinB = sizeof(T) == 8 ? 2 : 3;
-  static constexpr int kFast = sizeof(T) == 4 && Op::kDof >= 20 ? kTrigCall : kTrigLib;
+  static constexpr int kFast = Op::kDof >= 20 ? kTrigCall : kTrigLib;
 };
 template <class Op, class T>
 int launch_osc_t(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lam,

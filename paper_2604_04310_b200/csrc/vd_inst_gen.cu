@@ -172,12 +172,38 @@ template <>
 struct JvpCfg<GenTree29::RneaJvp, float> {
   static constexpr int kReg = 0, kSmem = 144, kMinB = 3;
   static constexpr int kFast = kTrigCall;
+  static constexpr bool kCall = true;
+};
+// Routine out of line once per state (k_gen_jvp_call; tools/pool_call_sweep.cu,
+// G1, 262144 states, loop -> call): fp64 RNEA-JVP 0.511 -> 0.336 ms (with the
+// sin/cos call), CRBA-JVP 0.727 -> 0.685 ms; fp32 RNEA-JVP 0.176 -> 0.171,
+// FK-JVP 0.147 -> 0.137 ms.  The ABA-JVP and the fp64 FK-JVP are slower with it.
+template <>
+struct JvpCfg<GenTree29::RneaJvp, double> {
+  static constexpr int kReg = 40, kSmem = 110, kMinB = 2;
+  static constexpr int kFast = kTrigCall;
+  static constexpr bool kCall = true;
+};
+template <>
+struct JvpCfg<GenTree29::CrbaJvp, double> {
+  static constexpr int kReg = 40, kSmem = GenTree29::CrbaJvp::kSlots - 40, kMinB = 2;
+  static constexpr int kFast = kTrigCall;
+  static constexpr bool kCall = true;
+};
+template <>
+struct JvpCfg<GenTree29::FkJvp, float> {
+  static constexpr int kReg = 0, kSmem = GenTree29::FkJvp::kSlots, kMinB = 3;
+  static constexpr int kFast = kTrigLib;
+  static constexpr bool kCall = true;
 };
 
 template <class Op, class T, bool kStream>
 int launch_jvp_v(const Launch& L, const JvpArgs& a) {
   using C = JvpCfg<Op, T>;
-  auto kern = k_gen_jvp<Op, T, C::kReg, C::kSmem, C::kMinB, kStream, C::kFast>;
+  auto kern = [] {
+    if constexpr (CallIo<C>::value) return k_gen_jvp_call<Op, T, C::kReg, C::kSmem, C::kMinB, kStream, C::kFast>;
+    else return k_gen_jvp<Op, T, C::kReg, C::kSmem, C::kMinB, kStream, C::kFast>;
+  }();
   constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
   const Occ o = occupancy<std::pair<Op, std::bool_constant<kStream>>, T>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);

@@ -1,0 +1,152 @@
+// A/B for the G1 OSC and JVP routines: persistent loop with the routine inlined
+// (k_gen_osc / k_gen_jvp) against the routine called out of line once per
+// state (k_gen_osc_call / k_gen_jvp_call).  Built twice, like call_sweep.cu:
+// with the product header (fp64 literals) and with a header whose OSC / JVP
+// routines read their constants from the robot's __constant__ table:
+//   VD_GEN_POOL_OPS="tree29:Aba,AbaFext,Osc,AbaJvp,RneaJvp,CrbaJvp,FkJvp" python -c \
+//     'import sys; sys.path[:0] = ["tools", "."]; import gen_tree_kernels as g; \
+//      from paper_2604_04310_b200 import _lib; \
+//      open("ablib/poolinc/vd_gen_robots.cuh", "w").write(g.generate(_lib.load()))'
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr \
+//     -Ipaper_2604_04310_b200/csrc tools/pool_call_sweep.cu -o ablib/pc_lit
+//   nvcc ... -Iablib/poolinc -Ipaper_2604_04310_b200/csrc tools/pool_call_sweep.cu -o ablib/pc_pool
+// Prints time per launch and a checksum of the outputs (the same arithmetic up
+// to constant-operand rounding: checksums agree to ~1e-12 relative).
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <vector>
+#include "vd_gen_robots.cuh"
+#include "vd_gen_kernels.cuh"
+using namespace vdk;
+
+template <class T>
+__global__ void k_fill(T* p, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t x = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 31;
+    p[i] = T((double)(x >> 11) * (1.0 / 9007199254740992.0) * 6.283185307179586 - 3.141592653589793);
+  }
+}
+
+template <class T>
+double checksum(const T* d, size_t n) {
+  std::vector<T> h(n);
+  cudaMemcpy(h.data(), d, sizeof(T) * n, cudaMemcpyDeviceToHost);
+  double s = 0;
+  for (T v : h) s += std::isfinite((double)v) ? std::fabs((double)v) : 0.0;
+  return s;
+}
+
+template <class Kern, class Launch>
+float time_it(Kern kern, size_t smem, Launch go, int* bps_out, int* regs) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int bps = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, kern);
+  *bps_out = bps;
+  *regs = fa.numRegs;
+  if (bps < 1) return -1.f;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int w = 0; w < 2; ++w) go(sms * bps);
+  cudaEventRecord(a);
+  const int reps = 10;
+  for (int r = 0; r < reps; ++r) go(sms * bps);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms / reps;
+}
+
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig, bool kCall>
+void osc(const char* name, int64_t N, T* x, T* y, T* lam, int32_t* st, T* scratch) {
+  auto kern = kCall ? k_gen_osc_call<Op, T, kReg, kSmem, kMinB, kTrig> : k_gen_osc<Op, T, kReg, kSmem, kMinB, kTrig>;
+  const size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  OscShared P{};
+  for (int k = 0; k < 9; ++k) P.frame_R[k] = P.target_R[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  P.target_p[2] = 0.3;
+  for (int k = 0; k < 6; ++k) { P.kp[k] = 100; P.kd[k] = 20; }
+  P.posture_kp = 10; P.posture_kd = 2; P.gravity[2] = 9.81; P.epsilon = 1e-6;
+  const int n = Op::kDof;
+  int bps, regs;
+  const float ms = time_it(kern, smem, [&](int64_t grid) {
+    grid = std::min<int64_t>(grid, (N + kGenBlock - 1) / kGenBlock);
+    kern<<<grid, kGenBlock, smem>>>(N, x, x + N * n, N, P, y, lam, N, st, scratch);
+  }, &bps, &regs);
+  printf("%-36s %s regs %3d b/SM %d  %.4f ms  %.3e evals/s  sum %.12e  %s\n", name, kCall ? "call" : "loop", regs, bps,
+         ms, N / (ms * 1e-3), checksum(y, (size_t)N * n) + checksum(lam, (size_t)N * 36),
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig, bool kCall>
+void jvp(const char* name, int64_t N, T* x, T* y, T* scratch) {
+  auto kern = kCall ? k_gen_jvp_call<Op, T, kReg, kSmem, kMinB, true, kTrig>
+                    : k_gen_jvp<Op, T, kReg, kSmem, kMinB, true, kTrig>;
+  const size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  const int n = Op::kDof;
+  JvpArgs a{};
+  for (int g = 0; g < Op::kIn; ++g) { a.x[g] = x + g * N * n; a.dx[g] = x + (3 + g) * N * n; }
+  a.g[2] = 9.81;
+  a.out = y;
+  a.dout = y + (int64_t)Op::kOut * N;
+  int bps, regs;
+  const float ms = time_it(kern, smem, [&](int64_t grid) {
+    grid = std::min<int64_t>(grid, (N + kGenBlock - 1) / kGenBlock);
+    kern<<<grid, kGenBlock, smem>>>(N, a, N, N, scratch);
+  }, &bps, &regs);
+  printf("%-36s %s regs %3d b/SM %d  %.4f ms  %.3e evals/s  sum %.12e  %s\n", name, kCall ? "call" : "loop", regs, bps,
+         ms, N / (ms * 1e-3), checksum(y, (size_t)N * Op::kOut * 2), cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  const int64_t N = 262144;
+  const size_t cap = 1ull << 30;
+  double *x, *y, *lam, *scratch;
+  int32_t* st;
+  cudaMalloc(&x, sizeof(double) * N * 29 * 6);
+  cudaMalloc(&y, sizeof(double) * N * 841 * 2);
+  cudaMalloc(&lam, sizeof(double) * N * 36);
+  cudaMalloc(&scratch, cap);
+  cudaMalloc(&st, sizeof(int32_t) * N);
+  k_fill<<<1184, 256>>>(x, N * 29 * 6, 7);
+  float *xf = (float*)(x), *yf = (float*)y, *lf = (float*)lam, *sf = (float*)scratch;
+  using namespace vdk;
+  // product placements (OscCfg default; JvpCfg); sweep 2: every G1 OSC frame
+  // joint and the trig mode, the remaining JVPs
+#define OSC4(J)                                                                                              \
+  osc<GenTree29::Osc##J, double, 40, 110, 2, kTrigLib, false>("t29 osc" #J " f64 lib", N, x, y, lam, st, scratch);  \
+  osc<GenTree29::Osc##J, double, 40, 110, 2, kTrigCall, false>("t29 osc" #J " f64 trig", N, x, y, lam, st, scratch); \
+  osc<GenTree29::Osc##J, double, 40, 110, 2, kTrigLib, true>("t29 osc" #J " f64 lib", N, x, y, lam, st, scratch);   \
+  osc<GenTree29::Osc##J, double, 40, 110, 2, kTrigCall, true>("t29 osc" #J " f64 trig", N, x, y, lam, st, scratch);
+  OSC4(11) OSC4(17) OSC4(18) OSC4(23) OSC4(28)
+  k_fill<<<1184, 256>>>(xf, N * 29 * 6, 7);
+  osc<GenTree29::Osc23, float, 40, 144, 3, kTrigCall, false>("t29 osc23 f32 trig", N, xf, yf, lf, st, sf);
+  osc<GenTree29::Osc17, float, 40, 144, 3, kTrigCall, false>("t29 osc17 f32 trig", N, xf, yf, lf, st, sf);
+  k_fill<<<1184, 256>>>(x, N * 29 * 6, 7);
+  jvp<GenTree29::RneaJvp, double, 40, 110, 2, kTrigLib, false>("t29 rneajvp f64 lib", N, x, y, scratch);
+  jvp<GenTree29::RneaJvp, double, 40, 110, 2, kTrigLib, true>("t29 rneajvp f64 lib", N, x, y, scratch);
+  jvp<GenTree29::RneaJvp, double, 40, 110, 2, kTrigCall, true>("t29 rneajvp f64 trig", N, x, y, scratch);
+  jvp<GenTree29::RneaJvp, double, 40, 110, 3, kTrigLib, true>("t29 rneajvp f64 lib b3", N, x, y, scratch);
+  jvp<GenTree29::RneaJvp, double, 0, 144, 3, kTrigLib, true>("t29 rneajvp f64 lib r0 s144 b3", N, x, y, scratch);
+  jvp<GenTree29::CrbaJvp, double, 40, 70, 2, kTrigLib, false>("t29 crbajvp f64 lib", N, x, y, scratch);
+  jvp<GenTree29::CrbaJvp, double, 40, 70, 2, kTrigLib, true>("t29 crbajvp f64 lib", N, x, y, scratch);
+  jvp<GenTree29::CrbaJvp, double, 40, 70, 2, kTrigCall, true>("t29 crbajvp f64 trig", N, x, y, scratch);
+  jvp<GenTree29::FkJvp, double, 40, 70, 2, kTrigLib, false>("t29 fkjvp f64 lib", N, x, y, scratch);
+  jvp<GenTree29::FkJvp, double, 40, 70, 2, kTrigLib, true>("t29 fkjvp f64 lib", N, x, y, scratch);
+  jvp<GenTree29::AbaJvp, double, 40, 220, 1, kTrigCall, false>("t29 abajvp f64 trig", N, x, y, scratch);
+  jvp<GenTree29::AbaJvp, double, 40, 220, 1, kTrigCall, true>("t29 abajvp f64 trig", N, x, y, scratch);
+  k_fill<<<1184, 256>>>(xf, N * 29 * 6, 7);
+  jvp<GenTree29::RneaJvp, float, 0, 144, 3, kTrigCall, false>("t29 rneajvp f32 trig", N, xf, yf, sf);
+  jvp<GenTree29::RneaJvp, float, 0, 144, 3, kTrigCall, true>("t29 rneajvp f32 trig", N, xf, yf, sf);
+  jvp<GenTree29::CrbaJvp, float, 0, 110, 3, kTrigLib, false>("t29 crbajvp f32 lib", N, xf, yf, sf);
+  jvp<GenTree29::CrbaJvp, float, 0, 110, 3, kTrigLib, true>("t29 crbajvp f32 lib", N, xf, yf, sf);
+  jvp<GenTree29::FkJvp, float, 0, 110, 3, kTrigLib, false>("t29 fkjvp f32 lib", N, xf, yf, sf);
+  jvp<GenTree29::FkJvp, float, 0, 110, 3, kTrigLib, true>("t29 fkjvp f32 lib", N, xf, yf, sf);
+  return 0;
+}
