@@ -354,7 +354,7 @@ def run_ours(args):
     # DRAM traffic per launch of this kernel at this N from the committed
     # `ncu --set full` capture (tools/capture_profiles.sh; ncu cannot run
     # inside the timed bench)
-    prof = next((os.path.join(ROOT, "profiles", f"{r}_chain7_aba_f64.json") for r in ("r02", "r01")
+    prof = next((os.path.join(ROOT, "profiles", f"{r}_chain7_aba_f64.json") for r in ("r02b", "r02", "r01")
                  if os.path.exists(os.path.join(ROOT, "profiles", f"{r}_chain7_aba_f64.json"))), "")
     if prof:
         with open(prof) as f:

@@ -130,14 +130,14 @@ def main():
     specs = [("chain7_aba_f64", "k_gen_async<GenChain7::Aba, double> (generated, cp.async state prefetch, fast fp64 "
                                 "sincos)", 4194304,
               bench.flops_per_eval("chain7", "aba"), 224),
-             ("tree29_aba_f64", "k_gen<GenTree29::Aba, double> (generated)", 262144, bench.flops_per_eval("tree29", "aba"), 928),
+             ("tree29_aba_f64", "k_gen_call<GenTree29::Aba, double> (generated, constants from the __constant__ table, routine out of line per state)", 262144, bench.flops_per_eval("tree29", "aba"), 928),
              ("tree29_rnea_f64", "k_gen<GenTree29::Rnea, double> (generated)", 262144,
               bench.flops_per_eval("tree29", "rnea"), 928),
              ("tree29_crba_f64", "k_gen<GenTree29::Crba, double> (generated)", 262144,
               bench.flops_per_eval("tree29", "crba"), 232 + 6728),
              ("tree29_crba_packed_f64", "k_gen<GenTree29::CrbaPacked, double> (generated, 242 packed planes)", 262144,
               bench.flops_per_eval("tree29", "crba"), 232 + 242 * 8),
-             ("tree29_osc_f64", "k_gen_osc<GenTree29::Osc23, double> (generated, frame l_palm)", 262144, None,
+             ("tree29_osc_f64", "k_gen_osc<GenTree29::Osc23, double> (generated, frame l_palm, out-of-line sin/cos)", 262144, None,
               464 + 232 + 288)]
     for key, name, states, fl, bps in specs:
         rep = os.path.join(OUT, f"{r}_{key}.ncu-rep")
