@@ -104,19 +104,64 @@ void jvp(const char* name, int64_t N, T* x, T* y, T* scratch) {
          ms, N / (ms * 1e-3), checksum(y, (size_t)N * Op::kOut * 2), cudaGetErrorString(cudaGetLastError()));
 }
 
-int main() {
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig, bool kStream, bool kCall>
+void gen(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch) {
+  auto kern = kCall ? k_gen_call<Op, T, kReg, kSmem, kMinB, kTrig, kStream> : k_gen<Op, T, kReg, kSmem, kMinB, kTrig, kStream>;
+  const size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  const int n = Op::kDof;
+  int bps, regs;
+  const float ms = time_it(kern, smem, [&](int64_t grid) {
+    grid = std::min<int64_t>(grid, (N + kGenBlock - 1) / kGenBlock);
+    kern<<<grid, kGenBlock, smem>>>(N, x, x + N * n, x + 2 * N * n, N, T(0), T(0), T(9.81), y, N, st, scratch, nullptr,
+                                    nullptr);
+  }, &bps, &regs);
+  printf("%-36s %s regs %3d b/SM %d  %.4f ms  %.3e evals/s  sum %.12e  %s\n", name, kCall ? "call" : "loop", regs, bps,
+         ms, N / (ms * 1e-3), checksum(y, (size_t)N * Op::kOut), cudaGetErrorString(cudaGetLastError()));
+}
+
+int main(int argc, char** argv) {
+  const bool more = argc > 1 && !strcmp(argv[1], "more");
   const int64_t N = 262144;
   const size_t cap = 1ull << 30;
   double *x, *y, *lam, *scratch;
   int32_t* st;
   cudaMalloc(&x, sizeof(double) * N * 29 * 6);
   cudaMalloc(&y, sizeof(double) * N * 841 * 2);
-  cudaMalloc(&lam, sizeof(double) * N * 36);
+  cudaMalloc(&lam, sizeof(double) * 1048576 * 36);  // sweep 3 runs chain7 at 1M states
   cudaMalloc(&scratch, cap);
   cudaMalloc(&st, sizeof(int32_t) * N);
   k_fill<<<1184, 256>>>(x, N * 29 * 6, 7);
   float *xf = (float*)(x), *yf = (float*)y, *lf = (float*)lam, *sf = (float*)scratch;
   using namespace vdk;
+  if (more) {  // sweep 3: the remaining generated routines, loop vs per-state call
+    const int64_t N7 = 1048576;
+    gen<GenTree29::RneaBias, double, 0, 72, 3, kTrigCall, false, false>("t29 rneabias f64", N, x, y, st, scratch);
+    gen<GenTree29::RneaBias, double, 0, 72, 3, kTrigCall, false, true>("t29 rneabias f64", N, x, y, st, scratch);
+    gen<GenTree29::RneaGrav, double, 0, 55, 3, kTrigCall, false, false>("t29 rneagrav f64", N, x, y, st, scratch);
+    gen<GenTree29::RneaGrav, double, 0, 55, 3, kTrigCall, false, true>("t29 rneagrav f64", N, x, y, st, scratch);
+    gen<GenTree29::Rnea, double, 58, 55, 2, kTrigCall, false, false>("t29 rnea f64", N, x, y, st, scratch);
+    gen<GenTree29::Rnea, double, 58, 55, 2, kTrigCall, false, true>("t29 rnea f64", N, x, y, st, scratch);
+    gen<GenChain7::Rnea, double, GenChain7::Rnea::kSlots, 0, 4, kTrigFast, false, false>("c7 rnea f64 1M", N7, x, y, st, scratch);
+    gen<GenChain7::Rnea, double, GenChain7::Rnea::kSlots, 0, 4, kTrigFast, false, true>("c7 rnea f64 1M", N7, x, y, st, scratch);
+    jvp<GenChain7::AbaJvp, double, 40, 89, 2, kTrigLib, false>("c7 abajvp f64 1M", N7, x, y, scratch);
+    jvp<GenChain7::AbaJvp, double, 40, 89, 2, kTrigLib, true>("c7 abajvp f64 1M", N7, x, y, scratch);
+    jvp<GenChain7::RneaJvp, double, 40, 16, 2, kTrigLib, false>("c7 rneajvp f64 1M", N7, x, y, scratch);
+    jvp<GenChain7::RneaJvp, double, 40, 16, 2, kTrigLib, true>("c7 rneajvp f64 1M", N7, x, y, scratch);
+    jvp<GenChain7::CrbaJvp, double, 28, 0, 2, kTrigLib, false>("c7 crbajvp f64 1M", N7, x, y, scratch);
+    jvp<GenChain7::CrbaJvp, double, 28, 0, 2, kTrigLib, true>("c7 crbajvp f64 1M", N7, x, y, scratch);
+    jvp<GenChain7::FkJvp, double, 28, 0, 2, kTrigLib, false>("c7 fkjvp f64 1M", N7, x, y, scratch);
+    jvp<GenChain7::FkJvp, double, 28, 0, 2, kTrigLib, true>("c7 fkjvp f64 1M", N7, x, y, scratch);
+    osc<GenChain7::Osc6, double, 80, 67, 2, kTrigLib, false>("c7 osc6 f64 1M", N7, x, y, lam, st, scratch);
+    osc<GenChain7::Osc6, double, 80, 67, 2, kTrigLib, true>("c7 osc6 f64 1M", N7, x, y, lam, st, scratch);
+    k_fill<<<1184, 256>>>(xf, N * 29 * 6, 7);
+    jvp<GenChain7::AbaJvp, float, 0, 129, 2, kTrigLib, false>("c7 abajvp f32 1M", N7, xf, yf, sf);
+    jvp<GenChain7::AbaJvp, float, 0, 129, 2, kTrigLib, true>("c7 abajvp f32 1M", N7, xf, yf, sf);
+    gen<GenTree29::Rnea, float, 55, 0, 3, kTrigCall, false, false>("t29 rnea f32", N, xf, yf, st, sf);
+    gen<GenTree29::Rnea, float, 55, 0, 3, kTrigCall, false, true>("t29 rnea f32", N, xf, yf, st, sf);
+    osc<GenChain7::Osc6, float, 60, 87, 2, kTrigLib, false>("c7 osc6 f32 1M", N7, xf, yf, lf, st, sf);
+    osc<GenChain7::Osc6, float, 60, 87, 2, kTrigLib, true>("c7 osc6 f32 1M", N7, xf, yf, lf, st, sf);
+    return 0;
+  }
   // product placements (OscCfg default; JvpCfg); sweep 2: every G1 OSC frame
   // joint and the trig mode, the remaining JVPs
 #define OSC4(J)                                                                                              \
