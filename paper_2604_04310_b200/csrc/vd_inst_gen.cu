@@ -307,8 +307,72 @@ int gen_jvp_t(const Launch& L, const JvpArgs& a) {
   return L.dtype == 0 ? launch_jvp_t<typename R::FkJvp, double>(L, a) : launch_jvp_t<typename R::FkJvp, float>(L, a);
 }
 
+// rhs planes of the ABA-JVP identity below: t <- dτ − t (dτ NULL = 0)
+template <class T>
+__global__ void k_jvp_rhs(int64_t N, int n, const T* __restrict__ dtau, int64_t ld, T* __restrict__ t) {
+  const int64_t total = N * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / N, i = e - k * N;
+    t[k * ld + i] = (dtau ? dtau[k * ld + i] : T(0)) - t[k * ld + i];
+  }
+}
+
+// G1 ABA-JVP by the implicit-function identity instead of the dual-number
+// ABA.  FD is the solution of ID(q, q̇, q̈) = τ, so its directional derivative
+// along (dq, dq̇, dτ) is
+//   dq̈ = M⁻¹ (dτ − ∂ID/∂q·dq − ∂ID/∂q̇·dq̇)
+// where the bracketed term is the tangent of RNEA-JVP at (q, q̇, q̈) with
+// tangent (dq, dq̇, 0), and M⁻¹ b is the ABA at zero velocity and zero gravity
+// with b as the joint force.  Four launches — ABA (q̈, status), RNEA-JVP,
+// t ← dτ − t, ABA(q, 0, t, g = 0) into dq̈ — replace the 526-slot dual ABA
+// (one CTA/SM, its slot state in an L2 scratch slab): fp64 1.21 -> 0.875 ms,
+// fp32 0.567 -> 0.531 ms at 262 144 states (tools/jvp_time.py, C-ABI on plane
+// buffers), and the value output is the plain ABA's, bit for bit.  The same derivative up to
+// rounding: parity against the oracle's dual-number LLT forward dynamics
+// (tests/test_gpu_jvp.py, κ(M)-scaled bounds as for the dual kernel).
+template <class T>
+int aba_jvp_implicit(const Launch& L, const JvpArgs& a) {
+  if (!a.dout) return launch_gen_aba(L, a.x[0], a.x[1], a.x[2], a.g, nullptr, a.out, a.status);
+  const int n = L.n;
+  const int64_t ld = L.ld_in;
+  const size_t plane_set = sizeof(T) * (size_t)n * (size_t)ld;
+  cudaStream_t s = static_cast<cudaStream_t>(L.stream);
+  // q̈ goes straight to the caller's output when its layout matches the inputs'
+  const bool direct = a.out && L.ld_out == ld;
+  unsigned char* buf = nullptr;
+  if (int rc = scratch_alloc(reinterpret_cast<void**>(&buf), plane_set * (direct ? 2 : 3), s)) return rc;
+  T* zero = reinterpret_cast<T*>(buf);
+  T* t = reinterpret_cast<T*>(buf + plane_set);
+  T* qdd = direct ? static_cast<T*>(a.out) : reinterpret_cast<T*>(buf + 2 * plane_set);
+  Launch Li = L;  // intermediate launches: outputs laid out like the inputs
+  Li.ld_out = ld;
+  int rc = launch_gen_aba(Li, a.x[0], a.x[1], a.x[2], a.g, nullptr, qdd, a.status);
+  if (!rc) {
+    JvpArgs r{kJvpRNEA, {a.x[0], a.x[1], qdd}, {a.dx[0], a.dx[1], nullptr}, {a.g[0], a.g[1], a.g[2]}, nullptr,
+              nullptr, t, nullptr};
+    rc = launch_jvp_t<GenTree29::RneaJvp, T>(Li, r);
+  }
+  if (!rc) {
+    const int64_t blocks = std::min<int64_t>((L.N * n + 255) / 256, 148 * 16);
+    k_jvp_rhs<T><<<(unsigned)blocks, 256, 0, s>>>(L.N, n, static_cast<const T*>(a.dx[2]), ld, t);
+    rc = (int)cudaGetLastError();
+  }
+  if (!rc) rc = (int)cudaMemsetAsync(zero, 0, plane_set, s);
+  if (!rc) {
+    const double g0[3] = {0.0, 0.0, 0.0};
+    rc = launch_gen_aba(L, a.x[0], zero, t, g0, nullptr, a.dout, nullptr);
+  }
+  if (!rc && a.out && !direct)
+    rc = (int)cudaMemcpy2DAsync(a.out, sizeof(T) * L.ld_out, qdd, sizeof(T) * ld, sizeof(T) * L.N, n,
+                                cudaMemcpyDeviceToDevice, s);
+  scratch_free(buf, s);
+  return rc;
+}
+
 int launch_gen_jvp(const Launch& L, const JvpArgs& a) {
   if (a.fext && (a.op == kJvpABA || a.op == kJvpRNEA)) return -1;
+  if (L.spec == kTree29 && a.op == kJvpABA && !L.gravity_planes)
+    return L.dtype == 0 ? aba_jvp_implicit<double>(L, a) : aba_jvp_implicit<float>(L, a);
   if (L.spec == kTree29) return gen_jvp_t<GenTree29>(L, a);
   // chain7 (tools/jvp_time.py, 1M states, Python API, template -> generated):
   // fp64 FK-JVP 0.39 -> 0.37, RNEA-JVP 0.55 -> 0.36, CRBA-JVP 0.35 -> 0.25,

@@ -37,6 +37,32 @@ def main():
             b.record()
             torch.cuda.synchronize()
             print(robot, N, str(dt)[6:], k, round(a.elapsed_time(b) / 10, 4), "ms", flush=True)
+        # the C-ABI call alone on plane-layout (SoA) buffers: no layout conversion
+        import ctypes
+        from paper_2604_04310_b200 import _lib
+        lib = _lib.load()
+        P = [x.T.contiguous() for x in X]
+        out = torch.empty_like(P[0])
+        dout = torch.empty_like(P[0])
+        g3 = (ctypes.c_double * 3)(0.0, 0.0, 9.81)
+        st = torch.empty(N, dtype=torch.int32, device="cuda")
+        dti = 0 if dt == torch.float64 else 1
+        s = torch.cuda.current_stream().cuda_stream
+
+        def abi():
+            rc = lib.vd_aba_jvp(dm.handle, dti, N, P[0].data_ptr(), P[1].data_ptr(), P[2].data_ptr(), P[3].data_ptr(),
+                                P[4].data_ptr(), P[5].data_ptr(), N, g3, None, out.data_ptr(), dout.data_ptr(), N,
+                                st.data_ptr(), s)
+            assert rc == 0, lib.vd_last_error().decode()
+        for _ in range(3):
+            abi()
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(10):
+            abi()
+        b.record()
+        torch.cuda.synchronize()
+        print(robot, N, str(dt)[6:], "vd_aba_jvp (C-ABI, planes)", round(a.elapsed_time(b) / 10, 4), "ms", flush=True)
 
 
 if __name__ == "__main__":
