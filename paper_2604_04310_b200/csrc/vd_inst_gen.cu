@@ -156,7 +156,8 @@ struct JvpCfg {
   static constexpr int kFast = kTrigLib;
 };
 
-// G1 ABA-JVP (526 slots): one CTA/SM with 220 shared slots keeps the scratch
+// G1 ABA-JVP (526 slots; measured as the dual routine, now replaced by
+// aba_jvp_implicit below): one CTA/SM with 220 shared slots keeps the scratch
 // slab in L2 (async_sweep "jvp", 262144 states: fp64 r40 s110 b2 1.50 ->
 // r40 s220 b1 1.24 ms; fp32 s220 b2 0.72 -> r40 s220 b2 0.64 ms); G1 fp32
 // RNEA-JVP s220 b2 0.27 -> s144 b3 0.25 ms.
@@ -296,8 +297,12 @@ int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShar
 
 template <class R>
 int gen_jvp_t(const Launch& L, const JvpArgs& a) {
-  if (a.op == kJvpABA)
-    return L.dtype == 0 ? launch_jvp_t<typename R::AbaJvp, double>(L, a) : launch_jvp_t<typename R::AbaJvp, float>(L, a);
+  // (the G1 ABA-JVP takes the implicit-function form below, never the dual routine)
+  if constexpr (!std::is_same_v<R, GenTree29>) {
+    if (a.op == kJvpABA)
+      return L.dtype == 0 ? launch_jvp_t<typename R::AbaJvp, double>(L, a)
+                          : launch_jvp_t<typename R::AbaJvp, float>(L, a);
+  }
   if (a.op == kJvpRNEA)
     return L.dtype == 0 ? launch_jvp_t<typename R::RneaJvp, double>(L, a)
                         : launch_jvp_t<typename R::RneaJvp, float>(L, a);
@@ -371,7 +376,7 @@ int aba_jvp_implicit(const Launch& L, const JvpArgs& a) {
 
 int launch_gen_jvp(const Launch& L, const JvpArgs& a) {
   if (a.fext && (a.op == kJvpABA || a.op == kJvpRNEA)) return -1;
-  if (L.spec == kTree29 && a.op == kJvpABA && !L.gravity_planes)
+  if (L.spec == kTree29 && a.op == kJvpABA)
     return L.dtype == 0 ? aba_jvp_implicit<double>(L, a) : aba_jvp_implicit<float>(L, a);
   if (L.spec == kTree29) return gen_jvp_t<GenTree29>(L, a);
   // chain7 (tools/jvp_time.py, 1M states, Python API, template -> generated):
