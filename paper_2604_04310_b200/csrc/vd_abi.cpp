@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -72,6 +73,9 @@ int set_error(int code, const std::string& msg, int line = 0, int col = 0) {
 }
 int from_failure(const vdh::Failure& f) { return set_error(f.code, f.what(), f.line, f.column); }
 int cuda_fail(cudaError_t e, const char* where) {
+  // Consume the thread's last-error state: a failed API call (not a sticky
+  // context error) must not resurface as the result of the next launch check.
+  cudaGetLastError();
   return set_error(VD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 void copy_str(const std::string& s, char* buf, size_t len) {
@@ -779,6 +783,11 @@ struct HostOp {
   int out_width;
 };
 
+// Chunks in flight per device: each slot owns a stream, device buffers and an
+// event, and a slot is reused only once its previous chunk's D2H has landed.
+// (3 or 4 slots measured the same as 2: tools/e2e_chunk.py.)
+constexpr int kPipeSlots = 2;
+
 struct DevCtx {
   std::mutex mu;
   int device = -1;
@@ -786,18 +795,19 @@ struct DevCtx {
   uint64_t fp = 0;
   int n = -1;
   const void* jit_id = nullptr;  // the model's JIT module the cached device model was created with
-  cudaStream_t st[2] = {nullptr, nullptr};
-  cudaEvent_t done[2] = {nullptr, nullptr};
-  double* din[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-  double* dout[2] = {nullptr, nullptr};
-  int32_t* dst[2] = {nullptr, nullptr};
-  double* pin_in[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};  // staging (pageable inputs)
-  double* pin_out[2] = {nullptr, nullptr};
-  int32_t* pin_st[2] = {nullptr, nullptr};
+  cudaStream_t st[kPipeSlots] = {};
+  cudaEvent_t done[kPipeSlots] = {};
+  double* din[kPipeSlots][3] = {};
+  double* dout[kPipeSlots] = {};
+  int32_t* dst[kPipeSlots] = {};
+  double* pin_in[kPipeSlots][3] = {};  // staging (pageable inputs)
+  double* pin_out[kPipeSlots] = {};
+  int32_t* pin_st[kPipeSlots] = {};
   int64_t cap = 0;      // states per chunk buffer
   int64_t cap_in = 0;   // doubles per input chunk buffer
   int64_t cap_out = 0;  // doubles per output chunk buffer
-  int64_t cap_pin = 0;
+  int64_t cap_pin = 0;     // doubles per pinned staging buffer
+  int64_t cap_pin_st = 0;  // states per pinned status buffer
 };
 
 DevCtx& ctx_for(int device) {
@@ -838,7 +848,7 @@ int prepare_ctx(DevCtx& c, vd_model m, int n, int64_t chunk, int width, bool sta
     c.jit_id = jit_id;
   }
   if (!c.st[0]) {
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kPipeSlots; ++k) {
       if ((e = cudaStreamCreateWithFlags(&c.st[k], cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
       if ((e = cudaEventCreateWithFlags(&c.done[k], cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
     }
@@ -847,13 +857,13 @@ int prepare_ctx(DevCtx& c, vd_model m, int n, int64_t chunk, int width, bool sta
   if (chunk * n > c.cap_in || need_out > c.cap_out || c.cap < chunk) {
     // Release everything and zero the capacities first: a failed cudaMalloc
     // below must leave the context empty, never holding freed pointers.
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kPipeSlots; ++b) {
       for (int k = 0; k < 3; ++k) cudaFree(std::exchange(c.din[b][k], nullptr));
       cudaFree(std::exchange(c.dout[b], nullptr));
       cudaFree(std::exchange(c.dst[b], nullptr));
     }
     c.cap = c.cap_in = c.cap_out = 0;
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kPipeSlots; ++b) {
       for (int k = 0; k < 3; ++k)
         if ((e = cudaMalloc(&c.din[b][k], sizeof(double) * n * chunk)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
       if ((e = cudaMalloc(&c.dout[b], sizeof(double) * need_out)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
@@ -863,14 +873,16 @@ int prepare_ctx(DevCtx& c, vd_model m, int n, int64_t chunk, int width, bool sta
     c.cap_in = chunk * n;
     c.cap_out = need_out;
   }
-  if (staging && c.cap_pin < chunk * std::max(n, width)) {
-    for (int b = 0; b < 2; ++b) {
+  // (the status buffers are sized by states, the value buffers by planes: a
+  // wide-output call with small chunks must not leave a short status buffer)
+  if (staging && (c.cap_pin < chunk * std::max(n, width) || c.cap_pin_st < chunk)) {
+    for (int b = 0; b < kPipeSlots; ++b) {
       for (int k = 0; k < 3; ++k) cudaFreeHost(std::exchange(c.pin_in[b][k], nullptr));
       cudaFreeHost(std::exchange(c.pin_out[b], nullptr));
       cudaFreeHost(std::exchange(c.pin_st[b], nullptr));
     }
-    c.cap_pin = 0;
-    for (int b = 0; b < 2; ++b) {
+    c.cap_pin = c.cap_pin_st = 0;
+    for (int b = 0; b < kPipeSlots; ++b) {
       const int64_t cnt = chunk * std::max(n, width);
       for (int k = 0; k < 3; ++k)
         if ((e = cudaMallocHost(&c.pin_in[b][k], sizeof(double) * cnt)) != cudaSuccess) return cuda_fail(e, "pinned");
@@ -878,9 +890,17 @@ int prepare_ctx(DevCtx& c, vd_model m, int n, int64_t chunk, int width, bool sta
       if ((e = cudaMallocHost(&c.pin_st[b], sizeof(int32_t) * chunk)) != cudaSuccess) return cuda_fail(e, "pinned");
     }
     c.cap_pin = chunk * std::max(n, width);
+    c.cap_pin_st = chunk;
   }
   return VD_OK;
 }
+
+// Bytes of input + output per pipeline chunk (internal knob for
+// tools/e2e_chunk.py; vdi_set_host_chunk_bytes).
+// 96 MB: Panda 4M states 14.7 ms at 48 MB, 14.4 ms at 96 MB, 14.6 at 192 MB
+// (pinned buffers; the same box copies the bytes in 13.2 ms).
+constexpr int64_t kChunkBytesDefault = 96ll << 20;
+std::atomic<int64_t> g_chunk_bytes{kChunkBytesDefault};
 
 // Stream one device's shard [b, e) through the double-buffered pipeline.
 int run_shard(DevCtx& c, vd_model m, const HostOp& op, int64_t N, int64_t b, int64_t e, const double* const* inputs,
@@ -888,20 +908,33 @@ int run_shard(DevCtx& c, vd_model m, const HostOp& op, int64_t N, int64_t b, int
   const int n = m->m.dof();
   const int width = op.out_width;
   const int64_t len = e - b;
-  int64_t chunk = std::min<int64_t>(len, std::max<int64_t>(65536, (int64_t)(48ll << 20) / (8ll * (n * op.n_in + width))));
+  int64_t chunk = std::min<int64_t>(len, std::max<int64_t>(65536, g_chunk_bytes.load() / (8ll * (n * op.n_in + width))));
   chunk = (chunk + 127) / 128 * 128;  // device leading dimension: a multiple of the kernels' tile
   bool pinned = is_pinned(out);
   for (int k = 0; k < op.n_in; ++k) pinned = pinned && is_pinned(inputs[k]);
   const bool st_direct = pinned && status && is_pinned(status);
   if (int rc = prepare_ctx(c, m, n, chunk, width, !pinned || (op.kind == 2 && !st_direct))) return rc;
-  const int64_t nchunks = (len + chunk - 1) / chunk;
+  // Chunk plan: full chunks, then a geometric taper (halving down to 16 K
+  // states) over the last two chunks' worth, so the kernel + D2H that drain
+  // after the last H2D move a small chunk, not a full one.
+  std::vector<std::pair<int64_t, int64_t>> plan;
+  for (int64_t lo = b; lo < e;) {
+    const int64_t rem = e - lo;
+    int64_t cl = chunk;
+    if (rem <= 2 * chunk) cl = std::max<int64_t>(16384, ((rem + 1) / 2 + 127) / 128 * 128);
+    cl = std::min(cl, rem);
+    plan.emplace_back(lo, cl);
+    lo += cl;
+  }
+  const int64_t nchunks = (int64_t)plan.size();
   std::vector<int32_t> st_host;
   int32_t* st_dst = status;
   if (op.kind == 2 && !status) {
     st_host.resize((size_t)len);
     st_dst = st_host.data() - b;  // indexed with the global row below
   }
-  std::vector<int64_t> pending_lo(2, -1), pending_len(2, 0);
+  const int nslots = kPipeSlots;
+  std::vector<int64_t> pending_lo(kPipeSlots, -1), pending_len(kPipeSlots, 0);
   auto finish_slot = [&](int slot) -> int {
     if (pending_lo[(size_t)slot] < 0) return VD_OK;
     cudaError_t ce = cudaEventSynchronize(c.done[slot]);
@@ -919,9 +952,9 @@ int run_shard(DevCtx& c, vd_model m, const HostOp& op, int64_t N, int64_t b, int
     return VD_OK;
   };
   for (int64_t k = 0; k < nchunks; ++k) {
-    const int slot = (int)(k & 1);
+    const int slot = (int)(k % nslots);
     if (int rc = finish_slot(slot)) return rc;
-    const int64_t lo = b + k * chunk, cl = std::min<int64_t>(chunk, e - lo);
+    const int64_t lo = plan[(size_t)k].first, cl = plan[(size_t)k].second;
     cudaStream_t s = c.st[slot];
     cudaError_t ce = cudaSuccess;
     for (int i = 0; i < op.n_in && ce == cudaSuccess; ++i) {
@@ -959,8 +992,9 @@ int run_shard(DevCtx& c, vd_model m, const HostOp& op, int64_t N, int64_t b, int
     pending_lo[(size_t)slot] = lo;
     pending_len[(size_t)slot] = cl;
   }
-  for (int slot = 0; slot < 2; ++slot)
-    if (int rc = finish_slot(slot)) return rc;
+  // drain in issue order
+  for (int64_t k = std::max<int64_t>(0, nchunks - nslots); k < nchunks; ++k)
+    if (int rc = finish_slot((int)(k % nslots))) return rc;
   return VD_OK;
 }
 
@@ -1032,5 +1066,9 @@ int vd_batch_forward_dynamics_host(vd_model m, int64_t N, const double* q, const
   const double* in[3] = {q, qd, tau};
   return host_batch(m, HostOp{2, 3, m ? m->m.dof() : 0}, N, in, g3, qdd, status, devices, n_devices);
 }
+
+// ---- internal (not in the public header): host-pipeline chunk size (bytes
+// of inputs + outputs per chunk; <= 0 restores the default)
+void vdi_set_host_chunk_bytes(int64_t bytes) { g_chunk_bytes.store(bytes > 0 ? bytes : kChunkBytesDefault); }
 
 }  // extern "C"

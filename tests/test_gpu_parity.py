@@ -501,6 +501,40 @@ def test_host_batch_api(vd, cuda, omodels):
     assert rel_err(got, qdd, axis=1)[cosb > 0.05].max() <= 1e-8
 
 
+def test_host_batch_chunk_plan(vd, cuda, omodels):
+    """The host pipeline streams full chunks, then halving chunks over the last
+    two chunks' worth (vd_abi.cpp run_shard): with the chunk knob at its
+    65 536-state floor, 300 000 Panda states run as 3 full, 4 tapered and one
+    remainder chunk, bitwise equal to one device call (pageable numpy buffers
+    through the staging path, and pinned torch buffers direct)."""
+    import ctypes
+    lib = vd._lib.load()
+    lib.vdi_set_host_chunk_bytes.argtypes = [ctypes.c_int64]
+    lib.vdi_set_host_chunk_bytes.restype = None
+    om = omodels["chain7"]
+    m, dm = _dm(vd, "chain7")
+    N = 300000
+    b = vd.random_states(m, N, 77, False, True)
+    dev = vd.forward_dynamics(dm, _t(b.q), _t(b.qd), _t(b.tau)).cpu().numpy()
+    lib.vdi_set_host_chunk_bytes(1)
+    try:
+        got = vd.batch_forward_dynamics(m, b)
+        assert np.array_equal(got, dev)
+        hq, hqd, htau = (torch.as_tensor(np.ascontiguousarray(a.T)).pin_memory() for a in (b.q, b.qd, b.tau))
+        hout = torch.empty_like(hq).pin_memory()
+        hst = torch.full((N,), -1, dtype=torch.int32).pin_memory()
+        devs = (ctypes.c_int * 1)(0)
+        rc = lib.vd_batch_forward_dynamics_host(m.handle, N, hq.data_ptr(), hqd.data_ptr(), htau.data_ptr(), None,
+                                                hout.data_ptr(), hst.data_ptr(), devs, 1)
+        assert rc == 0, lib.vd_last_error().decode()
+        assert np.array_equal(hout.numpy().T, dev) and int(hst.abs().max()) == 0
+    finally:
+        lib.vdi_set_host_chunk_bytes(0)
+    idx = np.arange(0, N, 997)
+    ref, _ = om.forward_dynamics(b.q[idx], b.qd[idx], b.tau[idx])
+    assert rel_err(dev[idx], ref, axis=1).max() <= TOL64
+
+
 def test_batch_eval(vd, cuda, omodels):
     """batch_eval (batch.hpp:76-126): fn runs once per contiguous shard on its
     device; the concatenation is bitwise identical for any partition (here 1
