@@ -58,6 +58,7 @@ enum : int {
   kTrigLib = 0,   // the library sincos / sincosf, inlined at every joint
   kTrigFast = 1,  // vd_sincos_f64 / vd_sincos_f32 (vd_sincos.cuh), inlined
   kTrigCall = 2,  // the library routine, one out-of-line copy per kernel
+  kTrigFastCall = 3,  // vd_sincos_f64 / vd_sincos_f32, one out-of-line copy per kernel
 };
 
 #if defined(__CUDA_ARCH__)
@@ -81,6 +82,19 @@ static __device__ __noinline__ float2 vd_sincos_call(float x) {
   sincosf(x, &r.x, &r.y);
   return r;
 }
+// kTrigFastCall: the Cody-Waite / fdlibm routine out of line, so its
+// __constant__ coefficients are read inside the called function (constant-bank
+// operands) and cannot be hoisted out of a persistent loop
+static __device__ __noinline__ double2 vd_sincos_fast_call(double x) {
+  double2 r;
+  vd_sincos_f64(x, &r.x, &r.y);
+  return r;
+}
+static __device__ __noinline__ float2 vd_sincos_fast_call(float x) {
+  float2 r;
+  vd_sincos_f32(x, &r.x, &r.y);
+  return r;
+}
 template <class T> __device__ __forceinline__ bool vd_isfinite(T x) { return isfinite(x); }
 #else
 template <class T> inline void vd_sincos(T x, T* s, T* c) { *s = std::sin(x); *c = std::cos(x); }
@@ -96,6 +110,12 @@ VD_HD void vd_sincos_cx(T x, T* s, T* c) {
   if constexpr (int(Cx::kFastTrig) == kTrigFast && sizeof(T) == 4) { vd_sincos_f32(x, s, c); return; }
   if constexpr (int(Cx::kFastTrig) == kTrigCall) {
     const auto r = vd_sincos_call(x);
+    *s = r.x;
+    *c = r.y;
+    return;
+  }
+  if constexpr (int(Cx::kFastTrig) == kTrigFastCall) {
+    const auto r = vd_sincos_fast_call(x);
     *s = r.x;
     *c = r.y;
     return;

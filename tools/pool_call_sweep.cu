@@ -133,6 +133,33 @@ int main(int argc, char** argv) {
   k_fill<<<1184, 256>>>(x, N * 29 * 6, 7);
   float *xf = (float*)(x), *yf = (float*)y, *lf = (float*)lam, *sf = (float*)scratch;
   using namespace vdk;
+  if (argc > 1 && !strcmp(argv[1], "trig")) {  // sweep 4: library sincos vs vd_sincos, both out of line
+    gen<GenTree29::Aba, double, 40, 113, 2, kTrigCall, true, true>("t29 aba f64 libcall", N, x, y, st, scratch);
+    gen<GenTree29::Aba, double, 40, 113, 2, kTrigFastCall, true, true>("t29 aba f64 fastcall", N, x, y, st, scratch);
+    gen<GenTree29::Rnea, double, 58, 55, 2, kTrigCall, false, false>("t29 rnea f64 libcall", N, x, y, st, scratch);
+    gen<GenTree29::Rnea, double, 58, 55, 2, kTrigFastCall, false, false>("t29 rnea f64 fastcall", N, x, y, st, scratch);
+    gen<GenTree29::RneaBias, double, 0, 72, 3, kTrigCall, false, false>("t29 rneabias f64 libcall", N, x, y, st, scratch);
+    gen<GenTree29::RneaBias, double, 0, 72, 3, kTrigFastCall, false, false>("t29 rneabias f64 fastcall", N, x, y, st, scratch);
+    gen<GenTree29::Crba, double, 0, 55, 3, kTrigLib, true, false>("t29 crba f64 lib", N, x, y, st, scratch);
+    gen<GenTree29::Crba, double, 0, 55, 3, kTrigFastCall, true, false>("t29 crba f64 fastcall", N, x, y, st, scratch);
+    gen<GenTree29::Fk, double, 0, 55, 3, kTrigLib, false, false>("t29 fk f64 lib", N, x, y, st, scratch);
+    gen<GenTree29::Fk, double, 0, 55, 3, kTrigFastCall, false, false>("t29 fk f64 fastcall", N, x, y, st, scratch);
+    osc<GenTree29::Osc23, double, 40, 110, 2, kTrigCall, false>("t29 osc23 f64 libcall", N, x, y, lam, st, scratch);
+    osc<GenTree29::Osc23, double, 40, 110, 2, kTrigFastCall, false>("t29 osc23 f64 fastcall", N, x, y, lam, st, scratch);
+    jvp<GenTree29::RneaJvp, double, 40, 110, 2, kTrigCall, true>("t29 rneajvp f64 libcall", N, x, y, scratch);
+    jvp<GenTree29::RneaJvp, double, 40, 110, 2, kTrigFastCall, true>("t29 rneajvp f64 fastcall", N, x, y, scratch);
+    const int64_t N7 = 1048576;
+    gen<GenChain7::Rnea, double, GenChain7::Rnea::kSlots, 0, 4, kTrigFast, false, false>("c7 rnea f64 1M fast", N7, x, y, st, scratch);
+    gen<GenChain7::Rnea, double, GenChain7::Rnea::kSlots, 0, 4, kTrigFastCall, false, false>("c7 rnea f64 1M fastcall", N7, x, y, st, scratch);
+    k_fill<<<1184, 256>>>(xf, N * 29 * 6, 7);
+    gen<GenTree29::AbaMixed, float, 40, 122, 3, kTrigCall, true, false>("t29 abamixed f32 libcall", N, xf, yf, st, sf);
+    gen<GenTree29::AbaMixed, float, 40, 122, 3, kTrigFastCall, true, false>("t29 abamixed f32 fastcall", N, xf, yf, st, sf);
+    gen<GenTree29::Rnea, float, 55, 0, 3, kTrigCall, false, false>("t29 rnea f32 libcall", N, xf, yf, st, sf);
+    gen<GenTree29::Rnea, float, 55, 0, 3, kTrigFastCall, false, false>("t29 rnea f32 fastcall", N, xf, yf, st, sf);
+    osc<GenTree29::Osc23, float, 40, 144, 3, kTrigCall, false>("t29 osc23 f32 libcall", N, xf, yf, lf, st, sf);
+    osc<GenTree29::Osc23, float, 40, 144, 3, kTrigFastCall, false>("t29 osc23 f32 fastcall", N, xf, yf, lf, st, sf);
+    return 0;
+  }
   if (more) {  // sweep 3: the remaining generated routines, loop vs per-state call
     const int64_t N7 = 1048576;
     gen<GenTree29::RneaBias, double, 0, 72, 3, kTrigCall, false, false>("t29 rneabias f64", N, x, y, st, scratch);
