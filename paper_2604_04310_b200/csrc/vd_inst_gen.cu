@@ -91,10 +91,13 @@ struct Cfg<GenTree29::Crba, float> {
 // registers at 3 CTAs/SM 0.112 ms (vs 0.133 with the dense routine's
 // placement); fp32 in shared memory at 6 CTAs/SM 0.061 ms; chain7 fp64 all in
 // registers 0.21 ms at 4M states (85 % of HBM)
+// fp64 with the out-of-line sin/cos and evict-first output
+// (tools/pool_call_sweep.cu crbap): 0.114 -> 0.104 ms
 template <>
 struct Cfg<GenTree29::CrbaPacked, double> {
   static constexpr int kReg = GenTree29::CrbaPacked::kSlots, kSmem = 0, kMinB = 3;
-  static constexpr int kFast = kTrigLib;
+  static constexpr int kFast = kTrigCall;
+  static constexpr bool kStream = true;
 };
 template <>
 struct Cfg<GenTree29::CrbaPacked, float> {

@@ -160,6 +160,39 @@ int main(int argc, char** argv) {
     osc<GenTree29::Osc23, float, 40, 144, 3, kTrigFastCall, false>("t29 osc23 f32 fastcall", N, xf, yf, lf, st, sf);
     return 0;
   }
+  if (argc > 1 && !strcmp(argv[1], "crbap")) {  // sweep 5: G1 packed CRBA placement / evict-first output
+    constexpr int S = GenTree29::CrbaPacked::kSlots;
+    gen<GenTree29::CrbaPacked, double, S, 0, 3, kTrigLib, false, false>("t29 crbap f64 r55 b3", N, x, y, st, scratch);
+    gen<GenTree29::CrbaPacked, double, S, 0, 3, kTrigLib, true, false>("t29 crbap f64 r55 b3 cs", N, x, y, st, scratch);
+    gen<GenTree29::CrbaPacked, double, S, 0, 4, kTrigLib, true, false>("t29 crbap f64 r55 b4 cs", N, x, y, st, scratch);
+    gen<GenTree29::CrbaPacked, double, 0, S, 4, kTrigLib, true, false>("t29 crbap f64 s55 b4 cs", N, x, y, st, scratch);
+    gen<GenTree29::CrbaPacked, double, 0, S, 5, kTrigLib, true, false>("t29 crbap f64 s55 b5 cs", N, x, y, st, scratch);
+    gen<GenTree29::CrbaPacked, double, S, 0, 3, kTrigCall, true, false>("t29 crbap f64 r55 b3 cs trig", N, x, y, st, scratch);
+    gen<GenTree29::Crba, double, 0, 55, 3, kTrigLib, true, false>("t29 crba f64 s55 b3 cs", N, x, y, st, scratch);
+    k_fill<<<1184, 256>>>(xf, N * 29 * 6, 7);
+    gen<GenTree29::CrbaPacked, float, 0, S, 6, kTrigLib, false, false>("t29 crbap f32 s55 b6", N, xf, yf, st, sf);
+    gen<GenTree29::CrbaPacked, float, 0, S, 6, kTrigLib, true, false>("t29 crbap f32 s55 b6 cs", N, xf, yf, st, sf);
+    return 0;
+  }
+  if (argc > 1 && !strcmp(argv[1], "fk")) {  // sweep 6: out-of-line sin/cos / evict-first for FK, gravity, CRBA
+    gen<GenTree29::Fk, double, 0, 55, 3, kTrigLib, false, false>("t29 fk f64 lib", N, x, y, st, scratch);
+    gen<GenTree29::Fk, double, 0, 55, 3, kTrigCall, false, false>("t29 fk f64 trig", N, x, y, st, scratch);
+    gen<GenTree29::Fk, double, 0, 55, 3, kTrigLib, true, false>("t29 fk f64 lib cs", N, x, y, st, scratch);
+    gen<GenTree29::Fk, double, 0, 55, 3, kTrigCall, true, false>("t29 fk f64 trig cs", N, x, y, st, scratch);
+    gen<GenTree29::RneaGrav, double, 0, 55, 3, kTrigLib, false, false>("t29 grav f64 lib", N, x, y, st, scratch);
+    gen<GenTree29::RneaGrav, double, 0, 55, 3, kTrigCall, false, false>("t29 grav f64 trig", N, x, y, st, scratch);
+    gen<GenTree29::Crba, double, 0, 55, 3, kTrigLib, true, false>("t29 crba f64 lib cs", N, x, y, st, scratch);
+    gen<GenTree29::Crba, double, 0, 55, 3, kTrigCall, true, false>("t29 crba f64 trig cs", N, x, y, st, scratch);
+    k_fill<<<1184, 256>>>(xf, N * 29 * 6, 7);
+    constexpr int S = GenTree29::CrbaPacked::kSlots;
+    gen<GenTree29::CrbaPacked, float, 0, S, 6, kTrigLib, false, false>("t29 crbap f32 lib", N, xf, yf, st, sf);
+    gen<GenTree29::CrbaPacked, float, 0, S, 6, kTrigCall, false, false>("t29 crbap f32 trig", N, xf, yf, st, sf);
+    gen<GenTree29::Fk, float, 0, 55, 4, kTrigLib, false, false>("t29 fk f32 lib", N, xf, yf, st, sf);
+    gen<GenTree29::Fk, float, 0, 55, 4, kTrigCall, false, false>("t29 fk f32 trig", N, xf, yf, st, sf);
+    gen<GenTree29::Crba, float, 0, 55, 4, kTrigLib, true, false>("t29 crba f32 lib cs", N, xf, yf, st, sf);
+    gen<GenTree29::Crba, float, 0, 55, 4, kTrigCall, true, false>("t29 crba f32 trig cs", N, xf, yf, st, sf);
+    return 0;
+  }
   if (more) {  // sweep 3: the remaining generated routines, loop vs per-state call
     const int64_t N7 = 1048576;
     gen<GenTree29::RneaBias, double, 0, 72, 3, kTrigCall, false, false>("t29 rneabias f64", N, x, y, st, scratch);
