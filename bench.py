@@ -492,8 +492,8 @@ def run_configs(vd, lib, dev, stream, sptr, args, rank, world):
         pose = torch.empty((12, N), dtype=dt, device=dev)
         J = torch.empty((42, N), dtype=dt, device=dev)
         fid = chain.frame_index("ee")
-        fn_s = lambda sp: lib.vd_jacobian(dc.handle, code, N, q.data_ptr(), N, fid, pose.data_ptr(),  # noqa
-                                          J.data_ptr(), N, sp)
+        pq, pp, pj = q.data_ptr(), pose.data_ptr(), J.data_ptr()
+        fn_s = lambda sp: lib.vd_jacobian(dc.handle, code, N, pq, N, fid, pp, pj, N, sp)  # noqa
         key = f"2_panda_fk_jacobian_b4096_{'f64' if code == 0 else 'f32'}"
         rec(key, N, event_time(lambda: fn_s(sptr), 200, 20, stream), flops_per_eval("chain7", "fk"))
         gms = graph_time(fn_s, 400, 20)
@@ -507,10 +507,17 @@ def run_configs(vd, lib, dev, stream, sptr, args, rank, world):
         M = torch.empty((49, N), dtype=dt, device=dev)
         b = torch.empty((7, N), dtype=dt, device=dev)
         a = torch.empty((7, N), dtype=dt, device=dev)
-        fn = lambda: lib.vd_dynamics(dc.handle, code, N, q.data_ptr(), qd.data_ptr(), tau.data_ptr(), N, None,  # noqa
-                                     M.data_ptr(), b.data_ptr(), a.data_ptr(), N, None, sptr)
+        ptrs = [t.data_ptr() for t in (q, qd, tau, M, b, a)]  # resolved once, as a C caller holds them
+        fn_s = lambda sp: lib.vd_dynamics(dc.handle, code, N, ptrs[0], ptrs[1], ptrs[2], N, None,  # noqa
+                                          ptrs[3], ptrs[4], ptrs[5], N, None, sp)
         fl = flops_per_eval("chain7", "crba") + flops_per_eval("chain7", "rnea") + flops_per_eval("chain7", "aba")
-        rec(f"3_panda_M_bias_aba_b65536_{'f64' if code == 0 else 'f32'}", N, event_time(fn, 50, warm, stream), fl)
+        key = f"3_panda_M_bias_aba_b65536_{'f64' if code == 0 else 'f32'}"
+        rec(key, N, event_time(lambda: fn_s(sptr), 50, warm, stream), fl)
+        gms = graph_time(fn_s, 200, 20)
+        if gms:  # ~20 us per call: the one-call-per-step loop can be host-bound here
+            out[key].update({"ms_graph": round(gms, 5), "evals_per_s_graph": N / (gms * 1e-3),
+                             "algorithmic_tflops_graph": round(fl * N / (gms * 1e-3) / 1e12, 4),
+                             "note": "ms: one host call per step; ms_graph: CUDA-graph replay of the same calls"})
     # config 4: G1 RNEA + ABA, batch 262144 (fp64 and fp32)
     for dt, code in ((torch.float64, 0), (torch.float32, 1)):
         N = 262144

@@ -655,8 +655,11 @@ class Algo:
         return Joint(self.g, self.rb, i, cs=(self.load(m[1]), self.load(m[2])))
 
     def gravity(self):
-        self.g.raw(f"const {self.g.ty} ga0 = cx.g(0), ga1 = cx.g(1), ga2 = cx.g(2);")
-        return [ZERO, ZERO, ZERO, Ex(s="ga0"), Ex(s="ga1"), Ex(s="ga2")]
+        # emitted once per routine (a fused routine runs several recursions)
+        if getattr(self, "_gvec", None) is None:
+            self.g.raw(f"const {self.g.ty} ga0 = cx.g(0), ga1 = cx.g(1), ga2 = cx.g(2);")
+            self._gvec = [ZERO, ZERO, ZERO, Ex(s="ga0"), Ex(s="ga1"), Ex(s="ga2")]
+        return self._gvec
 
     def finish(self):
         for gi in sorted(self.g.groups_read):
@@ -695,7 +698,7 @@ def fext_body(g, W, i):
     return g.matTvec(R, g.vsub(fw[:3], g.cross3(p, fw[3:]))) + g.matTvec(R, fw[3:])
 
 
-def gen_aba(rb, hp=(), tau_prologue=False, dual=False, fext=False):
+def gen_aba(rb, hp=(), tau_prologue=False, dual=False, fext=False, A0=None, og=0):
     """ABA (Featherstone RBDA Table 7.1; oracle forward_dynamics,
     dynamics.hpp:421-444).  x(0) = q, x(1) = q̇, x(2) = τ; y(0, i) = q̈_i.
 
@@ -714,7 +717,7 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False, fext=False):
     # tau_prologue: τ loaded with q, q̇ up front into slots (faster for the
     # fp32 routine; for fp64 those 29 slots displace pass-2 state from shared
     # memory and it measured slower, so τ is read at each joint's pass-2 step)
-    A = Algo(rb, True, hp, extra=(2,) if tau_prologue else (), dual=dual)
+    A = A0 or Algo(rb, True, hp, extra=(2,) if tau_prologue else (), dual=dual)
     g = A.g
     layout = {}
 
@@ -783,7 +786,7 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False, fext=False):
             v = g.vadd(X.motion_to_child(vp), X.S(qdi))
             a1 = g.vadd(X.motion_to_child(ap), g.crm(v, X.S(qdi)))
         qdd = g.sub(A.load(udr), g.sdot([A.load(r) for r in Udr], a1))
-        g.output(0, i, qdd)
+        g.output(og, i, qdd)
         g.check_finite(qdd)
         if rb.children[i]:
             a = g.vadd(a1, X.S(qdd))
@@ -792,6 +795,20 @@ def gen_aba(rb, hp=(), tau_prologue=False, dual=False, fext=False):
 
     for r in rb.roots:
         down(r, None, None)
+    return A.finish() if A0 is None else A
+
+
+def gen_dyn(rb):
+    """The fused forward-dynamics call (vd_dynamics; oracle crba +
+    rnea(q, q̇, 0) + forward_dynamics, dynamics.hpp:330-444) as one routine:
+    y(0, c·n + r) = M(r, c) (dense, as gen_crba), y(1, i) = bias c + g (as
+    gen_rnea with q̈ = 0), y(2, i) = q̈ (as gen_aba).  The three recursions
+    share one prologue (every joint's sin/cos and q̇ parked once) and one
+    gravity read; x(2) = τ is read in the ABA's pass 2."""
+    A = Algo(rb, True)
+    gen_crba(rb, A0=A, og=0)
+    gen_rnea(rb, True, False, A0=A, og=1)
+    gen_aba(rb, A0=A, og=2)
     return A.finish()
 
 
@@ -917,7 +934,7 @@ def gen_aba_role(rb, r):
     return A.finish()
 
 
-def gen_rnea(rb, with_qd, with_qdd, dual=False, fext=False):
+def gen_rnea(rb, with_qd, with_qdd, dual=False, fext=False, A0=None, og=0):
     """RNEA (rnea_loop, dynamics.hpp:272-327; Alg. 1 of PAPER.md:141-151):
     x(0) = q, x(1) = q̇ (if with_qd), x(2) = q̈ (if with_qdd); y(0, i) = τ_i.
     with_qdd = False is the bias term c + g (dynamics.hpp:434-435), with_qd =
@@ -926,7 +943,7 @@ def gen_rnea(rb, with_qd, with_qdd, dual=False, fext=False):
     fext: f_i −= ⁱX₀* f_ext,i (dynamics.hpp:243-245, rnea_loop 316-318), the
     world transform carried down the DFS and rebuilt from the child between
     siblings."""
-    A = Algo(rb, with_qd, extra=(2,) if with_qdd else (), dual=dual)
+    A = A0 or Algo(rb, with_qd, extra=(2,) if with_qdd else (), dual=dual)
     g = A.g
     gvec = A.gravity()
 
@@ -952,17 +969,17 @@ def gen_rnea(rb, with_qd, with_qdd, dual=False, fext=False):
         if rb.children[i]:
             X = A.joint(i)
         tau = X.Sdot(f)
-        g.output(0, i, tau)
+        g.output(og, i, tau)
         if vp is None:
             return None, None
         return X.force_to_parent(f), (world_of_parent(g, X, W) if fext else None)
 
     for r in rb.roots:
         rec(r, None, None)
-    return A.finish()
+    return A.finish() if A0 is None else A
 
 
-def gen_crba(rb, dual=False, packed=False):
+def gen_crba(rb, dual=False, packed=False, A0=None, og=0):
     """CRBA (crba_loop, dynamics.hpp:369-400; Alg. 2 of PAPER.md:156-165):
     x(0) = q; y(0, c·n + r) = M(r, c), dense, with exact zeros between
     branches (dynamics.hpp:330-335, test_dynamics.cpp:200-216).  packed: only
@@ -971,7 +988,7 @@ def gen_crba(rb, dual=False, packed=False):
     inertias (10-parameter form) are summed leaf -> root in one DFS; each
     column is emitted as soon as its composite is complete, walking the force
     F = Ic S up the ancestor chain."""
-    A = Algo(rb, False, dual=dual)
+    A = A0 or Algo(rb, False, dual=dual)
     g = A.g
     n = rb.n
     related = [[False] * n for _ in range(n)]
@@ -980,11 +997,11 @@ def gen_crba(rb, dual=False, packed=False):
     def emit(r, c, val):
         related[r][c] = related[c][r] = True
         if packed:
-            g.output(0, pidx[(r, c)], val)
+            g.output(og, pidx[(r, c)], val)
             return
-        g.output(0, c * n + r, val)
+        g.output(og, c * n + r, val)
         if r != c:
-            g.output(0, r * n + c, val)
+            g.output(og, r * n + c, val)
 
     def rec(i):
         Ic = rb.rb(i)
@@ -1008,8 +1025,8 @@ def gen_crba(rb, dual=False, packed=False):
     for c in range(n if not packed else 0):
         for r in range(n):
             if not related[r][c]:
-                g.output(0, c * n + r, ZERO)
-    return A.finish()
+                g.output(og, c * n + r, ZERO)
+    return A.finish() if A0 is None else A
 
 
 def Joint_Sdot(g, rb, j, f):
@@ -1780,6 +1797,23 @@ def emit_body(name, cls, rb, ops=None, tasks=True, task_joints=None, pool_ops=()
                 f"    static constexpr int kFlops = {A.g.flops};",
                 f"    static constexpr int kIn = {nin};",
                 f"    static constexpr int kOut = {nout(rb)};",
+                "    template <class T, class Cx>",
+                "    VD_HD static bool run(Cx& cx) {"]
+        out += ["    " + ln for ln in A.g.lines]
+        out += ["    }", "  };"]
+    # the fused M + bias + q̈ routine (vd_dynamics, config 3) for serial chains
+    # of the builtin set (the branched G1 runs three launches: its fused state
+    # would not fit on chip)
+    if ops is None and all(p == i - 1 for i, p in enumerate(rb.parent)):
+        A = gen_dyn(rb)
+        out += [f"  // Dyn (M, bias, q̈): {A.g.flops} mul/add after folding; {A.nslot} slots",
+                "  struct Dyn {",
+                f"    static constexpr int kSlots = {A.nslot};",
+                f"    static constexpr int kDof = {rb.n};",
+                f"    static constexpr int kPrologue = {A.nprologue};",
+                f"    static constexpr int kFlops = {A.g.flops};",
+                "    static constexpr int kIn = 3;",
+                f"    static constexpr int kOut = {rb.n * rb.n + 2 * rb.n};",
                 "    template <class T, class Cx>",
                 "    VD_HD static bool run(Cx& cx) {"]
         out += ["    " + ln for ln in A.g.lines]

@@ -192,6 +192,7 @@ int launch_dynamics(const Launch& L, const void* q, const void* qd, const void* 
     if (qdd && (rc = launch_aba(L, q, qd, tau, g3, nullptr, qdd, status)) != 0) return rc;
     return 0;
   }
+  if (const int rc = launch_gen_dyn(L, q, qd, tau, g3, M, bias, qdd, status); rc >= 0) return rc;
   if (L.spec == kTree29) {
     // generated kernels, one per output (each re-derives the joint
     // transforms; cheaper than the fused loop kernel's local-memory state)

@@ -467,6 +467,62 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
   }
 }
 
+// Fused forward-dynamics context (GenRobot::Dyn): output group 0 = M (n²
+// planes), 1 = bias (n), 2 = q̈ (n); a NULL group is not written.
+template <class T, int kSlots, int kReg, int kSmem, int kTrig = kTrigLib, bool kStream = false>
+struct GenDynCx : GenCx<T, kSlots, kReg, kSmem, kTrig, kStream> {
+  T* outs_[3];
+  __device__ __forceinline__ void y(int o, int k, T v) const {
+    T* p = outs_[o];
+    if (this->active && p) {
+      if constexpr (kStream) __stcs(p + k * this->ldo, v);
+      else p[k * this->ldo] = v;
+    }
+  }
+};
+
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig = kTrigLib, bool kStream = false>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen_dyn(int64_t N, const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau, int64_t ldi,
+              T g0, T g1, T g2, T* __restrict__ M, T* __restrict__ bias, T* __restrict__ qdd, int64_t ldo,
+              int32_t* __restrict__ status, T* __restrict__ scratch) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenDynCx<T, Op::kSlots, kReg, kSmem, kTrig, kStream>;
+  Cx cx;
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  cx.sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  cx.sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  cx.g3[0] = g0;
+  cx.g3[1] = g1;
+  cx.g3[2] = g2;
+  cx.fx_ = nullptr;
+  cx.gp_ = nullptr;
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride) {
+    const int64_t i0 = base + threadIdx.x;
+    cx.active = i0 < N;
+    const int64_t i = cx.active ? i0 : N - 1;
+    int64_t ld, lo;
+    asm volatile("mov.b64 %0, %1;" : "=l"(ld) : "l"(ldi));
+    asm volatile("mov.b64 %0, %1;" : "=l"(lo) : "l"(ldo));
+    cx.ld = ld;
+    cx.ldo = lo;
+    cx.in_[0] = q + i;
+    cx.in_[1] = qd + i;
+    cx.in_[2] = tau + i;
+    cx.out_ = nullptr;
+    cx.outs_[0] = M ? M + i : nullptr;
+    cx.outs_[1] = bias ? bias + i : nullptr;
+    cx.outs_[2] = qdd ? qdd + i : nullptr;
+    const bool ok = Op::template run<T>(cx);
+    if (cx.active) {
+      if (!ok && qdd)
+        for (int j = 0; j < Op::kDof; ++j) qdd[(int64_t)j * ldo + i] = T(0);
+      if (status) status[i] = ok ? 0 : 7;
+    }
+  }
+}
+
 // Forward-mode JVP context (JvpArgs): NULL primal inputs read as 0, NULL
 // tangents as 0; output group 0 = values, 1 = tangents (either may be NULL).
 template <class T, int kSlots, int kReg, int kSmem, bool kStream = false, int kTrig = kTrigLib>

@@ -291,6 +291,30 @@ int gen_osc_t(const Launch& L, const void* q, const void* qd, const OscShared& P
   return rc;
 }
 
+// Panda M + bias + q̈ in one generated routine (GenChain7::Dyn: one prologue,
+// CRBA, RNEA at q̈ = 0 and ABA straight-line; tools/dyn_sweep.cu, against
+// the fused template kernel k_tiled<OpDyn> 20.5 us / 0.083 / 1.277 ms at
+// 65536 / 262144 / 4M states): r40 s25 at 3 CTAs/SM with the Cody-Waite
+// sin/cos 19.1 us / 0.070 / 1.040 ms.  fp64 only (the fp32 call keeps the
+// template kernel); per-state gravity takes the three-launch split.
+int launch_gen_dyn(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
+                   void* bias, void* qdd, int32_t* status) {
+  if (L.spec != kChain7 || L.dtype != 0 || L.gravity_planes) return -1;
+  using Op = GenChain7::Dyn;
+  using T = double;
+  constexpr int kReg = 40, kSmem = Op::kSlots - 40, kMinB = 3;
+  auto kern = k_gen_dyn<Op, T, kReg, kSmem, kMinB, kTrigFast, false>;
+  constexpr size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
+  const Occ o = occupancy<Op, T>(kern, smem);
+  const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
+  cudaStream_t s = static_cast<cudaStream_t>(L.stream);
+  static_assert(gen_scratch_per_thread<Op, T, kReg, kSmem>() == 0, "every Dyn slot on chip");
+  const T g0 = g3 ? T(g3[0]) : T(0), g1 = g3 ? T(g3[1]) : T(0), g2 = g3 ? T(g3[2]) : T(9.81);
+  kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, (const T*)q, (const T*)qd, (const T*)tau, L.ld_in, g0, g1, g2,
+                                                 (T*)M, (T*)bias, (T*)qdd, L.ld_out, status, nullptr);
+  return (int)cudaGetLastError();
+}
+
 int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,
                    int32_t* status) {
   if (L.spec == kTree29) return gen_osc_t<GenTree29>(L, q, qd, P, tau, lambda, status);

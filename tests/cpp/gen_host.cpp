@@ -19,6 +19,7 @@ struct HostCx {
   // OSC parameters (gen_osc_host layout): fR 9, fp 3, tR 9, tp 3, kp 6, kd 6, aff 6, pkp, pkd, eps, posture n
   const double* P = nullptr;
   T* Y1 = nullptr;
+  T* Y2 = nullptr;  // output group 2 (the fused Dyn routine's q̈)
   const T* DX[3] = {nullptr, nullptr, nullptr};  // JVP tangents (NULL = 0)
   const T* FX = nullptr;                         // external wrenches, plane 6 j + k
   T x(int g, int j) const { return X[g] ? X[g][j * ld + i] : T(0); }
@@ -37,7 +38,7 @@ struct HostCx {
     std::memcpy(&v, &slots[k], sizeof(double));
     return v;
   }
-  void y(int o, int k, T v) const { (o == 0 ? Y : Y1)[k * ld + i] = v; }
+  void y(int o, int k, T v) const { (o == 0 ? Y : o == 1 ? Y1 : Y2)[k * ld + i] = v; }
   T fR(int k) const { return T(P[k]); }
   T fp(int k) const { return T(P[9 + k]); }
   T tR(int k) const { return T(P[12 + k]); }
@@ -107,6 +108,23 @@ int osc(int fj, long N, const double* q, const double* qd, const double* g, cons
   return bad;
 }
 }  // namespace
+
+// the fused chain7 M + bias + q̈ routine (GenChain7::Dyn), fp64
+extern "C" int gen_dyn_host(long N, const double* q, const double* qd, const double* tau, const double* g, double* M,
+                            double* bias, double* qdd, int* status) {
+  using Op = vdk::GenChain7::Dyn;
+  std::vector<double> slots(Op::kSlots + 1);
+  int bad = 0;
+  for (long i = 0; i < N; ++i) {
+    HostCx<double> cx{{q, qd, tau}, g, M, N, i, slots.data()};
+    cx.Y1 = bias;
+    cx.Y2 = qdd;
+    const bool ok = Op::template run<double>(cx);
+    status[i] = ok ? 0 : 7;
+    bad += !ok;
+  }
+  return bad;
+}
 
 // generated osc_step on frame joint fj (fp64); -1 when no variant exists for fj
 extern "C" int gen_osc_host(int robot, int fj, long N, const double* q, const double* qd, const double* g,

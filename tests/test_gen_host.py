@@ -335,3 +335,33 @@ def test_generated_fext_routines_match_oracle(genlib, name, code, f32):
     eps = np.finfo(np.float32 if f32 else np.float64).eps
     assert err[cond < 1e5].max(initial=0) <= tol
     assert np.all(err <= np.maximum(tol, om.n * eps * cond))
+
+
+def test_generated_fused_dynamics(genlib):
+    """GenChain7::Dyn (one prologue, CRBA + RNEA at q̈ = 0 + ABA) against the
+    oracle's crba, rnea and LLT forward dynamics, and against the separately
+    generated Crba / RneaBias / Aba routines on the same inputs."""
+    om = Model.builtin("chain7")
+    N, n = 1024, 7
+    q, qd, _, tau = om.random_states(N, 88, True, True)
+    F = lambda a: np.asfortranarray(a)  # noqa: E731
+    M = np.zeros((N, n * n), order="F")
+    b = np.zeros((N, n), order="F")
+    a = np.zeros((N, n), order="F")
+    st = np.zeros(N, dtype=np.int32)
+    g = np.array([0.0, 0.0, 9.81])
+    genlib.gen_dyn_host.argtypes = [ctypes.c_long] + [ctypes.c_void_p] * 8
+    bad = genlib.gen_dyn_host(N, _p(F(q)), _p(F(qd)), _p(F(tau)), _p(g), _p(M), _p(b), _p(a), _p(st))
+    assert bad == 0 and not st.any()
+    Mo = M.reshape(N, n, n).transpose(0, 2, 1)  # plane c·n + r = M(r, c)
+    assert rel_err(Mo, om.crba(q), axis=1).max() <= 1e-10
+    assert rel_err(b, om.rnea(q, qd, np.zeros_like(q)), axis=1).max() <= 1e-10
+    ref, _ = om.forward_dynamics(q, qd, tau)
+    assert rel_err(a, ref, axis=1).max() <= 1e-10
+    # the same expression graphs as the separate routines (up to FMA contraction)
+    aba, _, _ = _run(genlib, 1, 0, [q, qd, tau], n)
+    bias, _, _ = _run(genlib, 1, 2, [q, qd], n)
+    crba, _, _ = _run(genlib, 1, 4, [q], n * n)
+    assert rel_err(a, aba, axis=1).max() <= 1e-13
+    assert rel_err(b, bias, axis=1).max() <= 1e-13
+    assert rel_err(M, crba, axis=1).max() <= 1e-13

@@ -8,6 +8,8 @@
 #include <cmath>
 #include <vector>
 #include "vd_kernels.cuh"
+#include "vd_gen_robots.cuh"
+#include "vd_gen_kernels.cuh"
 using namespace vdk;
 
 template <class T, int kMB>
@@ -71,6 +73,46 @@ void run(const char* name, int64_t N, T* x, T* y, int32_t* st) {
          cudaGetErrorString(cudaGetLastError()));
 }
 
+// the generated fused routine (GenChain7::Dyn, k_gen_dyn)
+template <int kReg, int kSmem, int kMinB, int kTrig, bool kStream>
+void gen(const char* name, int64_t N, double* x, double* y, int32_t* st, double* scratch) {
+  using Op = GenChain7::Dyn;
+  auto kern = k_gen_dyn<Op, double, kReg, kSmem, kMinB, kTrig, kStream>;
+  const size_t smem = (size_t)kSmem * kGenBlock * sizeof(double);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int bps = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, kern);
+  if (bps < 1) { printf("%s does not fit\n", name); return; }
+  const int64_t grid = std::min<int64_t>((int64_t)sms * bps, (N + kGenBlock - 1) / kGenBlock);
+  const int n = 7;
+  auto go = [&] {
+    kern<<<grid, kGenBlock, smem>>>(N, x, x + n * N, x + 2 * n * N, N, 0.0, 0.0, 9.81, y, y + 49 * N, y + 56 * N, N,
+                                    st, scratch);
+  };
+  for (int w = 0; w < 3; ++w) go();
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int reps = N > 1000000 ? 10 : 200;
+  cudaEventRecord(a);
+  for (int r = 0; r < reps; ++r) go();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  ms /= reps;
+  std::vector<double> h((size_t)N * 63);
+  cudaMemcpy(h.data(), y, sizeof(double) * h.size(), cudaMemcpyDeviceToHost);
+  double md = 0;
+  for (size_t k = 0; k < h.size(); ++k) md = std::max(md, std::fabs(h[k] - g_ref[k]) / std::max(1.0, std::fabs(g_ref[k])));
+  printf("%-26s N %8lld  regs %3d lmem %4zu b/SM %d grid %lld  %.5f ms  %.3e evals/s  maxdiff vs k_tiled %.2e  %s\n",
+         name, (long long)N, fa.numRegs, fa.localSizeBytes, bps, (long long)grid, ms, N / (ms * 1e-3), md,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
 int main() {
   double *x, *y;
   int32_t* st;
@@ -78,10 +120,21 @@ int main() {
   cudaMalloc(&x, sizeof(double) * NM * 21);
   cudaMalloc(&y, sizeof(double) * NM * 63);
   cudaMalloc(&st, sizeof(int32_t) * NM);
+  double* scratch;
+  cudaMalloc(&scratch, 1ull << 30);
+  constexpr int S = GenChain7::Dyn::kSlots;
   for (int64_t N : {65536ll, 262144ll, 4194304ll}) {
     k_fill<<<1184, 256>>>(x, N * 21, 3);
     run<double, 3>("dyn f64", N, x, y, st);
-    run<double, 4>("dyn f64", N, x, y, st);
+    gen<S, 0, 2, kTrigFast, false>("gen r65 b2 fast", N, x, y, st, scratch);
+    gen<S, 0, 3, kTrigFast, false>("gen r65 b3 fast", N, x, y, st, scratch);
+    gen<S, 0, 3, kTrigFast, true>("gen r65 b3 fast cs", N, x, y, st, scratch);
+    gen<S, 0, 3, kTrigLib, false>("gen r65 b3 lib", N, x, y, st, scratch);
+    gen<S, 0, 4, kTrigFast, false>("gen r65 b4 fast", N, x, y, st, scratch);
+    gen<40, S - 40, 3, kTrigFast, false>("gen r40 s25 b3 fast", N, x, y, st, scratch);
+    gen<24, S - 24, 3, kTrigFast, false>("gen r24 s41 b3 fast", N, x, y, st, scratch);
+    gen<24, S - 24, 4, kTrigFast, false>("gen r24 s41 b4 fast", N, x, y, st, scratch);
+    gen<0, S, 4, kTrigFast, false>("gen s65 b4 fast", N, x, y, st, scratch);
   }
   return 0;
 }
