@@ -295,14 +295,15 @@ int gen_osc_t(const Launch& L, const void* q, const void* qd, const OscShared& P
 // CRBA, RNEA at q̈ = 0 and ABA straight-line; tools/dyn_sweep.cu, against
 // the fused template kernel k_tiled<OpDyn> 20.5 us / 0.083 / 1.277 ms at
 // 65536 / 262144 / 4M states): r40 s25 at 3 CTAs/SM with the Cody-Waite
-// sin/cos 19.1 us / 0.070 / 1.040 ms.  fp64 only (the fp32 call keeps the
-// template kernel); per-state gravity takes the three-launch split.
-int launch_gen_dyn(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
-                   void* bias, void* qdd, int32_t* status) {
-  if (L.spec != kChain7 || L.dtype != 0 || L.gravity_planes) return -1;
+// sin/cos 19.1 us / 0.070 / 1.040 ms.  fp32 (template 16.4 us / 0.648 ms at
+// 65536 / 4M): every slot in registers at 4 CTAs/SM, 12.3 us / 0.561 ms.
+// Per-state gravity takes the three-launch split.
+template <class T>
+int launch_gen_dyn_t(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
+                     void* bias, void* qdd, int32_t* status) {
   using Op = GenChain7::Dyn;
-  using T = double;
-  constexpr int kReg = 40, kSmem = Op::kSlots - 40, kMinB = 3;
+  constexpr bool f64 = sizeof(T) == 8;
+  constexpr int kReg = f64 ? 40 : Op::kSlots, kSmem = Op::kSlots - kReg, kMinB = f64 ? 3 : 4;
   auto kern = k_gen_dyn<Op, T, kReg, kSmem, kMinB, kTrigFast, false>;
   constexpr size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
   const Occ o = occupancy<Op, T>(kern, smem);
@@ -313,6 +314,12 @@ int launch_gen_dyn(const Launch& L, const void* q, const void* qd, const void* t
   kern<<<(unsigned)blocks, kGenBlock, smem, s>>>(L.N, (const T*)q, (const T*)qd, (const T*)tau, L.ld_in, g0, g1, g2,
                                                  (T*)M, (T*)bias, (T*)qdd, L.ld_out, status, nullptr);
   return (int)cudaGetLastError();
+}
+int launch_gen_dyn(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
+                   void* bias, void* qdd, int32_t* status) {
+  if (L.spec != kChain7 || L.gravity_planes) return -1;
+  return L.dtype == 0 ? launch_gen_dyn_t<double>(L, q, qd, tau, g3, M, bias, qdd, status)
+                      : launch_gen_dyn_t<float>(L, q, qd, tau, g3, M, bias, qdd, status);
 }
 
 int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,

@@ -89,7 +89,7 @@ int launch_gen_fk(const Launch& L, const void* q, void* frames);
 // which: 0 Jacobian, 1 diff-IK, 2 manipulability, 4 manipulability JVP along dq (y0 w, y1 dw)
 int launch_gen_task(const Launch& L, int which, int frame_joint, const TaskShared& P, const void* q, void* y0,
                     void* y1, int32_t* status, const void* dq = nullptr);
-// generated fused M + bias + q̈ (chain7 fp64); -1 when not applicable
+// generated fused M + bias + q̈ (chain7, fp64 and fp32); -1 when not applicable
 int launch_gen_dyn(const Launch& L, const void* q, const void* qd, const void* tau, const double* g3, void* M,
                    void* bias, void* qdd, int32_t* status);
 int launch_gen_osc(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lambda,

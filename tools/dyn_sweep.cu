@@ -5,6 +5,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr \
 //          -Xptxas -v -Ipaper_2604_04310_b200/csrc tools/dyn_sweep.cu -o ablib/dyn_sweep
 #include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 #include "vd_kernels.cuh"
@@ -74,11 +75,11 @@ void run(const char* name, int64_t N, T* x, T* y, int32_t* st) {
 }
 
 // the generated fused routine (GenChain7::Dyn, k_gen_dyn)
-template <int kReg, int kSmem, int kMinB, int kTrig, bool kStream>
-void gen(const char* name, int64_t N, double* x, double* y, int32_t* st, double* scratch) {
+template <int kReg, int kSmem, int kMinB, int kTrig, bool kStream, class T = double>
+void gen(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch) {
   using Op = GenChain7::Dyn;
-  auto kern = k_gen_dyn<Op, double, kReg, kSmem, kMinB, kTrig, kStream>;
-  const size_t smem = (size_t)kSmem * kGenBlock * sizeof(double);
+  auto kern = k_gen_dyn<Op, T, kReg, kSmem, kMinB, kTrig, kStream>;
+  const size_t smem = (size_t)kSmem * kGenBlock * sizeof(T);
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int bps = 0, sms = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kGenBlock, smem);
@@ -89,8 +90,8 @@ void gen(const char* name, int64_t N, double* x, double* y, int32_t* st, double*
   const int64_t grid = std::min<int64_t>((int64_t)sms * bps, (N + kGenBlock - 1) / kGenBlock);
   const int n = 7;
   auto go = [&] {
-    kern<<<grid, kGenBlock, smem>>>(N, x, x + n * N, x + 2 * n * N, N, 0.0, 0.0, 9.81, y, y + 49 * N, y + 56 * N, N,
-                                    st, scratch);
+    kern<<<grid, kGenBlock, smem>>>(N, x, x + n * N, x + 2 * n * N, N, T(0), T(0), T(9.81), y, y + 49 * N, y + 56 * N,
+                                    N, st, scratch);
   };
   for (int w = 0; w < 3; ++w) go();
   cudaEvent_t a, b;
@@ -104,10 +105,11 @@ void gen(const char* name, int64_t N, double* x, double* y, int32_t* st, double*
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
   ms /= reps;
-  std::vector<double> h((size_t)N * 63);
-  cudaMemcpy(h.data(), y, sizeof(double) * h.size(), cudaMemcpyDeviceToHost);
+  std::vector<T> h((size_t)N * 63);
+  cudaMemcpy(h.data(), y, sizeof(T) * h.size(), cudaMemcpyDeviceToHost);
   double md = 0;
-  for (size_t k = 0; k < h.size(); ++k) md = std::max(md, std::fabs(h[k] - g_ref[k]) / std::max(1.0, std::fabs(g_ref[k])));
+  for (size_t k = 0; k < h.size(); ++k)
+    md = std::max(md, std::fabs((double)h[k] - g_ref[k]) / std::max(1.0, std::fabs(g_ref[k])));
   printf("%-26s N %8lld  regs %3d lmem %4zu b/SM %d grid %lld  %.5f ms  %.3e evals/s  maxdiff vs k_tiled %.2e  %s\n",
          name, (long long)N, fa.numRegs, fa.localSizeBytes, bps, (long long)grid, ms, N / (ms * 1e-3), md,
          cudaGetErrorString(cudaGetLastError()));
@@ -123,6 +125,21 @@ int main() {
   double* scratch;
   cudaMalloc(&scratch, 1ull << 30);
   constexpr int S = GenChain7::Dyn::kSlots;
+  if (getenv("DYN_F32")) {  // fp32: template kernel vs the generated routine
+    float *xf = (float*)x, *yf = (float*)y, *sf = (float*)scratch;
+    for (int64_t N : {65536ll, 4194304ll}) {
+      k_fill<<<1184, 256>>>(xf, N * 21, 3);
+      run<float, 3>("dyn f32", N, xf, yf, st);
+      gen<40, S - 40, 3, kTrigFast, false, float>("gen f32 r40 s25 b3 fast", N, xf, yf, st, sf);
+      gen<40, S - 40, 4, kTrigFast, false, float>("gen f32 r40 s25 b4 fast", N, xf, yf, st, sf);
+      gen<S, 0, 4, kTrigFast, false, float>("gen f32 r65 b4 fast", N, xf, yf, st, sf);
+      gen<S, 0, 5, kTrigFast, false, float>("gen f32 r65 b5 fast", N, xf, yf, st, sf);
+      gen<24, S - 24, 5, kTrigFast, false, float>("gen f32 r24 s41 b5 fast", N, xf, yf, st, sf);
+      gen<24, S - 24, 5, kTrigLib, false, float>("gen f32 r24 s41 b5 lib", N, xf, yf, st, sf);
+      gen<0, S, 6, kTrigFast, false, float>("gen f32 s65 b6 fast", N, xf, yf, st, sf);
+    }
+    return 0;
+  }
   for (int64_t N : {65536ll, 262144ll, 4194304ll}) {
     k_fill<<<1184, 256>>>(x, N * 21, 3);
     run<double, 3>("dyn f64", N, x, y, st);
