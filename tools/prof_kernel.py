@@ -42,6 +42,12 @@ def main():
             rc = lib.vd_crba(dm.handle, code, N, x[0].data_ptr(), N, out.data_ptr(), N, s)
         elif op == "crbap":
             rc = lib.vd_crba_packed(dm.handle, code, N, x[0].data_ptr(), N, out.data_ptr(), N, s)
+        elif op == "dyn":  # vd_dynamics: M (n² planes), bias, q̈
+            if _ == 0:
+                bq = torch.empty((n, N), dtype=tdt, device="cuda")
+                aq = torch.empty((n, N), dtype=tdt, device="cuda")
+            rc = lib.vd_dynamics(dm.handle, code, N, x[0].data_ptr(), x[1].data_ptr(), x[2].data_ptr(), N, None,
+                                 out.data_ptr(), bq.data_ptr(), aq.data_ptr(), N, None, s)
         elif op == "fk":
             rc = lib.vd_fk(dm.handle, code, N, x[0].data_ptr(), N, out.data_ptr(), N, s)
         elif op == "osc":
