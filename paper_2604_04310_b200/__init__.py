@@ -680,8 +680,10 @@ def crba_jvp(dm, q, dq):
 
 def forward_dynamics_jvp(dm, q, qd, tau, dq=None, dqd=None, dtau=None, gravity=None, fext=None,
                          return_status=False):
-    """(q̈, dq̈) by the articulated-body algorithm on duals; SingularInertiaError
-    as forward_dynamics unless return_status."""
+    """(q̈, dq̈) by the articulated-body algorithm on duals (the G1 builtin:
+    dq̈ = M⁻¹(dτ − ∂ID·(dq, dq̇)) from its ABA and RNEA-JVP, q̈ bit for bit the
+    plain forward_dynamics); SingularInertiaError as forward_dynamics unless
+    return_status."""
     torch = _torch()
     qs, (qds, taus, dqs, dqds, dtaus), N, dev = _prep(dm, q, (qd, "qd"), (tau, "tau"), (dq, "dq"), (dqd, "dqd"),
                                                         (dtau, "dtau"))
@@ -710,8 +712,9 @@ def rnea_derivatives(dm, q, qd, qdd, gravity=None):
 
 def forward_dynamics_derivatives(dm, q, qd, tau, gravity=None):
     """(∂q̈/∂q, ∂q̈/∂q̇, ∂q̈/∂τ), each (N, n, n): jacobian_fwd (autodiff.hpp:67-84)
-    of forward dynamics by the dual-number ABA, n passes per argument
-    (∂q̈/∂τ = M⁻¹).  SingularInertiaError as forward_dynamics."""
+    of forward dynamics by the library's ABA-JVP (the dual-number ABA; for the
+    G1 its implicit-function form), n passes per argument (∂q̈/∂τ = M⁻¹).
+    SingularInertiaError as forward_dynamics."""
     return _jac_fwd(dm, q, lambda e, zero: forward_dynamics_jvp(dm, q, qd, tau, e, zero, zero, gravity)[1],
                     lambda e, zero: forward_dynamics_jvp(dm, q, qd, tau, zero, e, zero, gravity)[1],
                     lambda e, zero: forward_dynamics_jvp(dm, q, qd, tau, zero, zero, e, gravity)[1])
