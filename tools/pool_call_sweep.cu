@@ -193,6 +193,19 @@ int main(int argc, char** argv) {
     gen<GenTree29::Crba, float, 0, 55, 4, kTrigCall, true, false>("t29 crba f32 trig cs", N, xf, yf, st, sf);
     return 0;
   }
+  if (argc > 1 && !strcmp(argv[1], "c7rnea")) {  // sweep 7: Panda RNEA placement / evict-first, 1M states
+    const int64_t N7 = 1048576;
+    constexpr int S = GenChain7::Rnea::kSlots;
+    gen<GenChain7::Rnea, double, S, 0, 4, kTrigFast, false, false>("c7 rnea f64 r b4", N7, x, y, st, scratch);
+    gen<GenChain7::Rnea, double, S, 0, 4, kTrigFast, true, false>("c7 rnea f64 r b4 cs", N7, x, y, st, scratch);
+    gen<GenChain7::Rnea, double, S, 0, 3, kTrigFast, true, false>("c7 rnea f64 r b3 cs", N7, x, y, st, scratch);
+    gen<GenChain7::Rnea, double, 0, S, 5, kTrigFast, true, false>("c7 rnea f64 s b5 cs", N7, x, y, st, scratch);
+    gen<GenChain7::Rnea, double, 0, S, 6, kTrigFast, true, false>("c7 rnea f64 s b6 cs", N7, x, y, st, scratch);
+    gen<GenChain7::Rnea, double, S, 0, 4, kTrigLib, true, false>("c7 rnea f64 r b4 cs lib", N7, x, y, st, scratch);
+    gen<GenChain7::RneaBias, double, GenChain7::RneaBias::kSlots, 0, 4, kTrigFast, false, false>("c7 bias f64 r b4", N7, x, y, st, scratch);
+    gen<GenChain7::RneaBias, double, GenChain7::RneaBias::kSlots, 0, 4, kTrigFast, true, false>("c7 bias f64 r b4 cs", N7, x, y, st, scratch);
+    return 0;
+  }
   if (more) {  // sweep 3: the remaining generated routines, loop vs per-state call
     const int64_t N7 = 1048576;
     gen<GenTree29::RneaBias, double, 0, 72, 3, kTrigCall, false, false>("t29 rneabias f64", N, x, y, st, scratch);
