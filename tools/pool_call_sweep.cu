@@ -129,7 +129,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&y, sizeof(double) * N * 841 * 2);
   cudaMalloc(&lam, sizeof(double) * 1048576 * 36);  // sweep 3 runs chain7 at 1M states
   cudaMalloc(&scratch, cap);
-  cudaMalloc(&st, sizeof(int32_t) * N);
+  cudaMalloc(&st, sizeof(int32_t) * 4194304);  // the chain7 sweeps run up to 4M states
   k_fill<<<1184, 256>>>(x, N * 29 * 6, 7);
   float *xf = (float*)(x), *yf = (float*)y, *lf = (float*)lam, *sf = (float*)scratch;
   using namespace vdk;
@@ -204,6 +204,25 @@ int main(int argc, char** argv) {
     gen<GenChain7::Rnea, double, S, 0, 4, kTrigLib, true, false>("c7 rnea f64 r b4 cs lib", N7, x, y, st, scratch);
     gen<GenChain7::RneaBias, double, GenChain7::RneaBias::kSlots, 0, 4, kTrigFast, false, false>("c7 bias f64 r b4", N7, x, y, st, scratch);
     gen<GenChain7::RneaBias, double, GenChain7::RneaBias::kSlots, 0, 4, kTrigFast, true, false>("c7 bias f64 r b4 cs", N7, x, y, st, scratch);
+    return 0;
+  }
+  if (argc > 1 && !strcmp(argv[1], "c7ck")) {  // sweep 8: generated Panda CRBA / FK at 4M (template: 0.355 / 0.579 ms)
+    const int64_t N7 = 4194304;
+    constexpr int SC = GenChain7::Crba::kSlots, SF = GenChain7::Fk::kSlots;
+    gen<GenChain7::Crba, double, SC, 0, 3, kTrigFast, false, false>("c7 crba f64 r b3", N7, x, y, st, scratch);
+    gen<GenChain7::Crba, double, SC, 0, 3, kTrigFast, true, false>("c7 crba f64 r b3 cs", N7, x, y, st, scratch);
+    gen<GenChain7::Crba, double, SC, 0, 4, kTrigFast, true, false>("c7 crba f64 r b4 cs", N7, x, y, st, scratch);
+    gen<GenChain7::Crba, double, 0, SC, 4, kTrigFast, true, false>("c7 crba f64 s b4 cs", N7, x, y, st, scratch);
+    gen<GenChain7::Crba, double, SC, 0, 4, kTrigLib, true, false>("c7 crba f64 r b4 cs lib", N7, x, y, st, scratch);
+    gen<GenChain7::Fk, double, SF, 0, 3, kTrigFast, false, false>("c7 fk f64 r b3", N7, x, y, st, scratch);
+    gen<GenChain7::Fk, double, SF, 0, 3, kTrigFast, true, false>("c7 fk f64 r b3 cs", N7, x, y, st, scratch);
+    gen<GenChain7::Fk, double, SF, 0, 4, kTrigFast, true, false>("c7 fk f64 r b4 cs", N7, x, y, st, scratch);
+    gen<GenChain7::Fk, double, SF, 0, 4, kTrigLib, true, false>("c7 fk f64 r b4 cs lib", N7, x, y, st, scratch);
+    k_fill<<<1184, 256>>>(xf, N * 29 * 6, 7);
+    gen<GenChain7::Crba, float, SC, 0, 4, kTrigLib, true, false>("c7 crba f32 r b4 cs lib", N7, xf, yf, st, sf);
+    gen<GenChain7::Crba, float, SC, 0, 6, kTrigLib, true, false>("c7 crba f32 r b6 cs lib", N7, xf, yf, st, sf);
+    gen<GenChain7::Fk, float, SF, 0, 4, kTrigLib, true, false>("c7 fk f32 r b4 cs lib", N7, xf, yf, st, sf);
+    gen<GenChain7::Fk, float, SF, 0, 6, kTrigLib, true, false>("c7 fk f32 r b6 cs lib", N7, xf, yf, st, sf);
     return 0;
   }
   if (more) {  // sweep 3: the remaining generated routines, loop vs per-state call
