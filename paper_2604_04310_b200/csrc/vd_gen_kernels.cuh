@@ -418,6 +418,88 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
   }
 }
 
+// k_gen_osc with double-buffered asynchronous state input (OscCfg::kAsync):
+// the OSC routine reads q again at its end (posture torque), so the
+// single-buffer release scheme of k_gen_async would start the next state's
+// q copy only then.  Here state s reads its q, q̇ from shared buffer s & 1
+// while the copies of state s + 1 land in the other buffer, issued as state
+// s starts.  Shared memory per thread: kSmem slots, then 2 × 2 × kDof inputs.
+template <class T, int kSlots, int kReg, int kSmem, int kTrig, int kDof>
+struct GenOscDbCx : GenOscCx<T, kSlots, kReg, kSmem, kTrig> {
+  uint32_t ib;  // shared address of this state's input element (0, 0)
+  static __device__ __forceinline__ uint32_t off(int g, int j) {
+    return (uint32_t)((g * kDof + j) * kGenBlock * (int)sizeof(T));
+  }
+  __device__ __forceinline__ T x(int g, int j) const { return GenMem<T>::lds(ib + off(g, j)); }
+  static __device__ __forceinline__ void fetch(uint32_t buf, const T* q, const T* qd, int64_t ld) {
+#pragma unroll
+    for (int j = 0; j < kDof; ++j) vd_cp_async<false>(buf + off(0, j), q + j * ld, 0);
+#pragma unroll
+    for (int j = 0; j < kDof; ++j) vd_cp_async<false>(buf + off(1, j), qd + j * ld, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+};
+
+template <class Op, class T, int kSmem>
+constexpr size_t gen_osc_db_smem() {
+  return (size_t)(kSmem + 4 * Op::kDof) * kGenBlock * sizeof(T);
+}
+
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig = kTrigLib>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen_osc_db(int64_t N, const T* __restrict__ q, const T* __restrict__ qd, int64_t ldi,
+                 const __grid_constant__ OscShared P, T* __restrict__ tau, T* __restrict__ lam, int64_t ldo,
+                 int32_t* __restrict__ status, T* __restrict__ scratch) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenOscDbCx<T, Op::kSlots, kReg, kSmem, kTrig, Op::kDof>;
+  Cx cx;
+  cx.P = &P;
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  cx.sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  cx.sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  const uint32_t ib0 = cx.sm + (uint32_t)(kSmem * kGenBlock * sizeof(T));
+  const uint32_t ib1 = ib0 + (uint32_t)(2 * Op::kDof * kGenBlock * sizeof(T));
+  {
+    const int64_t i = slot < N ? slot : N - 1;
+    Cx::fetch(ib0, q + i, qd + i, ldi);
+  }
+  int buf = 0;
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride, buf ^= 1) {
+    const int64_t i0 = base + threadIdx.x;
+    cx.active = i0 < N;
+    const int64_t i = cx.active ? i0 : N - 1;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    // the next state's inputs into the other buffer (its previous reader,
+    // state s - 1, has finished)
+    if (base + stride < N) {
+      const int64_t inext = i0 + stride < N ? i0 + stride : N - 1;
+      Cx::fetch(buf ? ib0 : ib1, q + inext, qd + inext, ldi);
+    }
+    cx.ib = buf ? ib1 : ib0;
+    int64_t ld, lo;
+    asm volatile("mov.b64 %0, %1;" : "=l"(ld) : "l"(ldi));
+    asm volatile("mov.b64 %0, %1;" : "=l"(lo) : "l"(ldo));
+    cx.ld = ld;
+    cx.ldo = lo;
+    cx.in_[0] = q + i;
+    cx.in_[1] = qd + i;
+    cx.in_[2] = q + i;
+    cx.out_ = tau + i;
+    cx.out1_ = lam ? lam + i : nullptr;
+    const bool ok = Op::template run<T>(cx);
+    if (cx.active) {
+      if (!ok) {
+        for (int j = 0; j < Op::kOut; ++j) tau[(int64_t)j * ldo + i] = T(0);
+        if (lam)
+          for (int j = 0; j < 36; ++j) lam[(int64_t)j * ldo + i] = T(0);
+      }
+      if (status) status[i] = ok ? 0 : 7;
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // k_gen_osc with the routine called out of line once per state (OscCfg::kCall;
 // see k_gen_call): a routine that reads its model constants from the robot's
 // __constant__ table (codegen POOL_OPS) gets them as constant-bank operands.

@@ -159,8 +159,13 @@ template <class Op, class T>
 int launch_osc_t(const Launch& L, const void* q, const void* qd, const OscShared& P, void* tau, void* lam,
                  int32_t* status) {
   using C = OscCfg<Op, T>;
-  auto kern = k_gen_osc<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast>;
-  constexpr size_t smem = (size_t)C::kSmem * kGenBlock * sizeof(T);
+  // OscCfg::kAsync: double-buffered asynchronous state input (k_gen_osc_db)
+  constexpr bool kDb = AsyncIo<C>::value;
+  auto kern = [] {
+    if constexpr (kDb) return k_gen_osc_db<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast>;
+    else return k_gen_osc<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast>;
+  }();
+  constexpr size_t smem = kDb ? gen_osc_db_smem<Op, T, C::kSmem>() : (size_t)C::kSmem * kGenBlock * sizeof(T);
   const Occ o = occupancy<Op, T>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
   cudaStream_t s = static_cast<cudaStream_t>(L.stream);

@@ -136,10 +136,13 @@ struct Cfg<GenTree29::AbaMixedFext, float> : Cfg<GenTree29::AbaMixed, float> {};
 // chain7 (Panda `ee`), N = 4M, tools/async_sweep.cu "more": every slot on
 // chip.  fp64 r80 s67 b2 1.45 ms, fp32 r60 s87 1.56 -> 0.70 ms, against the
 // templated osc_one kernel 2.35 / 1.57 ms.
+// fp32 with double-buffered asynchronous q, q̇ (k_gen_osc_db; pool_call_sweep
+// oscdb, 2M states): 0.347 -> 0.332 ms; fp64 0.725 -> 0.716 ms, kept plain.
 template <class T>
 struct OscCfg<GenChain7::Osc6, T> {
   static constexpr int kReg = sizeof(T) == 8 ? 80 : 60, kSmem = sizeof(T) == 8 ? 67 : 87, kMinB = 2;
   static constexpr int kFast = kTrigLib;
+  static constexpr bool kAsync = sizeof(T) == 4;
 };
 
 namespace {

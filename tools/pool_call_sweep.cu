@@ -84,6 +84,27 @@ void osc(const char* name, int64_t N, T* x, T* y, T* lam, int32_t* st, T* scratc
          cudaGetErrorString(cudaGetLastError()));
 }
 
+// double-buffered asynchronous input (k_gen_osc_db) against the plain kernel
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig, bool kDb>
+void oscdb(const char* name, int64_t N, T* x, T* y, T* lam, int32_t* st, T* scratch) {
+  auto kern = kDb ? k_gen_osc_db<Op, T, kReg, kSmem, kMinB, kTrig> : k_gen_osc<Op, T, kReg, kSmem, kMinB, kTrig>;
+  const size_t smem = kDb ? gen_osc_db_smem<Op, T, kSmem>() : (size_t)kSmem * kGenBlock * sizeof(T);
+  OscShared P{};
+  for (int k = 0; k < 9; ++k) P.frame_R[k] = P.target_R[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  P.target_p[2] = 0.3;
+  for (int k = 0; k < 6; ++k) { P.kp[k] = 100; P.kd[k] = 20; }
+  P.posture_kp = 10; P.posture_kd = 2; P.gravity[2] = 9.81; P.epsilon = 1e-6;
+  const int n = Op::kDof;
+  int bps, regs;
+  const float ms = time_it(kern, smem, [&](int64_t grid) {
+    grid = std::min<int64_t>(grid, (N + kGenBlock - 1) / kGenBlock);
+    kern<<<grid, kGenBlock, smem>>>(N, x, x + N * n, N, P, y, lam, N, st, scratch);
+  }, &bps, &regs);
+  printf("%-36s %s regs %3d b/SM %d  %.4f ms  %.3e evals/s  sum %.12e  %s\n", name, kDb ? "db  " : "plain", regs, bps,
+         ms, N / (ms * 1e-3), checksum(y, (size_t)N * n) + checksum(lam, (size_t)N * 36),
+         cudaGetErrorString(cudaGetLastError()));
+}
+
 template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig, bool kCall>
 void jvp(const char* name, int64_t N, T* x, T* y, T* scratch) {
   auto kern = kCall ? k_gen_jvp_call<Op, T, kReg, kSmem, kMinB, true, kTrig>
@@ -127,7 +148,7 @@ int main(int argc, char** argv) {
   int32_t* st;
   cudaMalloc(&x, sizeof(double) * N * 29 * 6);
   cudaMalloc(&y, sizeof(double) * N * 841 * 2);
-  cudaMalloc(&lam, sizeof(double) * 1048576 * 36);  // sweep 3 runs chain7 at 1M states
+  cudaMalloc(&lam, sizeof(double) * 2097152 * 36);  // sweeps 3 / 9 run chain7 at 1M / 2M states
   cudaMalloc(&scratch, cap);
   cudaMalloc(&st, sizeof(int32_t) * 4194304);  // the chain7 sweeps run up to 4M states
   k_fill<<<1184, 256>>>(x, N * 29 * 6, 7);
@@ -204,6 +225,18 @@ int main(int argc, char** argv) {
     gen<GenChain7::Rnea, double, S, 0, 4, kTrigLib, true, false>("c7 rnea f64 r b4 cs lib", N7, x, y, st, scratch);
     gen<GenChain7::RneaBias, double, GenChain7::RneaBias::kSlots, 0, 4, kTrigFast, false, false>("c7 bias f64 r b4", N7, x, y, st, scratch);
     gen<GenChain7::RneaBias, double, GenChain7::RneaBias::kSlots, 0, 4, kTrigFast, true, false>("c7 bias f64 r b4 cs", N7, x, y, st, scratch);
+    return 0;
+  }
+  if (argc > 1 && !strcmp(argv[1], "oscdb")) {  // sweep 9: Panda OSC, double-buffered asynchronous input
+    const int64_t N7 = 2097152;
+    oscdb<GenChain7::Osc6, double, 80, 67, 2, kTrigLib, false>("c7 osc6 f64 r80 s67 b2", N7, x, y, lam, st, scratch);
+    oscdb<GenChain7::Osc6, double, 80, 67, 2, kTrigLib, true>("c7 osc6 f64 r80 s67 b2", N7, x, y, lam, st, scratch);
+    oscdb<GenChain7::Osc6, double, 80, 67, 2, kTrigFast, true>("c7 osc6 f64 r80 s67 b2 fast", N7, x, y, lam, st, scratch);
+    oscdb<GenChain7::Osc6, double, 60, 87, 2, kTrigLib, true>("c7 osc6 f64 r60 s87 b2", N7, x, y, lam, st, scratch);
+    k_fill<<<1184, 256>>>(xf, N * 29 * 6, 7);
+    oscdb<GenChain7::Osc6, float, 60, 87, 2, kTrigLib, false>("c7 osc6 f32 r60 s87 b2", N7, xf, yf, lf, st, sf);
+    oscdb<GenChain7::Osc6, float, 60, 87, 2, kTrigLib, true>("c7 osc6 f32 r60 s87 b2", N7, xf, yf, lf, st, sf);
+    oscdb<GenChain7::Osc6, float, 60, 87, 3, kTrigLib, true>("c7 osc6 f32 r60 s87 b3", N7, xf, yf, lf, st, sf);
     return 0;
   }
   if (argc > 1 && !strcmp(argv[1], "c7ck")) {  // sweep 8: generated Panda CRBA / FK at 4M (template: 0.355 / 0.579 ms)
