@@ -227,6 +227,16 @@ int main(int argc, char** argv) {
     gen<GenChain7::RneaBias, double, GenChain7::RneaBias::kSlots, 0, 4, kTrigFast, true, false>("c7 bias f64 r b4 cs", N7, x, y, st, scratch);
     return 0;
   }
+  if (argc > 1 && !strcmp(argv[1], "g1osc")) {  // sweep 10: G1 OSC placements with the out-of-line sin/cos
+    osc<GenTree29::Osc23, double, 40, 110, 2, kTrigCall, false>("t29 osc23 f64 r40 s110 b2", N, x, y, lam, st, scratch);
+    osc<GenTree29::Osc23, double, 24, 110, 2, kTrigCall, false>("t29 osc23 f64 r24 s110 b2", N, x, y, lam, st, scratch);
+    osc<GenTree29::Osc23, double, 56, 110, 2, kTrigCall, false>("t29 osc23 f64 r56 s110 b2", N, x, y, lam, st, scratch);
+    osc<GenTree29::Osc23, double, 40, 100, 2, kTrigCall, false>("t29 osc23 f64 r40 s100 b2", N, x, y, lam, st, scratch);
+    osc<GenTree29::Osc23, double, 0, 72, 3, kTrigCall, false>("t29 osc23 f64 r0 s72 b3", N, x, y, lam, st, scratch);
+    osc<GenTree29::Osc23, double, 24, 72, 3, kTrigCall, false>("t29 osc23 f64 r24 s72 b3", N, x, y, lam, st, scratch);
+    osc<GenTree29::Osc23, double, 40, 214, 1, kTrigCall, false>("t29 osc23 f64 r40 s214 b1", N, x, y, lam, st, scratch);
+    return 0;
+  }
   if (argc > 1 && !strcmp(argv[1], "oscdb")) {  // sweep 9: Panda OSC, double-buffered asynchronous input
     const int64_t N7 = 2097152;
     oscdb<GenChain7::Osc6, double, 80, 67, 2, kTrigLib, false>("c7 osc6 f64 r80 s67 b2", N7, x, y, lam, st, scratch);
