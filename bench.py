@@ -354,7 +354,7 @@ def run_ours(args):
     # DRAM traffic per launch of this kernel at this N from the committed
     # `ncu --set full` capture (tools/capture_profiles.sh; ncu cannot run
     # inside the timed bench)
-    prof = next((os.path.join(ROOT, "profiles", f"{r}_chain7_aba_f64.json") for r in ("r02b", "r02", "r01")
+    prof = next((os.path.join(ROOT, "profiles", f"{r}_chain7_aba_f64.json") for r in ("r02d", "r02b", "r02", "r01")
                  if os.path.exists(os.path.join(ROOT, "profiles", f"{r}_chain7_aba_f64.json"))), "")
     if prof:
         with open(prof) as f:
@@ -548,7 +548,7 @@ def run_configs(vd, lib, dev, stream, sptr, args, rank, world):
              "hbm_frac": round(byts / (ms * 1e-3) / 1e9 / measured_peaks().get("hbm_gbs", 6650.0), 4)})
     del Md, Mp, q
     # the headline workload in fp32 (the north star's fp32 mode, 1e-4 parity):
-    # Panda ABA, 4M states per GPU, generated kernel with async state input
+    # Panda ABA, 4M states per GPU, generated kernel with double-buffered async state input
     N = N_HEAD
     q, qd, x = states(7, N, torch.float32)
     a32 = torch.empty((7, N), dtype=torch.float32, device=dev)

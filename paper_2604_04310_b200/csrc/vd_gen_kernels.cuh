@@ -418,6 +418,84 @@ __global__ void __launch_bounds__(kGenBlock, kMinB)
   }
 }
 
+// k_gen with double-buffered asynchronous state input (Cfg::kDb):
+// state s reads its inputs from shared buffer s & 1 while the cp.async copies
+// of state s + 1 (every input group) land in the other, issued as state s
+// starts; the routine's fetch_next release points are not used.  Shared
+// memory per thread: kSmem slots, then 2 × kIn × kDof inputs.
+template <class T, int kSlots, int kReg, int kSmem, int kFast, bool kStream, int kDof>
+struct GenDbCx : GenCx<T, kSlots, kReg, kSmem, kFast, kStream> {
+  uint32_t ib;
+  static __device__ __forceinline__ uint32_t off(int g, int j) {
+    return (uint32_t)((g * kDof + j) * kGenBlock * (int)sizeof(T));
+  }
+  __device__ __forceinline__ T x(int g, int j) const { return GenMem<T>::lds(ib + off(g, j)); }
+  __device__ __forceinline__ T g(int k) const { return this->g3[k]; }
+};
+
+template <class Op, class T, int kSmem>
+constexpr size_t gen_db_smem() {
+  return (size_t)(kSmem + 2 * Op::kIn * Op::kDof) * kGenBlock * sizeof(T);
+}
+
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kFast = kTrigLib, bool kStream = false>
+__global__ void __launch_bounds__(kGenBlock, kMinB)
+    k_gen_db(int64_t N, const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2, int64_t ldi,
+             T g0, T g1, T g2, T* __restrict__ y, int64_t ldo, int32_t* __restrict__ status, T* __restrict__ scratch,
+             const T* __restrict__ fext, const T* __restrict__) {
+  extern __shared__ __align__(16) unsigned char vd_gen_smem[];
+  using Cx = GenDbCx<T, Op::kSlots, kReg, kSmem, kFast, kStream, Op::kDof>;
+  Cx cx;
+  uint64_t pol = 0;
+  if constexpr (kStream) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const int64_t slot = (int64_t)blockIdx.x * kGenBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kGenBlock;
+  cx.sb = scratch + (slot >> 5) * (int64_t)(Cx::kGlobal * 32) + (slot & 31);
+  cx.sm = (uint32_t)__cvta_generic_to_shared(vd_gen_smem) + threadIdx.x * (uint32_t)sizeof(T);
+  cx.g3[0] = g0;
+  cx.g3[1] = g1;
+  cx.g3[2] = g2;
+  cx.gp_ = nullptr;
+  const uint32_t ib0 = cx.sm + (uint32_t)(kSmem * kGenBlock * sizeof(T));
+  const uint32_t ib1 = ib0 + (uint32_t)(Op::kIn * Op::kDof * kGenBlock * sizeof(T));
+  const T* xs[3] = {x0, Op::kIn > 1 ? x1 : x0, Op::kIn > 2 ? x2 : x0};
+  auto fetch = [&](uint32_t buf, int64_t i) {
+#pragma unroll
+    for (int g = 0; g < Op::kIn; ++g)
+#pragma unroll
+      for (int j = 0; j < Op::kDof; ++j) vd_cp_async<kStream>(buf + Cx::off(g, j), xs[g] + i + j * ldi, pol);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  fetch(ib0, slot < N ? slot : N - 1);
+  int buf = 0;
+  for (int64_t base = (int64_t)blockIdx.x * kGenBlock; base < N; base += stride, buf ^= 1) {
+    const int64_t i0 = base + threadIdx.x;
+    cx.active = i0 < N;
+    const int64_t i = cx.active ? i0 : N - 1;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (base + stride < N) fetch(buf ? ib0 : ib1, i0 + stride < N ? i0 + stride : N - 1);
+    cx.ib = buf ? ib1 : ib0;
+    int64_t ld, lo;
+    asm volatile("mov.b64 %0, %1;" : "=l"(ld) : "l"(ldi));
+    asm volatile("mov.b64 %0, %1;" : "=l"(lo) : "l"(ldo));
+    cx.ld = ld;
+    cx.ldo = lo;
+    cx.in_[0] = xs[0] + i;
+    cx.in_[1] = xs[1] + i;
+    cx.in_[2] = xs[2] + i;
+    cx.out_ = y + i;
+    cx.fx_ = fext ? fext + i : nullptr;  // external wrenches stay global reads
+    const bool ok = Op::template run<T>(cx);
+    if (cx.active) {
+      if (!ok) {
+        for (int j = 0; j < Op::kOut; ++j) y[(int64_t)j * ldo + i] = T(0);
+      }
+      if (status) status[i] = ok ? 0 : 7;
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // k_gen_osc with double-buffered asynchronous state input (OscCfg::kAsync):
 // the OSC routine reads q again at its end (posture torque), so the
 // single-buffer release scheme of k_gen_async would start the next state's

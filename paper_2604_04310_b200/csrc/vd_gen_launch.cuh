@@ -39,6 +39,12 @@ template <class C, class = void>
 struct AsyncIo : std::false_type {};
 template <class C>
 struct AsyncIo<C, std::void_t<decltype(C::kAsync)>> : std::bool_constant<C::kAsync> {};
+// kDb (k_gen_db): double-buffered asynchronous input, every group of the next
+// state copied while the current one computes; false unless a Cfg sets it
+template <class C, class = void>
+struct DbIo : std::false_type {};
+template <class C>
+struct DbIo<C, std::void_t<decltype(C::kDb)>> : std::bool_constant<C::kDb> {};
 struct Occ {
   int blocks_per_sm = 0, sms = 0;
 };
@@ -74,10 +80,12 @@ struct CallIo : std::false_type {};
 template <class C>
 struct CallIo<C, std::void_t<decltype(C::kCall)>> : std::bool_constant<C::kCall> {};
 
-// The kernel of a Cfg (kMode 0 k_gen, 1 k_gen_async, 2 k_gen_call).
+// The kernel of a Cfg (kMode 0 k_gen, 1 k_gen_async, 2 k_gen_call, 3 k_gen_db).
 template <class Op, class T, class C, int kMode>
 constexpr auto gen_kernel() {
-  if constexpr (kMode == 1)
+  if constexpr (kMode == 3)
+    return k_gen_db<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
+  else if constexpr (kMode == 1)
     return k_gen_async<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
   else if constexpr (kMode == 2)
     return k_gen_call<Op, T, C::kReg, C::kSmem, C::kMinB, C::kFast, StreamIo<C>::value>;
@@ -91,7 +99,9 @@ int launch_gen(const Launch& L, const void* x0, const void* x1, const void* x2, 
   using C = Cfg<Op, T>;
   constexpr bool kAsync = kMode == 1;
   auto kern = gen_kernel<Op, T, C, kMode>();
-  constexpr size_t smem = kAsync ? gen_async_smem<Op, T, C::kReg, C::kSmem>() : (size_t)C::kSmem * kGenBlock * sizeof(T);
+  constexpr size_t smem = kMode == 3 ? gen_db_smem<Op, T, C::kSmem>()
+                         : kAsync  ? gen_async_smem<Op, T, C::kReg, C::kSmem>()
+                                   : (size_t)C::kSmem * kGenBlock * sizeof(T);
   const Occ o = occupancy<Op, T, kMode>(kern, smem);
   const int64_t blocks = std::min<int64_t>((L.N + kGenBlock - 1) / kGenBlock, (int64_t)o.sms * o.blocks_per_sm);
   cudaStream_t s = static_cast<cudaStream_t>(L.stream);
@@ -124,6 +134,9 @@ int launch_gen(const Launch& L, const void* x0, const void* x1, const void* x2, 
 template <class Op, class T>
 int launch_t(const Launch& L, const void* x0, const void* x1, const void* x2, const double* g3, void* y,
              int32_t* status, const void* fext = nullptr) {
+  if constexpr (DbIo<Cfg<Op, T>>::value) {
+    if (!L.gravity_planes) return launch_gen<Op, T, 3>(L, x0, x1, x2, g3, y, status, fext);
+  }
   if constexpr (AsyncIo<Cfg<Op, T>>::value) {
     if (!L.gravity_planes) return launch_gen<Op, T, 1>(L, x0, x1, x2, g3, y, status, fext);
   }

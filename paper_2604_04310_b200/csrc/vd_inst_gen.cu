@@ -18,27 +18,33 @@ namespace vdk {
 // The headline kernel, N = 4M states (tools/async_sweep.cu, one B200):
 // plain k_gen r44 s28 b4 0.599 ms; async r30 s35 b4 0.555, + evict-first
 // 0.548, r24 s41 (3 CTAs/SM) 0.543 ms; the templated TMA kernel 0.61 ms.
+// Double-buffered input (k_gen_db, every group of the next state in flight
+// for a whole state; tools/pool_call_sweep.cu gdb4): r44 s21 b3 0.520 ms
+// against the async kernel's 0.536-0.541 in the same run, same results.
 template <>
 struct Cfg<GenChain7::Aba, double> {
-  static constexpr int kReg = 24, kSmem = 41, kMinB = 3;
+  static constexpr int kReg = 44, kSmem = 21, kMinB = 3;
   static constexpr int kFast = kTrigFast;
-  static constexpr bool kStream = true, kAsync = true;
+  static constexpr bool kStream = true, kDb = true;
 };
 // chain7 fp32 ABA: generated + async, 0.41 ms for the templated TMA kernel ->
 // r40 s25 (6 CTAs/SM) 0.299 ms at 4M states with sincosf -> r30 s35 (5
-// CTAs/SM) 0.287 ms with vd_sincos_f32 (async_sweep c7f)
+// CTAs/SM) 0.287 ms with vd_sincos_f32 (async_sweep c7f) -> double-buffered
+// input 0.278 ms (gdb4)
 template <>
 struct Cfg<GenChain7::Aba, float> {
   static constexpr int kReg = 30, kSmem = 35, kMinB = 5;
   static constexpr int kFast = kTrigFast;
-  static constexpr bool kAsync = true;
+  static constexpr bool kDb = true;
 };
 // chain7 RNEA family: all slots in registers, fast fp64 sincos (gen_sweep:
-// fp64 0.252 vs 0.261 ms templated, fp32 0.142 vs 0.153 ms at 4M states)
+// fp64 0.252 vs 0.261 ms templated, fp32 0.142 vs 0.153 ms at 4M states);
+// double-buffered input (gdb4): fp64 0.258 -> 0.240 ms, fp32 0.147 -> 0.139 ms
 template <class T, int kSlotsAll>
 struct Chain7RneaCfg {
   static constexpr int kReg = kSlotsAll, kSmem = 0, kMinB = sizeof(T) == 8 ? 4 : 6;
   static constexpr int kFast = sizeof(T) == 8 ? kTrigFast : kTrigLib;  // fp32: vd_sincos_f32 measured 4 % slower
+  static constexpr bool kDb = true;
 };
 template <class T>
 struct Cfg<GenChain7::Rnea, T> : Chain7RneaCfg<T, GenChain7::Rnea::kSlots> {};

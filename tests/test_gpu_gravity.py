@@ -84,7 +84,15 @@ def test_rnea_family_per_state_gravity(vd, cuda, oracle, name, kind, dtype):
         if kind != "generic":
             # generated routine: identical arithmetic to the per-call launch
             same = _per_group(grp, G, lambda s, g: _np(per_call(g))[s], (N, n))
-            assert np.array_equal(got, same), op
+            if (name, kind) == ("chain7", "spec"):
+                # the per-call Panda RNEA family runs the double-buffered-input
+                # kernel (k_gen_db), per-state gravity the plain one (launch_t):
+                # the same routine compiled twice, so ptxas may contract
+                # differently; equal to rounding
+                tol = 1e-13 if dtype == torch.float64 else 1e-5
+                assert rel_err(got, same, axis=1).max() <= tol, op
+            else:
+                assert np.array_equal(got, same), op
 
 
 @pytest.mark.parametrize("name,kind", CASES)
@@ -119,7 +127,7 @@ def test_aba_per_state_gravity(vd, cuda, oracle, name, kind, dtype):
         per_call = lambda s, g: _np(vd.forward_dynamics(dm, tq, tqd, ttau, gravity=vd.GravitySpec(g)))[s]  # noqa: E731
         same = _per_group(grp, G, per_call, (N, n))
         if (name, kind) == ("chain7", "spec"):
-            # the per-call Panda ABA is the asynchronous-input kernel, per-state
+            # the per-call Panda ABA is the double-buffered-input kernel, per-state
             # gravity the plain one (launch_t): the same routine compiled twice,
             # so ptxas may contract differently; equal to rounding (× κ(M))
             assert np.all(rel_err(got, same, axis=1) <= bound)

@@ -105,6 +105,26 @@ void oscdb(const char* name, int64_t N, T* x, T* y, T* lam, int32_t* st, T* scra
          cudaGetErrorString(cudaGetLastError()));
 }
 
+// double-buffered asynchronous input (k_gen_db) against k_gen / k_gen_async
+template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig, bool kStream, int kMode>
+void gdb(const char* name, int64_t N, T* x, T* y, int32_t* st, T* scratch) {
+  auto kern = kMode == 2 ? k_gen_db<Op, T, kReg, kSmem, kMinB, kTrig, kStream>
+              : kMode == 1 ? k_gen_async<Op, T, kReg, kSmem, kMinB, kTrig, kStream>
+                           : k_gen<Op, T, kReg, kSmem, kMinB, kTrig, kStream>;
+  const size_t smem = kMode == 2 ? gen_db_smem<Op, T, kSmem>()
+                      : kMode == 1 ? gen_async_smem<Op, T, kReg, kSmem>() : (size_t)kSmem * kGenBlock * sizeof(T);
+  const int n = Op::kDof;
+  int bps, regs;
+  const float ms = time_it(kern, smem, [&](int64_t grid) {
+    grid = std::min<int64_t>(grid, (N + kGenBlock - 1) / kGenBlock);
+    kern<<<grid, kGenBlock, smem>>>(N, x, x + N * n, x + 2 * N * n, N, T(0), T(0), T(9.81), y, N, st, scratch, nullptr,
+                                    nullptr);
+  }, &bps, &regs);
+  printf("%-36s %s regs %3d b/SM %d  %.4f ms  %.3e evals/s  sum %.12e  %s\n", name,
+         kMode == 2 ? "db   " : kMode == 1 ? "async" : "plain", regs, bps, ms, N / (ms * 1e-3),
+         checksum(y, (size_t)N * Op::kOut), cudaGetErrorString(cudaGetLastError()));
+}
+
 template <class Op, class T, int kReg, int kSmem, int kMinB, int kTrig, bool kCall>
 void jvp(const char* name, int64_t N, T* x, T* y, T* scratch) {
   auto kern = kCall ? k_gen_jvp_call<Op, T, kReg, kSmem, kMinB, true, kTrig>
@@ -146,7 +166,7 @@ int main(int argc, char** argv) {
   const size_t cap = 1ull << 30;
   double *x, *y, *lam, *scratch;
   int32_t* st;
-  cudaMalloc(&x, sizeof(double) * N * 29 * 6);
+  cudaMalloc(&x, sizeof(double) * 4194304 * 21);  // >= N * 29 * 6; the chain7 sweeps run 4M states
   cudaMalloc(&y, sizeof(double) * N * 841 * 2);
   cudaMalloc(&lam, sizeof(double) * 2097152 * 36);  // sweeps 3 / 9 run chain7 at 1M / 2M states
   cudaMalloc(&scratch, cap);
@@ -225,6 +245,47 @@ int main(int argc, char** argv) {
     gen<GenChain7::Rnea, double, S, 0, 4, kTrigLib, true, false>("c7 rnea f64 r b4 cs lib", N7, x, y, st, scratch);
     gen<GenChain7::RneaBias, double, GenChain7::RneaBias::kSlots, 0, 4, kTrigFast, false, false>("c7 bias f64 r b4", N7, x, y, st, scratch);
     gen<GenChain7::RneaBias, double, GenChain7::RneaBias::kSlots, 0, 4, kTrigFast, true, false>("c7 bias f64 r b4 cs", N7, x, y, st, scratch);
+    return 0;
+  }
+  if (argc > 1 && !strcmp(argv[1], "gdb")) {  // sweep 11: double-buffered input, Panda RNEA / ABA at 2M
+    const int64_t N7 = 2097152;
+    constexpr int SR = GenChain7::Rnea::kSlots;
+    gdb<GenChain7::Rnea, double, SR, 0, 4, kTrigFast, false, 0>("c7 rnea f64 b4", N7, x, y, st, scratch);
+    gdb<GenChain7::Rnea, double, SR, 0, 4, kTrigFast, false, 2>("c7 rnea f64 b4", N7, x, y, st, scratch);
+    gdb<GenChain7::Rnea, double, SR, 0, 4, kTrigFast, true, 2>("c7 rnea f64 b4 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Rnea, double, SR, 0, 3, kTrigFast, false, 2>("c7 rnea f64 b3", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 24, 41, 3, kTrigFast, true, 1>("c7 aba f64 r24 s41 b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 24, 41, 3, kTrigFast, true, 2>("c7 aba f64 r24 s41 b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 44, 21, 3, kTrigFast, true, 2>("c7 aba f64 r44 s21 b3 cs", N7, x, y, st, scratch);
+    k_fill<<<1184, 256>>>(xf, N * 29 * 6, 7);
+    constexpr int SRf = GenChain7::Rnea::kSlots;
+    gdb<GenChain7::Rnea, float, SRf, 0, 6, kTrigLib, false, 0>("c7 rnea f32 b6", N7, xf, yf, st, sf);
+    gdb<GenChain7::Rnea, float, SRf, 0, 6, kTrigLib, false, 2>("c7 rnea f32 b6", N7, xf, yf, st, sf);
+    gdb<GenChain7::Aba, float, 30, 35, 5, kTrigFast, false, 1>("c7 aba f32 r30 s35 b5", N7, xf, yf, st, sf);
+    gdb<GenChain7::Aba, float, 30, 35, 5, kTrigFast, false, 2>("c7 aba f32 r30 s35 b5", N7, xf, yf, st, sf);
+    return 0;
+  }
+  if (argc > 1 && !strcmp(argv[1], "gdb4")) {  // sweep 12: double-buffered input at 4M states (headline size)
+    const int64_t N7 = 4194304;
+    k_fill<<<1184, 256>>>(x, N7 * 21, 9);
+    constexpr int SA = GenChain7::Aba::kSlots, SR = GenChain7::Rnea::kSlots;
+    gdb<GenChain7::Aba, double, 24, 41, 3, kTrigFast, true, 1>("c7 aba f64 r24 s41 b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 44, SA - 44, 3, kTrigFast, true, 2>("c7 aba f64 r44 b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 44, SA - 44, 3, kTrigFast, false, 2>("c7 aba f64 r44 b3", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 34, SA - 34, 3, kTrigFast, true, 2>("c7 aba f64 r34 b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 54, SA - 54, 3, kTrigFast, true, 2>("c7 aba f64 r54 b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, SA, 0, 3, kTrigFast, true, 2>("c7 aba f64 rall b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 24, 41, 3, kTrigFast, true, 1>("c7 aba f64 r24 s41 b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Rnea, double, SR, 0, 4, kTrigFast, false, 0>("c7 rnea f64 b4", N7, x, y, st, scratch);
+    gdb<GenChain7::Rnea, double, SR, 0, 4, kTrigFast, false, 2>("c7 rnea f64 b4", N7, x, y, st, scratch);
+    float* xf4 = (float*)x;
+    k_fill<<<1184, 256>>>(xf4, N7 * 21, 9);
+    gdb<GenChain7::Aba, float, 30, 35, 5, kTrigFast, false, 1>("c7 aba f32 r30 s35 b5", N7, xf4, yf, st, sf);
+    gdb<GenChain7::Aba, float, 30, 35, 5, kTrigFast, false, 2>("c7 aba f32 r30 s35 b5", N7, xf4, yf, st, sf);
+    gdb<GenChain7::Aba, float, 40, 25, 5, kTrigFast, false, 2>("c7 aba f32 r40 s25 b5", N7, xf4, yf, st, sf);
+    gdb<GenChain7::Aba, float, 30, 35, 6, kTrigFast, false, 2>("c7 aba f32 r30 s35 b6", N7, xf4, yf, st, sf);
+    gdb<GenChain7::Rnea, float, SR, 0, 6, kTrigLib, false, 0>("c7 rnea f32 b6", N7, xf4, yf, st, sf);
+    gdb<GenChain7::Rnea, float, SR, 0, 6, kTrigLib, false, 2>("c7 rnea f32 b6", N7, xf4, yf, st, sf);
     return 0;
   }
   if (argc > 1 && !strcmp(argv[1], "g1osc")) {  // sweep 10: G1 OSC placements with the out-of-line sin/cos

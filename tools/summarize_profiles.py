@@ -127,7 +127,7 @@ def main():
 
     out = {}
     # (key, kernel, states per launch, algorithmic flops / state, algorithmic bytes / state)
-    specs = [("chain7_aba_f64", "k_gen_async<GenChain7::Aba, double> (generated, cp.async state prefetch, fast fp64 "
+    specs = [("chain7_aba_f64", "k_gen_db<GenChain7::Aba, double> (generated, double-buffered cp.async state input, fast fp64 "
                                 "sincos)", 4194304,
               bench.flops_per_eval("chain7", "aba"), 224),
              ("tree29_aba_f64", "k_gen_call<GenTree29::Aba, double> (generated, constants from the __constant__ table, routine out of line per state)", 262144, bench.flops_per_eval("tree29", "aba"), 928),
