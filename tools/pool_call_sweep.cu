@@ -288,6 +288,24 @@ int main(int argc, char** argv) {
     gdb<GenChain7::Rnea, float, SR, 0, 6, kTrigLib, false, 2>("c7 rnea f32 b6", N7, xf4, yf, st, sf);
     return 0;
   }
+  if (argc > 1 && !strcmp(argv[1], "gdb5")) {  // sweep 13: double-buffered input for further routines
+    const int64_t N7 = 4194304;
+    k_fill<<<1184, 256>>>(x, N7 * 21, 9);
+    constexpr int SP = GenChain7::CrbaPacked::kSlots, SG = GenChain7::RneaGrav::kSlots;
+    gdb<GenChain7::CrbaPacked, double, SP, 0, 4, kTrigLib, false, 0>("c7 crbap f64 b4", N7, x, y, st, scratch);
+    gdb<GenChain7::CrbaPacked, double, SP, 0, 4, kTrigLib, false, 2>("c7 crbap f64 b4", N7, x, y, st, scratch);
+    gdb<GenChain7::CrbaPacked, double, SP, 0, 4, kTrigLib, true, 2>("c7 crbap f64 b4 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::RneaGrav, double, SG, 0, 4, kTrigFast, false, 0>("c7 grav f64 b4", N7, x, y, st, scratch);
+    gdb<GenChain7::RneaGrav, double, SG, 0, 4, kTrigFast, false, 2>("c7 grav f64 b4", N7, x, y, st, scratch);
+    k_fill<<<1184, 256>>>(x, N * 29 * 6, 7);
+    gdb<GenTree29::Rnea, float, 55, 0, 3, kTrigCall, false, 0>("t29 rnea f32 r55 b3", N, xf, yf, st, sf);
+    gdb<GenTree29::Rnea, float, 55, 0, 2, kTrigCall, false, 2>("t29 rnea f32 r55 b2", N, xf, yf, st, sf);
+    gdb<GenTree29::RneaBias, double, 0, 72, 3, kTrigCall, false, 0>("t29 bias f64 s72 b3", N, x, y, st, scratch);
+    gdb<GenTree29::RneaBias, double, 0, 40, 3, kTrigCall, false, 2>("t29 bias f64 s40 b3", N, x, y, st, scratch);
+    gdb<GenTree29::Crba, double, 0, 55, 3, kTrigLib, true, 0>("t29 crba f64 s55 b3 cs", N, x, y, st, scratch);
+    gdb<GenTree29::Crba, double, 0, 55, 3, kTrigLib, true, 2>("t29 crba f64 s55 b3 cs", N, x, y, st, scratch);
+    return 0;
+  }
   if (argc > 1 && !strcmp(argv[1], "g1osc")) {  // sweep 10: G1 OSC placements with the out-of-line sin/cos
     osc<GenTree29::Osc23, double, 40, 110, 2, kTrigCall, false>("t29 osc23 f64 r40 s110 b2", N, x, y, lam, st, scratch);
     osc<GenTree29::Osc23, double, 24, 110, 2, kTrigCall, false>("t29 osc23 f64 r24 s110 b2", N, x, y, lam, st, scratch);
