@@ -288,6 +288,18 @@ int main(int argc, char** argv) {
     gdb<GenChain7::Rnea, float, SR, 0, 6, kTrigLib, false, 2>("c7 rnea f32 b6", N7, xf4, yf, st, sf);
     return 0;
   }
+  if (argc > 1 && !strcmp(argv[1], "gdb6")) {  // sweep 14: headline ABA fp64 db placements around r44 s21
+    const int64_t N7 = 4194304;
+    k_fill<<<1184, 256>>>(x, N7 * 21, 9);
+    constexpr int SA = GenChain7::Aba::kSlots;
+    gdb<GenChain7::Aba, double, 44, SA - 44, 3, kTrigFast, true, 2>("c7 aba f64 r44 b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 40, SA - 40, 3, kTrigFast, true, 2>("c7 aba f64 r40 b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 48, SA - 48, 3, kTrigFast, true, 2>("c7 aba f64 r48 b3 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 44, SA - 44, 3, kTrigLib, true, 2>("c7 aba f64 r44 b3 cs lib", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 44, SA - 44, 2, kTrigFast, true, 2>("c7 aba f64 r44 b2 cs", N7, x, y, st, scratch);
+    gdb<GenChain7::Aba, double, 44, SA - 44, 3, kTrigFast, true, 2>("c7 aba f64 r44 b3 cs", N7, x, y, st, scratch);
+    return 0;
+  }
   if (argc > 1 && !strcmp(argv[1], "gdb5")) {  // sweep 13: double-buffered input for further routines
     const int64_t N7 = 4194304;
     k_fill<<<1184, 256>>>(x, N7 * 21, 9);
